@@ -1,0 +1,234 @@
+/* dgds_b200.h — C ABI of the B200-native Distributed Grouped Draft Server (DGDS).
+ *
+ * Drop-in boundary for the reference draft-server hot path
+ * (/root/reference/proj/include/rollsim/dgds.hpp:51-162, cst.hpp:16-138,
+ *  engine.hpp:28-92). Plain pointers and sizes only; no C++ or torch types.
+ * Host buffers unless a function says "device". Every function returns an int
+ * status (DGDS_OK or a negative code; message via dgds_last_error()) and never
+ * throws across the boundary.
+ *
+ * Reference interface each entry point replaces:
+ *   dgds_create / dgds_destroy      DraftServer::DraftServer(DgdsParams)       dgds.hpp:53, dgds.cpp:19-23
+ *   dgds_shard_of_group             shard_of_group                             dgds.hpp:46, dgds.cpp:10-14
+ *   dgds_intern                     (group-id string -> handle; the reference keys std::map by string)
+ *   dgds_register_group             DraftServer::register_group                dgds.hpp:59, dgds.cpp:99-110
+ *   dgds_drop_group                 DraftServer::drop_group                    dgds.hpp:60, dgds.cpp:112-116
+ *   dgds_sweep_expired              DraftServer::sweep_expired                 dgds.hpp:61, dgds.cpp:118-128
+ *   dgds_has_group / dgds_group_version / dgds_stored_tokens / dgds_shard_group_count
+ *                                   DraftServer::has_group/group_version, GroupDraftIndex::stored_tokens,
+ *                                   DraftServer::shard_group_count             dgds.hpp:69-72, cst.hpp:75
+ *   dgds_update_batch               DraftServer::update_cst x n (call order)   dgds.hpp:55-56, dgds.cpp:36-51
+ *                                    -> GroupDraftIndex::append                 cst.cpp:118-133
+ *   dgds_speculate_batch            DraftServer::speculate x n /               dgds.hpp:64-65, dgds.cpp:130-138
+ *                                   DraftClient::batch_speculate (fetch_period 0) dgds.cpp:274-292
+ *                                    -> GroupDraftIndex::speculate              cst.cpp:153-228
+ *   dgds_verify_batch               Instance::decode_step verification          engine.cpp:115-143
+ *   dgds_draft_len                  Instance::decode_step draft-length policy   engine.cpp:78-85
+ *   dgds_*_device                   zero-copy forms of the batch calls over device buffers and a
+ *                                   cudaStream_t (PAPER.md:359 batch_speculate(..., void* pattern_buffer_ptr,
+ *                                   void* output_buffer_ptr, ...); SPEC.md:263 leaves it to us).
+ *
+ * Semantics are the reference's, record by record, including: an out-of-order
+ * append is a VALUE (ok=0, acked=stored count) and still creates the request's
+ * stream; an empty append is ok without a version bump; update auto-registers an
+ * unknown or expired group with the default TTL; speculate on an unknown group
+ * yields zero candidates and does not check expiry. Deliberate divergence: a
+ * batch is validated as a whole before anything is applied (negative request id
+ * or token, bad args -> DGDS_EINVAL and no effect), where the reference throws
+ * after partially applying (cst.cpp:120,126-128).
+ */
+#ifndef DGDS_B200_H
+#define DGDS_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DGDS_OK 0
+#define DGDS_EINVAL (-1)      /* std::invalid_argument in the reference */
+#define DGDS_ECUDA (-2)       /* CUDA runtime error */
+#define DGDS_ENOMEM (-3)      /* device or host allocation failed */
+#define DGDS_EUNSUPPORTED (-4) /* outside this build's device limits (see DGDS_MAX_*) */
+#define DGDS_EBUFFER (-5)     /* caller output buffer too small */
+#define DGDS_ESTATE (-6)      /* bad handle / call order */
+
+#define DGDS_MAX_DEPTH 32 /* max_pattern_len + max_spec_len (one warp lane per trie level) */
+#define DGDS_MAX_TOP_K 32
+
+typedef struct dgds_server dgds_server;
+
+/* DgdsParams (dgds.hpp:18-24) + Limits (cst.hpp:44-47) + device capacity plan. */
+typedef struct dgds_params {
+  int32_t shard_count;         /* logical shards for shard_group_count(); >= 1 */
+  int32_t append_batch_tokens; /* kept for the client facade (dgds.hpp:21) */
+  double fetch_period;         /* kept for the client facade (dgds.hpp:20) */
+  double default_ttl_seconds;  /* auto-registration TTL (dgds.hpp:22) */
+  int32_t max_pattern_len;     /* Limits (cst.hpp:45) */
+  int32_t max_spec_len;        /* Limits (cst.hpp:46) */
+  int32_t device;              /* CUDA device ordinal */
+  int32_t reserved0;
+  uint64_t expected_nodes;     /* initial trie capacity in nodes (0 = 1<<20); grows by rebuild */
+  uint64_t expected_streams;   /* initial request-stream capacity (0 = 4096) */
+} dgds_params;
+
+/* SpeculationArgs (cst.hpp:16-23); 32 bytes. */
+typedef struct dgds_spec_args {
+  int32_t max_spec_tokens;
+  int32_t pattern_lookup_max;
+  int32_t pattern_lookup_min;
+  int32_t top_k;
+  double min_step_freq;
+  int64_t min_support;
+} dgds_spec_args;
+
+/* UpdateReply (dgds.hpp:39-43). */
+typedef struct dgds_update_reply {
+  int32_t ok;
+  int32_t reserved0;
+  uint64_t version;
+  uint64_t acked_tokens;
+} dgds_update_reply;
+
+/* Caller-owned candidate buffers for n queries: query q, candidate c in
+ * [0, n_cands[q]) has lens[q*k_stride+c] tokens at tokens[(q*k_stride+c)*s_stride ...],
+ * score scores[q*k_stride+c] (IEEE double, bit-exact with DraftCandidate::score) and
+ * support supports[q*k_stride+c]. Candidates are in candidate_before order
+ * (cst.cpp:29-33). k_stride >= max top_k, s_stride >= max min(max_spec_tokens, max_spec_len). */
+typedef struct dgds_candidates {
+  int32_t k_stride;
+  int32_t s_stride;
+  int32_t* n_cands;
+  int32_t* lens;
+  double* scores;
+  int64_t* supports;
+  int32_t* tokens;
+} dgds_candidates;
+
+/* Verification outputs per request (StepReport::PerRequest, engine.hpp:85-90). */
+typedef struct dgds_verify_out {
+  int32_t* drafted;
+  int32_t* accepted; /* emitted - 1 */
+  int32_t* emitted;
+} dgds_verify_out;
+
+/* Device-side counters of one query launch, for SURVEY.md §8(d)'s algorithmic
+ * bytes: B_q = 4|p| + 32 + 32F + sum_exp(32 + 32 ceil(8c/32)) + sum_cand(4|tokens| + 16). */
+typedef struct dgds_query_stats {
+  uint64_t queries;
+  uint64_t pattern_tokens;
+  uint64_t suffix_lookups; /* F */
+  uint64_t expansions;
+  uint64_t child_sectors;  /* sum ceil(8c/32) */
+  uint64_t cands;
+  uint64_t cand_tokens;
+  uint64_t algorithmic_bytes;
+} dgds_query_stats;
+
+const char* dgds_last_error(void);
+const char* dgds_version_string(void);
+
+uint64_t dgds_fnv1a64(const void* data, size_t n); /* detail::fnv1a64 (bytes.hpp:89-96) */
+int32_t dgds_shard_of_group(const char* group_id, size_t len, int32_t shard_count);
+
+int dgds_create(const dgds_params* params, dgds_server** out);
+int dgds_destroy(dgds_server* s);
+/* The CUDA stream (cudaStream_t) the server orders its work on. */
+void* dgds_cuda_stream(dgds_server* s);
+
+/* Group-id string -> stable handle (interned; no registration side effect). */
+int dgds_intern(dgds_server* s, const char* group_id, size_t len, int32_t* handle);
+
+int dgds_register_group(dgds_server* s, int32_t handle, double ttl_seconds, double now);
+int dgds_drop_group(dgds_server* s, int32_t handle);
+int dgds_sweep_expired(dgds_server* s, double now);
+int dgds_has_group(dgds_server* s, int32_t handle, int32_t* out);
+int dgds_group_version(dgds_server* s, int32_t handle, uint64_t* out);
+int dgds_stored_tokens(dgds_server* s, int32_t handle, int32_t request_id, uint64_t* out);
+int dgds_shard_group_count(dgds_server* s, int32_t shard, uint64_t* out);
+/* Device-side trie size: nodes in use (synchronises). */
+int dgds_node_count(dgds_server* s, uint64_t* out);
+
+/* n update_cst calls, applied in array order. Record i appends
+ * tokens[tok_offsets[i] .. tok_offsets[i+1]) for (handles[i], request_ids[i]).
+ * Host buffers; returns after the replies are final (the device insertion is
+ * enqueued on the server stream and ordered before any later query). */
+int dgds_update_batch(dgds_server* s, int64_t n, const int32_t* handles, const int32_t* request_ids,
+                      const uint64_t* prev_counts, const uint64_t* tok_offsets, const int32_t* tokens, double now,
+                      dgds_update_reply* replies);
+
+/* Same, with the token payload already in device memory (d_tokens, record order);
+ * metadata stays on the host. The kernel is enqueued on `stream` (NULL = server stream). */
+int dgds_update_batch_device(dgds_server* s, int64_t n, const int32_t* handles, const int32_t* request_ids,
+                             const uint64_t* prev_counts, const uint64_t* tok_offsets, const int32_t* d_tokens,
+                             double now, dgds_update_reply* replies, void* stream);
+
+/* n speculate calls. Query q uses patterns[pat_offsets[q] .. pat_offsets[q+1]) and
+ * args[q * args_stride] (args_stride 0 = one shared args). Host buffers; blocks until done.
+ * verify_truth (optional, may be NULL): fused verification as engine.cpp:115-143 with
+ * truth_next[q*truth_stride ..], truth_left[q], limit[q] -> vout. */
+int dgds_speculate_batch(dgds_server* s, int64_t n, const int32_t* handles, const uint64_t* pat_offsets,
+                         const int32_t* patterns, const dgds_spec_args* args, int64_t args_stride,
+                         dgds_candidates* out);
+
+/* Zero-copy query over device buffers, enqueued on `stream` (NULL = server stream), no sync.
+ * d_handles[n], d_pat_len[n], d_patterns[n * pat_stride] (the LAST d_pat_len[q] tokens of each
+ * pattern, left-aligned; only the last max_pattern_len can matter), d_args[q * args_stride].
+ * max_top_k bounds args.top_k over the batch (selects the kernel instance).
+ * Optional fused verify: d_truth (n * truth_stride next ground-truth tokens), d_truth_left[n],
+ * d_limit[n] -> d_vout (all device) — may be NULL. Optional d_stats accumulates counters. */
+int dgds_speculate_device(dgds_server* s, int64_t n, const int32_t* d_handles, const int32_t* d_pat_len,
+                          const int32_t* d_patterns, int32_t pat_stride, const dgds_spec_args* d_args,
+                          int64_t args_stride, int32_t max_top_k, const dgds_candidates* d_out,
+                          const int32_t* d_truth, int32_t truth_stride, const int32_t* d_truth_left,
+                          const int32_t* d_limit, const dgds_verify_out* d_vout, dgds_query_stats* d_stats,
+                          void* stream);
+
+/* Verification of existing candidates (engine.cpp:115-143), host buffers. */
+int dgds_verify_batch(dgds_server* s, int64_t n, const dgds_candidates* cands, const int32_t* truth_next,
+                      int32_t truth_stride, const int32_t* truth_left, const int32_t* limit,
+                      dgds_verify_out* out);
+
+/* Draft length policy (engine.cpp:78-85): sd disabled -> 0; adaptive -> min(cap, budget / n_running); max(.,0). */
+int32_t dgds_draft_len(int32_t sd_enabled, int32_t adaptive, int32_t per_request_cap, int32_t batch_token_budget,
+                       int32_t n_running);
+
+/* ---- multi-GPU routing helpers (device, enqueued on `stream`) ----
+ * Bucket n fixed-size records of rec_words 32-bit words by owner rank (owner[i] in [0, world)):
+ * d_out receives the records grouped by owner in stable order, d_counts[world] the bucket sizes,
+ * d_perm[i] the destination index of record i (for the inverse scatter of replies). */
+int dgds_route_pack(int64_t n, int32_t world, const int32_t* d_owner, const uint32_t* d_records, int32_t rec_words,
+                    uint32_t* d_out, int64_t* d_counts, int64_t* d_perm, void* stream);
+/* Inverse: d_out[i] = d_in[d_perm[i]] for n records of rec_words words. */
+int dgds_route_unpack(int64_t n, const uint32_t* d_in, int32_t rec_words, const int64_t* d_perm, uint32_t* d_out,
+                      void* stream);
+
+/* ---- synthetic grouped-rollout traces (generate_workload, workload.cpp:51-103) ---- */
+typedef struct dgds_workload_cfg {
+  int32_t num_groups;
+  int32_t group_size;
+  int32_t length_family; /* 0 lognormal, 1 pareto (workload.hpp:19-25) */
+  int32_t vocab_size;
+  double location;
+  double scale;
+  double group_correlation;
+  double noise_base;
+  double pattern_similarity;
+  double prompt_mean;
+  double prompt_spread;
+  int32_t max_tokens;
+  int32_t reserved0;
+  uint64_t seed;
+} dgds_workload_cfg;
+
+/* Pass 1 (tokens == NULL): fills lengths[num_groups*group_size] and prompt_lens[num_groups] (may be NULL).
+ * Pass 2: also writes all outputs back to back (group-major, request-minor) into tokens. */
+int dgds_generate_workload(const dgds_workload_cfg* cfg, int64_t* lengths, int32_t* prompt_lens, int32_t* tokens);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DGDS_B200_H */

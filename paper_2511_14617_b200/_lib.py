@@ -1,0 +1,170 @@
+"""ctypes binding of libdgds_b200.so (the C ABI in include/dgds_b200.h).
+
+The library is the only implementation: if it is missing or no CUDA device is
+present, the calls fail loudly — there is no CPU fallback path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libdgds_b200.so")
+
+DGDS_OK = 0
+DGDS_EINVAL = -1
+DGDS_ECUDA = -2
+DGDS_ENOMEM = -3
+DGDS_EUNSUPPORTED = -4
+DGDS_EBUFFER = -5
+DGDS_ESTATE = -6
+MAX_DEPTH = 32
+MAX_TOP_K = 32
+
+
+class Params(C.Structure):
+    _fields_ = [
+        ("shard_count", C.c_int32),
+        ("append_batch_tokens", C.c_int32),
+        ("fetch_period", C.c_double),
+        ("default_ttl_seconds", C.c_double),
+        ("max_pattern_len", C.c_int32),
+        ("max_spec_len", C.c_int32),
+        ("device", C.c_int32),
+        ("reserved0", C.c_int32),
+        ("expected_nodes", C.c_uint64),
+        ("expected_streams", C.c_uint64),
+    ]
+
+
+class SpecArgs(C.Structure):
+    _fields_ = [
+        ("max_spec_tokens", C.c_int32),
+        ("pattern_lookup_max", C.c_int32),
+        ("pattern_lookup_min", C.c_int32),
+        ("top_k", C.c_int32),
+        ("min_step_freq", C.c_double),
+        ("min_support", C.c_int64),
+    ]
+
+
+class UpdateReplyC(C.Structure):
+    _fields_ = [("ok", C.c_int32), ("reserved0", C.c_int32), ("version", C.c_uint64), ("acked_tokens", C.c_uint64)]
+
+
+class Candidates(C.Structure):
+    _fields_ = [
+        ("k_stride", C.c_int32),
+        ("s_stride", C.c_int32),
+        ("n_cands", C.c_void_p),
+        ("lens", C.c_void_p),
+        ("scores", C.c_void_p),
+        ("supports", C.c_void_p),
+        ("tokens", C.c_void_p),
+    ]
+
+
+class VerifyOut(C.Structure):
+    _fields_ = [("drafted", C.c_void_p), ("accepted", C.c_void_p), ("emitted", C.c_void_p)]
+
+
+class QueryStats(C.Structure):
+    _fields_ = [
+        ("queries", C.c_uint64),
+        ("pattern_tokens", C.c_uint64),
+        ("suffix_lookups", C.c_uint64),
+        ("expansions", C.c_uint64),
+        ("child_sectors", C.c_uint64),
+        ("cands", C.c_uint64),
+        ("cand_tokens", C.c_uint64),
+        ("algorithmic_bytes", C.c_uint64),
+    ]
+
+
+class WorkloadCfg(C.Structure):
+    _fields_ = [
+        ("num_groups", C.c_int32),
+        ("group_size", C.c_int32),
+        ("length_family", C.c_int32),
+        ("vocab_size", C.c_int32),
+        ("location", C.c_double),
+        ("scale", C.c_double),
+        ("group_correlation", C.c_double),
+        ("noise_base", C.c_double),
+        ("pattern_similarity", C.c_double),
+        ("prompt_mean", C.c_double),
+        ("prompt_spread", C.c_double),
+        ("max_tokens", C.c_int32),
+        ("reserved0", C.c_int32),
+        ("seed", C.c_uint64),
+    ]
+
+
+class DgdsError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"dgds error {code}: {msg}")
+        self.code = code
+
+
+_P = C.c_void_p
+_I32 = C.c_int32
+_I64 = C.c_int64
+_U64 = C.c_uint64
+_D = C.c_double
+
+EXPORTS = {
+    "dgds_last_error": (C.c_char_p, []),
+    "dgds_version_string": (C.c_char_p, []),
+    "dgds_fnv1a64": (_U64, [_P, C.c_size_t]),
+    "dgds_shard_of_group": (_I32, [C.c_char_p, C.c_size_t, _I32]),
+    "dgds_create": (C.c_int, [C.POINTER(Params), C.POINTER(_P)]),
+    "dgds_destroy": (C.c_int, [_P]),
+    "dgds_cuda_stream": (_P, [_P]),
+    "dgds_intern": (C.c_int, [_P, C.c_char_p, C.c_size_t, C.POINTER(_I32)]),
+    "dgds_register_group": (C.c_int, [_P, _I32, _D, _D]),
+    "dgds_drop_group": (C.c_int, [_P, _I32]),
+    "dgds_sweep_expired": (C.c_int, [_P, _D]),
+    "dgds_has_group": (C.c_int, [_P, _I32, C.POINTER(_I32)]),
+    "dgds_group_version": (C.c_int, [_P, _I32, C.POINTER(_U64)]),
+    "dgds_stored_tokens": (C.c_int, [_P, _I32, _I32, C.POINTER(_U64)]),
+    "dgds_shard_group_count": (C.c_int, [_P, _I32, C.POINTER(_U64)]),
+    "dgds_node_count": (C.c_int, [_P, C.POINTER(_U64)]),
+    "dgds_update_batch": (C.c_int, [_P, _I64, _P, _P, _P, _P, _P, _D, _P]),
+    "dgds_update_batch_device": (C.c_int, [_P, _I64, _P, _P, _P, _P, _P, _D, _P, _P]),
+    "dgds_speculate_batch": (C.c_int, [_P, _I64, _P, _P, _P, _P, _I64, C.POINTER(Candidates)]),
+    "dgds_speculate_device": (C.c_int, [_P, _I64, _P, _P, _P, _I32, _P, _I64, _I32, C.POINTER(Candidates), _P, _I32,
+                                        _P, _P, C.POINTER(VerifyOut), _P, _P]),
+    "dgds_verify_batch": (C.c_int, [_P, _I64, C.POINTER(Candidates), _P, _I32, _P, _P, C.POINTER(VerifyOut)]),
+    "dgds_draft_len": (_I32, [_I32, _I32, _I32, _I32, _I32]),
+    "dgds_route_pack": (C.c_int, [_I64, _I32, _P, _P, _I32, _P, _P, _P, _P]),
+    "dgds_route_unpack": (C.c_int, [_I64, _P, _I32, _P, _P, _P]),
+    "dgds_generate_workload": (C.c_int, [C.POINTER(WorkloadCfg), _P, _P, _P]),
+}
+
+_lib = None
+
+
+def lib():
+    """Load libdgds_b200.so (building it first if this checkout has nvcc and no .so)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            from . import build as _b
+
+            _b.build()
+        L = C.CDLL(LIB_PATH)
+        for name, (res, args) in EXPORTS.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+    return _lib
+
+
+def check(rc: int):
+    if rc == DGDS_OK:
+        return
+    msg = lib().dgds_last_error().decode(errors="replace")
+    if rc == DGDS_EINVAL:
+        raise ValueError(msg)  # std::invalid_argument in the reference
+    raise DgdsError(rc, msg)

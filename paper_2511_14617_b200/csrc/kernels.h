@@ -1,0 +1,88 @@
+// kernels.h — host-side launch interface of the sm_100a kernels (K1 append,
+// K2 draft query + fused K3 verify, standalone verify, arena rebuild, routing).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/dgds_b200.h"
+#include "trie.cuh"
+
+namespace dgds {
+
+// One warp per segment: all records of one request stream inside one batch, in
+// call order, as `npieces` token runs starting at stream position `start`.
+struct AppendSeg {
+  uint32_t stream;  // stream slot (row of DevTrie::active)
+  uint32_t root;    // group root id
+  uint64_t start;   // tokens stored for the stream before this batch
+  uint32_t piece0;
+  uint32_t npieces;
+  uint64_t pad_;
+};
+static_assert(sizeof(AppendSeg) == 32, "AppendSeg is 32 B");
+
+struct AppendPiece {
+  uint64_t tok_off;  // into the batch token buffer
+  uint32_t n;
+  uint32_t pad_;
+};
+
+cudaError_t launch_append(const DevTrie& T, const AppendSeg* d_segs, int64_t nseg, const AppendPiece* d_pieces,
+                          const int32_t* d_tokens, cudaStream_t st);
+
+struct QueryLaunch {
+  DevTrie T;
+  const uint32_t* root_of;
+  int32_t n_handles;
+  int32_t S;  // shared-memory token stride per path (>= lim_spec, >= 1)
+  int64_t n;
+  const int32_t* handles;
+  const int32_t* pat_len;
+  const int32_t* patterns;
+  int32_t pat_stride;
+  int32_t k_stride;
+  const dgds_spec_args* args;
+  int64_t args_stride;
+  int32_t s_stride;
+  int32_t truth_stride;
+  int32_t* n_cands;
+  int32_t* lens;
+  double* scores;
+  int64_t* supports;
+  int32_t* tokens;
+  const int32_t* truth;
+  const int32_t* truth_left;
+  const int32_t* limit;
+  int32_t* v_drafted;
+  int32_t* v_accepted;
+  int32_t* v_emitted;
+  dgds_query_stats* stats;
+  int32_t* err_flag;  // set to 1 by any query with invalid args (device API)
+};
+
+// max_k selects the template instance (K = next power of two >= max_k).
+cudaError_t launch_query(const QueryLaunch& L, int32_t max_k, cudaStream_t st);
+
+cudaError_t launch_verify(int64_t n, int32_t k_stride, int32_t s_stride, const int32_t* n_cands, const int32_t* lens,
+                          const int32_t* tokens, const int32_t* truth, int32_t truth_stride, const int32_t* truth_left,
+                          const int32_t* limit, int32_t* drafted, int32_t* accepted, int32_t* emitted,
+                          cudaStream_t st);
+
+cudaError_t launch_set_u32(uint32_t* dst, uint32_t value, cudaStream_t st);
+
+// Arena rebuild (growth + garbage collection of dropped groups): re-insert every
+// live node of `from` into `to`, one trie depth per launch so parents are
+// re-keyed before their children. root_alive: bitmap over root indices.
+cudaError_t launch_rebuild_level(const DevTrie& from, const DevTrie& to, uint32_t depth, const uint32_t* root_alive,
+                                 uint32_t* remap, cudaStream_t st);
+cudaError_t launch_remap_active(uint32_t* active, const uint32_t* streams, const uint32_t* sizes, int64_t nstreams,
+                                const uint32_t* remap, uint64_t old_cap, cudaStream_t st);
+
+cudaError_t launch_route_pack(int64_t n, int32_t world, const int32_t* owner, const uint32_t* records,
+                              int32_t rec_words, uint32_t* out, int64_t* counts, int64_t* perm, void* scratch,
+                              cudaStream_t st);
+cudaError_t launch_route_unpack(int64_t n, const uint32_t* in, int32_t rec_words, const int64_t* perm, uint32_t* out,
+                                cudaStream_t st);
+
+}  // namespace dgds

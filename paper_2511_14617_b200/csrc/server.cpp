@@ -1,0 +1,874 @@
+// server.cpp — host side of the B200 DGDS: the extern "C" ABI declared in
+// include/dgds_b200.h over the sm_100a kernels in kernels.cu.
+//
+// Host work here is O(records) bookkeeping that the reference performs per
+// call under its shard mutex (proj/src/dgds.cpp:36-51,99-138): group lookup
+// with lazy TTL expiry, auto-registration, per-stream gap check and version
+// numbering in call order (cst.cpp:118-133). Record replies are therefore
+// final before any device work completes. All trie work — insertion, suffix
+// match, beam, verification — runs on the GPU; there is no CPU fallback: a
+// missing device is an error.
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "../../include/dgds_b200.h"
+#include "kernels.h"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define DGDS_CUDA(call)                                                                       \
+  do {                                                                                        \
+    cudaError_t e_ = (call);                                                                  \
+    if (e_ != cudaSuccess) return fail(DGDS_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+uint64_t fnv1a64(const void* data, size_t n) {  // detail::fnv1a64 (bytes.hpp:89-96)
+  const auto* p = static_cast<const unsigned char*>(data);
+  uint64_t h = 0xcbf29ce484222325ull;
+  for (size_t i = 0; i < n; ++i) {
+    h ^= p[i];
+    h *= 0x100000001b3ull;
+  }
+  return h;
+}
+
+constexpr double kMaxLoad = 0.70;     // rebuild threshold
+constexpr double kTargetLoad = 0.45;  // load right after a rebuild
+constexpr uint32_t kRootCap = 1u << 22;
+constexpr uint64_t kMaxCap = 0xFFFFFFFFull - kRootCap - 2;
+
+struct PinnedBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  ~PinnedBuf() {
+    if (p) cudaFreeHost(p);
+  }
+  int ensure(size_t bytes) {
+    if (bytes <= cap) return DGDS_OK;
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    size_t c = std::max<size_t>(bytes, cap * 2);
+    if (cudaHostAlloc(&p, c, cudaHostAllocDefault) != cudaSuccess) {
+      cap = 0;
+      return fail(DGDS_ENOMEM, "cudaHostAlloc failed");
+    }
+    cap = c;
+    return DGDS_OK;
+  }
+};
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+  int ensure(size_t bytes) {
+    if (bytes <= cap) return DGDS_OK;
+    if (p) cudaFree(p);
+    p = nullptr;
+    size_t c = std::max<size_t>(bytes, cap * 2);
+    if (cudaMalloc(&p, c) != cudaSuccess) {
+      cap = 0;
+      return fail(DGDS_ENOMEM, "cudaMalloc failed");
+    }
+    cap = c;
+    return DGDS_OK;
+  }
+};
+
+struct StreamRec {
+  uint64_t stored = 0;
+  uint32_t slot = 0;
+  int64_t batch_seg = -1;  // segment index in the batch being built
+  uint64_t batch_stamp = 0;
+};
+
+struct GroupRec {
+  std::string gid;
+  int32_t shard = 0;
+  bool alive = false;
+  uint32_t root = 0;
+  double ttl = 0.0;
+  double expires = 0.0;
+  uint64_t version = 0;
+  std::unordered_map<int32_t, StreamRec> streams;
+};
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+}  // namespace
+
+struct dgds_server {
+  dgds_params p{};
+  int32_t D = 0;
+  cudaStream_t st = nullptr;
+  cudaEvent_t staging_free = nullptr;
+  dgds::DevTrie T{};
+  unsigned long long* d_used = nullptr;
+  uint64_t used_ub = 0;  // upper bound on occupied slots since the last exact read
+
+  uint32_t* d_root_of = nullptr;
+  size_t root_of_cap = 0;
+  uint32_t next_root_index = 0;
+
+  uint64_t stream_cap = 0;
+  uint32_t next_stream = 0;
+  std::vector<uint32_t> free_streams;
+
+  std::unordered_map<std::string, int32_t> intern;
+  std::vector<GroupRec> groups;
+  std::vector<uint64_t> shard_counts;
+  uint64_t batch_stamp = 0;
+
+  PinnedBuf h_stage, h_out;
+  DevBuf d_stage, d_out;
+  int32_t* d_err = nullptr;
+  std::mutex mu;  // calls on one handle are serialized
+};
+
+namespace {
+
+int set_root(dgds_server* s, int32_t handle, uint32_t root) {
+  if (static_cast<size_t>(handle) >= s->root_of_cap) {
+    size_t nc = std::max<size_t>(1024, s->root_of_cap * 2);
+    while (nc <= static_cast<size_t>(handle)) nc *= 2;
+    uint32_t* nb = nullptr;
+    DGDS_CUDA(cudaMalloc(&nb, nc * sizeof(uint32_t)));
+    DGDS_CUDA(cudaMemsetAsync(nb, 0, nc * sizeof(uint32_t), s->st));
+    if (s->d_root_of) {
+      DGDS_CUDA(cudaMemcpyAsync(nb, s->d_root_of, s->root_of_cap * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s->st));
+      DGDS_CUDA(cudaStreamSynchronize(s->st));
+      cudaFree(s->d_root_of);
+    }
+    s->d_root_of = nb;
+    s->root_of_cap = nc;
+  }
+  DGDS_CUDA(dgds::launch_set_u32(s->d_root_of + handle, root, s->st));
+  return DGDS_OK;
+}
+
+int alloc_stream_slot(dgds_server* s, uint32_t* out) {
+  if (!s->free_streams.empty()) {
+    *out = s->free_streams.back();
+    s->free_streams.pop_back();
+    return DGDS_OK;
+  }
+  if (s->next_stream >= s->stream_cap) {
+    uint64_t nc = std::max<uint64_t>(1024, s->stream_cap * 2);
+    uint32_t* na = nullptr;
+    DGDS_CUDA(cudaMalloc(&na, nc * dgds::kWarp * sizeof(uint32_t)));
+    if (s->T.active) {
+      DGDS_CUDA(cudaMemcpyAsync(na, s->T.active, s->stream_cap * dgds::kWarp * sizeof(uint32_t),
+                                cudaMemcpyDeviceToDevice, s->st));
+      DGDS_CUDA(cudaStreamSynchronize(s->st));
+      cudaFree(s->T.active);
+    }
+    s->T.active = na;
+    s->stream_cap = nc;
+  }
+  *out = s->next_stream++;
+  return DGDS_OK;
+}
+
+void retire_group(dgds_server* s, GroupRec& g) {
+  if (!g.alive) return;
+  for (auto& kv : g.streams) s->free_streams.push_back(kv.second.slot);
+  g.streams.clear();
+  g.alive = false;
+  g.version = 0;
+  s->shard_counts[g.shard] -= 1;
+  set_root(s, static_cast<int32_t>(&g - s->groups.data()), 0u);
+}
+
+int create_group(dgds_server* s, GroupRec& g, double ttl, double now) {
+  if (s->next_root_index >= kRootCap) return fail(DGDS_EUNSUPPORTED, "group root ids exhausted");
+  g.root = dgds::kRootTop - s->next_root_index++;
+  g.alive = true;
+  g.ttl = ttl;
+  g.expires = now + ttl;
+  g.version = 0;
+  g.streams.clear();
+  s->shard_counts[g.shard] += 1;
+  return set_root(s, static_cast<int32_t>(&g - s->groups.data()), g.root);
+}
+
+// find_entry with lazy expiry (dgds.cpp:25-34)
+bool live_entry(dgds_server* s, GroupRec& g, double now) {
+  if (!g.alive) return false;
+  if (g.expires < now) {
+    retire_group(s, g);
+    return false;
+  }
+  return true;
+}
+
+int check_handle(dgds_server* s, int32_t h) {
+  if (h < 0 || static_cast<size_t>(h) >= s->groups.size()) return fail(DGDS_EINVAL, "bad group handle");
+  return DGDS_OK;
+}
+
+// validate_args (cst.cpp:18-25) + device limits
+int check_args(const dgds_spec_args& a) {
+  if (a.pattern_lookup_min < 1 || a.pattern_lookup_min > a.pattern_lookup_max)
+    return fail(DGDS_EINVAL, "speculation args: need 1 <= pattern_lookup_min <= pattern_lookup_max");
+  if (a.max_spec_tokens < 0) return fail(DGDS_EINVAL, "speculation args: max_spec_tokens must be >= 0");
+  if (a.top_k < 1) return fail(DGDS_EINVAL, "speculation args: top_k must be >= 1");
+  if (a.min_step_freq < 0.0) return fail(DGDS_EINVAL, "speculation args: min_step_freq must be >= 0");
+  if (a.min_support < 0) return fail(DGDS_EINVAL, "speculation args: min_support must be >= 0");
+  if (a.top_k > DGDS_MAX_TOP_K) return fail(DGDS_EUNSUPPORTED, "top_k above DGDS_MAX_TOP_K");
+  return DGDS_OK;
+}
+
+uint64_t cap_for(uint64_t nodes, double load) {
+  uint64_t c = static_cast<uint64_t>(std::ceil(static_cast<double>(nodes) / load));
+  return std::max<uint64_t>(c, 1024);
+}
+
+int read_used(dgds_server* s, uint64_t* out) {
+  unsigned long long u = 0;
+  DGDS_CUDA(cudaMemcpyAsync(&u, s->d_used, sizeof(u), cudaMemcpyDeviceToHost, s->st));
+  DGDS_CUDA(cudaStreamSynchronize(s->st));
+  *out = u;
+  return DGDS_OK;
+}
+
+// Grow (and garbage-collect dropped groups) by rebuilding into a larger table.
+int rebuild(dgds_server* s, uint64_t new_cap) {
+  if (new_cap > kMaxCap) new_cap = kMaxCap;
+  dgds::DevTrie to = s->T;
+  to.cap = new_cap;
+  DGDS_CUDA(cudaMalloc(&to.slots, new_cap * sizeof(dgds::Slot)));
+  DGDS_CUDA(cudaMemsetAsync(to.slots, 0, new_cap * sizeof(dgds::Slot), s->st));
+  unsigned long long* d_used_new = nullptr;
+  DGDS_CUDA(cudaMalloc(&d_used_new, sizeof(unsigned long long)));
+  DGDS_CUDA(cudaMemsetAsync(d_used_new, 0, sizeof(unsigned long long), s->st));
+  to.used = d_used_new;
+  std::vector<uint32_t> alive((kRootCap + 31) / 32, 0);
+  std::vector<uint32_t> live_slots, live_sizes;
+  for (auto& g : s->groups) {
+    if (!g.alive) continue;
+    const uint32_t r = dgds::kRootTop - g.root;
+    alive[r >> 5] |= 1u << (r & 31);
+    for (auto& kv : g.streams) {
+      live_slots.push_back(kv.second.slot);
+      live_sizes.push_back(static_cast<uint32_t>(std::min<uint64_t>(kv.second.stored, s->D)));
+    }
+  }
+  uint32_t *d_alive = nullptr, *d_remap = nullptr, *d_ls = nullptr;
+  DGDS_CUDA(cudaMalloc(&d_alive, alive.size() * 4));
+  DGDS_CUDA(cudaMalloc(&d_remap, s->T.cap * 4));
+  DGDS_CUDA(cudaMalloc(&d_ls, std::max<size_t>(1, live_slots.size()) * 8));
+  DGDS_CUDA(cudaMemcpyAsync(d_alive, alive.data(), alive.size() * 4, cudaMemcpyHostToDevice, s->st));
+  DGDS_CUDA(cudaMemsetAsync(d_remap, 0, s->T.cap * 4, s->st));
+  if (!live_slots.empty()) {
+    DGDS_CUDA(cudaMemcpyAsync(d_ls, live_slots.data(), live_slots.size() * 4, cudaMemcpyHostToDevice, s->st));
+    DGDS_CUDA(cudaMemcpyAsync(d_ls + live_slots.size(), live_sizes.data(), live_sizes.size() * 4,
+                              cudaMemcpyHostToDevice, s->st));
+  }
+  for (int d = 1; d <= s->D; ++d) DGDS_CUDA(dgds::launch_rebuild_level(s->T, to, d, d_alive, d_remap, s->st));
+  DGDS_CUDA(dgds::launch_remap_active(s->T.active, d_ls, d_ls + live_slots.size(),
+                                      static_cast<int64_t>(live_slots.size()), d_remap, s->T.cap, s->st));
+  DGDS_CUDA(cudaStreamSynchronize(s->st));  // host vectors above must outlive the copies
+  cudaFree(d_alive);
+  cudaFree(d_remap);
+  cudaFree(d_ls);
+  cudaFree(s->T.slots);
+  cudaFree(s->d_used);
+  s->T.slots = to.slots;
+  s->T.cap = new_cap;
+  s->T.used = d_used_new;
+  s->d_used = d_used_new;
+  return read_used(s, &s->used_ub);
+}
+
+int ensure_capacity(dgds_server* s, uint64_t worst_new) {
+  const double limit = kMaxLoad * static_cast<double>(s->T.cap);
+  if (static_cast<double>(s->used_ub + worst_new) <= limit) return DGDS_OK;
+  int rc = read_used(s, &s->used_ub);
+  if (rc) return rc;
+  if (static_cast<double>(s->used_ub + worst_new) <= limit) return DGDS_OK;
+  const uint64_t want = std::max<uint64_t>(cap_for(s->used_ub + worst_new, kTargetLoad), s->T.cap * 2);
+  if (s->used_ub + worst_new > static_cast<uint64_t>(kMaxLoad * static_cast<double>(std::min(want, kMaxCap))))
+    return fail(DGDS_ENOMEM, "draft-index arena exceeds the 32-bit node-id space");
+  return rebuild(s, want);
+}
+
+// Window insertions at positions start+1 .. start+n: sum min(D, pos).
+uint64_t worst_windows(uint64_t start, uint64_t n, uint64_t D) {
+  uint64_t total = 0;
+  const uint64_t lo = start + 1, hi = start + n;  // inclusive positions
+  if (lo <= D) {
+    const uint64_t top = std::min(hi, D);
+    total += (lo + top) * (top - lo + 1) / 2;
+  }
+  if (hi > D) total += (hi - std::max(lo, D + 1) + 1) * D;
+  return total;
+}
+
+struct PendingPiece {
+  int64_t seg;
+  uint64_t tok_off;
+  uint32_t n;
+};
+
+// Shared host logic of update_batch / update_batch_device: replies in call
+// order (DraftServer::update_cst, dgds.cpp:36-51 -> GroupDraftIndex::append,
+// cst.cpp:118-133), plus the device segment table.
+int plan_updates(dgds_server* s, int64_t n, const int32_t* handles, const int32_t* rids, const uint64_t* prev,
+                 const uint64_t* offs, double now, dgds_update_reply* rep, std::vector<dgds::AppendSeg>& segs,
+                 std::vector<dgds::AppendPiece>& pieces, uint64_t* worst) {
+  for (int64_t i = 0; i < n; ++i) {
+    int rc = check_handle(s, handles[i]);
+    if (rc) return rc;
+    if (rids[i] < 0) return fail(DGDS_EINVAL, "request_id must be nonnegative");
+    if (offs[i + 1] < offs[i]) return fail(DGDS_EINVAL, "token offsets must be nondecreasing");
+  }
+  const uint64_t stamp = ++s->batch_stamp;
+  std::vector<PendingPiece> pend;
+  segs.clear();
+  *worst = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    GroupRec& g = s->groups[handles[i]];
+    if (!live_entry(s, g, now)) {
+      int rc = create_group(s, g, s->p.default_ttl_seconds, now);  // auto-register (dgds.cpp:42-47)
+      if (rc) return rc;
+    }
+    g.expires = now + g.ttl;
+    auto it = g.streams.find(rids[i]);
+    if (it == g.streams.end()) {  // a mismatched append still creates the stream (cst.cpp:121)
+      StreamRec sr;
+      int rc = alloc_stream_slot(s, &sr.slot);
+      if (rc) return rc;
+      it = g.streams.emplace(rids[i], sr).first;
+    }
+    StreamRec& sr = it->second;
+    const uint64_t cnt = offs[i + 1] - offs[i];
+    if (prev[i] != sr.stored) {
+      rep[i] = dgds_update_reply{0, 0, g.version, sr.stored};
+      continue;
+    }
+    if (cnt == 0) {
+      rep[i] = dgds_update_reply{1, 0, g.version, sr.stored};
+      continue;
+    }
+    if (sr.batch_stamp != stamp) {
+      sr.batch_stamp = stamp;
+      sr.batch_seg = static_cast<int64_t>(segs.size());
+      dgds::AppendSeg sg{};
+      sg.stream = sr.slot;
+      sg.root = g.root;
+      sg.start = sr.stored;
+      segs.push_back(sg);
+    }
+    pend.push_back(PendingPiece{sr.batch_seg, offs[i], static_cast<uint32_t>(cnt)});
+    *worst += worst_windows(sr.stored, cnt, static_cast<uint64_t>(s->D));
+    sr.stored += cnt;
+    g.version += 1;
+    rep[i] = dgds_update_reply{1, 0, g.version, sr.stored};
+  }
+  // group pieces by segment, keeping call order inside a segment
+  std::vector<uint32_t> cnt(segs.size() + 1, 0);
+  for (const auto& pp : pend) cnt[pp.seg + 1]++;
+  for (size_t k = 0; k < segs.size(); ++k) {
+    segs[k].piece0 = cnt[k];
+    segs[k].npieces = cnt[k + 1];
+    cnt[k + 1] += cnt[k];
+  }
+  pieces.assign(pend.size(), dgds::AppendPiece{});
+  std::vector<uint32_t> fill(segs.size(), 0);
+  for (const auto& pp : pend) {
+    const uint32_t at = segs[pp.seg].piece0 + fill[pp.seg]++;
+    pieces[at] = dgds::AppendPiece{pp.tok_off, pp.n, 0};
+  }
+  return DGDS_OK;
+}
+
+// Make `st` (user stream) and the server stream observe one total order.
+struct StreamJoin {
+  dgds_server* s;
+  cudaStream_t user;
+  cudaEvent_t ev = nullptr;
+  StreamJoin(dgds_server* srv, void* u) : s(srv), user(static_cast<cudaStream_t>(u)) {
+    if (user && user != s->st) {
+      cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+      cudaEventRecord(ev, s->st);
+      cudaStreamWaitEvent(user, ev, 0);
+    }
+  }
+  cudaStream_t stream() const { return (user && user != s->st) ? user : s->st; }
+  ~StreamJoin() {
+    if (ev) {
+      cudaEventRecord(ev, user);
+      cudaStreamWaitEvent(s->st, ev, 0);
+      cudaEventDestroy(ev);
+    }
+  }
+};
+
+}  // namespace
+
+extern "C" {
+
+const char* dgds_last_error(void) { return g_err.c_str(); }
+const char* dgds_version_string(void) { return "dgds-b200 0.1 (sm_100a)"; }
+
+uint64_t dgds_fnv1a64(const void* data, size_t n) { return fnv1a64(data, n); }
+
+int32_t dgds_shard_of_group(const char* gid, size_t len, int32_t shard_count) {  // dgds.cpp:10-14
+  if (shard_count < 1) return fail(DGDS_EINVAL, "shard_count must be >= 1");
+  return static_cast<int32_t>(fnv1a64(gid, len) % static_cast<uint64_t>(shard_count));
+}
+
+int dgds_create(const dgds_params* params, dgds_server** out) {
+  if (!params || !out) return fail(DGDS_EINVAL, "null argument");
+  const dgds_params& p = *params;
+  if (p.shard_count < 1) return fail(DGDS_EINVAL, "shard_count must be >= 1");
+  if (p.max_pattern_len < 1 || p.max_spec_len < 0) return fail(DGDS_EINVAL, "draft index limits out of range");
+  if (p.max_pattern_len + p.max_spec_len > DGDS_MAX_DEPTH)
+    return fail(DGDS_EUNSUPPORTED, "max_pattern_len + max_spec_len exceeds DGDS_MAX_DEPTH (32)");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return fail(DGDS_ECUDA, "no CUDA device");
+  if (p.device < 0 || p.device >= ndev) return fail(DGDS_EINVAL, "bad device ordinal");
+  DGDS_CUDA(cudaSetDevice(p.device));
+  auto s = std::make_unique<dgds_server>();
+  s->p = p;
+  s->D = p.max_pattern_len + p.max_spec_len;
+  s->shard_counts.assign(p.shard_count, 0);
+  DGDS_CUDA(cudaStreamCreateWithFlags(&s->st, cudaStreamNonBlocking));
+  DGDS_CUDA(cudaEventCreateWithFlags(&s->staging_free, cudaEventDisableTiming));
+  const uint64_t nodes = p.expected_nodes ? p.expected_nodes : (1ull << 20);
+  uint64_t cap = std::min(cap_for(nodes, 0.5), kMaxCap);
+  s->T.cap = cap;
+  s->T.depth_cap = s->D;
+  s->T.lim_pattern = p.max_pattern_len;
+  s->T.lim_spec = p.max_spec_len;
+  DGDS_CUDA(cudaMalloc(&s->T.slots, cap * sizeof(dgds::Slot)));
+  DGDS_CUDA(cudaMemsetAsync(s->T.slots, 0, cap * sizeof(dgds::Slot), s->st));
+  DGDS_CUDA(cudaMalloc(&s->d_used, sizeof(unsigned long long)));
+  DGDS_CUDA(cudaMemsetAsync(s->d_used, 0, sizeof(unsigned long long), s->st));
+  s->T.used = s->d_used;
+  s->stream_cap = std::max<uint64_t>(p.expected_streams ? p.expected_streams : 4096, 64);
+  DGDS_CUDA(cudaMalloc(&s->T.active, s->stream_cap * dgds::kWarp * sizeof(uint32_t)));
+  DGDS_CUDA(cudaMalloc(&s->d_err, sizeof(int32_t)));
+  DGDS_CUDA(cudaMemsetAsync(s->d_err, 0, sizeof(int32_t), s->st));
+  s->root_of_cap = 1024;
+  DGDS_CUDA(cudaMalloc(&s->d_root_of, s->root_of_cap * sizeof(uint32_t)));
+  DGDS_CUDA(cudaMemsetAsync(s->d_root_of, 0, s->root_of_cap * sizeof(uint32_t), s->st));
+  DGDS_CUDA(cudaStreamSynchronize(s->st));
+  *out = s.release();
+  return DGDS_OK;
+}
+
+int dgds_destroy(dgds_server* s) {
+  if (!s) return DGDS_OK;
+  cudaSetDevice(s->p.device);
+  if (s->st) cudaStreamSynchronize(s->st);
+  cudaFree(s->T.slots);
+  cudaFree(s->T.active);
+  cudaFree(s->d_used);
+  cudaFree(s->d_root_of);
+  cudaFree(s->d_err);
+  if (s->staging_free) cudaEventDestroy(s->staging_free);
+  if (s->st) cudaStreamDestroy(s->st);
+  delete s;
+  return DGDS_OK;
+}
+
+void* dgds_cuda_stream(dgds_server* s) { return s ? static_cast<void*>(s->st) : nullptr; }
+
+int dgds_intern(dgds_server* s, const char* gid, size_t len, int32_t* handle) {
+  std::lock_guard<std::mutex> lk(s->mu);
+  std::string key(gid, len);
+  auto it = s->intern.find(key);
+  if (it != s->intern.end()) {
+    *handle = it->second;
+    return DGDS_OK;
+  }
+  const int32_t h = static_cast<int32_t>(s->groups.size());
+  GroupRec g;
+  g.gid = key;
+  g.shard = static_cast<int32_t>(fnv1a64(gid, len) % static_cast<uint64_t>(s->p.shard_count));
+  s->groups.push_back(std::move(g));
+  s->intern.emplace(std::move(key), h);
+  *handle = h;
+  return DGDS_OK;
+}
+
+int dgds_register_group(dgds_server* s, int32_t h, double ttl, double now) {  // dgds.cpp:99-110
+  std::lock_guard<std::mutex> lk(s->mu);
+  if (int rc = check_handle(s, h)) return rc;
+  if (!(ttl > 0.0)) return fail(DGDS_EINVAL, "register_group: ttl_seconds must be > 0");
+  cudaSetDevice(s->p.device);
+  GroupRec& g = s->groups[h];
+  if (!live_entry(s, g, now)) return create_group(s, g, ttl, now);
+  g.ttl = ttl;
+  g.expires = now + ttl;
+  return DGDS_OK;
+}
+
+int dgds_drop_group(dgds_server* s, int32_t h) {  // dgds.cpp:112-116
+  std::lock_guard<std::mutex> lk(s->mu);
+  if (int rc = check_handle(s, h)) return rc;
+  cudaSetDevice(s->p.device);
+  retire_group(s, s->groups[h]);
+  return DGDS_OK;
+}
+
+int dgds_sweep_expired(dgds_server* s, double now) {  // dgds.cpp:118-128
+  std::lock_guard<std::mutex> lk(s->mu);
+  cudaSetDevice(s->p.device);
+  for (auto& g : s->groups)
+    if (g.alive && g.expires < now) retire_group(s, g);
+  return DGDS_OK;
+}
+
+int dgds_has_group(dgds_server* s, int32_t h, int32_t* out) {
+  std::lock_guard<std::mutex> lk(s->mu);
+  if (int rc = check_handle(s, h)) return rc;
+  *out = s->groups[h].alive ? 1 : 0;
+  return DGDS_OK;
+}
+
+int dgds_group_version(dgds_server* s, int32_t h, uint64_t* out) {
+  std::lock_guard<std::mutex> lk(s->mu);
+  if (int rc = check_handle(s, h)) return rc;
+  *out = s->groups[h].alive ? s->groups[h].version : 0;
+  return DGDS_OK;
+}
+
+int dgds_stored_tokens(dgds_server* s, int32_t h, int32_t rid, uint64_t* out) {
+  std::lock_guard<std::mutex> lk(s->mu);
+  if (int rc = check_handle(s, h)) return rc;
+  const GroupRec& g = s->groups[h];
+  auto it = g.streams.find(rid);
+  *out = (g.alive && it != g.streams.end()) ? it->second.stored : 0;
+  return DGDS_OK;
+}
+
+int dgds_shard_group_count(dgds_server* s, int32_t shard, uint64_t* out) {
+  std::lock_guard<std::mutex> lk(s->mu);
+  if (shard < 0 || shard >= s->p.shard_count) return fail(DGDS_EINVAL, "bad shard");
+  *out = s->shard_counts[shard];
+  return DGDS_OK;
+}
+
+int dgds_node_count(dgds_server* s, uint64_t* out) {
+  std::lock_guard<std::mutex> lk(s->mu);
+  cudaSetDevice(s->p.device);
+  uint64_t u = 0;
+  if (int rc = read_used(s, &u)) return rc;
+  s->used_ub = u;
+  // + group roots, matching nodes_.size() (root counted) per live group
+  uint64_t roots = 0;
+  for (const auto& g : s->groups) roots += g.alive ? 1 : 0;
+  *out = u + roots;
+  return DGDS_OK;
+}
+
+int dgds_update_batch(dgds_server* s, int64_t n, const int32_t* handles, const int32_t* rids, const uint64_t* prev,
+                      const uint64_t* offs, const int32_t* tokens, double now, dgds_update_reply* rep) {
+  if (n < 0) return fail(DGDS_EINVAL, "negative batch size");
+  if (n == 0) return DGDS_OK;
+  std::lock_guard<std::mutex> lk(s->mu);
+  DGDS_CUDA(cudaSetDevice(s->p.device));
+  const uint64_t ntok = offs[n] - offs[0];
+  for (uint64_t i = offs[0]; i < offs[n]; ++i)
+    if (tokens[i] < 0) return fail(DGDS_EINVAL, "negative token");
+  std::vector<dgds::AppendSeg> segs;
+  std::vector<dgds::AppendPiece> pieces;
+  uint64_t worst = 0;
+  if (int rc = plan_updates(s, n, handles, rids, prev, offs, now, rep, segs, pieces, &worst)) return rc;
+  if (segs.empty()) return DGDS_OK;
+  if (int rc = ensure_capacity(s, worst)) return rc;
+  // one pinned staging block -> one H2D copy: segs | pieces | tokens
+  const size_t b_seg = segs.size() * sizeof(dgds::AppendSeg);
+  const size_t o_piece = align_up(b_seg, 256);
+  const size_t b_piece = pieces.size() * sizeof(dgds::AppendPiece);
+  const size_t o_tok = align_up(o_piece + b_piece, 256);
+  const size_t total = o_tok + ntok * sizeof(int32_t);
+  DGDS_CUDA(cudaEventSynchronize(s->staging_free));
+  if (int rc = s->h_stage.ensure(total)) return rc;
+  if (int rc = s->d_stage.ensure(total)) return rc;
+  char* h = static_cast<char*>(s->h_stage.p);
+  std::memcpy(h, segs.data(), b_seg);
+  for (auto& pc : pieces) pc.tok_off -= offs[0];
+  std::memcpy(h + o_piece, pieces.data(), b_piece);
+  std::memcpy(h + o_tok, tokens + offs[0], ntok * sizeof(int32_t));
+  char* d = static_cast<char*>(s->d_stage.p);
+  DGDS_CUDA(cudaMemcpyAsync(d, h, total, cudaMemcpyHostToDevice, s->st));
+  DGDS_CUDA(cudaEventRecord(s->staging_free, s->st));
+  DGDS_CUDA(dgds::launch_append(s->T, reinterpret_cast<const dgds::AppendSeg*>(d), static_cast<int64_t>(segs.size()),
+                                reinterpret_cast<const dgds::AppendPiece*>(d + o_piece),
+                                reinterpret_cast<const int32_t*>(d + o_tok), s->st));
+  s->used_ub += worst;
+  return DGDS_OK;
+}
+
+int dgds_update_batch_device(dgds_server* s, int64_t n, const int32_t* handles, const int32_t* rids,
+                             const uint64_t* prev, const uint64_t* offs, const int32_t* d_tokens, double now,
+                             dgds_update_reply* rep, void* stream) {
+  if (n < 0) return fail(DGDS_EINVAL, "negative batch size");
+  if (n == 0) return DGDS_OK;
+  std::lock_guard<std::mutex> lk(s->mu);
+  DGDS_CUDA(cudaSetDevice(s->p.device));
+  std::vector<dgds::AppendSeg> segs;
+  std::vector<dgds::AppendPiece> pieces;
+  uint64_t worst = 0;
+  if (int rc = plan_updates(s, n, handles, rids, prev, offs, now, rep, segs, pieces, &worst)) return rc;
+  if (segs.empty()) return DGDS_OK;
+  if (int rc = ensure_capacity(s, worst)) return rc;
+  StreamJoin join(s, stream);
+  const size_t b_seg = segs.size() * sizeof(dgds::AppendSeg);
+  const size_t o_piece = align_up(b_seg, 256);
+  const size_t total = o_piece + pieces.size() * sizeof(dgds::AppendPiece);
+  DGDS_CUDA(cudaEventSynchronize(s->staging_free));
+  if (int rc = s->h_stage.ensure(total)) return rc;
+  if (int rc = s->d_stage.ensure(total)) return rc;
+  char* h = static_cast<char*>(s->h_stage.p);
+  std::memcpy(h, segs.data(), b_seg);
+  std::memcpy(h + o_piece, pieces.data(), pieces.size() * sizeof(dgds::AppendPiece));
+  char* d = static_cast<char*>(s->d_stage.p);
+  DGDS_CUDA(cudaMemcpyAsync(d, h, total, cudaMemcpyHostToDevice, join.stream()));
+  DGDS_CUDA(cudaEventRecord(s->staging_free, join.stream()));
+  DGDS_CUDA(dgds::launch_append(s->T, reinterpret_cast<const dgds::AppendSeg*>(d), static_cast<int64_t>(segs.size()),
+                                reinterpret_cast<const dgds::AppendPiece*>(d + o_piece), d_tokens, join.stream()));
+  s->used_ub += worst;
+  return DGDS_OK;
+}
+
+int dgds_speculate_batch(dgds_server* s, int64_t n, const int32_t* handles, const uint64_t* pat_offs,
+                         const int32_t* patterns, const dgds_spec_args* args, int64_t args_stride,
+                         dgds_candidates* out) {
+  if (n < 0) return fail(DGDS_EINVAL, "negative batch size");
+  if (n == 0) return DGDS_OK;
+  if (!out) return fail(DGDS_EINVAL, "null output");
+  std::lock_guard<std::mutex> lk(s->mu);
+  DGDS_CUDA(cudaSetDevice(s->p.device));
+  const int64_t nargs = args_stride ? n : 1;
+  int32_t max_k = 1, max_s = 1;
+  for (int64_t i = 0; i < nargs; ++i) {
+    const dgds_spec_args& a = args[i * args_stride];
+    if (int rc = check_args(a)) return rc;
+    max_k = std::max(max_k, a.top_k);
+    max_s = std::max(max_s, std::min(a.max_spec_tokens, s->p.max_spec_len));
+  }
+  for (int64_t i = 0; i < n; ++i) {
+    if (int rc = check_handle(s, handles[i])) return rc;
+    if (pat_offs[i + 1] < pat_offs[i]) return fail(DGDS_EINVAL, "pattern offsets must be nondecreasing");
+  }
+  if (out->k_stride < max_k || out->s_stride < max_s) return fail(DGDS_EBUFFER, "candidate buffer strides too small");
+  const int32_t P = s->p.max_pattern_len;  // only the last max_pattern_len tokens can matter
+  // staging: handles | pat_len | patterns | args
+  const size_t o_len = align_up(n * 4, 256);
+  const size_t o_pat = align_up(o_len + n * 4, 256);
+  const size_t o_args = align_up(o_pat + static_cast<size_t>(n) * P * 4, 256);
+  const size_t in_total = o_args + nargs * sizeof(dgds_spec_args);
+  DGDS_CUDA(cudaEventSynchronize(s->staging_free));
+  if (int rc = s->h_stage.ensure(in_total)) return rc;
+  if (int rc = s->d_stage.ensure(in_total)) return rc;
+  char* h = static_cast<char*>(s->h_stage.p);
+  std::memcpy(h, handles, n * 4);
+  int32_t* hl = reinterpret_cast<int32_t*>(h + o_len);
+  int32_t* hp = reinterpret_cast<int32_t*>(h + o_pat);
+  for (int64_t i = 0; i < n; ++i) {
+    const uint64_t L = pat_offs[i + 1] - pat_offs[i];
+    hl[i] = static_cast<int32_t>(std::min<uint64_t>(L, 0x7FFFFFFF));
+    const uint64_t keep = std::min<uint64_t>(L, static_cast<uint64_t>(P));
+    std::memcpy(hp + i * P, patterns + pat_offs[i + 1] - keep, keep * 4);
+  }
+  std::memcpy(h + o_args, args, nargs * sizeof(dgds_spec_args));
+  // device outputs (internal strides), one pinned block back
+  const int32_t K = max_k, Sx = max_s;
+  const size_t o_sc = 0;
+  const size_t o_sp = align_up(o_sc + n * K * 8, 256);
+  const size_t o_nc = align_up(o_sp + n * K * 8, 256);
+  const size_t o_ln = align_up(o_nc + n * 4, 256);
+  const size_t o_tk = align_up(o_ln + n * K * 4, 256);
+  const size_t out_total = o_tk + static_cast<size_t>(n) * K * Sx * 4;
+  if (int rc = s->h_out.ensure(out_total)) return rc;
+  if (int rc = s->d_out.ensure(out_total)) return rc;
+  char* d = static_cast<char*>(s->d_stage.p);
+  char* dout = static_cast<char*>(s->d_out.p);
+  DGDS_CUDA(cudaMemcpyAsync(d, h, in_total, cudaMemcpyHostToDevice, s->st));
+  DGDS_CUDA(cudaEventRecord(s->staging_free, s->st));
+  dgds::QueryLaunch L{};
+  L.T = s->T;
+  L.root_of = s->d_root_of;
+  L.n_handles = static_cast<int32_t>(s->root_of_cap);
+  L.S = std::max(1, s->p.max_spec_len);
+  L.n = n;
+  L.handles = reinterpret_cast<const int32_t*>(d);
+  L.pat_len = reinterpret_cast<const int32_t*>(d + o_len);
+  L.patterns = reinterpret_cast<const int32_t*>(d + o_pat);
+  L.pat_stride = P;
+  L.args = reinterpret_cast<const dgds_spec_args*>(d + o_args);
+  L.args_stride = args_stride ? 1 : 0;
+  L.k_stride = K;
+  L.s_stride = Sx;
+  L.scores = reinterpret_cast<double*>(dout + o_sc);
+  L.supports = reinterpret_cast<int64_t*>(dout + o_sp);
+  L.n_cands = reinterpret_cast<int32_t*>(dout + o_nc);
+  L.lens = reinterpret_cast<int32_t*>(dout + o_ln);
+  L.tokens = reinterpret_cast<int32_t*>(dout + o_tk);
+  L.err_flag = s->d_err;
+  DGDS_CUDA(dgds::launch_query(L, max_k, s->st));
+  DGDS_CUDA(cudaMemcpyAsync(s->h_out.p, dout, out_total, cudaMemcpyDeviceToHost, s->st));
+  DGDS_CUDA(cudaStreamSynchronize(s->st));
+  const char* ho = static_cast<const char*>(s->h_out.p);
+  const double* sc = reinterpret_cast<const double*>(ho + o_sc);
+  const int64_t* sp = reinterpret_cast<const int64_t*>(ho + o_sp);
+  const int32_t* nc = reinterpret_cast<const int32_t*>(ho + o_nc);
+  const int32_t* ln = reinterpret_cast<const int32_t*>(ho + o_ln);
+  const int32_t* tk = reinterpret_cast<const int32_t*>(ho + o_tk);
+  for (int64_t q = 0; q < n; ++q) {
+    out->n_cands[q] = nc[q];
+    for (int c = 0; c < nc[q]; ++c) {
+      const int64_t si = q * K + c, di = q * out->k_stride + c;
+      out->lens[di] = ln[si];
+      out->scores[di] = sc[si];
+      out->supports[di] = sp[si];
+      std::memcpy(out->tokens + di * out->s_stride, tk + si * Sx, ln[si] * 4);
+    }
+  }
+  return DGDS_OK;
+}
+
+int dgds_speculate_device(dgds_server* s, int64_t n, const int32_t* d_handles, const int32_t* d_pat_len,
+                          const int32_t* d_patterns, int32_t pat_stride, const dgds_spec_args* d_args,
+                          int64_t args_stride, int32_t max_top_k, const dgds_candidates* d_out,
+                          const int32_t* d_truth, int32_t truth_stride, const int32_t* d_truth_left,
+                          const int32_t* d_limit, const dgds_verify_out* d_vout, dgds_query_stats* d_stats,
+                          void* stream) {
+  if (n < 0) return fail(DGDS_EINVAL, "negative batch size");
+  if (n == 0) return DGDS_OK;
+  if (max_top_k < 1 || max_top_k > DGDS_MAX_TOP_K) return fail(DGDS_EUNSUPPORTED, "max_top_k out of range");
+  if (pat_stride < s->p.max_pattern_len) return fail(DGDS_EINVAL, "pat_stride must be >= max_pattern_len");
+  if (d_out && (d_out->k_stride < max_top_k || d_out->s_stride < 1)) return fail(DGDS_EBUFFER, "bad output strides");
+  if (d_vout && (!d_truth || !d_truth_left || !d_limit)) return fail(DGDS_EINVAL, "verify needs truth inputs");
+  std::lock_guard<std::mutex> lk(s->mu);
+  DGDS_CUDA(cudaSetDevice(s->p.device));
+  StreamJoin join(s, stream);
+  dgds::QueryLaunch L{};
+  L.T = s->T;
+  L.root_of = s->d_root_of;
+  L.n_handles = static_cast<int32_t>(s->root_of_cap);
+  L.S = std::max(1, s->p.max_spec_len);
+  L.n = n;
+  L.handles = d_handles;
+  L.pat_len = d_pat_len;
+  L.patterns = d_patterns;
+  L.pat_stride = pat_stride;
+  L.args = d_args;
+  L.args_stride = args_stride;
+  if (d_out) {
+    L.k_stride = d_out->k_stride;
+    L.s_stride = d_out->s_stride;
+    L.n_cands = d_out->n_cands;
+    L.lens = d_out->lens;
+    L.scores = d_out->scores;
+    L.supports = d_out->supports;
+    L.tokens = d_out->tokens;
+  }
+  if (d_vout) {
+    L.truth = d_truth;
+    L.truth_stride = truth_stride;
+    L.truth_left = d_truth_left;
+    L.limit = d_limit;
+    L.v_drafted = d_vout->drafted;
+    L.v_accepted = d_vout->accepted;
+    L.v_emitted = d_vout->emitted;
+  }
+  L.stats = d_stats;
+  L.err_flag = s->d_err;
+  DGDS_CUDA(dgds::launch_query(L, max_top_k, join.stream()));
+  return DGDS_OK;
+}
+
+int dgds_verify_batch(dgds_server* s, int64_t n, const dgds_candidates* c, const int32_t* truth, int32_t truth_stride,
+                      const int32_t* truth_left, const int32_t* limit, dgds_verify_out* out) {
+  if (n < 0) return fail(DGDS_EINVAL, "negative batch size");
+  if (n == 0) return DGDS_OK;
+  std::lock_guard<std::mutex> lk(s->mu);
+  DGDS_CUDA(cudaSetDevice(s->p.device));
+  const int K = c->k_stride, Sx = c->s_stride;
+  const size_t o_ln = align_up(n * 4, 256);
+  const size_t o_tk = align_up(o_ln + n * K * 4, 256);
+  const size_t o_tr = align_up(o_tk + static_cast<size_t>(n) * K * Sx * 4, 256);
+  const size_t o_tl = align_up(o_tr + static_cast<size_t>(n) * truth_stride * 4, 256);
+  const size_t o_lm = align_up(o_tl + n * 4, 256);
+  const size_t in_total = o_lm + n * 4;
+  DGDS_CUDA(cudaEventSynchronize(s->staging_free));
+  if (int rc = s->h_stage.ensure(in_total)) return rc;
+  if (int rc = s->d_stage.ensure(in_total)) return rc;
+  if (int rc = s->h_out.ensure(n * 12)) return rc;
+  if (int rc = s->d_out.ensure(n * 12)) return rc;
+  char* h = static_cast<char*>(s->h_stage.p);
+  std::memcpy(h, c->n_cands, n * 4);
+  std::memcpy(h + o_ln, c->lens, n * K * 4);
+  std::memcpy(h + o_tk, c->tokens, static_cast<size_t>(n) * K * Sx * 4);
+  std::memcpy(h + o_tr, truth, static_cast<size_t>(n) * truth_stride * 4);
+  std::memcpy(h + o_tl, truth_left, n * 4);
+  std::memcpy(h + o_lm, limit, n * 4);
+  char* d = static_cast<char*>(s->d_stage.p);
+  int32_t* dv = static_cast<int32_t*>(s->d_out.p);
+  DGDS_CUDA(cudaMemcpyAsync(d, h, in_total, cudaMemcpyHostToDevice, s->st));
+  DGDS_CUDA(cudaEventRecord(s->staging_free, s->st));
+  DGDS_CUDA(dgds::launch_verify(n, K, Sx, reinterpret_cast<const int32_t*>(d), reinterpret_cast<const int32_t*>(d + o_ln),
+                                reinterpret_cast<const int32_t*>(d + o_tk), reinterpret_cast<const int32_t*>(d + o_tr),
+                                truth_stride, reinterpret_cast<const int32_t*>(d + o_tl),
+                                reinterpret_cast<const int32_t*>(d + o_lm), dv, dv + n, dv + 2 * n, s->st));
+  DGDS_CUDA(cudaMemcpyAsync(s->h_out.p, dv, n * 12, cudaMemcpyDeviceToHost, s->st));
+  DGDS_CUDA(cudaStreamSynchronize(s->st));
+  const int32_t* hv = static_cast<const int32_t*>(s->h_out.p);
+  std::memcpy(out->drafted, hv, n * 4);
+  std::memcpy(out->accepted, hv + n, n * 4);
+  std::memcpy(out->emitted, hv + 2 * n, n * 4);
+  return DGDS_OK;
+}
+
+int32_t dgds_draft_len(int32_t sd_enabled, int32_t adaptive, int32_t cap, int32_t budget, int32_t n_running) {
+  if (!sd_enabled) return 0;  // engine.cpp:78-85
+  if (n_running < 1) n_running = 1;
+  const int32_t d = adaptive ? std::min(cap, budget / n_running) : cap;
+  return std::max(d, 0);
+}
+
+int dgds_route_pack(int64_t n, int32_t world, const int32_t* d_owner, const uint32_t* d_records, int32_t rec_words,
+                    uint32_t* d_out, int64_t* d_counts, int64_t* d_perm, void* stream) {
+  if (world < 1 || world > 8) return fail(DGDS_EUNSUPPORTED, "route_pack supports 1..8 ranks");
+  if (n < 0 || rec_words < 1) return fail(DGDS_EINVAL, "bad route_pack sizes");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int64_t ntiles = std::max<int64_t>(1, (n + 1023) / 1024);
+  void* scratch = nullptr;
+  DGDS_CUDA(cudaMallocAsync(&scratch, ntiles * world * sizeof(int64_t), st));
+  cudaError_t e = dgds::launch_route_pack(n, world, d_owner, d_records, rec_words, d_out, d_counts, d_perm, scratch, st);
+  cudaFreeAsync(scratch, st);
+  if (e != cudaSuccess) return fail(DGDS_ECUDA, cudaGetErrorString(e));
+  return DGDS_OK;
+}
+
+int dgds_route_unpack(int64_t n, const uint32_t* d_in, int32_t rec_words, const int64_t* d_perm, uint32_t* d_out,
+                      void* stream) {
+  DGDS_CUDA(dgds::launch_route_unpack(n, d_in, rec_words, d_perm, d_out, static_cast<cudaStream_t>(stream)));
+  return DGDS_OK;
+}
+
+}  // extern "C"
