@@ -167,8 +167,7 @@ int dgds_update_batch_device(dgds_server* s, int64_t n, const int32_t* handles, 
 
 /* n speculate calls. Query q uses patterns[pat_offsets[q] .. pat_offsets[q+1]) and
  * args[q * args_stride] (args_stride 0 = one shared args). Host buffers; blocks until done.
- * verify_truth (optional, may be NULL): fused verification as engine.cpp:115-143 with
- * truth_next[q*truth_stride ..], truth_left[q], limit[q] -> vout. */
+ */
 int dgds_speculate_batch(dgds_server* s, int64_t n, const int32_t* handles, const uint64_t* pat_offsets,
                          const int32_t* patterns, const dgds_spec_args* args, int64_t args_stride,
                          dgds_candidates* out);
@@ -186,6 +185,13 @@ int dgds_speculate_device(dgds_server* s, int64_t n, const int32_t* d_handles, c
                           const int32_t* d_limit, const dgds_verify_out* d_vout, dgds_query_stats* d_stats,
                           void* stream);
 
+/* dgds_speculate_batch + fused verification (engine.cpp:115-143) in one host call:
+ * truth_next[q*truth_stride ..], truth_left[q], limit[q] -> vout (host buffers). */
+int dgds_speculate_verify_batch(dgds_server* s, int64_t n, const int32_t* handles, const uint64_t* pat_offsets,
+                                const int32_t* patterns, const dgds_spec_args* args, int64_t args_stride,
+                                const int32_t* truth_next, int32_t truth_stride, const int32_t* truth_left,
+                                const int32_t* limit, dgds_candidates* out, dgds_verify_out* vout);
+
 /* Verification of existing candidates (engine.cpp:115-143), host buffers. */
 int dgds_verify_batch(dgds_server* s, int64_t n, const dgds_candidates* cands, const int32_t* truth_next,
                       int32_t truth_stride, const int32_t* truth_left, const int32_t* limit,
@@ -194,6 +200,17 @@ int dgds_verify_batch(dgds_server* s, int64_t n, const dgds_candidates* cands, c
 /* Draft length policy (engine.cpp:78-85): sd disabled -> 0; adaptive -> min(cap, budget / n_running); max(.,0). */
 int32_t dgds_draft_len(int32_t sd_enabled, int32_t adaptive, int32_t per_request_cap, int32_t batch_token_budget,
                        int32_t n_running);
+
+/* ---- kernel timing (CUDA events around every append / query launch, on the launch stream) ---- */
+typedef struct dgds_profile {
+  uint64_t append_launches;
+  uint64_t query_launches;
+  double append_ms; /* summed device time of the append kernels */
+  double query_ms;  /* summed device time of the query kernels */
+} dgds_profile;
+int dgds_profile_enable(dgds_server* s, int32_t on);
+/* Synchronises on the recorded events; reset != 0 clears the accumulators. */
+int dgds_profile_read(dgds_server* s, dgds_profile* out, int32_t reset);
 
 /* ---- multi-GPU routing helpers (device, enqueued on `stream`) ----
  * Bucket n fixed-size records of rec_words 32-bit words by owner rank (owner[i] in [0, world)):

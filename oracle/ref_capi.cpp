@@ -9,6 +9,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <barrier>
 #include <chrono>
 #include <cstring>
 #include <map>
@@ -433,3 +434,143 @@ int64_t orc_ref_replay(const void* trace, const orc_replay_cfg* cfg, int32_t* st
 }
 
 }  // extern "C"
+
+extern "C" {
+
+// ---------------------------------------------------------------------------
+// CPU baseline: the reference GroupDraftIndex driven thread-per-shard over the
+// host cores: groups are partitioned by the reference
+// shard_of_group(gid, T); every thread owns its shard's indexes, so there is no
+// locking. Phases per step: append (one record per stream) then queries with
+// verification (engine.cpp:115-143 rule), each bracketed by a barrier and
+// timed with steady_clock.
+
+typedef struct orc_bench_cfg {
+  int32_t threads;
+  int32_t n_streams;      // streams in the sample (group-major)
+  int32_t group_size;
+  int32_t steps;          // timed + warmup steps provided in the schedule
+  int32_t record_tokens;  // tokens per append record (DraftClient flush size)
+  int32_t queries_per_step;
+  int32_t max_pattern_len, max_spec_len;  // Limits
+  int32_t pad_;
+  orc_args args;
+} orc_bench_cfg;
+
+// out[0] prefill seconds, out[1] prefill tokens, then per step s:
+// out[2+4s] append seconds, out[3+4s] tokens appended, out[4+4s] query seconds, out[5+4s] queries
+int orc_ref_bench(const orc_bench_cfg* cfg, const char* const* gids, const int32_t* tokens, const int64_t* offsets,
+                  const int64_t* prefill, const int32_t* q_stream, const int64_t* q_pos, double* out) {
+  try {
+    const int T = std::max(1, cfg->threads);
+    const int S = cfg->n_streams, G = cfg->group_size;
+    const int ngroups = S / G;
+    GroupDraftIndex::Limits lim;
+    lim.max_pattern_len = cfg->max_pattern_len;
+    lim.max_spec_len = cfg->max_spec_len;
+    std::vector<std::unique_ptr<GroupDraftIndex>> idx(ngroups);
+    std::vector<int> owner(ngroups);
+    std::vector<std::vector<int>> mine(T);
+    for (int g = 0; g < ngroups; ++g) {
+      idx[g] = std::make_unique<GroupDraftIndex>(gids[g], lim);
+      owner[g] = shard_of_group(gids[g], T);
+      mine[owner[g]].push_back(g);
+    }
+    const SpeculationArgs a = to_args(&cfg->args);
+    const int rt = cfg->record_tokens;
+    std::vector<int64_t> pos(prefill, prefill + S);
+    // queries of each step bucketed by owner thread (outside the timed phases)
+    std::vector<std::vector<std::vector<int64_t>>> qb(cfg->steps, std::vector<std::vector<int64_t>>(T));
+    for (int s = 0; s < cfg->steps; ++s)
+      for (int i = 0; i < cfg->queries_per_step; ++i) {
+        const int64_t k = static_cast<int64_t>(s) * cfg->queries_per_step + i;
+        qb[s][owner[q_stream[k] / G]].push_back(k);
+      }
+    std::barrier sync(T + 1);
+    std::atomic<int64_t> appended{0};
+    std::atomic<int64_t> sink{0};
+    auto worker = [&](int t) {
+      // prefill: records of rt tokens, round-robin over the thread's streams
+      sync.arrive_and_wait();
+      for (int g : mine[t]) {
+        for (int r = 0; r < G; ++r) {
+          const int st = g * G + r;
+          for (int64_t p = 0; p < prefill[st]; p += rt) {
+            const int64_t n = std::min<int64_t>(rt, prefill[st] - p);
+            idx[g]->append(r, static_cast<uint64_t>(p), std::span<const Token>(tokens + offsets[st] + p, n));
+          }
+        }
+      }
+      sync.arrive_and_wait();
+      for (int s = 0; s < cfg->steps; ++s) {
+        sync.arrive_and_wait();  // append phase
+        int64_t app = 0;
+        for (int g : mine[t])
+          for (int r = 0; r < G; ++r) {
+            const int st = g * G + r;
+            const int64_t len = offsets[st + 1] - offsets[st];
+            const int64_t p = pos[st];
+            const int64_t n = std::min<int64_t>(rt, len - p);
+            if (n <= 0) continue;
+            idx[g]->append(r, static_cast<uint64_t>(p), std::span<const Token>(tokens + offsets[st] + p, n));
+            pos[st] = p + n;
+            app += n;
+          }
+        appended += app;
+        sync.arrive_and_wait();
+        sync.arrive_and_wait();  // query phase
+        int64_t acc_sum = 0;
+        for (int64_t k : qb[s][t]) {
+          const int st = q_stream[k];
+          const int64_t p = q_pos[k];
+          const int64_t plen = std::min<int64_t>(a.pattern_lookup_max, p);
+          auto c = idx[st / G]->speculate(std::span<const Token>(tokens + offsets[st] + p - plen, plen), a);
+          const int64_t len = offsets[st + 1] - offsets[st];
+          const int truth_left = static_cast<int>(len - p);
+          int acc = 0;
+          for (const auto& d : c) {
+            int m = 0;
+            const int cap = std::min<int>(static_cast<int>(d.tokens.size()), truth_left);
+            while (m < cap && d.tokens[m] == tokens[offsets[st] + p + m]) ++m;
+            acc = std::max(acc, m);
+          }
+          acc_sum += std::min(acc + 1, truth_left);
+        }
+        sink += acc_sum;
+        sync.arrive_and_wait();
+      }
+    };
+    std::vector<std::thread> th;
+    for (int t = 0; t < T; ++t) th.emplace_back(worker, t);
+    using clk = std::chrono::steady_clock;
+    auto secs = [](clk::time_point a0, clk::time_point b0) { return std::chrono::duration<double>(b0 - a0).count(); };
+    sync.arrive_and_wait();
+    auto t0 = clk::now();
+    sync.arrive_and_wait();
+    out[0] = secs(t0, clk::now());
+    int64_t pre = 0;
+    for (int st = 0; st < S; ++st) pre += prefill[st];
+    out[1] = static_cast<double>(pre);
+    for (int s = 0; s < cfg->steps; ++s) {
+      appended = 0;
+      auto a0 = clk::now();
+      sync.arrive_and_wait();
+      sync.arrive_and_wait();
+      auto a1 = clk::now();
+      sync.arrive_and_wait();
+      sync.arrive_and_wait();
+      auto a2 = clk::now();
+      out[2 + 4 * s] = secs(a0, a1);
+      out[3 + 4 * s] = static_cast<double>(appended.load());
+      out[4 + 4 * s] = secs(a1, a2);
+      out[5 + 4 * s] = static_cast<double>(cfg->queries_per_step);
+    }
+    for (auto& x : th) x.join();
+    return sink.load() >= 0 ? 0 : 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
+}  // extern "C" (bench)

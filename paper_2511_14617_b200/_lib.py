@@ -81,6 +81,11 @@ class QueryStats(C.Structure):
     ]
 
 
+class Profile(C.Structure):
+    _fields_ = [("append_launches", C.c_uint64), ("query_launches", C.c_uint64), ("append_ms", C.c_double),
+                ("query_ms", C.c_double)]
+
+
 class WorkloadCfg(C.Structure):
     _fields_ = [
         ("num_groups", C.c_int32),
@@ -134,6 +139,10 @@ EXPORTS = {
     "dgds_speculate_batch": (C.c_int, [_P, _I64, _P, _P, _P, _P, _I64, C.POINTER(Candidates)]),
     "dgds_speculate_device": (C.c_int, [_P, _I64, _P, _P, _P, _I32, _P, _I64, _I32, C.POINTER(Candidates), _P, _I32,
                                         _P, _P, C.POINTER(VerifyOut), _P, _P]),
+    "dgds_speculate_verify_batch": (C.c_int, [_P, _I64, _P, _P, _P, _P, _I64, _P, _I32, _P, _P,
+                                              C.POINTER(Candidates), C.POINTER(VerifyOut)]),
+    "dgds_profile_enable": (C.c_int, [_P, _I32]),
+    "dgds_profile_read": (C.c_int, [_P, C.POINTER(Profile), _I32]),
     "dgds_verify_batch": (C.c_int, [_P, _I64, C.POINTER(Candidates), _P, _I32, _P, _P, C.POINTER(VerifyOut)]),
     "dgds_draft_len": (_I32, [_I32, _I32, _I32, _I32, _I32]),
     "dgds_route_pack": (C.c_int, [_I64, _I32, _P, _P, _I32, _P, _P, _P, _P]),

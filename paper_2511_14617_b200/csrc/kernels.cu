@@ -201,7 +201,7 @@ __global__ void __launch_bounds__(kBlock) k_query(QueryLaunch P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = lane_id();
   const int wib = threadIdx.x / kWarp;
-  const int64_t q = static_cast<int64_t>(blockIdx.x) * kWarpsPerBlock + wib;
+  const int64_t q = static_cast<int64_t>(blockIdx.x) * (blockDim.x / kWarp) + wib;
   if (q >= P.n) return;  // warp-uniform
 
   const int S = P.S;
@@ -683,13 +683,16 @@ __global__ void k_route_gather(int64_t n, const uint32_t* __restrict__ in, int32
 template <int K>
 cudaError_t launch_query_k(const QueryLaunch& L, cudaStream_t st) {
   const QSmemLayout Ly = qsmem_layout(K, L.S);
-  const size_t smem = static_cast<size_t>(Ly.total) * kWarpsPerBlock;
+  constexpr int kSmemBudget = 200 * 1024;
+  int wpb = kWarpsPerBlock;
+  while (wpb > 1 && Ly.total * wpb > kSmemBudget) --wpb;
+  const size_t smem = static_cast<size_t>(Ly.total) * wpb;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(k_query<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
   }
-  const int64_t blocks = (L.n + kWarpsPerBlock - 1) / kWarpsPerBlock;
-  k_query<K><<<static_cast<unsigned>(blocks), kBlock, smem, st>>>(L);
+  const int64_t blocks = (L.n + wpb - 1) / wpb;
+  k_query<K><<<static_cast<unsigned>(blocks), wpb * kWarp, smem, st>>>(L);
   return cudaGetLastError();
 }
 

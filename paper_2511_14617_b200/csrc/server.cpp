@@ -142,6 +142,13 @@ struct dgds_server {
   DevBuf d_stage, d_out;
   int32_t* d_err = nullptr;
   std::mutex mu;  // calls on one handle are serialized
+
+  // kernel timing: event pairs around launches (kind 0 append, 1 query)
+  bool profiling = false;
+  std::vector<cudaEvent_t> ev_pool;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_pending[2];
+  uint64_t prof_launches[2] = {0, 0};
+  double prof_ms[2] = {0.0, 0.0};
 };
 
 namespace {
@@ -401,6 +408,38 @@ int plan_updates(dgds_server* s, int64_t n, const int32_t* handles, const int32_
   return DGDS_OK;
 }
 
+cudaEvent_t pooled_event(dgds_server* s) {
+  if (!s->ev_pool.empty()) {
+    cudaEvent_t e = s->ev_pool.back();
+    s->ev_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+
+// Brackets one kernel launch with events on its stream when profiling is on.
+struct LaunchTimer {
+  dgds_server* s;
+  int kind;
+  cudaStream_t st;
+  cudaEvent_t a = nullptr, b = nullptr;
+  LaunchTimer(dgds_server* srv, int k, cudaStream_t stream) : s(srv), kind(k), st(stream) {
+    if (s->profiling) {
+      a = pooled_event(s);
+      b = pooled_event(s);
+      cudaEventRecord(a, st);
+    }
+  }
+  ~LaunchTimer() {
+    if (a) {
+      cudaEventRecord(b, st);
+      s->ev_pending[kind].emplace_back(a, b);
+    }
+  }
+};
+
 // Make `st` (user stream) and the server stream observe one total order.
 struct StreamJoin {
   dgds_server* s;
@@ -487,6 +526,12 @@ int dgds_destroy(dgds_server* s) {
   cudaFree(s->d_root_of);
   cudaFree(s->d_err);
   if (s->staging_free) cudaEventDestroy(s->staging_free);
+  for (auto e : s->ev_pool) cudaEventDestroy(e);
+  for (auto& v : s->ev_pending)
+    for (auto& pr : v) {
+      cudaEventDestroy(pr.first);
+      cudaEventDestroy(pr.second);
+    }
   if (s->st) cudaStreamDestroy(s->st);
   delete s;
   return DGDS_OK;
@@ -615,9 +660,12 @@ int dgds_update_batch(dgds_server* s, int64_t n, const int32_t* handles, const i
   char* d = static_cast<char*>(s->d_stage.p);
   DGDS_CUDA(cudaMemcpyAsync(d, h, total, cudaMemcpyHostToDevice, s->st));
   DGDS_CUDA(cudaEventRecord(s->staging_free, s->st));
-  DGDS_CUDA(dgds::launch_append(s->T, reinterpret_cast<const dgds::AppendSeg*>(d), static_cast<int64_t>(segs.size()),
-                                reinterpret_cast<const dgds::AppendPiece*>(d + o_piece),
-                                reinterpret_cast<const int32_t*>(d + o_tok), s->st));
+  {
+    LaunchTimer lt(s, 0, s->st);
+    DGDS_CUDA(dgds::launch_append(s->T, reinterpret_cast<const dgds::AppendSeg*>(d),
+                                  static_cast<int64_t>(segs.size()), reinterpret_cast<const dgds::AppendPiece*>(d + o_piece),
+                                  reinterpret_cast<const int32_t*>(d + o_tok), s->st));
+  }
   s->used_ub += worst;
   return DGDS_OK;
 }
@@ -648,15 +696,20 @@ int dgds_update_batch_device(dgds_server* s, int64_t n, const int32_t* handles, 
   char* d = static_cast<char*>(s->d_stage.p);
   DGDS_CUDA(cudaMemcpyAsync(d, h, total, cudaMemcpyHostToDevice, join.stream()));
   DGDS_CUDA(cudaEventRecord(s->staging_free, join.stream()));
-  DGDS_CUDA(dgds::launch_append(s->T, reinterpret_cast<const dgds::AppendSeg*>(d), static_cast<int64_t>(segs.size()),
-                                reinterpret_cast<const dgds::AppendPiece*>(d + o_piece), d_tokens, join.stream()));
+  {
+    LaunchTimer lt(s, 0, join.stream());
+    DGDS_CUDA(dgds::launch_append(s->T, reinterpret_cast<const dgds::AppendSeg*>(d),
+                                  static_cast<int64_t>(segs.size()),
+                                  reinterpret_cast<const dgds::AppendPiece*>(d + o_piece), d_tokens, join.stream()));
+  }
   s->used_ub += worst;
   return DGDS_OK;
 }
 
-int dgds_speculate_batch(dgds_server* s, int64_t n, const int32_t* handles, const uint64_t* pat_offs,
-                         const int32_t* patterns, const dgds_spec_args* args, int64_t args_stride,
-                         dgds_candidates* out) {
+int dgds_speculate_verify_batch(dgds_server* s, int64_t n, const int32_t* handles, const uint64_t* pat_offs,
+                                const int32_t* patterns, const dgds_spec_args* args, int64_t args_stride,
+                                const int32_t* truth, int32_t truth_stride, const int32_t* truth_left,
+                                const int32_t* limit, dgds_candidates* out, dgds_verify_out* vout) {
   if (n < 0) return fail(DGDS_EINVAL, "negative batch size");
   if (n == 0) return DGDS_OK;
   if (!out) return fail(DGDS_EINVAL, "null output");
@@ -695,6 +748,31 @@ int dgds_speculate_batch(dgds_server* s, int64_t n, const int32_t* handles, cons
     std::memcpy(hp + i * P, patterns + pat_offs[i + 1] - keep, keep * 4);
   }
   std::memcpy(h + o_args, args, nargs * sizeof(dgds_spec_args));
+  const bool verify = vout != nullptr;
+  size_t o_tr = 0, o_tl = 0, o_lm = 0, in_all = in_total;
+  if (verify) {
+    if (!truth || !truth_left || !limit || truth_stride < 0) return fail(DGDS_EINVAL, "verify needs truth inputs");
+    o_tr = align_up(in_total, 256);
+    o_tl = align_up(o_tr + static_cast<size_t>(n) * truth_stride * 4, 256);
+    o_lm = align_up(o_tl + n * 4, 256);
+    in_all = o_lm + n * 4;
+    if (int rc = s->h_stage.ensure(in_all)) return rc;
+    if (int rc = s->d_stage.ensure(in_all)) return rc;
+    h = static_cast<char*>(s->h_stage.p);
+    std::memcpy(h, handles, n * 4);  // re-stage after a possible reallocation
+    hl = reinterpret_cast<int32_t*>(h + o_len);
+    hp = reinterpret_cast<int32_t*>(h + o_pat);
+    for (int64_t i = 0; i < n; ++i) {
+      const uint64_t Lp = pat_offs[i + 1] - pat_offs[i];
+      hl[i] = static_cast<int32_t>(std::min<uint64_t>(Lp, 0x7FFFFFFF));
+      const uint64_t keep = std::min<uint64_t>(Lp, static_cast<uint64_t>(P));
+      std::memcpy(hp + i * P, patterns + pat_offs[i + 1] - keep, keep * 4);
+    }
+    std::memcpy(h + o_args, args, nargs * sizeof(dgds_spec_args));
+    std::memcpy(h + o_tr, truth, static_cast<size_t>(n) * truth_stride * 4);
+    std::memcpy(h + o_tl, truth_left, n * 4);
+    std::memcpy(h + o_lm, limit, n * 4);
+  }
   // device outputs (internal strides), one pinned block back
   const int32_t K = max_k, Sx = max_s;
   const size_t o_sc = 0;
@@ -702,12 +780,13 @@ int dgds_speculate_batch(dgds_server* s, int64_t n, const int32_t* handles, cons
   const size_t o_nc = align_up(o_sp + n * K * 8, 256);
   const size_t o_ln = align_up(o_nc + n * 4, 256);
   const size_t o_tk = align_up(o_ln + n * K * 4, 256);
-  const size_t out_total = o_tk + static_cast<size_t>(n) * K * Sx * 4;
+  const size_t o_v = align_up(o_tk + static_cast<size_t>(n) * K * Sx * 4, 256);
+  const size_t out_total = o_v + (verify ? static_cast<size_t>(n) * 12 : 0);
   if (int rc = s->h_out.ensure(out_total)) return rc;
   if (int rc = s->d_out.ensure(out_total)) return rc;
   char* d = static_cast<char*>(s->d_stage.p);
   char* dout = static_cast<char*>(s->d_out.p);
-  DGDS_CUDA(cudaMemcpyAsync(d, h, in_total, cudaMemcpyHostToDevice, s->st));
+  DGDS_CUDA(cudaMemcpyAsync(d, h, in_all, cudaMemcpyHostToDevice, s->st));
   DGDS_CUDA(cudaEventRecord(s->staging_free, s->st));
   dgds::QueryLaunch L{};
   L.T = s->T;
@@ -729,7 +808,19 @@ int dgds_speculate_batch(dgds_server* s, int64_t n, const int32_t* handles, cons
   L.lens = reinterpret_cast<int32_t*>(dout + o_ln);
   L.tokens = reinterpret_cast<int32_t*>(dout + o_tk);
   L.err_flag = s->d_err;
-  DGDS_CUDA(dgds::launch_query(L, max_k, s->st));
+  if (verify) {
+    L.truth = reinterpret_cast<const int32_t*>(d + o_tr);
+    L.truth_stride = truth_stride;
+    L.truth_left = reinterpret_cast<const int32_t*>(d + o_tl);
+    L.limit = reinterpret_cast<const int32_t*>(d + o_lm);
+    L.v_drafted = reinterpret_cast<int32_t*>(dout + o_v);
+    L.v_accepted = L.v_drafted + n;
+    L.v_emitted = L.v_drafted + 2 * n;
+  }
+  {
+    LaunchTimer lt(s, 1, s->st);
+    DGDS_CUDA(dgds::launch_query(L, max_k, s->st));
+  }
   DGDS_CUDA(cudaMemcpyAsync(s->h_out.p, dout, out_total, cudaMemcpyDeviceToHost, s->st));
   DGDS_CUDA(cudaStreamSynchronize(s->st));
   const char* ho = static_cast<const char*>(s->h_out.p);
@@ -748,7 +839,20 @@ int dgds_speculate_batch(dgds_server* s, int64_t n, const int32_t* handles, cons
       std::memcpy(out->tokens + di * out->s_stride, tk + si * Sx, ln[si] * 4);
     }
   }
+  if (verify) {
+    const int32_t* hv = reinterpret_cast<const int32_t*>(ho + o_v);
+    std::memcpy(vout->drafted, hv, n * 4);
+    std::memcpy(vout->accepted, hv + n, n * 4);
+    std::memcpy(vout->emitted, hv + 2 * n, n * 4);
+  }
   return DGDS_OK;
+}
+
+int dgds_speculate_batch(dgds_server* s, int64_t n, const int32_t* handles, const uint64_t* pat_offs,
+                         const int32_t* patterns, const dgds_spec_args* args, int64_t args_stride,
+                         dgds_candidates* out) {
+  return dgds_speculate_verify_batch(s, n, handles, pat_offs, patterns, args, args_stride, nullptr, 0, nullptr,
+                                     nullptr, out, nullptr);
 }
 
 int dgds_speculate_device(dgds_server* s, int64_t n, const int32_t* d_handles, const int32_t* d_pat_len,
@@ -798,7 +902,10 @@ int dgds_speculate_device(dgds_server* s, int64_t n, const int32_t* d_handles, c
   }
   L.stats = d_stats;
   L.err_flag = s->d_err;
-  DGDS_CUDA(dgds::launch_query(L, max_top_k, join.stream()));
+  {
+    LaunchTimer lt(s, 1, join.stream());
+    DGDS_CUDA(dgds::launch_query(L, max_top_k, join.stream()));
+  }
   return DGDS_OK;
 }
 
@@ -849,6 +956,38 @@ int32_t dgds_draft_len(int32_t sd_enabled, int32_t adaptive, int32_t cap, int32_
   if (n_running < 1) n_running = 1;
   const int32_t d = adaptive ? std::min(cap, budget / n_running) : cap;
   return std::max(d, 0);
+}
+
+int dgds_profile_enable(dgds_server* s, int32_t on) {
+  std::lock_guard<std::mutex> lk(s->mu);
+  s->profiling = on != 0;
+  return DGDS_OK;
+}
+
+int dgds_profile_read(dgds_server* s, dgds_profile* out, int32_t reset) {
+  std::lock_guard<std::mutex> lk(s->mu);
+  DGDS_CUDA(cudaSetDevice(s->p.device));
+  for (int k = 0; k < 2; ++k) {
+    for (auto& pr : s->ev_pending[k]) {
+      DGDS_CUDA(cudaEventSynchronize(pr.second));
+      float ms = 0.f;
+      DGDS_CUDA(cudaEventElapsedTime(&ms, pr.first, pr.second));
+      s->prof_ms[k] += ms;
+      s->prof_launches[k] += 1;
+      s->ev_pool.push_back(pr.first);
+      s->ev_pool.push_back(pr.second);
+    }
+    s->ev_pending[k].clear();
+  }
+  out->append_launches = s->prof_launches[0];
+  out->query_launches = s->prof_launches[1];
+  out->append_ms = s->prof_ms[0];
+  out->query_ms = s->prof_ms[1];
+  if (reset) {
+    s->prof_launches[0] = s->prof_launches[1] = 0;
+    s->prof_ms[0] = s->prof_ms[1] = 0.0;
+  }
+  return DGDS_OK;
 }
 
 int dgds_route_pack(int64_t n, int32_t world, const int32_t* d_owner, const uint32_t* d_records, int32_t rec_words,

@@ -49,6 +49,7 @@ struct SlotView {  // the fields a query needs, from one 256-bit load
   uint32_t count;
   uint32_t first_child;
   uint32_t next_sibling;
+  unsigned long long tail;  // depth | root (unused by queries)
 };
 
 struct DevTrie {
@@ -90,7 +91,7 @@ __device__ __forceinline__ SlotView load_slot_nc(const Slot* p) {
   v.count = static_cast<uint32_t>(b);
   v.first_child = static_cast<uint32_t>(b >> 32);
   v.next_sibling = static_cast<uint32_t>(c);
-  (void)d_unused;
+  v.tail = d_unused;
   return v;
 }
 
