@@ -384,7 +384,7 @@ def main_b200(args):
         srv.update_device(app["h"], app["r"], app["prev"], app["offs"], app["d_tok"].data_ptr(), 0.0, 0)
         _lib.check(L.dgds_speculate_device(
             srv.handle, Q, C.c_void_p(qd["h"].data_ptr()), C.c_void_p(qd["pl"].data_ptr()),
-            C.c_void_p(qd["pat"].data_ptr()), 8, C.c_void_p(d_args.data_ptr()), 0, kq, C.byref(cand),
+            C.c_void_p(qd["pat"].data_ptr()), 8, C.c_void_p(d_args.data_ptr()), 0, kq, dl, C.byref(cand),
             C.c_void_p(qd["tru"].data_ptr()), dl, C.c_void_p(qd["tl"].data_ptr()), C.c_void_p(qd["lim"].data_ptr()),
             C.byref(vo), C.c_void_p(d_stats.data_ptr()) if stats else None, None))
 

@@ -175,12 +175,14 @@ int dgds_speculate_batch(dgds_server* s, int64_t n, const int32_t* handles, cons
 /* Zero-copy query over device buffers, enqueued on `stream` (NULL = server stream), no sync.
  * d_handles[n], d_pat_len[n], d_patterns[n * pat_stride] (the LAST d_pat_len[q] tokens of each
  * pattern, left-aligned; only the last max_pattern_len can matter), d_args[q * args_stride].
- * max_top_k bounds args.top_k over the batch (selects the kernel instance).
+ * max_top_k bounds args.top_k and max_spec bounds min(args.max_spec_tokens, max_spec_len) over the
+ * batch (they select the kernel instance; max_spec <= 0 means max_spec_len). A query outside the
+ * bounds returns no candidates and raises the server's device error flag.
  * Optional fused verify: d_truth (n * truth_stride next ground-truth tokens), d_truth_left[n],
  * d_limit[n] -> d_vout (all device) — may be NULL. Optional d_stats accumulates counters. */
 int dgds_speculate_device(dgds_server* s, int64_t n, const int32_t* d_handles, const int32_t* d_pat_len,
                           const int32_t* d_patterns, int32_t pat_stride, const dgds_spec_args* d_args,
-                          int64_t args_stride, int32_t max_top_k, const dgds_candidates* d_out,
+                          int64_t args_stride, int32_t max_top_k, int32_t max_spec, const dgds_candidates* d_out,
                           const int32_t* d_truth, int32_t truth_stride, const int32_t* d_truth_left,
                           const int32_t* d_limit, const dgds_verify_out* d_vout, dgds_query_stats* d_stats,
                           void* stream);

@@ -137,7 +137,8 @@ EXPORTS = {
     "dgds_update_batch": (C.c_int, [_P, _I64, _P, _P, _P, _P, _P, _D, _P]),
     "dgds_update_batch_device": (C.c_int, [_P, _I64, _P, _P, _P, _P, _P, _D, _P, _P]),
     "dgds_speculate_batch": (C.c_int, [_P, _I64, _P, _P, _P, _P, _I64, C.POINTER(Candidates)]),
-    "dgds_speculate_device": (C.c_int, [_P, _I64, _P, _P, _P, _I32, _P, _I64, _I32, C.POINTER(Candidates), _P, _I32,
+    "dgds_speculate_device": (C.c_int, [_P, _I64, _P, _P, _P, _I32, _P, _I64, _I32, _I32, C.POINTER(Candidates), _P,
+                                        _I32,
                                         _P, _P, C.POINTER(VerifyOut), _P, _P]),
     "dgds_speculate_verify_batch": (C.c_int, [_P, _I64, _P, _P, _P, _P, _I64, _P, _I32, _P, _P,
                                               C.POINTER(Candidates), C.POINTER(VerifyOut)]),

@@ -1,19 +1,21 @@
 // kernels.cu — sm_100a kernels of the DGDS hot path.
 //
-//   K1 k_append      batched incremental insertion of appended tokens into the
-//                    per-group counted suffix tries (GroupDraftIndex::append /
-//                    insert_token / ensure_child, proj/src/cst.cpp:90-133).
-//   K2 k_query<K>    batched longest-suffix match + top-k beam expansion
-//                    (GroupDraftIndex::speculate, cst.cpp:153-228), one warp per
-//                    request, with
-//   K3               fused verification / accept length (Instance::decode_step,
-//                    proj/src/engine.cpp:115-143); k_verify is the standalone form.
-//   k_rebuild_level  arena growth + GC of dropped groups (no reference analogue:
-//                    the reference's EdgeMap::grow, cst.cpp:63-74, rehashes keys only).
-//   k_route_*        owner bucketing for the multi-GPU all-to-all (dgds.cpp:10-14 routing).
+//   K1 k_append        batched incremental insertion of appended tokens into the
+//                      per-group counted suffix tries (GroupDraftIndex::append /
+//                      insert_token / ensure_child, proj/src/cst.cpp:90-133).
+//   K2 k_query<G,S>    batched longest-suffix match + top-k beam expansion
+//                      (GroupDraftIndex::speculate, cst.cpp:153-228): one G-lane
+//                      tile (sub-warp) per request, with
+//   K3                 fused verification / accept length (Instance::decode_step,
+//                      proj/src/engine.cpp:115-143); k_verify is the standalone form.
+//   k_rebuild_*        arena growth + GC of dropped groups (cst.cpp:63-74 grows the
+//                      reference's EdgeMap; here the whole slot table is re-placed).
+//   k_route_*          owner bucketing for the multi-GPU all-to-all (dgds.cpp:10-14 routing).
 //
 // Nothing here is a dense contraction, so there is no tensor-core path: every
 // kernel is bound by dependent 32-B sector accesses to HBM / L2.
+#include <cooperative_groups.h>
+#include <cooperative_groups/reduce.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -21,6 +23,8 @@
 #include "kernels.h"
 
 namespace dgds {
+
+namespace cg = cooperative_groups;
 
 namespace {
 
@@ -33,32 +37,40 @@ __device__ __forceinline__ int lane_id() { return threadIdx.x & (kWarp - 1); }
 // ---------------------------------------------------------------------------
 // K1: append
 //
-// One warp per stream segment. Lane i keeps active[i], the node of the last
-// (i+1)-token context of the stream (Stream::active, cst.hpp:115-118). For
-// each new token t the lanes i < min(depth_cap, len+1) ensure the child
-// (active[i-1], t) — lane 0 uses the group root — and bump its count, exactly
-// insert_token's loop (cst.cpp:105-116) with the depth levels in parallel:
-// up to 24 independent claim-or-find CASes in flight per warp per token.
+// One warp per stream segment. Lane i owns window length i+1 (Stream::active[i],
+// cst.hpp:115-118). Per token t, lanes i < min(depth_cap, len+1) claim-or-find
+// the window that ends at t: key {hash, parent = active[i-1] of the previous
+// token (group root for lane 0), t}, then count it — insert_token's loop
+// (cst.cpp:105-116) with the depth levels in parallel.
+//
+// Pass 1 only computes every window's content hash for the whole segment and
+// prefetches its home slot into L2; pass 2 runs the inherently sequential
+// claim chain (a token's parents are the previous token's nodes), whose CASes
+// then hit L2 instead of DRAM.
 
-struct EnsureResult {
-  uint32_t id;
-  bool inserted;
-};
-
-__device__ __forceinline__ EnsureResult ensure_child(const DevTrie& T, uint32_t parent, int32_t token, uint32_t depth,
-                                                     uint32_t root) {
-  const unsigned long long key = edge_key(parent, token);
-  uint64_t i = home_slot(key, T.cap);
+__device__ __forceinline__ void claim(const DevTrie& T, unsigned long long h, uint32_t parent, int32_t token,
+                                      uint32_t root, uint32_t& id, bool& inserted) {
+  const unsigned long long pt = pack_pt(parent, token);
+  uint64_t i = home_slot(h, T.cap);
   while (true) {
     Slot* s = T.slots + i;
-    const unsigned long long old = atomicCAS(&s->key, 0ull, key);
-    if (old == 0ull || old == key) {
+    unsigned long long o0, o1;
+    // 128-bit CAS on {h, parent|token}: empty -> ours (claim), else returns the occupant
+    asm volatile(
+        "{\n\t.reg .b128 c, v, o;\n\t"
+        "mov.b128 c, {%2, %3};\n\t"
+        "mov.b128 v, {%4, %5};\n\t"
+        "atom.global.cas.b128 o, [%6], c, v;\n\t"
+        "mov.b128 {%0, %1}, o;\n\t}"
+        : "=l"(o0), "=l"(o1)
+        : "l"(0ull), "l"(0ull), "l"(h), "l"(pt), "l"(s)
+        : "memory");
+    if (o0 == 0ull || (o0 == h && o1 == pt)) {
       atomicAdd(&s->count, 1u);  // RED: result unused
-      if (old == 0ull) {
-        s->depth = depth;
-        s->root = root;
-      }
-      return EnsureResult{static_cast<uint32_t>(i + 1), old == 0ull};
+      inserted = (o0 == 0ull);
+      if (inserted) s->root = root;
+      id = static_cast<uint32_t>(i + 1);
+      return;
     }
     i = (i + 1 == T.cap) ? 0 : i + 1;
   }
@@ -75,40 +87,81 @@ __global__ void __launch_bounds__(kBlock) k_append(DevTrie T, const AppendSeg* _
 
   for (int64_t sg = warp; sg < nseg; sg += nwarps) {
     const AppendSeg g = segs[sg];
-    uint64_t len = g.start;
+    const uint64_t len0 = g.start;
     uint32_t* act_row = T.active + static_cast<uint64_t>(g.stream) * kWarp;
-    uint32_t a = (lane < D && static_cast<uint64_t>(lane) < len) ? act_row[lane] : 0u;
-    // deferred sibling link of the node this lane created at the previous token
+    int32_t* tail_row = T.tail + static_cast<uint64_t>(g.stream) * kWarp;
+    const unsigned long long hr = root_hash(g.root);
+
+    // hashes of the windows ending at the last stored token, from the tail ring
+    unsigned long long h_init = 0;
+    {
+      const int have = static_cast<int>(min(static_cast<uint64_t>(D), len0));
+      const int32_t mytail = tail_row[lane];
+      for (int k = have; k > 0; --k) {  // positions len0-k .. len0-1
+        const int32_t t = __shfl_sync(kFull, mytail, static_cast<int>((len0 - k) & 31));
+        const unsigned long long up = __shfl_up_sync(kFull, h_init, 1);
+        h_init = hash_step(lane == 0 ? hr : up, t);
+      }
+    }
+
+    // pass 1: hash every window of the segment and prefetch its home slot
+    {
+      unsigned long long h = h_init;
+      uint64_t len = len0;
+      for (uint32_t p = 0; p < g.npieces; ++p) {
+        const AppendPiece pc = pieces[g.piece0 + p];
+        for (uint32_t base = 0; base < pc.n; base += kWarp) {
+          const int32_t tchunk = (base + lane < pc.n) ? tokens[pc.tok_off + base + lane] : 0;
+          const uint32_t cnt = min(static_cast<uint32_t>(kWarp), pc.n - base);
+          for (uint32_t j = 0; j < cnt; ++j) {
+            const int32_t t = __shfl_sync(kFull, tchunk, j);
+            const unsigned long long up = __shfl_up_sync(kFull, h, 1);
+            h = hash_step(lane == 0 ? hr : up, t);
+            if (static_cast<uint64_t>(lane) < min(static_cast<uint64_t>(D), len + 1))
+              prefetch_l2(T.slots + home_slot(key_hash(h), T.cap));
+            ++len;
+          }
+        }
+      }
+    }
+
+    // pass 2: the dependent claim chain
+    uint64_t len = len0;
+    unsigned long long h = h_init;
+    uint32_t a = (lane < D && static_cast<uint64_t>(lane) < len0) ? act_row[lane] : 0u;
     uint32_t link_slot = 0, link_prev = 0;
     bool link_pending = false;
-
     for (uint32_t p = 0; p < g.npieces; ++p) {
       const AppendPiece pc = pieces[g.piece0 + p];
       for (uint32_t base = 0; base < pc.n; base += kWarp) {
-        // stage 32 tokens per coalesced load, broadcast by shuffle
         const int32_t tchunk = (base + lane < pc.n) ? tokens[pc.tok_off + base + lane] : 0;
         const uint32_t cnt = min(static_cast<uint32_t>(kWarp), pc.n - base);
         for (uint32_t j = 0; j < cnt; ++j) {
           const int32_t t = __shfl_sync(kFull, tchunk, j);
           const int newsize = static_cast<int>(min(static_cast<uint64_t>(D), len + 1));
+          const unsigned long long hup = __shfl_up_sync(kFull, h, 1);
+          h = hash_step(lane == 0 ? hr : hup, t);
           uint32_t parent = __shfl_up_sync(kFull, a, 1);
           if (lane == 0) parent = g.root;
           if (lane < newsize) {
-            const EnsureResult r = ensure_child(T, parent, t, static_cast<uint32_t>(lane + 1), g.root);
+            uint32_t id;
+            bool ins;
+            claim(T, key_hash(h), parent, t, g.root, id, ins);
             if (link_pending) {
               T.slots[link_slot].next_sibling = link_prev;
               link_pending = false;
             }
-            if (r.inserted) {
+            if (ins) {
               ++inserted_total;
-              if (!is_root_id(parent, T.cap)) {
-                link_prev = atomicExch(&T.slots[parent - 1].first_child, r.id);
-                link_slot = r.id - 1;
+              if (!is_root_id(parent, T.cap)) {  // root child lists are never enumerated
+                link_prev = atomicExch(&T.slots[parent - 1].first_child, id);
+                link_slot = id - 1;
                 link_pending = true;
               }
             }
-            a = r.id;
+            a = id;
           }
+          if (lane == static_cast<int>(len & 31)) tail_row[lane] = t;  // ring of the last 32 tokens
           ++len;
         }
       }
@@ -116,64 +169,48 @@ __global__ void __launch_bounds__(kBlock) k_append(DevTrie T, const AppendSeg* _
     if (link_pending) T.slots[link_slot].next_sibling = link_prev;
     if (lane < D && static_cast<uint64_t>(lane) < len) act_row[lane] = a;
   }
-  // one counter update per warp
   for (int o = 16; o > 0; o >>= 1) inserted_total += __shfl_xor_sync(kFull, inserted_total, o);
   if (lane == 0 && inserted_total) atomicAdd(T.used, inserted_total);
 }
 
 // ---------------------------------------------------------------------------
-// K2 + K3: draft query with fused verification.
+// K2 + K3: draft query with fused verification, one G-lane tile per request.
 //
-// One warp per request. Phase A (longest admissible suffix, cst.cpp:160-178):
-// lane l walks the suffix of length start-l from the group root, so all
-// candidate lengths are probed concurrently; the lowest successful lane is the
-// reference's first (longest) success. Phase B (beam, cst.cpp:180-221): lane b
-// owns beam path b and walks its child list, keeping its own top-k qualifying
-// children; the union of the per-lane top-k lists contains the pool's top-k,
-// which a warp-wide rank selection extracts with the reference's exact total
-// order: FP64 score (cnt/parent_cnt products, IEEE round-to-nearest, in the
-// reference's operation order) desc, support desc, token path lexicographic
-// asc. Paths of equal length compare lexicographically as (parent path rank,
-// token), so only ranks — not token arrays — are compared inside the beam.
-// Finals keep the reference's rule: a path is final only when it has no
-// qualifying child (cst.cpp:213-214), and the kept set is the top-k under
-// candidate_before (cst.cpp:29-33,225-227).
+// Phase A (longest admissible suffix, cst.cpp:160-178). For start <= 8 (the
+// default Limits), the tile probes ALL prefixes of ALL admissible suffixes
+// by content hash in one parallel round trip, then checks each suffix's
+// parent chain (root -> ... -> suffix) from the probe records; a mismatch
+// (hash collision) falls back to an exact (parent, token) probe. The longest
+// fully present suffix is the reference's first success, with no fallback
+// after it. Longer patterns walk each suffix with exact probes.
+//
+// Phase B (beam, cst.cpp:180-221). Lane b owns beam path b (its tokens live in
+// registers) and walks its child list; qualifying children are merged one by
+// one into a tile-distributed sorted pool of size top_k — lane r holds rank r
+// under path_before: FP64 score desc (cnt / parent_cnt products, IEEE
+// round-to-nearest, reference operation order), support desc, token path
+// lexicographic asc. Equal-length paths compare as (parent path rank, token),
+// so only ranks travel. Finals follow cst.cpp:213-214 (a path is final only
+// when it has no qualifying child) and are kept top-k under candidate_before
+// (cst.cpp:29-33,225-227) by lane 0 in shared memory.
 
-struct QSmemLayout {
-  int beam_tok, fin_tok, fin_score, fin_sup, fin_len, cl_score, cl_cnt, cl_tok, cl_id, cl_fc, cl_n, nb_node, nb_fc,
-      nb_score, nb_sup, nb_lex, nb_tok_src, nb_tok, total;
-};
-
-__host__ __device__ inline QSmemLayout qsmem_layout(int K, int S) {
-  QSmemLayout L{};
-  int off = 0;
-  auto take = [&](int bytes, int align) {
-    off = (off + align - 1) / align * align;
-    const int r = off;
-    off += bytes;
-    return r;
+template <int G, int S>
+struct __align__(16) GroupScratch {
+  union {
+    struct {
+      uint32_t wid[36];
+      uint32_t wpar[36];
+      uint32_t scnt[8];
+      uint32_t sfc[8];
+    } a;
+    struct {
+      double score[G];
+      long long sup[G];
+      int32_t len[G];
+      int32_t tok[G][S];
+    } f;
   };
-  L.fin_score = take(8 * K, 8);
-  L.fin_sup = take(8 * K, 8);
-  L.cl_score = take(8 * K * K, 8);
-  L.nb_score = take(8 * K, 8);
-  L.nb_sup = take(8 * K, 8);
-  L.beam_tok = take(4 * 2 * K * S, 4);
-  L.fin_tok = take(4 * K * S, 4);
-  L.fin_len = take(4 * K, 4);
-  L.cl_cnt = take(4 * K * K, 4);
-  L.cl_tok = take(4 * K * K, 4);
-  L.cl_id = take(4 * K * K, 4);
-  L.cl_fc = take(4 * K * K, 4);
-  L.cl_n = take(4 * K, 4);
-  L.nb_node = take(4 * K, 4);
-  L.nb_fc = take(4 * K, 4);
-  L.nb_lex = take(4 * K, 4);
-  L.nb_tok_src = take(4 * K, 4);
-  L.nb_tok = take(4 * K, 4);
-  L.total = (off + 15) / 16 * 16;
-  return L;
-}
+};
 
 // lexicographic compare of token arrays (std::vector<int>::operator<)
 __device__ __forceinline__ bool tokens_less(const int32_t* a, int la, const int32_t* b, int lb) {
@@ -183,326 +220,321 @@ __device__ __forceinline__ bool tokens_less(const int32_t* a, int la, const int3
   return la < lb;
 }
 
-// candidate_before (cst.cpp:29-33)
-__device__ __forceinline__ bool cand_before(double sa, int64_t pa, const int32_t* ta, int la, double sb, int64_t pb,
-                                            const int32_t* tb, int lb) {
+__device__ __forceinline__ bool cand_before(double sa, long long pa, const int32_t* ta, int la, double sb,
+                                            long long pb, const int32_t* tb, int lb) {
   if (sa != sb) return sa > sb;
   if (pa != pb) return pa > pb;
   return tokens_less(ta, la, tb, lb);
 }
 
-__device__ __forceinline__ int warp_sum_i(int v) {
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
-  return v;
+template <int S>
+__device__ __forceinline__ void set_tok(int32_t (&tok)[S], int d, int32_t v) {
+#pragma unroll
+  for (int i = 0; i < S; ++i)
+    if (i == d) tok[i] = v;
 }
 
-template <int K>
+template <int G, int S>
 __global__ void __launch_bounds__(kBlock) k_query(QueryLaunch P) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int lane = lane_id();
-  const int wib = threadIdx.x / kWarp;
-  const int64_t q = static_cast<int64_t>(blockIdx.x) * (blockDim.x / kWarp) + wib;
-  if (q >= P.n) return;  // warp-uniform
-
-  const int S = P.S;
-  const QSmemLayout Ly = qsmem_layout(K, S);
-  unsigned char* base = smem_raw + static_cast<size_t>(wib) * Ly.total;
-  int32_t* beam_tok = reinterpret_cast<int32_t*>(base + Ly.beam_tok);  // [2][K][S]
-  int32_t* fin_tok = reinterpret_cast<int32_t*>(base + Ly.fin_tok);    // [K][S]
-  double* fin_score = reinterpret_cast<double*>(base + Ly.fin_score);
-  int64_t* fin_sup = reinterpret_cast<int64_t*>(base + Ly.fin_sup);
-  int32_t* fin_len = reinterpret_cast<int32_t*>(base + Ly.fin_len);
-  double* cl_score = reinterpret_cast<double*>(base + Ly.cl_score);  // [K][K] per-lane sibling lists
-  uint32_t* cl_cnt = reinterpret_cast<uint32_t*>(base + Ly.cl_cnt);
-  int32_t* cl_tok = reinterpret_cast<int32_t*>(base + Ly.cl_tok);
-  uint32_t* cl_id = reinterpret_cast<uint32_t*>(base + Ly.cl_id);
-  uint32_t* cl_fc = reinterpret_cast<uint32_t*>(base + Ly.cl_fc);
-  int32_t* cl_n = reinterpret_cast<int32_t*>(base + Ly.cl_n);
-  uint32_t* nb_node = reinterpret_cast<uint32_t*>(base + Ly.nb_node);
-  uint32_t* nb_fc = reinterpret_cast<uint32_t*>(base + Ly.nb_fc);
-  double* nb_score = reinterpret_cast<double*>(base + Ly.nb_score);
-  int64_t* nb_sup = reinterpret_cast<int64_t*>(base + Ly.nb_sup);
-  int32_t* nb_lex = reinterpret_cast<int32_t*>(base + Ly.nb_lex);
-  int32_t* nb_tok_src = reinterpret_cast<int32_t*>(base + Ly.nb_tok_src);
-  int32_t* nb_tok = reinterpret_cast<int32_t*>(base + Ly.nb_tok);
+  __shared__ GroupScratch<G, S> scratch[kBlock / G];
+  const cg::thread_block_tile<G> tile = cg::tiled_partition<G>(cg::this_thread_block());
+  const int gl = tile.thread_rank();
+  const int gib = threadIdx.x / G;
+  const int64_t q = static_cast<int64_t>(blockIdx.x) * (blockDim.x / G) + gib;
+  if (q >= P.n) return;  // tile-uniform
+  GroupScratch<G, S>& sm = scratch[gib];
 
   const DevTrie& T = P.T;
   const dgds_spec_args a = P.args[q * P.args_stride];
-  const int32_t h = P.handles[q];
-  const uint32_t root = (h >= 0 && h < P.n_handles) ? P.root_of[h] : 0u;
+  const int32_t hdl = P.handles[q];
+  const uint32_t root = (hdl >= 0 && hdl < P.n_handles) ? P.root_of[hdl] : 0u;
   const int plen = P.pat_len[q];
   const int eff_pmax = min(a.pattern_lookup_max, T.lim_pattern);  // cst.cpp:156-158
   const int eff_smax = min(a.max_spec_tokens, T.lim_spec);
   const int kq = a.top_k;
   const bool bad_args = a.pattern_lookup_min < 1 || a.pattern_lookup_min > a.pattern_lookup_max ||
-                        a.max_spec_tokens < 0 || a.top_k < 1 || a.top_k > K || !(a.min_step_freq >= 0.0) ||
-                        a.min_support < 0;
-  if (bad_args && lane == 0 && P.err_flag) atomicExch(P.err_flag, 1);
+                        a.max_spec_tokens < 0 || a.top_k < 1 || a.top_k > G || !(a.min_step_freq >= 0.0) ||
+                        a.min_support < 0 || eff_smax > S;
+  if (bad_args && gl == 0 && P.err_flag) atomicExch(P.err_flag, 1);
 
-  int nf = 0;  // finals kept (warp-uniform)
+  int nf = 0;  // finals kept (tile-uniform)
   int st_lookups = 0, st_exp = 0, st_csec = 0;
 
-  // Insert one finished path (tokens in shared memory) into the top-kq finals.
-  auto finals_offer = [&](const int32_t* toks, int len, double sc, int64_t sup) {
-    if (lane == 0) {
-      if (nf < kq) {
-        for (int i = 0; i < len; ++i) fin_tok[nf * S + i] = toks[i];
-        fin_len[nf] = len;
-        fin_score[nf] = sc;
-        fin_sup[nf] = sup;
-        ++nf;
-      } else {
-        int w = 0;  // worst kept final
-        for (int c = 1; c < nf; ++c)
-          if (cand_before(fin_score[w], fin_sup[w], fin_tok + w * S, fin_len[w], fin_score[c], fin_sup[c],
-                          fin_tok + c * S, fin_len[c]))
-            w = c;
-        if (cand_before(sc, sup, toks, len, fin_score[w], fin_sup[w], fin_tok + w * S, fin_len[w])) {
-          for (int i = 0; i < len; ++i) fin_tok[w * S + i] = toks[i];
-          fin_len[w] = len;
-          fin_score[w] = sc;
-          fin_sup[w] = sup;
-        }
-      }
-    }
-    nf = __shfl_sync(kFull, nf, 0);
-  };
-
   if (!bad_args && root != 0u && plen > 0 && a.pattern_lookup_min <= eff_pmax) {
-    // ---- phase A: all admissible suffix lengths in parallel ----
-    // nlen <= lim_pattern < DGDS_MAX_DEPTH = 32 lanes (checked at server creation).
+    // ---------------- phase A ----------------
     const int start = min(eff_pmax, plen);
     const int nlen = start - a.pattern_lookup_min + 1;
-    const int row_len = min(plen, P.pat_stride);  // the row holds the last row_len tokens
-    const int32_t* pat = P.patterns + q * static_cast<int64_t>(P.pat_stride);
-    bool ok = false;
-    uint32_t node = 0;
-    SlotView rec{};
-    int looks = 0;
-    if (lane < nlen) {
-      const int len = start - lane;
-      const int32_t* pt = pat + (row_len - len);
-      uint32_t nd = root;
-      ok = true;
-      for (int i = 0; i < len; ++i) {
-        ++looks;
-        nd = find_child(T, nd, pt[i], rec);
-        if (nd == 0u) {
-          ok = false;
-          break;
+    const int row_len = min(plen, P.pat_stride);
+    // row[0..start) = the last `start` pattern tokens; suffix j (length start-j) starts at row + j
+    const int32_t* row = P.patterns + q * static_cast<int64_t>(P.pat_stride) + (row_len - start);
+    const unsigned long long h0 = root_hash(root);
+    const bool fast = start <= 8;
+    if (fast) {
+      const int W = nlen * start - nlen * (nlen - 1) / 2;
+      for (int w = gl; w < W; w += G) {
+        int j = 0, rem = w;
+        while (rem >= start - j) {
+          rem -= start - j;
+          ++j;
+        }
+        const int i = rem + 1;  // prefix length of suffix j
+        unsigned long long h = h0;
+        for (int t = 0; t < i; ++t) h = hash_step(h, row[j + t]);
+        SlotView r;
+        const uint32_t id = find_by_content(T, key_hash(h), row[j + i - 1], r);
+        sm.a.wid[w] = id;
+        sm.a.wpar[w] = id ? r.parent : 0u;
+        if (i == start - j) {
+          sm.a.scnt[j] = id ? r.count : 0u;
+          sm.a.sfc[j] = id ? r.first_child : 0u;
         }
       }
-      node = nd;
+      tile.sync();
     }
-    const unsigned okm = __ballot_sync(kFull, ok);
-    const int win = okm ? __ffs(okm) - 1 : kWarp;
-    st_lookups = warp_sum_i(lane <= win ? looks : 0);
-    if (okm) {
-      {
-        // ---- phase B: beam ----
-        const uint32_t locus_cnt = __shfl_sync(kFull, rec.count, win);
-        const uint32_t locus_fc = __shfl_sync(kFull, rec.first_child, win);
-        const uint32_t locus = __shfl_sync(kFull, node, win);
-        int nb = 1;
-        if (lane == 0) nb_lex[0] = 0;
-        __syncwarp();
-        uint32_t b_node = locus, b_fc = locus_fc;
-        double b_score = 1.0;
-        int64_t b_sup = static_cast<int64_t>(locus_cnt);
-        int b_lex = 0;
-        int cur = 0;
-        int d = 0;
-        for (; d < eff_smax && nb > 0; ++d) {
-          // expansion: lane b walks the child list of beam path b
-          bool grew = false;
-          int nchild = 0;
-          if (lane < nb) {
-            int my_n = 0;
-            double* ls = cl_score + lane * K;
-            uint32_t* lc = cl_cnt + lane * K;
-            int32_t* lt = cl_tok + lane * K;
-            uint32_t* li = cl_id + lane * K;
-            uint32_t* lf = cl_fc + lane * K;
-            uint32_t c = b_fc;
-            while (c != 0u) {
-              const SlotView r = load_slot_nc(T.slots + (c - 1));
-              ++nchild;
-              const int64_t cnt = static_cast<int64_t>(r.count);
-              const double step = __ddiv_rn(static_cast<double>(cnt), static_cast<double>(b_sup));
-              if (!(step < a.min_step_freq) && !(cnt < a.min_support)) {
-                grew = true;
-                const double sc = __dmul_rn(b_score, step);
-                const int32_t tok = static_cast<int32_t>(static_cast<uint32_t>(r.key));
-                // sorted insert (siblings: same parent path, so the token decides ties)
-                int pos = my_n;
-                while (pos > 0) {
-                  const int pp = pos - 1;
-                  const bool better = (sc != ls[pp]) ? (sc > ls[pp])
-                                      : (cnt != static_cast<int64_t>(lc[pp])) ? (cnt > static_cast<int64_t>(lc[pp]))
-                                                                               : (tok < lt[pp]);
-                  if (!better) break;
-                  --pos;
-                }
-                if (pos < kq) {
-                  const int last = my_n < kq ? my_n : kq - 1;
-                  for (int m = last; m > pos; --m) {
-                    ls[m] = ls[m - 1];
-                    lc[m] = lc[m - 1];
-                    lt[m] = lt[m - 1];
-                    li[m] = li[m - 1];
-                    lf[m] = lf[m - 1];
-                  }
-                  ls[pos] = sc;
-                  lc[pos] = r.count;
-                  lt[pos] = tok;
-                  li[pos] = c;
-                  lf[pos] = r.first_child;
-                  if (my_n < kq) ++my_n;
-                }
-              }
-              c = r.next_sibling;
+    int winner = -1;
+    uint32_t locus_cnt = 0, locus_fc = 0;
+    for (int u0 = 0; u0 < nlen; u0 += G) {
+      const int j = u0 + gl;
+      bool ok = false;
+      int looks = 0;
+      uint32_t cnt = 0, fc = 0;
+      if (j < nlen) {
+        const int L = start - j;
+        const int b0 = j * start - j * (j - 1) / 2;
+        uint32_t prev = root;
+        unsigned long long h = h0;
+        ok = true;
+        for (int i = 1; i <= L; ++i) {
+          ++looks;
+          const int32_t tk = row[j + i - 1];
+          h = hash_step(h, tk);
+          uint32_t id;
+          if (fast && sm.a.wid[b0 + i - 1] != 0u && sm.a.wpar[b0 + i - 1] == prev) {
+            id = sm.a.wid[b0 + i - 1];
+            if (i == L) {
+              cnt = sm.a.scnt[j];
+              fc = sm.a.sfc[j];
             }
-            cl_n[lane] = my_n;
-          }
-          st_exp += nb;
-          st_csec += warp_sum_i(lane < nb ? (8 * nchild + 31) / 32 : 0);
-          __syncwarp();
-          // paths with no qualifying child become finals (non-empty ones: d > 0)
-          unsigned finm = __ballot_sync(kFull, lane < nb && !grew && d > 0);
-          while (finm) {
-            const int b = __ffs(finm) - 1;
-            finm &= finm - 1;
-            const double sc = __shfl_sync(kFull, b_score, b);
-            const int64_t sp = __shfl_sync(kFull, b_sup, b);
-            finals_offer(beam_tok + (cur * K + b) * S, d, sc, sp);
-          }
-          // select the next beam: rank every listed child under path_before
-          const int slots = nb * kq;
-          int nb_next = 0;
-          for (int m0 = 0; m0 < slots; m0 += kWarp) {
-            const int m = m0 + lane;
-            bool valid = false;
-            int rank = 0, b = 0, j = 0;
-            double sc = 0;
-            int64_t sp = 0;
-            int plex = 0;
-            int32_t tok = 0;
-            if (m < slots) {
-              b = m / kq;
-              j = m - b * kq;
-              valid = j < cl_n[b];
-            }
-            if (valid) {
-              sc = cl_score[b * K + j];
-              sp = static_cast<int64_t>(cl_cnt[b * K + j]);
-              tok = cl_tok[b * K + j];
-              plex = nb_lex[b];
-              for (int b2 = 0; b2 < nb; ++b2) {
-                const int n2 = cl_n[b2];
-                const int plex2 = nb_lex[b2];
-                for (int j2 = 0; j2 < n2; ++j2) {
-                  const double sc2 = cl_score[b2 * K + j2];
-                  const int64_t sp2 = static_cast<int64_t>(cl_cnt[b2 * K + j2]);
-                  const int32_t tok2 = cl_tok[b2 * K + j2];
-                  const bool before = (sc2 != sc)   ? (sc2 > sc)
-                                      : (sp2 != sp) ? (sp2 > sp)
-                                      : (plex2 != plex) ? (plex2 < plex)
-                                                        : (tok2 < tok);
-                  rank += before ? 1 : 0;
-                }
-              }
-            }
-            nb_next += warp_sum_i(valid ? 1 : 0);
-            if (valid && rank < kq) {
-              nb_node[rank] = cl_id[b * K + j];
-              nb_fc[rank] = cl_fc[b * K + j];
-              nb_score[rank] = sc;
-              nb_sup[rank] = sp;
-              nb_tok_src[rank] = b;
-              nb_tok[rank] = tok;
+          } else if (fast && sm.a.wid[b0 + i - 1] == 0u) {
+            id = 0;  // no slot with this content at all: the window is absent
+          } else {
+            SlotView r;
+            id = find_exact(T, key_hash(h), prev, tk, r);
+            if (id && i == L) {
+              cnt = r.count;
+              fc = r.first_child;
             }
           }
-          if (nb_next > kq) nb_next = kq;
-          // beam slot b currently holds the parent lexrank in nb_lex[b]; compute the
-          // children's lexrank among the selected set before overwriting it
-          __syncwarp();
-          int new_lex = 0;
-          if (lane < nb_next) {
-            const int src = nb_tok_src[lane];
-            const int pl = nb_lex[src];
-            const int32_t tk = nb_tok[lane];
-            for (int o = 0; o < nb_next; ++o) {
-              const int pl2 = nb_lex[nb_tok_src[o]];
-              const int32_t tk2 = nb_tok[o];
-              new_lex += (pl2 < pl || (pl2 == pl && tk2 < tk)) ? 1 : 0;
-            }
-            // tokens: parent path + new token
-            const int32_t* src_tok = beam_tok + (cur * K + src) * S;
-            int32_t* dst_tok = beam_tok + ((cur ^ 1) * K + lane) * S;
-            for (int i = 0; i < d; ++i) dst_tok[i] = src_tok[i];
-            dst_tok[d] = tk;
+          if (id == 0u) {
+            ok = false;
+            break;
           }
-          __syncwarp();
-          if (lane < nb_next) {
-            nb_lex[lane] = new_lex;
-            b_node = nb_node[lane];
-            b_fc = nb_fc[lane];
-            b_score = nb_score[lane];
-            b_sup = nb_sup[lane];
-            b_lex = new_lex;
-          }
-          __syncwarp();
-          nb = nb_next;
-          cur ^= 1;
-        }
-        (void)b_node;
-        (void)b_lex;
-        // leftover beam paths (d tokens each) are finals when non-empty
-        if (d > 0) {
-          for (int b = 0; b < nb; ++b) {
-            const double sc = __shfl_sync(kFull, b_score, b);
-            const int64_t sp = __shfl_sync(kFull, b_sup, b);
-            finals_offer(beam_tok + (cur * K + b) * S, d, sc, sp);
-          }
+          prev = id;
         }
       }
-    }  // no match at any admissible length: empty (no shorter fallback once matched)
+      const unsigned m = tile.ballot(ok);
+      if (m) {
+        const int w = __ffs(m) - 1;
+        st_lookups += cg::reduce(tile, gl <= w ? looks : 0, cg::plus<int>());
+        winner = u0 + w;
+        locus_cnt = tile.shfl(cnt, w);
+        locus_fc = tile.shfl(fc, w);
+        break;
+      }
+      st_lookups += cg::reduce(tile, looks, cg::plus<int>());
+    }
+    tile.sync();  // phase-A scratch is dead from here (reused for finals)
+
+    if (winner >= 0) {
+      // ---------------- phase B ----------------
+      int32_t tok[S];
+#pragma unroll
+      for (int i = 0; i < S; ++i) tok[i] = 0;
+      int nb = 1;
+      uint32_t b_fc = locus_fc;
+      double b_score = 1.0;
+      long long b_sup = static_cast<long long>(locus_cnt);
+      int b_lex = 0;
+      const double msf = a.min_step_freq;
+      const long long msup = a.min_support;
+
+      auto finals_offer = [&](int b, int len) {
+        int32_t ct[S];
+#pragma unroll
+        for (int i = 0; i < S; ++i) ct[i] = tile.shfl(tok[i], b);
+        const double cs = tile.shfl(b_score, b);
+        const long long cp = tile.shfl(b_sup, b);
+        if (gl == 0) {
+          int dst = -1;
+          if (nf < kq) {
+            dst = nf++;
+          } else {
+            int w = 0;  // worst kept final
+            for (int c = 1; c < nf; ++c)
+              if (cand_before(sm.f.score[w], sm.f.sup[w], sm.f.tok[w], sm.f.len[w], sm.f.score[c], sm.f.sup[c],
+                              sm.f.tok[c], sm.f.len[c]))
+                w = c;
+            bool better;
+            if (cs != sm.f.score[w]) {
+              better = cs > sm.f.score[w];
+            } else if (cp != sm.f.sup[w]) {
+              better = cp > sm.f.sup[w];
+            } else {
+              int r = 0;  // lexicographic compare of ct[0..len) with the kept final
+              const int m = len < sm.f.len[w] ? len : sm.f.len[w];
+#pragma unroll
+              for (int i = 0; i < S; ++i)
+                if (r == 0 && i < m && ct[i] != sm.f.tok[w][i]) r = ct[i] < sm.f.tok[w][i] ? -1 : 1;
+              better = r < 0 || (r == 0 && len < sm.f.len[w]);
+            }
+            if (better) dst = w;
+          }
+          if (dst >= 0) {
+#pragma unroll
+            for (int i = 0; i < S; ++i)
+              if (i < len) sm.f.tok[dst][i] = ct[i];
+            sm.f.len[dst] = len;
+            sm.f.score[dst] = cs;
+            sm.f.sup[dst] = cp;
+          }
+        }
+        nf = tile.shfl(nf, 0);
+      };
+
+      int d = 0;
+      for (; d < eff_smax && nb > 0; ++d) {
+        // pool entry held by lane r (rank r), r < np
+        double p_score = 0.0;
+        long long p_sup = 0;
+        int p_lex = 0, p_src = 0;
+        int32_t p_tok = 0;
+        uint32_t p_fc = 0;
+        int np = 0;
+        uint32_t c = gl < nb ? b_fc : 0u;
+        bool grew = false;
+        int nchild = 0;
+        while (tile.any(c != 0u)) {
+          SlotView r{};
+          const bool have = c != 0u;
+          if (have) r = load_slot_nc(T.slots + (c - 1));
+          bool qual = false;
+          double sc = 0.0;
+          const long long cnt = static_cast<long long>(r.count);
+          if (have) {
+            ++nchild;
+            const double step = __ddiv_rn(static_cast<double>(cnt), static_cast<double>(b_sup));
+            qual = !(step < msf) && !(cnt < msup);
+            if (qual) {
+              grew = true;
+              sc = __dmul_rn(b_score, step);
+            }
+          }
+          unsigned m = tile.ballot(qual);
+          while (m) {  // merge lane b's candidate into the sorted pool
+            const int b = __ffs(m) - 1;
+            m &= m - 1;
+            const double cs = tile.shfl(sc, b);
+            const long long cp = tile.shfl(cnt, b);
+            const int cl = tile.shfl(b_lex, b);
+            const int32_t ct = tile.shfl(r.token, b);
+            const uint32_t cfc = tile.shfl(r.first_child, b);
+            const bool before = gl < np && (p_score != cs ? p_score > cs
+                                            : p_sup != cp ? p_sup > cp
+                                            : p_lex != cl ? p_lex < cl
+                                                          : p_tok < ct);
+            const int pos = __popc(tile.ballot(before));
+            if (pos < kq) {
+              const double us = tile.shfl_up(p_score, 1);
+              const long long up = tile.shfl_up(p_sup, 1);
+              const int ul = tile.shfl_up(p_lex, 1);
+              const int usrc = tile.shfl_up(p_src, 1);
+              const int32_t ut = tile.shfl_up(p_tok, 1);
+              const uint32_t ufc = tile.shfl_up(p_fc, 1);
+              if (gl > pos && gl <= np) {
+                p_score = us;
+                p_sup = up;
+                p_lex = ul;
+                p_src = usrc;
+                p_tok = ut;
+                p_fc = ufc;
+              }
+              if (gl == pos) {
+                p_score = cs;
+                p_sup = cp;
+                p_lex = cl;
+                p_src = b;
+                p_tok = ct;
+                p_fc = cfc;
+              }
+              np = min(np + 1, kq);
+            }
+          }
+          c = have ? r.next_sibling : 0u;
+        }
+        st_exp += nb;
+        st_csec += cg::reduce(tile, gl < nb ? (8 * nchild + 31) / 32 : 0, cg::plus<int>());
+        // paths without a qualifying child are final (when non-empty, i.e. d > 0)
+        unsigned fm = tile.ballot(gl < nb && !grew && d > 0);
+        while (fm) {
+          const int b = __ffs(fm) - 1;
+          fm &= fm - 1;
+          finals_offer(b, d);
+        }
+        // the pool becomes the next beam: lane r takes pool rank r
+#pragma unroll
+        for (int i = 0; i < S; ++i) tok[i] = tile.shfl(tok[i], p_src);
+        set_tok<S>(tok, d, p_tok);
+        int lex = 0;
+        for (int o = 0; o < np; ++o) {
+          const int ol = tile.shfl(p_lex, o);
+          const int32_t ot = tile.shfl(p_tok, o);
+          lex += (ol < p_lex || (ol == p_lex && ot < p_tok)) ? 1 : 0;
+        }
+        b_fc = p_fc;
+        b_score = p_score;
+        b_sup = p_sup;
+        b_lex = lex;
+        nb = np;
+      }
+      if (d > 0)
+        for (int b = 0; b < nb; ++b) finals_offer(b, d);  // leftover beam (cst.cpp:222-223)
+    }
   }
 
   // ---- output in candidate_before order ----
-  __syncwarp();
+  tile.sync();
   int my_rank = 0;
-  if (lane < nf) {
+  if (gl < nf) {
     for (int c = 0; c < nf; ++c)
-      my_rank += cand_before(fin_score[c], fin_sup[c], fin_tok + c * S, fin_len[c], fin_score[lane], fin_sup[lane],
-                             fin_tok + lane * S, fin_len[lane])
+      my_rank += cand_before(sm.f.score[c], sm.f.sup[c], sm.f.tok[c], sm.f.len[c], sm.f.score[gl], sm.f.sup[gl],
+                             sm.f.tok[gl], sm.f.len[gl])
                      ? 1
                      : 0;
   }
   if (P.n_cands) {
-    if (lane == 0) P.n_cands[q] = nf;
-    if (lane < nf) {
+    if (gl == 0) P.n_cands[q] = nf;
+    if (gl < nf) {
       const int64_t o = q * P.k_stride + my_rank;
-      P.lens[o] = fin_len[lane];
-      P.scores[o] = fin_score[lane];
-      P.supports[o] = fin_sup[lane];
+      P.lens[o] = sm.f.len[gl];
+      P.scores[o] = sm.f.score[gl];
+      P.supports[o] = sm.f.sup[gl];
       int32_t* dst = P.tokens + o * P.s_stride;
-      for (int i = 0; i < fin_len[lane]; ++i) dst[i] = fin_tok[lane * S + i];
+      for (int i = 0; i < sm.f.len[gl]; ++i) dst[i] = sm.f.tok[gl][i];
     }
   }
 
   // ---- K3: verification (engine.cpp:115-143) ----
   if (P.v_emitted) {
     int drafted = 0, match = 0;
-    if (lane < nf) {
-      drafted = fin_len[lane];
+    if (gl < nf) {
+      drafted = sm.f.len[gl];
       const int32_t* tr = P.truth + q * static_cast<int64_t>(P.truth_stride);
-      const int cap = min(fin_len[lane], P.truth_left[q]);
-      while (match < cap && fin_tok[lane * S + match] == tr[match]) ++match;
+      const int cap = min(sm.f.len[gl], P.truth_left[q]);
+      while (match < cap && sm.f.tok[gl][match] == tr[match]) ++match;
     }
-    drafted = warp_sum_i(drafted);
-    for (int o = 16; o > 0; o >>= 1) match = max(match, __shfl_xor_sync(kFull, match, o));
-    if (lane == 0) {
+    drafted = cg::reduce(tile, drafted, cg::plus<int>());
+    match = cg::reduce(tile, match, cg::greater<int>());
+    if (gl == 0) {
       const int emitted = min(match + 1, P.limit[q]);
       P.v_drafted[q] = drafted;
       P.v_accepted[q] = emitted - 1;
@@ -511,21 +543,19 @@ __global__ void __launch_bounds__(kBlock) k_query(QueryLaunch P) {
   }
 
   if (P.stats) {
-    int ctoks = lane < nf ? fin_len[lane] : 0;
-    ctoks = warp_sum_i(ctoks);
-    if (lane == 0) {
+    const int ctoks = cg::reduce(tile, gl < nf ? sm.f.len[gl] : 0, cg::plus<int>());
+    if (gl == 0) {
       const uint64_t B = 4ull * plen + 32ull + 32ull * st_lookups + 32ull * st_exp + 32ull * st_csec +
                          4ull * ctoks + 16ull * nf;
-      atomicAdd(reinterpret_cast<unsigned long long*>(&P.stats->queries), 1ull);
-      atomicAdd(reinterpret_cast<unsigned long long*>(&P.stats->pattern_tokens), static_cast<unsigned long long>(plen));
-      atomicAdd(reinterpret_cast<unsigned long long*>(&P.stats->suffix_lookups),
-                static_cast<unsigned long long>(st_lookups));
-      atomicAdd(reinterpret_cast<unsigned long long*>(&P.stats->expansions), static_cast<unsigned long long>(st_exp));
-      atomicAdd(reinterpret_cast<unsigned long long*>(&P.stats->child_sectors),
-                static_cast<unsigned long long>(st_csec));
-      atomicAdd(reinterpret_cast<unsigned long long*>(&P.stats->cands), static_cast<unsigned long long>(nf));
-      atomicAdd(reinterpret_cast<unsigned long long*>(&P.stats->cand_tokens), static_cast<unsigned long long>(ctoks));
-      atomicAdd(reinterpret_cast<unsigned long long*>(&P.stats->algorithmic_bytes), static_cast<unsigned long long>(B));
+      unsigned long long* s = reinterpret_cast<unsigned long long*>(P.stats);
+      atomicAdd(s + 0, 1ull);
+      atomicAdd(s + 1, static_cast<unsigned long long>(plen));
+      atomicAdd(s + 2, static_cast<unsigned long long>(st_lookups));
+      atomicAdd(s + 3, static_cast<unsigned long long>(st_exp));
+      atomicAdd(s + 4, static_cast<unsigned long long>(st_csec));
+      atomicAdd(s + 5, static_cast<unsigned long long>(nf));
+      atomicAdd(s + 6, static_cast<unsigned long long>(ctoks));
+      atomicAdd(s + 7, static_cast<unsigned long long>(B));
     }
   }
 }
@@ -560,39 +590,41 @@ __global__ void k_verify(int64_t n, int32_t k_stride, int32_t s_stride, const in
 __global__ void k_set_u32(uint32_t* dst, uint32_t v) { *dst = v; }
 
 // ---------------------------------------------------------------------------
-// rebuild: re-insert live nodes of depth `depth` from `from` into `to`
+// rebuild. Pass 1 re-places every live slot of `from` at its home in `to`
+// (keys are unique, so claiming an empty slot suffices) and records
+// old id -> new id. Pass 2 rewrites parents through the map and relinks the
+// child lists. Slots of dropped groups (root not alive) are not carried over.
 
-__global__ void k_rebuild_level(DevTrie from, DevTrie to, uint32_t depth, const uint32_t* __restrict__ root_alive,
-                                uint32_t* remap) {
+__global__ void k_rebuild_place(DevTrie from, DevTrie to, const uint32_t* __restrict__ root_alive, uint32_t* remap) {
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
   for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < from.cap; i += stride) {
     const Slot s = from.slots[i];
-    if (s.key == 0ull || s.depth != depth) continue;
+    remap[i] = 0;
+    if (s.h == 0ull) continue;
     const uint32_t ridx = kRootTop - s.root;
-    if (!((root_alive[ridx >> 5] >> (ridx & 31)) & 1u)) {
-      remap[i] = 0;
-      continue;
-    }
-    const uint32_t parent = static_cast<uint32_t>(s.key >> 32);
-    uint32_t np = parent;
-    if (!is_root_id(parent, from.cap)) {
-      np = remap[parent - 1];
-      if (np == 0u) {
-        remap[i] = 0;
-        continue;
-      }
-    }
-    const unsigned long long key = edge_key(np, static_cast<int32_t>(static_cast<uint32_t>(s.key)));
-    uint64_t j = home_slot(key, to.cap);
-    while (atomicCAS(&to.slots[j].key, 0ull, key) != 0ull) j = (j + 1 == to.cap) ? 0 : j + 1;
+    if (!((root_alive[ridx >> 5] >> (ridx & 31)) & 1u)) continue;
+    uint64_t j = home_slot(s.h, to.cap);
+    while (atomicCAS(&to.slots[j].h, 0ull, s.h) != 0ull) j = (j + 1 == to.cap) ? 0 : j + 1;
     Slot* d = to.slots + j;
+    d->parent = s.parent;  // old id until pass 2
+    d->token = s.token;
     d->count = s.count;
-    d->depth = s.depth;
     d->root = s.root;
-    const uint32_t nid = static_cast<uint32_t>(j + 1);
-    if (!is_root_id(np, to.cap)) d->next_sibling = atomicExch(&to.slots[np - 1].first_child, nid);
-    remap[i] = nid;
+    remap[i] = static_cast<uint32_t>(j + 1);
     atomicAdd(to.used, 1ull);
+  }
+}
+
+__global__ void k_rebuild_link(DevTrie to, const uint32_t* __restrict__ remap) {
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t j = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < to.cap; j += stride) {
+    Slot* d = to.slots + j;
+    if (d->h == 0ull) continue;
+    const uint32_t op = d->parent;
+    if (op == d->root) continue;  // depth 1: parent is the group root
+    const uint32_t np = remap[op - 1];
+    d->parent = np;
+    d->next_sibling = atomicExch(&to.slots[np - 1].first_child, static_cast<uint32_t>(j + 1));
   }
 }
 
@@ -614,7 +646,6 @@ __global__ void k_remap_active(uint32_t* active, const uint32_t* __restrict__ st
 constexpr int kRouteTile = 1024;
 
 __global__ void k_route_count(int64_t n, int32_t world, const int32_t* __restrict__ owner, int64_t* tile_counts) {
-  // tile_counts[o * ntiles + tile]
   extern __shared__ int sh_cnt[];
   for (int o = threadIdx.x; o < world; o += blockDim.x) sh_cnt[o] = 0;
   __syncthreads();
@@ -626,9 +657,7 @@ __global__ void k_route_count(int64_t n, int32_t world, const int32_t* __restric
   for (int o = threadIdx.x; o < world; o += blockDim.x) tile_counts[o * ntiles + blockIdx.x] = sh_cnt[o];
 }
 
-__global__ void k_route_scan(int64_t total_entries, int32_t world, int64_t ntiles, int64_t* tile_counts,
-                             int64_t* counts) {
-  // single thread: exclusive scan in (owner, tile) order; tiny (world * ntiles entries)
+__global__ void k_route_scan(int32_t world, int64_t ntiles, int64_t* tile_counts, int64_t* counts) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   int64_t run = 0;
   for (int o = 0; o < world; ++o) {
@@ -641,18 +670,15 @@ __global__ void k_route_scan(int64_t total_entries, int32_t world, int64_t ntile
     }
     counts[o] = c;
   }
-  (void)total_entries;
 }
 
 __global__ void k_route_scatter(int64_t n, int32_t world, const int32_t* __restrict__ owner,
                                 const uint32_t* __restrict__ rec, int32_t rw, const int64_t* __restrict__ tile_off,
                                 uint32_t* out, int64_t* perm) {
-  // one block per tile; stable ranks within the tile, warp by warp
   __shared__ int warp_cnt[kRouteTile / kWarp][8];
   const int64_t ntiles = gridDim.x;
   const int64_t t0 = static_cast<int64_t>(blockIdx.x) * kRouteTile;
   const int warp = threadIdx.x / kWarp, lane = lane_id();
-  // this kernel is launched with kRouteTile threads and world <= 8 in the fast path
   const int64_t i = t0 + threadIdx.x;
   const int o = (i < n) ? owner[i] : -1;
   int my_rank_in_warp = 0;
@@ -680,20 +706,19 @@ __global__ void k_route_gather(int64_t n, const uint32_t* __restrict__ in, int32
   out[t] = in[perm[i] * rw + k];
 }
 
-template <int K>
-cudaError_t launch_query_k(const QueryLaunch& L, cudaStream_t st) {
-  const QSmemLayout Ly = qsmem_layout(K, L.S);
-  constexpr int kSmemBudget = 200 * 1024;
-  int wpb = kWarpsPerBlock;
-  while (wpb > 1 && Ly.total * wpb > kSmemBudget) --wpb;
-  const size_t smem = static_cast<size_t>(Ly.total) * wpb;
-  if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(k_query<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    if (e != cudaSuccess) return e;
-  }
-  const int64_t blocks = (L.n + wpb - 1) / wpb;
-  k_query<K><<<static_cast<unsigned>(blocks), wpb * kWarp, smem, st>>>(L);
+template <int G, int S>
+cudaError_t launch_query_gs(const QueryLaunch& L, cudaStream_t st) {
+  const int per_block = kBlock / G;
+  const int64_t blocks = (L.n + per_block - 1) / per_block;
+  k_query<G, S><<<static_cast<unsigned>(blocks), kBlock, 0, st>>>(L);
   return cudaGetLastError();
+}
+
+template <int G>
+cudaError_t launch_query_g(const QueryLaunch& L, int32_t max_s, cudaStream_t st) {
+  if (max_s <= 8) return launch_query_gs<G, 8>(L, st);
+  if (max_s <= 16) return launch_query_gs<G, 16>(L, st);
+  return launch_query_gs<G, 32>(L, st);
 }
 
 }  // namespace
@@ -706,14 +731,11 @@ cudaError_t launch_append(const DevTrie& T, const AppendSeg* d_segs, int64_t nse
   return cudaGetLastError();
 }
 
-cudaError_t launch_query(const QueryLaunch& L, int32_t max_k, cudaStream_t st) {
+cudaError_t launch_query(const QueryLaunch& L, int32_t max_k, int32_t max_s, cudaStream_t st) {
   if (L.n <= 0) return cudaSuccess;
-  if (max_k <= 1) return launch_query_k<1>(L, st);
-  if (max_k <= 2) return launch_query_k<2>(L, st);
-  if (max_k <= 4) return launch_query_k<4>(L, st);
-  if (max_k <= 8) return launch_query_k<8>(L, st);
-  if (max_k <= 16) return launch_query_k<16>(L, st);
-  return launch_query_k<32>(L, st);
+  if (max_k <= 4) return launch_query_g<4>(L, max_s, st);
+  if (max_k <= 8) return launch_query_g<8>(L, max_s, st);
+  return launch_query_g<32>(L, max_s, st);
 }
 
 cudaError_t launch_verify(int64_t n, int32_t k_stride, int32_t s_stride, const int32_t* n_cands, const int32_t* lens,
@@ -732,15 +754,17 @@ cudaError_t launch_set_u32(uint32_t* dst, uint32_t value, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_rebuild_level(const DevTrie& from, const DevTrie& to, uint32_t depth, const uint32_t* root_alive,
-                                 uint32_t* remap, cudaStream_t st) {
-  k_rebuild_level<<<148 * 8, 256, 0, st>>>(from, to, depth, root_alive, remap);
+cudaError_t launch_rebuild(const DevTrie& from, const DevTrie& to, const uint32_t* root_alive, uint32_t* remap,
+                           cudaStream_t st) {
+  k_rebuild_place<<<148 * 8, 256, 0, st>>>(from, to, root_alive, remap);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  k_rebuild_link<<<148 * 8, 256, 0, st>>>(to, remap);
   return cudaGetLastError();
 }
 
 cudaError_t launch_remap_active(uint32_t* active, const uint32_t* streams, const uint32_t* sizes, int64_t nstreams,
-                                const uint32_t* remap, uint64_t old_cap, cudaStream_t st) {
-  (void)old_cap;
+                                const uint32_t* remap, cudaStream_t st) {
   if (nstreams <= 0) return cudaSuccess;
   const int64_t threads = nstreams * kWarp;
   k_remap_active<<<static_cast<unsigned>((threads + 255) / 256), 256, 0, st>>>(active, streams, sizes, nstreams,
@@ -753,15 +777,13 @@ cudaError_t launch_route_pack(int64_t n, int32_t world, const int32_t* owner, co
                               cudaStream_t st) {
   if (world > 8) return cudaErrorInvalidValue;
   const int64_t ntiles = (n + kRouteTile - 1) / kRouteTile;
-  int64_t* tile_counts = static_cast<int64_t*>(scratch);  // world * ntiles
-  if (n > 0) {
+  int64_t* tile_counts = static_cast<int64_t*>(scratch);
+  if (n > 0)
     k_route_count<<<static_cast<unsigned>(ntiles), 256, world * sizeof(int), st>>>(n, world, owner, tile_counts);
-  }
-  k_route_scan<<<1, 1, 0, st>>>(world * ntiles, world, ntiles, tile_counts, counts);
-  if (n > 0) {
+  k_route_scan<<<1, 1, 0, st>>>(world, ntiles, tile_counts, counts);
+  if (n > 0)
     k_route_scatter<<<static_cast<unsigned>(ntiles), kRouteTile, 0, st>>>(n, world, owner, records, rec_words,
                                                                             tile_counts, out, perm);
-  }
   return cudaGetLastError();
 }
 

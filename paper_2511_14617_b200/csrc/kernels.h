@@ -35,7 +35,7 @@ struct QueryLaunch {
   DevTrie T;
   const uint32_t* root_of;
   int32_t n_handles;
-  int32_t S;  // shared-memory token stride per path (>= lim_spec, >= 1)
+  int32_t reserved0;
   int64_t n;
   const int32_t* handles;
   const int32_t* pat_len;
@@ -61,8 +61,9 @@ struct QueryLaunch {
   int32_t* err_flag;  // set to 1 by any query with invalid args (device API)
 };
 
-// max_k selects the template instance (K = next power of two >= max_k).
-cudaError_t launch_query(const QueryLaunch& L, int32_t max_k, cudaStream_t st);
+// max_k selects the tile width (4, 8 or 32 lanes per request); max_s bounds
+// min(max_spec_tokens, max_spec_len) over the batch (per-path token registers).
+cudaError_t launch_query(const QueryLaunch& L, int32_t max_k, int32_t max_s, cudaStream_t st);
 
 cudaError_t launch_verify(int64_t n, int32_t k_stride, int32_t s_stride, const int32_t* n_cands, const int32_t* lens,
                           const int32_t* tokens, const int32_t* truth, int32_t truth_stride, const int32_t* truth_left,
@@ -71,13 +72,14 @@ cudaError_t launch_verify(int64_t n, int32_t k_stride, int32_t s_stride, const i
 
 cudaError_t launch_set_u32(uint32_t* dst, uint32_t value, cudaStream_t st);
 
-// Arena rebuild (growth + garbage collection of dropped groups): re-insert every
-// live node of `from` into `to`, one trie depth per launch so parents are
-// re-keyed before their children. root_alive: bitmap over root indices.
-cudaError_t launch_rebuild_level(const DevTrie& from, const DevTrie& to, uint32_t depth, const uint32_t* root_alive,
-                                 uint32_t* remap, cudaStream_t st);
+// Arena rebuild (growth + garbage collection of dropped groups): re-place every
+// live slot of `from` in `to` (home slots depend on content only), then rewrite
+// parents / child lists through the old->new id map. root_alive: bitmap over
+// root indices.
+cudaError_t launch_rebuild(const DevTrie& from, const DevTrie& to, const uint32_t* root_alive, uint32_t* remap,
+                           cudaStream_t st);
 cudaError_t launch_remap_active(uint32_t* active, const uint32_t* streams, const uint32_t* sizes, int64_t nstreams,
-                                const uint32_t* remap, uint64_t old_cap, cudaStream_t st);
+                                const uint32_t* remap, cudaStream_t st);
 
 cudaError_t launch_route_pack(int64_t n, int32_t world, const int32_t* owner, const uint32_t* records,
                               int32_t rec_words, uint32_t* out, int64_t* counts, int64_t* perm, void* scratch,

@@ -181,14 +181,20 @@ int alloc_stream_slot(dgds_server* s, uint32_t* out) {
   if (s->next_stream >= s->stream_cap) {
     uint64_t nc = std::max<uint64_t>(1024, s->stream_cap * 2);
     uint32_t* na = nullptr;
+    int32_t* nt = nullptr;
     DGDS_CUDA(cudaMalloc(&na, nc * dgds::kWarp * sizeof(uint32_t)));
+    DGDS_CUDA(cudaMalloc(&nt, nc * dgds::kWarp * sizeof(int32_t)));
     if (s->T.active) {
       DGDS_CUDA(cudaMemcpyAsync(na, s->T.active, s->stream_cap * dgds::kWarp * sizeof(uint32_t),
                                 cudaMemcpyDeviceToDevice, s->st));
+      DGDS_CUDA(cudaMemcpyAsync(nt, s->T.tail, s->stream_cap * dgds::kWarp * sizeof(int32_t),
+                                cudaMemcpyDeviceToDevice, s->st));
       DGDS_CUDA(cudaStreamSynchronize(s->st));
       cudaFree(s->T.active);
+      cudaFree(s->T.tail);
     }
     s->T.active = na;
+    s->T.tail = nt;
     s->stream_cap = nc;
   }
   *out = s->next_stream++;
@@ -290,9 +296,9 @@ int rebuild(dgds_server* s, uint64_t new_cap) {
     DGDS_CUDA(cudaMemcpyAsync(d_ls + live_slots.size(), live_sizes.data(), live_sizes.size() * 4,
                               cudaMemcpyHostToDevice, s->st));
   }
-  for (int d = 1; d <= s->D; ++d) DGDS_CUDA(dgds::launch_rebuild_level(s->T, to, d, d_alive, d_remap, s->st));
+  DGDS_CUDA(dgds::launch_rebuild(s->T, to, d_alive, d_remap, s->st));
   DGDS_CUDA(dgds::launch_remap_active(s->T.active, d_ls, d_ls + live_slots.size(),
-                                      static_cast<int64_t>(live_slots.size()), d_remap, s->T.cap, s->st));
+                                      static_cast<int64_t>(live_slots.size()), d_remap, s->st));
   DGDS_CUDA(cudaStreamSynchronize(s->st));  // host vectors above must outlive the copies
   cudaFree(d_alive);
   cudaFree(d_remap);
@@ -506,6 +512,7 @@ int dgds_create(const dgds_params* params, dgds_server** out) {
   s->T.used = s->d_used;
   s->stream_cap = std::max<uint64_t>(p.expected_streams ? p.expected_streams : 4096, 64);
   DGDS_CUDA(cudaMalloc(&s->T.active, s->stream_cap * dgds::kWarp * sizeof(uint32_t)));
+  DGDS_CUDA(cudaMalloc(&s->T.tail, s->stream_cap * dgds::kWarp * sizeof(int32_t)));
   DGDS_CUDA(cudaMalloc(&s->d_err, sizeof(int32_t)));
   DGDS_CUDA(cudaMemsetAsync(s->d_err, 0, sizeof(int32_t), s->st));
   s->root_of_cap = 1024;
@@ -522,6 +529,7 @@ int dgds_destroy(dgds_server* s) {
   if (s->st) cudaStreamSynchronize(s->st);
   cudaFree(s->T.slots);
   cudaFree(s->T.active);
+  cudaFree(s->T.tail);
   cudaFree(s->d_used);
   cudaFree(s->d_root_of);
   cudaFree(s->d_err);
@@ -792,7 +800,6 @@ int dgds_speculate_verify_batch(dgds_server* s, int64_t n, const int32_t* handle
   L.T = s->T;
   L.root_of = s->d_root_of;
   L.n_handles = static_cast<int32_t>(s->root_of_cap);
-  L.S = std::max(1, s->p.max_spec_len);
   L.n = n;
   L.handles = reinterpret_cast<const int32_t*>(d);
   L.pat_len = reinterpret_cast<const int32_t*>(d + o_len);
@@ -819,7 +826,7 @@ int dgds_speculate_verify_batch(dgds_server* s, int64_t n, const int32_t* handle
   }
   {
     LaunchTimer lt(s, 1, s->st);
-    DGDS_CUDA(dgds::launch_query(L, max_k, s->st));
+    DGDS_CUDA(dgds::launch_query(L, max_k, max_s, s->st));
   }
   DGDS_CUDA(cudaMemcpyAsync(s->h_out.p, dout, out_total, cudaMemcpyDeviceToHost, s->st));
   DGDS_CUDA(cudaStreamSynchronize(s->st));
@@ -857,10 +864,11 @@ int dgds_speculate_batch(dgds_server* s, int64_t n, const int32_t* handles, cons
 
 int dgds_speculate_device(dgds_server* s, int64_t n, const int32_t* d_handles, const int32_t* d_pat_len,
                           const int32_t* d_patterns, int32_t pat_stride, const dgds_spec_args* d_args,
-                          int64_t args_stride, int32_t max_top_k, const dgds_candidates* d_out,
+                          int64_t args_stride, int32_t max_top_k, int32_t max_spec, const dgds_candidates* d_out,
                           const int32_t* d_truth, int32_t truth_stride, const int32_t* d_truth_left,
                           const int32_t* d_limit, const dgds_verify_out* d_vout, dgds_query_stats* d_stats,
                           void* stream) {
+  if (max_spec <= 0 || max_spec > s->p.max_spec_len) max_spec = std::max(1, s->p.max_spec_len);
   if (n < 0) return fail(DGDS_EINVAL, "negative batch size");
   if (n == 0) return DGDS_OK;
   if (max_top_k < 1 || max_top_k > DGDS_MAX_TOP_K) return fail(DGDS_EUNSUPPORTED, "max_top_k out of range");
@@ -874,7 +882,6 @@ int dgds_speculate_device(dgds_server* s, int64_t n, const int32_t* d_handles, c
   L.T = s->T;
   L.root_of = s->d_root_of;
   L.n_handles = static_cast<int32_t>(s->root_of_cap);
-  L.S = std::max(1, s->p.max_spec_len);
   L.n = n;
   L.handles = d_handles;
   L.pat_len = d_pat_len;
@@ -904,7 +911,7 @@ int dgds_speculate_device(dgds_server* s, int64_t n, const int32_t* d_handles, c
   L.err_flag = s->d_err;
   {
     LaunchTimer lt(s, 1, join.stream());
-    DGDS_CUDA(dgds::launch_query(L, max_top_k, join.stream()));
+    DGDS_CUDA(dgds::launch_query(L, max_top_k, max_spec, join.stream()));
   }
   return DGDS_OK;
 }

@@ -2,27 +2,27 @@
 //
 // One arena per GPU holds the counted suffix tries of every prompt group the
 // GPU owns (reference: one GroupDraftIndex per group, proj/src/cst.cpp:79-116).
-// B200-first layout: a single open-addressing table of 32-byte SLOTS, one DRAM
-// sector each, where a slot IS a trie node:
+// B200-first layout: one open-addressing table of 32-byte SLOTS — one DRAM
+// sector each — where a slot IS a trie node:
 //
-//   key          u64  (parent_id << 32) | uint32(token); 0 = empty slot
-//   count        u32  occurrences of the window this node spells (Node::count)
-//   first_child  u32  id of the most recently created child, 0 = none
+//   h            u64  rolling content hash of (group root, window tokens); 0 = empty
+//   parent       u32  node id of the window without its last token (root id at depth 1)
+//   token        i32  last token of the window
+//   count        u32  occurrences of the window (Node::count, cst.hpp:93)
+//   first_child  u32  most recently created child, 0 = none (Node::first_child)
 //   next_sibling u32  prepend-linked sibling list (Node::next_sibling)
-//   depth        u32  window length (1..depth_cap); used by the rebuild only
-//   root         u32  id of the group root this node hangs under (rebuild GC)
-//   pad          u32
+//   root         u32  group root id (lets a rebuild drop dead groups)
 //
-// A node's id is (slot index + 1), so a key lookup returns the node record in
-// the same 32-B sector — the reference needs an EdgeMap probe (keys_ + vals_)
-// plus a separate nodes_[] access per edge (cst.cpp:38-47,86-103). Inserting a
-// window is ONE atomicCAS on the home slot (claim-or-find) and a RED on the
-// count in the same sector; no node allocator exists at all.
+// Node id = slot index + 1. The 16-byte key {h, parent, token} is matched
+// EXACTLY — (parent, token) is the reference's edge key (cst.cpp:86-88) — so
+// hash collisions can cost a probe but never change a result. The hash only
+// chooses the HOME slot, and because it depends on window content rather than
+// on node ids, (a) append can compute and prefetch the home slot of every
+// window of a record before the dependent claim chain runs, and (b) a draft
+// query can probe all prefixes of all candidate suffixes in one parallel round
+// trip instead of walking parent -> child (cst.cpp:160-178).
 //
-// Group roots are not slots: root ids are 0xFFFFFFFF - r for root index r, so
-// (parent, token) keys stay unique across all groups in the arena. Root child
-// lists are never enumerated (a draft query's locus is never the root,
-// cst.cpp:179), so roots need no storage.
+// Group roots are not slots: root ids are 0xFFFFFFFF - r for root index r.
 #pragma once
 
 #include <cstdint>
@@ -32,34 +32,38 @@ namespace dgds {
 
 constexpr int kWarp = 32;
 constexpr uint32_t kRootTop = 0xFFFFFFFFu;
+constexpr unsigned long long kHashMul = 0x9E3779B97F4A7C15ull;  // odd multiplier of the rolling hash
 
 struct __align__(32) Slot {
-  unsigned long long key;
+  unsigned long long h;
+  uint32_t parent;
+  int32_t token;
   uint32_t count;
   uint32_t first_child;
   uint32_t next_sibling;
-  uint32_t depth;
   uint32_t root;
-  uint32_t pad;
 };
 static_assert(sizeof(Slot) == 32, "slot must be one 32-B sector");
 
-struct SlotView {  // the fields a query needs, from one 256-bit load
-  unsigned long long key;
+struct SlotView {  // one 256-bit load
+  unsigned long long h;
+  uint32_t parent;
+  int32_t token;
   uint32_t count;
   uint32_t first_child;
   uint32_t next_sibling;
-  unsigned long long tail;  // depth | root (unused by queries)
+  uint32_t root;
 };
 
 struct DevTrie {
   Slot* slots;
-  uint64_t cap;            // slots (ids 1..cap); arbitrary (fast-range reduction, not a mask)
-  uint32_t* active;        // [stream_cap][32]: active[i] = node of the last (i+1)-token context
+  uint64_t cap;              // slots (ids 1..cap); arbitrary size (fast-range reduction)
+  uint32_t* active;          // [stream][32]: node of the last (i+1)-token context (Stream::active, cst.hpp:117)
+  int32_t* tail;             // [stream][32]: ring of the last 32 tokens (position & 31)
   unsigned long long* used;  // occupied slots (device counter)
-  int32_t depth_cap;       // max_pattern_len + max_spec_len (cst.cpp:106-107)
-  int32_t lim_pattern;     // Limits::max_pattern_len
-  int32_t lim_spec;        // Limits::max_spec_len
+  int32_t depth_cap;         // max_pattern_len + max_spec_len (cst.cpp:106-107)
+  int32_t lim_pattern;       // Limits::max_pattern_len
+  int32_t lim_spec;          // Limits::max_spec_len
   int32_t pad_;
 };
 
@@ -72,38 +76,62 @@ __host__ __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
 
 __host__ __device__ __forceinline__ bool is_root_id(uint32_t id, uint64_t cap) { return id > cap; }
 
-__device__ __forceinline__ unsigned long long edge_key(uint32_t parent, int32_t token) {
-  return (static_cast<unsigned long long>(parent) << 32) | static_cast<uint32_t>(token);
+// Hash of the empty window of a group, and one rolling step.
+__device__ __forceinline__ unsigned long long root_hash(uint32_t root) { return splitmix64(root); }
+__device__ __forceinline__ unsigned long long hash_step(unsigned long long h, int32_t t) {
+  return h * kHashMul + static_cast<uint32_t>(t) + 1ull;
+}
+__device__ __forceinline__ unsigned long long key_hash(unsigned long long h) { return h ? h : 1ull; }
+
+__device__ __forceinline__ unsigned long long pack_pt(uint32_t parent, int32_t token) {
+  return static_cast<unsigned long long>(parent) |
+         (static_cast<unsigned long long>(static_cast<uint32_t>(token)) << 32);
 }
 
-// Home slot: Lemire fast-range over the 64-bit hash (uniform for any cap).
-__device__ __forceinline__ uint64_t home_slot(unsigned long long key, uint64_t cap) {
-  return __umul64hi(splitmix64(key), cap);
+// Home slot: Lemire fast-range over a remixed hash (uniform for any cap).
+__device__ __forceinline__ uint64_t home_slot(unsigned long long h, uint64_t cap) {
+  return __umul64hi(splitmix64(h), cap);
 }
 
-// One 32-byte sector per node visit (LDG.E.ENL2.256 on sm_100a), through the
-// non-coherent path: query kernels never run concurrently with an append.
 __device__ __forceinline__ SlotView load_slot_nc(const Slot* p) {
-  unsigned long long a, b, c, d_unused;
-  asm("ld.global.nc.v4.u64 {%0,%1,%2,%3}, [%4];" : "=l"(a), "=l"(b), "=l"(c), "=l"(d_unused) : "l"(p));
+  unsigned long long a, b, c, d;
+  asm("ld.global.nc.v4.u64 {%0,%1,%2,%3}, [%4];" : "=l"(a), "=l"(b), "=l"(c), "=l"(d) : "l"(p));
   SlotView v;
-  v.key = a;
-  v.count = static_cast<uint32_t>(b);
-  v.first_child = static_cast<uint32_t>(b >> 32);
-  v.next_sibling = static_cast<uint32_t>(c);
-  v.tail = d_unused;
+  v.h = a;
+  v.parent = static_cast<uint32_t>(b);
+  v.token = static_cast<int32_t>(static_cast<uint32_t>(b >> 32));
+  v.count = static_cast<uint32_t>(c);
+  v.first_child = static_cast<uint32_t>(c >> 32);
+  v.next_sibling = static_cast<uint32_t>(d);
+  v.root = static_cast<uint32_t>(d >> 32);
   return v;
 }
 
-// Read-only lookup of child (parent, token): returns the node id (0 = absent)
-// and its slot record. Mirrors GroupDraftIndex::child_of (cst.cpp:86-88).
-__device__ __forceinline__ uint32_t find_child(const DevTrie& T, uint32_t parent, int32_t token, SlotView& rec) {
-  const unsigned long long key = edge_key(parent, token);
-  uint64_t i = home_slot(key, T.cap);
+__device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
+
+// Exact lookup of the window (parent, token) whose content hash is h
+// (GroupDraftIndex::child_of, cst.cpp:86-88). Returns the node id, 0 if absent.
+__device__ __forceinline__ uint32_t find_exact(const DevTrie& T, unsigned long long h, uint32_t parent, int32_t token,
+                                               SlotView& rec) {
+  const unsigned long long pt = pack_pt(parent, token);
+  uint64_t i = home_slot(h, T.cap);
   while (true) {
     rec = load_slot_nc(T.slots + i);
-    if (rec.key == key) return static_cast<uint32_t>(i + 1);
-    if (rec.key == 0ull) return 0;
+    if (rec.h == h && pack_pt(rec.parent, rec.token) == pt) return static_cast<uint32_t>(i + 1);
+    if (rec.h == 0ull) return 0;
+    i = (i + 1 == T.cap) ? 0 : i + 1;
+  }
+}
+
+// Parent-free probe: first slot with content hash h and last token `token`.
+// Exactness is restored by the caller's parent-chain check (find_exact on mismatch).
+__device__ __forceinline__ uint32_t find_by_content(const DevTrie& T, unsigned long long h, int32_t token,
+                                                    SlotView& rec) {
+  uint64_t i = home_slot(h, T.cap);
+  while (true) {
+    rec = load_slot_nc(T.slots + i);
+    if (rec.h == h && rec.token == token) return static_cast<uint32_t>(i + 1);
+    if (rec.h == 0ull) return 0;
     i = (i + 1 == T.cap) ? 0 : i + 1;
   }
 }
