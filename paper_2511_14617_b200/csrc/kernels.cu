@@ -48,35 +48,61 @@ __device__ __forceinline__ int lane_id() { return threadIdx.x & (kWarp - 1); }
 // claim chain (a token's parents are the previous token's nodes), whose CASes
 // then hit L2 instead of DRAM.
 
+// 16-byte key of a slot through L2 (coherent with the CASes of other warps).
+__device__ __forceinline__ void load_key_cg(const Slot* p, unsigned long long& k0, unsigned long long& k1) {
+  asm volatile("ld.global.cg.v2.u64 {%0,%1}, [%2];" : "=l"(k0), "=l"(k1) : "l"(p));
+}
+
+__device__ __forceinline__ void cas128(Slot* s, unsigned long long h, unsigned long long pt, unsigned long long& o0,
+                                       unsigned long long& o1) {
+  // {h, parent|token}: empty -> ours (claim), else returns the occupant
+  asm volatile(
+      "{\n\t.reg .b128 c, v, o;\n\t"
+      "mov.b128 c, {%2, %3};\n\t"
+      "mov.b128 v, {%4, %5};\n\t"
+      "atom.global.cas.b128 o, [%6], c, v;\n\t"
+      "mov.b128 {%0, %1}, o;\n\t}"
+      : "=l"(o0), "=l"(o1)
+      : "l"(0ull), "l"(0ull), "l"(h), "l"(pt), "l"(s)
+      : "memory");
+}
+
+// Claim-or-find of window {h, parent, token} (ensure_child, cst.cpp:90-103):
+// read the bucket's 4 keys in one line read, bump the count of a match, else
+// CAS the first empty slot; a lost race re-examines the rest of the bucket.
 __device__ __forceinline__ void claim(const DevTrie& T, unsigned long long h, uint32_t parent, int32_t token,
                                       uint32_t root, uint32_t& id, bool& inserted) {
   const unsigned long long pt = pack_pt(parent, token);
-  uint64_t i = home_slot(h, T.cap);
+  const uint64_t nb = T.cap / kBucket;
+  uint64_t b = home_bucket(h, nb);
   while (true) {
-    Slot* s = T.slots + i;
-    unsigned long long o0, o1;
-    // 128-bit CAS on {h, parent|token}: empty -> ours (claim), else returns the occupant
-    asm volatile(
-        "{\n\t.reg .b128 c, v, o;\n\t"
-        "mov.b128 c, {%2, %3};\n\t"
-        "mov.b128 v, {%4, %5};\n\t"
-        "atom.global.cas.b128 o, [%6], c, v;\n\t"
-        "mov.b128 {%0, %1}, o;\n\t}"
-        : "=l"(o0), "=l"(o1)
-        : "l"(0ull), "l"(0ull), "l"(h), "l"(pt), "l"(s)
-        : "memory");
-    if (o0 == 0ull || (o0 == h && o1 == pt)) {
-      atomicAdd(&s->count, 1u);  // RED: result unused
-      inserted = (o0 == 0ull);
-      if (inserted) s->root = root;
-      id = static_cast<uint32_t>(i + 1);
-      return;
+    Slot* base = T.slots + b * kBucket;
+    unsigned long long k0[kBucket], k1[kBucket];
+#pragma unroll
+    for (int s = 0; s < kBucket; ++s) load_key_cg(base + s, k0[s], k1[s]);
+#pragma unroll
+    for (int s = 0; s < kBucket; ++s) {
+      bool mine = k0[s] == h && k1[s] == pt;
+      bool ins = false;
+      if (!mine && k0[s] == 0ull) {
+        unsigned long long o0, o1;
+        cas128(base + s, h, pt, o0, o1);
+        ins = o0 == 0ull;
+        mine = ins || (o0 == h && o1 == pt);
+      }
+      if (mine) {
+        atomicAdd(&base[s].count, 1u);  // RED: result unused
+        if (ins) base[s].root = root;
+        inserted = ins;
+        id = static_cast<uint32_t>(b * kBucket + s + 1);
+        return;
+      }
     }
-    i = (i + 1 == T.cap) ? 0 : i + 1;
+    b = (b + 1 == nb) ? 0 : b + 1;
   }
 }
 
-__global__ void __launch_bounds__(kBlock) k_append(DevTrie T, const AppendSeg* __restrict__ segs, int64_t nseg,
+__global__ void __launch_bounds__(kBlock, 4) k_append(DevTrie T, const AppendSeg* __restrict__ segs, int64_t nseg,
                                                    const AppendPiece* __restrict__ pieces,
                                                    const int32_t* __restrict__ tokens) {
   const int lane = lane_id();
@@ -118,7 +144,7 @@ __global__ void __launch_bounds__(kBlock) k_append(DevTrie T, const AppendSeg* _
             const unsigned long long up = __shfl_up_sync(kFull, h, 1);
             h = hash_step(lane == 0 ? hr : up, t);
             if (static_cast<uint64_t>(lane) < min(static_cast<uint64_t>(D), len + 1))
-              prefetch_l2(T.slots + home_slot(key_hash(h), T.cap));
+              prefetch_l2_line(T.slots + home_bucket(key_hash(h), T.cap / kBucket) * kBucket);
             ++len;
           }
         }
@@ -235,7 +261,7 @@ __device__ __forceinline__ void set_tok(int32_t (&tok)[S], int d, int32_t v) {
 }
 
 template <int G, int S>
-__global__ void __launch_bounds__(kBlock) k_query(QueryLaunch P) {
+__global__ void __launch_bounds__(kBlock, 4) k_query(QueryLaunch P) {
   __shared__ GroupScratch<G, S> scratch[kBlock / G];
   const cg::thread_block_tile<G> tile = cg::tiled_partition<G>(cg::this_thread_block());
   const int gl = tile.thread_rank();
@@ -245,6 +271,11 @@ __global__ void __launch_bounds__(kBlock) k_query(QueryLaunch P) {
   GroupScratch<G, S>& sm = scratch[gib];
 
   const DevTrie& T = P.T;
+  if (P.v_emitted && gl == 0) {  // verification inputs are needed last: start their loads now
+    prefetch_l1(P.truth + q * static_cast<int64_t>(P.truth_stride));
+    prefetch_l1(P.truth_left + q);
+    prefetch_l1(P.limit + q);
+  }
   const dgds_spec_args a = P.args[q * P.args_stride];
   const int32_t hdl = P.handles[q];
   const uint32_t root = (hdl >= 0 && hdl < P.n_handles) ? P.root_of[hdl] : 0u;
@@ -269,19 +300,32 @@ __global__ void __launch_bounds__(kBlock) k_query(QueryLaunch P) {
     const int32_t* row = P.patterns + q * static_cast<int64_t>(P.pat_stride) + (row_len - start);
     const unsigned long long h0 = root_hash(root);
     const bool fast = start <= 8;
-    if (fast) {
-      const int W = nlen * start - nlen * (nlen - 1) / 2;
-      for (int w = gl; w < W; w += G) {
-        int j = 0, rem = w;
+    int32_t pr[8];  // the (<= 8) tokens of the fast path, loaded together
+#pragma unroll
+    for (int i = 0; i < 8; ++i) pr[i] = (fast && i < start) ? row[i] : 0;
+    auto tok_at = [&](int x) -> int32_t {
+      if (!fast) return row[x];
+      int32_t v = 0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        if (i == x) v = pr[i];
+      return v;
+    };
+    // window w of the flattened (suffix j, prefix i) list; suffix j starts at window b0(j)
+    auto b0 = [&](int j) { return j * start - j * (j - 1) / 2; };
+    // one parallel round of content probes for every prefix of suffixes [jlo, jhi)
+    auto probe_range = [&](int jlo, int jhi) {
+      for (int w = b0(jlo) + gl; w < b0(jhi); w += G) {
+        int j = jlo, rem = w - b0(jlo);
         while (rem >= start - j) {
           rem -= start - j;
           ++j;
         }
         const int i = rem + 1;  // prefix length of suffix j
         unsigned long long h = h0;
-        for (int t = 0; t < i; ++t) h = hash_step(h, row[j + t]);
+        for (int t = 0; t < i; ++t) h = hash_step(h, tok_at(j + t));
         SlotView r;
-        const uint32_t id = find_by_content(T, key_hash(h), row[j + i - 1], r);
+        const uint32_t id = find_by_content(T, key_hash(h), tok_at(j + i - 1), r);
         sm.a.wid[w] = id;
         sm.a.wpar[w] = id ? r.parent : 0u;
         if (i == start - j) {
@@ -290,58 +334,68 @@ __global__ void __launch_bounds__(kBlock) k_query(QueryLaunch P) {
         }
       }
       tile.sync();
-    }
+    };
     int winner = -1;
     uint32_t locus_cnt = 0, locus_fc = 0;
-    for (int u0 = 0; u0 < nlen; u0 += G) {
-      const int j = u0 + gl;
-      bool ok = false;
-      int looks = 0;
-      uint32_t cnt = 0, fc = 0;
-      if (j < nlen) {
-        const int L = start - j;
-        const int b0 = j * start - j * (j - 1) / 2;
-        uint32_t prev = root;
-        unsigned long long h = h0;
-        ok = true;
-        for (int i = 1; i <= L; ++i) {
-          ++looks;
-          const int32_t tk = row[j + i - 1];
-          h = hash_step(h, tk);
-          uint32_t id;
-          if (fast && sm.a.wid[b0 + i - 1] != 0u && sm.a.wpar[b0 + i - 1] == prev) {
-            id = sm.a.wid[b0 + i - 1];
-            if (i == L) {
-              cnt = sm.a.scnt[j];
-              fc = sm.a.sfc[j];
+    // check suffixes [jlo, jhi) in order; the first present one is the locus
+    auto verify_range = [&](int jlo, int jhi) {
+      for (int u0 = jlo; u0 < jhi; u0 += G) {
+        const int j = u0 + gl;
+        bool ok = false;
+        int looks = 0;
+        uint32_t cnt = 0, fc = 0;
+        if (j < jhi) {
+          const int L = start - j;
+          const int bj = b0(j);
+          uint32_t prev = root;
+          unsigned long long h = h0;
+          ok = true;
+          for (int i = 1; i <= L; ++i) {
+            ++looks;
+            const int32_t tk = tok_at(j + i - 1);
+            h = hash_step(h, tk);
+            uint32_t id;
+            if (fast && sm.a.wid[bj + i - 1] != 0u && sm.a.wpar[bj + i - 1] == prev) {
+              id = sm.a.wid[bj + i - 1];
+              if (i == L) {
+                cnt = sm.a.scnt[j];
+                fc = sm.a.sfc[j];
+              }
+            } else if (fast && sm.a.wid[bj + i - 1] == 0u) {
+              id = 0;  // no slot with this content at all: the window is absent
+            } else {   // hash collision (or long pattern): exact (parent, token) probe
+              SlotView r;
+              id = find_exact(T, key_hash(h), prev, tk, r);
+              if (id && i == L) {
+                cnt = r.count;
+                fc = r.first_child;
+              }
             }
-          } else if (fast && sm.a.wid[b0 + i - 1] == 0u) {
-            id = 0;  // no slot with this content at all: the window is absent
-          } else {
-            SlotView r;
-            id = find_exact(T, key_hash(h), prev, tk, r);
-            if (id && i == L) {
-              cnt = r.count;
-              fc = r.first_child;
+            if (id == 0u) {
+              ok = false;
+              break;
             }
+            prev = id;
           }
-          if (id == 0u) {
-            ok = false;
-            break;
-          }
-          prev = id;
         }
+        const unsigned m = tile.ballot(ok);
+        if (m) {
+          const int w = __ffs(m) - 1;
+          st_lookups += cg::reduce(tile, gl <= w ? looks : 0, cg::plus<int>());
+          winner = u0 + w;
+          locus_cnt = tile.shfl(cnt, w);
+          locus_fc = tile.shfl(fc, w);
+          return;
+        }
+        st_lookups += cg::reduce(tile, looks, cg::plus<int>());
       }
-      const unsigned m = tile.ballot(ok);
-      if (m) {
-        const int w = __ffs(m) - 1;
-        st_lookups += cg::reduce(tile, gl <= w ? looks : 0, cg::plus<int>());
-        winner = u0 + w;
-        locus_cnt = tile.shfl(cnt, w);
-        locus_fc = tile.shfl(fc, w);
-        break;
-      }
-      st_lookups += cg::reduce(tile, looks, cg::plus<int>());
+    };
+    // the longest suffix first (it usually hits), the shorter ones only when it misses
+    if (fast) probe_range(0, 1);
+    verify_range(0, 1);
+    if (winner < 0 && nlen > 1) {
+      if (fast) probe_range(1, nlen);
+      verify_range(1, nlen);
     }
     tile.sync();  // phase-A scratch is dead from here (reused for finals)
 
@@ -427,6 +481,7 @@ __global__ void __launch_bounds__(kBlock) k_query(QueryLaunch P) {
             if (qual) {
               grew = true;
               sc = __dmul_rn(b_score, step);
+              if (r.first_child) prefetch_l1(T.slots + (r.first_child - 1));  // next level's first load
             }
           }
           unsigned m = tile.ballot(qual);
@@ -603,8 +658,16 @@ __global__ void k_rebuild_place(DevTrie from, DevTrie to, const uint32_t* __rest
     if (s.h == 0ull) continue;
     const uint32_t ridx = kRootTop - s.root;
     if (!((root_alive[ridx >> 5] >> (ridx & 31)) & 1u)) continue;
-    uint64_t j = home_slot(s.h, to.cap);
-    while (atomicCAS(&to.slots[j].h, 0ull, s.h) != 0ull) j = (j + 1 == to.cap) ? 0 : j + 1;
+    const uint64_t nbk = to.cap / kBucket;
+    uint64_t bk = home_bucket(s.h, nbk);
+    uint64_t j = 0;
+    for (bool done = false; !done;) {
+      for (int q = 0; q < kBucket && !done; ++q) {
+        j = bk * kBucket + q;
+        done = atomicCAS(&to.slots[j].h, 0ull, s.h) == 0ull;
+      }
+      if (!done) bk = (bk + 1 == nbk) ? 0 : bk + 1;
+    }
     Slot* d = to.slots + j;
     d->parent = s.parent;  // old id until pass 2
     d->token = s.token;

@@ -88,9 +88,14 @@ __device__ __forceinline__ unsigned long long pack_pt(uint32_t parent, int32_t t
          (static_cast<unsigned long long>(static_cast<uint32_t>(token)) << 32);
 }
 
-// Home slot: Lemire fast-range over a remixed hash (uniform for any cap).
-__device__ __forceinline__ uint64_t home_slot(unsigned long long h, uint64_t cap) {
-  return __umul64hi(splitmix64(h), cap);
+// Slots are grouped in BUCKETS of 4 (one 128-B line). Probing is linear at
+// bucket granularity: a lookup reads a whole line per step, so a window is
+// usually resolved with one line read whatever its position inside the bucket.
+constexpr int kBucket = 4;
+
+// Home bucket: Lemire fast-range over a remixed hash (uniform for any size).
+__device__ __forceinline__ uint64_t home_bucket(unsigned long long h, uint64_t nbuckets) {
+  return __umul64hi(splitmix64(h), nbuckets);
 }
 
 __device__ __forceinline__ SlotView load_slot_nc(const Slot* p) {
@@ -107,33 +112,50 @@ __device__ __forceinline__ SlotView load_slot_nc(const Slot* p) {
   return v;
 }
 
-__device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
+// 16-byte key {h, parent|token} of a slot, read-only path.
+__device__ __forceinline__ void load_key_nc(const Slot* p, unsigned long long& k0, unsigned long long& k1) {
+  asm("ld.global.nc.v2.u64 {%0,%1}, [%2];" : "=l"(k0), "=l"(k1) : "l"(p));
+}
 
-// Exact lookup of the window (parent, token) whose content hash is h
-// (GroupDraftIndex::child_of, cst.cpp:86-88). Returns the node id, 0 if absent.
-__device__ __forceinline__ uint32_t find_exact(const DevTrie& T, unsigned long long h, uint32_t parent, int32_t token,
-                                               SlotView& rec) {
+__device__ __forceinline__ void prefetch_l2_line(const void* p) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], 128;" ::"l"(p) : "memory");
+}
+__device__ __forceinline__ void prefetch_l1(const void* p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
+
+// Bucket probe on the read-only path. exact: match {h, parent|token};
+// otherwise match {h, token} (content probe — the caller checks the parent).
+// Returns the node id (slot + 1), 0 if absent; rec = the matched slot.
+template <bool kExact>
+__device__ __forceinline__ uint32_t probe(const DevTrie& T, unsigned long long h, uint32_t parent, int32_t token,
+                                          SlotView& rec) {
+  const uint64_t nb = T.cap / kBucket;
   const unsigned long long pt = pack_pt(parent, token);
-  uint64_t i = home_slot(h, T.cap);
+  uint64_t b = home_bucket(h, nb);
   while (true) {
-    rec = load_slot_nc(T.slots + i);
-    if (rec.h == h && pack_pt(rec.parent, rec.token) == pt) return static_cast<uint32_t>(i + 1);
-    if (rec.h == 0ull) return 0;
-    i = (i + 1 == T.cap) ? 0 : i + 1;
+    const Slot* base = T.slots + b * kBucket;
+    unsigned long long k0[kBucket], k1[kBucket];
+#pragma unroll
+    for (int s = 0; s < kBucket; ++s) load_key_nc(base + s, k0[s], k1[s]);
+#pragma unroll
+    for (int s = 0; s < kBucket; ++s) {
+      const bool hit = k0[s] == h && (kExact ? k1[s] == pt : static_cast<int32_t>(k1[s] >> 32) == token);
+      if (hit) {
+        rec = load_slot_nc(base + s);  // same sector as the key: an L1 hit
+        return static_cast<uint32_t>(b * kBucket + s + 1);
+      }
+      if (k0[s] == 0ull) return 0;
+    }
+    b = (b + 1 == nb) ? 0 : b + 1;
   }
 }
 
-// Parent-free probe: first slot with content hash h and last token `token`.
-// Exactness is restored by the caller's parent-chain check (find_exact on mismatch).
+__device__ __forceinline__ uint32_t find_exact(const DevTrie& T, unsigned long long h, uint32_t parent, int32_t token,
+                                               SlotView& rec) {
+  return probe<true>(T, h, parent, token, rec);
+}
 __device__ __forceinline__ uint32_t find_by_content(const DevTrie& T, unsigned long long h, int32_t token,
                                                     SlotView& rec) {
-  uint64_t i = home_slot(h, T.cap);
-  while (true) {
-    rec = load_slot_nc(T.slots + i);
-    if (rec.h == h && rec.token == token) return static_cast<uint32_t>(i + 1);
-    if (rec.h == 0ull) return 0;
-    i = (i + 1 == T.cap) ? 0 : i + 1;
-  }
+  return probe<false>(T, h, 0u, token, rec);
 }
 
 }  // namespace dgds
