@@ -14,8 +14,6 @@
 //
 // Nothing here is a dense contraction, so there is no tensor-core path: every
 // kernel is bound by dependent 32-B sector accesses to HBM / L2.
-#include <cooperative_groups.h>
-#include <cooperative_groups/reduce.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -23,8 +21,6 @@
 #include "kernels.h"
 
 namespace dgds {
-
-namespace cg = cooperative_groups;
 
 namespace {
 
@@ -68,8 +64,9 @@ __device__ __forceinline__ void cas128(Slot* s, unsigned long long h, unsigned l
 }
 
 // Claim-or-find of window {h, parent, token} (ensure_child, cst.cpp:90-103):
-// read the bucket's 4 keys in one line read, bump the count of a match, else
-// CAS the first empty slot; a lost race re-examines the rest of the bucket.
+// read the bucket's 4 keys in one line read; a match only bumps the count,
+// otherwise ONE CAS claims the first empty slot (a single CAS site keeps the
+// lanes of the warp convergent). A lost race re-reads the same bucket.
 __device__ __forceinline__ void claim(const DevTrie& T, unsigned long long h, uint32_t parent, int32_t token,
                                       uint32_t root, uint32_t& id, bool& inserted) {
   const unsigned long long pt = pack_pt(parent, token);
@@ -80,25 +77,31 @@ __device__ __forceinline__ void claim(const DevTrie& T, unsigned long long h, ui
     unsigned long long k0[kBucket], k1[kBucket];
 #pragma unroll
     for (int s = 0; s < kBucket; ++s) load_key_cg(base + s, k0[s], k1[s]);
+    int found = -1, empty = -1;
 #pragma unroll
-    for (int s = 0; s < kBucket; ++s) {
-      bool mine = k0[s] == h && k1[s] == pt;
-      bool ins = false;
-      if (!mine && k0[s] == 0ull) {
-        unsigned long long o0, o1;
-        cas128(base + s, h, pt, o0, o1);
-        ins = o0 == 0ull;
-        mine = ins || (o0 == h && o1 == pt);
-      }
-      if (mine) {
-        atomicAdd(&base[s].count, 1u);  // RED: result unused
-        if (ins) base[s].root = root;
-        inserted = ins;
-        id = static_cast<uint32_t>(b * kBucket + s + 1);
-        return;
+    for (int s = kBucket - 1; s >= 0; --s) {  // first match / first empty in probe order
+      if (k0[s] == h && k1[s] == pt) found = s;
+      if (k0[s] == 0ull) {
+        empty = s;
+        found = found > s ? -1 : found;  // nothing valid lies beyond an empty slot
       }
     }
-    b = (b + 1 == nb) ? 0 : b + 1;
+    bool ins = false;
+    if (found < 0 && empty >= 0) {
+      unsigned long long o0, o1;
+      cas128(base + empty, h, pt, o0, o1);
+      ins = o0 == 0ull;
+      if (ins || (o0 == h && o1 == pt)) found = empty;
+      else continue;  // lost the slot to another key: re-read this bucket
+    }
+    if (found >= 0) {
+      atomicAdd(&base[found].count, 1u);  // RED: result unused
+      if (ins) base[found].root = root;
+      inserted = ins;
+      id = static_cast<uint32_t>(b * kBucket + found + 1);
+      return;
+    }
+    b = (b + 1 == nb) ? 0 : b + 1;  // bucket full without a match
   }
 }
 
@@ -200,25 +203,30 @@ __global__ void __launch_bounds__(kBlock, 4) k_append(DevTrie T, const AppendSeg
 }
 
 // ---------------------------------------------------------------------------
-// K2 + K3: draft query with fused verification, one G-lane tile per request.
+// K2 + K3: draft query with fused verification.
 //
-// Phase A (longest admissible suffix, cst.cpp:160-178). For start <= 8 (the
-// default Limits), the tile probes ALL prefixes of ALL admissible suffixes
-// by content hash in one parallel round trip, then checks each suffix's
-// parent chain (root -> ... -> suffix) from the probe records; a mismatch
-// (hash collision) falls back to an exact (parent, token) probe. The longest
-// fully present suffix is the reference's first success, with no fallback
-// after it. Longer patterns walk each suffix with exact probes.
+// A warp serves 32/G requests, one G-lane tile each, and runs them in LOCK
+// STEP: every loop bound is warp-uniform (the max over the warp's tiles) and
+// per-tile work is predicated, so the dependent memory chains of all tiles
+// issue together instead of serialising behind divergent branches.
 //
-// Phase B (beam, cst.cpp:180-221). Lane b owns beam path b (its tokens live in
-// registers) and walks its child list; qualifying children are merged one by
-// one into a tile-distributed sorted pool of size top_k — lane r holds rank r
+// Phase A (longest admissible suffix, cst.cpp:160-178). The longest suffix is
+// tried first: its (<= 8) prefixes are probed by content hash in one round
+// (two probes in flight per lane), then the parent chain root -> ... -> suffix
+// is checked from the probe records; a parent mismatch (hash collision) falls
+// back to an exact (parent, token) probe. Only when it is absent are the
+// shorter suffixes probed, in order; the first present one is the locus and
+// there is no fallback after it.
+//
+// Phase B (beam, cst.cpp:180-221). Lane b owns beam path b (tokens in
+// registers) and walks its child list; qualifying children are merged one at a
+// time into a tile-distributed sorted pool of size top_k — lane r holds rank r
 // under path_before: FP64 score desc (cnt / parent_cnt products, IEEE
 // round-to-nearest, reference operation order), support desc, token path
 // lexicographic asc. Equal-length paths compare as (parent path rank, token),
-// so only ranks travel. Finals follow cst.cpp:213-214 (a path is final only
-// when it has no qualifying child) and are kept top-k under candidate_before
-// (cst.cpp:29-33,225-227) by lane 0 in shared memory.
+// so only ranks travel. Finals follow cst.cpp:213-214 (final only with no
+// qualifying child) and are kept top-k under candidate_before (cst.cpp:29-33,
+// 225-227) by the tile's lane 0 in shared memory.
 
 template <int G, int S>
 struct __align__(16) GroupScratch {
@@ -260,304 +268,440 @@ __device__ __forceinline__ void set_tok(int32_t (&tok)[S], int d, int32_t v) {
     if (i == d) tok[i] = v;
 }
 
+// tile-width collectives over a full, convergent warp
+template <int G>
+struct Tile {
+  int tbase;
+  __device__ __forceinline__ unsigned ballot(bool p) const {
+    const unsigned m = __ballot_sync(kFull, p);
+    return G == 32 ? m : (m >> tbase) & ((1u << G) - 1u);
+  }
+  template <class T>
+  __device__ __forceinline__ T shfl(T v, int src) const {
+    return __shfl_sync(kFull, v, src, G);
+  }
+  template <class T>
+  __device__ __forceinline__ T shfl_up(T v, int d) const {
+    return __shfl_up_sync(kFull, v, d, G);
+  }
+  __device__ __forceinline__ int sum(int v) const {
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o, G);
+    return v;
+  }
+  __device__ __forceinline__ int max(int v) const {
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) v = ::max(v, __shfl_xor_sync(kFull, v, o, G));
+    return v;
+  }
+};
+
+__device__ __forceinline__ unsigned long long ld_nc_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm("ld.global.nc.u64 %0, [%1];" : "=l"(v) : "l"(p));
+  return v;
+}
+
+// Resolve a content probe whose home-bucket hashes (hb[]) are already loaded.
+__device__ __forceinline__ uint32_t resolve_content(const DevTrie& T, unsigned long long h, int32_t token, uint64_t b,
+                                                    const unsigned long long (&hb)[kBucket], SlotView& rec) {
+  const uint64_t nb = T.cap / kBucket;
+  bool first = true;
+  while (true) {
+    const Slot* base = T.slots + b * kBucket;
+#pragma unroll
+    for (int s = 0; s < kBucket; ++s) {
+      const unsigned long long hs = first ? hb[s] : ld_nc_u64(&base[s].h);
+      if (hs == h) {
+        rec = load_slot_nc(base + s);  // same sector as the hash: an L1 hit
+        if (rec.token == token) return static_cast<uint32_t>(b * kBucket + s + 1);
+      }
+      if (hs == 0ull) return 0;
+    }
+    first = false;
+    b = (b + 1 == nb) ? 0 : b + 1;
+  }
+}
+
 template <int G, int S>
 __global__ void __launch_bounds__(kBlock, 4) k_query(QueryLaunch P) {
-  __shared__ GroupScratch<G, S> scratch[kBlock / G];
-  const cg::thread_block_tile<G> tile = cg::tiled_partition<G>(cg::this_thread_block());
-  const int gl = tile.thread_rank();
+  constexpr int kTiles = kBlock / G;
+  __shared__ GroupScratch<G, S> scratch[kTiles];
+  const int lane = lane_id();
+  const int gl = lane % G;
+  const Tile<G> tile{lane - gl};
   const int gib = threadIdx.x / G;
-  const int64_t q = static_cast<int64_t>(blockIdx.x) * (blockDim.x / G) + gib;
-  if (q >= P.n) return;  // tile-uniform
+  const int64_t q = static_cast<int64_t>(blockIdx.x) * kTiles + gib;
+  const bool valid = q < P.n;  // invalid tiles stay (convergence) but do nothing
+  const int64_t qi = valid ? q : 0;
   GroupScratch<G, S>& sm = scratch[gib];
-
   const DevTrie& T = P.T;
-  if (P.v_emitted && gl == 0) {  // verification inputs are needed last: start their loads now
-    prefetch_l1(P.truth + q * static_cast<int64_t>(P.truth_stride));
-    prefetch_l1(P.truth_left + q);
-    prefetch_l1(P.limit + q);
+
+  const dgds_spec_args a = P.args[qi * P.args_stride];
+  const int32_t hdl = P.handles[qi];
+  const int plen = P.pat_len[qi];
+  int32_t tleft = 0, lim = 0;
+  if (P.v_emitted) {
+    tleft = P.truth_left[qi];
+    lim = P.limit[qi];
   }
-  const dgds_spec_args a = P.args[q * P.args_stride];
-  const int32_t hdl = P.handles[q];
-  const uint32_t root = (hdl >= 0 && hdl < P.n_handles) ? P.root_of[hdl] : 0u;
-  const int plen = P.pat_len[q];
+  const uint32_t root = (valid && hdl >= 0 && hdl < P.n_handles) ? P.root_of[hdl] : 0u;
   const int eff_pmax = min(a.pattern_lookup_max, T.lim_pattern);  // cst.cpp:156-158
   const int eff_smax = min(a.max_spec_tokens, T.lim_spec);
   const int kq = a.top_k;
   const bool bad_args = a.pattern_lookup_min < 1 || a.pattern_lookup_min > a.pattern_lookup_max ||
                         a.max_spec_tokens < 0 || a.top_k < 1 || a.top_k > G || !(a.min_step_freq >= 0.0) ||
                         a.min_support < 0 || eff_smax > S;
-  if (bad_args && gl == 0 && P.err_flag) atomicExch(P.err_flag, 1);
+  if (valid && bad_args && gl == 0 && P.err_flag) atomicExch(P.err_flag, 1);
 
-  int nf = 0;  // finals kept (tile-uniform)
+  const int start = max(0, min(eff_pmax, plen));
+  const int nlen = start - a.pattern_lookup_min + 1;
+  const bool act = valid && !bad_args && root != 0u && plen > 0 && a.pattern_lookup_min <= eff_pmax && nlen > 0;
+  const bool fast = start <= 8;
+  const int row_len = min(plen, P.pat_stride);
+  // row[0..start) = the last `start` pattern tokens; suffix j (length start-j) starts at row + j
+  const int32_t* row = P.patterns + qi * static_cast<int64_t>(P.pat_stride) + (row_len - start);
+  int32_t pr[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) pr[i] = (act && fast && i < start) ? row[i] : 0;
+  auto tok_at = [&](int x) -> int32_t {
+    int32_t v = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      if (i == x) v = pr[i];
+    return (act && !fast) ? row[x] : v;
+  };
+  const unsigned long long h0 = root_hash(root);
+  auto hash_prefix = [&](int j, int i) {  // hash of row[j .. j+i)
+    unsigned long long h = h0;
+#pragma unroll
+    for (int t = 0; t < 8; ++t)
+      if (t < i) h = hash_step(h, tok_at(j + t));
+    return key_hash(h);
+  };
+  auto b0 = [&](int j) { return j * start - j * (j - 1) / 2; };  // first window of suffix j
+
   int st_lookups = 0, st_exp = 0, st_csec = 0;
+  int winner = -1;
+  uint32_t locus_cnt = 0, locus_fc = 0;
+  const uint64_t nbk = T.cap / kBucket;
 
-  if (!bad_args && root != 0u && plen > 0 && a.pattern_lookup_min <= eff_pmax) {
-    // ---------------- phase A ----------------
-    const int start = min(eff_pmax, plen);
-    const int nlen = start - a.pattern_lookup_min + 1;
-    const int row_len = min(plen, P.pat_stride);
-    // row[0..start) = the last `start` pattern tokens; suffix j (length start-j) starts at row + j
-    const int32_t* row = P.patterns + q * static_cast<int64_t>(P.pat_stride) + (row_len - start);
-    const unsigned long long h0 = root_hash(root);
-    const bool fast = start <= 8;
-    int32_t pr[8];  // the (<= 8) tokens of the fast path, loaded together
+  // ---------------- phase A ----------------
+  // (1) the longest suffix: windows i = gl+1 and gl+1+G, both probes in flight
+  {
+    const int i1 = gl + 1, i2 = gl + 1 + G;
+    const bool d1 = act && fast && i1 <= start;
+    const bool d2 = act && fast && G < 8 && i2 <= start;
+    const unsigned long long h1 = hash_prefix(0, i1), h2 = hash_prefix(0, i2);
+    const uint64_t bk1 = home_bucket(h1, nbk), bk2 = home_bucket(h2, nbk);
+    unsigned long long x[kBucket], y[kBucket];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) pr[i] = (fast && i < start) ? row[i] : 0;
-    auto tok_at = [&](int x) -> int32_t {
-      if (!fast) return row[x];
-      int32_t v = 0;
-#pragma unroll
-      for (int i = 0; i < 8; ++i)
-        if (i == x) v = pr[i];
-      return v;
-    };
-    // window w of the flattened (suffix j, prefix i) list; suffix j starts at window b0(j)
-    auto b0 = [&](int j) { return j * start - j * (j - 1) / 2; };
-    // one parallel round of content probes for every prefix of suffixes [jlo, jhi)
-    auto probe_range = [&](int jlo, int jhi) {
-      for (int w = b0(jlo) + gl; w < b0(jhi); w += G) {
-        int j = jlo, rem = w - b0(jlo);
-        while (rem >= start - j) {
+    for (int s = 0; s < kBucket; ++s) {
+      x[s] = d1 ? ld_nc_u64(&T.slots[bk1 * kBucket + s].h) : 0ull;
+      y[s] = d2 ? ld_nc_u64(&T.slots[bk2 * kBucket + s].h) : 0ull;
+    }
+    if (d1) {
+      SlotView r;
+      const uint32_t id = resolve_content(T, h1, tok_at(i1 - 1), bk1, x, r);
+      sm.a.wid[i1 - 1] = id;
+      sm.a.wpar[i1 - 1] = id ? r.parent : 0u;
+      if (i1 == start) {
+        sm.a.scnt[0] = id ? r.count : 0u;
+        sm.a.sfc[0] = id ? r.first_child : 0u;
+      }
+    }
+    if (d2) {
+      SlotView r;
+      const uint32_t id = resolve_content(T, h2, tok_at(i2 - 1), bk2, y, r);
+      sm.a.wid[i2 - 1] = id;
+      sm.a.wpar[i2 - 1] = id ? r.parent : 0u;
+      if (i2 == start) {
+        sm.a.scnt[0] = id ? r.count : 0u;
+        sm.a.sfc[0] = id ? r.first_child : 0u;
+      }
+    }
+    __syncwarp();
+  }
+  // check the chain of suffix j from the probe records (exact fallback on mismatch)
+  auto check_suffix = [&](int j, int& looks, uint32_t& cnt, uint32_t& fc) -> bool {
+    const int L = start - j;
+    const int bj = b0(j);
+    uint32_t prev = root;
+    unsigned long long h = h0;
+    for (int i = 1; i <= L; ++i) {
+      ++looks;
+      const int32_t tk = tok_at(j + i - 1);
+      h = hash_step(h, tk);
+      uint32_t id;
+      if (fast && sm.a.wid[bj + i - 1] != 0u && sm.a.wpar[bj + i - 1] == prev) {
+        id = sm.a.wid[bj + i - 1];
+        if (i == L) {
+          cnt = sm.a.scnt[j];
+          fc = sm.a.sfc[j];
+        }
+      } else if (fast && sm.a.wid[bj + i - 1] == 0u) {
+        id = 0;  // no slot with this content at all: the window is absent
+      } else {   // hash collision or long pattern: exact (parent, token) probe
+        SlotView r;
+        id = find_exact(T, key_hash(h), prev, tk, r);
+        if (id && i == L) {
+          cnt = r.count;
+          fc = r.first_child;
+        }
+      }
+      if (id == 0u) return false;
+      prev = id;
+    }
+    return true;
+  };
+  {
+    int looks = 0;
+    uint32_t cnt = 0, fc = 0;
+    const bool ok = act && gl == 0 && check_suffix(0, looks, cnt, fc);
+    st_lookups = tile.shfl(looks, 0);
+    if (tile.shfl(static_cast<int>(ok), 0)) {
+      winner = 0;
+      locus_cnt = tile.shfl(cnt, 0);
+      locus_fc = tile.shfl(fc, 0);
+    }
+  }
+  // (2) only when the longest suffix is absent: the shorter ones, in order
+  const bool need2 = act && winner < 0 && nlen > 1;
+  if (__any_sync(kFull, need2)) {
+    if (__any_sync(kFull, need2 && fast)) {
+      const int W = need2 && fast ? b0(nlen) - b0(1) : 0;
+      const int Wmax = tile.max(W);
+      const int iters = __reduce_max_sync(kFull, (Wmax + G - 1) / G);
+      for (int it = 0; it < iters; ++it) {
+        const int w = b0(1) + gl + it * G;
+        const bool dw = w < b0(1) + W;
+        int j = 1, rem = w - b0(1);
+        while (dw && rem >= start - j) {
           rem -= start - j;
           ++j;
         }
-        const int i = rem + 1;  // prefix length of suffix j
-        unsigned long long h = h0;
-        for (int t = 0; t < i; ++t) h = hash_step(h, tok_at(j + t));
+        const int i = rem + 1;
+        uint32_t id = 0;
         SlotView r;
-        const uint32_t id = find_by_content(T, key_hash(h), tok_at(j + i - 1), r);
-        sm.a.wid[w] = id;
-        sm.a.wpar[w] = id ? r.parent : 0u;
-        if (i == start - j) {
-          sm.a.scnt[j] = id ? r.count : 0u;
-          sm.a.sfc[j] = id ? r.first_child : 0u;
-        }
-      }
-      tile.sync();
-    };
-    int winner = -1;
-    uint32_t locus_cnt = 0, locus_fc = 0;
-    // check suffixes [jlo, jhi) in order; the first present one is the locus
-    auto verify_range = [&](int jlo, int jhi) {
-      for (int u0 = jlo; u0 < jhi; u0 += G) {
-        const int j = u0 + gl;
-        bool ok = false;
-        int looks = 0;
-        uint32_t cnt = 0, fc = 0;
-        if (j < jhi) {
-          const int L = start - j;
-          const int bj = b0(j);
-          uint32_t prev = root;
-          unsigned long long h = h0;
-          ok = true;
-          for (int i = 1; i <= L; ++i) {
-            ++looks;
-            const int32_t tk = tok_at(j + i - 1);
-            h = hash_step(h, tk);
-            uint32_t id;
-            if (fast && sm.a.wid[bj + i - 1] != 0u && sm.a.wpar[bj + i - 1] == prev) {
-              id = sm.a.wid[bj + i - 1];
-              if (i == L) {
-                cnt = sm.a.scnt[j];
-                fc = sm.a.sfc[j];
-              }
-            } else if (fast && sm.a.wid[bj + i - 1] == 0u) {
-              id = 0;  // no slot with this content at all: the window is absent
-            } else {   // hash collision (or long pattern): exact (parent, token) probe
-              SlotView r;
-              id = find_exact(T, key_hash(h), prev, tk, r);
-              if (id && i == L) {
-                cnt = r.count;
-                fc = r.first_child;
-              }
-            }
-            if (id == 0u) {
-              ok = false;
-              break;
-            }
-            prev = id;
+        if (dw) {
+          const unsigned long long h = hash_prefix(j, i);
+          unsigned long long hb[kBucket];
+          const uint64_t bk = home_bucket(h, nbk);
+#pragma unroll
+          for (int s = 0; s < kBucket; ++s) hb[s] = ld_nc_u64(&T.slots[bk * kBucket + s].h);
+          id = resolve_content(T, h, tok_at(j + i - 1), bk, hb, r);
+          sm.a.wid[w] = id;
+          sm.a.wpar[w] = id ? r.parent : 0u;
+          if (i == start - j) {
+            sm.a.scnt[j] = id ? r.count : 0u;
+            sm.a.sfc[j] = id ? r.first_child : 0u;
           }
         }
-        const unsigned m = tile.ballot(ok);
+      }
+      __syncwarp();
+    }
+    // lanes check suffixes 1.., G at a time, in order
+    const int rounds = __reduce_max_sync(kFull, need2 ? (nlen - 1 + G - 1) / G : 0);
+    bool done = !need2;
+    for (int u = 0; u < rounds; ++u) {
+      const int j = 1 + u * G + gl;
+      int looks = 0;
+      uint32_t cnt = 0, fc = 0;
+      const bool ok = !done && j < nlen && check_suffix(j, looks, cnt, fc);
+      const unsigned m = tile.ballot(ok);
+      if (!done) {
         if (m) {
           const int w = __ffs(m) - 1;
-          st_lookups += cg::reduce(tile, gl <= w ? looks : 0, cg::plus<int>());
-          winner = u0 + w;
+          st_lookups += tile.sum(gl <= w ? looks : 0);
+          winner = 1 + u * G + w;
           locus_cnt = tile.shfl(cnt, w);
           locus_fc = tile.shfl(fc, w);
-          return;
+          done = true;
+        } else {
+          st_lookups += tile.sum(looks);
         }
-        st_lookups += cg::reduce(tile, looks, cg::plus<int>());
+      } else {
+        (void)tile.sum(0);
+        (void)tile.shfl(cnt, 0);
+        (void)tile.shfl(fc, 0);
       }
-    };
-    // the longest suffix first (it usually hits), the shorter ones only when it misses
-    if (fast) probe_range(0, 1);
-    verify_range(0, 1);
-    if (winner < 0 && nlen > 1) {
-      if (fast) probe_range(1, nlen);
-      verify_range(1, nlen);
     }
-    tile.sync();  // phase-A scratch is dead from here (reused for finals)
+  }
+  __syncwarp();  // phase-A scratch is dead from here (reused for finals)
 
-    if (winner >= 0) {
-      // ---------------- phase B ----------------
-      int32_t tok[S];
+  // ---------------- phase B ----------------
+  int nf = 0;  // finals kept (tile-uniform)
+  int32_t tok[S];
 #pragma unroll
-      for (int i = 0; i < S; ++i) tok[i] = 0;
-      int nb = 1;
-      uint32_t b_fc = locus_fc;
-      double b_score = 1.0;
-      long long b_sup = static_cast<long long>(locus_cnt);
-      int b_lex = 0;
-      const double msf = a.min_step_freq;
-      const long long msup = a.min_support;
+  for (int i = 0; i < S; ++i) tok[i] = 0;
+  int nb = winner >= 0 ? 1 : 0;
+  uint32_t b_fc = locus_fc;
+  double b_score = 1.0;
+  long long b_sup = static_cast<long long>(locus_cnt);
+  int b_lex = 0;
+  int dl = 0;  // depth reached (tokens per beam path)
+  const double msf = a.min_step_freq;
+  const long long msup = a.min_support;
 
-      auto finals_offer = [&](int b, int len) {
-        int32_t ct[S];
+  // offer beam path b (dl tokens) of each tile with want=true to its finals
+  auto finals_offer = [&](bool want, int b) {
+    int32_t ct[S];
 #pragma unroll
-        for (int i = 0; i < S; ++i) ct[i] = tile.shfl(tok[i], b);
-        const double cs = tile.shfl(b_score, b);
-        const long long cp = tile.shfl(b_sup, b);
-        if (gl == 0) {
-          int dst = -1;
-          if (nf < kq) {
-            dst = nf++;
-          } else {
-            int w = 0;  // worst kept final
-            for (int c = 1; c < nf; ++c)
-              if (cand_before(sm.f.score[w], sm.f.sup[w], sm.f.tok[w], sm.f.len[w], sm.f.score[c], sm.f.sup[c],
-                              sm.f.tok[c], sm.f.len[c]))
-                w = c;
-            bool better;
-            if (cs != sm.f.score[w]) {
-              better = cs > sm.f.score[w];
-            } else if (cp != sm.f.sup[w]) {
-              better = cp > sm.f.sup[w];
-            } else {
-              int r = 0;  // lexicographic compare of ct[0..len) with the kept final
-              const int m = len < sm.f.len[w] ? len : sm.f.len[w];
+    for (int i = 0; i < S; ++i) ct[i] = tile.shfl(tok[i], b);
+    const double cs = tile.shfl(b_score, b);
+    const long long cp = tile.shfl(b_sup, b);
+    if (want && gl == 0) {
+      const int len = dl;
+      int dst = -1;
+      if (nf < kq) {
+        dst = nf++;
+      } else {
+        int w = 0;  // worst kept final
+        for (int c = 1; c < nf; ++c)
+          if (cand_before(sm.f.score[w], sm.f.sup[w], sm.f.tok[w], sm.f.len[w], sm.f.score[c], sm.f.sup[c],
+                          sm.f.tok[c], sm.f.len[c]))
+            w = c;
+        bool better;
+        if (cs != sm.f.score[w]) {
+          better = cs > sm.f.score[w];
+        } else if (cp != sm.f.sup[w]) {
+          better = cp > sm.f.sup[w];
+        } else {
+          int r = 0;  // lexicographic compare of ct[0..len) with the kept final
+          const int m = len < sm.f.len[w] ? len : sm.f.len[w];
 #pragma unroll
-              for (int i = 0; i < S; ++i)
-                if (r == 0 && i < m && ct[i] != sm.f.tok[w][i]) r = ct[i] < sm.f.tok[w][i] ? -1 : 1;
-              better = r < 0 || (r == 0 && len < sm.f.len[w]);
-            }
-            if (better) dst = w;
-          }
-          if (dst >= 0) {
-#pragma unroll
-            for (int i = 0; i < S; ++i)
-              if (i < len) sm.f.tok[dst][i] = ct[i];
-            sm.f.len[dst] = len;
-            sm.f.score[dst] = cs;
-            sm.f.sup[dst] = cp;
-          }
+          for (int i = 0; i < S; ++i)
+            if (r == 0 && i < m && ct[i] != sm.f.tok[w][i]) r = ct[i] < sm.f.tok[w][i] ? -1 : 1;
+          better = r < 0 || (r == 0 && len < sm.f.len[w]);
         }
-        nf = tile.shfl(nf, 0);
-      };
-
-      int d = 0;
-      for (; d < eff_smax && nb > 0; ++d) {
-        // pool entry held by lane r (rank r), r < np
-        double p_score = 0.0;
-        long long p_sup = 0;
-        int p_lex = 0, p_src = 0;
-        int32_t p_tok = 0;
-        uint32_t p_fc = 0;
-        int np = 0;
-        uint32_t c = gl < nb ? b_fc : 0u;
-        bool grew = false;
-        int nchild = 0;
-        while (tile.any(c != 0u)) {
-          SlotView r{};
-          const bool have = c != 0u;
-          if (have) r = load_slot_nc(T.slots + (c - 1));
-          bool qual = false;
-          double sc = 0.0;
-          const long long cnt = static_cast<long long>(r.count);
-          if (have) {
-            ++nchild;
-            const double step = __ddiv_rn(static_cast<double>(cnt), static_cast<double>(b_sup));
-            qual = !(step < msf) && !(cnt < msup);
-            if (qual) {
-              grew = true;
-              sc = __dmul_rn(b_score, step);
-              if (r.first_child) prefetch_l1(T.slots + (r.first_child - 1));  // next level's first load
-            }
-          }
-          unsigned m = tile.ballot(qual);
-          while (m) {  // merge lane b's candidate into the sorted pool
-            const int b = __ffs(m) - 1;
-            m &= m - 1;
-            const double cs = tile.shfl(sc, b);
-            const long long cp = tile.shfl(cnt, b);
-            const int cl = tile.shfl(b_lex, b);
-            const int32_t ct = tile.shfl(r.token, b);
-            const uint32_t cfc = tile.shfl(r.first_child, b);
-            const bool before = gl < np && (p_score != cs ? p_score > cs
-                                            : p_sup != cp ? p_sup > cp
-                                            : p_lex != cl ? p_lex < cl
-                                                          : p_tok < ct);
-            const int pos = __popc(tile.ballot(before));
-            if (pos < kq) {
-              const double us = tile.shfl_up(p_score, 1);
-              const long long up = tile.shfl_up(p_sup, 1);
-              const int ul = tile.shfl_up(p_lex, 1);
-              const int usrc = tile.shfl_up(p_src, 1);
-              const int32_t ut = tile.shfl_up(p_tok, 1);
-              const uint32_t ufc = tile.shfl_up(p_fc, 1);
-              if (gl > pos && gl <= np) {
-                p_score = us;
-                p_sup = up;
-                p_lex = ul;
-                p_src = usrc;
-                p_tok = ut;
-                p_fc = ufc;
-              }
-              if (gl == pos) {
-                p_score = cs;
-                p_sup = cp;
-                p_lex = cl;
-                p_src = b;
-                p_tok = ct;
-                p_fc = cfc;
-              }
-              np = min(np + 1, kq);
-            }
-          }
-          c = have ? r.next_sibling : 0u;
-        }
-        st_exp += nb;
-        st_csec += cg::reduce(tile, gl < nb ? (8 * nchild + 31) / 32 : 0, cg::plus<int>());
-        // paths without a qualifying child are final (when non-empty, i.e. d > 0)
-        unsigned fm = tile.ballot(gl < nb && !grew && d > 0);
-        while (fm) {
-          const int b = __ffs(fm) - 1;
-          fm &= fm - 1;
-          finals_offer(b, d);
-        }
-        // the pool becomes the next beam: lane r takes pool rank r
-#pragma unroll
-        for (int i = 0; i < S; ++i) tok[i] = tile.shfl(tok[i], p_src);
-        set_tok<S>(tok, d, p_tok);
-        int lex = 0;
-        for (int o = 0; o < np; ++o) {
-          const int ol = tile.shfl(p_lex, o);
-          const int32_t ot = tile.shfl(p_tok, o);
-          lex += (ol < p_lex || (ol == p_lex && ot < p_tok)) ? 1 : 0;
-        }
-        b_fc = p_fc;
-        b_score = p_score;
-        b_sup = p_sup;
-        b_lex = lex;
-        nb = np;
+        if (better) dst = w;
       }
-      if (d > 0)
-        for (int b = 0; b < nb; ++b) finals_offer(b, d);  // leftover beam (cst.cpp:222-223)
+      if (dst >= 0) {
+#pragma unroll
+        for (int i = 0; i < S; ++i)
+          if (i < len) sm.f.tok[dst][i] = ct[i];
+        sm.f.len[dst] = len;
+        sm.f.score[dst] = cs;
+        sm.f.sup[dst] = cp;
+      }
     }
+    nf = tile.shfl(nf, 0);
+  };
+
+  for (int d = 0; __any_sync(kFull, nb > 0 && d < eff_smax); ++d) {
+    const bool live = nb > 0 && d < eff_smax;  // tile-uniform
+    // pool entry held by lane r (rank r), r < np
+    double p_score = 0.0;
+    long long p_sup = 0;
+    int p_lex = 0, p_src = 0;
+    int32_t p_tok = 0;
+    uint32_t p_fc = 0;
+    int np = 0;
+    uint32_t c = (live && gl < nb) ? b_fc : 0u;
+    bool grew = false;
+    int nchild = 0;
+    while (__any_sync(kFull, c != 0u)) {
+      SlotView r{};
+      const bool have = c != 0u;
+      if (have) r = load_slot_nc(T.slots + (c - 1));
+      bool qual = false;
+      double sc = 0.0;
+      const long long cnt = static_cast<long long>(r.count);
+      if (have) {
+        ++nchild;
+        const double step = __ddiv_rn(static_cast<double>(cnt), static_cast<double>(b_sup));
+        qual = !(step < msf) && !(cnt < msup);
+        if (qual) {
+          grew = true;
+          sc = __dmul_rn(b_score, step);
+          if (r.first_child) prefetch_l1(T.slots + (r.first_child - 1));  // the next level's first load
+        }
+      }
+      unsigned m = tile.ballot(qual);
+      while (__any_sync(kFull, m != 0u)) {  // merge one candidate per tile into its sorted pool
+        const bool has = m != 0u;
+        const int b = has ? __ffs(m) - 1 : 0;
+        if (has) m &= m - 1;
+        const double cs = tile.shfl(sc, b);
+        const long long cp = tile.shfl(cnt, b);
+        const int cl = tile.shfl(b_lex, b);
+        const int32_t ct = tile.shfl(r.token, b);
+        const uint32_t cfc = tile.shfl(r.first_child, b);
+        const bool before = has && gl < np &&
+                            (p_score != cs ? p_score > cs
+                             : p_sup != cp ? p_sup > cp
+                             : p_lex != cl ? p_lex < cl
+                                           : p_tok < ct);
+        const int pos = __popc(tile.ballot(before));
+        const bool ins = has && pos < kq;
+        const double us = tile.shfl_up(p_score, 1);
+        const long long up = tile.shfl_up(p_sup, 1);
+        const int ul = tile.shfl_up(p_lex, 1);
+        const int usrc = tile.shfl_up(p_src, 1);
+        const int32_t ut = tile.shfl_up(p_tok, 1);
+        const uint32_t ufc = tile.shfl_up(p_fc, 1);
+        if (ins && gl > pos && gl <= np) {
+          p_score = us;
+          p_sup = up;
+          p_lex = ul;
+          p_src = usrc;
+          p_tok = ut;
+          p_fc = ufc;
+        }
+        if (ins && gl == pos) {
+          p_score = cs;
+          p_sup = cp;
+          p_lex = cl;
+          p_src = b;
+          p_tok = ct;
+          p_fc = cfc;
+        }
+        if (ins) np = min(np + 1, kq);
+      }
+      c = have ? r.next_sibling : 0u;
+    }
+    if (live) {
+      st_exp += nb;
+    }
+    st_csec += tile.sum((live && gl < nb) ? (8 * nchild + 31) / 32 : 0);
+    // paths without a qualifying child are final (when non-empty, i.e. d > 0)
+    unsigned fm = tile.ballot(live && gl < nb && !grew && d > 0);
+    while (__any_sync(kFull, fm != 0u)) {
+      const bool has = fm != 0u;
+      const int b = has ? __ffs(fm) - 1 : 0;
+      if (has) fm &= fm - 1;
+      finals_offer(has, b);
+    }
+    // the pool becomes the next beam: lane r takes pool rank r
+    int32_t nt[S];
+#pragma unroll
+    for (int i = 0; i < S; ++i) nt[i] = tile.shfl(tok[i], p_src);
+    int lex = 0;
+    for (int o = 0; o < tile.max(live ? np : 0); ++o) {
+      const int ol = tile.shfl(p_lex, o);
+      const int32_t ot = tile.shfl(p_tok, o);
+      lex += (o < np && (ol < p_lex || (ol == p_lex && ot < p_tok))) ? 1 : 0;
+    }
+    if (live) {
+#pragma unroll
+      for (int i = 0; i < S; ++i) tok[i] = nt[i];
+      set_tok<S>(tok, d, p_tok);
+      b_fc = p_fc;
+      b_score = p_score;
+      b_sup = p_sup;
+      b_lex = lex;
+      nb = np;
+      dl = d + 1;
+    }
+  }
+  // leftover beam paths (dl tokens each) are finals when non-empty (cst.cpp:222-223)
+  {
+    const int rounds = __reduce_max_sync(kFull, dl > 0 ? nb : 0);
+    for (int b = 0; b < rounds; ++b) finals_offer(dl > 0 && b < nb, b);
   }
 
   // ---- output in candidate_before order ----
-  tile.sync();
+  __syncwarp();
   int my_rank = 0;
   if (gl < nf) {
     for (int c = 0; c < nf; ++c)
@@ -566,7 +710,7 @@ __global__ void __launch_bounds__(kBlock, 4) k_query(QueryLaunch P) {
                      ? 1
                      : 0;
   }
-  if (P.n_cands) {
+  if (P.n_cands && valid) {
     if (gl == 0) P.n_cands[q] = nf;
     if (gl < nf) {
       const int64_t o = q * P.k_stride + my_rank;
@@ -583,14 +727,22 @@ __global__ void __launch_bounds__(kBlock, 4) k_query(QueryLaunch P) {
     int drafted = 0, match = 0;
     if (gl < nf) {
       drafted = sm.f.len[gl];
-      const int32_t* tr = P.truth + q * static_cast<int64_t>(P.truth_stride);
-      const int cap = min(sm.f.len[gl], P.truth_left[q]);
-      while (match < cap && sm.f.tok[gl][match] == tr[match]) ++match;
+      const int32_t* tr = P.truth + qi * static_cast<int64_t>(P.truth_stride);
+      const int cap = min(sm.f.len[gl], tleft);
+      int32_t trv[S];
+#pragma unroll
+      for (int i = 0; i < S; ++i) trv[i] = i < cap ? tr[i] : 0;  // independent loads
+      bool run = true;
+#pragma unroll
+      for (int i = 0; i < S; ++i) {
+        run = run && i < cap && sm.f.tok[gl][i] == trv[i];
+        match += run ? 1 : 0;
+      }
     }
-    drafted = cg::reduce(tile, drafted, cg::plus<int>());
-    match = cg::reduce(tile, match, cg::greater<int>());
-    if (gl == 0) {
-      const int emitted = min(match + 1, P.limit[q]);
+    drafted = tile.sum(drafted);
+    match = tile.max(match);
+    if (valid && gl == 0) {
+      const int emitted = min(match + 1, lim);
       P.v_drafted[q] = drafted;
       P.v_accepted[q] = emitted - 1;
       P.v_emitted[q] = emitted;
@@ -598,8 +750,8 @@ __global__ void __launch_bounds__(kBlock, 4) k_query(QueryLaunch P) {
   }
 
   if (P.stats) {
-    const int ctoks = cg::reduce(tile, gl < nf ? sm.f.len[gl] : 0, cg::plus<int>());
-    if (gl == 0) {
+    const int ctoks = tile.sum(gl < nf ? sm.f.len[gl] : 0);
+    if (valid && gl == 0) {
       const uint64_t B = 4ull * plen + 32ull + 32ull * st_lookups + 32ull * st_exp + 32ull * st_csec +
                          4ull * ctoks + 16ull * nf;
       unsigned long long* s = reinterpret_cast<unsigned long long*>(P.stats);
