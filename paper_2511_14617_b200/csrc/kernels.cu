@@ -459,10 +459,12 @@ __global__ void __launch_bounds__(kBlock, 4) k_query(QueryLaunch P) {
     uint32_t cnt = 0, fc = 0;
     const bool ok = act && gl == 0 && check_suffix(0, looks, cnt, fc);
     st_lookups = tile.shfl(looks, 0);
-    if (tile.shfl(static_cast<int>(ok), 0)) {
+    const bool ok0 = tile.shfl(static_cast<int>(ok), 0) != 0;
+    const uint32_t c0 = tile.shfl(cnt, 0), f0 = tile.shfl(fc, 0);
+    if (ok0) {
       winner = 0;
-      locus_cnt = tile.shfl(cnt, 0);
-      locus_fc = tile.shfl(fc, 0);
+      locus_cnt = c0;
+      locus_fc = f0;
     }
   }
   // (2) only when the longest suffix is absent: the shorter ones, in order
@@ -509,21 +511,19 @@ __global__ void __launch_bounds__(kBlock, 4) k_query(QueryLaunch P) {
       uint32_t cnt = 0, fc = 0;
       const bool ok = !done && j < nlen && check_suffix(j, looks, cnt, fc);
       const unsigned m = tile.ballot(ok);
+      const int w = m ? __ffs(m) - 1 : G - 1;
+      // collectives at one call site for every lane (tiles that are done add 0)
+      const int add = tile.sum((!done && gl <= w) ? looks : 0);
+      const uint32_t wc = tile.shfl(cnt, w);
+      const uint32_t wf = tile.shfl(fc, w);
       if (!done) {
+        st_lookups += add;
         if (m) {
-          const int w = __ffs(m) - 1;
-          st_lookups += tile.sum(gl <= w ? looks : 0);
           winner = 1 + u * G + w;
-          locus_cnt = tile.shfl(cnt, w);
-          locus_fc = tile.shfl(fc, w);
+          locus_cnt = wc;
+          locus_fc = wf;
           done = true;
-        } else {
-          st_lookups += tile.sum(looks);
         }
-      } else {
-        (void)tile.sum(0);
-        (void)tile.shfl(cnt, 0);
-        (void)tile.shfl(fc, 0);
       }
     }
   }
@@ -677,7 +677,8 @@ __global__ void __launch_bounds__(kBlock, 4) k_query(QueryLaunch P) {
 #pragma unroll
     for (int i = 0; i < S; ++i) nt[i] = tile.shfl(tok[i], p_src);
     int lex = 0;
-    for (int o = 0; o < tile.max(live ? np : 0); ++o) {
+    const int npmax = __reduce_max_sync(kFull, live ? np : 0);  // warp-uniform bound
+    for (int o = 0; o < npmax; ++o) {
       const int ol = tile.shfl(p_lex, o);
       const int32_t ot = tile.shfl(p_tok, o);
       lex += (o < np && (ol < p_lex || (ol == p_lex && ot < p_tok))) ? 1 : 0;
@@ -691,7 +692,7 @@ __global__ void __launch_bounds__(kBlock, 4) k_query(QueryLaunch P) {
       b_sup = p_sup;
       b_lex = lex;
       nb = np;
-      dl = d + 1;
+      if (np > 0) dl = d + 1;
     }
   }
   // leftover beam paths (dl tokens each) are finals when non-empty (cst.cpp:222-223)
