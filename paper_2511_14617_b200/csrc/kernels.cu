@@ -382,6 +382,8 @@ __global__ void __launch_bounds__(kBlock, 4) k_query(QueryLaunch P) {
   auto b0 = [&](int j) { return j * start - j * (j - 1) / 2; };  // first window of suffix j
 
   int st_lookups = 0, st_exp = 0, st_csec = 0;
+  long long tA = P.dbg ? clock64() : 0;  // phase timing (debug only)
+  int it_child = 0, it_merge = 0, it_depth = 0;
   int winner = -1;
   uint32_t locus_cnt = 0, locus_fc = 0;
   const uint64_t nbk = T.cap / kBucket;
@@ -529,6 +531,7 @@ __global__ void __launch_bounds__(kBlock, 4) k_query(QueryLaunch P) {
   }
   __syncwarp();  // phase-A scratch is dead from here (reused for finals)
 
+  long long tB = P.dbg ? clock64() : 0;
   // ---------------- phase B ----------------
   int nf = 0;  // finals kept (tile-uniform)
   int32_t tok[S];
@@ -600,7 +603,9 @@ __global__ void __launch_bounds__(kBlock, 4) k_query(QueryLaunch P) {
     uint32_t c = (live && gl < nb) ? b_fc : 0u;
     bool grew = false;
     int nchild = 0;
+    ++it_depth;
     while (__any_sync(kFull, c != 0u)) {
+      ++it_child;
       SlotView r{};
       const bool have = c != 0u;
       if (have) r = load_slot_nc(T.slots + (c - 1));
@@ -619,6 +624,7 @@ __global__ void __launch_bounds__(kBlock, 4) k_query(QueryLaunch P) {
       }
       unsigned m = tile.ballot(qual);
       while (__any_sync(kFull, m != 0u)) {  // merge one candidate per tile into its sorted pool
+        ++it_merge;
         const bool has = m != 0u;
         const int b = has ? __ffs(m) - 1 : 0;
         if (has) m &= m - 1;
@@ -701,6 +707,7 @@ __global__ void __launch_bounds__(kBlock, 4) k_query(QueryLaunch P) {
     for (int b = 0; b < rounds; ++b) finals_offer(dl > 0 && b < nb, b);
   }
 
+  long long tC = P.dbg ? clock64() : 0;
   // ---- output in candidate_before order ----
   __syncwarp();
   int my_rank = 0;
@@ -750,6 +757,17 @@ __global__ void __launch_bounds__(kBlock, 4) k_query(QueryLaunch P) {
     }
   }
 
+  if (P.dbg && valid && gl == 0) {
+    long long* o = P.dbg + q * 8;
+    o[0] = tB - tA;
+    o[1] = tC - tB;
+    o[2] = clock64() - tC;
+    o[3] = it_depth;
+    o[4] = it_child;
+    o[5] = it_merge;
+    o[6] = winner;
+    o[7] = nf;
+  }
   if (P.stats) {
     const int ctoks = tile.sum(gl < nf ? sm.f.len[gl] : 0);
     if (valid && gl == 0) {

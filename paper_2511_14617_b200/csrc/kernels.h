@@ -59,6 +59,7 @@ struct QueryLaunch {
   int32_t* v_emitted;
   dgds_query_stats* stats;
   int32_t* err_flag;  // set to 1 by any query with invalid args (device API)
+  long long* dbg;     // optional per-query phase timing [n][8] (debug)
 };
 
 // max_k selects the tile width (4, 8 or 32 lanes per request); max_s bounds

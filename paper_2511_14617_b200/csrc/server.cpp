@@ -143,6 +143,7 @@ struct dgds_server {
   int32_t* d_err = nullptr;
   std::mutex mu;  // calls on one handle are serialized
 
+  long long* d_dbg = nullptr;  // optional per-query phase timing buffer (debug)
   // kernel timing: event pairs around launches (kind 0 append, 1 query)
   bool profiling = false;
   std::vector<cudaEvent_t> ev_pool;
@@ -909,6 +910,7 @@ int dgds_speculate_device(dgds_server* s, int64_t n, const int32_t* d_handles, c
   }
   L.stats = d_stats;
   L.err_flag = s->d_err;
+  L.dbg = s->d_dbg;
   {
     LaunchTimer lt(s, 1, join.stream());
     DGDS_CUDA(dgds::launch_query(L, max_top_k, max_spec, join.stream()));
@@ -963,6 +965,13 @@ int32_t dgds_draft_len(int32_t sd_enabled, int32_t adaptive, int32_t cap, int32_
   if (n_running < 1) n_running = 1;
   const int32_t d = adaptive ? std::min(cap, budget / n_running) : cap;
   return std::max(d, 0);
+}
+
+// Debug: record per-query phase cycles of device-API query launches into d_buf[n][8].
+extern "C" int dgds_debug_query_timing(dgds_server* s, void* d_buf) {
+  std::lock_guard<std::mutex> lk(s->mu);
+  s->d_dbg = static_cast<long long*>(d_buf);
+  return DGDS_OK;
 }
 
 int dgds_profile_enable(dgds_server* s, int32_t on) {
