@@ -199,7 +199,12 @@ __global__ void __launch_bounds__(kBlock, 4) k_append(DevTrie T, const AppendSeg
     if (lane < D && static_cast<uint64_t>(lane) < len) act_row[lane] = a;
   }
   for (int o = 16; o > 0; o >>= 1) inserted_total += __shfl_xor_sync(kFull, inserted_total, o);
-  if (lane == 0 && inserted_total) atomicAdd(T.used, inserted_total);
+  __shared__ unsigned long long blk_ins;
+  if (threadIdx.x == 0) blk_ins = 0ull;
+  __syncthreads();
+  if (lane == 0 && inserted_total) atomicAdd(&blk_ins, inserted_total);
+  __syncthreads();
+  if (threadIdx.x == 0 && blk_ins) atomicAdd(T.used, blk_ins);  // one global atomic per block
 }
 
 // ---------------------------------------------------------------------------
@@ -769,20 +774,27 @@ __global__ void __launch_bounds__(kBlock, 4) k_query(QueryLaunch P) {
     o[7] = nf;
   }
   if (P.stats) {
+    // per-block reduction, then one atomic per counter per block (same-address
+    // atomics from every request would serialise in one L2 slice)
+    __shared__ unsigned long long blk[8];
+    if (threadIdx.x < 8) blk[threadIdx.x] = 0ull;
+    __syncthreads();
     const int ctoks = tile.sum(gl < nf ? sm.f.len[gl] : 0);
     if (valid && gl == 0) {
       const uint64_t B = 4ull * plen + 32ull + 32ull * st_lookups + 32ull * st_exp + 32ull * st_csec +
                          4ull * ctoks + 16ull * nf;
-      unsigned long long* s = reinterpret_cast<unsigned long long*>(P.stats);
-      atomicAdd(s + 0, 1ull);
-      atomicAdd(s + 1, static_cast<unsigned long long>(plen));
-      atomicAdd(s + 2, static_cast<unsigned long long>(st_lookups));
-      atomicAdd(s + 3, static_cast<unsigned long long>(st_exp));
-      atomicAdd(s + 4, static_cast<unsigned long long>(st_csec));
-      atomicAdd(s + 5, static_cast<unsigned long long>(nf));
-      atomicAdd(s + 6, static_cast<unsigned long long>(ctoks));
-      atomicAdd(s + 7, static_cast<unsigned long long>(B));
+      atomicAdd(&blk[0], 1ull);
+      atomicAdd(&blk[1], static_cast<unsigned long long>(plen));
+      atomicAdd(&blk[2], static_cast<unsigned long long>(st_lookups));
+      atomicAdd(&blk[3], static_cast<unsigned long long>(st_exp));
+      atomicAdd(&blk[4], static_cast<unsigned long long>(st_csec));
+      atomicAdd(&blk[5], static_cast<unsigned long long>(nf));
+      atomicAdd(&blk[6], static_cast<unsigned long long>(ctoks));
+      atomicAdd(&blk[7], static_cast<unsigned long long>(B));
     }
+    __syncthreads();
+    if (threadIdx.x < 8 && blk[threadIdx.x])
+      atomicAdd(reinterpret_cast<unsigned long long*>(P.stats) + threadIdx.x, blk[threadIdx.x]);
   }
 }
 
