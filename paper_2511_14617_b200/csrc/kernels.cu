@@ -39,10 +39,10 @@ __device__ __forceinline__ int lane_id() { return threadIdx.x & (kWarp - 1); }
 // token (group root for lane 0), t}, then count it — insert_token's loop
 // (cst.cpp:105-116) with the depth levels in parallel.
 //
-// Pass 1 only computes every window's content hash for the whole segment and
-// prefetches its home slot into L2; pass 2 runs the inherently sequential
-// claim chain (a token's parents are the previous token's nodes), whose CASes
-// then hit L2 instead of DRAM.
+// The claim chain is inherently sequential (a token's parents are the previous
+// token's nodes), but its ADDRESSES are not: home buckets depend on window
+// content only, so a look-ahead hash prefetches them into L2 a few tokens
+// ahead and the chain's line reads / CASes hit L2 instead of DRAM.
 
 // 16-byte key of a slot through L2 (coherent with the CASes of other warps).
 __device__ __forceinline__ void load_key_cg(const Slot* p, unsigned long long& k0, unsigned long long& k1) {
@@ -113,6 +113,9 @@ __global__ void __launch_bounds__(kBlock, 4) k_append(DevTrie T, const AppendSeg
   const int64_t nwarps = static_cast<int64_t>(gridDim.x) * blockDim.x / kWarp;
   const int D = T.depth_cap;
   unsigned long long inserted_total = 0;
+  constexpr int kStage = 128, kAhead = 4;
+  __shared__ int32_t stage[kWarpsPerBlock][kStage];
+  int32_t* stage_w = stage[threadIdx.x / kWarp];
 
   for (int64_t sg = warp; sg < nseg; sg += nwarps) {
     const AppendSeg g = segs[sg];
@@ -133,67 +136,75 @@ __global__ void __launch_bounds__(kBlock, 4) k_append(DevTrie T, const AppendSeg
       }
     }
 
-    // pass 1: hash every window of the segment and prefetch its home slot
-    {
-      unsigned long long h = h_init;
-      uint64_t len = len0;
-      for (uint32_t p = 0; p < g.npieces; ++p) {
-        const AppendPiece pc = pieces[g.piece0 + p];
-        for (uint32_t base = 0; base < pc.n; base += kWarp) {
-          const int32_t tchunk = (base + lane < pc.n) ? tokens[pc.tok_off + base + lane] : 0;
-          const uint32_t cnt = min(static_cast<uint32_t>(kWarp), pc.n - base);
-          for (uint32_t j = 0; j < cnt; ++j) {
-            const int32_t t = __shfl_sync(kFull, tchunk, j);
-            const unsigned long long up = __shfl_up_sync(kFull, h, 1);
-            h = hash_step(lane == 0 ? hr : up, t);
-            if (static_cast<uint64_t>(lane) < min(static_cast<uint64_t>(D), len + 1))
-              prefetch_l2_line(T.slots + home_bucket(key_hash(h), T.cap / kBucket) * kBucket);
-            ++len;
-          }
-        }
-      }
-    }
-
-    // pass 2: the dependent claim chain
+    // The segment's tokens are staged through shared memory kStage at a time.
+    // A second rolling hash runs kAhead tokens in front of the claim chain and
+    // prefetches those windows' home buckets into L2, so each claim's line read
+    // and CAS hit L2 while only ~4 tokens x 24 windows x 128 B per warp are in
+    // flight (the whole-segment footprint would not fit in L2).
     uint64_t len = len0;
-    unsigned long long h = h_init;
+    unsigned long long h = h_init, hp = h_init;
+    uint64_t lenp = len0;
     uint32_t a = (lane < D && static_cast<uint64_t>(lane) < len0) ? act_row[lane] : 0u;
     uint32_t link_slot = 0, link_prev = 0;
     bool link_pending = false;
-    for (uint32_t p = 0; p < g.npieces; ++p) {
-      const AppendPiece pc = pieces[g.piece0 + p];
-      for (uint32_t base = 0; base < pc.n; base += kWarp) {
-        const int32_t tchunk = (base + lane < pc.n) ? tokens[pc.tok_off + base + lane] : 0;
-        const uint32_t cnt = min(static_cast<uint32_t>(kWarp), pc.n - base);
-        for (uint32_t j = 0; j < cnt; ++j) {
-          const int32_t t = __shfl_sync(kFull, tchunk, j);
-          const int newsize = static_cast<int>(min(static_cast<uint64_t>(D), len + 1));
-          const unsigned long long hup = __shfl_up_sync(kFull, h, 1);
-          h = hash_step(lane == 0 ? hr : hup, t);
-          uint32_t parent = __shfl_up_sync(kFull, a, 1);
-          if (lane == 0) parent = g.root;
-          if (lane < newsize) {
-            uint32_t id;
-            bool ins;
-            claim(T, key_hash(h), parent, t, g.root, id, ins);
-            if (link_pending) {
-              T.slots[link_slot].next_sibling = link_prev;
-              link_pending = false;
-            }
-            if (ins) {
-              ++inserted_total;
-              if (!is_root_id(parent, T.cap)) {  // root child lists are never enumerated
-                link_prev = atomicExch(&T.slots[parent - 1].first_child, id);
-                link_slot = id - 1;
-                link_pending = true;
-              }
-            }
-            a = id;
-          }
-          if (lane == static_cast<int>(len & 31)) tail_row[lane] = t;  // ring of the last 32 tokens
-          ++len;
+    uint32_t p = 0, poff = 0;
+    while (p < g.npieces) {
+      int filled = 0;  // stage the next <= kStage tokens (coalesced)
+      while (filled < kStage && p < g.npieces) {
+        const AppendPiece pc = pieces[g.piece0 + p];
+        const uint32_t take = min(static_cast<uint32_t>(kStage - filled), pc.n - poff);
+        for (uint32_t k = lane; k < take; k += kWarp) stage_w[filled + k] = tokens[pc.tok_off + poff + k];
+        filled += static_cast<int>(take);
+        poff += take;
+        if (poff == pc.n) {
+          ++p;
+          poff = 0;
         }
       }
+      __syncwarp();
+      auto advance_ahead = [&](int j) {
+        const int32_t t = stage_w[j];
+        const unsigned long long up = __shfl_up_sync(kFull, hp, 1);
+        hp = hash_step(lane == 0 ? hr : up, t);
+        if (static_cast<uint64_t>(lane) < min(static_cast<uint64_t>(D), lenp + 1))
+          prefetch_l2_line(T.slots + home_bucket(key_hash(hp), T.cap / kBucket) * kBucket);
+        ++lenp;
+      };
+      const int ahead = min(kAhead, filled);
+      for (int j = 0; j < ahead; ++j) advance_ahead(j);
+      for (int j = 0; j < filled; ++j) {
+        if (j + kAhead < filled) advance_ahead(j + kAhead);
+        const int32_t t = stage_w[j];
+        const int newsize = static_cast<int>(min(static_cast<uint64_t>(D), len + 1));
+        const unsigned long long hup = __shfl_up_sync(kFull, h, 1);
+        h = hash_step(lane == 0 ? hr : hup, t);
+        uint32_t parent = __shfl_up_sync(kFull, a, 1);
+        if (lane == 0) parent = g.root;
+        if (lane < newsize) {
+          uint32_t id;
+          bool ins;
+          claim(T, key_hash(h), parent, t, g.root, id, ins);
+          if (link_pending) {
+            T.slots[link_slot].next_sibling = link_prev;
+            link_pending = false;
+          }
+          if (ins) {
+            ++inserted_total;
+            if (!is_root_id(parent, T.cap)) {  // root child lists are never enumerated
+              link_prev = atomicExch(&T.slots[parent - 1].first_child, id);
+              link_slot = id - 1;
+              link_pending = true;
+            }
+          }
+          a = id;
+        }
+        if (lane == static_cast<int>(len & 31)) tail_row[lane] = t;  // ring of the last 32 tokens
+        ++len;
+      }
+      // the look-ahead hash restarts from the claim chain at the next stage
+      hp = h;
+      lenp = len;
+      __syncwarp();
     }
     if (link_pending) T.slots[link_slot].next_sibling = link_prev;
     if (lane < D && static_cast<uint64_t>(lane) < len) act_row[lane] = a;
@@ -394,12 +405,31 @@ __global__ void __launch_bounds__(kBlock, 4) k_query(QueryLaunch P) {
   const uint64_t nbk = T.cap / kBucket;
 
   // ---------------- phase A ----------------
-  // (1) the longest suffix: windows i = gl+1 and gl+1+G, both probes in flight
+  // (1) the longest suffix: windows i = gl+1 and gl+1+G, both probes in flight.
+  // Its windows are prefixes of row[0..start): hash them once with static indexing.
+  unsigned long long hpre[9];
+  hpre[0] = h0;
+#pragma unroll
+  for (int i = 1; i <= 8; ++i) hpre[i] = hash_step(hpre[i - 1], pr[i - 1]);
   {
     const int i1 = gl + 1, i2 = gl + 1 + G;
     const bool d1 = act && fast && i1 <= start;
     const bool d2 = act && fast && G < 8 && i2 <= start;
-    const unsigned long long h1 = hash_prefix(0, i1), h2 = hash_prefix(0, i2);
+    unsigned long long h1 = 0, h2 = 0;
+    int32_t t1 = 0, t2 = 0;
+#pragma unroll
+    for (int i = 1; i <= 8; ++i) {
+      if (i == i1) {
+        h1 = hpre[i];
+        t1 = pr[i - 1];
+      }
+      if (i == i2) {
+        h2 = hpre[i];
+        t2 = pr[i - 1];
+      }
+    }
+    h1 = key_hash(h1);
+    h2 = key_hash(h2);
     const uint64_t bk1 = home_bucket(h1, nbk), bk2 = home_bucket(h2, nbk);
     unsigned long long x[kBucket], y[kBucket];
 #pragma unroll
@@ -409,7 +439,7 @@ __global__ void __launch_bounds__(kBlock, 4) k_query(QueryLaunch P) {
     }
     if (d1) {
       SlotView r;
-      const uint32_t id = resolve_content(T, h1, tok_at(i1 - 1), bk1, x, r);
+      const uint32_t id = resolve_content(T, h1, t1, bk1, x, r);
       sm.a.wid[i1 - 1] = id;
       sm.a.wpar[i1 - 1] = id ? r.parent : 0u;
       if (i1 == start) {
@@ -419,7 +449,7 @@ __global__ void __launch_bounds__(kBlock, 4) k_query(QueryLaunch P) {
     }
     if (d2) {
       SlotView r;
-      const uint32_t id = resolve_content(T, h2, tok_at(i2 - 1), bk2, y, r);
+      const uint32_t id = resolve_content(T, h2, t2, bk2, y, r);
       sm.a.wid[i2 - 1] = id;
       sm.a.wpar[i2 - 1] = id ? r.parent : 0u;
       if (i2 == start) {
@@ -464,7 +494,30 @@ __global__ void __launch_bounds__(kBlock, 4) k_query(QueryLaunch P) {
   {
     int looks = 0;
     uint32_t cnt = 0, fc = 0;
-    const bool ok = act && gl == 0 && check_suffix(0, looks, cnt, fc);
+    bool ok = false;
+    if (act && gl == 0) {
+      // fast check of the longest suffix from the probe records
+      bool dead = false, slow = false;
+      uint32_t prev = root;
+#pragma unroll
+      for (int i = 1; i <= 8; ++i) {
+        if (fast && i <= start && !dead && !slow) {
+          ++looks;
+          const uint32_t id = sm.a.wid[i - 1];
+          if (id == 0u) dead = true;
+          else if (sm.a.wpar[i - 1] != prev) slow = true;  // hash collision: exact walk below
+          else prev = id;
+        }
+      }
+      if (fast && !slow) {
+        ok = !dead;
+        cnt = sm.a.scnt[0];
+        fc = sm.a.sfc[0];
+      } else {
+        looks = 0;
+        ok = check_suffix(0, looks, cnt, fc);
+      }
+    }
     st_lookups = tile.shfl(looks, 0);
     const bool ok0 = tile.shfl(static_cast<int>(ok), 0) != 0;
     const uint32_t c0 = tile.shfl(cnt, 0), f0 = tile.shfl(fc, 0);
