@@ -88,10 +88,11 @@ __device__ __forceinline__ unsigned long long pack_pt(uint32_t parent, int32_t t
          (static_cast<unsigned long long>(static_cast<uint32_t>(token)) << 32);
 }
 
-// Slots are grouped in BUCKETS of 4 (one 128-B line). Probing is linear at
-// bucket granularity: a lookup reads a whole line per step, so a window is
-// usually resolved with one line read whatever its position inside the bucket.
-constexpr int kBucket = 4;
+// Slots are grouped in BUCKETS of 2 (64 B = one DRAM access at the L2's 64-B
+// fetch granularity). Probing is linear at bucket granularity: a lookup reads a
+// whole bucket per step; at load 0.42 that is 1.12 bucket reads per access
+// (4-slot 128-B buckets: 1.03 reads but two DRAM accesses each).
+constexpr int kBucket = 2;
 
 // Home bucket: Lemire fast-range over a remixed hash (uniform for any size).
 __device__ __forceinline__ uint64_t home_bucket(unsigned long long h, uint64_t nbuckets) {
@@ -117,8 +118,8 @@ __device__ __forceinline__ void load_key_nc(const Slot* p, unsigned long long& k
   asm("ld.global.nc.v2.u64 {%0,%1}, [%2];" : "=l"(k0), "=l"(k1) : "l"(p));
 }
 
-__device__ __forceinline__ void prefetch_l2_line(const void* p) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], 128;" ::"l"(p) : "memory");
+__device__ __forceinline__ void prefetch_l2_line(const void* p) {  // one bucket
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], 64;" ::"l"(p) : "memory");
 }
 __device__ __forceinline__ void prefetch_l1(const void* p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
 
