@@ -63,12 +63,18 @@ __device__ __forceinline__ void cas128(Slot* s, unsigned long long h, unsigned l
       : "memory");
 }
 
+// {next_sibling, root} of a new node in one 64-bit store
+__device__ __forceinline__ void store_link(Slot* s, uint32_t next_sibling, uint32_t root) {
+  *reinterpret_cast<unsigned long long*>(&s->next_sibling) =
+      static_cast<unsigned long long>(next_sibling) | (static_cast<unsigned long long>(root) << 32);
+}
+
 // Claim-or-find of window {h, parent, token} (ensure_child, cst.cpp:90-103):
 // read the bucket's 4 keys in one line read; a match only bumps the count,
 // otherwise ONE CAS claims the first empty slot (a single CAS site keeps the
 // lanes of the warp convergent). A lost race re-reads the same bucket.
 __device__ __forceinline__ void claim(const DevTrie& T, unsigned long long h, uint32_t parent, int32_t token,
-                                      uint32_t root, uint32_t& id, bool& inserted) {
+                                      uint32_t& id, bool& inserted) {
   const unsigned long long pt = pack_pt(parent, token);
   const uint64_t nb = T.cap / kBucket;
   uint64_t b = home_bucket(h, nb);
@@ -95,8 +101,7 @@ __device__ __forceinline__ void claim(const DevTrie& T, unsigned long long h, ui
       else continue;  // lost the slot to another key: re-read this bucket
     }
     if (found >= 0) {
-      atomicAdd(&base[found].count, 1u);  // RED: result unused
-      if (ins) base[found].root = root;
+      if (!ins) atomicAdd(&base[found].count, 1u);  // RED; an insert's occurrence is implicit
       inserted = ins;
       id = static_cast<uint32_t>(b * kBucket + found + 1);
       return;
@@ -183,9 +188,9 @@ __global__ void __launch_bounds__(kBlock, 4) k_append(DevTrie T, const AppendSeg
         if (lane < newsize) {
           uint32_t id;
           bool ins;
-          claim(T, key_hash(h), parent, t, g.root, id, ins);
-          if (link_pending) {
-            T.slots[link_slot].next_sibling = link_prev;
+          claim(T, key_hash(h), parent, t, id, ins);
+          if (link_pending) {  // {next_sibling, root} of the node created at the previous token
+            store_link(T.slots + link_slot, link_prev, g.root);
             link_pending = false;
           }
           if (ins) {
@@ -194,6 +199,8 @@ __global__ void __launch_bounds__(kBlock, 4) k_append(DevTrie T, const AppendSeg
               link_prev = atomicExch(&T.slots[parent - 1].first_child, id);
               link_slot = id - 1;
               link_pending = true;
+            } else {
+              store_link(T.slots + (id - 1), 0u, g.root);
             }
           }
           a = id;
@@ -206,7 +213,7 @@ __global__ void __launch_bounds__(kBlock, 4) k_append(DevTrie T, const AppendSeg
       lenp = len;
       __syncwarp();
     }
-    if (link_pending) T.slots[link_slot].next_sibling = link_prev;
+    if (link_pending) store_link(T.slots + link_slot, link_prev, g.root);
     if (lane < D && static_cast<uint64_t>(lane) < len) act_row[lane] = a;
   }
   for (int o = 16; o > 0; o >>= 1) inserted_total += __shfl_xor_sync(kFull, inserted_total, o);
@@ -443,7 +450,7 @@ __global__ void __launch_bounds__(kBlock, 4) k_query(QueryLaunch P) {
       sm.a.wid[i1 - 1] = id;
       sm.a.wpar[i1 - 1] = id ? r.parent : 0u;
       if (i1 == start) {
-        sm.a.scnt[0] = id ? r.count : 0u;
+        sm.a.scnt[0] = id ? occurrences(r.count) : 0u;
         sm.a.sfc[0] = id ? r.first_child : 0u;
       }
     }
@@ -453,7 +460,7 @@ __global__ void __launch_bounds__(kBlock, 4) k_query(QueryLaunch P) {
       sm.a.wid[i2 - 1] = id;
       sm.a.wpar[i2 - 1] = id ? r.parent : 0u;
       if (i2 == start) {
-        sm.a.scnt[0] = id ? r.count : 0u;
+        sm.a.scnt[0] = id ? occurrences(r.count) : 0u;
         sm.a.sfc[0] = id ? r.first_child : 0u;
       }
     }
@@ -482,7 +489,7 @@ __global__ void __launch_bounds__(kBlock, 4) k_query(QueryLaunch P) {
         SlotView r;
         id = find_exact(T, key_hash(h), prev, tk, r);
         if (id && i == L) {
-          cnt = r.count;
+          cnt = occurrences(r.count);
           fc = r.first_child;
         }
       }
@@ -555,7 +562,7 @@ __global__ void __launch_bounds__(kBlock, 4) k_query(QueryLaunch P) {
           sm.a.wid[w] = id;
           sm.a.wpar[w] = id ? r.parent : 0u;
           if (i == start - j) {
-            sm.a.scnt[j] = id ? r.count : 0u;
+            sm.a.scnt[j] = id ? occurrences(r.count) : 0u;
             sm.a.sfc[j] = id ? r.first_child : 0u;
           }
         }
@@ -669,7 +676,7 @@ __global__ void __launch_bounds__(kBlock, 4) k_query(QueryLaunch P) {
       if (have) r = load_slot_nc(T.slots + (c - 1));
       bool qual = false;
       double sc = 0.0;
-      const long long cnt = static_cast<long long>(r.count);
+      const long long cnt = have ? static_cast<long long>(occurrences(r.count)) : 0ll;
       if (have) {
         ++nchild;
         const double step = __ddiv_rn(static_cast<double>(cnt), static_cast<double>(b_sup));

@@ -8,7 +8,9 @@
 //   h            u64  rolling content hash of (group root, window tokens); 0 = empty
 //   parent       u32  node id of the window without its last token (root id at depth 1)
 //   token        i32  last token of the window
-//   count        u32  occurrences of the window (Node::count, cst.hpp:93)
+//   count        u32  occurrences of the window MINUS ONE (Node::count - 1, cst.hpp:93):
+//                     the inserting occurrence is implicit, so an insert never
+//                     touches the counter and only repeat occurrences add to it
 //   first_child  u32  most recently created child, 0 = none (Node::first_child)
 //   next_sibling u32  prepend-linked sibling list (Node::next_sibling)
 //   root         u32  group root id (lets a rebuild drop dead groups)
@@ -98,6 +100,9 @@ constexpr int kBucket = 2;
 __device__ __forceinline__ uint64_t home_bucket(unsigned long long h, uint64_t nbuckets) {
   return __umul64hi(splitmix64(h), nbuckets);
 }
+
+// occurrences of a node from its stored counter (see Slot::count)
+__device__ __forceinline__ uint32_t occurrences(uint32_t stored) { return stored + 1u; }
 
 __device__ __forceinline__ SlotView load_slot_nc(const Slot* p) {
   unsigned long long a, b, c, d;
