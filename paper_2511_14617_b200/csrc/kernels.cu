@@ -76,16 +76,16 @@ __device__ __forceinline__ void store_link(Slot* s, uint32_t next_sibling, uint3
 __device__ __forceinline__ void claim(const DevTrie& T, unsigned long long h, uint32_t parent, int32_t token,
                                       uint32_t& id, bool& inserted) {
   const unsigned long long pt = pack_pt(parent, token);
-  const uint64_t nb = T.cap / kBucket;
+  const uint64_t cap = T.cap;
+  const uint64_t nb = cap / kBucket;
   uint64_t b = home_bucket(h, nb);
   while (true) {
-    Slot* base = T.slots + b * kBucket;
-    unsigned long long k0[kBucket], k1[kBucket];
+    unsigned long long k0[kWindow], k1[kWindow];
 #pragma unroll
-    for (int s = 0; s < kBucket; ++s) load_key_cg(base + s, k0[s], k1[s]);
+    for (int s = 0; s < kWindow; ++s) load_key_cg(T.slots + window_slot(b, s, cap), k0[s], k1[s]);
     int found = -1, empty = -1;
 #pragma unroll
-    for (int s = kBucket - 1; s >= 0; --s) {  // first match / first empty in probe order
+    for (int s = kWindow - 1; s >= 0; --s) {  // first match / first empty in probe order
       if (k0[s] == h && k1[s] == pt) found = s;
       if (k0[s] == 0ull) {
         empty = s;
@@ -95,18 +95,20 @@ __device__ __forceinline__ void claim(const DevTrie& T, unsigned long long h, ui
     bool ins = false;
     if (found < 0 && empty >= 0) {
       unsigned long long o0, o1;
-      cas128(base + empty, h, pt, o0, o1);
+      cas128(T.slots + window_slot(b, empty, cap), h, pt, o0, o1);
       ins = o0 == 0ull;
       if (ins || (o0 == h && o1 == pt)) found = empty;
-      else continue;  // lost the slot to another key: re-read this bucket
+      else continue;  // lost the slot to another key: re-read this window
     }
     if (found >= 0) {
-      if (!ins) atomicAdd(&base[found].count, 1u);  // RED; an insert's occurrence is implicit
+      const uint64_t i = window_slot(b, found, cap);
+      if (!ins) atomicAdd(&T.slots[i].count, 1u);  // RED; an insert's occurrence is implicit
       inserted = ins;
-      id = static_cast<uint32_t>(b * kBucket + found + 1);
+      id = static_cast<uint32_t>(i + 1);
       return;
     }
-    b = (b + 1 == nb) ? 0 : b + 1;  // bucket full without a match
+    b += kWindow / kBucket;  // window full without a match
+    if (b >= nb) b -= nb;
   }
 }
 
@@ -144,7 +146,7 @@ __global__ void __launch_bounds__(kBlock, 4) k_append(DevTrie T, const AppendSeg
     // The segment's tokens are staged through shared memory kStage at a time.
     // A second rolling hash runs kAhead tokens in front of the claim chain and
     // prefetches those windows' home buckets into L2, so each claim's line read
-    // and CAS hit L2 while only ~4 tokens x 24 windows x 64 B per warp are in
+    // and CAS hit L2 while only ~4 tokens x 24 windows x 128 B per warp are in
     // flight (the whole-segment footprint would not fit in L2).
     uint64_t len = len0;
     unsigned long long h = h_init, hp = h_init;
@@ -172,7 +174,7 @@ __global__ void __launch_bounds__(kBlock, 4) k_append(DevTrie T, const AppendSeg
         const unsigned long long up = __shfl_up_sync(kFull, hp, 1);
         hp = hash_step(lane == 0 ? hr : up, t);
         if (static_cast<uint64_t>(lane) < min(static_cast<uint64_t>(D), lenp + 1))
-          prefetch_l2_line(T.slots + home_bucket(key_hash(hp), T.cap / kBucket) * kBucket);
+          prefetch_l2_window(T.slots + home_bucket(key_hash(hp), T.cap / kBucket) * kBucket);
         ++lenp;
       };
       const int ahead = min(kAhead, filled);
@@ -325,24 +327,26 @@ __device__ __forceinline__ unsigned long long ld_nc_u64(const unsigned long long
   return v;
 }
 
-// Resolve a content probe whose home-bucket hashes (hb[]) are already loaded.
+// Resolve a content probe whose first probe window (hb[]) is already loaded.
 __device__ __forceinline__ uint32_t resolve_content(const DevTrie& T, unsigned long long h, int32_t token, uint64_t b,
-                                                    const unsigned long long (&hb)[kBucket], SlotView& rec) {
-  const uint64_t nb = T.cap / kBucket;
+                                                    const unsigned long long (&hb)[kWindow], SlotView& rec) {
+  const uint64_t cap = T.cap;
+  const uint64_t nb = cap / kBucket;
   bool first = true;
   while (true) {
-    const Slot* base = T.slots + b * kBucket;
 #pragma unroll
-    for (int s = 0; s < kBucket; ++s) {
-      const unsigned long long hs = first ? hb[s] : ld_nc_u64(&base[s].h);
+    for (int s = 0; s < kWindow; ++s) {
+      const uint64_t i = window_slot(b, s, cap);
+      const unsigned long long hs = first ? hb[s] : ld_nc_u64(&T.slots[i].h);
       if (hs == h) {
-        rec = load_slot_nc(base + s);  // same sector as the hash: an L1 hit
-        if (rec.token == token) return static_cast<uint32_t>(b * kBucket + s + 1);
+        rec = load_slot_nc(T.slots + i);  // same sector as the hash: an L1 hit
+        if (rec.token == token) return static_cast<uint32_t>(i + 1);
       }
       if (hs == 0ull) return 0;
     }
     first = false;
-    b = (b + 1 == nb) ? 0 : b + 1;
+    b += kWindow / kBucket;
+    if (b >= nb) b -= nb;
   }
 }
 
@@ -438,11 +442,11 @@ __global__ void __launch_bounds__(kBlock, 4) k_query(QueryLaunch P) {
     h1 = key_hash(h1);
     h2 = key_hash(h2);
     const uint64_t bk1 = home_bucket(h1, nbk), bk2 = home_bucket(h2, nbk);
-    unsigned long long x[kBucket], y[kBucket];
+    unsigned long long x[kWindow], y[kWindow];
 #pragma unroll
-    for (int s = 0; s < kBucket; ++s) {
-      x[s] = d1 ? ld_nc_u64(&T.slots[bk1 * kBucket + s].h) : 0ull;
-      y[s] = d2 ? ld_nc_u64(&T.slots[bk2 * kBucket + s].h) : 0ull;
+    for (int s = 0; s < kWindow; ++s) {
+      x[s] = d1 ? ld_nc_u64(&T.slots[window_slot(bk1, s, T.cap)].h) : 0ull;
+      y[s] = d2 ? ld_nc_u64(&T.slots[window_slot(bk2, s, T.cap)].h) : 0ull;
     }
     if (d1) {
       SlotView r;
@@ -554,10 +558,10 @@ __global__ void __launch_bounds__(kBlock, 4) k_query(QueryLaunch P) {
         SlotView r;
         if (dw) {
           const unsigned long long h = hash_prefix(j, i);
-          unsigned long long hb[kBucket];
+          unsigned long long hb[kWindow];
           const uint64_t bk = home_bucket(h, nbk);
 #pragma unroll
-          for (int s = 0; s < kBucket; ++s) hb[s] = ld_nc_u64(&T.slots[bk * kBucket + s].h);
+          for (int s = 0; s < kWindow; ++s) hb[s] = ld_nc_u64(&T.slots[window_slot(bk, s, T.cap)].h);
           id = resolve_content(T, h, tok_at(j + i - 1), bk, hb, r);
           sm.a.wid[w] = id;
           sm.a.wpar[w] = id ? r.parent : 0u;

@@ -52,7 +52,7 @@ uint64_t fnv1a64(const void* data, size_t n) {  // detail::fnv1a64 (bytes.hpp:89
 constexpr double kMaxLoad = 0.70;     // rebuild threshold
 constexpr double kTargetLoad = 0.45;  // load right after a rebuild
 constexpr uint32_t kRootCap = 1u << 22;
-constexpr uint64_t kMaxCap = 0xFFFFFFFFull - kRootCap - 2;
+constexpr uint64_t kMaxCap = (0xFFFFFFFFull - kRootCap - 2) / 4 * 4;
 
 struct PinnedBuf {
   void* p = nullptr;
@@ -251,9 +251,10 @@ int check_args(const dgds_spec_args& a) {
   return DGDS_OK;
 }
 
-uint64_t cap_for(uint64_t nodes, double load) {
+uint64_t cap_for(uint64_t nodes, double load) {  // slots, a multiple of the probe window
   uint64_t c = static_cast<uint64_t>(std::ceil(static_cast<double>(nodes) / load));
-  return std::max<uint64_t>(c, 1024);
+  c = std::max<uint64_t>(c, 1024);
+  return (c + dgds::kWindow - 1) / dgds::kWindow * dgds::kWindow;
 }
 
 int read_used(dgds_server* s, uint64_t* out) {
@@ -266,7 +267,7 @@ int read_used(dgds_server* s, uint64_t* out) {
 
 // Grow (and garbage-collect dropped groups) by rebuilding into a larger table.
 int rebuild(dgds_server* s, uint64_t new_cap) {
-  if (new_cap > kMaxCap) new_cap = kMaxCap;
+  if (new_cap > kMaxCap) new_cap = kMaxCap / dgds::kWindow * dgds::kWindow;
   dgds::DevTrie to = s->T;
   to.cap = new_cap;
   DGDS_CUDA(cudaMalloc(&to.slots, new_cap * sizeof(dgds::Slot)));
@@ -501,7 +502,7 @@ int dgds_create(const dgds_params* params, dgds_server** out) {
   DGDS_CUDA(cudaStreamCreateWithFlags(&s->st, cudaStreamNonBlocking));
   DGDS_CUDA(cudaEventCreateWithFlags(&s->staging_free, cudaEventDisableTiming));
   const uint64_t nodes = p.expected_nodes ? p.expected_nodes : (1ull << 20);
-  uint64_t cap = std::min(cap_for(nodes, 0.5), kMaxCap);
+  uint64_t cap = std::min(cap_for(nodes, 0.5), kMaxCap);  // both multiples of the probe window
   s->T.cap = cap;
   s->T.depth_cap = s->D;
   s->T.lim_pattern = p.max_pattern_len;

@@ -95,6 +95,16 @@ __device__ __forceinline__ unsigned long long pack_pt(uint32_t parent, int32_t t
 // whole bucket per step; at load 0.42 that is 1.12 bucket reads per access
 // (4-slot 128-B buckets: 1.03 reads but two DRAM accesses each).
 constexpr int kBucket = 2;
+// A probe step reads kWindow consecutive slots (home bucket + the next one) in
+// one round trip, so an overflow into the next bucket costs no extra latency;
+// probing remains plain linear probing over slots.
+constexpr int kWindow = 4;
+
+// slot index k of the probe window that starts at bucket b (wraps at the end)
+__device__ __forceinline__ uint64_t window_slot(uint64_t b, int k, uint64_t cap) {
+  const uint64_t i = b * kBucket + static_cast<uint64_t>(k);
+  return i < cap ? i : i - cap;
+}
 
 // Home bucket: Lemire fast-range over a remixed hash (uniform for any size).
 __device__ __forceinline__ uint64_t home_bucket(unsigned long long h, uint64_t nbuckets) {
@@ -123,8 +133,8 @@ __device__ __forceinline__ void load_key_nc(const Slot* p, unsigned long long& k
   asm("ld.global.nc.v2.u64 {%0,%1}, [%2];" : "=l"(k0), "=l"(k1) : "l"(p));
 }
 
-__device__ __forceinline__ void prefetch_l2_line(const void* p) {  // one bucket
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], 64;" ::"l"(p) : "memory");
+__device__ __forceinline__ void prefetch_l2_window(const void* p) {  // home + next bucket
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], 128;" ::"l"(p) : "memory");
 }
 __device__ __forceinline__ void prefetch_l1(const void* p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
 
@@ -134,24 +144,26 @@ __device__ __forceinline__ void prefetch_l1(const void* p) { asm volatile("prefe
 template <bool kExact>
 __device__ __forceinline__ uint32_t probe(const DevTrie& T, unsigned long long h, uint32_t parent, int32_t token,
                                           SlotView& rec) {
-  const uint64_t nb = T.cap / kBucket;
+  const uint64_t cap = T.cap;
+  const uint64_t nb = cap / kBucket;
   const unsigned long long pt = pack_pt(parent, token);
   uint64_t b = home_bucket(h, nb);
   while (true) {
-    const Slot* base = T.slots + b * kBucket;
-    unsigned long long k0[kBucket], k1[kBucket];
+    unsigned long long k0[kWindow], k1[kWindow];
 #pragma unroll
-    for (int s = 0; s < kBucket; ++s) load_key_nc(base + s, k0[s], k1[s]);
+    for (int s = 0; s < kWindow; ++s) load_key_nc(T.slots + window_slot(b, s, cap), k0[s], k1[s]);
 #pragma unroll
-    for (int s = 0; s < kBucket; ++s) {
+    for (int s = 0; s < kWindow; ++s) {
       const bool hit = k0[s] == h && (kExact ? k1[s] == pt : static_cast<int32_t>(k1[s] >> 32) == token);
       if (hit) {
-        rec = load_slot_nc(base + s);  // same sector as the key: an L1 hit
-        return static_cast<uint32_t>(b * kBucket + s + 1);
+        const uint64_t i = window_slot(b, s, cap);
+        rec = load_slot_nc(T.slots + i);  // same sector as the key: an L1 hit
+        return static_cast<uint32_t>(i + 1);
       }
       if (k0[s] == 0ull) return 0;
     }
-    b = (b + 1 == nb) ? 0 : b + 1;
+    b += kWindow / kBucket;
+    if (b >= nb) b -= nb;
   }
 }
 
