@@ -146,7 +146,7 @@ __global__ void __launch_bounds__(kBlock, 4) k_append(DevTrie T, const AppendSeg
     // The segment's tokens are staged through shared memory kStage at a time.
     // A second rolling hash runs kAhead tokens in front of the claim chain and
     // prefetches those windows' home buckets into L2, so each claim's line read
-    // and CAS hit L2 while only ~4 tokens x 24 windows x 128 B per warp are in
+    // and CAS hit L2 while only ~4 tokens x 24 windows x 64 B per warp are in
     // flight (the whole-segment footprint would not fit in L2).
     uint64_t len = len0;
     unsigned long long h = h_init, hp = h_init;
