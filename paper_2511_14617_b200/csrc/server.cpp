@@ -14,6 +14,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -507,6 +508,8 @@ int dgds_create(const dgds_params* params, dgds_server** out) {
   s->T.depth_cap = s->D;
   s->T.lim_pattern = p.max_pattern_len;
   s->T.lim_spec = p.max_spec_len;
+  s->T.ahead = 0;  // the bulk L2 prefetch measured slower than the register preload alone
+  if (const char* e = std::getenv("DGDS_PREFETCH_AHEAD")) s->T.ahead = std::max(0, std::atoi(e));
   DGDS_CUDA(cudaMalloc(&s->T.slots, cap * sizeof(dgds::Slot)));
   DGDS_CUDA(cudaMemsetAsync(s->T.slots, 0, cap * sizeof(dgds::Slot), s->st));
   DGDS_CUDA(cudaMalloc(&s->d_used, sizeof(unsigned long long)));

@@ -66,7 +66,7 @@ struct DevTrie {
   int32_t depth_cap;         // max_pattern_len + max_spec_len (cst.cpp:106-107)
   int32_t lim_pattern;       // Limits::max_pattern_len
   int32_t lim_spec;          // Limits::max_spec_len
-  int32_t pad_;
+  int32_t ahead;             // append look-ahead (tokens) of the L2 prefetch; 0 = off
 };
 
 __host__ __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
