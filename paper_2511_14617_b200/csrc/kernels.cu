@@ -69,20 +69,20 @@ __device__ __forceinline__ void store_link(Slot* s, uint32_t next_sibling, uint3
       static_cast<unsigned long long>(next_sibling) | (static_cast<unsigned long long>(root) << 32);
 }
 
-// Claim-or-find of window {h, parent, token} (ensure_child, cst.cpp:90-103).
-// The first probe window's keys (k0/k1 from bucket b) may have been read
-// EARLY — keys never change once set, and a stale "empty" just makes the CAS
-// return the occupant — so the caller can overlap that read with the previous
-// token's claim. A key match only bumps the count; otherwise ONE CAS claims
-// the first empty slot (one CAS site keeps the warp convergent); a lost race
-// re-reads the window.
+// Claim-or-find of window {h, parent, token} (ensure_child, cst.cpp:90-103):
+// read the bucket's 4 keys in one line read; a match only bumps the count,
+// otherwise ONE CAS claims the first empty slot (a single CAS site keeps the
+// lanes of the warp convergent). A lost race re-reads the same bucket.
 __device__ __forceinline__ void claim(const DevTrie& T, unsigned long long h, uint32_t parent, int32_t token,
-                                      uint64_t b, unsigned long long (&k0)[kWindow],
-                                      unsigned long long (&k1)[kWindow], uint32_t& id, bool& inserted) {
+                                      uint32_t& id, bool& inserted) {
   const unsigned long long pt = pack_pt(parent, token);
   const uint64_t cap = T.cap;
   const uint64_t nb = cap / kBucket;
+  uint64_t b = home_bucket(h, nb);
   while (true) {
+    unsigned long long k0[kWindow], k1[kWindow];
+#pragma unroll
+    for (int s = 0; s < kWindow; ++s) load_key_cg(T.slots + window_slot(b, s, cap), k0[s], k1[s]);
     int found = -1, empty = -1;
 #pragma unroll
     for (int s = kWindow - 1; s >= 0; --s) {  // first match / first empty in probe order
@@ -97,13 +97,8 @@ __device__ __forceinline__ void claim(const DevTrie& T, unsigned long long h, ui
       unsigned long long o0, o1;
       cas128(T.slots + window_slot(b, empty, cap), h, pt, o0, o1);
       ins = o0 == 0ull;
-      if (ins || (o0 == h && o1 == pt)) {
-        found = empty;
-      } else {  // lost the slot to another key: re-read this window
-#pragma unroll
-        for (int q = 0; q < kWindow; ++q) load_key_cg(T.slots + window_slot(b, q, cap), k0[q], k1[q]);
-        continue;
-      }
+      if (ins || (o0 == h && o1 == pt)) found = empty;
+      else continue;  // lost the slot to another key: re-read this window
     }
     if (found >= 0) {
       const uint64_t i = window_slot(b, found, cap);
@@ -114,8 +109,6 @@ __device__ __forceinline__ void claim(const DevTrie& T, unsigned long long h, ui
     }
     b += kWindow / kBucket;  // window full without a match
     if (b >= nb) b -= nb;
-#pragma unroll
-    for (int q = 0; q < kWindow; ++q) load_key_cg(T.slots + window_slot(b, q, cap), k0[q], k1[q]);
   }
 }
 
@@ -127,8 +120,7 @@ __global__ void __launch_bounds__(kBlock, 4) k_append(DevTrie T, const AppendSeg
   const int64_t nwarps = static_cast<int64_t>(gridDim.x) * blockDim.x / kWarp;
   const int D = T.depth_cap;
   unsigned long long inserted_total = 0;
-  constexpr int kStage = 128;
-  const int kAhead = T.ahead;
+  constexpr int kStage = 128, kAhead = 4;
   __shared__ int32_t stage[kWarpsPerBlock][kStage];
   int32_t* stage_w = stage[threadIdx.x / kWarp];
 
@@ -152,10 +144,10 @@ __global__ void __launch_bounds__(kBlock, 4) k_append(DevTrie T, const AppendSeg
     }
 
     // The segment's tokens are staged through shared memory kStage at a time.
-    // Home buckets depend on window content only, so the keys of token j+1's
-    // windows are read into registers while token j's claims (CAS) are in
-    // flight: the dependent chain pays ~one L2 round trip per token instead of
-    // a DRAM read plus the CAS. (Optional: an L2 prefetch T.ahead tokens ahead.)
+    // Optionally (T.ahead > 0) a second rolling hash runs ahead of the claim
+    // chain and prefetches those windows' home buckets into L2. Measured on
+    // C2 it is slower than none (the kernel is bound by random DRAM accesses,
+    // not by the chain's latency), so the server leaves it off by default.
     uint64_t len = len0;
     unsigned long long h = h_init, hp = h_init;
     uint64_t lenp = len0;
@@ -163,7 +155,6 @@ __global__ void __launch_bounds__(kBlock, 4) k_append(DevTrie T, const AppendSeg
     uint32_t link_slot = 0, link_prev = 0;
     bool link_pending = false;
     uint32_t p = 0, poff = 0;
-    const uint64_t nbk = T.cap / kBucket;
     while (p < g.npieces) {
       int filled = 0;  // stage the next <= kStage tokens (coalesced)
       while (filled < kStage && p < g.npieces) {
@@ -183,43 +174,23 @@ __global__ void __launch_bounds__(kBlock, 4) k_append(DevTrie T, const AppendSeg
         const unsigned long long up = __shfl_up_sync(kFull, hp, 1);
         hp = hash_step(lane == 0 ? hr : up, t);
         if (static_cast<uint64_t>(lane) < min(static_cast<uint64_t>(D), lenp + 1))
-          prefetch_l2_window(T.slots + home_bucket(key_hash(hp), nbk) * kBucket);
+          prefetch_l2_window(T.slots + home_bucket(key_hash(hp), T.cap / kBucket) * kBucket);
         ++lenp;
       };
-      if (kAhead > 0)
-        for (int j = 0; j < min(kAhead, filled); ++j) advance_ahead(j);
-      // preload the first token's home window
-      unsigned long long hn, nk0[kWindow], nk1[kWindow];
-      uint64_t nbkt;
-      auto preload = [&](int j, uint64_t at_len) {  // hash + key read for the token at position at_len
-        const unsigned long long up = __shfl_up_sync(kFull, h, 1);
-        hn = hash_step(lane == 0 ? hr : up, stage_w[j]);
-        nbkt = home_bucket(key_hash(hn), nbk);
-        if (static_cast<uint64_t>(lane) < min(static_cast<uint64_t>(D), at_len + 1)) {
-#pragma unroll
-          for (int q = 0; q < kWindow; ++q) load_key_cg(T.slots + window_slot(nbkt, q, T.cap), nk0[q], nk1[q]);
-        }
-      };
-      preload(0, len);
+      const int ahead = min(kAhead, filled);
+      for (int j = 0; j < ahead; ++j) advance_ahead(j);
       for (int j = 0; j < filled; ++j) {
-        if (kAhead > 0 && j + kAhead < filled) advance_ahead(j + kAhead);
+        if (j + kAhead < filled) advance_ahead(j + kAhead);
         const int32_t t = stage_w[j];
         const int newsize = static_cast<int>(min(static_cast<uint64_t>(D), len + 1));
-        h = hn;
-        const uint64_t bk = nbkt;
-        unsigned long long k0[kWindow], k1[kWindow];
-#pragma unroll
-        for (int q = 0; q < kWindow; ++q) {
-          k0[q] = nk0[q];
-          k1[q] = nk1[q];
-        }
-        if (j + 1 < filled) preload(j + 1, len + 1);  // next token's keys, in flight during this claim
+        const unsigned long long hup = __shfl_up_sync(kFull, h, 1);
+        h = hash_step(lane == 0 ? hr : hup, t);
         uint32_t parent = __shfl_up_sync(kFull, a, 1);
         if (lane == 0) parent = g.root;
         if (lane < newsize) {
           uint32_t id;
           bool ins;
-          claim(T, key_hash(h), parent, t, bk, k0, k1, id, ins);
+          claim(T, key_hash(h), parent, t, id, ins);
           if (link_pending) {  // {next_sibling, root} of the node created at the previous token
             store_link(T.slots + link_slot, link_prev, g.root);
             link_pending = false;
