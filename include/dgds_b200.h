@@ -211,6 +211,10 @@ typedef struct dgds_profile {
   double query_ms;  /* summed device time of the query kernels */
 } dgds_profile;
 int dgds_profile_enable(dgds_server* s, int32_t on);
+/* Debug: record per-query phase cycles of later device-API query launches into d_buf[n][8] (NULL = off). */
+int dgds_debug_query_timing(dgds_server* s, void* d_buf);
+/* Device->host bytes moved by the last host-buffer query call (results are compacted on device). */
+int dgds_last_transfer(dgds_server* s, uint64_t* d2h_bytes);
 /* Synchronises on the recorded events; reset != 0 clears the accumulators. */
 int dgds_profile_read(dgds_server* s, dgds_profile* out, int32_t reset);
 

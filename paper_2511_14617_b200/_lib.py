@@ -143,6 +143,8 @@ EXPORTS = {
     "dgds_speculate_verify_batch": (C.c_int, [_P, _I64, _P, _P, _P, _P, _I64, _P, _I32, _P, _P,
                                               C.POINTER(Candidates), C.POINTER(VerifyOut)]),
     "dgds_profile_enable": (C.c_int, [_P, _I32]),
+    "dgds_last_transfer": (C.c_int, [_P, C.POINTER(_U64)]),
+    "dgds_debug_query_timing": (C.c_int, [_P, _P]),
     "dgds_profile_read": (C.c_int, [_P, C.POINTER(Profile), _I32]),
     "dgds_verify_batch": (C.c_int, [_P, _I64, C.POINTER(Candidates), _P, _I32, _P, _P, C.POINTER(VerifyOut)]),
     "dgds_draft_len": (_I32, [_I32, _I32, _I32, _I32, _I32]),

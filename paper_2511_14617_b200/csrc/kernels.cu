@@ -1106,3 +1106,92 @@ cudaError_t launch_route_unpack(int64_t n, const uint32_t* in, int32_t rec_words
 }
 
 }  // namespace dgds
+
+// ---------------------------------------------------------------------------
+// Compaction of query results for the host path: strided [n][K][S] candidate
+// buffers -> dense per-candidate records + dense tokens, so the device->host
+// copy carries only real candidates.
+#include <cub/block/block_scan.cuh>
+
+namespace dgds {
+namespace {
+
+constexpr int kCmpBlock = 256;
+
+__global__ void k_cmp_count(int64_t n, int32_t K, const int32_t* __restrict__ n_cands,
+                            const int32_t* __restrict__ lens, long long* block_sums) {
+  const int64_t q = static_cast<int64_t>(blockIdx.x) * kCmpBlock + threadIdx.x;
+  int c = 0, t = 0;
+  if (q < n) {
+    c = n_cands[q];
+    for (int j = 0; j < c; ++j) t += lens[q * K + j];
+  }
+  using BS = cub::BlockScan<int, kCmpBlock>;
+  __shared__ typename BS::TempStorage tmp;
+  int cs, ts;
+  BS(tmp).InclusiveSum(c, cs);
+  __syncthreads();
+  BS(tmp).InclusiveSum(t, ts);
+  if (threadIdx.x == kCmpBlock - 1) {
+    block_sums[2 * blockIdx.x] = cs;
+    block_sums[2 * blockIdx.x + 1] = ts;
+  }
+}
+
+__global__ void k_cmp_scan(int64_t nblocks, long long* block_sums, long long* totals) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  long long c = 0, t = 0;
+  for (int64_t b = 0; b < nblocks; ++b) {
+    const long long bc = block_sums[2 * b], bt = block_sums[2 * b + 1];
+    block_sums[2 * b] = c;
+    block_sums[2 * b + 1] = t;
+    c += bc;
+    t += bt;
+  }
+  totals[0] = c;
+  totals[1] = t;
+}
+
+__global__ void k_cmp_scatter(int64_t n, int32_t K, int32_t S, const int32_t* __restrict__ n_cands,
+                              const int32_t* __restrict__ lens, const double* __restrict__ scores,
+                              const int64_t* __restrict__ supports, const int32_t* __restrict__ tokens,
+                              const long long* __restrict__ block_sums, CandMeta* meta, int32_t* tok_out) {
+  const int64_t q = static_cast<int64_t>(blockIdx.x) * kCmpBlock + threadIdx.x;
+  int c = 0, t = 0;
+  if (q < n) {
+    c = n_cands[q];
+    for (int j = 0; j < c; ++j) t += lens[q * K + j];
+  }
+  using BS = cub::BlockScan<int, kCmpBlock>;
+  __shared__ typename BS::TempStorage tmp;
+  int co, to;
+  BS(tmp).ExclusiveSum(c, co);
+  __syncthreads();
+  BS(tmp).ExclusiveSum(t, to);
+  if (q >= n) return;
+  long long cb = block_sums[2 * blockIdx.x] + co, tb = block_sums[2 * blockIdx.x + 1] + to;
+  for (int j = 0; j < c; ++j) {
+    const int64_t si = q * K + j;
+    const int L = lens[si];
+    meta[cb + j] = CandMeta{scores[si], supports[si], L, 0};
+    for (int i = 0; i < L; ++i) tok_out[tb + i] = tokens[si * S + i];
+    tb += L;
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_compact(int64_t n, int32_t K, int32_t S, const int32_t* n_cands, const int32_t* lens,
+                           const double* scores, const int64_t* supports, const int32_t* tokens,
+                           long long* block_sums, long long* totals, CandMeta* meta, int32_t* tok_out,
+                           cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  const int64_t nb = (n + kCmpBlock - 1) / kCmpBlock;
+  k_cmp_count<<<static_cast<unsigned>(nb), kCmpBlock, 0, st>>>(n, K, n_cands, lens, block_sums);
+  k_cmp_scan<<<1, 1, 0, st>>>(nb, block_sums, totals);
+  k_cmp_scatter<<<static_cast<unsigned>(nb), kCmpBlock, 0, st>>>(n, K, S, n_cands, lens, scores, supports, tokens,
+                                                                  block_sums, meta, tok_out);
+  return cudaGetLastError();
+}
+
+}  // namespace dgds

@@ -82,6 +82,19 @@ cudaError_t launch_rebuild(const DevTrie& from, const DevTrie& to, const uint32_
 cudaError_t launch_remap_active(uint32_t* active, const uint32_t* streams, const uint32_t* sizes, int64_t nstreams,
                                 const uint32_t* remap, cudaStream_t st);
 
+// Dense per-candidate record of the host path's compacted results.
+struct CandMeta {
+  double score;
+  int64_t support;
+  int32_t len;
+  int32_t pad;
+};
+// block_sums: 2 * ceil(n / 256) scratch; totals[0] = candidates, totals[1] = tokens.
+cudaError_t launch_compact(int64_t n, int32_t K, int32_t S, const int32_t* n_cands, const int32_t* lens,
+                           const double* scores, const int64_t* supports, const int32_t* tokens,
+                           long long* block_sums, long long* totals, CandMeta* meta, int32_t* tok_out,
+                           cudaStream_t st);
+
 cudaError_t launch_route_pack(int64_t n, int32_t world, const int32_t* owner, const uint32_t* records,
                               int32_t rec_words, uint32_t* out, int64_t* counts, int64_t* perm, void* scratch,
                               cudaStream_t st);

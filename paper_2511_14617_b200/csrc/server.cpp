@@ -18,6 +18,7 @@
 #include <cstring>
 #include <memory>
 #include <mutex>
+#include <thread>
 #include <string>
 #include <unordered_map>
 #include <vector>
@@ -145,6 +146,7 @@ struct dgds_server {
   std::mutex mu;  // calls on one handle are serialized
 
   long long* d_dbg = nullptr;  // optional per-query phase timing buffer (debug)
+  uint64_t last_d2h_bytes = 0;  // device->host bytes of the last host-path query call
   // kernel timing: event pairs around launches (kind 0 append, 1 query)
   bool profiling = false;
   std::vector<cudaEvent_t> ev_pool;
@@ -794,9 +796,13 @@ int dgds_speculate_verify_batch(dgds_server* s, int64_t n, const int32_t* handle
   const size_t o_ln = align_up(o_nc + n * 4, 256);
   const size_t o_tk = align_up(o_ln + n * K * 4, 256);
   const size_t o_v = align_up(o_tk + static_cast<size_t>(n) * K * Sx * 4, 256);
-  const size_t out_total = o_v + (verify ? static_cast<size_t>(n) * 12 : 0);
-  if (int rc = s->h_out.ensure(out_total)) return rc;
-  if (int rc = s->d_out.ensure(out_total)) return rc;
+  // compacted results: [totals | n_cands | verify] then [meta | tokens]
+  const int64_t nblk = (n + 255) / 256;
+  const size_t o_bs = align_up(o_v + (verify ? static_cast<size_t>(n) * 12 : 0), 256);
+  const size_t o_cmeta = align_up(o_bs + static_cast<size_t>(nblk) * 16 + 16, 256);
+  const size_t o_ctok = align_up(o_cmeta + static_cast<size_t>(n) * K * sizeof(dgds::CandMeta), 256);
+  const size_t dev_total = o_ctok + static_cast<size_t>(n) * K * Sx * 4;
+  if (int rc = s->d_out.ensure(dev_total)) return rc;
   char* d = static_cast<char*>(s->d_stage.p);
   char* dout = static_cast<char*>(s->d_out.p);
   DGDS_CUDA(cudaMemcpyAsync(d, h, in_all, cudaMemcpyHostToDevice, s->st));
@@ -833,26 +839,74 @@ int dgds_speculate_verify_batch(dgds_server* s, int64_t n, const int32_t* handle
     LaunchTimer lt(s, 1, s->st);
     DGDS_CUDA(dgds::launch_query(L, max_k, max_s, s->st));
   }
-  DGDS_CUDA(cudaMemcpyAsync(s->h_out.p, dout, out_total, cudaMemcpyDeviceToHost, s->st));
+  long long* d_bs = reinterpret_cast<long long*>(dout + o_bs);
+  long long* d_tot = d_bs + 2 * nblk;
+  auto* d_meta = reinterpret_cast<dgds::CandMeta*>(dout + o_cmeta);
+  int32_t* d_ctok = reinterpret_cast<int32_t*>(dout + o_ctok);
+  DGDS_CUDA(dgds::launch_compact(n, K, Sx, L.n_cands, L.lens, L.scores, L.supports, L.tokens, d_bs, d_tot, d_meta,
+                                 d_ctok, s->st));
+  // host block 1: totals | n_cands | verify ; block 2: meta | tokens
+  const size_t h1 = 16 + static_cast<size_t>(n) * 4 + (verify ? static_cast<size_t>(n) * 12 : 0);
+  const size_t h_meta_max = static_cast<size_t>(n) * K * sizeof(dgds::CandMeta);
+  if (int rc = s->h_out.ensure(align_up(h1, 256) + h_meta_max + static_cast<size_t>(n) * K * Sx * 4)) return rc;
+  char* ho = static_cast<char*>(s->h_out.p);
+  DGDS_CUDA(cudaMemcpyAsync(ho, d_tot, 16, cudaMemcpyDeviceToHost, s->st));
+  DGDS_CUDA(cudaMemcpyAsync(ho + 16, dout + o_nc, n * 4, cudaMemcpyDeviceToHost, s->st));
+  if (verify) DGDS_CUDA(cudaMemcpyAsync(ho + 16 + n * 4, dout + o_v, n * 12, cudaMemcpyDeviceToHost, s->st));
   DGDS_CUDA(cudaStreamSynchronize(s->st));
-  const char* ho = static_cast<const char*>(s->h_out.p);
-  const double* sc = reinterpret_cast<const double*>(ho + o_sc);
-  const int64_t* sp = reinterpret_cast<const int64_t*>(ho + o_sp);
-  const int32_t* nc = reinterpret_cast<const int32_t*>(ho + o_nc);
-  const int32_t* ln = reinterpret_cast<const int32_t*>(ho + o_ln);
-  const int32_t* tk = reinterpret_cast<const int32_t*>(ho + o_tk);
-  for (int64_t q = 0; q < n; ++q) {
-    out->n_cands[q] = nc[q];
-    for (int c = 0; c < nc[q]; ++c) {
-      const int64_t si = q * K + c, di = q * out->k_stride + c;
-      out->lens[di] = ln[si];
-      out->scores[di] = sc[si];
-      out->supports[di] = sp[si];
-      std::memcpy(out->tokens + di * out->s_stride, tk + si * Sx, ln[si] * 4);
+  const long long ncand = reinterpret_cast<const long long*>(ho)[0];
+  const long long ntok = reinterpret_cast<const long long*>(ho)[1];
+  char* hm = ho + align_up(h1, 256);
+  char* ht = hm + ncand * sizeof(dgds::CandMeta);
+  if (ncand > 0) {
+    DGDS_CUDA(cudaMemcpyAsync(hm, d_meta, ncand * sizeof(dgds::CandMeta), cudaMemcpyDeviceToHost, s->st));
+    if (ntok > 0) DGDS_CUDA(cudaMemcpyAsync(ht, d_ctok, ntok * 4, cudaMemcpyDeviceToHost, s->st));
+    DGDS_CUDA(cudaStreamSynchronize(s->st));
+  }
+  s->last_d2h_bytes = 16 + n * 4 + (verify ? n * 12 : 0) + ncand * sizeof(dgds::CandMeta) + ntok * 4;
+  const int32_t* nc = reinterpret_cast<const int32_t*>(ho + 16);
+  const auto* meta = reinterpret_cast<const dgds::CandMeta*>(hm);
+  const int32_t* tk = reinterpret_cast<const int32_t*>(ht);
+  // scatter into the caller's strided buffers, in parallel chunks
+  const int nthreads = n >= 16384 ? 8 : 1;
+  std::vector<int64_t> cstart(nthreads + 1, 0), tstart(nthreads + 1, 0);
+  const int64_t chunk = (n + nthreads - 1) / nthreads;
+  {
+    int64_t c = 0, t = 0, q = 0;
+    for (int w = 0; w < nthreads; ++w) {
+      cstart[w] = c;
+      tstart[w] = t;
+      const int64_t qe = std::min<int64_t>(n, (w + 1) * chunk);
+      for (; q < qe; ++q) {
+        for (int j = 0; j < nc[q]; ++j) t += meta[c + j].len;
+        c += nc[q];
+      }
     }
   }
+  auto work = [&](int w) {
+    int64_t c = cstart[w], t = tstart[w];
+    const int64_t qe = std::min<int64_t>(n, (w + 1) * chunk);
+    for (int64_t q = w * chunk; q < qe; ++q) {
+      out->n_cands[q] = nc[q];
+      for (int j = 0; j < nc[q]; ++j, ++c) {
+        const int64_t di = q * out->k_stride + j;
+        out->lens[di] = meta[c].len;
+        out->scores[di] = meta[c].score;
+        out->supports[di] = meta[c].support;
+        std::memcpy(out->tokens + di * out->s_stride, tk + t, meta[c].len * 4);
+        t += meta[c].len;
+      }
+    }
+  };
+  if (nthreads == 1) {
+    work(0);
+  } else {
+    std::vector<std::thread> th;
+    for (int w = 0; w < nthreads; ++w) th.emplace_back(work, w);
+    for (auto& x : th) x.join();
+  }
   if (verify) {
-    const int32_t* hv = reinterpret_cast<const int32_t*>(ho + o_v);
+    const int32_t* hv = reinterpret_cast<const int32_t*>(ho + 16 + n * 4);
     std::memcpy(vout->drafted, hv, n * 4);
     std::memcpy(vout->accepted, hv + n, n * 4);
     std::memcpy(vout->emitted, hv + 2 * n, n * 4);
@@ -972,9 +1026,14 @@ int32_t dgds_draft_len(int32_t sd_enabled, int32_t adaptive, int32_t cap, int32_
 }
 
 // Debug: record per-query phase cycles of device-API query launches into d_buf[n][8].
-extern "C" int dgds_debug_query_timing(dgds_server* s, void* d_buf) {
+int dgds_debug_query_timing(dgds_server* s, void* d_buf) {
   std::lock_guard<std::mutex> lk(s->mu);
   s->d_dbg = static_cast<long long*>(d_buf);
+  return DGDS_OK;
+}
+
+int dgds_last_transfer(dgds_server* s, uint64_t* d2h_bytes) {
+  *d2h_bytes = s->last_d2h_bytes;
   return DGDS_OK;
 }
 
