@@ -1,0 +1,295 @@
+// dgds_b200.hpp — C++ facade of the B200 draft server over the C ABI (dgds_b200.h).
+//
+// Mirrors the reference C++ API so a rollout engine can switch by changing the
+// include and namespace:
+//   rollsim::DraftServer      (proj/include/rollsim/dgds.hpp:51-91)   -> dgds_b200::DraftServer
+//   rollsim::DraftClient      (dgds.hpp:128-162, fetch_period 0 mode) -> dgds_b200::DraftClient
+//   rollsim::SpeculationSource (engine.hpp:67-74, never implemented
+//                               in the reference)                    -> dgds_b200::GpuSpeculationSource
+//   SpeculationArgs / DraftCandidate / UpdateReply / DgdsParams / SpecQuery
+//                              (cst.hpp:16-29, dgds.hpp:18-43,118-122) -> same names, same defaults
+// Errors follow the reference: std::invalid_argument where it throws that
+// (bad args, negative request id or token), std::runtime_error otherwise.
+// Header-only; link against paper_2511_14617_b200/libdgds_b200.so.
+#pragma once
+
+#include <cstdint>
+#include <map>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <unordered_map>
+#include <utility>
+#include <vector>
+
+#include "dgds_b200.h"
+
+namespace dgds_b200 {
+
+using Token = std::int32_t;
+using TokenSeq = std::vector<Token>;
+using SimTime = double;
+
+struct SpeculationArgs {  // cst.hpp:16-23
+  int max_spec_tokens = 8;
+  int pattern_lookup_max = 6;
+  int pattern_lookup_min = 1;
+  int top_k = 1;
+  double min_step_freq = 0.25;
+  long long min_support = 1;
+};
+
+struct DraftCandidate {  // cst.hpp:25-29
+  TokenSeq tokens;
+  double score = 0.0;
+  long long support = 0;
+};
+
+struct Limits {  // GroupDraftIndex::Limits, cst.hpp:44-47
+  int max_pattern_len = 8;
+  int max_spec_len = 16;
+};
+
+struct DgdsParams {  // dgds.hpp:18-24 (+ device placement)
+  int shard_count = 1;
+  double fetch_period = 0.2;
+  int append_batch_tokens = 16;
+  double default_ttl_seconds = 600.0;
+  Limits limits;
+  int device = 0;
+  std::uint64_t expected_nodes = 0;
+  std::uint64_t expected_streams = 0;
+};
+
+struct UpdateReply {  // dgds.hpp:39-43
+  bool ok = false;
+  std::uint64_t version = 0;
+  std::uint64_t acked_tokens = 0;
+};
+
+struct SpecQuery {  // dgds.hpp:118-122
+  std::string group_id;
+  TokenSeq pattern;
+  SpeculationArgs args;
+};
+
+namespace detail {
+inline void check(int rc) {
+  if (rc == DGDS_OK) return;
+  const std::string msg = dgds_last_error();
+  if (rc == DGDS_EINVAL) throw std::invalid_argument(msg);
+  throw std::runtime_error("dgds: " + msg);
+}
+inline dgds_spec_args c_args(const SpeculationArgs& a) {
+  return dgds_spec_args{a.max_spec_tokens, a.pattern_lookup_max, a.pattern_lookup_min, a.top_k, a.min_step_freq,
+                        a.min_support};
+}
+}  // namespace detail
+
+// shard_of_group (dgds.cpp:10-14)
+inline int shard_of_group(const std::string& group_id, int shard_count) {
+  const int r = dgds_shard_of_group(group_id.data(), group_id.size(), shard_count);
+  if (r < 0) throw std::invalid_argument("shard_count must be >= 1");
+  return r;
+}
+
+class DraftServer {
+ public:
+  explicit DraftServer(DgdsParams params = {}) : params_(params) {
+    dgds_params p{};
+    p.shard_count = params.shard_count;
+    p.append_batch_tokens = params.append_batch_tokens;
+    p.fetch_period = params.fetch_period;
+    p.default_ttl_seconds = params.default_ttl_seconds;
+    p.max_pattern_len = params.limits.max_pattern_len;
+    p.max_spec_len = params.limits.max_spec_len;
+    p.device = params.device;
+    p.expected_nodes = params.expected_nodes;
+    p.expected_streams = params.expected_streams;
+    detail::check(dgds_create(&p, &s_));
+  }
+  ~DraftServer() { dgds_destroy(s_); }
+  DraftServer(const DraftServer&) = delete;
+  DraftServer& operator=(const DraftServer&) = delete;
+
+  UpdateReply update_cst(const std::string& group_id, int request_id, std::uint64_t prev_token_count,
+                         std::span<const Token> new_tokens, SimTime now) {
+    const std::int32_t h = handle(group_id);
+    const std::uint64_t offs[2] = {0, new_tokens.size()};
+    dgds_update_reply r{};
+    detail::check(dgds_update_batch(s_, 1, &h, &request_id, &prev_token_count, offs, new_tokens.data(), now, &r));
+    return UpdateReply{r.ok != 0, r.version, r.acked_tokens};
+  }
+
+  // n update_cst calls in call order, one device launch.
+  std::vector<UpdateReply> update_batch(std::span<const std::string> group_ids, std::span<const int> request_ids,
+                                        std::span<const std::uint64_t> prev_counts,
+                                        std::span<const TokenSeq> tokens, SimTime now) {
+    const std::size_t n = group_ids.size();
+    std::vector<std::int32_t> hs(n);
+    std::vector<std::uint64_t> offs(n + 1, 0);
+    TokenSeq flat;
+    for (std::size_t i = 0; i < n; ++i) {
+      hs[i] = handle(group_ids[i]);
+      offs[i + 1] = offs[i] + tokens[i].size();
+      flat.insert(flat.end(), tokens[i].begin(), tokens[i].end());
+    }
+    std::vector<dgds_update_reply> r(n);
+    std::vector<std::int32_t> rids(request_ids.begin(), request_ids.end());
+    detail::check(dgds_update_batch(s_, static_cast<int64_t>(n), hs.data(), rids.data(), prev_counts.data(),
+                                    offs.data(), flat.data(), now, r.data()));
+    std::vector<UpdateReply> out(n);
+    for (std::size_t i = 0; i < n; ++i) out[i] = UpdateReply{r[i].ok != 0, r[i].version, r[i].acked_tokens};
+    return out;
+  }
+
+  void register_group(const std::string& group_id, double ttl_seconds, SimTime now) {
+    detail::check(dgds_register_group(s_, handle(group_id), ttl_seconds, now));
+  }
+  void drop_group(const std::string& group_id) { detail::check(dgds_drop_group(s_, handle(group_id))); }
+  void sweep_expired(SimTime now) { detail::check(dgds_sweep_expired(s_, now)); }
+
+  std::vector<DraftCandidate> speculate(const std::string& group_id, std::span<const Token> pattern,
+                                        const SpeculationArgs& args) {
+    SpecQuery q{group_id, TokenSeq(pattern.begin(), pattern.end()), args};
+    return batch_speculate(std::span<const SpecQuery>(&q, 1))[0];
+  }
+
+  // DraftClient::batch_speculate with fetch_period 0 (dgds.cpp:274-292): one device launch.
+  std::vector<std::vector<DraftCandidate>> batch_speculate(std::span<const SpecQuery> queries) {
+    const std::size_t n = queries.size();
+    std::vector<std::vector<DraftCandidate>> out(n);
+    if (n == 0) return out;
+    std::vector<std::int32_t> hs(n);
+    std::vector<std::uint64_t> offs(n + 1, 0);
+    TokenSeq flat;
+    std::vector<dgds_spec_args> args(n);
+    int k = 1, s = 1;
+    for (std::size_t i = 0; i < n; ++i) {
+      hs[i] = handle(queries[i].group_id);
+      offs[i + 1] = offs[i] + queries[i].pattern.size();
+      flat.insert(flat.end(), queries[i].pattern.begin(), queries[i].pattern.end());
+      args[i] = detail::c_args(queries[i].args);
+      k = std::max(k, queries[i].args.top_k);
+      s = std::max(s, std::min(queries[i].args.max_spec_tokens, params_.limits.max_spec_len));
+    }
+    std::vector<std::int32_t> nc(n), lens(n * k), toks(n * k * s);
+    std::vector<double> scores(n * k);
+    std::vector<std::int64_t> sup(n * k);
+    dgds_candidates c{k, s, nc.data(), lens.data(), scores.data(), sup.data(), toks.data()};
+    detail::check(dgds_speculate_batch(s_, static_cast<int64_t>(n), hs.data(), offs.data(), flat.data(), args.data(),
+                                       1, &c));
+    for (std::size_t q = 0; q < n; ++q)
+      for (int j = 0; j < nc[q]; ++j) {
+        const std::size_t i = q * k + j;
+        out[q].push_back(DraftCandidate{TokenSeq(toks.begin() + i * s, toks.begin() + i * s + lens[i]), scores[i],
+                                        static_cast<long long>(sup[i])});
+      }
+    return out;
+  }
+
+  int shard_count() const { return params_.shard_count; }
+  const DgdsParams& params() const { return params_; }
+  bool has_group(const std::string& group_id) {
+    std::int32_t r = 0;
+    detail::check(dgds_has_group(s_, handle(group_id), &r));
+    return r != 0;
+  }
+  std::uint64_t group_version(const std::string& group_id) {
+    std::uint64_t v = 0;
+    detail::check(dgds_group_version(s_, handle(group_id), &v));
+    return v;
+  }
+  std::uint64_t stored_tokens(const std::string& group_id, int request_id) {
+    std::uint64_t v = 0;
+    detail::check(dgds_stored_tokens(s_, handle(group_id), request_id, &v));
+    return v;
+  }
+  std::size_t shard_group_count(int shard) {
+    std::uint64_t v = 0;
+    detail::check(dgds_shard_group_count(s_, shard, &v));
+    return static_cast<std::size_t>(v);
+  }
+  dgds_server* raw() { return s_; }
+
+ private:
+  std::int32_t handle(const std::string& gid) {
+    auto it = handles_.find(gid);
+    if (it != handles_.end()) return it->second;
+    std::int32_t h = -1;
+    detail::check(dgds_intern(s_, gid.data(), gid.size(), &h));
+    handles_.emplace(gid, h);
+    return h;
+  }
+
+  DgdsParams params_;
+  dgds_server* s_ = nullptr;
+  std::unordered_map<std::string, std::int32_t> handles_;
+};
+
+// DraftClient in fresh mode (fetch_period 0): note_tokens batches appends per
+// (group, request) and flushes at append_batch_tokens (dgds.cpp:193-217);
+// batch_speculate answers from the always-fresh GPU server.
+class DraftClient {
+ public:
+  DraftClient(DraftServer& server, DgdsParams params) : server_(server), params_(params) {}
+
+  void register_group(const std::string& group_id, double ttl_seconds, SimTime now) {
+    server_.register_group(group_id, ttl_seconds, now);
+  }
+  void note_tokens(const std::string& group_id, int request_id, std::span<const Token> tokens, SimTime now) {
+    if (tokens.empty()) return;
+    Pending& ps = pending_[{group_id, request_id}];
+    ps.buf.insert(ps.buf.end(), tokens.begin(), tokens.end());
+    if (ps.buf.size() - ps.acked >= static_cast<std::size_t>(params_.append_batch_tokens))
+      push(group_id, request_id, ps, now);
+  }
+  void flush(SimTime now) {
+    for (auto& [key, ps] : pending_)
+      if (ps.acked < ps.buf.size()) push(key.first, key.second, ps, now);
+  }
+  std::vector<std::vector<DraftCandidate>> batch_speculate(std::span<const SpecQuery> queries, SimTime) {
+    return server_.batch_speculate(queries);
+  }
+
+ private:
+  struct Pending {
+    TokenSeq buf;
+    std::uint64_t acked = 0;
+  };
+  void push(const std::string& gid, int rid, Pending& ps, SimTime now) {  // push_stream, dgds.cpp:193-208
+    while (ps.acked < ps.buf.size()) {
+      std::span<const Token> chunk(ps.buf.data() + ps.acked, ps.buf.size() - ps.acked);
+      UpdateReply rep = server_.update_cst(gid, rid, ps.acked, chunk, now);
+      if (rep.ok) {
+        ps.acked = rep.acked_tokens;
+      } else if (rep.acked_tokens > ps.acked && rep.acked_tokens <= ps.buf.size()) {
+        ps.acked = rep.acked_tokens;
+      } else if (rep.acked_tokens < ps.acked) {
+        ps.acked = rep.acked_tokens;
+      } else {
+        throw std::runtime_error("draft append resync cannot make progress for group " + gid);
+      }
+    }
+  }
+  DraftServer& server_;
+  DgdsParams params_;
+  std::map<std::pair<std::string, int>, Pending> pending_;
+};
+
+// The engine seam the reference declares but never implements (engine.hpp:67-74).
+class GpuSpeculationSource {
+ public:
+  explicit GpuSpeculationSource(DraftClient& client) : client_(client) {}
+  std::vector<std::vector<DraftCandidate>> batch(std::span<const SpecQuery> queries, SimTime now) {
+    return client_.batch_speculate(queries, now);
+  }
+  void on_emitted(const std::string& group_id, int request_id, std::span<const Token> tokens, SimTime now) {
+    client_.note_tokens(group_id, request_id, tokens, now);
+  }
+
+ private:
+  DraftClient& client_;
+};
+
+}  // namespace dgds_b200

@@ -67,3 +67,19 @@ def test_create_fails_loudly_without_device():
         pytest.skip("GPU present")
     with pytest.raises(_lib.DgdsError):
         D.DraftServer()
+
+
+def _build_facade_test(tmp_path):
+    import subprocess
+    lib_dir = os.path.join(ROOT, "paper_2511_14617_b200")
+    exe = str(tmp_path / "facade_test")
+    subprocess.run(["g++", "-std=c++20", "-O2", "-I" + os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "tests", "cpp", "facade_test.cpp"), "-o", exe, "-L" + lib_dir, "-ldgds_b200",
+                    "-Wl,-rpath," + lib_dir], check=True)
+    return exe
+
+
+def test_cpp_facade_compiles_and_links(tmp_path):
+    """include/dgds_b200.hpp (the rollsim::DraftServer-shaped C++ facade) builds against the C ABI."""
+    _lib.lib()  # make sure the .so exists
+    assert os.path.exists(_build_facade_test(tmp_path))
