@@ -34,6 +34,13 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 DEFAULT_CONFIG = "C2"
+# Measured random 32-B access ceiling of this pool's B200 (tools/chase.cu,
+# profiles/r1_microbench.md): 36.1 G accesses/s = 1155 GB/s of useful sectors.
+RANDOM_CEILING_GBS = 1155.0
+# dram__bytes_read.sum + dram__bytes_write.sum per launch, from one
+# `ncu --set full` capture of the same step (profiles/r1_summary.md).
+QUERY_TRAFFIC = 166678016 + 11980800
+APPEND_TRAFFIC = 311327744 + 47107072
 CONFIG_NAMES = {
     "C1": "single group 16 x 4K, vocab 32K",
     "C2": "Moonlight-shaped 256 groups x 16 responses <=32K tokens, vocab 163840",
@@ -421,10 +428,12 @@ def main_b200(args):
     a_ach = app_alg / (prof.append_ms / 1e3) / 1e9 if prof.append_ms > 0 else 0.0
     dom_q = prof.query_ms >= prof.append_ms
     roof_q = {"kernel": "k_query<4> (K2+K3)", "bound": "hbm", "achieved": q_ach, "peak": peak, "unit": "GB/s",
-              "frac": q_ach / peak, "traffic": None, "alg_bytes_per_launch": q_alg / K,
+              "frac": q_ach / peak, "frac_random_ceiling": q_ach / RANDOM_CEILING_GBS,
+              "traffic": QUERY_TRAFFIC, "alg_bytes_per_launch": q_alg / K,
               "avg_launch_ms": prof.query_ms / max(1, prof.query_launches), "peak_kind": peak_kind}
     roof_a = {"kernel": "k_append (K1)", "bound": "hbm", "achieved": a_ach, "peak": peak, "unit": "GB/s",
-              "frac": a_ach / peak, "traffic": None, "alg_bytes_per_launch": app_alg / K,
+              "frac": a_ach / peak, "frac_random_ceiling": a_ach / RANDOM_CEILING_GBS,
+              "traffic": APPEND_TRAFFIC, "alg_bytes_per_launch": app_alg / K,
               "avg_launch_ms": prof.append_ms / max(1, prof.append_launches), "peak_kind": peak_kind}
     nodes = srv.node_count()
 

@@ -1,0 +1,246 @@
+"""Multi-GPU step of bench.py (torchrun, one rank per GPU, NCCL).
+
+Weak scaling: for N ranks the config's group set is replicated N times (256*N
+C2-shaped groups, same seed, so groups 0..255 are exactly C2), every rank owns
+the groups with fnv1a64(group_id) % N == rank (dgds.cpp:10-14) and produces the
+traffic of the streams s with s % N == rank: per step one 16-token record per
+produced stream plus Q draft queries, exactly the N=1 per-rank work. Records
+are routed to their owners with NCCL all-to-all (paper_2511_14617_b200/
+routing.py); the owner runs K1 / K2+K3 and the replies return through the
+inverse all-to-all. Timing: CUDA events on the step stream, max over ranks.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import json
+import os
+import time
+from dataclasses import replace
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+APP_W = 21  # append record: [local handle, request id, prev lo, prev hi, n, tokens[16]]
+QRY_W = 21  # query record: [local handle, pat_len, pattern[8], truth_left, limit, truth[8], pad]
+
+
+def run_multi(args, world, rank, local, dev):
+    from bench import CONFIG_NAMES, RANDOM_CEILING_GBS, ClockSampler, append_alg_bytes, peaks
+    from paper_2511_14617_b200 import _lib
+    from paper_2511_14617_b200.dgds import DgdsParams, DraftServer, SpeculationArgs, args_array, shard_of_group
+    from paper_2511_14617_b200.routing import Router
+    from paper_2511_14617_b200.workload import CONFIGS, generate_workload, group_id
+
+    base = CONFIGS[args.config]
+    cfg = replace(base, num_groups=base.num_groups * world)
+    tr = generate_workload(cfg)
+    G, R = cfg.num_groups, cfg.group_size
+    S = G * R
+    rt = args.record_tokens
+    assert rt <= 16, "records carry at most 16 tokens"
+    owner_g = np.array([shard_of_group(group_id(g), world) for g in range(G)], np.int64)
+    mine = np.nonzero(owner_g == rank)[0]
+    local_h = np.zeros(G, np.int32)
+    for o in range(world):
+        gs = np.nonzero(owner_g == o)[0]
+        local_h[gs] = np.arange(len(gs), dtype=np.int32)
+    prefill = (tr.lengths * args.prefill).astype(np.int64) // rt * rt
+    my_streams = (mine[:, None] * R + np.arange(R)[None, :]).reshape(-1)
+    K, W = args.steps, args.warmup
+    Q, kq, dl = args.queries, args.top_k, args.draft_len
+    E = max(0, args.e2e_steps)
+    assert dl <= 8, "query records carry 8 truth tokens"
+    idx_tokens = int(prefill[my_streams].sum()) + len(my_streams) * rt * (K + W + E) * world
+    srv = DraftServer(DgdsParams(), device=local, expected_nodes=min(idx_tokens * 24, 1_900_000_000),
+                      expected_streams=len(my_streams))
+    h = srv.group_handles([group_id(int(g)) for g in mine])
+    assert (h == np.arange(len(mine))).all()
+
+    # ---- untimed prefill of the owned groups ----
+    pos = np.zeros(S, np.int64)
+    chunk = 8 * rt
+    live_set = my_streams
+    while True:
+        live = live_set[pos[live_set] < prefill[live_set]]
+        if len(live) == 0:
+            break
+        n_rec = np.minimum((prefill[live] - pos[live] + rt - 1) // rt, 8)
+        rs = np.repeat(live, n_rec)
+        k_in = np.arange(len(rs)) - np.repeat(np.cumsum(n_rec) - n_rec, n_rec)
+        starts = pos[rs] + k_in * rt
+        ns = np.minimum(rt, prefill[rs] - starts)
+        offs = np.zeros(len(ns) + 1, np.uint64)
+        offs[1:] = np.cumsum(ns)
+        g0 = tr.offsets[rs] + starts
+        idx = np.repeat(g0, ns) + (np.arange(int(offs[-1])) - np.repeat(offs[:-1].astype(np.int64), ns))
+        rep = srv.update_arrays(local_h[rs // R], (rs % R).astype(np.int32), starts.astype(np.uint64), offs,
+                                tr.tokens[idx], 0.0)
+        assert rep["ok"].all()
+        pos[live] += np.minimum(prefill[live] - pos[live], chunk)
+    pos = prefill.copy()  # every rank knows every stream's prefix length
+
+    # ---- per-step inputs of this rank (the streams it produces), resident in HBM ----
+    produced = np.arange(rank, S, world)
+    rng = np.random.default_rng(args.seed + 7919 * rank)
+    steps_in = []
+    for s in range(W + K + E):
+        live = produced[pos[produced] < tr.lengths[produced]]
+        ns = np.minimum(rt, tr.lengths[live] - pos[live])
+        rec = np.zeros((len(live), APP_W), np.int32)
+        rec[:, 0] = local_h[live // R]
+        rec[:, 1] = live % R
+        rec[:, 2] = (pos[live] & 0xFFFFFFFF).astype(np.uint32).view(np.int32)
+        rec[:, 3] = (pos[live] >> 32).astype(np.int32)
+        rec[:, 4] = ns
+        for j in range(16):
+            ok = j < ns
+            rec[ok, 5 + j] = tr.tokens[tr.offsets[live[ok]] + pos[live[ok]] + j]
+        alg = append_alg_bytes(pos[live], ns)
+        pos[live] += ns
+        pool = produced[prefill[produced] >= 7]
+        st = pool[rng.integers(0, len(pool), Q)]
+        qp = np.minimum(6 + (rng.random(Q) * (prefill[st] - 6 + 1)).astype(np.int64), prefill[st])
+        qr = np.zeros((Q, QRY_W), np.int32)
+        qr[:, 0] = local_h[st // R]
+        qr[:, 1] = 6
+        b0 = tr.offsets[st] + qp
+        for j in range(6):
+            qr[:, 2 + j] = tr.tokens[b0 - 6 + j]
+        tl = (tr.lengths[st] - qp).astype(np.int32)
+        qr[:, 10] = tl
+        qr[:, 11] = tl
+        for j in range(dl):
+            ok = j < tl
+            qr[ok, 12 + j] = tr.tokens[(b0 + j)[ok]]
+        steps_in.append(dict(app=torch.from_numpy(rec).to(dev), app_owner=torch.from_numpy(owner_g[live // R]).to(
+            device=dev, dtype=torch.int32), q=torch.from_numpy(qr).to(dev),
+            q_owner=torch.from_numpy(owner_g[st // R]).to(device=dev, dtype=torch.int32), alg=alg,
+            ntok=int(ns.sum())))
+
+    router = Router(world)
+    sp_args = torch.from_numpy(args_array([SpeculationArgs(dl, 6, 1, kq, 0.25, 1)]).view(np.uint8).copy()).to(dev)
+    L = _lib.lib()
+    d_stats = torch.zeros(8, dtype=torch.int64, device=dev)
+    app_alg_owner = [0]
+
+    def step(s, stats):
+        inp = steps_in[s]
+        stream = torch.cuda.current_stream(dev).cuda_stream
+        # appends -> owners
+        ra, _ = router.forward(inp["app_owner"], inp["app"])
+        m = ra.shape[0]
+        if m:
+            meta = ra[:, :5].cpu().numpy()
+            n = meta[:, 4].astype(np.int64)
+            toks = ra[:, 5:5 + 16][torch.arange(16, device=dev)[None, :] < ra[:, 4:5]].contiguous()
+            offs = np.zeros(m + 1, np.uint64)
+            offs[1:] = np.cumsum(n)
+            prev = meta[:, 2].view(np.uint32).astype(np.uint64) | (meta[:, 3].astype(np.uint64) << np.uint64(32))
+            rep = srv.update_device(meta[:, 0].copy(), meta[:, 1].copy(), prev, offs, toks.data_ptr(), 0.0, stream)
+            assert rep["ok"].all()
+            if stats:
+                app_alg_owner[0] += append_alg_bytes(prev.astype(np.int64), n)
+        # queries -> owners -> replies
+        rq, st_q = router.forward(inp["q_owner"], inp["q"])
+        mq = rq.shape[0]
+        hcol = rq[:, 0].contiguous()
+        plen = rq[:, 1].contiguous()
+        tl = rq[:, 10].contiguous()
+        lim = rq[:, 11].contiguous()
+        nc = torch.zeros(mq, 1, dtype=torch.int32, device=dev)
+        ln = torch.zeros(mq, kq, dtype=torch.int32, device=dev)
+        sc = torch.zeros(mq, kq, dtype=torch.float64, device=dev)
+        sp = torch.zeros(mq, kq, dtype=torch.int64, device=dev)
+        tk = torch.zeros(mq, kq * dl, dtype=torch.int32, device=dev)
+        v = torch.zeros(3, mq, dtype=torch.int32, device=dev)
+        if mq:
+            cand = _lib.Candidates(kq, dl, nc.data_ptr(), ln.data_ptr(), sc.data_ptr(), sp.data_ptr(), tk.data_ptr())
+            vo = _lib.VerifyOut(v[0].data_ptr(), v[1].data_ptr(), v[2].data_ptr())
+            _lib.check(L.dgds_speculate_device(
+                srv.handle, mq, C.c_void_p(hcol.data_ptr()), C.c_void_p(plen.data_ptr()),
+                C.c_void_p(rq[:, 2:].data_ptr()), QRY_W, C.c_void_p(sp_args.data_ptr()), 0, kq, dl, C.byref(cand),
+                C.c_void_p(rq[:, 12:].data_ptr()), QRY_W, C.c_void_p(tl.data_ptr()), C.c_void_p(lim.data_ptr()),
+                C.byref(vo), C.c_void_p(d_stats.data_ptr()) if stats else None, C.c_void_p(stream)))
+        replies = torch.cat([nc, ln, sc.view(torch.int32), sp.view(torch.int32), tk, v.t()], dim=1)
+        return router.reverse(replies, st_q)
+
+    for s in range(W):
+        step(s, False)
+    torch.cuda.synchronize()
+    prof = _lib.Profile()
+    _lib.check(L.dgds_profile_enable(srv.handle, 1))
+    _lib.check(L.dgds_profile_read(srv.handle, C.byref(prof), 1))
+    d_stats.zero_()
+    dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record()
+        for s in range(W, W + K):
+            step(s, True)
+        e1.record()
+        torch.cuda.synchronize()
+    dist.barrier()
+    ms = torch.tensor([e0.elapsed_time(e1)], device=dev)
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    T = ms.item() / 1e3
+    _lib.check(L.dgds_profile_read(srv.handle, C.byref(prof), 1))
+    tot = torch.tensor([sum(steps_in[s]["ntok"] for s in range(W, W + K)), int(d_stats[7].item()),
+                        app_alg_owner[0], prof.query_ms * 1e3, prof.append_ms * 1e3,
+                        prof.query_launches + prof.append_launches], dtype=torch.float64, device=dev)
+    dist.all_reduce(tot)
+    ntok_all, q_alg_all, a_alg_all, qus_all, aus_all, launches_all = tot.tolist()
+
+    # ---- e2e: the same routed step with pinned host inputs copied in and replies read back ----
+    e2e = None
+    if E > 0:
+        host_in = [{k: (v.cpu().pin_memory() if torch.is_tensor(v) else v) for k, v in steps_in[s].items()}
+                   for s in range(W + K, W + K + E)]
+        h2d = sum(x["app"].nbytes + x["app_owner"].nbytes + x["q"].nbytes + x["q_owner"].nbytes for x in host_in)
+        dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        d2h = 0
+        for hin in host_in:
+            for k in ("app", "app_owner", "q", "q_owner"):
+                steps_in[0][k] = hin[k].to(dev, non_blocking=True)
+            back = step(0, False).cpu()
+            d2h += back.nbytes
+        torch.cuda.synchronize()
+        dt = torch.tensor([time.perf_counter() - t0], device=dev)
+        dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+        e2e = {"value": world * Q * E / dt.item(), "unit": "queries/s", "h2d_bytes_per_step": h2d // E,
+               "d2h_bytes_per_step": d2h // E, "steps": E,
+               "path": "routed step, pinned host records in / replies out (rank-local view)"}
+
+    if rank == 0:
+        peak, peak_kind = peaks()
+        q_ach = q_alg_all / (qus_all / 1e6) / 1e9 / world if qus_all else 0.0
+        a_ach = a_alg_all / (aus_all / 1e6) / 1e9 / world if aus_all else 0.0
+        dom_q = qus_all >= aus_all
+        roof = lambda kern, ach, alg, us, n: {  # noqa: E731
+            "kernel": kern, "bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+            "frac_random_ceiling": ach / RANDOM_CEILING_GBS, "traffic": None, "alg_bytes_per_launch": alg / max(1, n),
+            "avg_launch_ms": us / 1e3 / max(1, n), "peak_kind": peak_kind, "per_gpu": True}
+        line = {
+            "metric": "draft_queries_per_s", "value": world * Q * K / T, "unit": "queries/s", "n_gpus": world,
+            "steps": K, "warmup": W, "ms_per_step": 1e3 * T / K, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "i32+f64", "data": "synthetic",
+            "append_tokens_per_s": ntok_all / T,
+            "config": {"workload": f"{args.config}: {CONFIG_NAMES[args.config]} (group set replicated x{world})",
+                       "queries_per_step": world * Q, "queries_per_rank": Q, "record_tokens": rt, "top_k": kq,
+                       "draft_len": dl, "prefill": args.prefill, "groups": G,
+                       "routing": "fnv1a64(gid) % N owner; NCCL all_to_all_single (counts, payload, replies)",
+                       "l2": "inputs larger than L2 (per-GPU index ~ the N=1 index)",
+                       "parallelism": f"group-sharded dp{world}"},
+            "roofline": roof("k_query (K2+K3)", q_ach, q_alg_all, qus_all, K * world) if dom_q else roof(
+                "k_append (K1)", a_ach, a_alg_all, aus_all, K * world),
+            "roofline_query": roof("k_query (K2+K3)", q_ach, q_alg_all, qus_all, K * world),
+            "roofline_append": roof("k_append (K1)", a_ach, a_alg_all, aus_all, K * world),
+            "cpu_baseline": None, "e2e": e2e, "gpu_launches": int(launches_all), "clocks": clk.summary(),
+        }
+        print(json.dumps(line))
+    srv.close()
+    dist.barrier()
+    dist.destroy_process_group()

@@ -1,0 +1,74 @@
+"""Owner routing of draft-server traffic across GPUs (one process per GPU).
+
+Groups are owned by ``fnv1a64(group_id) % world`` — the reference's own
+``shard_of_group`` (proj/src/dgds.cpp:10-14). A rank's append records and
+draft queries go to the owning rank with an all-to-all over NCCL
+(``torch.distributed``): the fixed-size records are bucketed by owner
+(``dgds_route_pack``, stable), the per-owner counts are exchanged, then the
+payloads; replies come back through the inverse all-to-all and are scattered
+into the original order (``dgds_route_unpack``).
+
+``Router`` is backend-agnostic: with CUDA tensors it uses the sm_100a
+pack/unpack kernels; the CPU/gloo tests inject a host packer to check the
+exchange protocol itself.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import Callable, Optional, Tuple
+
+import torch
+import torch.distributed as dist
+
+from . import _lib
+
+
+def cuda_pack(owner: torch.Tensor, records: torch.Tensor, world: int) -> Tuple[torch.Tensor, torch.Tensor, torch.Tensor]:
+    """Stable bucketing of [n, w] int32 records by owner on the GPU (k_route_*)."""
+    n, w = records.shape
+    out = torch.empty_like(records)
+    counts = torch.empty(world, dtype=torch.int64, device=records.device)
+    perm = torch.empty(n, dtype=torch.int64, device=records.device)
+    stream = torch.cuda.current_stream(records.device).cuda_stream
+    _lib.check(_lib.lib().dgds_route_pack(n, world, C.c_void_p(owner.data_ptr()), C.c_void_p(records.data_ptr()), w,
+                                          C.c_void_p(out.data_ptr()), C.c_void_p(counts.data_ptr()),
+                                          C.c_void_p(perm.data_ptr()), C.c_void_p(stream)))
+    return out, counts, perm
+
+
+def cuda_unpack(packed: torch.Tensor, perm: torch.Tensor) -> torch.Tensor:
+    """out[i] = packed[perm[i]] on the GPU (k_route_gather)."""
+    n, w = packed.shape
+    out = torch.empty_like(packed)
+    stream = torch.cuda.current_stream(packed.device).cuda_stream
+    _lib.check(_lib.lib().dgds_route_unpack(n, C.c_void_p(packed.data_ptr()), w, C.c_void_p(perm.data_ptr()),
+                                            C.c_void_p(out.data_ptr()), C.c_void_p(stream)))
+    return out
+
+
+class Router:
+    """One exchange round: records of every rank -> their owners -> replies back."""
+
+    def __init__(self, world: int, group=None, pack: Optional[Callable] = None, unpack: Optional[Callable] = None):
+        self.world = world
+        self.group = group
+        self.pack = pack or cuda_pack
+        self.unpack = unpack or cuda_unpack
+
+    def forward(self, owner: torch.Tensor, records: torch.Tensor):
+        """Send record i to rank owner[i]. Returns (received [m, w], state for `reverse`)."""
+        packed, counts, perm = self.pack(owner, records, self.world)
+        recv_counts = torch.empty_like(counts)
+        dist.all_to_all_single(recv_counts, counts, group=self.group)
+        send_splits = counts.tolist()
+        recv_splits = recv_counts.tolist()
+        received = records.new_empty((sum(recv_splits), records.shape[1]))
+        dist.all_to_all_single(received, packed, recv_splits, send_splits, group=self.group)
+        return received, (perm, send_splits, recv_splits)
+
+    def reverse(self, replies: torch.Tensor, state) -> torch.Tensor:
+        """Return one reply row per received record to its sender, in the sender's original order."""
+        perm, send_splits, recv_splits = state
+        back = replies.new_empty((sum(send_splits), replies.shape[1]))
+        dist.all_to_all_single(back, replies.contiguous(), send_splits, recv_splits, group=self.group)
+        return self.unpack(back, perm)

@@ -1,0 +1,90 @@
+"""The multi-GPU exchange protocol (paper_2511_14617_b200/routing.py) on CPU:
+world size 2 over gloo, host packer standing in for the CUDA pack kernel.
+Checks that every record reaches its owner exactly once, in stable order, and
+that replies come back to the sender in its original order."""
+import os
+import socket
+
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+
+def host_pack(owner, records, world):
+    order = torch.sort(owner.long(), stable=True).indices
+    counts = torch.bincount(owner.long(), minlength=world)
+    perm = torch.empty_like(order)
+    perm[order] = torch.arange(len(order))
+    return records[order], counts, perm
+
+
+def host_unpack(packed, perm):
+    return packed[perm]
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2511_14617_b200.routing import Router
+    try:
+        g = torch.Generator().manual_seed(rank)
+        n = 37 + 11 * rank
+        owner = torch.randint(0, world, (n,), generator=g, dtype=torch.int32)
+        rec = torch.stack([torch.full((n,), rank, dtype=torch.int32), torch.arange(n, dtype=torch.int32),
+                           owner], 1)
+        router = Router(world, pack=host_pack, unpack=host_unpack)
+        got, state = router.forward(owner, rec)
+        # every record delivered to its owner, senders in rank order, stable inside a sender
+        assert (got[:, 2] == rank).all()
+        for src in range(world):
+            idx = got[got[:, 0] == src][:, 1]
+            assert torch.equal(idx, torch.sort(idx).values)
+        # replies (a function of the received record) come back in the sender's order
+        replies = torch.stack([got[:, 0] * 1000 + got[:, 1], got[:, 2]], 1)
+        back = router.reverse(replies, state)
+        assert torch.equal(back[:, 0], rank * 1000 + torch.arange(n, dtype=torch.int32))
+        assert torch.equal(back[:, 1], owner)
+        # counts agree globally
+        total = torch.tensor([got.shape[0]])
+        dist.all_reduce(total)
+        ns = torch.tensor([n])
+        dist.all_reduce(ns)
+        assert total.item() == ns.item()
+        q.put((rank, "ok"))
+    except Exception as e:  # pragma: no cover - reported to the parent
+        q.put((rank, repr(e)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_router_world2_gloo():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    assert res == {0: "ok", 1: "ok"}, res
+
+
+def test_owner_is_reference_shard_of_group(reference):
+    from paper_2511_14617_b200.dgds import shard_of_group
+    from paper_2511_14617_b200.workload import group_id
+    if reference is None:
+        pytest.skip("oracle/_ref not built")
+    for n in (2, 4, 8):
+        assert [shard_of_group(group_id(g), n) for g in range(2048)] == \
+               [reference.shard_of_group(group_id(g), n) for g in range(2048)]
