@@ -127,20 +127,15 @@ def peaks():
 
 
 def append_alg_bytes(start: np.ndarray, n: np.ndarray, D: int = 24) -> int:
-    """B_app = 4 + 64 * min(D, t+1) per token at stream position t."""
-    total = 0
-    for s0, k in zip(start.tolist(), n.tolist()):
-        if k <= 0:
-            continue
-        lo, hi = s0 + 1, s0 + k  # t+1 ranges over lo..hi
-        full = 0
-        if lo <= D:
-            top = min(hi, D)
-            full += (lo + top) * (top - lo + 1) // 2
-        if hi > D:
-            full += (hi - max(lo, D + 1) + 1) * D
-        total += 4 * k + 64 * full
-    return total
+    """B_app = 4 + 64 * min(D, t+1) per token at stream position t (vectorised)."""
+    start = np.asarray(start, np.int64)
+    n = np.asarray(n, np.int64)
+    keep = n > 0
+    lo, hi, n = start[keep] + 1, start[keep] + n[keep], n[keep]  # t+1 ranges over lo..hi
+    top = np.minimum(hi, D)
+    ramp = np.where(lo <= D, (lo + top) * (top - lo + 1) // 2, 0)
+    flat = np.where(hi > D, (hi - np.maximum(lo, D + 1) + 1) * D, 0)
+    return int((4 * n + 64 * (ramp + flat)).sum())
 
 
 # ---------------------------------------------------------------------------

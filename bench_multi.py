@@ -124,11 +124,24 @@ def run_multi(args, world, rank, local, dev):
     d_stats = torch.zeros(8, dtype=torch.int64, device=dev)
     app_alg_owner = [0]
 
+    prof_host = {}
+    dbg = os.environ.get("DGDS_MULTI_BREAKDOWN") == "1"
+
+    def mark(name, t0):
+        if dbg:
+            torch.cuda.synchronize()
+            t1 = time.perf_counter()
+            prof_host[name] = prof_host.get(name, 0.0) + t1 - t0
+            return t1
+        return t0
+
     def step(s, stats):
         inp = steps_in[s]
         stream = torch.cuda.current_stream(dev).cuda_stream
+        t0 = time.perf_counter()
         # appends -> owners
         ra, _ = router.forward(inp["app_owner"], inp["app"])
+        t0 = mark("a2a_append", t0)
         m = ra.shape[0]
         if m:
             meta = ra[:, :5].cpu().numpy()
@@ -141,8 +154,10 @@ def run_multi(args, world, rank, local, dev):
             assert rep["ok"].all()
             if stats:
                 app_alg_owner[0] += append_alg_bytes(prev.astype(np.int64), n)
+        t0 = mark("append", t0)
         # queries -> owners -> replies
         rq, st_q = router.forward(inp["q_owner"], inp["q"])
+        t0 = mark("a2a_query", t0)
         mq = rq.shape[0]
         hcol = rq[:, 0].contiguous()
         plen = rq[:, 1].contiguous()
@@ -162,8 +177,11 @@ def run_multi(args, world, rank, local, dev):
                 C.c_void_p(rq[:, 2:].data_ptr()), QRY_W, C.c_void_p(sp_args.data_ptr()), 0, kq, dl, C.byref(cand),
                 C.c_void_p(rq[:, 12:].data_ptr()), QRY_W, C.c_void_p(tl.data_ptr()), C.c_void_p(lim.data_ptr()),
                 C.byref(vo), C.c_void_p(d_stats.data_ptr()) if stats else None, C.c_void_p(stream)))
+        t0 = mark("query", t0)
         replies = torch.cat([nc, ln, sc.view(torch.int32), sp.view(torch.int32), tk, v.t()], dim=1)
-        return router.reverse(replies, st_q)
+        back = router.reverse(replies, st_q)
+        mark("a2a_reply", t0)
+        return back
 
     for s in range(W):
         step(s, False)
@@ -214,6 +232,9 @@ def run_multi(args, world, rank, local, dev):
                "d2h_bytes_per_step": d2h // E, "steps": E,
                "path": "routed step, pinned host records in / replies out (rank-local view)"}
 
+    if dbg:
+        print(f"rank {rank} host breakdown (s over {K} steps):", {k: round(v, 4) for k, v in prof_host.items()},
+              flush=True)
     if rank == 0:
         peak, peak_kind = peaks()
         q_ach = q_alg_all / (qus_all / 1e6) / 1e9 / world if qus_all else 0.0
