@@ -29,7 +29,7 @@ def run_multi(args, world, rank, local, dev):
     from bench import CONFIG_NAMES, RANDOM_CEILING_GBS, ClockSampler, append_alg_bytes, peaks
     from paper_2511_14617_b200 import _lib
     from paper_2511_14617_b200.dgds import DgdsParams, DraftServer, SpeculationArgs, args_array, shard_of_group
-    from paper_2511_14617_b200.routing import Router
+    from paper_2511_14617_b200.routing import PaddedRouter
     from paper_2511_14617_b200.workload import CONFIGS, generate_workload, group_id
 
     base = CONFIGS[args.config]
@@ -118,69 +118,70 @@ def run_multi(args, world, rank, local, dev):
             q_owner=torch.from_numpy(owner_g[st // R]).to(device=dev, dtype=torch.int32), alg=alg,
             ntok=int(ns.sum())))
 
-    router = Router(world)
+    router = PaddedRouter(world)
+    capq = int(1.5 * Q / world) + 512
+    capa = int(1.5 * len(produced) / world) + 64
     sp_args = torch.from_numpy(args_array([SpeculationArgs(dl, 6, 1, kq, 0.25, 1)]).view(np.uint8).copy()).to(dev)
     L = _lib.lib()
     d_stats = torch.zeros(8, dtype=torch.int64, device=dev)
     app_alg_owner = [0]
-
-    prof_host = {}
-    dbg = os.environ.get("DGDS_MULTI_BREAKDOWN") == "1"
-
-    def mark(name, t0):
-        if dbg:
-            torch.cuda.synchronize()
-            t1 = time.perf_counter()
-            prof_host[name] = prof_host.get(name, 0.0) + t1 - t0
-            return t1
-        return t0
-
+    overflow = torch.zeros((), dtype=torch.bool, device=dev)
+    side = torch.cuda.Stream(dev)
+    ev_side = torch.cuda.Event()
+    meta_h = torch.empty((world * capa, 5), dtype=torch.int32).pin_memory()
+    mq = world * capq
+    nc = torch.zeros(mq, 1, dtype=torch.int32, device=dev)
+    ln = torch.zeros(mq, kq, dtype=torch.int32, device=dev)
+    sc = torch.zeros(mq, kq, dtype=torch.float64, device=dev)
+    sp = torch.zeros(mq, kq, dtype=torch.int64, device=dev)
+    tk = torch.zeros(mq, kq * dl, dtype=torch.int32, device=dev)
+    v = torch.zeros(3, mq, dtype=torch.int32, device=dev)
+    cand = _lib.Candidates(kq, dl, nc.data_ptr(), ln.data_ptr(), sc.data_ptr(), sp.data_ptr(), tk.data_ptr())
+    vo = _lib.VerifyOut(v[0].data_ptr(), v[1].data_ptr(), v[2].data_ptr())
     def step(s, stats):
+        """One tick in engine order (engine.cpp:88-161): draft queries (+ verify) on the
+        current index, then the appends of the tick's emitted tokens."""
+        nonlocal overflow
         inp = steps_in[s]
-        stream = torch.cuda.current_stream(dev).cuda_stream
-        t0 = time.perf_counter()
-        # appends -> owners
-        ra, _ = router.forward(inp["app_owner"], inp["app"])
-        t0 = mark("a2a_append", t0)
-        m = ra.shape[0]
-        if m:
-            meta = ra[:, :5].cpu().numpy()
-            n = meta[:, 4].astype(np.int64)
-            toks = ra[:, 5:5 + 16][torch.arange(16, device=dev)[None, :] < ra[:, 4:5]].contiguous()
-            offs = np.zeros(m + 1, np.uint64)
-            offs[1:] = np.cumsum(n)
-            prev = meta[:, 2].view(np.uint32).astype(np.uint64) | (meta[:, 3].astype(np.uint64) << np.uint64(32))
-            rep = srv.update_device(meta[:, 0].copy(), meta[:, 1].copy(), prev, offs, toks.data_ptr(), 0.0, stream)
-            assert rep["ok"].all()
-            if stats:
-                app_alg_owner[0] += append_alg_bytes(prev.astype(np.int64), n)
-        t0 = mark("append", t0)
-        # queries -> owners -> replies
-        rq, st_q = router.forward(inp["q_owner"], inp["q"])
-        t0 = mark("a2a_query", t0)
-        mq = rq.shape[0]
+        main = torch.cuda.current_stream(dev)
+        # (1) queries -> owners (static splits, no host sync)
+        rq, st_q = router.forward(inp["q_owner"], inp["q"], capq)
+        # (2) appends -> owners on a side stream; their metadata reaches the host while (3) runs
+        side.wait_stream(main)
+        with torch.cuda.stream(side):
+            ra, st_a = router.forward(inp["app_owner"], inp["app"], capa)
+            meta_h.copy_(ra[:, :5], non_blocking=True)
+            ev_side.record(side)
+        ra.record_stream(main)  # K1 reads the tokens on the main stream
+        # (3) owner: K2 + fused K3 over the received slots (padding has handle -1)
         hcol = rq[:, 0].contiguous()
         plen = rq[:, 1].contiguous()
         tl = rq[:, 10].contiguous()
         lim = rq[:, 11].contiguous()
-        nc = torch.zeros(mq, 1, dtype=torch.int32, device=dev)
-        ln = torch.zeros(mq, kq, dtype=torch.int32, device=dev)
-        sc = torch.zeros(mq, kq, dtype=torch.float64, device=dev)
-        sp = torch.zeros(mq, kq, dtype=torch.int64, device=dev)
-        tk = torch.zeros(mq, kq * dl, dtype=torch.int32, device=dev)
-        v = torch.zeros(3, mq, dtype=torch.int32, device=dev)
-        if mq:
-            cand = _lib.Candidates(kq, dl, nc.data_ptr(), ln.data_ptr(), sc.data_ptr(), sp.data_ptr(), tk.data_ptr())
-            vo = _lib.VerifyOut(v[0].data_ptr(), v[1].data_ptr(), v[2].data_ptr())
-            _lib.check(L.dgds_speculate_device(
-                srv.handle, mq, C.c_void_p(hcol.data_ptr()), C.c_void_p(plen.data_ptr()),
-                C.c_void_p(rq[:, 2:].data_ptr()), QRY_W, C.c_void_p(sp_args.data_ptr()), 0, kq, dl, C.byref(cand),
-                C.c_void_p(rq[:, 12:].data_ptr()), QRY_W, C.c_void_p(tl.data_ptr()), C.c_void_p(lim.data_ptr()),
-                C.byref(vo), C.c_void_p(d_stats.data_ptr()) if stats else None, C.c_void_p(stream)))
-        t0 = mark("query", t0)
+        _lib.check(L.dgds_speculate_device(
+            srv.handle, mq, C.c_void_p(hcol.data_ptr()), C.c_void_p(plen.data_ptr()),
+            C.c_void_p(rq[:, 2:].data_ptr()), QRY_W, C.c_void_p(sp_args.data_ptr()), 0, kq, dl, C.byref(cand),
+            C.c_void_p(rq[:, 12:].data_ptr()), QRY_W, C.c_void_p(tl.data_ptr()), C.c_void_p(lim.data_ptr()),
+            C.byref(vo), C.c_void_p(d_stats.data_ptr()) if stats else None, C.c_void_p(main.cuda_stream)))
         replies = torch.cat([nc, ln, sc.view(torch.int32), sp.view(torch.int32), tk, v.t()], dim=1)
-        back = router.reverse(replies, st_q)
-        mark("a2a_reply", t0)
+        back, ovq = router.reverse(replies, st_q)
+        # (4) host bookkeeping of the received appends overlaps the query kernel; K1 after it
+        ev_side.synchronize()
+        meta = meta_h.numpy()
+        rows = np.nonzero(meta[:, 0] >= 0)[0]
+        if len(rows):
+            m = meta[rows]
+            n = m[:, 4].astype(np.uint64)
+            prev = m[:, 2].view(np.uint32).astype(np.uint64) | (m[:, 3].astype(np.uint64) << np.uint64(32))
+            starts = rows.astype(np.uint64) * np.uint64(APP_W) + np.uint64(5)
+            main.wait_event(ev_side)
+            rep = srv.update_device_strided(m[:, 0].copy(), m[:, 1].copy(), prev, starts, n, ra.data_ptr(), 0.0,
+                                            main.cuda_stream)
+            if not rep["ok"].all():
+                raise RuntimeError("routed append out of order")
+            if stats:
+                app_alg_owner[0] += append_alg_bytes(prev.astype(np.int64), n.astype(np.int64))
+        overflow = overflow | ovq | st_a[1]
         return back
 
     for s in range(W):
@@ -232,9 +233,8 @@ def run_multi(args, world, rank, local, dev):
                "d2h_bytes_per_step": d2h // E, "steps": E,
                "path": "routed step, pinned host records in / replies out (rank-local view)"}
 
-    if dbg:
-        print(f"rank {rank} host breakdown (s over {K} steps):", {k: round(v, 4) for k, v in prof_host.items()},
-              flush=True)
+    if bool(overflow.item()):
+        raise RuntimeError("routing capacity overflow: results of this run are invalid")
     if rank == 0:
         peak, peak_kind = peaks()
         q_ach = q_alg_all / (qus_all / 1e6) / 1e9 / world if qus_all else 0.0

@@ -165,6 +165,13 @@ int dgds_update_batch_device(dgds_server* s, int64_t n, const int32_t* handles, 
                              const uint64_t* prev_counts, const uint64_t* tok_offsets, const int32_t* d_tokens,
                              double now, dgds_update_reply* replies, void* stream);
 
+/* Same as dgds_update_batch_device with record i's tokens at d_tokens[tok_starts[i] .. + tok_counts[i])
+ * (host arrays) — e.g. fixed-size routed records with the tokens inline. */
+int dgds_update_batch_device_strided(dgds_server* s, int64_t n, const int32_t* handles, const int32_t* request_ids,
+                                     const uint64_t* prev_counts, const uint64_t* tok_starts,
+                                     const uint64_t* tok_counts, const int32_t* d_tokens, double now,
+                                     dgds_update_reply* replies, void* stream);
+
 /* n speculate calls. Query q uses patterns[pat_offsets[q] .. pat_offsets[q+1]) and
  * args[q * args_stride] (args_stride 0 = one shared args). Host buffers; blocks until done.
  */

@@ -136,6 +136,7 @@ EXPORTS = {
     "dgds_node_count": (C.c_int, [_P, C.POINTER(_U64)]),
     "dgds_update_batch": (C.c_int, [_P, _I64, _P, _P, _P, _P, _P, _D, _P]),
     "dgds_update_batch_device": (C.c_int, [_P, _I64, _P, _P, _P, _P, _P, _D, _P, _P]),
+    "dgds_update_batch_device_strided": (C.c_int, [_P, _I64, _P, _P, _P, _P, _P, _P, _D, _P, _P]),
     "dgds_speculate_batch": (C.c_int, [_P, _I64, _P, _P, _P, _P, _I64, C.POINTER(Candidates)]),
     "dgds_speculate_device": (C.c_int, [_P, _I64, _P, _P, _P, _I32, _P, _I64, _I32, _I32, C.POINTER(Candidates), _P,
                                         _I32,

@@ -350,14 +350,18 @@ struct PendingPiece {
 // Shared host logic of update_batch / update_batch_device: replies in call
 // order (DraftServer::update_cst, dgds.cpp:36-51 -> GroupDraftIndex::append,
 // cst.cpp:118-133), plus the device segment table.
+// Record i's tokens are tokens[tok_start(i) .. tok_start(i) + tok_count(i)).
 int plan_updates(dgds_server* s, int64_t n, const int32_t* handles, const int32_t* rids, const uint64_t* prev,
-                 const uint64_t* offs, double now, dgds_update_reply* rep, std::vector<dgds::AppendSeg>& segs,
-                 std::vector<dgds::AppendPiece>& pieces, uint64_t* worst) {
+                 const uint64_t* offs, const uint64_t* counts, double now, dgds_update_reply* rep,
+                 std::vector<dgds::AppendSeg>& segs, std::vector<dgds::AppendPiece>& pieces, uint64_t* worst) {
+  // offs[n+1] cumulative (counts == nullptr), or offs[n] starts + counts[n]
+  auto tstart = [&](int64_t i) { return offs[i]; };
+  auto tcount = [&](int64_t i) { return counts ? counts[i] : offs[i + 1] - offs[i]; };
   for (int64_t i = 0; i < n; ++i) {
     int rc = check_handle(s, handles[i]);
     if (rc) return rc;
     if (rids[i] < 0) return fail(DGDS_EINVAL, "request_id must be nonnegative");
-    if (offs[i + 1] < offs[i]) return fail(DGDS_EINVAL, "token offsets must be nondecreasing");
+    if (!counts && offs[i + 1] < offs[i]) return fail(DGDS_EINVAL, "token offsets must be nondecreasing");
   }
   const uint64_t stamp = ++s->batch_stamp;
   std::vector<PendingPiece> pend;
@@ -378,7 +382,7 @@ int plan_updates(dgds_server* s, int64_t n, const int32_t* handles, const int32_
       it = g.streams.emplace(rids[i], sr).first;
     }
     StreamRec& sr = it->second;
-    const uint64_t cnt = offs[i + 1] - offs[i];
+    const uint64_t cnt = tcount(i);
     if (prev[i] != sr.stored) {
       rep[i] = dgds_update_reply{0, 0, g.version, sr.stored};
       continue;
@@ -396,7 +400,7 @@ int plan_updates(dgds_server* s, int64_t n, const int32_t* handles, const int32_
       sg.start = sr.stored;
       segs.push_back(sg);
     }
-    pend.push_back(PendingPiece{sr.batch_seg, offs[i], static_cast<uint32_t>(cnt)});
+    pend.push_back(PendingPiece{sr.batch_seg, tstart(i), static_cast<uint32_t>(cnt)});
     *worst += worst_windows(sr.stored, cnt, static_cast<uint64_t>(s->D));
     sr.stored += cnt;
     g.version += 1;
@@ -655,7 +659,7 @@ int dgds_update_batch(dgds_server* s, int64_t n, const int32_t* handles, const i
   std::vector<dgds::AppendSeg> segs;
   std::vector<dgds::AppendPiece> pieces;
   uint64_t worst = 0;
-  if (int rc = plan_updates(s, n, handles, rids, prev, offs, now, rep, segs, pieces, &worst)) return rc;
+  if (int rc = plan_updates(s, n, handles, rids, prev, offs, nullptr, now, rep, segs, pieces, &worst)) return rc;
   if (segs.empty()) return DGDS_OK;
   if (int rc = ensure_capacity(s, worst)) return rc;
   // one pinned staging block -> one H2D copy: segs | pieces | tokens
@@ -685,9 +689,9 @@ int dgds_update_batch(dgds_server* s, int64_t n, const int32_t* handles, const i
   return DGDS_OK;
 }
 
-int dgds_update_batch_device(dgds_server* s, int64_t n, const int32_t* handles, const int32_t* rids,
-                             const uint64_t* prev, const uint64_t* offs, const int32_t* d_tokens, double now,
-                             dgds_update_reply* rep, void* stream) {
+static int update_device_impl(dgds_server* s, int64_t n, const int32_t* handles, const int32_t* rids, const uint64_t* prev,
+                       const uint64_t* offs, const uint64_t* counts, const int32_t* d_tokens, double now,
+                       dgds_update_reply* rep, void* stream) {
   if (n < 0) return fail(DGDS_EINVAL, "negative batch size");
   if (n == 0) return DGDS_OK;
   std::lock_guard<std::mutex> lk(s->mu);
@@ -695,7 +699,7 @@ int dgds_update_batch_device(dgds_server* s, int64_t n, const int32_t* handles, 
   std::vector<dgds::AppendSeg> segs;
   std::vector<dgds::AppendPiece> pieces;
   uint64_t worst = 0;
-  if (int rc = plan_updates(s, n, handles, rids, prev, offs, now, rep, segs, pieces, &worst)) return rc;
+  if (int rc = plan_updates(s, n, handles, rids, prev, offs, counts, now, rep, segs, pieces, &worst)) return rc;
   if (segs.empty()) return DGDS_OK;
   if (int rc = ensure_capacity(s, worst)) return rc;
   StreamJoin join(s, stream);
@@ -719,6 +723,18 @@ int dgds_update_batch_device(dgds_server* s, int64_t n, const int32_t* handles, 
   }
   s->used_ub += worst;
   return DGDS_OK;
+}
+
+int dgds_update_batch_device(dgds_server* s, int64_t n, const int32_t* handles, const int32_t* rids,
+                             const uint64_t* prev, const uint64_t* offs, const int32_t* d_tokens, double now,
+                             dgds_update_reply* rep, void* stream) {
+  return update_device_impl(s, n, handles, rids, prev, offs, nullptr, d_tokens, now, rep, stream);
+}
+
+int dgds_update_batch_device_strided(dgds_server* s, int64_t n, const int32_t* handles, const int32_t* rids,
+                                     const uint64_t* prev, const uint64_t* tok_starts, const uint64_t* tok_counts,
+                                     const int32_t* d_tokens, double now, dgds_update_reply* rep, void* stream) {
+  return update_device_impl(s, n, handles, rids, prev, tok_starts, tok_counts, d_tokens, now, rep, stream);
 }
 
 int dgds_speculate_verify_batch(dgds_server* s, int64_t n, const int32_t* handles, const uint64_t* pat_offs,

@@ -246,6 +246,22 @@ class DraftServer:
                                              C.c_void_p(stream or None)))
         return rep
 
+    def update_device_strided(self, handles: np.ndarray, request_ids: np.ndarray, prev_counts: np.ndarray,
+                              tok_starts: np.ndarray, tok_counts: np.ndarray, d_tokens_ptr: int, now: float,
+                              stream: int = 0) -> np.ndarray:
+        """Host metadata + device tokens at d_tokens[tok_starts[i] ..+ tok_counts[i]] (routed records)."""
+        n = len(handles)
+        handles = np.ascontiguousarray(handles, np.int32)
+        request_ids = np.ascontiguousarray(request_ids, np.int32)
+        prev_counts = np.ascontiguousarray(prev_counts, np.uint64)
+        tok_starts = np.ascontiguousarray(tok_starts, np.uint64)
+        tok_counts = np.ascontiguousarray(tok_counts, np.uint64)
+        rep = np.zeros(n, self.REPLY_DTYPE)
+        check(lib().dgds_update_batch_device_strided(self._h, n, _ptr(handles), _ptr(request_ids), _ptr(prev_counts),
+                                                     _ptr(tok_starts), _ptr(tok_counts), C.c_void_p(d_tokens_ptr),
+                                                     float(now), _ptr(rep), C.c_void_p(stream or None)))
+        return rep
+
     def speculate(self, group_id: str, pattern: Sequence[int], args: SpeculationArgs) -> List[DraftCandidate]:
         """DraftServer::speculate (dgds.cpp:130-138)."""
         return self.speculate_batch([group_id], [pattern], [args])[0]

@@ -72,3 +72,31 @@ class Router:
         back = replies.new_empty((sum(send_splits), replies.shape[1]))
         dist.all_to_all_single(back, replies.contiguous(), send_splits, recv_splits, group=self.group)
         return self.unpack(back, perm)
+
+
+class PaddedRouter(Router):
+    """Fixed-capacity exchange: every rank sends `cap` slots to every rank, so the
+    split sizes are static and no host synchronisation is needed. Empty slots
+    carry -1 in column 0 (an invalid group handle: the query kernel answers it
+    with nothing, the append path skips it). Overflow (> cap records for one
+    owner) is reported as a device flag."""
+
+    def forward(self, owner: torch.Tensor, records: torch.Tensor, cap: int):
+        _, counts, perm = self.pack(owner, records, self.world)
+        own = owner.long()
+        starts = torch.cumsum(counts, 0) - counts
+        r = perm - starts[own]
+        overflow = (r >= cap).any()
+        idx = own * cap + r.clamp(max=cap - 1)
+        send = records.new_zeros((self.world * cap, records.shape[1]))
+        send[:, 0] = -1
+        send.index_copy_(0, idx, records)
+        recv = torch.empty_like(send)
+        dist.all_to_all_single(recv, send, group=self.group)
+        return recv, (idx, overflow)
+
+    def reverse(self, replies: torch.Tensor, state):
+        idx, overflow = state
+        back = torch.empty_like(replies)
+        dist.all_to_all_single(back, replies.contiguous(), group=self.group)
+        return back[idx], overflow

@@ -60,6 +60,19 @@ def _worker(rank, world, port, q):
         ns = torch.tensor([n])
         dist.all_reduce(ns)
         assert total.item() == ns.item()
+        # fixed-capacity variant (static splits, no host sync)
+        from paper_2511_14617_b200.routing import PaddedRouter
+        pr = PaddedRouter(world, pack=host_pack, unpack=host_unpack)
+        cap = 64
+        got2, st2 = pr.forward(owner, rec, cap)
+        valid = got2[got2[:, 0] >= 0]
+        assert (valid[:, 2] == rank).all()
+        tot2 = torch.tensor([valid.shape[0]])
+        dist.all_reduce(tot2)
+        assert tot2.item() == ns.item()
+        rep2 = torch.stack([got2[:, 0] * 1000 + got2[:, 1], got2[:, 2]], 1)
+        back2, ovf = pr.reverse(rep2, st2)
+        assert not bool(ovf) and torch.equal(back2, back)
         q.put((rank, "ok"))
     except Exception as e:  # pragma: no cover - reported to the parent
         q.put((rank, repr(e)))
