@@ -138,14 +138,27 @@ def run_multi(args, world, rank, local, dev):
     v = torch.zeros(3, mq, dtype=torch.int32, device=dev)
     cand = _lib.Candidates(kq, dl, nc.data_ptr(), ln.data_ptr(), sc.data_ptr(), sp.data_ptr(), tk.data_ptr())
     vo = _lib.VerifyOut(v[0].data_ptr(), v[1].data_ptr(), v[2].data_ptr())
+    prof_host = {}
+    dbg = os.environ.get("DGDS_MULTI_BREAKDOWN") == "1"
+
+    def mark(name, t0):
+        if not dbg:
+            return t0
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        prof_host[name] = prof_host.get(name, 0.0) + t1 - t0
+        return t1
+
     def step(s, stats):
         """One tick in engine order (engine.cpp:88-161): draft queries (+ verify) on the
         current index, then the appends of the tick's emitted tokens."""
         nonlocal overflow
         inp = steps_in[s]
         main = torch.cuda.current_stream(dev)
+        t0 = mark("start", time.perf_counter())
         # (1) queries -> owners (static splits, no host sync)
         rq, st_q = router.forward(inp["q_owner"], inp["q"], capq)
+        t0 = mark("q_fwd", t0)
         # (2) appends -> owners on a side stream; their metadata reaches the host while (3) runs
         side.wait_stream(main)
         with torch.cuda.stream(side):
@@ -153,6 +166,7 @@ def run_multi(args, world, rank, local, dev):
             meta_h.copy_(ra[:, :5], non_blocking=True)
             ev_side.record(side)
         ra.record_stream(main)  # K1 reads the tokens on the main stream
+        t0 = mark("a_fwd", t0)
         # (3) owner: K2 + fused K3 over the received slots (padding has handle -1)
         hcol = rq[:, 0].contiguous()
         plen = rq[:, 1].contiguous()
@@ -163,8 +177,10 @@ def run_multi(args, world, rank, local, dev):
             C.c_void_p(rq[:, 2:].data_ptr()), QRY_W, C.c_void_p(sp_args.data_ptr()), 0, kq, dl, C.byref(cand),
             C.c_void_p(rq[:, 12:].data_ptr()), QRY_W, C.c_void_p(tl.data_ptr()), C.c_void_p(lim.data_ptr()),
             C.byref(vo), C.c_void_p(d_stats.data_ptr()) if stats else None, C.c_void_p(main.cuda_stream)))
+        t0 = mark("q_kernel", t0)
         replies = torch.cat([nc, ln, sc.view(torch.int32), sp.view(torch.int32), tk, v.t()], dim=1)
         back, ovq = router.reverse(replies, st_q)
+        t0 = mark("q_rev", t0)
         # (4) host bookkeeping of the received appends overlaps the query kernel; K1 after it
         ev_side.synchronize()
         meta = meta_h.numpy()
@@ -182,6 +198,7 @@ def run_multi(args, world, rank, local, dev):
             if stats:
                 app_alg_owner[0] += append_alg_bytes(prev.astype(np.int64), n.astype(np.int64))
         overflow = overflow | ovq | st_a[1]
+        mark("append", t0)
         return back
 
     for s in range(W):
@@ -233,6 +250,8 @@ def run_multi(args, world, rank, local, dev):
                "d2h_bytes_per_step": d2h // E, "steps": E,
                "path": "routed step, pinned host records in / replies out (rank-local view)"}
 
+    if dbg:
+        print(f"rank {rank} breakdown (s, all steps):", {k: round(v, 4) for k, v in prof_host.items()}, flush=True)
     if bool(overflow.item()):
         raise RuntimeError("routing capacity overflow: results of this run are invalid")
     if rank == 0:
