@@ -296,7 +296,9 @@ def main_b200(args):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        import datetime
+        # short collective timeout: a failing rank must not leave its peers spinning on the box
+        dist.init_process_group("nccl", device_id=dev, timeout=datetime.timedelta(seconds=120))
     if world != args.gpus and rank == 0:
         print(f"warning: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
     if world > 1:

@@ -211,12 +211,22 @@ def run_multi(args, world, rank, local, dev):
     dist.barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    tp = None
+    if os.environ.get("DGDS_TORCH_PROFILE"):  # debug only: a timeline of the timed steps (numbers then invalid)
+        from torch.profiler import ProfilerActivity, profile
+        tp = profile(activities=[ProfilerActivity.CPU, ProfilerActivity.CUDA])
+        tp.__enter__()
     with ClockSampler(local) as clk:
         e0.record()
         for s in range(W, W + K):
             step(s, True)
         e1.record()
         torch.cuda.synchronize()
+    if tp is not None:
+        tp.__exit__(None, None, None)
+        if rank == 0:
+            print(tp.key_averages().table(sort_by="cuda_time_total", row_limit=22), flush=True)
+            print(tp.key_averages().table(sort_by="cpu_time_total", row_limit=22), flush=True)
     dist.barrier()
     ms = torch.tensor([e0.elapsed_time(e1)], device=dev)
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
