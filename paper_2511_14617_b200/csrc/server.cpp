@@ -16,6 +16,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <memory>
 #include <mutex>
 #include <thread>
@@ -1091,10 +1092,19 @@ int dgds_route_pack(int64_t n, int32_t world, const int32_t* d_owner, const uint
   if (n < 0 || rec_words < 1) return fail(DGDS_EINVAL, "bad route_pack sizes");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int64_t ntiles = std::max<int64_t>(1, (n + 1023) / 1024);
-  void* scratch = nullptr;
-  DGDS_CUDA(cudaMallocAsync(&scratch, ntiles * world * sizeof(int64_t), st));
-  cudaError_t e = dgds::launch_route_pack(n, world, d_owner, d_records, rec_words, d_out, d_counts, d_perm, scratch, st);
-  cudaFreeAsync(scratch, st);
+  // grow-only scratch per (device, stream): calls on one stream are ordered, calls on
+  // different streams may overlap, so they never share a buffer
+  static std::mutex scratch_mu;
+  static std::map<std::pair<int, cudaStream_t>, DevBuf> scratch;
+  int dev = 0;
+  DGDS_CUDA(cudaGetDevice(&dev));
+  DevBuf* buf;
+  {
+    std::lock_guard<std::mutex> lk(scratch_mu);
+    buf = &scratch[{dev, st}];
+  }
+  if (int rc = buf->ensure(ntiles * world * sizeof(int64_t))) return rc;
+  cudaError_t e = dgds::launch_route_pack(n, world, d_owner, d_records, rec_words, d_out, d_counts, d_perm, buf->p, st);
   if (e != cudaSuccess) return fail(DGDS_ECUDA, cudaGetErrorString(e));
   return DGDS_OK;
 }
