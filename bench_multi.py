@@ -149,6 +149,25 @@ def run_multi(args, world, rank, local, dev):
         prof_host[name] = prof_host.get(name, 0.0) + t1 - t0
         return t1
 
+    # Append records of a tick are routed one tick AHEAD (side stream, double-buffered):
+    # the owner's O(records) host bookkeeping then overlaps the previous tick's GPU work.
+    meta_bufs = [meta_h, torch.empty_like(meta_h).pin_memory()]
+    ev_bufs = [ev_side, torch.cuda.Event()]
+    inflight = {}
+
+    def route_appends(s):
+        if s >= len(steps_in) or s in inflight:
+            return
+        inp = steps_in[s]
+        k = s % 2
+        side.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(side):
+            ra, st_a = router.forward(inp["app_owner"], inp["app"], capa)
+            meta_bufs[k].copy_(ra[:, :5], non_blocking=True)
+            ev_bufs[k].record(side)
+        ra.record_stream(torch.cuda.current_stream(dev))  # K1 reads the tokens on the main stream
+        inflight[s] = (ra, st_a[1], k)
+
     def step(s, stats):
         """One tick in engine order (engine.cpp:88-161): draft queries (+ verify) on the
         current index, then the appends of the tick's emitted tokens."""
@@ -156,18 +175,11 @@ def run_multi(args, world, rank, local, dev):
         inp = steps_in[s]
         main = torch.cuda.current_stream(dev)
         t0 = mark("start", time.perf_counter())
+        route_appends(s)  # normally already in flight since the previous tick
         # (1) queries -> owners (static splits, no host sync)
         rq, st_q = router.forward(inp["q_owner"], inp["q"], capq)
         t0 = mark("q_fwd", t0)
-        # (2) appends -> owners on a side stream; their metadata reaches the host while (3) runs
-        side.wait_stream(main)
-        with torch.cuda.stream(side):
-            ra, st_a = router.forward(inp["app_owner"], inp["app"], capa)
-            meta_h.copy_(ra[:, :5], non_blocking=True)
-            ev_side.record(side)
-        ra.record_stream(main)  # K1 reads the tokens on the main stream
-        t0 = mark("a_fwd", t0)
-        # (3) owner: K2 + fused K3 over the received slots (padding has handle -1)
+        # (2) owner: K2 + fused K3 over the received slots (padding has handle -1)
         hcol = rq[:, 0].contiguous()
         plen = rq[:, 1].contiguous()
         tl = rq[:, 10].contiguous()
@@ -181,23 +193,26 @@ def run_multi(args, world, rank, local, dev):
         replies = torch.cat([nc, ln, sc.view(torch.int32), sp.view(torch.int32), tk, v.t()], dim=1)
         back, ovq = router.reverse(replies, st_q)
         t0 = mark("q_rev", t0)
-        # (4) host bookkeeping of the received appends overlaps the query kernel; K1 after it
-        ev_side.synchronize()
-        meta = meta_h.numpy()
+        # (3) the tick's appends: metadata arrived during the previous tick; bookkeeping, then K1
+        ra, ova, k = inflight.pop(s)
+        ev_bufs[k].synchronize()
+        meta = meta_bufs[k].numpy()
         rows = np.nonzero(meta[:, 0] >= 0)[0]
         if len(rows):
             m = meta[rows]
             n = m[:, 4].astype(np.uint64)
             prev = m[:, 2].view(np.uint32).astype(np.uint64) | (m[:, 3].astype(np.uint64) << np.uint64(32))
             starts = rows.astype(np.uint64) * np.uint64(APP_W) + np.uint64(5)
-            main.wait_event(ev_side)
+            main.wait_event(ev_bufs[k])
             rep = srv.update_device_strided(m[:, 0].copy(), m[:, 1].copy(), prev, starts, n, ra.data_ptr(), 0.0,
                                             main.cuda_stream)
             if not rep["ok"].all():
                 raise RuntimeError("routed append out of order")
             if stats:
                 app_alg_owner[0] += append_alg_bytes(prev.astype(np.int64), n.astype(np.int64))
-        overflow = overflow | ovq | st_a[1]
+        overflow = overflow | ovq | ova
+        # (4) route the next tick's appends now, so their metadata is home by then
+        route_appends(s + 1)
         mark("append", t0)
         return back
 
@@ -248,10 +263,10 @@ def run_multi(args, world, rank, local, dev):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         d2h = 0
-        for hin in host_in:
-            for k in ("app", "app_owner", "q", "q_owner"):
-                steps_in[0][k] = hin[k].to(dev, non_blocking=True)
-            back = step(0, False).cpu()
+        base_s = len(steps_in)
+        for j, hin in enumerate(host_in):
+            steps_in.append({k: hin[k].to(dev, non_blocking=True) for k in ("app", "app_owner", "q", "q_owner")})
+            back = step(base_s + j, False).cpu()
             d2h += back.nbytes
         torch.cuda.synchronize()
         dt = torch.tensor([time.perf_counter() - t0], device=dev)
