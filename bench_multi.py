@@ -130,14 +130,14 @@ def run_multi(args, world, rank, local, dev):
     ev_side = torch.cuda.Event()
     meta_h = torch.empty((world * capa, 5), dtype=torch.int32).pin_memory()
     mq = world * capq
-    nc = torch.zeros(mq, 1, dtype=torch.int32, device=dev)
-    ln = torch.zeros(mq, kq, dtype=torch.int32, device=dev)
-    sc = torch.zeros(mq, kq, dtype=torch.float64, device=dev)
-    sp = torch.zeros(mq, kq, dtype=torch.int64, device=dev)
-    tk = torch.zeros(mq, kq * dl, dtype=torch.int32, device=dev)
-    v = torch.zeros(3, mq, dtype=torch.int32, device=dev)
-    cand = _lib.Candidates(kq, dl, nc.data_ptr(), ln.data_ptr(), sc.data_ptr(), sp.data_ptr(), tk.data_ptr())
-    vo = _lib.VerifyOut(v[0].data_ptr(), v[1].data_ptr(), v[2].data_ptr())
+    # reply record: n_cands | lens[k] | pad | scores[k] f64 | supports[k] i64 | tokens[k][dl] | verify[3] | pad
+    off_sc = 2 + kq - (kq % 2)
+    off_sp = off_sc + 2 * kq
+    off_tk = off_sp + 2 * kq
+    off_v = off_tk + kq * dl
+    rep_w = (off_v + 3 + 1) // 2 * 2
+    layout = _lib.RecordLayout(QRY_W, 0, 1, 2, 10, 11, 12, rep_w, 0, 1, off_sc, off_sp, off_tk, off_v)
+    replies = torch.zeros((mq, rep_w), dtype=torch.int32, device=dev)
     prof_host = {}
     dbg = os.environ.get("DGDS_MULTI_BREAKDOWN") == "1"
 
@@ -179,18 +179,13 @@ def run_multi(args, world, rank, local, dev):
         # (1) queries -> owners (static splits, no host sync)
         rq, st_q = router.forward(inp["q_owner"], inp["q"], capq)
         t0 = mark("q_fwd", t0)
-        # (2) owner: K2 + fused K3 over the received slots (padding has handle -1)
-        hcol = rq[:, 0].contiguous()
-        plen = rq[:, 1].contiguous()
-        tl = rq[:, 10].contiguous()
-        lim = rq[:, 11].contiguous()
-        _lib.check(L.dgds_speculate_device(
-            srv.handle, mq, C.c_void_p(hcol.data_ptr()), C.c_void_p(plen.data_ptr()),
-            C.c_void_p(rq[:, 2:].data_ptr()), QRY_W, C.c_void_p(sp_args.data_ptr()), 0, kq, dl, C.byref(cand),
-            C.c_void_p(rq[:, 12:].data_ptr()), QRY_W, C.c_void_p(tl.data_ptr()), C.c_void_p(lim.data_ptr()),
-            C.byref(vo), C.c_void_p(d_stats.data_ptr()) if stats else None, C.c_void_p(main.cuda_stream)))
+        # (2) owner: K2 + fused K3 straight from the received query records into reply records
+        _lib.check(L.dgds_speculate_records(srv.handle, mq, C.c_void_p(rq.data_ptr()), C.byref(layout),
+                                            C.c_void_p(sp_args.data_ptr()), 0, kq, dl,
+                                            C.c_void_p(replies.data_ptr()),
+                                            C.c_void_p(d_stats.data_ptr()) if stats else None,
+                                            C.c_void_p(main.cuda_stream)))
         t0 = mark("q_kernel", t0)
-        replies = torch.cat([nc, ln, sc.view(torch.int32), sp.view(torch.int32), tk, v.t()], dim=1)
         back, ovq = router.reverse(replies, st_q)
         t0 = mark("q_rev", t0)
         # (3) the tick's appends: metadata arrived during the previous tick; bookkeeping, then K1

@@ -201,6 +201,35 @@ int dgds_speculate_verify_batch(dgds_server* s, int64_t n, const int32_t* handle
                                 const int32_t* truth_next, int32_t truth_stride, const int32_t* truth_left,
                                 const int32_t* limit, dgds_candidates* out, dgds_verify_out* vout);
 
+/* Fixed-size query / reply records (e.g. traffic routed between GPUs). Offsets in 32-bit words.
+ * Query record: group handle (-1 = empty slot: answered with nothing), pattern length, the last
+ * <= rec_words - off_pattern pattern tokens, truth_left, limit, next truth tokens.
+ * Reply record: n_cands, lens[k], scores[k] (f64), supports[k] (i64), tokens[k][max_spec],
+ * drafted/accepted/emitted (off_verify < 0: no verification). 8-byte fields need even offsets and an
+ * even reply width. */
+typedef struct dgds_query_record_layout {
+  int32_t rec_words;
+  int32_t off_handle;
+  int32_t off_pat_len;
+  int32_t off_pattern;
+  int32_t off_truth_left;
+  int32_t off_limit;
+  int32_t off_truth;
+  int32_t reply_words;
+  int32_t off_n_cands;
+  int32_t off_lens;
+  int32_t off_scores;
+  int32_t off_supports;
+  int32_t off_tokens;
+  int32_t off_verify;
+} dgds_query_record_layout;
+
+/* K2 + fused K3 directly over device query records, writing device reply records (zero-copy,
+ * enqueued on `stream`). max_spec also fixes the reply's per-candidate token stride. */
+int dgds_speculate_records(dgds_server* s, int64_t n, const int32_t* d_records, const dgds_query_record_layout* layout,
+                           const dgds_spec_args* d_args, int64_t args_stride, int32_t max_top_k, int32_t max_spec,
+                           int32_t* d_replies, dgds_query_stats* d_stats, void* stream);
+
 /* Verification of existing candidates (engine.cpp:115-143), host buffers. */
 int dgds_verify_batch(dgds_server* s, int64_t n, const dgds_candidates* cands, const int32_t* truth_next,
                       int32_t truth_stride, const int32_t* truth_left, const int32_t* limit,
@@ -231,6 +260,12 @@ int dgds_profile_read(dgds_server* s, dgds_profile* out, int32_t reset);
  * d_perm[i] the destination index of record i (for the inverse scatter of replies). */
 int dgds_route_pack(int64_t n, int32_t world, const int32_t* d_owner, const uint32_t* d_records, int32_t rec_words,
                     uint32_t* d_out, int64_t* d_counts, int64_t* d_perm, void* stream);
+/* Fixed-capacity variant: d_out holds world * cap records of rec_words words, bucket o at rows
+ * [o*cap, (o+1)*cap) (empty rows are all -1); d_slot[i] = row of record i; *d_overflow set to 1
+ * when a bucket would exceed cap. No host synchronisation: split sizes are static. */
+int dgds_route_pack_padded(int64_t n, int32_t world, const int32_t* d_owner, const uint32_t* d_records,
+                           int32_t rec_words, int64_t cap, uint32_t* d_out, int64_t* d_slot, int32_t* d_overflow,
+                           void* stream);
 /* Inverse: d_out[i] = d_in[d_perm[i]] for n records of rec_words words. */
 int dgds_route_unpack(int64_t n, const uint32_t* d_in, int32_t rec_words, const int64_t* d_perm, uint32_t* d_out,
                       void* stream);

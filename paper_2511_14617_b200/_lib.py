@@ -81,6 +81,12 @@ class QueryStats(C.Structure):
     ]
 
 
+class RecordLayout(C.Structure):
+    _fields_ = [(n, C.c_int32) for n in ("rec_words", "off_handle", "off_pat_len", "off_pattern", "off_truth_left",
+                                         "off_limit", "off_truth", "reply_words", "off_n_cands", "off_lens",
+                                         "off_scores", "off_supports", "off_tokens", "off_verify")]
+
+
 class Profile(C.Structure):
     _fields_ = [("append_launches", C.c_uint64), ("query_launches", C.c_uint64), ("append_ms", C.c_double),
                 ("query_ms", C.c_double)]
@@ -151,6 +157,8 @@ EXPORTS = {
     "dgds_draft_len": (_I32, [_I32, _I32, _I32, _I32, _I32]),
     "dgds_route_pack": (C.c_int, [_I64, _I32, _P, _P, _I32, _P, _P, _P, _P]),
     "dgds_route_unpack": (C.c_int, [_I64, _P, _I32, _P, _P, _P]),
+    "dgds_route_pack_padded": (C.c_int, [_I64, _I32, _P, _P, _I32, _I64, _P, _P, _P, _P]),
+    "dgds_speculate_records": (C.c_int, [_P, _I64, _P, C.POINTER(RecordLayout), _P, _I64, _I32, _I32, _P, _P, _P]),
     "dgds_generate_workload": (C.c_int, [C.POINTER(WorkloadCfg), _P, _P, _P]),
 }
 

@@ -365,12 +365,13 @@ __global__ void __launch_bounds__(kBlock, 4) k_query(QueryLaunch P) {
   const DevTrie& T = P.T;
 
   const dgds_spec_args a = P.args[qi * P.args_stride];
-  const int32_t hdl = P.handles[qi];
-  const int plen = P.pat_len[qi];
+  const int64_t qin = qi * P.in_qstride;  // per-query scalars: SoA (stride 1) or routed records
+  const int32_t hdl = P.handles[qin];
+  const int plen = P.pat_len[qin];
   int32_t tleft = 0, lim = 0;
   if (P.v_emitted) {
-    tleft = P.truth_left[qi];
-    lim = P.limit[qi];
+    tleft = P.truth_left[qin];
+    lim = P.limit[qin];
   }
   const uint32_t root = (valid && hdl >= 0 && hdl < P.n_handles) ? P.root_of[hdl] : 0u;
   const int eff_pmax = min(a.pattern_lookup_max, T.lim_pattern);  // cst.cpp:156-158
@@ -788,13 +789,12 @@ __global__ void __launch_bounds__(kBlock, 4) k_query(QueryLaunch P) {
                      : 0;
   }
   if (P.n_cands && valid) {
-    if (gl == 0) P.n_cands[q] = nf;
+    if (gl == 0) P.n_cands[q * P.out_qstride] = nf;
     if (gl < nf) {
-      const int64_t o = q * P.k_stride + my_rank;
-      P.lens[o] = sm.f.len[gl];
-      P.scores[o] = sm.f.score[gl];
-      P.supports[o] = sm.f.sup[gl];
-      int32_t* dst = P.tokens + o * P.s_stride;
+      P.lens[q * P.out_qstride + my_rank] = sm.f.len[gl];
+      P.scores[q * P.out_qstride8 + my_rank] = sm.f.score[gl];
+      P.supports[q * P.out_qstride8 + my_rank] = sm.f.sup[gl];
+      int32_t* dst = P.tokens + q * P.tok_qstride + static_cast<int64_t>(my_rank) * P.s_stride;
       for (int i = 0; i < sm.f.len[gl]; ++i) dst[i] = sm.f.tok[gl][i];
     }
   }
@@ -820,9 +820,9 @@ __global__ void __launch_bounds__(kBlock, 4) k_query(QueryLaunch P) {
     match = tile.max(match);
     if (valid && gl == 0) {
       const int emitted = min(match + 1, lim);
-      P.v_drafted[q] = drafted;
-      P.v_accepted[q] = emitted - 1;
-      P.v_emitted[q] = emitted;
+      P.v_drafted[q * P.v_qstride] = drafted;
+      P.v_accepted[q * P.v_qstride] = emitted - 1;
+      P.v_emitted[q * P.v_qstride] = emitted;
     }
   }
 
@@ -1007,6 +1007,50 @@ __global__ void k_route_scatter(int64_t n, int32_t world, const int32_t* __restr
   }
 }
 
+// padded mode: exclusive scan of tile counts restarted for every owner (position inside its bucket)
+__global__ void k_route_scan_local(int32_t world, int64_t ntiles, int64_t* tile_counts) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  for (int o = 0; o < world; ++o) {
+    int64_t run = 0;
+    for (int64_t t = 0; t < ntiles; ++t) {
+      const int64_t v = tile_counts[o * ntiles + t];
+      tile_counts[o * ntiles + t] = run;
+      run += v;
+    }
+  }
+}
+
+__global__ void k_route_scatter_padded(int64_t n, int32_t world, const int32_t* __restrict__ owner,
+                                       const uint32_t* __restrict__ rec, int32_t rw, int64_t cap,
+                                       const int64_t* __restrict__ tile_off, uint32_t* out, int64_t* slot,
+                                       int32_t* overflow) {
+  __shared__ int warp_cnt[kRouteTile / kWarp][8];
+  const int64_t ntiles = gridDim.x;
+  const int64_t t0 = static_cast<int64_t>(blockIdx.x) * kRouteTile;
+  const int warp = threadIdx.x / kWarp, lane = lane_id();
+  const int64_t i = t0 + threadIdx.x;
+  const int o = (i < n) ? owner[i] : -1;
+  int my_rank_in_warp = 0;
+  for (int w = 0; w < world; ++w) {
+    const unsigned m = __ballot_sync(kFull, o == w);
+    if (o == w) my_rank_in_warp = __popc(m & ((1u << lane) - 1u));
+    if (lane == 0) warp_cnt[warp][w] = __popc(m);
+  }
+  __syncthreads();
+  if (o >= 0) {
+    int64_t pos = tile_off[o * ntiles + blockIdx.x];
+    for (int w2 = 0; w2 < warp; ++w2) pos += warp_cnt[w2][o];
+    pos += my_rank_in_warp;
+    if (pos >= cap) {
+      atomicExch(overflow, 1);
+      pos = cap - 1;  // results are invalid; the flag says so
+    }
+    const int64_t row = o * cap + pos;
+    for (int k = 0; k < rw; ++k) out[row * rw + k] = rec[i * rw + k];
+    slot[i] = row;
+  }
+}
+
 __global__ void k_route_gather(int64_t n, const uint32_t* __restrict__ in, int32_t rw, const int64_t* __restrict__ perm,
                                uint32_t* out) {
   const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -1094,6 +1138,22 @@ cudaError_t launch_route_pack(int64_t n, int32_t world, const int32_t* owner, co
   if (n > 0)
     k_route_scatter<<<static_cast<unsigned>(ntiles), kRouteTile, 0, st>>>(n, world, owner, records, rec_words,
                                                                             tile_counts, out, perm);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_route_pack_padded(int64_t n, int32_t world, const int32_t* owner, const uint32_t* records,
+                                     int32_t rec_words, int64_t cap, uint32_t* out, int64_t* slot, int32_t* overflow,
+                                     void* scratch, cudaStream_t st) {
+  if (world > 8) return cudaErrorInvalidValue;
+  cudaError_t e = cudaMemsetAsync(out, 0xFF, static_cast<size_t>(world) * cap * rec_words * 4, st);
+  if (e != cudaSuccess || n <= 0) return e;
+  const int64_t ntiles = (n + kRouteTile - 1) / kRouteTile;
+  int64_t* tile_counts = static_cast<int64_t*>(scratch);
+  k_route_count<<<static_cast<unsigned>(ntiles), 256, world * sizeof(int), st>>>(n, world, owner, tile_counts);
+  k_route_scan_local<<<1, 1, 0, st>>>(world, ntiles, tile_counts);
+  k_route_scatter_padded<<<static_cast<unsigned>(ntiles), kRouteTile, 0, st>>>(n, world, owner, records, rec_words,
+                                                                                 cap, tile_counts, out, slot,
+                                                                                 overflow);
   return cudaGetLastError();
 }
 

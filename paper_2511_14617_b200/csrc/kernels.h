@@ -60,7 +60,23 @@ struct QueryLaunch {
   dgds_query_stats* stats;
   int32_t* err_flag;  // set to 1 by any query with invalid args (device API)
   long long* dbg;     // optional per-query phase timing [n][8] (debug)
+  // Per-query strides (elements). SoA buffers: in_qstride 1, out_qstride = out_qstride8 = k_stride,
+  // tok_qstride = k_stride * s_stride, v_qstride 1. Routed records: all = the record width.
+  int64_t in_qstride;   // handles, pat_len, truth_left, limit
+  int64_t out_qstride;  // n_cands, lens (int32 units)
+  int64_t out_qstride8; // scores, supports (8-byte units)
+  int64_t tok_qstride;  // tokens (int32 units; candidate c at + c * s_stride)
+  int64_t v_qstride;    // drafted / accepted / emitted
 };
+
+// SoA strides for a QueryLaunch whose outputs are [n][k_stride][s_stride] buffers.
+inline void soa_strides(QueryLaunch& L) {
+  L.in_qstride = 1;
+  L.out_qstride = L.k_stride;
+  L.out_qstride8 = L.k_stride;
+  L.tok_qstride = static_cast<int64_t>(L.k_stride) * L.s_stride;
+  L.v_qstride = 1;
+}
 
 // max_k selects the tile width (4, 8 or 32 lanes per request); max_s bounds
 // min(max_spec_tokens, max_spec_len) over the batch (per-path token registers).
@@ -98,6 +114,9 @@ cudaError_t launch_compact(int64_t n, int32_t K, int32_t S, const int32_t* n_can
 cudaError_t launch_route_pack(int64_t n, int32_t world, const int32_t* owner, const uint32_t* records,
                               int32_t rec_words, uint32_t* out, int64_t* counts, int64_t* perm, void* scratch,
                               cudaStream_t st);
+cudaError_t launch_route_pack_padded(int64_t n, int32_t world, const int32_t* owner, const uint32_t* records,
+                                     int32_t rec_words, int64_t cap, uint32_t* out, int64_t* slot, int32_t* overflow,
+                                     void* scratch, cudaStream_t st);
 cudaError_t launch_route_unpack(int64_t n, const uint32_t* in, int32_t rec_words, const int64_t* perm, uint32_t* out,
                                 cudaStream_t st);
 

@@ -837,6 +837,7 @@ int dgds_speculate_verify_batch(dgds_server* s, int64_t n, const int32_t* handle
   L.args_stride = args_stride ? 1 : 0;
   L.k_stride = K;
   L.s_stride = Sx;
+  dgds::soa_strides(L);
   L.scores = reinterpret_cast<double*>(dout + o_sc);
   L.supports = reinterpret_cast<int64_t*>(dout + o_sp);
   L.n_cands = reinterpret_cast<int32_t*>(dout + o_nc);
@@ -968,12 +969,15 @@ int dgds_speculate_device(dgds_server* s, int64_t n, const int32_t* d_handles, c
   if (d_out) {
     L.k_stride = d_out->k_stride;
     L.s_stride = d_out->s_stride;
+    dgds::soa_strides(L);
     L.n_cands = d_out->n_cands;
     L.lens = d_out->lens;
     L.scores = d_out->scores;
     L.supports = d_out->supports;
     L.tokens = d_out->tokens;
   }
+  L.in_qstride = 1;
+  L.v_qstride = 1;
   if (d_vout) {
     L.truth = d_truth;
     L.truth_stride = truth_stride;
@@ -982,6 +986,64 @@ int dgds_speculate_device(dgds_server* s, int64_t n, const int32_t* d_handles, c
     L.v_drafted = d_vout->drafted;
     L.v_accepted = d_vout->accepted;
     L.v_emitted = d_vout->emitted;
+  }
+  L.stats = d_stats;
+  L.err_flag = s->d_err;
+  L.dbg = s->d_dbg;
+  {
+    LaunchTimer lt(s, 1, join.stream());
+    DGDS_CUDA(dgds::launch_query(L, max_top_k, max_spec, join.stream()));
+  }
+  return DGDS_OK;
+}
+
+int dgds_speculate_records(dgds_server* s, int64_t n, const int32_t* d_records, const dgds_query_record_layout* lay,
+                           const dgds_spec_args* d_args, int64_t args_stride, int32_t max_top_k, int32_t max_spec,
+                           int32_t* d_replies, dgds_query_stats* d_stats, void* stream) {
+  if (n < 0) return fail(DGDS_EINVAL, "negative batch size");
+  if (n == 0) return DGDS_OK;
+  if (!lay || !d_records || !d_replies) return fail(DGDS_EINVAL, "null argument");
+  if (max_top_k < 1 || max_top_k > DGDS_MAX_TOP_K) return fail(DGDS_EUNSUPPORTED, "max_top_k out of range");
+  if (max_spec <= 0 || max_spec > s->p.max_spec_len) max_spec = std::max(1, s->p.max_spec_len);
+  const dgds_query_record_layout& y = *lay;
+  if (y.rec_words < 1 || y.reply_words < 1 || (y.reply_words & 1) || (y.off_scores & 1) || (y.off_supports & 1))
+    return fail(DGDS_EINVAL, "bad record layout (reply words and 8-byte fields must be even)");
+  if (y.rec_words - y.off_pattern < s->p.max_pattern_len)
+    return fail(DGDS_EINVAL, "query record pattern field shorter than max_pattern_len");
+  std::lock_guard<std::mutex> lk(s->mu);
+  DGDS_CUDA(cudaSetDevice(s->p.device));
+  StreamJoin join(s, stream);
+  dgds::QueryLaunch L{};
+  L.T = s->T;
+  L.root_of = s->d_root_of;
+  L.n_handles = static_cast<int32_t>(s->root_of_cap);
+  L.n = n;
+  L.handles = d_records + y.off_handle;
+  L.pat_len = d_records + y.off_pat_len;
+  L.patterns = d_records + y.off_pattern;
+  L.pat_stride = y.rec_words;
+  L.args = d_args;
+  L.args_stride = args_stride;
+  L.k_stride = max_top_k;
+  L.s_stride = max_spec;
+  L.in_qstride = y.rec_words;
+  L.n_cands = d_replies + y.off_n_cands;
+  L.lens = d_replies + y.off_lens;
+  L.scores = reinterpret_cast<double*>(d_replies + y.off_scores);
+  L.supports = reinterpret_cast<int64_t*>(d_replies + y.off_supports);
+  L.tokens = d_replies + y.off_tokens;
+  L.out_qstride = y.reply_words;
+  L.out_qstride8 = y.reply_words / 2;
+  L.tok_qstride = y.reply_words;
+  L.v_qstride = y.reply_words;
+  if (y.off_verify >= 0) {
+    L.truth = d_records + y.off_truth;
+    L.truth_stride = y.rec_words;
+    L.truth_left = d_records + y.off_truth_left;
+    L.limit = d_records + y.off_limit;
+    L.v_drafted = d_replies + y.off_verify;
+    L.v_accepted = d_replies + y.off_verify + 1;
+    L.v_emitted = d_replies + y.off_verify + 2;
   }
   L.stats = d_stats;
   L.err_flag = s->d_err;
@@ -1086,25 +1148,34 @@ int dgds_profile_read(dgds_server* s, dgds_profile* out, int32_t reset) {
   return DGDS_OK;
 }
 
+static DevBuf* route_scratch(cudaStream_t st, size_t bytes, int* rc);
+
 int dgds_route_pack(int64_t n, int32_t world, const int32_t* d_owner, const uint32_t* d_records, int32_t rec_words,
                     uint32_t* d_out, int64_t* d_counts, int64_t* d_perm, void* stream) {
   if (world < 1 || world > 8) return fail(DGDS_EUNSUPPORTED, "route_pack supports 1..8 ranks");
   if (n < 0 || rec_words < 1) return fail(DGDS_EINVAL, "bad route_pack sizes");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int64_t ntiles = std::max<int64_t>(1, (n + 1023) / 1024);
-  // grow-only scratch per (device, stream): calls on one stream are ordered, calls on
-  // different streams may overlap, so they never share a buffer
-  static std::mutex scratch_mu;
-  static std::map<std::pair<int, cudaStream_t>, DevBuf> scratch;
-  int dev = 0;
-  DGDS_CUDA(cudaGetDevice(&dev));
-  DevBuf* buf;
-  {
-    std::lock_guard<std::mutex> lk(scratch_mu);
-    buf = &scratch[{dev, st}];
-  }
-  if (int rc = buf->ensure(ntiles * world * sizeof(int64_t))) return rc;
+  int rc = 0;
+  DevBuf* buf = route_scratch(st, ntiles * world * sizeof(int64_t), &rc);
+  if (rc) return rc;
   cudaError_t e = dgds::launch_route_pack(n, world, d_owner, d_records, rec_words, d_out, d_counts, d_perm, buf->p, st);
+  if (e != cudaSuccess) return fail(DGDS_ECUDA, cudaGetErrorString(e));
+  return DGDS_OK;
+}
+
+int dgds_route_pack_padded(int64_t n, int32_t world, const int32_t* d_owner, const uint32_t* d_records,
+                           int32_t rec_words, int64_t cap, uint32_t* d_out, int64_t* d_slot, int32_t* d_overflow,
+                           void* stream) {
+  if (world < 1 || world > 8) return fail(DGDS_EUNSUPPORTED, "route_pack supports 1..8 ranks");
+  if (n < 0 || rec_words < 1 || cap < 1) return fail(DGDS_EINVAL, "bad route_pack sizes");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int64_t ntiles = std::max<int64_t>(1, (n + 1023) / 1024);
+  int rc = 0;
+  DevBuf* buf = route_scratch(st, ntiles * world * sizeof(int64_t), &rc);
+  if (rc) return rc;
+  cudaError_t e = dgds::launch_route_pack_padded(n, world, d_owner, d_records, rec_words, cap, d_out, d_slot,
+                                                 d_overflow, buf->p, st);
   if (e != cudaSuccess) return fail(DGDS_ECUDA, cudaGetErrorString(e));
   return DGDS_OK;
 }
@@ -1116,3 +1187,19 @@ int dgds_route_unpack(int64_t n, const uint32_t* d_in, int32_t rec_words, const 
 }
 
 }  // extern "C"
+
+// Grow-only routing scratch per (device, stream): calls on one stream are ordered,
+// calls on different streams may overlap, so they never share a buffer.
+static DevBuf* route_scratch(cudaStream_t st, size_t bytes, int* rc) {
+  static std::mutex scratch_mu;
+  static std::map<std::pair<int, cudaStream_t>, DevBuf> scratch;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  DevBuf* buf;
+  {
+    std::lock_guard<std::mutex> lk(scratch_mu);
+    buf = &scratch[{dev, st}];
+  }
+  *rc = buf->ensure(bytes);
+  return buf;
+}

@@ -74,29 +74,43 @@ class Router:
         return self.unpack(back, perm)
 
 
-class PaddedRouter(Router):
-    """Fixed-capacity exchange: every rank sends `cap` slots to every rank, so the
-    split sizes are static and no host synchronisation is needed. Empty slots
-    carry -1 in column 0 (an invalid group handle: the query kernel answers it
-    with nothing, the append path skips it). Overflow (> cap records for one
-    owner) is reported as a device flag."""
+def cuda_pack_padded(owner: torch.Tensor, records: torch.Tensor, world: int, cap: int):
+    """Stable bucketing straight into the fixed-capacity send layout (k_route_*_padded):
+    returns ([world*cap, w] with empty rows = -1, slot row of each record, overflow flag)."""
+    n, w = records.shape
+    out = torch.empty((world * cap, w), dtype=records.dtype, device=records.device)
+    slot = torch.empty(n, dtype=torch.int64, device=records.device)
+    overflow = torch.zeros(1, dtype=torch.int32, device=records.device)
+    stream = torch.cuda.current_stream(records.device).cuda_stream
+    _lib.check(_lib.lib().dgds_route_pack_padded(n, world, C.c_void_p(owner.data_ptr()),
+                                                 C.c_void_p(records.data_ptr()), w, cap, C.c_void_p(out.data_ptr()),
+                                                 C.c_void_p(slot.data_ptr()), C.c_void_p(overflow.data_ptr()),
+                                                 C.c_void_p(stream)))
+    return out, slot, overflow
+
+
+class PaddedRouter:
+    """Fixed-capacity exchange: every rank sends `cap` rows to every rank, so the
+    split sizes are static and no host synchronisation is needed. Empty rows are
+    -1 (an invalid group handle: the query kernel answers it with nothing, the
+    append path skips it). Overflow (> cap records for one owner) is reported as
+    a device flag."""
+
+    def __init__(self, world: int, group=None, pack_padded: Optional[Callable] = None,
+                 unpack: Optional[Callable] = None):
+        self.world = world
+        self.group = group
+        self.pack_padded = pack_padded or cuda_pack_padded
+        self.unpack = unpack or cuda_unpack
 
     def forward(self, owner: torch.Tensor, records: torch.Tensor, cap: int):
-        _, counts, perm = self.pack(owner, records, self.world)
-        own = owner.long()
-        starts = torch.cumsum(counts, 0) - counts
-        r = perm - starts[own]
-        overflow = (r >= cap).any()
-        idx = own * cap + r.clamp(max=cap - 1)
-        send = records.new_zeros((self.world * cap, records.shape[1]))
-        send[:, 0] = -1
-        send.index_copy_(0, idx, records)
+        send, slot, overflow = self.pack_padded(owner, records, self.world, cap)
         recv = torch.empty_like(send)
         dist.all_to_all_single(recv, send, group=self.group)
-        return recv, (idx, overflow)
+        return recv, (slot, overflow)
 
     def reverse(self, replies: torch.Tensor, state):
-        idx, overflow = state
+        slot, overflow = state
         back = torch.empty_like(replies)
         dist.all_to_all_single(back, replies.contiguous(), group=self.group)
-        return back[idx], overflow
+        return self.unpack(back, slot), overflow

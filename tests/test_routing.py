@@ -23,6 +23,21 @@ def host_unpack(packed, perm):
     return packed[perm]
 
 
+def host_pack_padded(owner, records, world, cap):
+    own = owner.long()
+    order = torch.sort(own, stable=True).indices
+    counts = torch.bincount(own, minlength=world)
+    starts = torch.cumsum(counts, 0) - counts
+    pos = torch.empty_like(order)
+    pos[order] = torch.arange(len(order))
+    r = pos - starts[own]
+    overflow = (r >= cap).any().to(torch.int32).reshape(1)
+    slot = own * cap + r.clamp(max=cap - 1)
+    out = torch.full((world * cap, records.shape[1]), -1, dtype=records.dtype)
+    out[slot] = records
+    return out, slot, overflow
+
+
 def _free_port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
@@ -62,7 +77,7 @@ def _worker(rank, world, port, q):
         assert total.item() == ns.item()
         # fixed-capacity variant (static splits, no host sync)
         from paper_2511_14617_b200.routing import PaddedRouter
-        pr = PaddedRouter(world, pack=host_pack, unpack=host_unpack)
+        pr = PaddedRouter(world, pack_padded=host_pack_padded, unpack=host_unpack)
         cap = 64
         got2, st2 = pr.forward(owner, rec, cap)
         valid = got2[got2[:, 0] >= 0]
