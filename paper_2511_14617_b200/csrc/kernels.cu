@@ -789,7 +789,7 @@ __global__ void __launch_bounds__(kBlock, 4) k_query(QueryLaunch P) {
                      : 0;
   }
   if (P.n_cands && valid) {
-    if (gl == 0) P.n_cands[q * P.out_qstride] = nf;
+    if (gl == 0) P.n_cands[q * P.nc_qstride] = nf;
     if (gl < nf) {
       P.lens[q * P.out_qstride + my_rank] = sm.f.len[gl];
       P.scores[q * P.out_qstride8 + my_rank] = sm.f.score[gl];

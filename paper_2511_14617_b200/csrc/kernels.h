@@ -63,7 +63,8 @@ struct QueryLaunch {
   // Per-query strides (elements). SoA buffers: in_qstride 1, out_qstride = out_qstride8 = k_stride,
   // tok_qstride = k_stride * s_stride, v_qstride 1. Routed records: all = the record width.
   int64_t in_qstride;   // handles, pat_len, truth_left, limit
-  int64_t out_qstride;  // n_cands, lens (int32 units)
+  int64_t nc_qstride;   // n_cands
+  int64_t out_qstride;  // lens (int32 units)
   int64_t out_qstride8; // scores, supports (8-byte units)
   int64_t tok_qstride;  // tokens (int32 units; candidate c at + c * s_stride)
   int64_t v_qstride;    // drafted / accepted / emitted
@@ -72,6 +73,7 @@ struct QueryLaunch {
 // SoA strides for a QueryLaunch whose outputs are [n][k_stride][s_stride] buffers.
 inline void soa_strides(QueryLaunch& L) {
   L.in_qstride = 1;
+  L.nc_qstride = 1;
   L.out_qstride = L.k_stride;
   L.out_qstride8 = L.k_stride;
   L.tok_qstride = static_cast<int64_t>(L.k_stride) * L.s_stride;

@@ -1032,6 +1032,7 @@ int dgds_speculate_records(dgds_server* s, int64_t n, const int32_t* d_records, 
   L.scores = reinterpret_cast<double*>(d_replies + y.off_scores);
   L.supports = reinterpret_cast<int64_t*>(d_replies + y.off_supports);
   L.tokens = d_replies + y.off_tokens;
+  L.nc_qstride = y.reply_words;
   L.out_qstride = y.reply_words;
   L.out_qstride8 = y.reply_words / 2;
   L.tok_qstride = y.reply_words;

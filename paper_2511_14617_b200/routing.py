@@ -37,9 +37,9 @@ def cuda_pack(owner: torch.Tensor, records: torch.Tensor, world: int) -> Tuple[t
 
 
 def cuda_unpack(packed: torch.Tensor, perm: torch.Tensor) -> torch.Tensor:
-    """out[i] = packed[perm[i]] on the GPU (k_route_gather)."""
-    n, w = packed.shape
-    out = torch.empty_like(packed)
+    """out[i] = packed[perm[i]] for i < len(perm), on the GPU (k_route_gather)."""
+    n, w = perm.shape[0], packed.shape[1]
+    out = torch.empty((n, w), dtype=packed.dtype, device=packed.device)
     stream = torch.cuda.current_stream(packed.device).cuda_stream
     _lib.check(_lib.lib().dgds_route_unpack(n, C.c_void_p(packed.data_ptr()), w, C.c_void_p(perm.data_ptr()),
                                             C.c_void_p(out.data_ptr()), C.c_void_p(stream)))
