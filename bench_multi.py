@@ -29,7 +29,8 @@ def run_multi(args, world, rank, local, dev):
     from bench import CONFIG_NAMES, RANDOM_CEILING_GBS, ClockSampler, append_alg_bytes, peaks
     from paper_2511_14617_b200 import _lib
     from paper_2511_14617_b200.dgds import DgdsParams, DraftServer, SpeculationArgs, args_array, shard_of_group
-    from paper_2511_14617_b200.routing import PaddedRouter
+    from paper_2511_14617_b200.peer import PeerExchange, speculate_routed
+    from paper_2511_14617_b200.routing import PaddedRouter, cuda_unpack
     from paper_2511_14617_b200.workload import CONFIGS, generate_workload, group_id
 
     base = CONFIGS[args.config]
@@ -152,15 +153,44 @@ def run_multi(args, world, rank, local, dev):
     # Append records of a tick are routed one tick AHEAD (side stream, double-buffered):
     # the owner's O(records) host bookkeeping then overlaps the previous tick's GPU work.
     meta_bufs = [meta_h, torch.empty_like(meta_h).pin_memory()]
+    cnt_bufs = [torch.zeros(world, dtype=torch.int32).pin_memory() for _ in range(2)]
     ev_bufs = [ev_side, torch.cuda.Event()]
+    ev_rep = [torch.cuda.Event(), torch.cuda.Event()]
     inflight = {}
+    use_px = args.route == "px"
+    if use_px:
+        # NVLink peer-memory exchange: q rows -> owners, replies -> senders, append rows -> owners
+        px = PeerExchange(world, rank, local, {"q": (capq, QRY_W), "rep": (capq, rep_w), "a": (capa, APP_W)})
+        q_slot = [torch.empty(Q, dtype=torch.int64, device=dev) for _ in range(2)]
+        a_slot = [torch.empty(max(1, len(produced)), dtype=torch.int64, device=dev) for _ in range(2)]
+        rep_view = {p: px.slab("rep", p) for p in (1, 2)}  # parity 1, 0
+        a_meta = {p: px.slab("a", p)[:, :5] for p in (1, 2)}
+        a_cnt = {p: px.counts("a", p) for p in (1, 2)}
 
     def route_appends(s):
         if s >= len(steps_in) or s in inflight:
             return
         inp = steps_in[s]
         k = s % 2
-        side.wait_stream(torch.cuda.current_stream(dev))
+        if "ready" in inp:  # e2e: the inputs were copied in on the main stream
+            side.wait_event(inp["ready"])
+        if use_px:
+            seq, par = s + 1, 2 - (s + 1) % 2
+            with torch.cuda.stream(side):
+                # this parity was last read by the owners' K1 of tick s-2; their replies of tick s-1
+                # (queued after that K1 on their streams) prove it is free
+                if s > 0:
+                    side.wait_event(ev_rep[(s - 1) % 2])
+                n_a = inp["app"].shape[0]
+                px.send("a", inp["app_owner"], inp["app"], seq, stable=True, slot=a_slot[k][:n_a], stream=side)
+                px.wait("a", seq, stream=side)
+                meta_bufs[k].copy_(a_meta[par], non_blocking=True)
+                cnt_bufs[k].copy_(a_cnt[par], non_blocking=True)
+                ev_bufs[k].record(side)
+            inflight[s] = (None, None, k)
+            return
+        # step inputs are resident before the timed region, so the side stream needs no
+        # dependency on the main stream: the next tick's exchange can run under this tick's kernels
         with torch.cuda.stream(side):
             ra, st_a = router.forward(inp["app_owner"], inp["app"], capa)
             meta_bufs[k].copy_(ra[:, :5], non_blocking=True)
@@ -176,36 +206,56 @@ def run_multi(args, world, rank, local, dev):
         main = torch.cuda.current_stream(dev)
         t0 = mark("start", time.perf_counter())
         route_appends(s)  # normally already in flight since the previous tick
-        # (1) queries -> owners (static splits, no host sync)
-        rq, st_q = router.forward(inp["q_owner"], inp["q"], capq)
-        t0 = mark("q_fwd", t0)
-        # (2) owner: K2 + fused K3 straight from the received query records into reply records
-        _lib.check(L.dgds_speculate_records(srv.handle, mq, C.c_void_p(rq.data_ptr()), C.byref(layout),
-                                            C.c_void_p(sp_args.data_ptr()), 0, kq, dl,
-                                            C.c_void_p(replies.data_ptr()),
-                                            C.c_void_p(d_stats.data_ptr()) if stats else None,
-                                            C.c_void_p(main.cuda_stream)))
-        t0 = mark("q_kernel", t0)
-        back, ovq = router.reverse(replies, st_q)
-        t0 = mark("q_rev", t0)
+        seq, k = s + 1, s % 2
+        if use_px:
+            # (1)+(2) queries stored into the owners' slabs; the owner's K2+K3 stores each reply
+            # straight into its sender's reply slab; (3) gather into query order
+            px.send("q", inp["q_owner"], inp["q"], seq, slot=q_slot[k], stream=main)
+            t0 = mark("q_fwd", t0)
+            speculate_routed(srv, px, "q", "rep", seq, layout, sp_args, kq, dl, d_stats if stats else None, main)
+            t0 = mark("q_kernel", t0)
+            px.wait("rep", seq, stream=main)
+            back = cuda_unpack(rep_view[2 - seq % 2], q_slot[k])
+            ev_rep[k].record(main)
+            t0 = mark("q_rev", t0)
+        else:
+            # (1) queries -> owners (static splits, no host sync)
+            rq, st_q = router.forward(inp["q_owner"], inp["q"], capq)
+            t0 = mark("q_fwd", t0)
+            # (2) owner: K2 + fused K3 straight from the received query records into reply records
+            _lib.check(L.dgds_speculate_records(srv.handle, mq, C.c_void_p(rq.data_ptr()), C.byref(layout),
+                                                C.c_void_p(sp_args.data_ptr()), 0, kq, dl,
+                                                C.c_void_p(replies.data_ptr()),
+                                                C.c_void_p(d_stats.data_ptr()) if stats else None,
+                                                C.c_void_p(main.cuda_stream)))
+            t0 = mark("q_kernel", t0)
+            back, ovq = router.reverse(replies, st_q)
+            t0 = mark("q_rev", t0)
         # (3) the tick's appends: metadata arrived during the previous tick; bookkeeping, then K1
         ra, ova, k = inflight.pop(s)
         ev_bufs[k].synchronize()
         meta = meta_bufs[k].numpy()
-        rows = np.nonzero(meta[:, 0] >= 0)[0]
+        if use_px:
+            cnt = cnt_bufs[k].numpy()
+            rows = np.concatenate([np.arange(o * capa, o * capa + int(cnt[o]), dtype=np.int64) for o in range(world)])
+            base_ptr = px.slab_ptr("a", seq)
+        else:
+            rows = np.nonzero(meta[:, 0] >= 0)[0]
+            base_ptr = ra.data_ptr()
         if len(rows):
             m = meta[rows]
             n = m[:, 4].astype(np.uint64)
             prev = m[:, 2].view(np.uint32).astype(np.uint64) | (m[:, 3].astype(np.uint64) << np.uint64(32))
             starts = rows.astype(np.uint64) * np.uint64(APP_W) + np.uint64(5)
             main.wait_event(ev_bufs[k])
-            rep = srv.update_device_strided(m[:, 0].copy(), m[:, 1].copy(), prev, starts, n, ra.data_ptr(), 0.0,
+            rep = srv.update_device_strided(m[:, 0].copy(), m[:, 1].copy(), prev, starts, n, base_ptr, 0.0,
                                             main.cuda_stream)
             if not rep["ok"].all():
                 raise RuntimeError("routed append out of order")
             if stats:
                 app_alg_owner[0] += append_alg_bytes(prev.astype(np.int64), n.astype(np.int64))
-        overflow = overflow | ovq | ova
+        if not use_px:
+            overflow = overflow | ovq | ova
         # (4) route the next tick's appends now, so their metadata is home by then
         route_appends(s + 1)
         mark("append", t0)
@@ -218,6 +268,7 @@ def run_multi(args, world, rank, local, dev):
     _lib.check(L.dgds_profile_enable(srv.handle, 1))
     _lib.check(L.dgds_profile_read(srv.handle, C.byref(prof), 1))
     d_stats.zero_()
+    px_l0 = px.status()[1] if use_px else 0
     dist.barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -242,9 +293,13 @@ def run_multi(args, world, rank, local, dev):
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
     T = ms.item() / 1e3
     _lib.check(L.dgds_profile_read(srv.handle, C.byref(prof), 1))
+    # our launches in the timed region: K1 + K2/K3 (server profile), plus the routing kernels —
+    # px send/wait/signal (counted by the exchange) and one gather per step
+    route_launches = (px.status()[1] - px_l0 + K) if use_px else 0
     tot = torch.tensor([sum(steps_in[s]["ntok"] for s in range(W, W + K)), int(d_stats[7].item()),
                         app_alg_owner[0], prof.query_ms * 1e3, prof.append_ms * 1e3,
-                        prof.query_launches + prof.append_launches], dtype=torch.float64, device=dev)
+                        prof.query_launches + prof.append_launches + route_launches], dtype=torch.float64,
+                       device=dev)
     dist.all_reduce(tot)
     ntok_all, q_alg_all, a_alg_all, qus_all, aus_all, launches_all = tot.tolist()
 
@@ -260,7 +315,10 @@ def run_multi(args, world, rank, local, dev):
         d2h = 0
         base_s = len(steps_in)
         for j, hin in enumerate(host_in):
-            steps_in.append({k: hin[k].to(dev, non_blocking=True) for k in ("app", "app_owner", "q", "q_owner")})
+            d_in = {k: hin[k].to(dev, non_blocking=True) for k in ("app", "app_owner", "q", "q_owner")}
+            d_in["ready"] = torch.cuda.Event()
+            d_in["ready"].record(torch.cuda.current_stream(dev))
+            steps_in.append(d_in)
             back = step(base_s + j, False).cpu()
             d2h += back.nbytes
         torch.cuda.synchronize()
@@ -272,6 +330,11 @@ def run_multi(args, world, rank, local, dev):
 
     if dbg:
         print(f"rank {rank} breakdown (s, all steps):", {k: round(v, 4) for k, v in prof_host.items()}, flush=True)
+    if use_px:
+        timed_out, _ = px.status()
+        if timed_out:
+            raise RuntimeError("peer exchange wait timed out: results of this run are invalid")
+        overflow = px.overflow.bool()
     if bool(overflow.item()):
         raise RuntimeError("routing capacity overflow: results of this run are invalid")
     if rank == 0:
@@ -291,7 +354,10 @@ def run_multi(args, world, rank, local, dev):
             "config": {"workload": f"{args.config}: {CONFIG_NAMES[args.config]} (group set replicated x{world})",
                        "queries_per_step": world * Q, "queries_per_rank": Q, "record_tokens": rt, "top_k": kq,
                        "draft_len": dl, "prefill": args.prefill, "groups": G,
-                       "routing": "fnv1a64(gid) % N owner; NCCL all_to_all_single (counts, payload, replies)",
+                       "routing": ("fnv1a64(gid) % N owner; NVLink peer-memory exchange: k_px_send stores rows "
+                                   "into the owner's slab, K2+K3 stores replies into the sender's slab (no collectives)"
+                                   if use_px else
+                                   "fnv1a64(gid) % N owner; NCCL all_to_all_single (counts, payload, replies)"),
                        "l2": "inputs larger than L2 (per-GPU index ~ the N=1 index)",
                        "parallelism": f"group-sharded dp{world}"},
             "roofline": roof("k_query (K2+K3)", q_ach, q_alg_all, qus_all, K * world) if dom_q else roof(
@@ -301,6 +367,10 @@ def run_multi(args, world, rank, local, dev):
             "cpu_baseline": None, "e2e": e2e, "gpu_launches": int(launches_all), "clocks": clk.summary(),
         }
         print(json.dumps(line))
+    dist.barrier()
+    torch.cuda.synchronize()
+    if use_px:
+        px.close()  # every rank is past its last exchange (barrier above)
     srv.close()
     dist.barrier()
     dist.destroy_process_group()

@@ -230,6 +230,15 @@ int dgds_speculate_records(dgds_server* s, int64_t n, const int32_t* d_records, 
                            const dgds_spec_args* d_args, int64_t args_stride, int32_t max_top_k, int32_t max_spec,
                            int32_t* d_replies, dgds_query_stats* d_stats, void* stream);
 
+/* Segmented form for owner routing: rows arrive as n_seg sender segments of seg_rows rows
+ * (row j of segment s valid while j < d_seg_count[s]); the reply of row j of segment s is
+ * written to seg_out[s] + j * reply_words — typically the sender's receive slab in NVLink
+ * peer memory (dgds_px_region). seg_out is a host array of n_seg device pointers. */
+int dgds_speculate_records_seg(dgds_server* s, int32_t n_seg, int64_t seg_rows, const int32_t* d_records,
+                               const int32_t* d_seg_count, const dgds_query_record_layout* layout,
+                               const dgds_spec_args* d_args, int64_t args_stride, int32_t max_top_k,
+                               int32_t max_spec, int32_t* const* seg_out, dgds_query_stats* d_stats, void* stream);
+
 /* Verification of existing candidates (engine.cpp:115-143), host buffers. */
 int dgds_verify_batch(dgds_server* s, int64_t n, const dgds_candidates* cands, const int32_t* truth_next,
                       int32_t truth_stride, const int32_t* truth_left, const int32_t* limit,
@@ -291,6 +300,41 @@ typedef struct dgds_workload_cfg {
 /* Pass 1 (tokens == NULL): fills lengths[num_groups*group_size] and prompt_lens[num_groups] (may be NULL).
  * Pass 2: also writes all outputs back to back (group-major, request-minor) into tokens. */
 int dgds_generate_workload(const dgds_workload_cfg* cfg, int64_t* lengths, int32_t* prompt_lens, int32_t* tokens);
+
+/* ---- peer exchange over NVLink / NVSwitch (one process per GPU, CUDA IPC) ----
+ * Replaces the all-to-all of the reference's shard routing (dgds.cpp:10-14 routes a
+ * group's traffic to shard fnv1a64(gid) % N) with stores straight into the owner's HBM.
+ * Each rank owns one zeroed region of region_bytes; every rank maps every region. A
+ * channel lives at caller-chosen byte offsets, identical in every region:
+ *   flags  u64[world]               sender r's sequence number at flag_off + 8r
+ *   counts i32[world] (per parity)  rows sender r delivered, at count_off + 4r
+ *   slab   i32[world][cap][words]   sender r's rows at slab_off + 4 * r * cap * words
+ * Sequence numbers start at 1 and grow by one per exchange of a channel. */
+typedef struct dgds_px dgds_px;
+#define DGDS_IPC_HANDLE_BYTES 64
+int dgds_px_create(int32_t device, int32_t world, int32_t rank, uint64_t region_bytes, dgds_px** out,
+                   void* handle_out /* DGDS_IPC_HANDLE_BYTES, may be NULL */);
+/* handles: world * DGDS_IPC_HANDLE_BYTES in rank order (this rank's entry is ignored) */
+int dgds_px_connect(dgds_px* px, const void* handles);
+/* All ranks in this process (tests; different devices need peer access) */
+int dgds_px_connect_local(dgds_px* const* all, int32_t world);
+int dgds_px_region(dgds_px* px, int32_t peer, void** base);
+/* Send record i (rec_words int32) to rank d_owner[i] (owners outside [0, world) are dropped):
+ * rows are written into the owner's slab, then counts and flag = seq are published.
+ * d_slot[i] = owner * cap + row (where the owner's reply lands in this rank's reply slab) or -1.
+ * stable != 0 keeps record order per owner (one CTA); otherwise rows are unordered.
+ * Rows beyond cap set *d_overflow = 1 (sticky) and are dropped. */
+int dgds_px_send(dgds_px* px, int64_t n, const int32_t* d_owner, const int32_t* d_records, int32_t rec_words,
+                 int64_t cap, uint64_t slab_off, uint64_t count_off, uint64_t flag_off, uint64_t seq,
+                 int32_t stable, int64_t* d_slot, int32_t* d_overflow, void* stream);
+/* Kernels enqueued after this see every sender's data of exchange `seq` (bounded spin). */
+int dgds_px_wait(dgds_px* px, uint64_t flag_off, uint64_t seq, void* stream);
+/* Publish flag = seq to every peer after the work already enqueued on `stream`. */
+int dgds_px_signal(dgds_px* px, uint64_t flag_off, uint64_t seq, void* stream);
+/* timed_out = 1 once a wait gave up (synchronous read); launches = px kernels enqueued. */
+int dgds_px_status(dgds_px* px, int32_t* timed_out, uint64_t* launches);
+int dgds_px_set_timeout(dgds_px* px, uint64_t timeout_ns);
+int dgds_px_destroy(dgds_px* px);
 
 #ifdef __cplusplus
 }

@@ -359,7 +359,11 @@ __global__ void __launch_bounds__(kBlock, 4) k_query(QueryLaunch P) {
   const Tile<G> tile{lane - gl};
   const int gib = threadIdx.x / G;
   const int64_t q = static_cast<int64_t>(blockIdx.x) * kTiles + gib;
-  const bool valid = q < P.n;  // invalid tiles stay (convergence) but do nothing
+  bool valid = q < P.n;  // invalid tiles stay (convergence) but do nothing
+  if (P.seg_rows > 0 && valid) {  // routed segments: rows past the sender's count are padding
+    const int64_t sg = q / P.seg_rows;
+    valid = q - sg * P.seg_rows < P.seg_count[sg];
+  }
   const int64_t qi = valid ? q : 0;
   GroupScratch<G, S>& sm = scratch[gib];
   const DevTrie& T = P.T;
@@ -369,7 +373,8 @@ __global__ void __launch_bounds__(kBlock, 4) k_query(QueryLaunch P) {
   const int32_t hdl = P.handles[qin];
   const int plen = P.pat_len[qin];
   int32_t tleft = 0, lim = 0;
-  if (P.v_emitted) {
+  const bool verify = P.v_emitted != nullptr || (P.rec_words_out > 0 && P.off_v >= 0);
+  if (verify) {
     tleft = P.truth_left[qin];
     lim = P.limit[qin];
   }
@@ -788,19 +793,48 @@ __global__ void __launch_bounds__(kBlock, 4) k_query(QueryLaunch P) {
                      ? 1
                      : 0;
   }
-  if (P.n_cands && valid) {
-    if (gl == 0) P.n_cands[q * P.nc_qstride] = nf;
+  // per-query output pointers: SoA buffers or one reply record (local or in peer memory)
+  int32_t *o_nc = nullptr, *o_len = nullptr, *o_tk = nullptr, *o_v = nullptr;
+  double* o_sc = nullptr;
+  int64_t* o_sp = nullptr;
+  if (P.rec_words_out > 0) {
+    int32_t* R;
+    if (P.seg_rows > 0) {
+      const int64_t sg = q / P.seg_rows;
+      R = P.seg_out[sg] + (q - sg * P.seg_rows) * P.rec_words_out;
+    } else {
+      R = P.rec_out + q * P.rec_words_out;
+    }
+    if (P.off_nc >= 0) {
+      o_nc = R + P.off_nc;
+      o_len = R + P.off_len;
+      o_sc = reinterpret_cast<double*>(R + P.off_sc);
+      o_sp = reinterpret_cast<int64_t*>(R + P.off_sp);
+      o_tk = R + P.off_tk;
+    }
+    if (P.off_v >= 0) o_v = R + P.off_v;
+  } else {
+    if (P.n_cands) {
+      o_nc = P.n_cands + q * P.nc_qstride;
+      o_len = P.lens + q * P.out_qstride;
+      o_sc = P.scores + q * P.out_qstride8;
+      o_sp = P.supports + q * P.out_qstride8;
+      o_tk = P.tokens + q * P.tok_qstride;
+    }
+  }
+  if (o_nc && valid) {
+    if (gl == 0) *o_nc = nf;
     if (gl < nf) {
-      P.lens[q * P.out_qstride + my_rank] = sm.f.len[gl];
-      P.scores[q * P.out_qstride8 + my_rank] = sm.f.score[gl];
-      P.supports[q * P.out_qstride8 + my_rank] = sm.f.sup[gl];
-      int32_t* dst = P.tokens + q * P.tok_qstride + static_cast<int64_t>(my_rank) * P.s_stride;
+      o_len[my_rank] = sm.f.len[gl];
+      o_sc[my_rank] = sm.f.score[gl];
+      o_sp[my_rank] = sm.f.sup[gl];
+      int32_t* dst = o_tk + static_cast<int64_t>(my_rank) * P.s_stride;
       for (int i = 0; i < sm.f.len[gl]; ++i) dst[i] = sm.f.tok[gl][i];
     }
   }
 
   // ---- K3: verification (engine.cpp:115-143) ----
-  if (P.v_emitted) {
+  if (verify) {
     int drafted = 0, match = 0;
     if (gl < nf) {
       drafted = sm.f.len[gl];
@@ -820,9 +854,15 @@ __global__ void __launch_bounds__(kBlock, 4) k_query(QueryLaunch P) {
     match = tile.max(match);
     if (valid && gl == 0) {
       const int emitted = min(match + 1, lim);
-      P.v_drafted[q * P.v_qstride] = drafted;
-      P.v_accepted[q * P.v_qstride] = emitted - 1;
-      P.v_emitted[q * P.v_qstride] = emitted;
+      if (P.rec_words_out > 0) {
+        o_v[0] = drafted;
+        o_v[1] = emitted - 1;
+        o_v[2] = emitted;
+      } else {
+        P.v_drafted[q * P.v_qstride] = drafted;
+        P.v_accepted[q * P.v_qstride] = emitted - 1;
+        P.v_emitted[q * P.v_qstride] = emitted;
+      }
     }
   }
 

@@ -3,6 +3,7 @@
 #pragma once
 
 #include <cstdint>
+#include <string>
 #include <cuda_runtime.h>
 
 #include "../../include/dgds_b200.h"
@@ -30,6 +31,10 @@ struct AppendPiece {
 
 cudaError_t launch_append(const DevTrie& T, const AppendSeg* d_segs, int64_t nseg, const AppendPiece* d_pieces,
                           const int32_t* d_tokens, cudaStream_t st);
+
+int set_error(int code, const std::string& msg);  // dgds_last_error() message (server.cpp)
+
+constexpr int kMaxSegments = 8;  // senders of a segmented query launch (ranks of one node)
 
 struct QueryLaunch {
   DevTrie T;
@@ -68,6 +73,16 @@ struct QueryLaunch {
   int64_t out_qstride8; // scores, supports (8-byte units)
   int64_t tok_qstride;  // tokens (int32 units; candidate c at + c * s_stride)
   int64_t v_qstride;    // drafted / accepted / emitted
+  // Reply-record output (rec_words_out > 0; replaces the SoA pointers above): the reply row of
+  // query q is R = rec_out + q * rec_words_out, or with seg_rows > 0 (rows arrive in per-sender
+  // segments of seg_rows, valid while j < seg_count[s]) R = seg_out[s] + j * rec_words_out —
+  // typically the sender's receive region in NVLink peer memory.
+  int32_t rec_words_out;
+  int32_t off_nc, off_len, off_sc, off_sp, off_tk, off_v;  // field offsets in the row (int32 units; -1 = absent)
+  int32_t* rec_out;
+  int64_t seg_rows;
+  const int32_t* seg_count;
+  int32_t* seg_out[kMaxSegments];
 };
 
 // SoA strides for a QueryLaunch whose outputs are [n][k_stride][s_stride] buffers.

@@ -104,6 +104,51 @@ struct StreamRec {
   uint64_t batch_stamp = 0;
 };
 
+// request-id -> stream: direct-indexed for small ids (the common case: a group's
+// responses are numbered 0..G-1), hashed beyond
+class StreamTable {
+ public:
+  static constexpr int32_t kDirect = 256;
+  StreamRec* find(int32_t rid) {
+    if (rid < kDirect) return rid < static_cast<int32_t>(present_.size()) && present_[rid] ? &direct_[rid] : nullptr;
+    auto it = far_.find(rid);
+    return it == far_.end() ? nullptr : &it->second;
+  }
+  StreamRec& insert(int32_t rid, const StreamRec& v) {
+    if (rid < kDirect) {
+      if (rid >= static_cast<int32_t>(present_.size())) {
+        present_.resize(rid + 1, 0);
+        direct_.resize(rid + 1);
+      }
+      present_[rid] = 1;
+      direct_[rid] = v;
+      ++n_;
+      return direct_[rid];
+    }
+    ++n_;
+    return far_.emplace(rid, v).first->second;
+  }
+  void clear() {
+    present_.clear();
+    direct_.clear();
+    far_.clear();
+    n_ = 0;
+  }
+  template <class F>
+  void for_each(F&& f) {
+    for (size_t i = 0; i < present_.size(); ++i)
+      if (present_[i]) f(static_cast<int32_t>(i), direct_[i]);
+    for (auto& kv : far_) f(kv.first, kv.second);
+  }
+  size_t size() const { return n_; }
+
+ private:
+  std::vector<uint8_t> present_;
+  std::vector<StreamRec> direct_;
+  std::unordered_map<int32_t, StreamRec> far_;
+  size_t n_ = 0;
+};
+
 struct GroupRec {
   std::string gid;
   int32_t shard = 0;
@@ -112,7 +157,7 @@ struct GroupRec {
   double ttl = 0.0;
   double expires = 0.0;
   uint64_t version = 0;
-  std::unordered_map<int32_t, StreamRec> streams;
+  StreamTable streams;
 };
 
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
@@ -208,7 +253,7 @@ int alloc_stream_slot(dgds_server* s, uint32_t* out) {
 
 void retire_group(dgds_server* s, GroupRec& g) {
   if (!g.alive) return;
-  for (auto& kv : g.streams) s->free_streams.push_back(kv.second.slot);
+  g.streams.for_each([&](int32_t, StreamRec& r) { s->free_streams.push_back(r.slot); });
   g.streams.clear();
   g.alive = false;
   g.version = 0;
@@ -286,10 +331,10 @@ int rebuild(dgds_server* s, uint64_t new_cap) {
     if (!g.alive) continue;
     const uint32_t r = dgds::kRootTop - g.root;
     alive[r >> 5] |= 1u << (r & 31);
-    for (auto& kv : g.streams) {
-      live_slots.push_back(kv.second.slot);
-      live_sizes.push_back(static_cast<uint32_t>(std::min<uint64_t>(kv.second.stored, s->D)));
-    }
+    g.streams.for_each([&](int32_t, StreamRec& r) {
+      live_slots.push_back(r.slot);
+      live_sizes.push_back(static_cast<uint32_t>(std::min<uint64_t>(r.stored, s->D)));
+    });
   }
   uint32_t *d_alive = nullptr, *d_remap = nullptr, *d_ls = nullptr;
   DGDS_CUDA(cudaMalloc(&d_alive, alive.size() * 4));
@@ -375,14 +420,14 @@ int plan_updates(dgds_server* s, int64_t n, const int32_t* handles, const int32_
       if (rc) return rc;
     }
     g.expires = now + g.ttl;
-    auto it = g.streams.find(rids[i]);
-    if (it == g.streams.end()) {  // a mismatched append still creates the stream (cst.cpp:121)
-      StreamRec sr;
-      int rc = alloc_stream_slot(s, &sr.slot);
+    StreamRec* found = g.streams.find(rids[i]);
+    if (!found) {  // a mismatched append still creates the stream (cst.cpp:121)
+      StreamRec fresh;
+      int rc = alloc_stream_slot(s, &fresh.slot);
       if (rc) return rc;
-      it = g.streams.emplace(rids[i], sr).first;
+      found = &g.streams.insert(rids[i], fresh);
     }
-    StreamRec& sr = it->second;
+    StreamRec& sr = *found;
     const uint64_t cnt = tcount(i);
     if (prev[i] != sr.stored) {
       rep[i] = dgds_update_reply{0, 0, g.version, sr.stored};
@@ -479,6 +524,10 @@ struct StreamJoin {
 };
 
 }  // namespace
+
+namespace dgds {
+int set_error(int code, const std::string& msg) { return fail(code, msg); }  // shared with peer.cu
+}  // namespace dgds
 
 extern "C" {
 
@@ -622,9 +671,9 @@ int dgds_group_version(dgds_server* s, int32_t h, uint64_t* out) {
 int dgds_stored_tokens(dgds_server* s, int32_t h, int32_t rid, uint64_t* out) {
   std::lock_guard<std::mutex> lk(s->mu);
   if (int rc = check_handle(s, h)) return rc;
-  const GroupRec& g = s->groups[h];
-  auto it = g.streams.find(rid);
-  *out = (g.alive && it != g.streams.end()) ? it->second.stored : 0;
+  GroupRec& g = s->groups[h];
+  StreamRec* r = g.streams.find(rid);
+  *out = (g.alive && r) ? r->stored : 0;
   return DGDS_OK;
 }
 
@@ -997,12 +1046,14 @@ int dgds_speculate_device(dgds_server* s, int64_t n, const int32_t* d_handles, c
   return DGDS_OK;
 }
 
-int dgds_speculate_records(dgds_server* s, int64_t n, const int32_t* d_records, const dgds_query_record_layout* lay,
-                           const dgds_spec_args* d_args, int64_t args_stride, int32_t max_top_k, int32_t max_spec,
-                           int32_t* d_replies, dgds_query_stats* d_stats, void* stream) {
+static int speculate_records_impl(dgds_server* s, int64_t n, const int32_t* d_records,
+                                  const dgds_query_record_layout* lay, const dgds_spec_args* d_args,
+                                  int64_t args_stride, int32_t max_top_k, int32_t max_spec, int32_t* d_replies,
+                                  int32_t n_seg, int64_t seg_rows, const int32_t* d_seg_count,
+                                  int32_t* const* seg_out, dgds_query_stats* d_stats, void* stream) {
   if (n < 0) return fail(DGDS_EINVAL, "negative batch size");
   if (n == 0) return DGDS_OK;
-  if (!lay || !d_records || !d_replies) return fail(DGDS_EINVAL, "null argument");
+  if (!lay || !d_records || !d_args || (!d_replies && !seg_out)) return fail(DGDS_EINVAL, "null argument");
   if (max_top_k < 1 || max_top_k > DGDS_MAX_TOP_K) return fail(DGDS_EUNSUPPORTED, "max_top_k out of range");
   if (max_spec <= 0 || max_spec > s->p.max_spec_len) max_spec = std::max(1, s->p.max_spec_len);
   const dgds_query_record_layout& y = *lay;
@@ -1027,24 +1078,24 @@ int dgds_speculate_records(dgds_server* s, int64_t n, const int32_t* d_records, 
   L.k_stride = max_top_k;
   L.s_stride = max_spec;
   L.in_qstride = y.rec_words;
-  L.n_cands = d_replies + y.off_n_cands;
-  L.lens = d_replies + y.off_lens;
-  L.scores = reinterpret_cast<double*>(d_replies + y.off_scores);
-  L.supports = reinterpret_cast<int64_t*>(d_replies + y.off_supports);
-  L.tokens = d_replies + y.off_tokens;
-  L.nc_qstride = y.reply_words;
-  L.out_qstride = y.reply_words;
-  L.out_qstride8 = y.reply_words / 2;
-  L.tok_qstride = y.reply_words;
-  L.v_qstride = y.reply_words;
+  L.rec_words_out = y.reply_words;
+  L.rec_out = d_replies;
+  if (seg_out) {
+    L.seg_rows = seg_rows;
+    L.seg_count = d_seg_count;
+    for (int i = 0; i < n_seg; ++i) L.seg_out[i] = seg_out[i];
+  }
+  L.off_nc = y.off_n_cands;
+  L.off_len = y.off_lens;
+  L.off_sc = y.off_scores;
+  L.off_sp = y.off_supports;
+  L.off_tk = y.off_tokens;
+  L.off_v = y.off_verify;
   if (y.off_verify >= 0) {
     L.truth = d_records + y.off_truth;
     L.truth_stride = y.rec_words;
     L.truth_left = d_records + y.off_truth_left;
     L.limit = d_records + y.off_limit;
-    L.v_drafted = d_replies + y.off_verify;
-    L.v_accepted = d_replies + y.off_verify + 1;
-    L.v_emitted = d_replies + y.off_verify + 2;
   }
   L.stats = d_stats;
   L.err_flag = s->d_err;
@@ -1054,6 +1105,25 @@ int dgds_speculate_records(dgds_server* s, int64_t n, const int32_t* d_records, 
     DGDS_CUDA(dgds::launch_query(L, max_top_k, max_spec, join.stream()));
   }
   return DGDS_OK;
+}
+
+int dgds_speculate_records(dgds_server* s, int64_t n, const int32_t* d_records, const dgds_query_record_layout* lay,
+                           const dgds_spec_args* d_args, int64_t args_stride, int32_t max_top_k, int32_t max_spec,
+                           int32_t* d_replies, dgds_query_stats* d_stats, void* stream) {
+  return speculate_records_impl(s, n, d_records, lay, d_args, args_stride, max_top_k, max_spec, d_replies, 0, 0,
+                                nullptr, nullptr, d_stats, stream);
+}
+
+int dgds_speculate_records_seg(dgds_server* s, int32_t n_seg, int64_t seg_rows, const int32_t* d_records,
+                               const int32_t* d_seg_count, const dgds_query_record_layout* lay,
+                               const dgds_spec_args* d_args, int64_t args_stride, int32_t max_top_k,
+                               int32_t max_spec, int32_t* const* seg_out, dgds_query_stats* d_stats, void* stream) {
+  if (n_seg < 1 || n_seg > dgds::kMaxSegments || seg_rows < 0) return fail(DGDS_EINVAL, "bad segment shape");
+  if (!d_seg_count || !seg_out) return fail(DGDS_EINVAL, "null argument");
+  for (int i = 0; i < n_seg; ++i)
+    if (!seg_out[i]) return fail(DGDS_EINVAL, "null segment output");
+  return speculate_records_impl(s, static_cast<int64_t>(n_seg) * seg_rows, d_records, lay, d_args, args_stride,
+                                max_top_k, max_spec, nullptr, n_seg, seg_rows, d_seg_count, seg_out, d_stats, stream);
 }
 
 int dgds_verify_batch(dgds_server* s, int64_t n, const dgds_candidates* c, const int32_t* truth, int32_t truth_stride,

@@ -1,0 +1,200 @@
+"""Owner routing over NVLink peer memory (one process per GPU) — no collectives.
+
+The reference routes a group's traffic to shard ``fnv1a64(gid) % N``
+(proj/src/dgds.cpp:10-14). Here each rank owns one device region that every
+other rank maps through CUDA IPC (``dgds_px_*`` in include/dgds_b200.h). A
+*channel* is a double-buffered slab per receiver, ``[parity][sender][rows][words]``
+int32, plus per-sender counts and a monotone sequence flag:
+
+- ``send``  scatters records into their owners' slabs (stores over NVLink) and
+  publishes counts + ``flag = seq`` (k_px_send_*);
+- ``wait``  makes later kernels on the stream see every sender's exchange ``seq``;
+- ``signal`` publishes ``flag = seq`` after kernels that wrote into peers' slabs
+  (the query kernel writes its reply records straight into the sender's reply
+  slab, ``dgds_speculate_records_seg``).
+
+Parity ``seq % 2`` selects the slab; a sender may rewrite a parity only after a
+round trip proves the receiver finished reading it (bench_multi.py keeps that
+order).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import Dict, List, Optional, Sequence, Tuple
+
+import torch
+
+from . import _lib
+
+_ALIGN = 256
+
+
+class _DevArray:
+    """__cuda_array_interface__ wrapper: a torch view of raw device memory."""
+
+    def __init__(self, ptr: int, shape: Tuple[int, ...], typestr: str):
+        self.__cuda_array_interface__ = {"shape": shape, "typestr": typestr, "data": (ptr, False), "version": 3,
+                                         "strides": None}
+
+
+def _view(ptr: int, shape: Tuple[int, ...], typestr: str, device: torch.device) -> torch.Tensor:
+    return torch.as_tensor(_DevArray(ptr, shape, typestr), device=device)
+
+
+@dataclass
+class Channel:
+    name: str
+    rows: int            # rows per sender in one slab
+    words: int           # int32 words per row
+    flag_off: int
+    count_off: Tuple[int, int]
+    slab_off: Tuple[int, int]
+
+
+def _layout(world: int, spec: Dict[str, Tuple[int, int]]) -> Tuple[Dict[str, Channel], int]:
+    off = 0
+    chans = {}
+    heads = {}
+    for name in spec:  # headers first: flags (8 B per sender) and two parities of counts
+        flag = off
+        off += 8 * world
+        c0 = off
+        off += 4 * world
+        c1 = off
+        off += 4 * world
+        off = (off + 63) // 64 * 64
+        heads[name] = (flag, (c0, c1))
+    off = (off + _ALIGN - 1) // _ALIGN * _ALIGN
+    for name, (rows, words) in spec.items():
+        slabs = []
+        for _ in range(2):
+            slabs.append(off)
+            off += (world * rows * words * 4 + _ALIGN - 1) // _ALIGN * _ALIGN
+        chans[name] = Channel(name, rows, words, heads[name][0], heads[name][1], (slabs[0], slabs[1]))
+    return chans, off
+
+
+class PeerExchange:
+    """One rank's end of the NVLink exchange. ``channels`` maps name -> (rows per sender, words)."""
+
+    def __init__(self, world: int, rank: int, device: int, channels: Dict[str, Tuple[int, int]], group=None,
+                 connect: bool = True):
+        self.world, self.rank = world, rank
+        self.device = torch.device("cuda", device)
+        self.ch, self.bytes = _layout(world, channels)
+        L = _lib.lib()
+        h = C.c_void_p()
+        self._handle = C.create_string_buffer(64)
+        _lib.check(L.dgds_px_create(device, world, rank, self.bytes, C.byref(h), self._handle))
+        self.h = h
+        self.overflow = torch.zeros(1, dtype=torch.int32, device=self.device)
+        self._bases: Optional[List[int]] = None
+        self._seg_ptrs: Dict[Tuple[str, int], C.Array] = {}
+        if connect and world > 1:
+            import torch.distributed as dist
+            hs = [None] * world
+            dist.all_gather_object(hs, self._handle.raw, group=group)
+            _lib.check(L.dgds_px_connect(self.h, b"".join(hs)))
+
+    @staticmethod
+    def local_group(world: int, device: int, channels: Dict[str, Tuple[int, int]]) -> List["PeerExchange"]:
+        """All `world` ranks in this process (tests on one GPU)."""
+        pxs = [PeerExchange(world, r, device, channels, connect=False) for r in range(world)]
+        arr = (C.c_void_p * world)(*[p.h.value for p in pxs])
+        _lib.check(_lib.lib().dgds_px_connect_local(arr, world))
+        return pxs
+
+    # ---- addresses ----
+    def bases(self) -> List[int]:
+        if self._bases is None:
+            out = []
+            for p in range(self.world):
+                b = C.c_void_p()
+                _lib.check(_lib.lib().dgds_px_region(self.h, p, C.byref(b)))
+                out.append(b.value)
+            self._bases = out
+        return self._bases
+
+    def slab_ptr(self, ch: str, seq: int) -> int:
+        return self.bases()[self.rank] + self.ch[ch].slab_off[seq % 2]
+
+    def counts_ptr(self, ch: str, seq: int) -> int:
+        return self.bases()[self.rank] + self.ch[ch].count_off[seq % 2]
+
+    def slab(self, ch: str, seq: int) -> torch.Tensor:
+        """This rank's received rows of exchange `seq`: [world * rows, words] (sender-major)."""
+        c = self.ch[ch]
+        return _view(self.bases()[self.rank] + c.slab_off[seq % 2], (self.world * c.rows, c.words), "<i4",
+                     self.device)
+
+    def counts(self, ch: str, seq: int) -> torch.Tensor:
+        c = self.ch[ch]
+        return _view(self.bases()[self.rank] + c.count_off[seq % 2], (self.world,), "<i4", self.device)
+
+    def seg_out(self, ch: str, seq: int) -> C.Array:
+        """Per peer p: where this rank's rows start in p's slab of `ch` (reply destinations)."""
+        key = (ch, seq % 2)
+        if key not in self._seg_ptrs:
+            c = self.ch[ch]
+            self._seg_ptrs[key] = (C.c_void_p * self.world)(
+                *[b + c.slab_off[seq % 2] + 4 * self.rank * c.rows * c.words for b in self.bases()])
+        return self._seg_ptrs[key]
+
+    # ---- exchange ----
+    def send(self, ch: str, owner: torch.Tensor, records: torch.Tensor, seq: int, stable: bool = False,
+             slot: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+        c = self.ch[ch]
+        n = records.shape[0]
+        assert records.dtype == torch.int32 and records.is_contiguous() and records.shape[1] == c.words
+        assert owner.dtype == torch.int32 and owner.is_contiguous() and owner.shape[0] == n
+        if slot is None:
+            slot = torch.empty(n, dtype=torch.int64, device=self.device)
+        st = stream if stream is not None else torch.cuda.current_stream(self.device)
+        _lib.check(_lib.lib().dgds_px_send(self.h, n, C.c_void_p(owner.data_ptr()), C.c_void_p(records.data_ptr()),
+                                           c.words, c.rows, c.slab_off[seq % 2], c.count_off[seq % 2], c.flag_off,
+                                           seq, 1 if stable else 0, C.c_void_p(slot.data_ptr()),
+                                           C.c_void_p(self.overflow.data_ptr()), C.c_void_p(st.cuda_stream)))
+        return slot
+
+    def wait(self, ch: str, seq: int, stream=None) -> None:
+        st = stream if stream is not None else torch.cuda.current_stream(self.device)
+        _lib.check(_lib.lib().dgds_px_wait(self.h, self.ch[ch].flag_off, seq, C.c_void_p(st.cuda_stream)))
+
+    def signal(self, ch: str, seq: int, stream=None) -> None:
+        st = stream if stream is not None else torch.cuda.current_stream(self.device)
+        _lib.check(_lib.lib().dgds_px_signal(self.h, self.ch[ch].flag_off, seq, C.c_void_p(st.cuda_stream)))
+
+    def status(self) -> Tuple[bool, int]:
+        t, n = _lib._I32(), _lib._U64()
+        _lib.check(_lib.lib().dgds_px_status(self.h, C.byref(t), C.byref(n)))
+        return bool(t.value), int(n.value)
+
+    def set_timeout(self, seconds: float) -> None:
+        _lib.check(_lib.lib().dgds_px_set_timeout(self.h, int(seconds * 1e9)))
+
+    def close(self) -> None:
+        if self.h:
+            _lib.lib().dgds_px_destroy(self.h)
+            self.h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def speculate_routed(srv, px: PeerExchange, q_ch: str, rep_ch: str, seq: int, layout, d_args: torch.Tensor,
+                     max_top_k: int, max_spec: int, stats: Optional[torch.Tensor] = None, stream=None) -> None:
+    """Owner side of a routed query exchange: K2 + fused K3 over the received query rows of
+    exchange `seq`, replies stored straight into each sender's `rep_ch` slab, then signalled."""
+    c = px.ch[q_ch]
+    st = stream if stream is not None else torch.cuda.current_stream(px.device)
+    px.wait(q_ch, seq, st)
+    _lib.check(_lib.lib().dgds_speculate_records_seg(
+        srv.handle, px.world, c.rows, C.c_void_p(px.slab_ptr(q_ch, seq)),
+        C.c_void_p(px.counts_ptr(q_ch, seq)), C.byref(layout), C.c_void_p(d_args.data_ptr()), 0, max_top_k,
+        max_spec, px.seg_out(rep_ch, seq), C.c_void_p(stats.data_ptr()) if stats is not None else None,
+        C.c_void_p(st.cuda_stream)))
+    px.signal(rep_ch, seq, st)
