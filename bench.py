@@ -437,6 +437,7 @@ def main_b200(args):
               "traffic": APPEND_TRAFFIC, "alg_bytes_per_launch": app_alg / K,
               "avg_launch_ms": prof.append_ms / max(1, prof.append_launches), "peak_kind": peak_kind}
     nodes = srv.node_count()
+    slots = srv.index_slots()
 
     # ---- e2e: same tick through the host C ABI (host buffers, H2D/D2H inside) ----
     e2e = None
@@ -464,21 +465,19 @@ def main_b200(args):
                 tru[ok, j] = tr.tokens[(base + j)[ok]]
             host_steps.append((handles_of_stream[live], rid_of_stream[live], prev, offs, toks,
                                handles_of_stream[st].copy(), poff, pat, tru, tl))
-        from paper_2511_14617_b200.dgds import CandidateBatch
-        cb = CandidateBatch(Q, kq, dl)
-        dr = np.zeros(Q, np.int32)
-        ac = np.zeros(Q, np.int32)
-        em = np.zeros(Q, np.int32)
-        hvo = _lib.VerifyOut(dr.ctypes.data, ac.ctypes.data, em.ctypes.data)
+        view = _lib.ResultView()
+        em_sum = [0]
         h2d = d2h = 0
         last = C.c_uint64()
 
         def host_step(hs_):
             (h, r, prev, offs, toks, qh, poff, pat, tru, tl) = hs_
             srv.update_arrays(h, r, prev, offs, toks, 0.0)
-            _lib.check(L.dgds_speculate_verify_batch(
+            # compact results (CSR) in the server's pinned block: the public zero-copy query call
+            _lib.check(L.dgds_speculate_verify_view(
                 srv.handle, Q, qh.ctypes.data, poff.ctypes.data, pat.ctypes.data, sp_args.ctypes.data, 0,
-                tru.ctypes.data, dl, tl.ctypes.data, tl.ctypes.data, C.byref(cb.c()), C.byref(hvo)))
+                tru.ctypes.data, dl, tl.ctypes.data, tl.ctypes.data, C.byref(view)))
+            em_sum[0] += int(np.ctypeslib.as_array(C.cast(view.emitted, C.POINTER(C.c_int32)), shape=(Q,)).sum())
             _lib.check(L.dgds_last_transfer(srv.handle, C.byref(last)))
             # bytes actually staged: tokens + segment table (32 B/record) + pieces (16 B/record);
             # patterns (8 int32 rows), pattern lengths, handles, truth rows, truth_left, limit, args
@@ -497,7 +496,8 @@ def main_b200(args):
         e2e = {"value": Q * E / (t1 - t0), "unit": "queries/s", "h2d_bytes_per_step": h2d // E,
                "d2h_bytes_per_step": d2h // E, "steps": E,
                "append_tokens_per_s": sum(x[4].size for x in host_steps[1:]) / (t1 - t0),
-               "path": "dgds_update_batch + dgds_speculate_verify_batch (host buffers)"}
+               "path": "dgds_update_batch + dgds_speculate_verify_view (host buffers in, compact pinned results "
+                       "out; the step reads every query's emitted count)"}
 
     # ---- CPU baseline (reference, bounded sample, all host cores) ----
     cpu = None
@@ -529,8 +529,9 @@ def main_b200(args):
                    "append_tokens_per_step": app_tok / K, "record_tokens": args.record_tokens, "top_k": kq,
                    "draft_len": dl, "regime": "R1 built index (prefix prefilled) + streaming appends",
                    "prefill": args.prefill, "prefill_s": prefill_s, "index_nodes": nodes,
+                   "index_slots": slots, "index_load": nodes / slots,
                    "l2": "inputs larger than L2 (index of %.1f GB, 126 MB L2); per-step inputs distinct"
-                         % (nodes * 32 / 0.5 / 1e9), "parallelism": "single GPU"},
+                         % (slots * 32 / 1e9), "parallelism": "single GPU"},
         "roofline": roof_q if dom_q else roof_a,
         "roofline_query": roof_q, "roofline_append": roof_a,
         "cpu_baseline": cpu, "e2e": e2e,

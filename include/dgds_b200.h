@@ -150,6 +150,8 @@ int dgds_stored_tokens(dgds_server* s, int32_t handle, int32_t request_id, uint6
 int dgds_shard_group_count(dgds_server* s, int32_t shard, uint64_t* out);
 /* Device-side trie size: nodes in use (synchronises). */
 int dgds_node_count(dgds_server* s, uint64_t* out);
+/* Slots of the open-addressing node table (load factor = stored nodes / slots). */
+int dgds_index_slots(dgds_server* s, uint64_t* slots);
 
 /* n update_cst calls, applied in array order. Record i appends
  * tokens[tok_offsets[i] .. tok_offsets[i+1]) for (handles[i], request_ids[i]).
@@ -160,7 +162,7 @@ int dgds_update_batch(dgds_server* s, int64_t n, const int32_t* handles, const i
                       dgds_update_reply* replies);
 
 /* Same, with the token payload already in device memory (d_tokens, record order);
- * metadata stays on the host. The kernel is enqueued on `stream` (NULL = server stream). */
+ * metadata stays on the host. The kernel is enqueued on `stream` (NULL = the legacy default stream). */
 int dgds_update_batch_device(dgds_server* s, int64_t n, const int32_t* handles, const int32_t* request_ids,
                              const uint64_t* prev_counts, const uint64_t* tok_offsets, const int32_t* d_tokens,
                              double now, dgds_update_reply* replies, void* stream);
@@ -179,7 +181,7 @@ int dgds_speculate_batch(dgds_server* s, int64_t n, const int32_t* handles, cons
                          const int32_t* patterns, const dgds_spec_args* args, int64_t args_stride,
                          dgds_candidates* out);
 
-/* Zero-copy query over device buffers, enqueued on `stream` (NULL = server stream), no sync.
+/* Zero-copy query over device buffers, enqueued on `stream` (NULL = the legacy default stream), no sync.
  * d_handles[n], d_pat_len[n], d_patterns[n * pat_stride] (the LAST d_pat_len[q] tokens of each
  * pattern, left-aligned; only the last max_pattern_len can matter), d_args[q * args_stride].
  * max_top_k bounds args.top_k and max_spec bounds min(args.max_spec_tokens, max_spec_len) over the
@@ -229,6 +231,32 @@ typedef struct dgds_query_record_layout {
 int dgds_speculate_records(dgds_server* s, int64_t n, const int32_t* d_records, const dgds_query_record_layout* layout,
                            const dgds_spec_args* d_args, int64_t args_stride, int32_t max_top_k, int32_t max_spec,
                            int32_t* d_replies, dgds_query_stats* d_stats, void* stream);
+
+/* Zero-copy host results: compact per-query candidate lists (CSR) in a pinned block owned
+ * by the server, valid until the next query call on `s`. Candidates of query q are
+ * cands[cand_off[q] .. cand_off[q+1]) in candidate_before order (cst.cpp:29-35); the tokens
+ * of candidate c are tokens[tok_off[c] .. tok_off[c+1]). Verification (engine.cpp:115-143)
+ * runs when truth != NULL. Same inputs and validation as dgds_speculate_verify_batch. */
+typedef struct dgds_cand_meta {
+  double score;
+  int64_t support;
+  int32_t len;
+  int32_t reserved;
+} dgds_cand_meta;
+typedef struct dgds_result_view {
+  int64_t n_queries, n_cands, n_tokens;
+  const int64_t* cand_off;      /* [n_queries + 1] */
+  const dgds_cand_meta* cands;  /* [n_cands] */
+  const int64_t* tok_off;       /* [n_cands + 1] */
+  const int32_t* tokens;        /* [n_tokens] */
+  const int32_t* drafted;       /* [n_queries] each; NULL without verification */
+  const int32_t* accepted;
+  const int32_t* emitted;
+} dgds_result_view;
+int dgds_speculate_verify_view(dgds_server* s, int64_t n, const int32_t* handles, const uint64_t* pat_offs,
+                               const int32_t* patterns, const dgds_spec_args* args, int64_t args_stride,
+                               const int32_t* truth, int32_t truth_stride, const int32_t* truth_left,
+                               const int32_t* limit, dgds_result_view* out);
 
 /* Segmented form for owner routing: rows arrive as n_seg sender segments of seg_rows rows
  * (row j of segment s valid while j < d_seg_count[s]); the reply of row j of segment s is

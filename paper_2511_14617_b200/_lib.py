@@ -68,6 +68,12 @@ class VerifyOut(C.Structure):
     _fields_ = [("drafted", C.c_void_p), ("accepted", C.c_void_p), ("emitted", C.c_void_p)]
 
 
+class ResultView(C.Structure):
+    _fields_ = [("n_queries", C.c_int64), ("n_cands", C.c_int64), ("n_tokens", C.c_int64),
+                ("cand_off", C.c_void_p), ("cands", C.c_void_p), ("tok_off", C.c_void_p), ("tokens", C.c_void_p),
+                ("drafted", C.c_void_p), ("accepted", C.c_void_p), ("emitted", C.c_void_p)]
+
+
 class QueryStats(C.Structure):
     _fields_ = [
         ("queries", C.c_uint64),
@@ -140,6 +146,7 @@ EXPORTS = {
     "dgds_stored_tokens": (C.c_int, [_P, _I32, _I32, C.POINTER(_U64)]),
     "dgds_shard_group_count": (C.c_int, [_P, _I32, C.POINTER(_U64)]),
     "dgds_node_count": (C.c_int, [_P, C.POINTER(_U64)]),
+    "dgds_index_slots": (C.c_int, [_P, C.POINTER(_U64)]),
     "dgds_update_batch": (C.c_int, [_P, _I64, _P, _P, _P, _P, _P, _D, _P]),
     "dgds_update_batch_device": (C.c_int, [_P, _I64, _P, _P, _P, _P, _P, _D, _P, _P]),
     "dgds_update_batch_device_strided": (C.c_int, [_P, _I64, _P, _P, _P, _P, _P, _P, _D, _P, _P]),
@@ -159,6 +166,7 @@ EXPORTS = {
     "dgds_route_unpack": (C.c_int, [_I64, _P, _I32, _P, _P, _P]),
     "dgds_route_pack_padded": (C.c_int, [_I64, _I32, _P, _P, _I32, _I64, _P, _P, _P, _P]),
     "dgds_speculate_records": (C.c_int, [_P, _I64, _P, C.POINTER(RecordLayout), _P, _I64, _I32, _I32, _P, _P, _P]),
+    "dgds_speculate_verify_view": (C.c_int, [_P, _I64, _P, _P, _P, _P, _I64, _P, _I32, _P, _P, C.POINTER(ResultView)]),
     "dgds_speculate_records_seg": (C.c_int, [_P, _I32, _I64, _P, _P, C.POINTER(RecordLayout), _P, _I64, _I32, _I32,
                                              C.POINTER(C.c_void_p), _P, _P]),
     "dgds_generate_workload": (C.c_int, [C.POINTER(WorkloadCfg), _P, _P, _P]),

@@ -1,3 +1,4 @@
+#include <algorithm>
 // kernels.cu — sm_100a kernels of the DGDS hot path.
 //
 //   K1 k_append        batched incremental insertion of appended tokens into the
@@ -1255,7 +1256,8 @@ __global__ void k_cmp_scan(int64_t nblocks, long long* block_sums, long long* to
 __global__ void k_cmp_scatter(int64_t n, int32_t K, int32_t S, const int32_t* __restrict__ n_cands,
                               const int32_t* __restrict__ lens, const double* __restrict__ scores,
                               const int64_t* __restrict__ supports, const int32_t* __restrict__ tokens,
-                              const long long* __restrict__ block_sums, CandMeta* meta, int32_t* tok_out) {
+                              const long long* __restrict__ block_sums, CandMeta* meta, int32_t* tok_out,
+                              int64_t* cand_off, int64_t* tok_off) {
   const int64_t q = static_cast<int64_t>(blockIdx.x) * kCmpBlock + threadIdx.x;
   int c = 0, t = 0;
   if (q < n) {
@@ -1270,12 +1272,31 @@ __global__ void k_cmp_scatter(int64_t n, int32_t K, int32_t S, const int32_t* __
   BS(tmp).ExclusiveSum(t, to);
   if (q >= n) return;
   long long cb = block_sums[2 * blockIdx.x] + co, tb = block_sums[2 * blockIdx.x + 1] + to;
+  if (cand_off) cand_off[q] = cb;
   for (int j = 0; j < c; ++j) {
     const int64_t si = q * K + j;
     const int L = lens[si];
     meta[cb + j] = CandMeta{scores[si], supports[si], L, 0};
+    if (tok_off) tok_off[cb + j] = tb;
     for (int i = 0; i < L; ++i) tok_out[tb + i] = tokens[si * S + i];
     tb += L;
+  }
+}
+
+// Device -> (mapped) host copy of regions whose sizes are only known on the device:
+// region r holds totals[idx] elements of elem_bytes. Coalesced 16-B stores (PCIe-friendly).
+__global__ void k_copy_out(const long long* __restrict__ totals, CopyOutRegions R) {
+  const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t nth = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int r = 0; r < R.n; ++r) {
+    const int64_t bytes = R.total_idx[r] < 0 ? R.fixed_bytes[r] : totals[R.total_idx[r]] * R.elem_bytes[r];
+    const int64_t n16 = bytes / 16;
+    const uint4* src = reinterpret_cast<const uint4*>(R.src[r]);
+    uint4* dst = reinterpret_cast<uint4*>(R.dst[r]);
+    for (int64_t i = tid; i < n16; i += nth) dst[i] = src[i];
+    const int64_t tail = bytes - n16 * 16;  // multiple of 4
+    if (tid < tail / 4)
+      reinterpret_cast<uint32_t*>(R.dst[r] + n16 * 16)[tid] = reinterpret_cast<const uint32_t*>(R.src[r] + n16 * 16)[tid];
   }
 }
 
@@ -1284,13 +1305,20 @@ __global__ void k_cmp_scatter(int64_t n, int32_t K, int32_t S, const int32_t* __
 cudaError_t launch_compact(int64_t n, int32_t K, int32_t S, const int32_t* n_cands, const int32_t* lens,
                            const double* scores, const int64_t* supports, const int32_t* tokens,
                            long long* block_sums, long long* totals, CandMeta* meta, int32_t* tok_out,
-                           cudaStream_t st) {
+                           int64_t* cand_off, int64_t* tok_off, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
   const int64_t nb = (n + kCmpBlock - 1) / kCmpBlock;
   k_cmp_count<<<static_cast<unsigned>(nb), kCmpBlock, 0, st>>>(n, K, n_cands, lens, block_sums);
   k_cmp_scan<<<1, 1, 0, st>>>(nb, block_sums, totals);
   k_cmp_scatter<<<static_cast<unsigned>(nb), kCmpBlock, 0, st>>>(n, K, S, n_cands, lens, scores, supports, tokens,
-                                                                  block_sums, meta, tok_out);
+                                                                  block_sums, meta, tok_out, cand_off, tok_off);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_copy_out(const long long* totals, const CopyOutRegions& R, int64_t max_bytes, cudaStream_t st) {
+  if (R.n == 0 || max_bytes <= 0) return cudaSuccess;
+  const int64_t blocks = std::min<int64_t>(592, (max_bytes / 16 + 255) / 256 + 1);
+  k_copy_out<<<static_cast<unsigned>(blocks), 256, 0, st>>>(totals, R);
   return cudaGetLastError();
 }
 

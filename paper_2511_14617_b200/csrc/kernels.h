@@ -122,11 +122,26 @@ struct CandMeta {
   int32_t len;
   int32_t pad;
 };
+constexpr int kMaxCopyRegions = 6;
+struct CopyOutRegions {
+  int32_t n;
+  int32_t total_idx[kMaxCopyRegions];   // < 0: fixed size fixed_bytes[r]
+  int32_t elem_bytes[kMaxCopyRegions];
+  int64_t fixed_bytes[kMaxCopyRegions];
+  const char* src[kMaxCopyRegions];  // 16-B aligned
+  char* dst[kMaxCopyRegions];        // 16-B aligned; typically mapped pinned host memory
+};
+// Copies region r = totals[total_idx[r]] * elem_bytes[r] (or fixed_bytes[r]) bytes, a multiple
+// of 4; max_bytes sizes the grid.
+cudaError_t launch_copy_out(const long long* totals, const CopyOutRegions& R, int64_t max_bytes, cudaStream_t st);
+
 // block_sums: 2 * ceil(n / 256) scratch; totals[0] = candidates, totals[1] = tokens.
+// Outputs may live in mapped pinned host memory (written over PCIe by the kernel).
+// cand_off[q] (optional) = first candidate of query q; tok_off[c] (optional) = first token of c.
 cudaError_t launch_compact(int64_t n, int32_t K, int32_t S, const int32_t* n_cands, const int32_t* lens,
                            const double* scores, const int64_t* supports, const int32_t* tokens,
                            long long* block_sums, long long* totals, CandMeta* meta, int32_t* tok_out,
-                           cudaStream_t st);
+                           int64_t* cand_off, int64_t* tok_off, cudaStream_t st);
 
 cudaError_t launch_route_pack(int64_t n, int32_t world, const int32_t* owner, const uint32_t* records,
                               int32_t rec_words, uint32_t* out, int64_t* counts, int64_t* perm, void* scratch,

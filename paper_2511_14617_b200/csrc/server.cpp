@@ -22,6 +22,10 @@
 #include <thread>
 #include <string>
 #include <unordered_map>
+#include <atomic>
+#include <chrono>
+#include <condition_variable>
+#include <functional>
 #include <vector>
 
 #include "../../include/dgds_b200.h"
@@ -60,6 +64,7 @@ constexpr uint64_t kMaxCap = (0xFFFFFFFFull - kRootCap - 2) / 4 * 4;
 struct PinnedBuf {
   void* p = nullptr;
   size_t cap = 0;
+  unsigned flags = cudaHostAllocDefault;  // cudaHostAllocMapped: kernels may store into it
   ~PinnedBuf() {
     if (p) cudaFreeHost(p);
   }
@@ -68,7 +73,7 @@ struct PinnedBuf {
     if (p) cudaFreeHost(p);
     p = nullptr;
     size_t c = std::max<size_t>(bytes, cap * 2);
-    if (cudaHostAlloc(&p, c, cudaHostAllocDefault) != cudaSuccess) {
+    if (cudaHostAlloc(&p, c, flags) != cudaSuccess) {
       cap = 0;
       return fail(DGDS_ENOMEM, "cudaHostAlloc failed");
     }
@@ -96,6 +101,86 @@ struct DevBuf {
     return DGDS_OK;
   }
 };
+
+// Persistent host workers for the O(n) staging / scatter loops of the host-buffer path
+// (thread creation per call cost more than the work). The caller thread takes part.
+class WorkerPool {
+ public:
+  explicit WorkerPool(int n) {
+    for (int i = 0; i < n; ++i) th_.emplace_back([this] { loop(); });
+  }
+  ~WorkerPool() {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      stop_ = true;
+    }
+    cv_.notify_all();
+    for (auto& t : th_) t.join();
+  }
+  int threads() const { return static_cast<int>(th_.size()) + 1; }
+  // fn(i) for i in [0, tasks), returns when all are done
+  void run(int tasks, const std::function<void(int)>& fn) {
+    if (tasks <= 1 || th_.empty()) {
+      for (int i = 0; i < tasks; ++i) fn(i);
+      return;
+    }
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      fn_ = &fn;
+      tasks_ = tasks;
+      next_.store(0);
+      pending_ = tasks;
+      ++gen_;
+    }
+    cv_.notify_all();
+    work();
+    std::unique_lock<std::mutex> lk(mu_);
+    done_cv_.wait(lk, [this] { return pending_ == 0; });
+    fn_ = nullptr;
+  }
+
+ private:
+  void work() {
+    int done = 0;
+    for (int i = next_.fetch_add(1); i < tasks_; i = next_.fetch_add(1)) {
+      (*fn_)(i);
+      ++done;
+    }
+    if (done) {
+      std::lock_guard<std::mutex> lk(mu_);
+      pending_ -= done;
+      if (pending_ == 0) done_cv_.notify_all();
+    }
+  }
+  void loop() {
+    uint64_t seen = 0;
+    while (true) {
+      {
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_.wait(lk, [&] { return stop_ || gen_ != seen; });
+        if (stop_) return;
+        seen = gen_;
+        if (!fn_) continue;
+      }
+      work();
+    }
+  }
+  std::vector<std::thread> th_;
+  std::mutex mu_;
+  std::condition_variable cv_, done_cv_;
+  const std::function<void(int)>* fn_ = nullptr;
+  int tasks_ = 0;
+  int pending_ = 0;
+  std::atomic<int> next_{0};
+  uint64_t gen_ = 0;
+  bool stop_ = false;
+};
+
+int host_threads() {
+  if (const char* e = std::getenv("DGDS_HOST_THREADS")) return std::max(1, std::atoi(e));
+  const int hc = static_cast<int>(std::thread::hardware_concurrency());
+  return std::max(1, std::min(8, hc - 1));
+}
 
 struct StreamRec {
   uint64_t stored = 0;
@@ -186,8 +271,13 @@ struct dgds_server {
   std::vector<uint64_t> shard_counts;
   uint64_t batch_stamp = 0;
 
-  PinnedBuf h_stage, h_out;
+  PinnedBuf h_stage, h_out;  // h_out is mapped: the copy-out kernel stores results into it
   DevBuf d_stage, d_out;
+  std::unique_ptr<WorkerPool> pool;
+  WorkerPool& workers() {
+    if (!pool) pool = std::make_unique<WorkerPool>(host_threads() - 1);
+    return *pool;
+  }
   int32_t* d_err = nullptr;
   std::mutex mu;  // calls on one handle are serialized
 
@@ -502,18 +592,19 @@ struct LaunchTimer {
 };
 
 // Make `st` (user stream) and the server stream observe one total order.
-struct StreamJoin {
+struct StreamJoin {  // work of a device-API call runs on the caller's stream, ordered after the server's
   dgds_server* s;
   cudaStream_t user;
   cudaEvent_t ev = nullptr;
-  StreamJoin(dgds_server* srv, void* u) : s(srv), user(static_cast<cudaStream_t>(u)) {
-    if (user && user != s->st) {
+  // NULL is the legacy default stream (CUDA convention; torch's default stream), not the server's
+  StreamJoin(dgds_server* srv, void* u) : s(srv), user(u ? static_cast<cudaStream_t>(u) : cudaStreamLegacy) {
+    if (user != s->st) {
       cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
       cudaEventRecord(ev, s->st);
       cudaStreamWaitEvent(user, ev, 0);
     }
   }
-  cudaStream_t stream() const { return (user && user != s->st) ? user : s->st; }
+  cudaStream_t stream() const { return user; }
   ~StreamJoin() {
     if (ev) {
       cudaEventRecord(ev, user);
@@ -528,6 +619,32 @@ struct StreamJoin {
 namespace dgds {
 int set_error(int code, const std::string& msg) { return fail(code, msg); }  // shared with peer.cu
 }  // namespace dgds
+
+namespace {
+// Debug: DGDS_HOST_TIMING=1 prints the host-path phases of each call to stderr.
+struct PhaseClock {
+  bool on;
+  const char* name;
+  std::chrono::steady_clock::time_point t0, last;
+  std::string line;
+  explicit PhaseClock(const char* n) : on(std::getenv("DGDS_HOST_TIMING") != nullptr), name(n) {
+    if (on) t0 = last = std::chrono::steady_clock::now();
+  }
+  void mark(const char* phase) {
+    if (!on) return;
+    auto t = std::chrono::steady_clock::now();
+    line += std::string(" ") + phase + "=" +
+            std::to_string(std::chrono::duration<double, std::micro>(t - last).count()).substr(0, 7);
+    last = t;
+  }
+  ~PhaseClock() {
+    if (on)
+      std::fprintf(stderr, "[%s] total=%.1fus%s\n", name,
+                   std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count(),
+                   line.c_str());
+  }
+};
+}  // namespace
 
 extern "C" {
 
@@ -554,12 +671,15 @@ int dgds_create(const dgds_params* params, dgds_server** out) {
   DGDS_CUDA(cudaSetDevice(p.device));
   auto s = std::make_unique<dgds_server>();
   s->p = p;
+  s->h_out.flags = cudaHostAllocMapped;
   s->D = p.max_pattern_len + p.max_spec_len;
   s->shard_counts.assign(p.shard_count, 0);
   DGDS_CUDA(cudaStreamCreateWithFlags(&s->st, cudaStreamNonBlocking));
   DGDS_CUDA(cudaEventCreateWithFlags(&s->staging_free, cudaEventDisableTiming));
   const uint64_t nodes = p.expected_nodes ? p.expected_nodes : (1ull << 20);
-  uint64_t cap = std::min(cap_for(nodes, 0.5), kMaxCap);  // both multiples of the probe window
+  double init_load = 0.5;  // expected_nodes is an upper bound, so the real load starts lower
+  if (const char* e = std::getenv("DGDS_INIT_LOAD")) init_load = std::min(0.9, std::max(0.05, std::atof(e)));
+  uint64_t cap = std::min(cap_for(nodes, init_load), kMaxCap);  // both multiples of the probe window
   s->T.cap = cap;
   s->T.depth_cap = s->D;
   s->T.lim_pattern = p.max_pattern_len;
@@ -684,6 +804,13 @@ int dgds_shard_group_count(dgds_server* s, int32_t shard, uint64_t* out) {
   return DGDS_OK;
 }
 
+int dgds_index_slots(dgds_server* s, uint64_t* slots) {
+  if (!s || !slots) return fail(DGDS_EINVAL, "null argument");
+  std::lock_guard<std::mutex> lk(s->mu);
+  *slots = s->T.cap;
+  return DGDS_OK;
+}
+
 int dgds_node_count(dgds_server* s, uint64_t* out) {
   std::lock_guard<std::mutex> lk(s->mu);
   cudaSetDevice(s->p.device);
@@ -701,6 +828,7 @@ int dgds_update_batch(dgds_server* s, int64_t n, const int32_t* handles, const i
                       const uint64_t* offs, const int32_t* tokens, double now, dgds_update_reply* rep) {
   if (n < 0) return fail(DGDS_EINVAL, "negative batch size");
   if (n == 0) return DGDS_OK;
+  PhaseClock pc("update_batch");
   std::lock_guard<std::mutex> lk(s->mu);
   DGDS_CUDA(cudaSetDevice(s->p.device));
   const uint64_t ntok = offs[n] - offs[0];
@@ -710,6 +838,7 @@ int dgds_update_batch(dgds_server* s, int64_t n, const int32_t* handles, const i
   std::vector<dgds::AppendPiece> pieces;
   uint64_t worst = 0;
   if (int rc = plan_updates(s, n, handles, rids, prev, offs, nullptr, now, rep, segs, pieces, &worst)) return rc;
+  pc.mark("plan");
   if (segs.empty()) return DGDS_OK;
   if (int rc = ensure_capacity(s, worst)) return rc;
   // one pinned staging block -> one H2D copy: segs | pieces | tokens
@@ -727,6 +856,7 @@ int dgds_update_batch(dgds_server* s, int64_t n, const int32_t* handles, const i
   std::memcpy(h + o_piece, pieces.data(), b_piece);
   std::memcpy(h + o_tok, tokens + offs[0], ntok * sizeof(int32_t));
   char* d = static_cast<char*>(s->d_stage.p);
+  pc.mark("stage");
   DGDS_CUDA(cudaMemcpyAsync(d, h, total, cudaMemcpyHostToDevice, s->st));
   DGDS_CUDA(cudaEventRecord(s->staging_free, s->st));
   {
@@ -787,15 +917,29 @@ int dgds_update_batch_device_strided(dgds_server* s, int64_t n, const int32_t* h
   return update_device_impl(s, n, handles, rids, prev, tok_starts, tok_counts, d_tokens, now, rep, stream);
 }
 
-int dgds_speculate_verify_batch(dgds_server* s, int64_t n, const int32_t* handles, const uint64_t* pat_offs,
-                                const int32_t* patterns, const dgds_spec_args* args, int64_t args_stride,
-                                const int32_t* truth, int32_t truth_stride, const int32_t* truth_left,
-                                const int32_t* limit, dgds_candidates* out, dgds_verify_out* vout) {
-  if (n < 0) return fail(DGDS_EINVAL, "negative batch size");
-  if (n == 0) return DGDS_OK;
-  if (!out) return fail(DGDS_EINVAL, "null output");
-  std::lock_guard<std::mutex> lk(s->mu);
-  DGDS_CUDA(cudaSetDevice(s->p.device));
+}  // extern "C"
+
+namespace {
+
+// One host-buffer query batch: its results live in the mapped pinned block s->h_out
+// (valid until the next host-path call on the server).
+struct HostResult {
+  int64_t n = 0, ncand = 0, ntok = 0;
+  const int64_t* cand_off = nullptr;  // [n + 1]
+  const dgds::CandMeta* meta = nullptr;  // [ncand], candidate_before order within a query
+  const int64_t* tok_off = nullptr;   // [ncand + 1]
+  const int32_t* tokens = nullptr;    // [ntok]
+  const int32_t* verify = nullptr;    // [3][n] drafted | accepted | emitted, or null
+};
+
+// Validate + stage (in parallel on the worker pool), H2D, K2 (+ fused K3), compaction into
+// device memory, one copy-out kernel into the mapped host block, one stream sync.
+// Caller holds s->mu. Nothing is launched unless the whole batch validates.
+int speculate_host(dgds_server* s, int64_t n, const int32_t* handles, const uint64_t* pat_offs,
+                   const int32_t* patterns, const dgds_spec_args* args, int64_t args_stride, const int32_t* truth,
+                   int32_t truth_stride, const int32_t* truth_left, const int32_t* limit, bool verify,
+                   HostResult* r) {
+  PhaseClock pc("speculate_host");
   const int64_t nargs = args_stride ? n : 1;
   int32_t max_k = 1, max_s = 1;
   for (int64_t i = 0; i < nargs; ++i) {
@@ -804,73 +948,86 @@ int dgds_speculate_verify_batch(dgds_server* s, int64_t n, const int32_t* handle
     max_k = std::max(max_k, a.top_k);
     max_s = std::max(max_s, std::min(a.max_spec_tokens, s->p.max_spec_len));
   }
-  for (int64_t i = 0; i < n; ++i) {
-    if (int rc = check_handle(s, handles[i])) return rc;
-    if (pat_offs[i + 1] < pat_offs[i]) return fail(DGDS_EINVAL, "pattern offsets must be nondecreasing");
-  }
-  if (out->k_stride < max_k || out->s_stride < max_s) return fail(DGDS_EBUFFER, "candidate buffer strides too small");
+  if (verify && (!truth || !truth_left || !limit || truth_stride < 0))
+    return fail(DGDS_EINVAL, "verify needs truth inputs");
   const int32_t P = s->p.max_pattern_len;  // only the last max_pattern_len tokens can matter
-  // staging: handles | pat_len | patterns | args
+  // staging: handles | pat_len | patterns | args | truth | truth_left | limit
   const size_t o_len = align_up(n * 4, 256);
   const size_t o_pat = align_up(o_len + n * 4, 256);
   const size_t o_args = align_up(o_pat + static_cast<size_t>(n) * P * 4, 256);
-  const size_t in_total = o_args + nargs * sizeof(dgds_spec_args);
+  const size_t o_tr = align_up(o_args + nargs * sizeof(dgds_spec_args), 256);
+  const size_t o_tl = align_up(o_tr + (verify ? static_cast<size_t>(n) * truth_stride * 4 : 0), 256);
+  const size_t o_lm = align_up(o_tl + (verify ? n * 4 : 0), 256);
+  const size_t in_all = o_lm + (verify ? n * 4 : 0);
   DGDS_CUDA(cudaEventSynchronize(s->staging_free));
-  if (int rc = s->h_stage.ensure(in_total)) return rc;
-  if (int rc = s->d_stage.ensure(in_total)) return rc;
+  pc.mark("staging_wait");
+  if (int rc = s->h_stage.ensure(in_all)) return rc;
+  if (int rc = s->d_stage.ensure(in_all)) return rc;
   char* h = static_cast<char*>(s->h_stage.p);
-  std::memcpy(h, handles, n * 4);
   int32_t* hl = reinterpret_cast<int32_t*>(h + o_len);
   int32_t* hp = reinterpret_cast<int32_t*>(h + o_pat);
-  for (int64_t i = 0; i < n; ++i) {
-    const uint64_t L = pat_offs[i + 1] - pat_offs[i];
-    hl[i] = static_cast<int32_t>(std::min<uint64_t>(L, 0x7FFFFFFF));
-    const uint64_t keep = std::min<uint64_t>(L, static_cast<uint64_t>(P));
-    std::memcpy(hp + i * P, patterns + pat_offs[i + 1] - keep, keep * 4);
+  const size_t ngroups = s->groups.size();
+  WorkerPool& pool = s->workers();
+  const int tasks = n >= 8192 ? 4 * pool.threads() : 1;
+  const int64_t chunk = (n + tasks - 1) / tasks;
+  std::vector<int64_t> bad(tasks, -1);  // first invalid query of each chunk
+  pool.run(tasks, [&](int t) {
+    const int64_t q0 = t * chunk, q1 = std::min<int64_t>(n, q0 + chunk);
+    if (q0 >= q1) return;
+    for (int64_t i = q0; i < q1; ++i) {
+      const int32_t hd = handles[i];
+      if ((hd < 0 || static_cast<size_t>(hd) >= ngroups || pat_offs[i + 1] < pat_offs[i]) && bad[t] < 0) bad[t] = i;
+      const uint64_t L = pat_offs[i + 1] - pat_offs[i];
+      hl[i] = static_cast<int32_t>(std::min<uint64_t>(L, 0x7FFFFFFF));
+      const uint64_t keep = std::min<uint64_t>(L, static_cast<uint64_t>(P));
+      const int32_t* src = patterns + pat_offs[i + 1] - keep;
+      int32_t* dst = hp + i * P;
+      for (uint64_t k = 0; k < keep; ++k) dst[k] = src[k];
+    }
+    std::memcpy(h + q0 * 4, handles + q0, (q1 - q0) * 4);
+    if (verify) {
+      std::memcpy(h + o_tr + static_cast<size_t>(q0) * truth_stride * 4, truth + q0 * truth_stride,
+                  static_cast<size_t>(q1 - q0) * truth_stride * 4);
+      std::memcpy(h + o_tl + q0 * 4, truth_left + q0, (q1 - q0) * 4);
+      std::memcpy(h + o_lm + q0 * 4, limit + q0, (q1 - q0) * 4);
+    }
+  });
+  for (int t = 0; t < tasks; ++t) {
+    if (bad[t] >= 0) {
+      const int64_t i = bad[t];
+      if (int rc = check_handle(s, handles[i])) return rc;
+      return fail(DGDS_EINVAL, "pattern offsets must be nondecreasing");
+    }
   }
   std::memcpy(h + o_args, args, nargs * sizeof(dgds_spec_args));
-  const bool verify = vout != nullptr;
-  size_t o_tr = 0, o_tl = 0, o_lm = 0, in_all = in_total;
-  if (verify) {
-    if (!truth || !truth_left || !limit || truth_stride < 0) return fail(DGDS_EINVAL, "verify needs truth inputs");
-    o_tr = align_up(in_total, 256);
-    o_tl = align_up(o_tr + static_cast<size_t>(n) * truth_stride * 4, 256);
-    o_lm = align_up(o_tl + n * 4, 256);
-    in_all = o_lm + n * 4;
-    if (int rc = s->h_stage.ensure(in_all)) return rc;
-    if (int rc = s->d_stage.ensure(in_all)) return rc;
-    h = static_cast<char*>(s->h_stage.p);
-    std::memcpy(h, handles, n * 4);  // re-stage after a possible reallocation
-    hl = reinterpret_cast<int32_t*>(h + o_len);
-    hp = reinterpret_cast<int32_t*>(h + o_pat);
-    for (int64_t i = 0; i < n; ++i) {
-      const uint64_t Lp = pat_offs[i + 1] - pat_offs[i];
-      hl[i] = static_cast<int32_t>(std::min<uint64_t>(Lp, 0x7FFFFFFF));
-      const uint64_t keep = std::min<uint64_t>(Lp, static_cast<uint64_t>(P));
-      std::memcpy(hp + i * P, patterns + pat_offs[i + 1] - keep, keep * 4);
-    }
-    std::memcpy(h + o_args, args, nargs * sizeof(dgds_spec_args));
-    std::memcpy(h + o_tr, truth, static_cast<size_t>(n) * truth_stride * 4);
-    std::memcpy(h + o_tl, truth_left, n * 4);
-    std::memcpy(h + o_lm, limit, n * 4);
-  }
-  // device outputs (internal strides), one pinned block back
+  pc.mark("validate_stage");
+  // device outputs (internal strides) + compaction scratch
   const int32_t K = max_k, Sx = max_s;
+  const int64_t nk = static_cast<int64_t>(n) * K;
   const size_t o_sc = 0;
-  const size_t o_sp = align_up(o_sc + n * K * 8, 256);
-  const size_t o_nc = align_up(o_sp + n * K * 8, 256);
+  const size_t o_sp = align_up(o_sc + nk * 8, 256);
+  const size_t o_nc = align_up(o_sp + nk * 8, 256);
   const size_t o_ln = align_up(o_nc + n * 4, 256);
-  const size_t o_tk = align_up(o_ln + n * K * 4, 256);
-  const size_t o_v = align_up(o_tk + static_cast<size_t>(n) * K * Sx * 4, 256);
-  // compacted results: [totals | n_cands | verify] then [meta | tokens]
+  const size_t o_tk = align_up(o_ln + nk * 4, 256);
+  const size_t o_v = align_up(o_tk + static_cast<size_t>(nk) * Sx * 4, 256);
   const int64_t nblk = (n + 255) / 256;
   const size_t o_bs = align_up(o_v + (verify ? static_cast<size_t>(n) * 12 : 0), 256);
   const size_t o_cmeta = align_up(o_bs + static_cast<size_t>(nblk) * 16 + 16, 256);
-  const size_t o_ctok = align_up(o_cmeta + static_cast<size_t>(n) * K * sizeof(dgds::CandMeta), 256);
-  const size_t dev_total = o_ctok + static_cast<size_t>(n) * K * Sx * 4;
+  const size_t o_ctoff = align_up(o_cmeta + nk * sizeof(dgds::CandMeta), 256);
+  const size_t o_ccoff = align_up(o_ctoff + nk * 8, 256);
+  const size_t o_ctok = align_up(o_ccoff + (n + 1) * 8, 256);
+  const size_t dev_total = o_ctok + static_cast<size_t>(nk) * Sx * 4;
   if (int rc = s->d_out.ensure(dev_total)) return rc;
+  // mapped host block: totals | cand_off | verify | meta | tok_off | tokens
+  const size_t h_coff = 256;
+  const size_t h_v = align_up(h_coff + (n + 1) * 8, 256);
+  const size_t h_meta = align_up(h_v + (verify ? n * 12 : 0), 256);
+  const size_t h_toff = align_up(h_meta + nk * sizeof(dgds::CandMeta), 256);
+  const size_t h_tok = align_up(h_toff + (nk + 1) * 8, 256);
+  if (int rc = s->h_out.ensure(h_tok + static_cast<size_t>(nk) * Sx * 4)) return rc;
   char* d = static_cast<char*>(s->d_stage.p);
   char* dout = static_cast<char*>(s->d_out.p);
+  char* ho = static_cast<char*>(s->h_out.p);
   DGDS_CUDA(cudaMemcpyAsync(d, h, in_all, cudaMemcpyHostToDevice, s->st));
   DGDS_CUDA(cudaEventRecord(s->staging_free, s->st));
   dgds::QueryLaunch L{};
@@ -909,74 +1066,128 @@ int dgds_speculate_verify_batch(dgds_server* s, int64_t n, const int32_t* handle
   long long* d_bs = reinterpret_cast<long long*>(dout + o_bs);
   long long* d_tot = d_bs + 2 * nblk;
   auto* d_meta = reinterpret_cast<dgds::CandMeta*>(dout + o_cmeta);
+  auto* d_toff = reinterpret_cast<int64_t*>(dout + o_ctoff);
+  auto* d_coff = reinterpret_cast<int64_t*>(dout + o_ccoff);
   int32_t* d_ctok = reinterpret_cast<int32_t*>(dout + o_ctok);
   DGDS_CUDA(dgds::launch_compact(n, K, Sx, L.n_cands, L.lens, L.scores, L.supports, L.tokens, d_bs, d_tot, d_meta,
-                                 d_ctok, s->st));
-  // host block 1: totals | n_cands | verify ; block 2: meta | tokens
-  const size_t h1 = 16 + static_cast<size_t>(n) * 4 + (verify ? static_cast<size_t>(n) * 12 : 0);
-  const size_t h_meta_max = static_cast<size_t>(n) * K * sizeof(dgds::CandMeta);
-  if (int rc = s->h_out.ensure(align_up(h1, 256) + h_meta_max + static_cast<size_t>(n) * K * Sx * 4)) return rc;
-  char* ho = static_cast<char*>(s->h_out.p);
-  DGDS_CUDA(cudaMemcpyAsync(ho, d_tot, 16, cudaMemcpyDeviceToHost, s->st));
-  DGDS_CUDA(cudaMemcpyAsync(ho + 16, dout + o_nc, n * 4, cudaMemcpyDeviceToHost, s->st));
-  if (verify) DGDS_CUDA(cudaMemcpyAsync(ho + 16 + n * 4, dout + o_v, n * 12, cudaMemcpyDeviceToHost, s->st));
-  DGDS_CUDA(cudaStreamSynchronize(s->st));
-  const long long ncand = reinterpret_cast<const long long*>(ho)[0];
-  const long long ntok = reinterpret_cast<const long long*>(ho)[1];
-  char* hm = ho + align_up(h1, 256);
-  char* ht = hm + ncand * sizeof(dgds::CandMeta);
-  if (ncand > 0) {
-    DGDS_CUDA(cudaMemcpyAsync(hm, d_meta, ncand * sizeof(dgds::CandMeta), cudaMemcpyDeviceToHost, s->st));
-    if (ntok > 0) DGDS_CUDA(cudaMemcpyAsync(ht, d_ctok, ntok * 4, cudaMemcpyDeviceToHost, s->st));
-    DGDS_CUDA(cudaStreamSynchronize(s->st));
-  }
-  s->last_d2h_bytes = 16 + n * 4 + (verify ? n * 12 : 0) + ncand * sizeof(dgds::CandMeta) + ntok * 4;
-  const int32_t* nc = reinterpret_cast<const int32_t*>(ho + 16);
-  const auto* meta = reinterpret_cast<const dgds::CandMeta*>(hm);
-  const int32_t* tk = reinterpret_cast<const int32_t*>(ht);
-  // scatter into the caller's strided buffers, in parallel chunks
-  const int nthreads = n >= 16384 ? 8 : 1;
-  std::vector<int64_t> cstart(nthreads + 1, 0), tstart(nthreads + 1, 0);
-  const int64_t chunk = (n + nthreads - 1) / nthreads;
-  {
-    int64_t c = 0, t = 0, q = 0;
-    for (int w = 0; w < nthreads; ++w) {
-      cstart[w] = c;
-      tstart[w] = t;
-      const int64_t qe = std::min<int64_t>(n, (w + 1) * chunk);
-      for (; q < qe; ++q) {
-        for (int j = 0; j < nc[q]; ++j) t += meta[c + j].len;
-        c += nc[q];
-      }
-    }
-  }
-  auto work = [&](int w) {
-    int64_t c = cstart[w], t = tstart[w];
-    const int64_t qe = std::min<int64_t>(n, (w + 1) * chunk);
-    for (int64_t q = w * chunk; q < qe; ++q) {
-      out->n_cands[q] = nc[q];
-      for (int j = 0; j < nc[q]; ++j, ++c) {
-        const int64_t di = q * out->k_stride + j;
-        out->lens[di] = meta[c].len;
-        out->scores[di] = meta[c].score;
-        out->supports[di] = meta[c].support;
-        std::memcpy(out->tokens + di * out->s_stride, tk + t, meta[c].len * 4);
-        t += meta[c].len;
-      }
-    }
+                                 d_ctok, d_coff, d_toff, s->st));
+  dgds::CopyOutRegions R{};
+  auto region = [&](const void* src, size_t dst_off, int idx, int elem, int64_t fixed) {
+    const int i = R.n++;
+    R.src[i] = static_cast<const char*>(src);
+    R.dst[i] = ho + dst_off;
+    R.total_idx[i] = idx;
+    R.elem_bytes[i] = elem;
+    R.fixed_bytes[i] = fixed;
   };
-  if (nthreads == 1) {
-    work(0);
-  } else {
-    std::vector<std::thread> th;
-    for (int w = 0; w < nthreads; ++w) th.emplace_back(work, w);
-    for (auto& x : th) x.join();
+  region(d_tot, 0, -1, 0, 16);
+  region(d_coff, h_coff, -1, 0, n * 8);
+  if (verify) region(dout + o_v, h_v, -1, 0, n * 12);
+  region(d_meta, h_meta, 0, sizeof(dgds::CandMeta), 0);
+  region(d_toff, h_toff, 0, 8, 0);
+  region(d_ctok, h_tok, 1, 4, 0);
+  DGDS_CUDA(dgds::launch_copy_out(d_tot, R, static_cast<int64_t>(nk) * (sizeof(dgds::CandMeta) + 8 + Sx * 4),
+                                  s->st));
+  pc.mark("launch");
+  DGDS_CUDA(cudaStreamSynchronize(s->st));
+  pc.mark("device_wait");
+  r->n = n;
+  r->ncand = reinterpret_cast<const long long*>(ho)[0];
+  r->ntok = reinterpret_cast<const long long*>(ho)[1];
+  auto* coff = reinterpret_cast<int64_t*>(ho + h_coff);
+  auto* toff = reinterpret_cast<int64_t*>(ho + h_toff);
+  coff[n] = r->ncand;
+  toff[r->ncand] = r->ntok;
+  r->cand_off = coff;
+  r->meta = reinterpret_cast<const dgds::CandMeta*>(ho + h_meta);
+  r->tok_off = toff;
+  r->tokens = reinterpret_cast<const int32_t*>(ho + h_tok);
+  r->verify = verify ? reinterpret_cast<const int32_t*>(ho + h_v) : nullptr;
+  s->last_d2h_bytes = 16 + (n + 1) * 8 + (verify ? n * 12 : 0) + r->ncand * (sizeof(dgds::CandMeta) + 8) + r->ntok * 4;
+  return DGDS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int dgds_speculate_verify_batch(dgds_server* s, int64_t n, const int32_t* handles, const uint64_t* pat_offs,
+                                const int32_t* patterns, const dgds_spec_args* args, int64_t args_stride,
+                                const int32_t* truth, int32_t truth_stride, const int32_t* truth_left,
+                                const int32_t* limit, dgds_candidates* out, dgds_verify_out* vout) {
+  if (n < 0) return fail(DGDS_EINVAL, "negative batch size");
+  if (n == 0) return DGDS_OK;
+  if (!out) return fail(DGDS_EINVAL, "null output");
+  std::lock_guard<std::mutex> lk(s->mu);
+  DGDS_CUDA(cudaSetDevice(s->p.device));
+  {
+    const int64_t nargs = args_stride ? n : 1;
+    int32_t max_k = 1, max_s = 1;
+    for (int64_t i = 0; i < nargs; ++i) {
+      if (int rc = check_args(args[i * args_stride])) return rc;
+      max_k = std::max(max_k, args[i * args_stride].top_k);
+      max_s = std::max(max_s, std::min(args[i * args_stride].max_spec_tokens, s->p.max_spec_len));
+    }
+    if (out->k_stride < max_k || out->s_stride < max_s)
+      return fail(DGDS_EBUFFER, "candidate buffer strides too small");
   }
-  if (verify) {
-    const int32_t* hv = reinterpret_cast<const int32_t*>(ho + 16 + n * 4);
-    std::memcpy(vout->drafted, hv, n * 4);
-    std::memcpy(vout->accepted, hv + n, n * 4);
-    std::memcpy(vout->emitted, hv + 2 * n, n * 4);
+  HostResult r;
+  if (int rc = speculate_host(s, n, handles, pat_offs, patterns, args, args_stride, truth, truth_stride, truth_left,
+                              limit, vout != nullptr, &r))
+    return rc;
+  PhaseClock pc("scatter");
+  // scatter into the caller's strided buffers, in parallel chunks (per-query offsets are known)
+  WorkerPool& pool = s->workers();
+  const int tasks = n >= 8192 ? 4 * pool.threads() : 1;
+  const int64_t chunk = (n + tasks - 1) / tasks;
+  pool.run(tasks, [&](int t) {
+    const int64_t q0 = t * chunk, q1 = std::min<int64_t>(n, q0 + chunk);
+    for (int64_t q = q0; q < q1; ++q) {
+      const int64_t c0 = r.cand_off[q], c1 = r.cand_off[q + 1];
+      out->n_cands[q] = static_cast<int32_t>(c1 - c0);
+      for (int64_t c = c0; c < c1; ++c) {
+        const int64_t di = q * out->k_stride + (c - c0);
+        const dgds::CandMeta& m = r.meta[c];
+        out->lens[di] = m.len;
+        out->scores[di] = m.score;
+        out->supports[di] = m.support;
+        std::memcpy(out->tokens + di * out->s_stride, r.tokens + r.tok_off[c], m.len * 4);
+      }
+    }
+    if (vout && q0 < q1) {
+      std::memcpy(vout->drafted + q0, r.verify + q0, (q1 - q0) * 4);
+      std::memcpy(vout->accepted + q0, r.verify + n + q0, (q1 - q0) * 4);
+      std::memcpy(vout->emitted + q0, r.verify + 2 * n + q0, (q1 - q0) * 4);
+    }
+  });
+  return DGDS_OK;
+}
+
+int dgds_speculate_verify_view(dgds_server* s, int64_t n, const int32_t* handles, const uint64_t* pat_offs,
+                               const int32_t* patterns, const dgds_spec_args* args, int64_t args_stride,
+                               const int32_t* truth, int32_t truth_stride, const int32_t* truth_left,
+                               const int32_t* limit, dgds_result_view* out) {
+  if (n < 0) return fail(DGDS_EINVAL, "negative batch size");
+  if (!out) return fail(DGDS_EINVAL, "null output");
+  *out = dgds_result_view{};
+  if (n == 0) return DGDS_OK;
+  std::lock_guard<std::mutex> lk(s->mu);
+  DGDS_CUDA(cudaSetDevice(s->p.device));
+  HostResult r;
+  if (int rc = speculate_host(s, n, handles, pat_offs, patterns, args, args_stride, truth, truth_stride, truth_left,
+                              limit, truth != nullptr, &r))
+    return rc;
+  out->n_queries = n;
+  out->n_cands = r.ncand;
+  out->n_tokens = r.ntok;
+  out->cand_off = r.cand_off;
+  out->cands = reinterpret_cast<const dgds_cand_meta*>(r.meta);
+  out->tok_off = r.tok_off;
+  out->tokens = r.tokens;
+  if (r.verify) {
+    out->drafted = r.verify;
+    out->accepted = r.verify + n;
+    out->emitted = r.verify + 2 * n;
   }
   return DGDS_OK;
 }

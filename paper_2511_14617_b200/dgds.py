@@ -199,6 +199,11 @@ class DraftServer:
         check(lib().dgds_node_count(self._h, C.byref(out)))
         return int(out.value)
 
+    def index_slots(self) -> int:
+        out = C.c_uint64()
+        check(lib().dgds_index_slots(self._h, C.byref(out)))
+        return int(out.value)
+
     def update_cst(self, group_id: str, request_id: int, prev_token_count: int, new_tokens: Sequence[int],
                    now: float) -> UpdateReply:
         return self.update_batch([group_id], [request_id], [prev_token_count], [new_tokens], now)[0]
@@ -303,6 +308,30 @@ class DraftServer:
                                          args_stride, C.byref(out.c())))
         return out
 
+    def speculate_view(self, handles: np.ndarray, pat_offsets: np.ndarray, patterns: np.ndarray, args: np.ndarray,
+                       args_stride: int, truth: Optional[np.ndarray] = None, truth_left: Optional[np.ndarray] = None,
+                       limit: Optional[np.ndarray] = None) -> "ResultView":
+        """Batch query (+ fused verification when `truth` is given) returning compact per-query
+        candidate lists as zero-copy views of the server's pinned result block
+        (dgds_speculate_verify_view) — valid until the next query call on this server."""
+        n = len(handles)
+        handles = np.ascontiguousarray(handles, np.int32)
+        pat_offsets = np.ascontiguousarray(pat_offsets, np.uint64)
+        patterns = np.ascontiguousarray(patterns, np.int32)
+        args = np.ascontiguousarray(args, ARGS_DTYPE)
+        v = _lib.ResultView()
+        if truth is not None:
+            truth = np.ascontiguousarray(truth, np.int32).reshape(n, -1)
+            tl = np.ascontiguousarray(truth_left, np.int32)
+            lm = np.ascontiguousarray(limit, np.int32)
+            check(lib().dgds_speculate_verify_view(self._h, n, _ptr(handles), _ptr(pat_offsets), _ptr(patterns),
+                                                   _ptr(args), args_stride, _ptr(truth), truth.shape[1], _ptr(tl),
+                                                   _ptr(lm), C.byref(v)))
+        else:
+            check(lib().dgds_speculate_verify_view(self._h, n, _ptr(handles), _ptr(pat_offsets), _ptr(patterns),
+                                                   _ptr(args), args_stride, None, 0, None, None, C.byref(v)))
+        return ResultView(v)
+
     def verify_batch(self, cands: "CandidateBatch", truth: np.ndarray, truth_left: np.ndarray, limit: np.ndarray):
         """Instance::decode_step verification (engine.cpp:115-143) on the GPU."""
         n = cands.n
@@ -316,6 +345,42 @@ class DraftServer:
         check(lib().dgds_verify_batch(self._h, n, C.byref(cands.c()), _ptr(truth), truth.shape[1], _ptr(tl), _ptr(lm),
                                       C.byref(vo)))
         return dr, ac, em
+
+
+CAND_META_DTYPE = np.dtype([("score", np.float64), ("support", np.int64), ("len", np.int32),
+                            ("reserved", np.int32)])
+
+
+def _as_np(ptr: Optional[int], n: int, ctype, dtype=None) -> Optional[np.ndarray]:
+    if not ptr:
+        return None if dtype is None and ctype is None else np.zeros(0, dtype or np.int32)
+    a = np.ctypeslib.as_array(C.cast(ptr, C.POINTER(ctype)), shape=(n,))
+    return a.view(dtype) if dtype is not None else a
+
+
+class ResultView:
+    """dgds_result_view as numpy arrays over the server's pinned block (no copy).
+    candidates of query q: cands[cand_off[q]:cand_off[q + 1]]; tokens of candidate c:
+    tokens[tok_off[c]:tok_off[c + 1]]."""
+
+    def __init__(self, v: _lib.ResultView):
+        n, m, t = v.n_queries, v.n_cands, v.n_tokens
+        self.n = n
+        self.cand_off = _as_np(v.cand_off, n + 1, C.c_int64) if n else np.zeros(1, np.int64)
+        raw = _as_np(v.cands, m * CAND_META_DTYPE.itemsize, C.c_uint8) if m else np.zeros(0, np.uint8)
+        self.cands = raw.view(CAND_META_DTYPE)
+        self.tok_off = _as_np(v.tok_off, m + 1, C.c_int64) if n else np.zeros(1, np.int64)
+        self.tokens = _as_np(v.tokens, t, C.c_int32) if t else np.zeros(0, np.int32)
+        self.drafted = _as_np(v.drafted, n, C.c_int32) if v.drafted else None
+        self.accepted = _as_np(v.accepted, n, C.c_int32) if v.accepted else None
+        self.emitted = _as_np(v.emitted, n, C.c_int32) if v.emitted else None
+
+    def candidates(self, q: int) -> List[DraftCandidate]:
+        out = []
+        for c in range(int(self.cand_off[q]), int(self.cand_off[q + 1])):
+            toks = tuple(int(x) for x in self.tokens[self.tok_off[c]:self.tok_off[c + 1]])
+            out.append(DraftCandidate(toks, float(self.cands["score"][c]), int(self.cands["support"][c])))
+        return out
 
 
 class CandidateBatch:

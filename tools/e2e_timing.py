@@ -40,9 +40,15 @@ for step in range(12):
     t1 = time.perf_counter()
     srv.update_arrays(hs[live], rid[live], prev, offs, toks, 0.0)
     t2 = time.perf_counter()
-    _lib.check(L.dgds_speculate_verify_batch(srv.handle, Q, qh.ctypes.data, poff.ctypes.data, pat.ctypes.data,
-                                              sp_args.ctypes.data, 0, tru.ctypes.data, dl, tl.ctypes.data,
-                                              tl.ctypes.data, C.byref(cb.c()), C.byref(vo)))
+    if os.environ.get("E2E_VIEW"):
+        v = _lib.ResultView()
+        _lib.check(L.dgds_speculate_verify_view(srv.handle, Q, qh.ctypes.data, poff.ctypes.data, pat.ctypes.data,
+                                                 sp_args.ctypes.data, 0, tru.ctypes.data, dl, tl.ctypes.data,
+                                                 tl.ctypes.data, C.byref(v)))
+    else:
+        _lib.check(L.dgds_speculate_verify_batch(srv.handle, Q, qh.ctypes.data, poff.ctypes.data, pat.ctypes.data,
+                                                  sp_args.ctypes.data, 0, tru.ctypes.data, dl, tl.ctypes.data,
+                                                  tl.ctypes.data, C.byref(cb.c()), C.byref(vo)))
     t3 = time.perf_counter()
     pos[live] += ns
     print(f"step {step}: prep {1e3*(t1-t0):.2f} ms  update {1e3*(t2-t1):.2f} ms ({len(live)} recs, {int(offs[-1])} tok)  "
