@@ -160,9 +160,9 @@ def run_multi(args, world, rank, local, dev):
     use_px = args.route == "px"
     if use_px:
         # NVLink peer-memory exchange: q rows -> owners, replies -> senders, append rows -> owners
-        px = PeerExchange(world, rank, local, {"q": (capq, QRY_W), "rep": (capq, rep_w), "a": (capa, APP_W)})
-        q_slot = [torch.empty(Q, dtype=torch.int64, device=dev) for _ in range(2)]
-        a_slot = [torch.empty(max(1, len(produced)), dtype=torch.int64, device=dev) for _ in range(2)]
+        # replies land in a shared slab in query order: the query record's pad word carries its index
+        px = PeerExchange(world, rank, local, {"q": (capq, QRY_W), "rep": (Q, rep_w, "shared"),
+                                               "a": (capa, APP_W)})
         rep_view = {p: px.slab("rep", p) for p in (1, 2)}  # parity 1, 0
         a_meta = {p: px.slab("a", p)[:, :5] for p in (1, 2)}
         a_cnt = {p: px.counts("a", p) for p in (1, 2)}
@@ -181,8 +181,7 @@ def run_multi(args, world, rank, local, dev):
                 # (queued after that K1 on their streams) prove it is free
                 if s > 0:
                     side.wait_event(ev_rep[(s - 1) % 2])
-                n_a = inp["app"].shape[0]
-                px.send("a", inp["app_owner"], inp["app"], seq, stable=True, slot=a_slot[k][:n_a], stream=side)
+                px.send("a", inp["app_owner"], inp["app"], seq, stable=True, want_slot=False, stream=side)
                 px.wait("a", seq, stream=side)
                 meta_bufs[k].copy_(a_meta[par], non_blocking=True)
                 cnt_bufs[k].copy_(a_cnt[par], non_blocking=True)
@@ -210,12 +209,13 @@ def run_multi(args, world, rank, local, dev):
         if use_px:
             # (1)+(2) queries stored into the owners' slabs; the owner's K2+K3 stores each reply
             # straight into its sender's reply slab; (3) gather into query order
-            px.send("q", inp["q_owner"], inp["q"], seq, slot=q_slot[k], stream=main)
+            px.send("q", inp["q_owner"], inp["q"], seq, origin_word=QRY_W - 1, want_slot=False, stream=main)
             t0 = mark("q_fwd", t0)
-            speculate_routed(srv, px, "q", "rep", seq, layout, sp_args, kq, dl, d_stats if stats else None, main)
+            speculate_routed(srv, px, "q", "rep", seq, layout, sp_args, kq, dl, d_stats if stats else None, main,
+                             origin_field=QRY_W - 1)
             t0 = mark("q_kernel", t0)
             px.wait("rep", seq, stream=main)
-            back = cuda_unpack(rep_view[2 - seq % 2], q_slot[k])
+            back = rep_view[2 - seq % 2]  # [Q, rep_w] in query order, no gather
             ev_rep[k].record(main)
             t0 = mark("q_rev", t0)
         else:
@@ -285,6 +285,8 @@ def run_multi(args, world, rank, local, dev):
         torch.cuda.synchronize()
     if tp is not None:
         tp.__exit__(None, None, None)
+        os.makedirs("gpurun_out", exist_ok=True)
+        tp.export_chrome_trace(f"gpurun_out/trace_r{rank}.json")
         if rank == 0:
             print(tp.key_averages().table(sort_by="cuda_time_total", row_limit=22), flush=True)
             print(tp.key_averages().table(sort_by="cpu_time_total", row_limit=22), flush=True)
@@ -294,8 +296,8 @@ def run_multi(args, world, rank, local, dev):
     T = ms.item() / 1e3
     _lib.check(L.dgds_profile_read(srv.handle, C.byref(prof), 1))
     # our launches in the timed region: K1 + K2/K3 (server profile), plus the routing kernels —
-    # px send/wait/signal (counted by the exchange) and one gather per step
-    route_launches = (px.status()[1] - px_l0 + K) if use_px else 0
+    # px send/wait/signal (counted by the exchange)
+    route_launches = (px.status()[1] - px_l0) if use_px else 0
     tot = torch.tensor([sum(steps_in[s]["ntok"] for s in range(W, W + K)), int(d_stats[7].item()),
                         app_alg_owner[0], prof.query_ms * 1e3, prof.append_ms * 1e3,
                         prof.query_launches + prof.append_launches + route_launches], dtype=torch.float64,

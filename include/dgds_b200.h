@@ -260,12 +260,15 @@ int dgds_speculate_verify_view(dgds_server* s, int64_t n, const int32_t* handles
 
 /* Segmented form for owner routing: rows arrive as n_seg sender segments of seg_rows rows
  * (row j of segment s valid while j < d_seg_count[s]); the reply of row j of segment s is
- * written to seg_out[s] + j * reply_words — typically the sender's receive slab in NVLink
+ * written to seg_out[s] + r * reply_words with r = j, or with origin_field >= 0 r = the
+ * record's word origin_field (the query's index at its sender, stamped by dgds_px_send) —
+ * so replies land in the sender's final order, typically straight into its region in NVLink
  * peer memory (dgds_px_region). seg_out is a host array of n_seg device pointers. */
 int dgds_speculate_records_seg(dgds_server* s, int32_t n_seg, int64_t seg_rows, const int32_t* d_records,
                                const int32_t* d_seg_count, const dgds_query_record_layout* layout,
                                const dgds_spec_args* d_args, int64_t args_stride, int32_t max_top_k,
-                               int32_t max_spec, int32_t* const* seg_out, dgds_query_stats* d_stats, void* stream);
+                               int32_t max_spec, int32_t* const* seg_out, int32_t origin_field,
+                               dgds_query_stats* d_stats, void* stream);
 
 /* Verification of existing candidates (engine.cpp:115-143), host buffers. */
 int dgds_verify_batch(dgds_server* s, int64_t n, const dgds_candidates* cands, const int32_t* truth_next,
@@ -349,12 +352,13 @@ int dgds_px_connect_local(dgds_px* const* all, int32_t world);
 int dgds_px_region(dgds_px* px, int32_t peer, void** base);
 /* Send record i (rec_words int32) to rank d_owner[i] (owners outside [0, world) are dropped):
  * rows are written into the owner's slab, then counts and flag = seq are published.
- * d_slot[i] = owner * cap + row (where the owner's reply lands in this rank's reply slab) or -1.
- * stable != 0 keeps record order per owner (one CTA); otherwise rows are unordered.
+ * d_slot (optional) [i] = owner * cap + row, or -1. origin_word >= 0 overwrites that word of
+ * each delivered row with i (for replies stored in the sender's order). stable != 0 keeps
+ * record order per owner (one CTA); otherwise rows are unordered.
  * Rows beyond cap set *d_overflow = 1 (sticky) and are dropped. */
 int dgds_px_send(dgds_px* px, int64_t n, const int32_t* d_owner, const int32_t* d_records, int32_t rec_words,
                  int64_t cap, uint64_t slab_off, uint64_t count_off, uint64_t flag_off, uint64_t seq,
-                 int32_t stable, int64_t* d_slot, int32_t* d_overflow, void* stream);
+                 int32_t stable, int32_t origin_word, int64_t* d_slot, int32_t* d_overflow, void* stream);
 /* Kernels enqueued after this see every sender's data of exchange `seq` (bounded spin). */
 int dgds_px_wait(dgds_px* px, uint64_t flag_off, uint64_t seq, void* stream);
 /* Publish flag = seq to every peer after the work already enqueued on `stream`. */

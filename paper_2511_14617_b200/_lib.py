@@ -168,13 +168,13 @@ EXPORTS = {
     "dgds_speculate_records": (C.c_int, [_P, _I64, _P, C.POINTER(RecordLayout), _P, _I64, _I32, _I32, _P, _P, _P]),
     "dgds_speculate_verify_view": (C.c_int, [_P, _I64, _P, _P, _P, _P, _I64, _P, _I32, _P, _P, C.POINTER(ResultView)]),
     "dgds_speculate_records_seg": (C.c_int, [_P, _I32, _I64, _P, _P, C.POINTER(RecordLayout), _P, _I64, _I32, _I32,
-                                             C.POINTER(C.c_void_p), _P, _P]),
+                                             C.POINTER(C.c_void_p), _I32, _P, _P]),
     "dgds_generate_workload": (C.c_int, [C.POINTER(WorkloadCfg), _P, _P, _P]),
     "dgds_px_create": (C.c_int, [_I32, _I32, _I32, _U64, C.POINTER(C.c_void_p), _P]),
     "dgds_px_connect": (C.c_int, [_P, _P]),
     "dgds_px_connect_local": (C.c_int, [C.POINTER(C.c_void_p), _I32]),
     "dgds_px_region": (C.c_int, [_P, _I32, C.POINTER(C.c_void_p)]),
-    "dgds_px_send": (C.c_int, [_P, _I64, _P, _P, _I32, _I64, _U64, _U64, _U64, _U64, _I32, _P, _P, _P]),
+    "dgds_px_send": (C.c_int, [_P, _I64, _P, _P, _I32, _I64, _U64, _U64, _U64, _U64, _I32, _I32, _P, _P, _P]),
     "dgds_px_wait": (C.c_int, [_P, _U64, _U64, _P]),
     "dgds_px_signal": (C.c_int, [_P, _U64, _U64, _P]),
     "dgds_px_status": (C.c_int, [_P, C.POINTER(_I32), C.POINTER(_U64)]),

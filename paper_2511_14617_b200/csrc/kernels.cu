@@ -802,7 +802,8 @@ __global__ void __launch_bounds__(kBlock, 4) k_query(QueryLaunch P) {
     int32_t* R;
     if (P.seg_rows > 0) {
       const int64_t sg = q / P.seg_rows;
-      R = P.seg_out[sg] + (q - sg * P.seg_rows) * P.rec_words_out;
+      const int64_t row = P.seg_origin ? static_cast<int64_t>(P.seg_origin[q * P.in_qstride]) : q - sg * P.seg_rows;
+      R = P.seg_out[sg] + row * P.rec_words_out;
     } else {
       R = P.rec_out + q * P.rec_words_out;
     }

@@ -82,6 +82,7 @@ struct QueryLaunch {
   int32_t* rec_out;
   int64_t seg_rows;
   const int32_t* seg_count;
+  const int32_t* seg_origin;  // optional: the reply row is seg_origin[q * in_qstride] instead of j
   int32_t* seg_out[kMaxSegments];
 };
 

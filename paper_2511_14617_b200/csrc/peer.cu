@@ -6,12 +6,11 @@
 // set of double-buffered slabs [parity][sender][rows][words] plus per-sender
 // counts and a monotone sequence flag in each receiver's region:
 //
-//   k_px_send   — scatters records into slab rows of their owners (the owner's
-//                 region, over NVLink) and, in its last block, publishes the
-//                 per-owner counts followed by flag = seq with a system-scope
-//                 release. Slot allocation is warp-aggregated atomics
-//                 (unordered; queries) or a one-block stable partition (appends,
-//                 whose per-stream order matters).
+//   send        — k_px_count + k_px_scatter: a two-pass stable partition that
+//                 stores each record into its owner's slab (over NVLink) in record
+//                 order per owner, every thread fencing its own stores at system
+//                 scope; then k_px_publish stores the per-owner counts, fences
+//                 once and stores flag = seq in every receiver.
 //   k_px_wait   — one thread per sender spins (acquire, bounded) until the
 //                 sender's flag reaches seq; the kernels after it read the slab.
 //   k_px_signal — after the kernels that wrote replies into peers' slabs,
@@ -23,12 +22,17 @@
 
 #include <cstdint>
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
 
 #include "../../include/dgds_b200.h"
 #include "kernels.h"
+
+#ifndef DGDS_PX_FENCE
+#define DGDS_PX_FENCE 1  // 0: fence.sc.sys, 1: fence.acq_rel.sys, 2: (experiment) no per-thread fence
+#endif
 
 namespace {
 
@@ -46,6 +50,18 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long
 }
 __device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
   asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+// Release-pattern fence (prior stores before later stores, system scope). Lighter than the
+// sequentially consistent fence.sc.sys behind __threadfence_system().
+__device__ __forceinline__ void fence_release_sys() {
+#if DGDS_PX_FENCE == 0
+  __threadfence_system();
+#else
+  asm volatile("fence.acq_rel.sys;" ::: "memory");
+#endif
+}
+__device__ __forceinline__ void st_relaxed_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 __device__ __forceinline__ unsigned long long global_ns() {
   unsigned long long t;
@@ -68,6 +84,7 @@ struct SendArgs {
   int64_t* slot;        // per record: owner * cap + row, or -1 (not routed / overflow)
   int32_t* overflow;    // set to 1 when an owner receives more than cap rows (sticky)
   int32_t* cursor;      // [kMaxWorld] per-owner row cursors (zero between launches)
+  int32_t origin_word;  // >= 0: that word of each copied row is set to the record's source index
   unsigned* done;       // finished-block counter (zero between launches)
 };
 
@@ -75,84 +92,122 @@ __device__ __forceinline__ int32_t* dst_row(const SendArgs& A, int o, int64_t ro
   return reinterpret_cast<int32_t*>(A.peers.base[o] + A.slab_off) + (A.rank * A.cap + row) * A.words;
 }
 
-// Last block: publish counts, then the flag, to every receiver; reset the cursors.
-__device__ void publish(const SendArgs& A) {
-  __shared__ bool last;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence_system();  // this block's stores (observed through the barrier) before the count
-    last = atomicAdd(A.done, 1u) == gridDim.x - 1;
+// Copies the warp's nrec records (sources rec[w0 + r]) to their destination rows, lanes
+// walking the (record, word) pairs linearly so each store instruction covers contiguous words.
+// Optionally stamps word `origin_word` of the copy with the record's source index.
+__device__ __forceinline__ void warp_copy_rows(const SendArgs& A, int64_t w0, int nrec, int my_owner,
+                                               int64_t my_row, int lane) {
+  constexpr int kBatch = 24;  // loads in flight per lane before the stores (a warp's 32 rows of <= 24 words: one batch)
+  const int W = A.words;
+  const int total = nrec * W;
+  for (int base = 0; base < total; base += 32 * kBatch) {
+    int32_t v[kBatch];
+#pragma unroll
+    for (int u = 0; u < kBatch; ++u) {
+      const int idx = base + u * 32 + lane;
+      v[u] = 0;
+      if (idx < total) {
+        const int r = idx / W;
+        v[u] = A.rec[(w0 + r) * W + (idx - r * W)];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kBatch; ++u) {
+      const int idx = base + u * 32 + lane;
+      const int r = idx < total ? idx / W : 0;
+      const int64_t row = __shfl_sync(kFull, my_row, r);
+      const int o = __shfl_sync(kFull, my_owner, r);
+      if (idx < total && row >= 0) {
+        const int k = idx - r * W;
+        dst_row(A, o, row)[k] = k == A.origin_word ? static_cast<int32_t>(w0 + r) : v[u];
+      }
+    }
   }
-  __syncthreads();
-  if (!last || threadIdx.x != 0) return;
-  __threadfence_system();
-  for (int o = 0; o < A.world; ++o) {
-    const int32_t c = *reinterpret_cast<volatile int32_t*>(A.cursor + o);
-    *reinterpret_cast<volatile int32_t*>(A.peers.base[o] + A.count_off + 4 * A.rank) =
-        static_cast<int32_t>(c < A.cap ? c : A.cap);
-  }
-  __threadfence_system();
-  for (int o = 0; o < A.world; ++o)
-    st_release_sys(reinterpret_cast<unsigned long long*>(A.peers.base[o] + A.flag_off) + A.rank, A.seq);
-  for (int o = 0; o < A.world; ++o) A.cursor[o] = 0;
-  *A.done = 0;
 }
 
-// Unordered: each warp takes 32 records, allocates rows per owner with one atomic per
-// (warp, owner), then copies the rows cooperatively (lanes = words, coalesced stores).
-__global__ void __launch_bounds__(256) k_px_send_atomic(SendArgs A) {
+// Two-pass stable scatter. Block b owns records [b * chunk, (b + 1) * chunk).
+// Pass 1: per-block per-owner counts. Pass 2: a block's rows for owner o start after the
+// rows of all earlier blocks (record order kept per owner), copied warp-cooperatively.
+constexpr int kSendBlock = 256;
+constexpr int kMaxSendBlocks = 1024;
+
+__global__ void __launch_bounds__(kSendBlock) k_px_count(SendArgs A, int64_t chunk, int32_t* blk_cnt) {
+  __shared__ int cnt[kMaxWorld];
+  if (threadIdx.x < kMaxWorld) cnt[threadIdx.x] = 0;
+  __syncthreads();
+  const int64_t b0 = static_cast<int64_t>(blockIdx.x) * chunk, b1 = min(A.n, b0 + chunk);
   const int lane = threadIdx.x & 31;
-  const int64_t warps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
-  for (int64_t w0 = (static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32; w0 < A.n;
-       w0 += warps * 32) {
-    const int64_t i = w0 + lane;
-    int o = i < A.n ? A.owner[i] : -1;
+  for (int64_t i0 = b0; i0 < b1; i0 += kSendBlock) {
+    const int64_t i = i0 + threadIdx.x;
+    int o = i < b1 ? A.owner[i] : -1;
     if (o >= A.world) o = -1;
-    const unsigned grp = __match_any_sync(kFull, o);
-    const int leader = __ffs(grp) - 1;
-    int base = 0;
-    if (o >= 0 && lane == leader) base = atomicAdd(A.cursor + o, __popc(grp));
-    base = __shfl_sync(kFull, base, leader);
-    int64_t row = o >= 0 ? base + __popc(grp & ((1u << lane) - 1u)) : -1;
-    if (row >= A.cap) {
-      atomicExch(A.overflow, 1);
-      row = -1;
-    }
-    if (i < A.n) A.slot[i] = row >= 0 ? o * A.cap + row : -1;
-    const int nrec = A.n - w0 < 32 ? static_cast<int>(A.n - w0) : 32;
-    for (int r = 0; r < nrec; ++r) {
-      const int64_t rr = __shfl_sync(kFull, row, r);
-      const int oo = __shfl_sync(kFull, o, r);
-      if (rr < 0) continue;
-      const int32_t* src = A.rec + (w0 + r) * A.words;
-      int32_t* dst = dst_row(A, oo, rr);
-      for (int k = lane; k < A.words; k += 32) dst[k] = src[k];
+    for (int p = 0; p < A.world; ++p) {
+      const unsigned bal = __ballot_sync(kFull, o == p);
+      if (lane == 0 && bal) atomicAdd(&cnt[p], __popc(bal));
     }
   }
-  publish(A);
+  __syncthreads();
+  if (threadIdx.x < A.world) blk_cnt[blockIdx.x * kMaxWorld + threadIdx.x] = cnt[threadIdx.x];
 }
 
-// Stable (one block): chunk by chunk, rows are assigned in record order per owner.
-__global__ void __launch_bounds__(1024) k_px_send_stable(SendArgs A) {
-  __shared__ int wcnt[32][kMaxWorld];
-  __shared__ int base[kMaxWorld];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  if (threadIdx.x < kMaxWorld) base[threadIdx.x] = 0;
-  __syncthreads();
-  for (int64_t c0 = 0; c0 < A.n; c0 += blockDim.x) {
-    const int64_t i = c0 + threadIdx.x;
-    int o = i < A.n ? A.owner[i] : -1;
+__global__ void __launch_bounds__(kSendBlock) k_px_scatter(SendArgs A, int64_t chunk, const int32_t* blk_cnt) {
+  __shared__ int64_t base[kMaxWorld];
+  __shared__ int wcnt[kSendBlock / 32][kMaxWorld];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  {  // exclusive prefix over earlier blocks (and, for block 0, the totals): a block reduction
+    __shared__ int64_t part[kSendBlock / 32][2 * kMaxWorld];
+    int64_t pre[kMaxWorld], tot[kMaxWorld];
+#pragma unroll
+    for (int p = 0; p < kMaxWorld; ++p) pre[p] = tot[p] = 0;
+    for (unsigned k = threadIdx.x; k < gridDim.x; k += kSendBlock) {
+#pragma unroll
+      for (int p = 0; p < kMaxWorld; ++p) {
+        const int c = p < A.world ? blk_cnt[k * kMaxWorld + p] : 0;
+        tot[p] += c;
+        if (k < blockIdx.x) pre[p] += c;
+      }
+    }
+#pragma unroll
+    for (int p = 0; p < kMaxWorld; ++p) {
+      for (int d = 16; d > 0; d >>= 1) {
+        pre[p] += __shfl_xor_sync(kFull, pre[p], d);
+        tot[p] += __shfl_xor_sync(kFull, tot[p], d);
+      }
+    }
+    if (lane == 0) {
+#pragma unroll
+      for (int p = 0; p < kMaxWorld; ++p) {
+        part[wid][p] = pre[p];
+        part[wid][kMaxWorld + p] = tot[p];
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x < A.world) {
+      int64_t b = 0, t = 0;
+      for (int w = 0; w < kSendBlock / 32; ++w) {
+        b += part[w][threadIdx.x];
+        t += part[w][kMaxWorld + threadIdx.x];
+      }
+      base[threadIdx.x] = b;
+      (void)t;
+    }
+    __syncthreads();
+  }
+  const int64_t b0 = static_cast<int64_t>(blockIdx.x) * chunk, b1 = min(A.n, b0 + chunk);
+  for (int64_t i0 = b0; i0 < b1; i0 += kSendBlock) {
+    const int64_t i = i0 + threadIdx.x;
+    int o = i < b1 ? A.owner[i] : -1;
     if (o >= A.world) o = -1;
     unsigned mine = 0;
     for (int p = 0; p < A.world; ++p) {
-      const unsigned b = __ballot_sync(kFull, o == p);
-      if (lane == 0) wcnt[wid][p] = __popc(b);
-      if (o == p) mine = b;
+      const unsigned bal = __ballot_sync(kFull, o == p);
+      if (lane == 0) wcnt[wid][p] = __popc(bal);
+      if (o == p) mine = bal;
     }
     __syncthreads();
     int64_t row = -1;
     if (o >= 0) {
-      int r = base[o];
+      int64_t r = base[o];
       for (int w = 0; w < wid; ++w) r += wcnt[w][o];
       row = r + __popc(mine & ((1u << lane) - 1u));
       if (row >= A.cap) {
@@ -160,23 +215,46 @@ __global__ void __launch_bounds__(1024) k_px_send_stable(SendArgs A) {
         row = -1;
       }
     }
-    if (i < A.n) A.slot[i] = row >= 0 ? o * A.cap + row : -1;
-    if (row >= 0) {
-      const int32_t* src = A.rec + i * A.words;
-      int32_t* dst = dst_row(A, o, row);
-      for (int k = 0; k < A.words; ++k) dst[k] = src[k];
-    }
+    if (A.slot && i < b1) A.slot[i] = row >= 0 ? o * A.cap + row : -1;
+    const int64_t w0 = i0 + wid * 32;
+    if (w0 < b1) warp_copy_rows(A, w0, b1 - w0 < 32 ? static_cast<int>(b1 - w0) : 32, o, row, lane);
     __syncthreads();
     if (threadIdx.x < A.world) {
       int t = 0;
-      for (int w = 0; w < nw; ++w) t += wcnt[w][threadIdx.x];
+      for (int w = 0; w < kSendBlock / 32; ++w) t += wcnt[w][threadIdx.x];
       base[threadIdx.x] += t;
     }
     __syncthreads();
   }
-  if (threadIdx.x < A.world) A.cursor[threadIdx.x] = base[threadIdx.x];
-  __syncthreads();
-  publish(A);
+  // every thread's own row stores are performed at system scope before the grid completes;
+  // these fences overlap across all threads (no hand-off chain)
+#if DGDS_PX_FENCE != 2
+  fence_release_sys();
+#endif
+}
+
+// After the scatter kernel (stream order: its stores are complete): one thread stores each
+// receiver's count, one system-scope fence, then the flags. A single fence on the critical
+// path — per-block fences plus a last-block hand-off cost three sequential ones.
+__global__ void k_px_publish(SendArgs A, const int32_t* blk_cnt, int nb) {
+  const int lane = threadIdx.x;  // one warp
+  int64_t tot[kMaxWorld];
+#pragma unroll
+  for (int p = 0; p < kMaxWorld; ++p) tot[p] = 0;
+  for (int b = lane; b < nb; b += 32) {
+#pragma unroll
+    for (int p = 0; p < kMaxWorld; ++p) tot[p] += p < A.world ? blk_cnt[b * kMaxWorld + p] : 0;
+  }
+#pragma unroll
+  for (int p = 0; p < kMaxWorld; ++p)
+    for (int d = 16; d > 0; d >>= 1) tot[p] += __shfl_xor_sync(kFull, tot[p], d);
+  if (lane != 0) return;
+  for (int o = 0; o < A.world; ++o)
+    *reinterpret_cast<volatile int32_t*>(A.peers.base[o] + A.count_off + 4 * A.rank) =
+        static_cast<int32_t>(tot[o] < A.cap ? tot[o] : A.cap);
+  fence_release_sys();
+  for (int o = 0; o < A.world; ++o)
+    st_relaxed_sys(reinterpret_cast<unsigned long long*>(A.peers.base[o] + A.flag_off) + A.rank, A.seq);
 }
 
 __global__ void k_px_wait(const unsigned long long* flags, int world, unsigned long long seq, int32_t* status,
@@ -211,7 +289,9 @@ struct dgds_px {
   int32_t* d_cursor = nullptr;  // [2][kMaxWorld]: one set per send kernel kind in flight
   unsigned* d_done = nullptr;   // [2]
   int32_t* d_status = nullptr;
+  int32_t* d_blk_cnt = nullptr;  // [2][kMaxSendBlocks][kMaxWorld] per-block owner counts
   uint64_t launches = 0;
+  int sms = 148;
   uint64_t timeout_ns = 30ull * 1000 * 1000 * 1000;
   std::mutex mu;
 };
@@ -240,6 +320,7 @@ int dgds_px_create(int32_t device, int32_t world, int32_t rank, uint64_t region_
   px->world = world;
   px->rank = rank;
   px->bytes = region_bytes;
+  cudaDeviceGetAttribute(&px->sms, cudaDevAttrMultiProcessorCount, device);
   cudaError_t e = cudaMalloc(&px->local, region_bytes);
   if (e == cudaSuccess) e = cudaMemset(px->local, 0, region_bytes);
   if (e == cudaSuccess) e = cudaMalloc(&px->d_cursor, 2 * kMaxWorld * sizeof(int32_t) + 2 * sizeof(unsigned) + 16);
@@ -248,11 +329,13 @@ int dgds_px_create(int32_t device, int32_t world, int32_t rank, uint64_t region_
     px->d_status = reinterpret_cast<int32_t*>(px->d_done + 2);
     e = cudaMemset(px->d_cursor, 0, 2 * kMaxWorld * sizeof(int32_t) + 2 * sizeof(unsigned) + 16);
   }
+  if (e == cudaSuccess) e = cudaMalloc(&px->d_blk_cnt, 2ull * kMaxSendBlocks * kMaxWorld * sizeof(int32_t));
   if (e == cudaSuccess && handle_out) e = cudaIpcGetMemHandle(static_cast<cudaIpcMemHandle_t*>(handle_out), px->local);
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   if (e != cudaSuccess) {
     if (px->local) cudaFree(px->local);
     if (px->d_cursor) cudaFree(px->d_cursor);
+    if (px->d_blk_cnt) cudaFree(px->d_blk_cnt);
     delete px;
     return px_fail(DGDS_ECUDA, std::string("peer region: ") + cudaGetErrorString(e));
   }
@@ -304,8 +387,9 @@ int dgds_px_region(dgds_px* px, int32_t peer, void** base) {
 
 int dgds_px_send(dgds_px* px, int64_t n, const int32_t* d_owner, const int32_t* d_records, int32_t rec_words,
                  int64_t cap, uint64_t slab_off, uint64_t count_off, uint64_t flag_off, uint64_t seq,
-                 int32_t stable, int64_t* d_slot, int32_t* d_overflow, void* stream) {
-  if (!px || n < 0 || rec_words < 1 || cap < 0 || seq == 0 || !d_overflow || (n > 0 && (!d_owner || !d_records || !d_slot)))
+                 int32_t stable, int32_t origin_word, int64_t* d_slot, int32_t* d_overflow, void* stream) {
+  if (origin_word >= rec_words) return px_fail(DGDS_EINVAL, "origin word outside the record");
+  if (!px || n < 0 || rec_words < 1 || cap < 0 || seq == 0 || !d_overflow || (n > 0 && (!d_owner || !d_records)))
     return px_fail(DGDS_EINVAL, "bad send arguments");
   for (int p = 0; p < px->world; ++p)
     if (!px->peers.base[p]) return px_fail(DGDS_EINVAL, "peer not connected");
@@ -330,19 +414,21 @@ int dgds_px_send(dgds_px* px, int64_t n, const int32_t* d_owner, const int32_t* 
   A.seq = seq;
   A.slot = d_slot;
   A.overflow = d_overflow;
-  const int kind = stable ? 1 : 0;  // separate cursors: a stable and an atomic send may run concurrently
+  A.origin_word = origin_word < 0 ? -1 : origin_word;
+  const int kind = stable ? 1 : 0;  // separate scratch: a query and an append send may overlap
   A.cursor = px->d_cursor + kind * kMaxWorld;
   A.done = px->d_done + kind;
   auto st = static_cast<cudaStream_t>(stream);
-  if (stable) {
-    k_px_send_stable<<<1, 1024, 0, st>>>(A);
-  } else {
-    int sms = 148;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, px->device);
-    const int64_t warps = (n + 31) / 32;
-    const int blocks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((warps + 7) / 8, 4LL * sms)));
-    k_px_send_atomic<<<blocks, 256, 0, st>>>(A);
-  }
+  const int sms = px->sms;
+  const int64_t rounds = (n + kSendBlock - 1) / kSendBlock;
+  const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(rounds, std::min(4 * sms, kMaxSendBlocks)));
+  const int64_t chunk = (rounds + blocks - 1) / blocks * kSendBlock;
+  const int64_t nb = std::max<int64_t>(1, (n + chunk - 1) / chunk);
+  int32_t* blk = px->d_blk_cnt + kind * kMaxSendBlocks * kMaxWorld;
+  k_px_count<<<static_cast<unsigned>(nb), kSendBlock, 0, st>>>(A, chunk, blk);
+  k_px_scatter<<<static_cast<unsigned>(nb), kSendBlock, 0, st>>>(A, chunk, blk);
+  k_px_publish<<<1, 32, 0, st>>>(A, blk, static_cast<int>(nb));
+  ++px->launches;
   PX_CUDA(cudaGetLastError());
   ++px->launches;
   return DGDS_OK;
@@ -396,6 +482,7 @@ int dgds_px_destroy(dgds_px* px) {
     if (px->opened[p]) cudaIpcCloseMemHandle(px->peers.base[p]);
   cudaFree(px->local);
   cudaFree(px->d_cursor);
+  cudaFree(px->d_blk_cnt);
   delete px;
   return DGDS_OK;
 }

@@ -1261,7 +1261,8 @@ static int speculate_records_impl(dgds_server* s, int64_t n, const int32_t* d_re
                                   const dgds_query_record_layout* lay, const dgds_spec_args* d_args,
                                   int64_t args_stride, int32_t max_top_k, int32_t max_spec, int32_t* d_replies,
                                   int32_t n_seg, int64_t seg_rows, const int32_t* d_seg_count,
-                                  int32_t* const* seg_out, dgds_query_stats* d_stats, void* stream) {
+                                  int32_t* const* seg_out, int32_t origin_field, dgds_query_stats* d_stats,
+                                  void* stream) {
   if (n < 0) return fail(DGDS_EINVAL, "negative batch size");
   if (n == 0) return DGDS_OK;
   if (!lay || !d_records || !d_args || (!d_replies && !seg_out)) return fail(DGDS_EINVAL, "null argument");
@@ -1294,6 +1295,7 @@ static int speculate_records_impl(dgds_server* s, int64_t n, const int32_t* d_re
   if (seg_out) {
     L.seg_rows = seg_rows;
     L.seg_count = d_seg_count;
+    if (origin_field >= 0) L.seg_origin = d_records + origin_field;
     for (int i = 0; i < n_seg; ++i) L.seg_out[i] = seg_out[i];
   }
   L.off_nc = y.off_n_cands;
@@ -1322,19 +1324,22 @@ int dgds_speculate_records(dgds_server* s, int64_t n, const int32_t* d_records, 
                            const dgds_spec_args* d_args, int64_t args_stride, int32_t max_top_k, int32_t max_spec,
                            int32_t* d_replies, dgds_query_stats* d_stats, void* stream) {
   return speculate_records_impl(s, n, d_records, lay, d_args, args_stride, max_top_k, max_spec, d_replies, 0, 0,
-                                nullptr, nullptr, d_stats, stream);
+                                nullptr, nullptr, -1, d_stats, stream);
 }
 
 int dgds_speculate_records_seg(dgds_server* s, int32_t n_seg, int64_t seg_rows, const int32_t* d_records,
                                const int32_t* d_seg_count, const dgds_query_record_layout* lay,
                                const dgds_spec_args* d_args, int64_t args_stride, int32_t max_top_k,
-                               int32_t max_spec, int32_t* const* seg_out, dgds_query_stats* d_stats, void* stream) {
+                               int32_t max_spec, int32_t* const* seg_out, int32_t origin_field,
+                               dgds_query_stats* d_stats, void* stream) {
   if (n_seg < 1 || n_seg > dgds::kMaxSegments || seg_rows < 0) return fail(DGDS_EINVAL, "bad segment shape");
+  if (lay && origin_field >= lay->rec_words) return fail(DGDS_EINVAL, "origin field outside the record");
   if (!d_seg_count || !seg_out) return fail(DGDS_EINVAL, "null argument");
   for (int i = 0; i < n_seg; ++i)
     if (!seg_out[i]) return fail(DGDS_EINVAL, "null segment output");
   return speculate_records_impl(s, static_cast<int64_t>(n_seg) * seg_rows, d_records, lay, d_args, args_stride,
-                                max_top_k, max_spec, nullptr, n_seg, seg_rows, d_seg_count, seg_out, d_stats, stream);
+                                max_top_k, max_spec, nullptr, n_seg, seg_rows, d_seg_count, seg_out, origin_field,
+                                d_stats, stream);
 }
 
 int dgds_verify_batch(dgds_server* s, int64_t n, const dgds_candidates* c, const int32_t* truth, int32_t truth_stride,

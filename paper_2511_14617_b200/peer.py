@@ -45,14 +45,15 @@ def _view(ptr: int, shape: Tuple[int, ...], typestr: str, device: torch.device) 
 @dataclass
 class Channel:
     name: str
-    rows: int            # rows per sender in one slab
+    rows: int            # rows per sender in one slab (shared: rows of the whole slab)
     words: int           # int32 words per row
     flag_off: int
     count_off: Tuple[int, int]
     slab_off: Tuple[int, int]
+    shared: bool = False  # one [rows][words] slab that every sender addresses by row
 
 
-def _layout(world: int, spec: Dict[str, Tuple[int, int]]) -> Tuple[Dict[str, Channel], int]:
+def _layout(world: int, spec: Dict[str, tuple]) -> Tuple[Dict[str, Channel], int]:
     off = 0
     chans = {}
     heads = {}
@@ -66,17 +67,20 @@ def _layout(world: int, spec: Dict[str, Tuple[int, int]]) -> Tuple[Dict[str, Cha
         off = (off + 63) // 64 * 64
         heads[name] = (flag, (c0, c1))
     off = (off + _ALIGN - 1) // _ALIGN * _ALIGN
-    for name, (rows, words) in spec.items():
+    for name, sp in spec.items():
+        rows, words = sp[0], sp[1]
+        shared = len(sp) > 2 and sp[2] == "shared"
         slabs = []
         for _ in range(2):
             slabs.append(off)
-            off += (world * rows * words * 4 + _ALIGN - 1) // _ALIGN * _ALIGN
-        chans[name] = Channel(name, rows, words, heads[name][0], heads[name][1], (slabs[0], slabs[1]))
+            off += ((1 if shared else world) * rows * words * 4 + _ALIGN - 1) // _ALIGN * _ALIGN
+        chans[name] = Channel(name, rows, words, heads[name][0], heads[name][1], (slabs[0], slabs[1]), shared)
     return chans, off
 
 
 class PeerExchange:
-    """One rank's end of the NVLink exchange. ``channels`` maps name -> (rows per sender, words)."""
+    """One rank's end of the NVLink exchange. ``channels`` maps name -> (rows per sender, words)
+    or (rows, words, "shared") for a slab that senders address by row (replies in query order)."""
 
     def __init__(self, world: int, rank: int, device: int, channels: Dict[str, Tuple[int, int]], group=None,
                  connect: bool = True):
@@ -125,8 +129,8 @@ class PeerExchange:
     def slab(self, ch: str, seq: int) -> torch.Tensor:
         """This rank's received rows of exchange `seq`: [world * rows, words] (sender-major)."""
         c = self.ch[ch]
-        return _view(self.bases()[self.rank] + c.slab_off[seq % 2], (self.world * c.rows, c.words), "<i4",
-                     self.device)
+        rows = c.rows if c.shared else self.world * c.rows
+        return _view(self.bases()[self.rank] + c.slab_off[seq % 2], (rows, c.words), "<i4", self.device)
 
     def counts(self, ch: str, seq: int) -> torch.Tensor:
         c = self.ch[ch]
@@ -137,23 +141,28 @@ class PeerExchange:
         key = (ch, seq % 2)
         if key not in self._seg_ptrs:
             c = self.ch[ch]
-            self._seg_ptrs[key] = (C.c_void_p * self.world)(
-                *[b + c.slab_off[seq % 2] + 4 * self.rank * c.rows * c.words for b in self.bases()])
+            mine = 0 if c.shared else 4 * self.rank * c.rows * c.words
+            self._seg_ptrs[key] = (C.c_void_p * self.world)(*[b + c.slab_off[seq % 2] + mine for b in self.bases()])
         return self._seg_ptrs[key]
 
     # ---- exchange ----
     def send(self, ch: str, owner: torch.Tensor, records: torch.Tensor, seq: int, stable: bool = False,
-             slot: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+             slot: Optional[torch.Tensor] = None, origin_word: int = -1, want_slot: bool = True,
+             stream=None) -> Optional[torch.Tensor]:
+        """Rows to their owners' slabs of exchange `seq`. Returns the slot map
+        (owner * rows + row, -1 if dropped) unless want_slot is False; origin_word >= 0 stamps
+        each delivered row with its index here (replies then come back in this order)."""
         c = self.ch[ch]
         n = records.shape[0]
         assert records.dtype == torch.int32 and records.is_contiguous() and records.shape[1] == c.words
         assert owner.dtype == torch.int32 and owner.is_contiguous() and owner.shape[0] == n
-        if slot is None:
+        if slot is None and want_slot:
             slot = torch.empty(n, dtype=torch.int64, device=self.device)
         st = stream if stream is not None else torch.cuda.current_stream(self.device)
         _lib.check(_lib.lib().dgds_px_send(self.h, n, C.c_void_p(owner.data_ptr()), C.c_void_p(records.data_ptr()),
                                            c.words, c.rows, c.slab_off[seq % 2], c.count_off[seq % 2], c.flag_off,
-                                           seq, 1 if stable else 0, C.c_void_p(slot.data_ptr()),
+                                           seq, 1 if stable else 0, origin_word,
+                                           C.c_void_p(slot.data_ptr()) if slot is not None else None,
                                            C.c_void_p(self.overflow.data_ptr()), C.c_void_p(st.cuda_stream)))
         return slot
 
@@ -186,15 +195,17 @@ class PeerExchange:
 
 
 def speculate_routed(srv, px: PeerExchange, q_ch: str, rep_ch: str, seq: int, layout, d_args: torch.Tensor,
-                     max_top_k: int, max_spec: int, stats: Optional[torch.Tensor] = None, stream=None) -> None:
+                     max_top_k: int, max_spec: int, stats: Optional[torch.Tensor] = None, stream=None,
+                     origin_field: int = -1) -> None:
     """Owner side of a routed query exchange: K2 + fused K3 over the received query rows of
-    exchange `seq`, replies stored straight into each sender's `rep_ch` slab, then signalled."""
+    exchange `seq`, replies stored straight into each sender's `rep_ch` slab (at the row the
+    sender stamped into `origin_field` when >= 0, for a shared reply slab), then signalled."""
     c = px.ch[q_ch]
     st = stream if stream is not None else torch.cuda.current_stream(px.device)
     px.wait(q_ch, seq, st)
     _lib.check(_lib.lib().dgds_speculate_records_seg(
         srv.handle, px.world, c.rows, C.c_void_p(px.slab_ptr(q_ch, seq)),
         C.c_void_p(px.counts_ptr(q_ch, seq)), C.byref(layout), C.c_void_p(d_args.data_ptr()), 0, max_top_k,
-        max_spec, px.seg_out(rep_ch, seq), C.c_void_p(stats.data_ptr()) if stats is not None else None,
+        max_spec, px.seg_out(rep_ch, seq), origin_field, C.c_void_p(stats.data_ptr()) if stats is not None else None,
         C.c_void_p(st.cuda_stream)))
     px.signal(rep_ch, seq, st)
