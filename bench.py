@@ -84,6 +84,8 @@ class ClockSampler:
         self._stop = threading.Event()
         self._t = None
         try:
+            if os.environ.get("DGDS_NO_CLOCKS") == "1":  # debug only: a run without clock samples is invalid
+                raise RuntimeError("clock sampling disabled")
             import pynvml
             pynvml.nvmlInit()
             self.nv = pynvml

@@ -81,6 +81,16 @@ def run_multi(args, world, rank, local, dev):
         pos[live] += np.minimum(prefill[live] - pos[live], chunk)
     pos = prefill.copy()  # every rank knows every stream's prefix length
 
+    # owner-side algorithmic append bytes of every tick (the records of the owned streams,
+    # whoever produces them), computed here so no bookkeeping runs inside the timed region
+    own_alg = []
+    pos_own = prefill.copy()
+    for s in range(W + K + E):
+        live_o = my_streams[pos_own[my_streams] < tr.lengths[my_streams]]
+        ns_o = np.minimum(rt, tr.lengths[live_o] - pos_own[live_o])
+        own_alg.append(append_alg_bytes(pos_own[live_o], ns_o))
+        pos_own[live_o] += ns_o
+
     # ---- per-step inputs of this rank (the streams it produces), resident in HBM ----
     produced = np.arange(rank, S, world)
     rng = np.random.default_rng(args.seed + 7919 * rank)
@@ -128,6 +138,8 @@ def run_multi(args, world, rank, local, dev):
     app_alg_owner = [0]
     overflow = torch.zeros((), dtype=torch.bool, device=dev)
     side = torch.cuda.Stream(dev)
+    side_q = torch.cuda.Stream(dev)  # early query sends (px)
+    q_sent = set()
     ev_side = torch.cuda.Event()
     meta_h = torch.empty((world * capa, 5), dtype=torch.int32).pin_memory()
     mq = world * capq
@@ -140,14 +152,18 @@ def run_multi(args, world, rank, local, dev):
     layout = _lib.RecordLayout(QRY_W, 0, 1, 2, 10, 11, 12, rep_w, 0, 1, off_sc, off_sp, off_tk, off_v)
     replies = torch.zeros((mq, rep_w), dtype=torch.int32, device=dev)
     prof_host = {}
-    dbg = os.environ.get("DGDS_MULTI_BREAKDOWN") == "1"
+    dbg = os.environ.get("DGDS_MULTI_BREAKDOWN") == "1"  # device-synchronised phases (debug)
+    host_t = os.environ.get("DGDS_MULTI_HOSTTIME") == "1"  # host time per phase, no syncs (debug)
 
     def mark(name, t0):
-        if not dbg:
+        if not (dbg or host_t):
             return t0
-        torch.cuda.synchronize()
+        if dbg:
+            torch.cuda.synchronize()
         t1 = time.perf_counter()
         prof_host[name] = prof_host.get(name, 0.0) + t1 - t0
+        if name == "route_cur":
+            prof_host.setdefault("route_cur_each_us", []).append(round(1e6 * (t1 - t0)))
         return t1
 
     # Append records of a tick are routed one tick AHEAD (side stream, double-buffered):
@@ -164,8 +180,6 @@ def run_multi(args, world, rank, local, dev):
         px = PeerExchange(world, rank, local, {"q": (capq, QRY_W), "rep": (Q, rep_w, "shared"),
                                                "a": (capa, APP_W)})
         rep_view = {p: px.slab("rep", p) for p in (1, 2)}  # parity 1, 0
-        a_meta = {p: px.slab("a", p)[:, :5] for p in (1, 2)}
-        a_cnt = {p: px.counts("a", p) for p in (1, 2)}
 
     def route_appends(s):
         if s >= len(steps_in) or s in inflight:
@@ -175,7 +189,7 @@ def run_multi(args, world, rank, local, dev):
         if "ready" in inp:  # e2e: the inputs were copied in on the main stream
             side.wait_event(inp["ready"])
         if use_px:
-            seq, par = s + 1, 2 - (s + 1) % 2
+            seq = s + 1
             with torch.cuda.stream(side):
                 # this parity was last read by the owners' K1 of tick s-2; their replies of tick s-1
                 # (queued after that K1 on their streams) prove it is free
@@ -183,8 +197,13 @@ def run_multi(args, world, rank, local, dev):
                     side.wait_event(ev_rep[(s - 1) % 2])
                 px.send("a", inp["app_owner"], inp["app"], seq, stable=True, want_slot=False, stream=side)
                 px.wait("a", seq, stream=side)
-                meta_bufs[k].copy_(a_meta[par], non_blocking=True)
-                cnt_bufs[k].copy_(a_cnt[par], non_blocking=True)
+                # metadata columns of every row (one 2-D DMA) and the per-sender counts
+                _lib.check(L.dgds_copy_rows_d2h(C.c_void_p(meta_bufs[k].data_ptr()), 20,
+                                                C.c_void_p(px.slab_ptr("a", seq)), APP_W * 4, 20, world * capa,
+                                                C.c_void_p(side.cuda_stream)))
+                _lib.check(L.dgds_copy_rows_d2h(C.c_void_p(cnt_bufs[k].data_ptr()), 4 * world,
+                                                C.c_void_p(px.counts_ptr("a", seq)), 4 * world, 4 * world, 1,
+                                                C.c_void_p(side.cuda_stream)))
                 ev_bufs[k].record(side)
             inflight[s] = (None, None, k)
             return
@@ -197,6 +216,21 @@ def run_multi(args, world, rank, local, dev):
         ra.record_stream(torch.cuda.current_stream(dev))  # K1 reads the tokens on the main stream
         inflight[s] = (ra, st_a[1], k)
 
+    def send_queries(s):
+        """Queries of tick s go to their owners as soon as the replies of tick s-1 are home
+        (the point where an engine knows its next patterns), overlapping the owners' K1 of
+        tick s-1. The owner's slab parity of tick s was last read by its K2 of tick s-2."""
+        if not use_px or s >= len(steps_in) or s in q_sent:
+            return
+        inp = steps_in[s]
+        with torch.cuda.stream(side_q):
+            if "ready" in inp:
+                side_q.wait_event(inp["ready"])
+            if s > 0:
+                side_q.wait_event(ev_rep[(s - 1) % 2])
+            px.send("q", inp["q_owner"], inp["q"], s + 1, origin_word=QRY_W - 1, want_slot=False, stream=side_q)
+        q_sent.add(s)
+
     def step(s, stats):
         """One tick in engine order (engine.cpp:88-161): draft queries (+ verify) on the
         current index, then the appends of the tick's emitted tokens."""
@@ -205,11 +239,12 @@ def run_multi(args, world, rank, local, dev):
         main = torch.cuda.current_stream(dev)
         t0 = mark("start", time.perf_counter())
         route_appends(s)  # normally already in flight since the previous tick
+        t0 = mark("route_cur", t0)
         seq, k = s + 1, s % 2
         if use_px:
             # (1)+(2) queries stored into the owners' slabs; the owner's K2+K3 stores each reply
             # straight into its sender's reply slab; (3) gather into query order
-            px.send("q", inp["q_owner"], inp["q"], seq, origin_word=QRY_W - 1, want_slot=False, stream=main)
+            send_queries(s)  # normally already sent during the previous tick
             t0 = mark("q_fwd", t0)
             speculate_routed(srv, px, "q", "rep", seq, layout, sp_args, kq, dl, d_stats if stats else None, main,
                              origin_field=QRY_W - 1)
@@ -234,31 +269,42 @@ def run_multi(args, world, rank, local, dev):
         # (3) the tick's appends: metadata arrived during the previous tick; bookkeeping, then K1
         ra, ova, k = inflight.pop(s)
         ev_bufs[k].synchronize()
-        meta = meta_bufs[k].numpy()
+        t0 = mark("meta_wait", t0)
         if use_px:
-            cnt = cnt_bufs[k].numpy()
-            rows = np.concatenate([np.arange(o * capa, o * capa + int(cnt[o]), dtype=np.int64) for o in range(world)])
-            base_ptr = px.slab_ptr("a", seq)
-        else:
-            rows = np.nonzero(meta[:, 0] >= 0)[0]
-            base_ptr = ra.data_ptr()
-        if len(rows):
-            m = meta[rows]
-            n = m[:, 4].astype(np.uint64)
-            prev = m[:, 2].view(np.uint32).astype(np.uint64) | (m[:, 3].astype(np.uint64) << np.uint64(32))
-            starts = rows.astype(np.uint64) * np.uint64(APP_W) + np.uint64(5)
             main.wait_event(ev_bufs[k])
-            rep = srv.update_device_strided(m[:, 0].copy(), m[:, 1].copy(), prev, starts, n, base_ptr, 0.0,
-                                            main.cuda_stream)
-            if not rep["ok"].all():
+            t0 = mark("meta_np", t0)
+            nrej = C.c_int64()
+            _lib.check(L.dgds_update_batch_routed(srv.handle, world, capa, C.c_void_p(cnt_bufs[k].data_ptr()),
+                                                  C.c_void_p(meta_bufs[k].data_ptr()), 5,
+                                                  C.c_void_p(px.slab_ptr("a", seq)), APP_W, 0.0, C.byref(nrej),
+                                                  C.c_void_p(main.cuda_stream)))
+            if nrej.value:
                 raise RuntimeError("routed append out of order")
             if stats:
-                app_alg_owner[0] += append_alg_bytes(prev.astype(np.int64), n.astype(np.int64))
+                app_alg_owner[0] += own_alg[s]
+        else:
+            meta = meta_bufs[k].numpy()
+            rows = np.nonzero(meta[:, 0] >= 0)[0]
+            if len(rows):
+                m = meta[rows]
+                n = m[:, 4].astype(np.uint64)
+                prev = m[:, 2].view(np.uint32).astype(np.uint64) | (m[:, 3].astype(np.uint64) << np.uint64(32))
+                starts = rows.astype(np.uint64) * np.uint64(APP_W) + np.uint64(5)
+                main.wait_event(ev_bufs[k])
+                rep = srv.update_device_strided(m[:, 0].copy(), m[:, 1].copy(), prev, starts, n, ra.data_ptr(), 0.0,
+                                                main.cuda_stream)
+                if not rep["ok"].all():
+                    raise RuntimeError("routed append out of order")
+            if stats:
+                app_alg_owner[0] += own_alg[s]
         if not use_px:
             overflow = overflow | ovq | ova
+        t0 = mark("append_call", t0)
         # (4) route the next tick's appends now, so their metadata is home by then
         route_appends(s + 1)
-        mark("append", t0)
+        t0 = mark("route_next", t0)
+        send_queries(s + 1)
+        mark("send_next", t0)
         return back
 
     for s in range(W):
@@ -330,8 +376,9 @@ def run_multi(args, world, rank, local, dev):
                "d2h_bytes_per_step": d2h // E, "steps": E,
                "path": "routed step, pinned host records in / replies out (rank-local view)"}
 
-    if dbg:
-        print(f"rank {rank} breakdown (s, all steps):", {k: round(v, 4) for k, v in prof_host.items()}, flush=True)
+    if dbg or host_t:
+        print(f"rank {rank} breakdown (s, all steps):",
+              {k: (round(v, 4) if isinstance(v, float) else v) for k, v in prof_host.items()}, flush=True)
     if use_px:
         timed_out, _ = px.status()
         if timed_out:
@@ -341,8 +388,9 @@ def run_multi(args, world, rank, local, dev):
         raise RuntimeError("routing capacity overflow: results of this run are invalid")
     if rank == 0:
         peak, peak_kind = peaks()
-        q_ach = q_alg_all / (qus_all / 1e6) / 1e9 / world if qus_all else 0.0
-        a_ach = a_alg_all / (aus_all / 1e6) / 1e9 / world if aus_all else 0.0
+        # sums over ranks of bytes and of launch time: their ratio is the per-GPU rate
+        q_ach = q_alg_all / (qus_all / 1e6) / 1e9 if qus_all else 0.0
+        a_ach = a_alg_all / (aus_all / 1e6) / 1e9 if aus_all else 0.0
         dom_q = qus_all >= aus_all
         roof = lambda kern, ach, alg, us, n: {  # noqa: E731
             "kernel": kern, "bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,

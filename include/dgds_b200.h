@@ -232,6 +232,18 @@ int dgds_speculate_records(dgds_server* s, int64_t n, const int32_t* d_records, 
                            const dgds_spec_args* d_args, int64_t args_stride, int32_t max_top_k, int32_t max_spec,
                            int32_t* d_replies, dgds_query_stats* d_stats, void* stream);
 
+/* Appends delivered by owner routing (dgds_px_send): n_seg sender segments of seg_rows rows;
+ * segment g holds h_counts[g] valid rows. Row r = [handle, request_id, prev_lo, prev_hi, n,
+ * tokens[n] ...] of row_words int32 — metadata read from host memory h_meta (row r at
+ * h_meta + r * meta_stride), tokens from device memory d_rows. Same semantics as
+ * dgds_update_batch_device_strided; *n_rejected = replies with ok == false. */
+int dgds_update_batch_routed(dgds_server* s, int32_t n_seg, int64_t seg_rows, const int32_t* h_counts,
+                             const int32_t* h_meta, int32_t meta_stride, const int32_t* d_rows, int32_t row_words,
+                             double now, int64_t* n_rejected, void* stream);
+/* Strided device -> host copy (cudaMemcpy2DAsync): `rows` rows of `width` bytes. */
+int dgds_copy_rows_d2h(void* h_dst, int64_t dst_pitch, const void* d_src, int64_t src_pitch, int64_t width,
+                       int64_t rows, void* stream);
+
 /* Zero-copy host results: compact per-query candidate lists (CSR) in a pinned block owned
  * by the server, valid until the next query call on `s`. Candidates of query q are
  * cands[cand_off[q] .. cand_off[q+1]) in candidate_before order (cst.cpp:29-35); the tokens

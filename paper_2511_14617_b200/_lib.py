@@ -166,6 +166,9 @@ EXPORTS = {
     "dgds_route_unpack": (C.c_int, [_I64, _P, _I32, _P, _P, _P]),
     "dgds_route_pack_padded": (C.c_int, [_I64, _I32, _P, _P, _I32, _I64, _P, _P, _P, _P]),
     "dgds_speculate_records": (C.c_int, [_P, _I64, _P, C.POINTER(RecordLayout), _P, _I64, _I32, _I32, _P, _P, _P]),
+    "dgds_update_batch_routed": (C.c_int, [_P, _I32, _I64, _P, _P, _I32, _P, _I32, C.c_double, C.POINTER(_I64),
+                                           _P]),
+    "dgds_copy_rows_d2h": (C.c_int, [_P, _I64, _P, _I64, _I64, _I64, _P]),
     "dgds_speculate_verify_view": (C.c_int, [_P, _I64, _P, _P, _P, _P, _I64, _P, _I32, _P, _P, C.POINTER(ResultView)]),
     "dgds_speculate_records_seg": (C.c_int, [_P, _I32, _I64, _P, _P, C.POINTER(RecordLayout), _P, _I64, _I32, _I32,
                                              C.POINTER(C.c_void_p), _I32, _P, _P]),

@@ -917,6 +917,56 @@ int dgds_update_batch_device_strided(dgds_server* s, int64_t n, const int32_t* h
   return update_device_impl(s, n, handles, rids, prev, tok_starts, tok_counts, d_tokens, now, rep, stream);
 }
 
+int dgds_update_batch_routed(dgds_server* s, int32_t n_seg, int64_t seg_rows, const int32_t* h_counts,
+                             const int32_t* h_meta, int32_t meta_stride, const int32_t* d_rows, int32_t row_words,
+                             double now, int64_t* n_rejected, void* stream) {
+  if (!s || !h_counts || !h_meta || !d_rows || n_seg < 1 || seg_rows < 0 || meta_stride < 5 || row_words < 6)
+    return fail(DGDS_EINVAL, "bad routed append arguments");
+  int64_t n = 0;
+  for (int g = 0; g < n_seg; ++g) {
+    if (h_counts[g] < 0 || h_counts[g] > seg_rows) return fail(DGDS_EINVAL, "segment count out of range");
+    n += h_counts[g];
+  }
+  if (n_rejected) *n_rejected = 0;
+  if (n == 0) return DGDS_OK;
+  std::vector<int32_t> handles(n), rids(n);
+  std::vector<uint64_t> prev(n), starts(n), counts(n);
+  int64_t i = 0;
+  for (int g = 0; g < n_seg; ++g) {
+    for (int64_t j = 0; j < h_counts[g]; ++j, ++i) {
+      const int64_t row = g * seg_rows + j;
+      const int32_t* m = h_meta + row * meta_stride;
+      handles[i] = m[0];
+      rids[i] = m[1];
+      prev[i] = static_cast<uint64_t>(static_cast<uint32_t>(m[2])) | (static_cast<uint64_t>(static_cast<uint32_t>(m[3])) << 32);
+      const int32_t cnt = m[4];
+      if (cnt < 0 || cnt > row_words - 5) return fail(DGDS_EINVAL, "routed append token count out of range");
+      counts[i] = static_cast<uint64_t>(cnt);
+      starts[i] = static_cast<uint64_t>(row) * row_words + 5;
+    }
+  }
+  std::vector<dgds_update_reply> rep(n);
+  if (int rc = update_device_impl(s, n, handles.data(), rids.data(), prev.data(), starts.data(), counts.data(), d_rows,
+                                  now, rep.data(), stream))
+    return rc;
+  if (n_rejected) {
+    int64_t bad = 0;
+    for (const auto& r : rep) bad += r.ok ? 0 : 1;
+    *n_rejected = bad;
+  }
+  return DGDS_OK;
+}
+
+int dgds_copy_rows_d2h(void* h_dst, int64_t dst_pitch, const void* d_src, int64_t src_pitch, int64_t width,
+                       int64_t rows, void* stream) {
+  if (rows < 0 || width < 0 || (rows > 0 && (!h_dst || !d_src)) || dst_pitch < width || src_pitch < width)
+    return fail(DGDS_EINVAL, "bad strided copy");
+  if (rows == 0 || width == 0) return DGDS_OK;
+  DGDS_CUDA(cudaMemcpy2DAsync(h_dst, dst_pitch, d_src, src_pitch, width, rows, cudaMemcpyDeviceToHost,
+                              stream ? static_cast<cudaStream_t>(stream) : cudaStreamLegacy));
+  return DGDS_OK;
+}
+
 }  // extern "C"
 
 namespace {
