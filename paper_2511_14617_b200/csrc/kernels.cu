@@ -121,7 +121,8 @@ __global__ void __launch_bounds__(kBlock, 4) k_append(DevTrie T, const AppendSeg
   const int64_t nwarps = static_cast<int64_t>(gridDim.x) * blockDim.x / kWarp;
   const int D = T.depth_cap;
   unsigned long long inserted_total = 0;
-  constexpr int kStage = 128, kAhead = 4;
+  constexpr int kStage = 128;
+  const int kAhead = T.ahead;  // 0: no look-ahead prefetch (server default)
   __shared__ int32_t stage[kWarpsPerBlock][kStage];
   int32_t* stage_w = stage[threadIdx.x / kWarp];
 
@@ -181,7 +182,7 @@ __global__ void __launch_bounds__(kBlock, 4) k_append(DevTrie T, const AppendSeg
       const int ahead = min(kAhead, filled);
       for (int j = 0; j < ahead; ++j) advance_ahead(j);
       for (int j = 0; j < filled; ++j) {
-        if (j + kAhead < filled) advance_ahead(j + kAhead);
+        if (kAhead > 0 && j + kAhead < filled) advance_ahead(j + kAhead);
         const int32_t t = stage_w[j];
         const int newsize = static_cast<int>(min(static_cast<uint64_t>(D), len + 1));
         const unsigned long long hup = __shfl_up_sync(kFull, h, 1);
