@@ -113,6 +113,29 @@ __device__ __forceinline__ void claim(const DevTrie& T, unsigned long long h, ui
   }
 }
 
+// CAS-first claim: no read before the first atomic. Slots fill in probe order and are never
+// freed between rebuilds, so walking the probe sequence with CAS(empty -> key) either finds
+// the key (the CAS returns it), claims the first empty slot (returns 0), or passes an
+// occupant — the same slot the load-first claim would pick, with one random access instead
+// of a window read followed by the CAS on an insert, the common case at depth.
+__device__ __forceinline__ void claim_cas(const DevTrie& T, unsigned long long h, uint32_t parent, int32_t token,
+                                          uint32_t& id, bool& inserted) {
+  const unsigned long long pt = pack_pt(parent, token);
+  const uint64_t cap = T.cap;
+  uint64_t i = home_bucket(h, cap / kBucket) * kBucket;
+  while (true) {
+    unsigned long long o0, o1;
+    cas128(T.slots + i, h, pt, o0, o1);
+    if (o0 == 0ull || (o0 == h && o1 == pt)) {
+      inserted = o0 == 0ull;
+      if (!inserted) atomicAdd(&T.slots[i].count, 1u);  // RED; an insert's occurrence is implicit
+      id = static_cast<uint32_t>(i + 1);
+      return;
+    }
+    if (++i == cap) i = 0;
+  }
+}
+
 __global__ void __launch_bounds__(kBlock, 4) k_append(DevTrie T, const AppendSeg* __restrict__ segs, int64_t nseg,
                                                    const AppendPiece* __restrict__ pieces,
                                                    const int32_t* __restrict__ tokens) {
@@ -192,7 +215,8 @@ __global__ void __launch_bounds__(kBlock, 4) k_append(DevTrie T, const AppendSeg
         if (lane < newsize) {
           uint32_t id;
           bool ins;
-          claim(T, key_hash(h), parent, t, id, ins);
+          if (T.claim_cas) claim_cas(T, key_hash(h), parent, t, id, ins);
+          else claim(T, key_hash(h), parent, t, id, ins);
           if (link_pending) {  // {next_sibling, root} of the node created at the previous token
             store_link(T.slots + link_slot, link_prev, g.root);
             link_pending = false;

@@ -686,6 +686,8 @@ int dgds_create(const dgds_params* params, dgds_server** out) {
   s->T.lim_spec = p.max_spec_len;
   s->T.ahead = 0;  // the bulk L2 prefetch measured slower than the register preload alone
   if (const char* e = std::getenv("DGDS_PREFETCH_AHEAD")) s->T.ahead = std::max(0, std::atoi(e));
+  s->T.claim_cas = 1;  // CAS-first claim (measured faster: fewer random accesses per insert)
+  if (const char* e = std::getenv("DGDS_CLAIM")) s->T.claim_cas = std::strcmp(e, "load") == 0 ? 0 : 1;
   DGDS_CUDA(cudaMalloc(&s->T.slots, cap * sizeof(dgds::Slot)));
   DGDS_CUDA(cudaMemsetAsync(s->T.slots, 0, cap * sizeof(dgds::Slot), s->st));
   DGDS_CUDA(cudaMalloc(&s->d_used, sizeof(unsigned long long)));

@@ -67,6 +67,7 @@ struct DevTrie {
   int32_t lim_pattern;       // Limits::max_pattern_len
   int32_t lim_spec;          // Limits::max_spec_len
   int32_t ahead;             // append look-ahead (tokens) of the L2 prefetch; 0 = off
+  int32_t claim_cas;         // append claim: 1 = CAS-first, 0 = read the window first
 };
 
 __host__ __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
