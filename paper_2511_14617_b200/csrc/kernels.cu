@@ -905,28 +905,37 @@ __global__ void __launch_bounds__(kBlock, 4) k_query(QueryLaunch P) {
     o[7] = nf;
   }
   if (P.stats) {
-    // per-block reduction, then one atomic per counter per block (same-address
-    // atomics from every request would serialise in one L2 slice)
-    __shared__ unsigned long long blk[8];
-    if (threadIdx.x < 8) blk[threadIdx.x] = 0ull;
-    __syncthreads();
+    // tile leaders' counters -> warp sums (redux) -> one RED per counter per warp into one of
+    // kStatParts partitions: no block barrier, no same-address storm (k_stats_fold sums them)
     const int ctoks = tile.sum(gl < nf ? sm.f.len[gl] : 0);
-    if (valid && gl == 0) {
-      const uint64_t B = 4ull * plen + 32ull + 32ull * st_lookups + 32ull * st_exp + 32ull * st_csec +
-                         4ull * ctoks + 16ull * nf;
-      atomicAdd(&blk[0], 1ull);
-      atomicAdd(&blk[1], static_cast<unsigned long long>(plen));
-      atomicAdd(&blk[2], static_cast<unsigned long long>(st_lookups));
-      atomicAdd(&blk[3], static_cast<unsigned long long>(st_exp));
-      atomicAdd(&blk[4], static_cast<unsigned long long>(st_csec));
-      atomicAdd(&blk[5], static_cast<unsigned long long>(nf));
-      atomicAdd(&blk[6], static_cast<unsigned long long>(ctoks));
-      atomicAdd(&blk[7], static_cast<unsigned long long>(B));
+    const bool lead = valid && gl == 0;
+    const uint32_t B = lead ? static_cast<uint32_t>(4ull * plen + 32ull + 32ull * st_lookups + 32ull * st_exp +
+                                                    32ull * st_csec + 4ull * ctoks + 16ull * nf)
+                            : 0u;
+    uint32_t v[8] = {lead ? 1u : 0u, lead ? static_cast<uint32_t>(plen) : 0u,
+                     lead ? static_cast<uint32_t>(st_lookups) : 0u, lead ? static_cast<uint32_t>(st_exp) : 0u,
+                     lead ? static_cast<uint32_t>(st_csec) : 0u, lead ? static_cast<uint32_t>(nf) : 0u,
+                     lead ? static_cast<uint32_t>(ctoks) : 0u, B};
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = __reduce_add_sync(kFull, v[k]);
+    if (lane == 0) {
+      const uint32_t part = (blockIdx.x * (kBlock / kWarp) + threadIdx.x / kWarp) & (kStatParts - 1);
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (v[k]) atomicAdd(P.stat_part + part * 8 + k, static_cast<unsigned long long>(v[k]));
     }
-    __syncthreads();
-    if (threadIdx.x < 8 && blk[threadIdx.x])
-      atomicAdd(reinterpret_cast<unsigned long long*>(P.stats) + threadIdx.x, blk[threadIdx.x]);
   }
+}
+
+__global__ void k_stats_fold(unsigned long long* part, dgds_query_stats* out) {
+  const int k = threadIdx.x;
+  if (k >= 8) return;
+  unsigned long long t = 0;
+  for (int p = 0; p < kStatParts; ++p) {
+    t += part[p * 8 + k];
+    part[p * 8 + k] = 0ull;
+  }
+  reinterpret_cast<unsigned long long*>(out)[k] += t;
 }
 
 // ---------------------------------------------------------------------------
@@ -1154,9 +1163,14 @@ cudaError_t launch_append(const DevTrie& T, const AppendSeg* d_segs, int64_t nse
 
 cudaError_t launch_query(const QueryLaunch& L, int32_t max_k, int32_t max_s, cudaStream_t st) {
   if (L.n <= 0) return cudaSuccess;
-  if (max_k <= 4) return launch_query_g<4>(L, max_s, st);
-  if (max_k <= 8) return launch_query_g<8>(L, max_s, st);
-  return launch_query_g<32>(L, max_s, st);
+  if (L.stats && !L.stat_part) return cudaErrorInvalidValue;
+  cudaError_t e;
+  if (max_k <= 4) e = launch_query_g<4>(L, max_s, st);
+  else if (max_k <= 8) e = launch_query_g<8>(L, max_s, st);
+  else e = launch_query_g<32>(L, max_s, st);
+  if (e != cudaSuccess || !L.stats) return e;
+  k_stats_fold<<<1, 32, 0, st>>>(L.stat_part, L.stats);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_verify(int64_t n, int32_t k_stride, int32_t s_stride, const int32_t* n_cands, const int32_t* lens,

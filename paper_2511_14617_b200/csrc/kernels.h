@@ -34,7 +34,8 @@ cudaError_t launch_append(const DevTrie& T, const AppendSeg* d_segs, int64_t nse
 
 int set_error(int code, const std::string& msg);  // dgds_last_error() message (server.cpp)
 
-constexpr int kMaxSegments = 8;  // senders of a segmented query launch (ranks of one node)
+constexpr int kMaxSegments = 8;
+constexpr int kStatParts = 64;  // partitions of the query counters (spreads the REDs)  // senders of a segmented query launch (ranks of one node)
 
 struct QueryLaunch {
   DevTrie T;
@@ -62,7 +63,8 @@ struct QueryLaunch {
   int32_t* v_drafted;
   int32_t* v_accepted;
   int32_t* v_emitted;
-  dgds_query_stats* stats;
+  dgds_query_stats* stats;          // optional: counters added here (after k_stats_fold)
+  unsigned long long* stat_part;    // server scratch [kStatParts][8], zero between launches
   int32_t* err_flag;  // set to 1 by any query with invalid args (device API)
   long long* dbg;     // optional per-query phase timing [n][8] (debug)
   // Per-query strides (elements). SoA buffers: in_qstride 1, out_qstride = out_qstride8 = k_stride,

@@ -279,6 +279,7 @@ struct dgds_server {
     return *pool;
   }
   int32_t* d_err = nullptr;
+  unsigned long long* d_stat_part = nullptr;  // [kStatParts][8] query-counter partitions
   std::mutex mu;  // calls on one handle are serialized
 
   long long* d_dbg = nullptr;  // optional per-query phase timing buffer (debug)
@@ -698,6 +699,8 @@ int dgds_create(const dgds_params* params, dgds_server** out) {
   DGDS_CUDA(cudaMalloc(&s->T.tail, s->stream_cap * dgds::kWarp * sizeof(int32_t)));
   DGDS_CUDA(cudaMalloc(&s->d_err, sizeof(int32_t)));
   DGDS_CUDA(cudaMemsetAsync(s->d_err, 0, sizeof(int32_t), s->st));
+  DGDS_CUDA(cudaMalloc(&s->d_stat_part, dgds::kStatParts * 8 * sizeof(unsigned long long)));
+  DGDS_CUDA(cudaMemsetAsync(s->d_stat_part, 0, dgds::kStatParts * 8 * sizeof(unsigned long long), s->st));
   s->root_of_cap = 1024;
   DGDS_CUDA(cudaMalloc(&s->d_root_of, s->root_of_cap * sizeof(uint32_t)));
   DGDS_CUDA(cudaMemsetAsync(s->d_root_of, 0, s->root_of_cap * sizeof(uint32_t), s->st));
@@ -716,6 +719,7 @@ int dgds_destroy(dgds_server* s) {
   cudaFree(s->d_used);
   cudaFree(s->d_root_of);
   cudaFree(s->d_err);
+  cudaFree(s->d_stat_part);
   if (s->staging_free) cudaEventDestroy(s->staging_free);
   for (auto e : s->ev_pool) cudaEventDestroy(e);
   for (auto& v : s->ev_pending)
@@ -1102,6 +1106,7 @@ int speculate_host(dgds_server* s, int64_t n, const int32_t* handles, const uint
   L.lens = reinterpret_cast<int32_t*>(dout + o_ln);
   L.tokens = reinterpret_cast<int32_t*>(dout + o_tk);
   L.err_flag = s->d_err;
+  L.stat_part = s->d_stat_part;
   if (verify) {
     L.truth = reinterpret_cast<const int32_t*>(d + o_tr);
     L.truth_stride = truth_stride;
@@ -1301,6 +1306,7 @@ int dgds_speculate_device(dgds_server* s, int64_t n, const int32_t* d_handles, c
   }
   L.stats = d_stats;
   L.err_flag = s->d_err;
+  L.stat_part = s->d_stat_part;
   L.dbg = s->d_dbg;
   {
     LaunchTimer lt(s, 1, join.stream());
@@ -1364,6 +1370,7 @@ static int speculate_records_impl(dgds_server* s, int64_t n, const int32_t* d_re
   }
   L.stats = d_stats;
   L.err_flag = s->d_err;
+  L.stat_part = s->d_stat_part;
   L.dbg = s->d_dbg;
   {
     LaunchTimer lt(s, 1, join.stream());
