@@ -244,13 +244,9 @@ __global__ void __launch_bounds__(kBlock, 4) k_append(DevTrie T, const AppendSeg
     if (link_pending) store_link(T.slots + link_slot, link_prev, g.root);
     if (lane < D && static_cast<uint64_t>(lane) < len) act_row[lane] = a;
   }
-  for (int o = 16; o > 0; o >>= 1) inserted_total += __shfl_xor_sync(kFull, inserted_total, o);
-  __shared__ unsigned long long blk_ins;
-  if (threadIdx.x == 0) blk_ins = 0ull;
-  __syncthreads();
-  if (lane == 0 && inserted_total) atomicAdd(&blk_ins, inserted_total);
-  __syncthreads();
-  if (threadIdx.x == 0 && blk_ins) atomicAdd(T.used, blk_ins);  // one global atomic per block
+  // one RED per warp into a partition of the occupancy counter (no block barrier)
+  const unsigned long long ins_warp = __reduce_add_sync(kFull, static_cast<unsigned>(inserted_total));
+  if (lane == 0 && ins_warp) atomicAdd(T.used + ((warp & (kUsedParts - 1)) * 8), ins_warp);
 }
 
 // ---------------------------------------------------------------------------
@@ -997,7 +993,7 @@ __global__ void k_rebuild_place(DevTrie from, DevTrie to, const uint32_t* __rest
     d->count = s.count;
     d->root = s.root;
     remap[i] = static_cast<uint32_t>(j + 1);
-    atomicAdd(to.used, 1ull);
+    atomicAdd(to.used + ((i & (kUsedParts - 1)) * 8), 1ull);
   }
 }
 

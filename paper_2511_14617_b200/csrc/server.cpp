@@ -399,8 +399,10 @@ uint64_t cap_for(uint64_t nodes, double load) {  // slots, a multiple of the pro
 
 int read_used(dgds_server* s, uint64_t* out) {
   unsigned long long u = 0;
-  DGDS_CUDA(cudaMemcpyAsync(&u, s->d_used, sizeof(u), cudaMemcpyDeviceToHost, s->st));
+  unsigned long long parts[dgds::kUsedParts * 8];
+  DGDS_CUDA(cudaMemcpyAsync(parts, s->d_used, sizeof(parts), cudaMemcpyDeviceToHost, s->st));
   DGDS_CUDA(cudaStreamSynchronize(s->st));
+  for (int p = 0; p < dgds::kUsedParts; ++p) u += parts[p * 8];
   *out = u;
   return DGDS_OK;
 }
@@ -413,8 +415,8 @@ int rebuild(dgds_server* s, uint64_t new_cap) {
   DGDS_CUDA(cudaMalloc(&to.slots, new_cap * sizeof(dgds::Slot)));
   DGDS_CUDA(cudaMemsetAsync(to.slots, 0, new_cap * sizeof(dgds::Slot), s->st));
   unsigned long long* d_used_new = nullptr;
-  DGDS_CUDA(cudaMalloc(&d_used_new, sizeof(unsigned long long)));
-  DGDS_CUDA(cudaMemsetAsync(d_used_new, 0, sizeof(unsigned long long), s->st));
+  DGDS_CUDA(cudaMalloc(&d_used_new, dgds::kUsedParts * 8 * sizeof(unsigned long long)));
+  DGDS_CUDA(cudaMemsetAsync(d_used_new, 0, dgds::kUsedParts * 8 * sizeof(unsigned long long), s->st));
   to.used = d_used_new;
   std::vector<uint32_t> alive((kRootCap + 31) / 32, 0);
   std::vector<uint32_t> live_slots, live_sizes;
@@ -691,8 +693,8 @@ int dgds_create(const dgds_params* params, dgds_server** out) {
   if (const char* e = std::getenv("DGDS_CLAIM")) s->T.claim_cas = std::strcmp(e, "load") == 0 ? 0 : 1;
   DGDS_CUDA(cudaMalloc(&s->T.slots, cap * sizeof(dgds::Slot)));
   DGDS_CUDA(cudaMemsetAsync(s->T.slots, 0, cap * sizeof(dgds::Slot), s->st));
-  DGDS_CUDA(cudaMalloc(&s->d_used, sizeof(unsigned long long)));
-  DGDS_CUDA(cudaMemsetAsync(s->d_used, 0, sizeof(unsigned long long), s->st));
+  DGDS_CUDA(cudaMalloc(&s->d_used, dgds::kUsedParts * 8 * sizeof(unsigned long long)));
+  DGDS_CUDA(cudaMemsetAsync(s->d_used, 0, dgds::kUsedParts * 8 * sizeof(unsigned long long), s->st));
   s->T.used = s->d_used;
   s->stream_cap = std::max<uint64_t>(p.expected_streams ? p.expected_streams : 4096, 64);
   DGDS_CUDA(cudaMalloc(&s->T.active, s->stream_cap * dgds::kWarp * sizeof(uint32_t)));

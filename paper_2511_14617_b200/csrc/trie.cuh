@@ -33,6 +33,7 @@
 namespace dgds {
 
 constexpr int kWarp = 32;
+constexpr int kUsedParts = 64;  // partitions of the occupancy counter (index p * 8)
 constexpr uint32_t kRootTop = 0xFFFFFFFFu;
 constexpr unsigned long long kHashMul = 0x9E3779B97F4A7C15ull;  // odd multiplier of the rolling hash
 
@@ -62,7 +63,7 @@ struct DevTrie {
   uint64_t cap;              // slots (ids 1..cap); arbitrary size (fast-range reduction)
   uint32_t* active;          // [stream][32]: node of the last (i+1)-token context (Stream::active, cst.hpp:117)
   int32_t* tail;             // [stream][32]: ring of the last 32 tokens (position & 31)
-  unsigned long long* used;  // occupied slots (device counter)
+  unsigned long long* used;  // occupied slots: kUsedParts counters, 64 B apart (sum = occupancy)
   int32_t depth_cap;         // max_pattern_len + max_spec_len (cst.cpp:106-107)
   int32_t lim_pattern;       // Limits::max_pattern_len
   int32_t lim_spec;          // Limits::max_spec_len
