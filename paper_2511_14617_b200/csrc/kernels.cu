@@ -1275,18 +1275,35 @@ __global__ void k_cmp_count(int64_t n, int32_t K, const int32_t* __restrict__ n_
   }
 }
 
-__global__ void k_cmp_scan(int64_t nblocks, long long* block_sums, long long* totals) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  long long c = 0, t = 0;
-  for (int64_t b = 0; b < nblocks; ++b) {
-    const long long bc = block_sums[2 * b], bt = block_sums[2 * b + 1];
-    block_sums[2 * b] = c;
-    block_sums[2 * b + 1] = t;
-    c += bc;
-    t += bt;
+__global__ void __launch_bounds__(kCmpBlock) k_cmp_scan(int64_t nblocks, long long* block_sums, long long* totals) {
+  // exclusive scan of the per-block (candidates, tokens) sums, one block, kCmpBlock at a time
+  using BS = cub::BlockScan<long long, kCmpBlock>;
+  __shared__ typename BS::TempStorage tmp;
+  __shared__ long long carry[2];
+  if (threadIdx.x == 0) carry[0] = carry[1] = 0;
+  __syncthreads();
+  for (int64_t b0 = 0; b0 < nblocks; b0 += kCmpBlock) {
+    const int64_t b = b0 + threadIdx.x;
+    long long c = b < nblocks ? block_sums[2 * b] : 0, t = b < nblocks ? block_sums[2 * b + 1] : 0;
+    long long cx, tx, ct, tt;
+    BS(tmp).ExclusiveSum(c, cx, ct);
+    __syncthreads();
+    BS(tmp).ExclusiveSum(t, tx, tt);
+    if (b < nblocks) {
+      block_sums[2 * b] = carry[0] + cx;
+      block_sums[2 * b + 1] = carry[1] + tx;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      carry[0] += ct;
+      carry[1] += tt;
+    }
+    __syncthreads();
   }
-  totals[0] = c;
-  totals[1] = t;
+  if (threadIdx.x == 0) {
+    totals[0] = carry[0];
+    totals[1] = carry[1];
+  }
 }
 
 __global__ void k_cmp_scatter(int64_t n, int32_t K, int32_t S, const int32_t* __restrict__ n_cands,
@@ -1345,15 +1362,16 @@ cudaError_t launch_compact(int64_t n, int32_t K, int32_t S, const int32_t* n_can
   if (n <= 0) return cudaSuccess;
   const int64_t nb = (n + kCmpBlock - 1) / kCmpBlock;
   k_cmp_count<<<static_cast<unsigned>(nb), kCmpBlock, 0, st>>>(n, K, n_cands, lens, block_sums);
-  k_cmp_scan<<<1, 1, 0, st>>>(nb, block_sums, totals);
+  k_cmp_scan<<<1, kCmpBlock, 0, st>>>(nb, block_sums, totals);
   k_cmp_scatter<<<static_cast<unsigned>(nb), kCmpBlock, 0, st>>>(n, K, S, n_cands, lens, scores, supports, tokens,
                                                                   block_sums, meta, tok_out, cand_off, tok_off);
   return cudaGetLastError();
 }
 
-cudaError_t launch_copy_out(const long long* totals, const CopyOutRegions& R, int64_t max_bytes, cudaStream_t st) {
+cudaError_t launch_copy_out(const long long* totals, const CopyOutRegions& R, int64_t max_bytes, cudaStream_t st,
+                            int max_blocks) {
   if (R.n == 0 || max_bytes <= 0) return cudaSuccess;
-  const int64_t blocks = std::min<int64_t>(592, (max_bytes / 16 + 255) / 256 + 1);
+  const int64_t blocks = std::min<int64_t>(max_blocks, (max_bytes / 16 + 255) / 256 + 1);
   k_copy_out<<<static_cast<unsigned>(blocks), 256, 0, st>>>(totals, R);
   return cudaGetLastError();
 }

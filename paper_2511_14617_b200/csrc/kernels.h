@@ -136,7 +136,8 @@ struct CopyOutRegions {
 };
 // Copies region r = totals[total_idx[r]] * elem_bytes[r] (or fixed_bytes[r]) bytes, a multiple
 // of 4; max_bytes sizes the grid.
-cudaError_t launch_copy_out(const long long* totals, const CopyOutRegions& R, int64_t max_bytes, cudaStream_t st);
+cudaError_t launch_copy_out(const long long* totals, const CopyOutRegions& R, int64_t max_bytes, cudaStream_t st,
+                            int max_blocks = 592);
 
 // block_sums: 2 * ceil(n / 256) scratch; totals[0] = candidates, totals[1] = tokens.
 // Outputs may live in mapped pinned host memory (written over PCIe by the kernel).

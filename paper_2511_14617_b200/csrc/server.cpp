@@ -254,6 +254,10 @@ struct dgds_server {
   int32_t D = 0;
   cudaStream_t st = nullptr;
   cudaEvent_t staging_free = nullptr;
+  // host-path query inputs: own staging pair and copy stream, so their H2D overlaps the
+  // append kernel queued before them on `st`
+  cudaStream_t copy_st = nullptr;
+  cudaEvent_t q_staging_free = nullptr, q_h2d_done = nullptr;
   dgds::DevTrie T{};
   unsigned long long* d_used = nullptr;
   uint64_t used_ub = 0;  // upper bound on occupied slots since the last exact read
@@ -273,6 +277,10 @@ struct dgds_server {
 
   PinnedBuf h_stage, h_out;  // h_out is mapped: the copy-out kernel stores results into it
   DevBuf d_stage, d_out;
+  PinnedBuf hq_stage;  // mapped: the copy-in kernel reads it over PCIe
+  DevBuf dq_stage;
+  bool h2d_kernel = true;  // DGDS_H2D=dma: copy-engine H2D instead
+  int h2d_blocks = 148;    // one CTA per SM (measured best); DGDS_H2D_BLOCKS
   std::unique_ptr<WorkerPool> pool;
   WorkerPool& workers() {
     if (!pool) pool = std::make_unique<WorkerPool>(host_threads() - 1);
@@ -675,10 +683,17 @@ int dgds_create(const dgds_params* params, dgds_server** out) {
   auto s = std::make_unique<dgds_server>();
   s->p = p;
   s->h_out.flags = cudaHostAllocMapped;
+  s->hq_stage.flags = cudaHostAllocMapped;
+  if (const char* e = std::getenv("DGDS_H2D")) s->h2d_kernel = std::strcmp(e, "dma") != 0;
+  cudaDeviceGetAttribute(&s->h2d_blocks, cudaDevAttrMultiProcessorCount, p.device);
+  if (const char* e = std::getenv("DGDS_H2D_BLOCKS")) s->h2d_blocks = std::max(1, std::atoi(e));
   s->D = p.max_pattern_len + p.max_spec_len;
   s->shard_counts.assign(p.shard_count, 0);
   DGDS_CUDA(cudaStreamCreateWithFlags(&s->st, cudaStreamNonBlocking));
   DGDS_CUDA(cudaEventCreateWithFlags(&s->staging_free, cudaEventDisableTiming));
+  DGDS_CUDA(cudaStreamCreateWithFlags(&s->copy_st, cudaStreamNonBlocking));
+  DGDS_CUDA(cudaEventCreateWithFlags(&s->q_staging_free, cudaEventDisableTiming));
+  DGDS_CUDA(cudaEventCreateWithFlags(&s->q_h2d_done, cudaEventDisableTiming));
   const uint64_t nodes = p.expected_nodes ? p.expected_nodes : (1ull << 20);
   double init_load = 0.5;  // expected_nodes is an upper bound, so the real load starts lower
   if (const char* e = std::getenv("DGDS_INIT_LOAD")) init_load = std::min(0.9, std::max(0.05, std::atof(e)));
@@ -723,6 +738,9 @@ int dgds_destroy(dgds_server* s) {
   cudaFree(s->d_err);
   cudaFree(s->d_stat_part);
   if (s->staging_free) cudaEventDestroy(s->staging_free);
+  if (s->q_staging_free) cudaEventDestroy(s->q_staging_free);
+  if (s->q_h2d_done) cudaEventDestroy(s->q_h2d_done);
+  if (s->copy_st) cudaStreamDestroy(s->copy_st);
   for (auto e : s->ev_pool) cudaEventDestroy(e);
   for (auto& v : s->ev_pending)
     for (auto& pr : v) {
@@ -1017,11 +1035,11 @@ int speculate_host(dgds_server* s, int64_t n, const int32_t* handles, const uint
   const size_t o_tl = align_up(o_tr + (verify ? static_cast<size_t>(n) * truth_stride * 4 : 0), 256);
   const size_t o_lm = align_up(o_tl + (verify ? n * 4 : 0), 256);
   const size_t in_all = o_lm + (verify ? n * 4 : 0);
-  DGDS_CUDA(cudaEventSynchronize(s->staging_free));
+  DGDS_CUDA(cudaEventSynchronize(s->q_staging_free));
   pc.mark("staging_wait");
-  if (int rc = s->h_stage.ensure(in_all)) return rc;
-  if (int rc = s->d_stage.ensure(in_all)) return rc;
-  char* h = static_cast<char*>(s->h_stage.p);
+  if (int rc = s->hq_stage.ensure(align_up(in_all, 16))) return rc;  // the copy-in kernel moves 16-B units
+  if (int rc = s->dq_stage.ensure(align_up(in_all, 16))) return rc;
+  char* h = static_cast<char*>(s->hq_stage.p);
   int32_t* hl = reinterpret_cast<int32_t*>(h + o_len);
   int32_t* hp = reinterpret_cast<int32_t*>(h + o_pat);
   const size_t ngroups = s->groups.size();
@@ -1083,11 +1101,26 @@ int speculate_host(dgds_server* s, int64_t n, const int32_t* handles, const uint
   const size_t h_toff = align_up(h_meta + nk * sizeof(dgds::CandMeta), 256);
   const size_t h_tok = align_up(h_toff + (nk + 1) * 8, 256);
   if (int rc = s->h_out.ensure(h_tok + static_cast<size_t>(nk) * Sx * 4)) return rc;
-  char* d = static_cast<char*>(s->d_stage.p);
+  char* d = static_cast<char*>(s->dq_stage.p);
   char* dout = static_cast<char*>(s->d_out.p);
   char* ho = static_cast<char*>(s->h_out.p);
-  DGDS_CUDA(cudaMemcpyAsync(d, h, in_all, cudaMemcpyHostToDevice, s->st));
-  DGDS_CUDA(cudaEventRecord(s->staging_free, s->st));
+  // the copy stream runs the H2D under the append kernel already queued on st; the query
+  // kernel waits for both (dq_stage is free: the previous query call synchronised)
+  if (s->h2d_kernel) {  // the GPU pulls the mapped staging block (steadier than the copy engine here)
+    dgds::CopyOutRegions Rin{};
+    Rin.n = 1;
+    Rin.total_idx[0] = -1;
+    Rin.fixed_bytes[0] = static_cast<int64_t>(align_up(in_all, 16));
+    Rin.src[0] = h;
+    Rin.dst[0] = d;
+    // a narrow grid: enough reads in flight for PCIe, SMs left to the append kernel running beside it
+    DGDS_CUDA(dgds::launch_copy_out(nullptr, Rin, Rin.fixed_bytes[0], s->copy_st, s->h2d_blocks));
+  } else {
+    DGDS_CUDA(cudaMemcpyAsync(d, h, in_all, cudaMemcpyHostToDevice, s->copy_st));
+  }
+  DGDS_CUDA(cudaEventRecord(s->q_staging_free, s->copy_st));
+  DGDS_CUDA(cudaEventRecord(s->q_h2d_done, s->copy_st));
+  DGDS_CUDA(cudaStreamWaitEvent(s->st, s->q_h2d_done, 0));
   dgds::QueryLaunch L{};
   L.T = s->T;
   L.root_of = s->d_root_of;
