@@ -39,8 +39,8 @@ DEFAULT_CONFIG = "C2"
 RANDOM_CEILING_GBS = 1155.0
 # dram__bytes_read.sum + dram__bytes_write.sum per launch, from one
 # `ncu --set full` capture of the same step (profiles/r1_summary.md).
-QUERY_TRAFFIC = 166678016 + 11980800
-APPEND_TRAFFIC = 311327744 + 47107072
+QUERY_TRAFFIC = 167104000 + 13064192   # prof_query_r1h (k_query<4,8>, timed step)
+APPEND_TRAFFIC = 181989888 + 99027968  # prof_append_r1h (k_append, timed step)
 CONFIG_NAMES = {
     "C1": "single group 16 x 4K, vocab 32K",
     "C2": "Moonlight-shaped 256 groups x 16 responses <=32K tokens, vocab 163840",
@@ -537,7 +537,8 @@ def main_b200(args):
         "roofline": roof_q if dom_q else roof_a,
         "roofline_query": roof_q, "roofline_append": roof_a,
         "cpu_baseline": cpu, "e2e": e2e,
-        "gpu_launches": int(prof.append_launches + prof.query_launches),
+        # K1 and K2+K3 launches (server profile) + one counter-fold kernel per counted query launch
+        "gpu_launches": int(prof.append_launches + 2 * prof.query_launches),
         "wall_ms_per_step": 1e3 * (w1 - w0) / K,
         "clocks": clk.summary(),
     }

@@ -62,6 +62,7 @@ t = json.load(open("gpurun_out/e2e_trace.json"))
 ev = [e for e in t["traceEvents"] if e.get("ph") == "X" and e.get("cat") in ("kernel", "gpu_memcpy", "gpu_memset", "cuda_runtime")]
 ev.sort(key=lambda e: e["ts"])
 gpu = [e for e in ev if e.get("cat") != "cuda_runtime"]
-t0 = gpu[-12]["ts"] if len(gpu) > 12 else gpu[0]["ts"]
-for e in gpu[-14:]:
-    print(f"{e['ts'] - t0:9.1f} {e['dur']:8.1f} {e['ts'] - t0 + e['dur']:9.1f} s{e['args'].get('stream')} {e['name'][:60]}")
+t0 = gpu[-16]["ts"] if len(gpu) > 16 else gpu[0]["ts"]
+for e in [x for x in ev if x["ts"] >= t0 - 2000]:
+    kind = "GPU" if e.get("cat") != "cuda_runtime" else "cpu"
+    print(f"{kind} {e['ts'] - t0:9.1f} {e['dur']:8.1f} {e['ts'] - t0 + e['dur']:9.1f} s{e['args'].get('stream', '')} {e['name'][:60]}")
