@@ -54,6 +54,7 @@ extern "C" {
 #define DGDS_EUNSUPPORTED (-4) /* outside this build's device limits (see DGDS_MAX_*) */
 #define DGDS_EBUFFER (-5)     /* caller output buffer too small */
 #define DGDS_ESTATE (-6)      /* bad handle / call order */
+#define DGDS_EBLOB (-7)       /* malformed or inapplicable GDX1 blob (std::runtime_error in the reference) */
 
 #define DGDS_MAX_DEPTH 32 /* max_pattern_len + max_spec_len (one warp lane per trie level) */
 #define DGDS_MAX_TOP_K 32
@@ -343,6 +344,35 @@ typedef struct dgds_workload_cfg {
 /* Pass 1 (tokens == NULL): fills lengths[num_groups*group_size] and prompt_lens[num_groups] (may be NULL).
  * Pass 2: also writes all outputs back to back (group-major, request-minor) into tokens. */
 int dgds_generate_workload(const dgds_workload_cfg* cfg, int64_t* lengths, int32_t* prompt_lens, int32_t* tokens);
+
+/* ---- replica sync: GDX1 blobs (cst.cpp:233-329) and DraftServer::fetch_cst (dgds.cpp:53-97) ----
+ * Blobs are byte-identical to the reference's: "GDX1", kind (1 delta, 2 full), u16+group id,
+ * u64 from, u64 to, u32 count, then delta records {u32 rid, u64 start, u32 len, i32 tokens[len]}
+ * or full-snapshot streams {u32 rid, u64 len, i32 tokens[len]} in request-id order, all
+ * big-endian. The tokens come from the device history arena that the append kernel fills. */
+#define DGDS_FETCH_UP_TO_DATE 0
+#define DGDS_FETCH_DELTA 1
+#define DGDS_FETCH_FULL 2
+#define DGDS_FETCH_UNKNOWN_GROUP 3
+typedef struct dgds_fetch_reply {
+  int32_t kind;      /* DGDS_FETCH_* (FetchKind, dgds.hpp:31) */
+  int32_t reserved;
+  uint64_t version;  /* the group's current version */
+  uint64_t blob_off; /* the blob is (*blobs)[blob_off .. blob_off + blob_len) */
+  uint64_t blob_len;
+} dgds_fetch_reply;
+/* Per group: UnknownGroup if absent or expired (lazy expiry), else the expiry is refreshed and
+ * UpToDate / Delta (cached version still in the log) / Full (cached 0, from the future, or
+ * compacted). *blobs points into a server-owned pinned block valid until the next fetch. */
+int dgds_fetch_cst(dgds_server* s, int64_t n, const int32_t* handles, const uint64_t* cached_versions, double now,
+                   dgds_fetch_reply* replies, const uint8_t** blobs);
+/* compact_log: drop log entries before min(before_version, version) (dgds.cpp:153-158). */
+int dgds_compact_group(dgds_server* s, int32_t handle, uint64_t before_version);
+/* apply_blob on this server's copy of the group (a GPU-resident replica): a delta needs the
+ * replica at the blob's from-version; a full snapshot replaces the replica. Errors are
+ * DGDS_EBLOB with the reference's messages. *version = the replica's new version. */
+int dgds_apply_blob(dgds_server* s, int32_t handle, const uint8_t* blob, uint64_t len, double now,
+                    uint64_t* version);
 
 /* ---- peer exchange over NVLink / NVSwitch (one process per GPU, CUDA IPC) ----
  * Replaces the all-to-all of the reference's shard routing (dgds.cpp:10-14 routes a

@@ -266,6 +266,14 @@ class RefLib(_Lib):
         L.orc_ref_server_group_version.argtypes = [C.c_void_p, C.c_char_p]
         L.orc_ref_server_shard_group_count.restype = C.c_uint64
         L.orc_ref_server_shard_group_count.argtypes = [C.c_void_p, C.c_int32]
+        L.orc_ref_server_fetch.argtypes = [C.c_void_p, C.c_char_p, C.c_uint64, C.c_double, C.POINTER(C.c_int32),
+                                           C.POINTER(C.c_uint64), C.c_void_p, C.c_uint64, C.POINTER(C.c_uint64)]
+        L.orc_ref_server_compact.argtypes = [C.c_void_p, C.c_char_p, C.c_uint64]
+        L.orc_index_full_snapshot.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64, C.POINTER(C.c_uint64)]
+        L.orc_index_delta_since.argtypes = [C.c_void_p, C.c_uint64, C.POINTER(C.c_int32), C.c_void_p, C.c_uint64,
+                                            C.POINTER(C.c_uint64)]
+        L.orc_index_apply_blob.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64, C.POINTER(C.c_uint64)]
+        L.orc_index_compact.argtypes = [C.c_void_p, C.c_uint64]
         L.orc_ref_workload_new.restype = C.c_void_p
         L.orc_ref_workload_new.argtypes = [C.POINTER(OrcWcfg)]
         L.orc_ref_workload_free.argtypes = [C.c_void_p]
@@ -287,6 +295,50 @@ class RefLib(_Lib):
 
     def shard_of_group(self, gid: str, n: int) -> int:
         return int(self.L.orc_ref_shard_of_group(gid.encode(), n))
+
+    # ---- replica sync (GDX1 blobs) ----
+    def _blob_call(self, fn, *args):
+        cap = 1 << 16
+        while True:
+            buf = C.create_string_buffer(cap)
+            ln = C.c_uint64()
+            rc = fn(*args, buf, cap, C.byref(ln))
+            if rc == -2:
+                cap = int(ln.value)
+                continue
+            if rc != 0:
+                raise self.err()
+            return buf.raw[:ln.value]
+
+    def server_fetch(self, srv, gid: str, cached: int, now: float):
+        """DraftServer::fetch_cst for one group -> (kind, version, blob bytes)."""
+        kind, ver = C.c_int32(), C.c_uint64()
+        blob = self._blob_call(lambda b, c, l: self.L.orc_ref_server_fetch(srv, gid.encode(), cached, now,
+                                                                           C.byref(kind), C.byref(ver), b, c, l))
+        return int(kind.value), int(ver.value), blob
+
+    def server_compact(self, srv, gid: str, before: int):
+        if self.L.orc_ref_server_compact(srv, gid.encode(), before) != 0:
+            raise self.err()
+
+    def index_full_snapshot(self, idx) -> bytes:
+        return self._blob_call(lambda b, c, l: self.L.orc_index_full_snapshot(idx.h, b, c, l))
+
+    def index_delta_since(self, idx, since: int):
+        avail = C.c_int32()
+        blob = self._blob_call(lambda b, c, l: self.L.orc_index_delta_since(idx.h, since, C.byref(avail), b, c, l))
+        return blob if avail.value else None
+
+    def index_apply_blob(self, idx, blob: bytes) -> int:
+        ver = C.c_uint64()
+        buf = C.create_string_buffer(bytes(blob), len(blob))
+        if self.L.orc_index_apply_blob(idx.h, buf, len(blob), C.byref(ver)) != 0:
+            raise self.err()
+        return int(ver.value)
+
+    def index_compact(self, idx, before: int):
+        if self.L.orc_index_compact(idx.h, before) != 0:
+            raise self.err()
 
     def workload(self, **cfg):
         """generate_workload (proj/src/workload.cpp:51-103) -> (group_ids, prompt_lens, outputs)."""

@@ -226,6 +226,71 @@ uint64_t orc_ref_server_shard_group_count(const void* s, int32_t shard) {
 }
 
 // ---------------------------------------------------------------------------
+// replica sync (GDX1 blobs): fetch_cst / compact_group on the server, and
+// full_snapshot / delta_since / apply_blob on a GroupDraftIndex. Blobs are
+// copied into caller buffers; *len is always the full size (-2 = too small).
+
+namespace {
+int copy_blob(const std::vector<std::uint8_t>& b, uint8_t* buf, uint64_t cap, uint64_t* len) {
+  *len = b.size();
+  if (b.size() > cap) {
+    g_err = "blob buffer too small";
+    return -2;
+  }
+  if (!b.empty()) std::memcpy(buf, b.data(), b.size());
+  return 0;
+}
+}  // namespace
+
+int orc_ref_server_fetch(void* s, const char* gid, uint64_t cached, double now, int32_t* kind, uint64_t* version,
+                         uint8_t* buf, uint64_t cap, uint64_t* len) {
+  return guarded([&] {
+    std::string id(gid);
+    DraftCacheInfo info{id, cached};
+    auto r = static_cast<DraftServer*>(s)->fetch_cst(std::span<const std::string>(&id, 1),
+                                                     std::span<const DraftCacheInfo>(&info, 1), now);
+    *kind = static_cast<int32_t>(r[0].kind);
+    *version = r[0].version;
+    return copy_blob(r[0].blob, buf, cap, len);
+  });
+}
+
+int orc_ref_server_compact(void* s, const char* gid, uint64_t before) {
+  return guarded([&] {
+    static_cast<DraftServer*>(s)->compact_group(gid, before);
+    return 0;
+  });
+}
+
+int orc_index_full_snapshot(const void* idx, uint8_t* buf, uint64_t cap, uint64_t* len) {
+  return guarded([&] { return copy_blob(static_cast<const GroupDraftIndex*>(idx)->full_snapshot(), buf, cap, len); });
+}
+
+int orc_index_delta_since(const void* idx, uint64_t since, int32_t* available, uint8_t* buf, uint64_t cap,
+                          uint64_t* len) {
+  return guarded([&] {
+    auto d = static_cast<const GroupDraftIndex*>(idx)->delta_since(since);
+    *available = d.has_value() ? 1 : 0;
+    *len = 0;
+    return d.has_value() ? copy_blob(*d, buf, cap, len) : 0;
+  });
+}
+
+int orc_index_apply_blob(void* idx, const uint8_t* blob, uint64_t len, uint64_t* version) {
+  return guarded([&] {
+    *version = static_cast<GroupDraftIndex*>(idx)->apply_blob(std::span<const std::uint8_t>(blob, len));
+    return 0;
+  });
+}
+
+int orc_index_compact(void* idx, uint64_t before) {
+  return guarded([&] {
+    static_cast<GroupDraftIndex*>(idx)->compact_log(before);
+    return 0;
+  });
+}
+
+// ---------------------------------------------------------------------------
 // generate_workload (workload.cpp:51-103)
 
 typedef struct orc_wcfg {

@@ -18,6 +18,7 @@ DGDS_ENOMEM = -3
 DGDS_EUNSUPPORTED = -4
 DGDS_EBUFFER = -5
 DGDS_ESTATE = -6
+DGDS_EBLOB = -7
 MAX_DEPTH = 32
 MAX_TOP_K = 32
 
@@ -72,6 +73,11 @@ class ResultView(C.Structure):
     _fields_ = [("n_queries", C.c_int64), ("n_cands", C.c_int64), ("n_tokens", C.c_int64),
                 ("cand_off", C.c_void_p), ("cands", C.c_void_p), ("tok_off", C.c_void_p), ("tokens", C.c_void_p),
                 ("drafted", C.c_void_p), ("accepted", C.c_void_p), ("emitted", C.c_void_p)]
+
+
+class FetchReply(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("reserved", C.c_int32), ("version", C.c_uint64), ("blob_off", C.c_uint64),
+                ("blob_len", C.c_uint64)]
 
 
 class QueryStats(C.Structure):
@@ -166,6 +172,9 @@ EXPORTS = {
     "dgds_route_unpack": (C.c_int, [_I64, _P, _I32, _P, _P, _P]),
     "dgds_route_pack_padded": (C.c_int, [_I64, _I32, _P, _P, _I32, _I64, _P, _P, _P, _P]),
     "dgds_speculate_records": (C.c_int, [_P, _I64, _P, C.POINTER(RecordLayout), _P, _I64, _I32, _I32, _P, _P, _P]),
+    "dgds_fetch_cst": (C.c_int, [_P, _I64, _P, _P, C.c_double, C.POINTER(FetchReply), C.POINTER(C.c_void_p)]),
+    "dgds_compact_group": (C.c_int, [_P, _I32, _U64]),
+    "dgds_apply_blob": (C.c_int, [_P, _I32, _P, _U64, C.c_double, C.POINTER(_U64)]),
     "dgds_update_batch_routed": (C.c_int, [_P, _I32, _I64, _P, _P, _I32, _P, _I32, C.c_double, C.POINTER(_I64),
                                            _P]),
     "dgds_copy_rows_d2h": (C.c_int, [_P, _I64, _P, _I64, _I64, _I64, _P]),

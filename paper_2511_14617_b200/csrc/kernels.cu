@@ -185,7 +185,11 @@ __global__ void __launch_bounds__(kBlock, 4) k_append(DevTrie T, const AppendSeg
       while (filled < kStage && p < g.npieces) {
         const AppendPiece pc = pieces[g.piece0 + p];
         const uint32_t take = min(static_cast<uint32_t>(kStage - filled), pc.n - poff);
-        for (uint32_t k = lane; k < take; k += kWarp) stage_w[filled + k] = tokens[pc.tok_off + poff + k];
+        for (uint32_t k = lane; k < take; k += kWarp) {
+          const int32_t v = tokens[pc.tok_off + poff + k];
+          stage_w[filled + k] = v;
+          T.hist[pc.hist_off + poff + k] = v;  // history arena (coalesced)
+        }
         filled += static_cast<int>(take);
         poff += take;
         if (poff == pc.n) {
@@ -961,6 +965,37 @@ __global__ void k_verify(int64_t n, int32_t k_stride, int32_t s_stride, const in
   emitted[q] = em;
 }
 
+// GDX1 blob serialisation: warp per piece; byte stores (blob fields are not 4-B aligned).
+__device__ __forceinline__ void put_be(uint8_t* p, uint64_t v, int bytes) {
+  for (int b = 0; b < bytes; ++b) p[b] = static_cast<uint8_t>(v >> (8 * (bytes - 1 - b)));
+}
+
+__global__ void k_blob_fill(const BlobPiece* __restrict__ pieces, int64_t n, const int32_t* __restrict__ hist,
+                            uint8_t* out) {
+  const int lane = lane_id();
+  const int64_t nw = static_cast<int64_t>(gridDim.x) * (blockDim.x / kWarp);
+  for (int64_t w = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / kWarp; w < n; w += nw) {
+    const BlobPiece pc = pieces[w];
+    uint8_t* dst = out + pc.dst;
+    if (lane == 0 && pc.hdr_kind == 1) {  // delta record: u32 rid, u64 start, u32 len
+      put_be(dst - 16, pc.rid, 4);
+      put_be(dst - 12, pc.hdr_a, 8);
+      put_be(dst - 4, pc.len, 4);
+    } else if (lane == 0 && pc.hdr_kind == 2) {  // full-snapshot stream: u32 rid, u64 len
+      put_be(dst - 12, pc.rid, 4);
+      put_be(dst - 8, pc.hdr_a, 8);
+    }
+    for (uint32_t i = lane; i < pc.len; i += kWarp) {
+      const uint32_t v = static_cast<uint32_t>(hist[pc.src + i]);
+      uint8_t* q = dst + 4ull * i;
+      q[0] = static_cast<uint8_t>(v >> 24);
+      q[1] = static_cast<uint8_t>(v >> 16);
+      q[2] = static_cast<uint8_t>(v >> 8);
+      q[3] = static_cast<uint8_t>(v);
+    }
+  }
+}
+
 __global__ void k_set_u32(uint32_t* dst, uint32_t v) { *dst = v; }
 
 // ---------------------------------------------------------------------------
@@ -1177,6 +1212,14 @@ cudaError_t launch_verify(int64_t n, int32_t k_stride, int32_t s_stride, const i
   k_verify<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(n, k_stride, s_stride, n_cands, lens, tokens,
                                                                       truth, truth_stride, truth_left, limit, drafted,
                                                                       accepted, emitted);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_blob_fill(const BlobPiece* d_pieces, int64_t n, const int32_t* hist, uint8_t* out,
+                             cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  const int64_t blocks = std::min<int64_t>((n + 7) / 8, 148 * 8);
+  k_blob_fill<<<static_cast<unsigned>(blocks), 256, 0, st>>>(d_pieces, n, hist, out);
   return cudaGetLastError();
 }
 

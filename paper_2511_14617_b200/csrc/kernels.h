@@ -24,10 +24,27 @@ struct AppendSeg {
 static_assert(sizeof(AppendSeg) == 32, "AppendSeg is 32 B");
 
 struct AppendPiece {
-  uint64_t tok_off;  // into the batch token buffer
+  uint64_t tok_off;   // into the batch token buffer
+  uint64_t hist_off;  // where K1 copies the tokens in the history arena (DevTrie::hist)
   uint32_t n;
   uint32_t pad_;
 };
+
+// One piece of a GDX1 blob (cst.cpp:233-269), serialised big-endian on the device:
+// an optional header right before `dst` — kind 1: delta record {u32 rid, u64 start, u32 len}
+// (16 B), kind 2: full-snapshot stream {u32 rid, u64 len} (12 B) — then `len` tokens copied
+// from the history arena at src as big-endian i32.
+struct BlobPiece {
+  uint64_t src;  // history arena offset (tokens)
+  uint64_t dst;  // byte offset of the first token in the output
+  uint64_t hdr_a;  // start (kind 1) or stream length (kind 2)
+  uint32_t len;  // tokens
+  uint32_t rid;
+  uint32_t hdr_kind;
+  uint32_t pad_;
+};
+cudaError_t launch_blob_fill(const BlobPiece* d_pieces, int64_t n, const int32_t* hist, uint8_t* out,
+                             cudaStream_t st);
 
 cudaError_t launch_append(const DevTrie& T, const AppendSeg* d_segs, int64_t nseg, const AppendPiece* d_pieces,
                           const int32_t* d_tokens, cudaStream_t st);

@@ -184,7 +184,20 @@ int host_threads() {
   return std::max(1, std::min(8, hc - 1));
 }
 
+struct HistChunk {  // tokens of one accepted append in the history arena
+  uint64_t off;
+  uint32_t len;
+};
+
+struct LogRec {  // GroupDraftIndex::LogEntry (cst.hpp:120-124) + where its tokens live
+  uint64_t off;
+  uint64_t start;
+  uint32_t len;
+  int32_t rid;
+};
+
 struct StreamRec {
+  std::vector<HistChunk> chunks;  // the stream's tokens, in order (full snapshots)
   uint64_t stored = 0;
   uint32_t slot = 0;
   int64_t batch_seg = -1;  // segment index in the batch being built
@@ -245,6 +258,8 @@ struct GroupRec {
   double expires = 0.0;
   uint64_t version = 0;
   StreamTable streams;
+  std::vector<LogRec> log;  // entries of versions log_floor+1 .. version (delta blobs)
+  uint64_t log_floor = 0;
 };
 
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
@@ -263,6 +278,11 @@ struct dgds_server {
   dgds::DevTrie T{};
   unsigned long long* d_used = nullptr;
   uint64_t used_ub = 0;  // upper bound on occupied slots since the last exact read
+
+  int32_t* d_hist = nullptr;  // append-only token history (GDX1 blobs); K1 fills it
+  uint64_t hist_cap = 0, hist_used = 0;
+  DevBuf d_blob, d_blob_pieces;
+  PinnedBuf h_blob;
 
   uint32_t* d_root_of = nullptr;
   size_t root_of_cap = 0;
@@ -356,6 +376,9 @@ void retire_group(dgds_server* s, GroupRec& g) {
   if (!g.alive) return;
   g.streams.for_each([&](int32_t, StreamRec& r) { s->free_streams.push_back(r.slot); });
   g.streams.clear();
+  g.log.clear();
+  g.log.shrink_to_fit();
+  g.log_floor = 0;
   g.alive = false;
   g.version = 0;
   s->shard_counts[g.shard] -= 1;
@@ -370,6 +393,8 @@ int create_group(dgds_server* s, GroupRec& g, double ttl, double now) {
   g.expires = now + ttl;
   g.version = 0;
   g.streams.clear();
+  g.log.clear();
+  g.log_floor = 0;
   s->shard_counts[g.shard] += 1;
   return set_root(s, static_cast<int32_t>(&g - s->groups.data()), g.root);
 }
@@ -493,8 +518,26 @@ uint64_t worst_windows(uint64_t start, uint64_t n, uint64_t D) {
 struct PendingPiece {
   int64_t seg;
   uint64_t tok_off;
+  uint64_t hist_off;
   uint32_t n;
 };
+
+// Grow the history arena to hold hist_used tokens (stream-ordered copy; rare).
+int ensure_hist(dgds_server* s) {
+  if (s->hist_used <= s->hist_cap) return DGDS_OK;
+  uint64_t nc = std::max<uint64_t>(s->hist_used, s->hist_cap * 2);
+  int32_t* nb = nullptr;
+  if (cudaMalloc(&nb, nc * sizeof(int32_t)) != cudaSuccess) return fail(DGDS_ENOMEM, "history arena allocation failed");
+  if (s->d_hist) {
+    DGDS_CUDA(cudaStreamSynchronize(s->st));  // appends in flight finish writing the old arena
+    DGDS_CUDA(cudaMemcpy(nb, s->d_hist, s->hist_cap * sizeof(int32_t), cudaMemcpyDeviceToDevice));
+    cudaFree(s->d_hist);
+  }
+  s->d_hist = nb;
+  s->hist_cap = nc;
+  s->T.hist = nb;
+  return DGDS_OK;
+}
 
 // Shared host logic of update_batch / update_batch_device: replies in call
 // order (DraftServer::update_cst, dgds.cpp:36-51 -> GroupDraftIndex::append,
@@ -549,7 +592,11 @@ int plan_updates(dgds_server* s, int64_t n, const int32_t* handles, const int32_
       sg.start = sr.stored;
       segs.push_back(sg);
     }
-    pend.push_back(PendingPiece{sr.batch_seg, tstart(i), static_cast<uint32_t>(cnt)});
+    const uint64_t hoff = s->hist_used;
+    s->hist_used += cnt;
+    pend.push_back(PendingPiece{sr.batch_seg, tstart(i), hoff, static_cast<uint32_t>(cnt)});
+    g.log.push_back(LogRec{hoff, sr.stored, static_cast<uint32_t>(cnt), rids[i]});
+    sr.chunks.push_back(HistChunk{hoff, static_cast<uint32_t>(cnt)});
     *worst += worst_windows(sr.stored, cnt, static_cast<uint64_t>(s->D));
     sr.stored += cnt;
     g.version += 1;
@@ -567,7 +614,7 @@ int plan_updates(dgds_server* s, int64_t n, const int32_t* handles, const int32_
   std::vector<uint32_t> fill(segs.size(), 0);
   for (const auto& pp : pend) {
     const uint32_t at = segs[pp.seg].piece0 + fill[pp.seg]++;
-    pieces[at] = dgds::AppendPiece{pp.tok_off, pp.n, 0};
+    pieces[at] = dgds::AppendPiece{pp.tok_off, pp.hist_off, pp.n, 0};
   }
   return DGDS_OK;
 }
@@ -718,6 +765,9 @@ int dgds_create(const dgds_params* params, dgds_server** out) {
   DGDS_CUDA(cudaMalloc(&s->T.tail, s->stream_cap * dgds::kWarp * sizeof(int32_t)));
   DGDS_CUDA(cudaMalloc(&s->d_err, sizeof(int32_t)));
   DGDS_CUDA(cudaMemsetAsync(s->d_err, 0, sizeof(int32_t), s->st));
+  s->hist_cap = std::max<uint64_t>(1ull << 20, nodes / 20);  // ~ tokens (nodes per token ~ 17-24)
+  DGDS_CUDA(cudaMalloc(&s->d_hist, s->hist_cap * sizeof(int32_t)));
+  s->T.hist = s->d_hist;
   DGDS_CUDA(cudaMalloc(&s->d_stat_part, dgds::kStatParts * 8 * sizeof(unsigned long long)));
   DGDS_CUDA(cudaMemsetAsync(s->d_stat_part, 0, dgds::kStatParts * 8 * sizeof(unsigned long long), s->st));
   s->root_of_cap = 1024;
@@ -739,6 +789,7 @@ int dgds_destroy(dgds_server* s) {
   cudaFree(s->d_root_of);
   cudaFree(s->d_err);
   cudaFree(s->d_stat_part);
+  cudaFree(s->d_hist);
   if (s->staging_free) cudaEventDestroy(s->staging_free);
   if (s->q_staging_free) cudaEventDestroy(s->q_staging_free);
   if (s->q_h2d_done) cudaEventDestroy(s->q_h2d_done);
@@ -852,12 +903,15 @@ int dgds_node_count(dgds_server* s, uint64_t* out) {
   return DGDS_OK;
 }
 
-int dgds_update_batch(dgds_server* s, int64_t n, const int32_t* handles, const int32_t* rids, const uint64_t* prev,
-                      const uint64_t* offs, const int32_t* tokens, double now, dgds_update_reply* rep) {
+}  // extern "C"
+
+// dgds_update_batch without the lock (also the replica path of dgds_apply_blob)
+static int update_batch_locked(dgds_server* s, int64_t n, const int32_t* handles, const int32_t* rids,
+                               const uint64_t* prev, const uint64_t* offs, const int32_t* tokens, double now,
+                               dgds_update_reply* rep) {
   if (n < 0) return fail(DGDS_EINVAL, "negative batch size");
   if (n == 0) return DGDS_OK;
   PhaseClock pc("update_batch");
-  std::lock_guard<std::mutex> lk(s->mu);
   DGDS_CUDA(cudaSetDevice(s->p.device));
   const uint64_t ntok = offs[n] - offs[0];
   for (uint64_t i = offs[0]; i < offs[n]; ++i)
@@ -869,6 +923,7 @@ int dgds_update_batch(dgds_server* s, int64_t n, const int32_t* handles, const i
   pc.mark("plan");
   if (segs.empty()) return DGDS_OK;
   if (int rc = ensure_capacity(s, worst)) return rc;
+  if (int rc = ensure_hist(s)) return rc;
   // one pinned staging block -> one H2D copy: segs | pieces | tokens
   const size_t b_seg = segs.size() * sizeof(dgds::AppendSeg);
   const size_t o_piece = align_up(b_seg, 256);
@@ -897,6 +952,16 @@ int dgds_update_batch(dgds_server* s, int64_t n, const int32_t* handles, const i
   return DGDS_OK;
 }
 
+extern "C" int dgds_update_batch(dgds_server* s, int64_t n, const int32_t* handles, const int32_t* rids,
+                                 const uint64_t* prev, const uint64_t* offs, const int32_t* tokens, double now,
+                                 dgds_update_reply* rep) {
+  if (!s) return fail(DGDS_EINVAL, "null server");
+  std::lock_guard<std::mutex> lk(s->mu);
+  return update_batch_locked(s, n, handles, rids, prev, offs, tokens, now, rep);
+}
+
+extern "C" {
+
 static int update_device_impl(dgds_server* s, int64_t n, const int32_t* handles, const int32_t* rids, const uint64_t* prev,
                        const uint64_t* offs, const uint64_t* counts, const int32_t* d_tokens, double now,
                        dgds_update_reply* rep, void* stream) {
@@ -910,6 +975,7 @@ static int update_device_impl(dgds_server* s, int64_t n, const int32_t* handles,
   if (int rc = plan_updates(s, n, handles, rids, prev, offs, counts, now, rep, segs, pieces, &worst)) return rc;
   if (segs.empty()) return DGDS_OK;
   if (int rc = ensure_capacity(s, worst)) return rc;
+  if (int rc = ensure_hist(s)) return rc;
   StreamJoin join(s, stream);
   const size_t b_seg = segs.size() * sizeof(dgds::AppendSeg);
   const size_t o_piece = align_up(b_seg, 256);
@@ -1586,3 +1652,274 @@ static DevBuf* route_scratch(cudaStream_t st, size_t bytes, int* rc) {
   *rc = buf->ensure(bytes);
   return buf;
 }
+
+// ---------------------------------------------------------------------------
+// Replica sync: GDX1 delta / full-snapshot blobs (GroupDraftIndex::delta_since /
+// full_snapshot / apply_blob / compact_log, cst.cpp:233-329) and
+// DraftServer::fetch_cst (dgds.cpp:53-97). Blobs are big-endian (bytes.hpp).
+// The tokens come from the device history arena that K1 fills; the record
+// framing and byte swap are done by k_blob_fill, the preamble on the host.
+
+namespace {
+
+constexpr uint8_t kBlobDelta = 1, kBlobFull = 2;
+
+size_t blob_preamble_bytes(const std::string& gid) { return 4 + 1 + 2 + gid.size() + 8 + 8 + 4; }
+
+void put_be(uint8_t*& p, uint64_t v, int bytes) {
+  for (int b = bytes - 1; b >= 0; --b) *p++ = static_cast<uint8_t>(v >> (8 * b));
+}
+
+void write_preamble(uint8_t* p, uint8_t kind, const std::string& gid, uint64_t from, uint64_t to, uint32_t n) {
+  *p++ = 'G';
+  *p++ = 'D';
+  *p++ = 'X';
+  *p++ = '1';
+  *p++ = kind;
+  put_be(p, gid.size(), 2);
+  std::memcpy(p, gid.data(), gid.size());
+  p += gid.size();
+  put_be(p, from, 8);
+  put_be(p, to, 8);
+  put_be(p, n, 4);
+}
+
+struct BlobReader {  // detail::ByteReader (bytes.hpp) over a caller buffer
+  const uint8_t* p;
+  const uint8_t* end;
+  bool ok = true;
+  uint64_t get(int bytes) {
+    if (end - p < bytes) {
+      ok = false;
+      p = end;
+      return 0;
+    }
+    uint64_t v = 0;
+    for (int b = 0; b < bytes; ++b) v = (v << 8) | *p++;
+    return v;
+  }
+  std::string str() {
+    const uint64_t n = get(2);
+    if (!ok || static_cast<uint64_t>(end - p) < n) {
+      ok = false;
+      return {};
+    }
+    std::string s(reinterpret_cast<const char*>(p), n);
+    p += n;
+    return s;
+  }
+};
+
+}  // namespace
+
+extern "C" {
+
+int dgds_fetch_cst(dgds_server* s, int64_t n, const int32_t* handles, const uint64_t* cached, double now,
+                   dgds_fetch_reply* rep, const uint8_t** blobs) {
+  if (!s || n < 0 || (n > 0 && (!handles || !cached || !rep || !blobs))) return fail(DGDS_EINVAL, "null argument");
+  std::lock_guard<std::mutex> lk(s->mu);
+  DGDS_CUDA(cudaSetDevice(s->p.device));
+  for (int64_t i = 0; i < n; ++i)
+    if (int rc = check_handle(s, handles[i])) return rc;
+  std::vector<dgds::BlobPiece> pieces;
+  struct Pre {
+    int64_t i;
+    uint8_t kind;
+    uint64_t from, to;
+    uint32_t count;
+  };
+  std::vector<Pre> pre;
+  uint64_t total = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    GroupRec& g = s->groups[handles[i]];
+    dgds_fetch_reply& r = rep[i];
+    r = dgds_fetch_reply{};
+    if (!live_entry(s, g, now)) {  // lazy expiry erases it (dgds.cpp:25-34)
+      r.kind = DGDS_FETCH_UNKNOWN_GROUP;
+      continue;
+    }
+    g.expires = now + g.ttl;
+    const uint64_t cur = g.version, c = cached[i];
+    r.version = cur;
+    if (c == cur && c != 0) {
+      r.kind = DGDS_FETCH_UP_TO_DATE;
+      continue;
+    }
+    if (c == cur) {  // both 0: nothing appended yet, the reference answers UpToDate too
+      r.kind = DGDS_FETCH_UP_TO_DATE;
+      continue;
+    }
+    const bool delta = c != 0 && c < cur && c >= g.log_floor;  // else Full (stale, fresh or compacted)
+    const uint64_t base = (total + 7) & ~7ull;
+    uint64_t pos = base + blob_preamble_bytes(g.gid);
+    if (delta) {
+      const size_t first = static_cast<size_t>(c - g.log_floor);
+      for (size_t k = first; k < g.log.size(); ++k) {
+        const LogRec& e = g.log[k];
+        pos += 16;
+        pieces.push_back(dgds::BlobPiece{e.off, pos, e.start, e.len, static_cast<uint32_t>(e.rid), 1, 0});
+        pos += 4ull * e.len;
+      }
+      pre.push_back(Pre{i, kBlobDelta, c, cur, static_cast<uint32_t>(g.log.size() - first)});
+    } else {
+      std::vector<std::pair<int32_t, StreamRec*>> st;  // std::map order: request id ascending
+      g.streams.for_each([&](int32_t rid, StreamRec& sr) { st.emplace_back(rid, &sr); });
+      std::sort(st.begin(), st.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
+      for (auto& [rid, sr] : st) {
+        pos += 12;
+        if (sr->chunks.empty()) {
+          pieces.push_back(dgds::BlobPiece{0, pos, 0, 0, static_cast<uint32_t>(rid), 2, 0});
+          continue;
+        }
+        bool first = true;
+        for (const HistChunk& ch : sr->chunks) {
+          pieces.push_back(dgds::BlobPiece{ch.off, pos, sr->stored, ch.len, static_cast<uint32_t>(rid),
+                                           first ? 2u : 0u, 0});
+          first = false;
+          pos += 4ull * ch.len;
+        }
+      }
+      pre.push_back(Pre{i, kBlobFull, 0, cur, static_cast<uint32_t>(st.size())});
+    }
+    r.kind = delta ? DGDS_FETCH_DELTA : DGDS_FETCH_FULL;
+    r.blob_off = base;
+    r.blob_len = pos - base;
+    total = pos;
+  }
+  if (total == 0) {
+    *blobs = static_cast<const uint8_t*>(s->h_blob.p);
+    return DGDS_OK;
+  }
+  if (int rc = s->d_blob.ensure(total)) return rc;
+  if (int rc = s->h_blob.ensure(total)) return rc;
+  if (!pieces.empty()) {
+    if (int rc = s->d_blob_pieces.ensure(pieces.size() * sizeof(dgds::BlobPiece))) return rc;
+    DGDS_CUDA(cudaMemcpyAsync(s->d_blob_pieces.p, pieces.data(), pieces.size() * sizeof(dgds::BlobPiece),
+                              cudaMemcpyHostToDevice, s->st));
+    DGDS_CUDA(dgds::launch_blob_fill(static_cast<const dgds::BlobPiece*>(s->d_blob_pieces.p),
+                                     static_cast<int64_t>(pieces.size()), s->d_hist,
+                                     static_cast<uint8_t*>(s->d_blob.p), s->st));
+  }
+  DGDS_CUDA(cudaMemcpyAsync(s->h_blob.p, s->d_blob.p, total, cudaMemcpyDeviceToHost, s->st));
+  DGDS_CUDA(cudaStreamSynchronize(s->st));
+  uint8_t* hb = static_cast<uint8_t*>(s->h_blob.p);
+  for (const Pre& p : pre) {
+    const GroupRec& g = s->groups[handles[p.i]];
+    write_preamble(hb + rep[p.i].blob_off, p.kind, g.gid, p.from, p.to, p.count);
+  }
+  *blobs = hb;
+  return DGDS_OK;
+}
+
+int dgds_compact_group(dgds_server* s, int32_t h, uint64_t before_version) {  // dgds.cpp:153-158, cst.cpp:324-329
+  if (!s) return fail(DGDS_EINVAL, "null server");
+  std::lock_guard<std::mutex> lk(s->mu);
+  if (int rc = check_handle(s, h)) return rc;
+  GroupRec& g = s->groups[h];
+  if (!g.alive) return DGDS_OK;
+  const uint64_t floor = std::min(before_version, g.version);
+  if (floor <= g.log_floor) return DGDS_OK;
+  g.log.erase(g.log.begin(), g.log.begin() + static_cast<std::ptrdiff_t>(floor - g.log_floor));
+  g.log_floor = floor;
+  return DGDS_OK;
+}
+
+int dgds_apply_blob(dgds_server* s, int32_t h, const uint8_t* blob, uint64_t len, double now, uint64_t* version) {
+  if (!s || (!blob && len)) return fail(DGDS_EINVAL, "null argument");
+  std::lock_guard<std::mutex> lk(s->mu);
+  if (int rc = check_handle(s, h)) return rc;
+  GroupRec& g = s->groups[h];
+  BlobReader r{blob, blob + len};
+  char magic[4];
+  for (char& c : magic) c = static_cast<char>(r.get(1));
+  if (!r.ok || std::memcmp(magic, "GDX1", 4) != 0) return fail(DGDS_EBLOB, "bad draft blob magic");
+  const uint8_t kind = static_cast<uint8_t>(r.get(1));
+  const std::string gid = r.str();
+  if (!r.ok) return fail(DGDS_EBLOB, "truncated record");
+  if (gid != g.gid) return fail(DGDS_EBLOB, "draft blob for group " + gid + " applied to " + g.gid);
+  const uint64_t from = r.get(8), to = r.get(8);
+  if (!r.ok) return fail(DGDS_EBLOB, "truncated record");
+  if (!live_entry(s, g, now)) {  // a replica starts empty (version 0)
+    if (int rc = create_group(s, g, s->p.default_ttl_seconds, now)) return rc;
+  }
+  g.expires = now + g.ttl;
+  std::vector<int32_t> rids, toks;
+  std::vector<uint64_t> prevs, offs{0};
+  auto read_tokens = [&](uint64_t cnt) -> bool {
+    if (static_cast<uint64_t>(r.end - r.p) / 4 < cnt) {
+      r.ok = false;
+      return false;
+    }
+    for (uint64_t k = 0; k < cnt; ++k) toks.push_back(static_cast<int32_t>(static_cast<uint32_t>(r.get(4))));
+    return true;
+  };
+  if (kind == kBlobDelta) {
+    if (from != g.version)
+      return fail(DGDS_EBLOB, "delta expects replica at version " + std::to_string(from) + ", replica is at " +
+                                  std::to_string(g.version));
+    const uint64_t cnt = r.get(4);
+    // entries apply in order; like the reference, stop at the first one out of order
+    std::unordered_map<int32_t, uint64_t> stored;
+    bool bad = false;
+    for (uint64_t k = 0; k < cnt && r.ok; ++k) {
+      const int32_t rid = static_cast<int32_t>(static_cast<uint32_t>(r.get(4)));
+      const uint64_t start = r.get(8);
+      const uint64_t n = r.get(4);
+      if (!r.ok || !read_tokens(n)) break;
+      auto it = stored.find(rid);
+      if (it == stored.end()) {
+        const StreamRec* sr = g.streams.find(rid);
+        it = stored.emplace(rid, sr ? sr->stored : 0).first;
+      }
+      if (n > 0 && start != it->second) {  // append() would reply ok=false
+        toks.resize(offs.back());
+        bad = true;
+        break;
+      }
+      it->second += n;
+      rids.push_back(rid);
+      prevs.push_back(start);
+      offs.push_back(toks.size());
+    }
+    if (!r.ok && !bad) return fail(DGDS_EBLOB, "truncated record");
+    std::vector<int32_t> hs(rids.size(), h);
+    std::vector<dgds_update_reply> rep(rids.size());
+    if (!rids.empty()) {
+      if (int rc = update_batch_locked(s, static_cast<int64_t>(rids.size()), hs.data(), rids.data(), prevs.data(),
+                                       offs.data(), toks.data(), now, rep.data()))
+        return rc;
+    }
+    if (bad) return fail(DGDS_EBLOB, "delta entry out of order during apply");
+    if (g.version != to) return fail(DGDS_EBLOB, "delta apply ended at unexpected version");
+  } else if (kind == kBlobFull) {
+    const uint64_t cnt = r.get(4);
+    for (uint64_t k = 0; k < cnt && r.ok; ++k) {
+      rids.push_back(static_cast<int32_t>(static_cast<uint32_t>(r.get(4))));
+      const uint64_t n = r.get(8);
+      if (!r.ok || !read_tokens(n)) break;
+      prevs.push_back(0);
+      offs.push_back(toks.size());
+    }
+    if (!r.ok) return fail(DGDS_EBLOB, "truncated record");
+    // replace the replica: a fresh root, no streams, no history (cst.cpp:300-318)
+    const double ttl = g.ttl;
+    retire_group(s, g);
+    if (int rc = create_group(s, g, ttl, now)) return rc;
+    std::vector<int32_t> hs(rids.size(), h);
+    std::vector<dgds_update_reply> rep(rids.size());
+    if (!rids.empty()) {
+      if (int rc = update_batch_locked(s, static_cast<int64_t>(rids.size()), hs.data(), rids.data(), prevs.data(),
+                                       offs.data(), toks.data(), now, rep.data()))
+        return rc;
+    }
+    g.version = to;  // a restored replica owns no history older than the snapshot
+    g.log.clear();
+    g.log_floor = to;
+  } else {
+    return fail(DGDS_EBLOB, "unknown draft blob kind");
+  }
+  if (version) *version = g.version;
+  return DGDS_OK;
+}
+
+}  // extern "C"

@@ -69,6 +69,7 @@ struct DevTrie {
   int32_t lim_spec;          // Limits::max_spec_len
   int32_t ahead;             // append look-ahead (tokens) of the L2 prefetch; 0 = off
   int32_t claim_cas;         // append claim: 1 = CAS-first, 0 = read the window first
+  int32_t* hist;             // append-only token history (replica sync blobs); K1 copies every token
 };
 
 __host__ __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {

@@ -63,6 +63,17 @@ class DraftCandidate:
         return (self.tokens, np.float64(self.score).view(np.uint64).item(), self.support)
 
 
+class FetchKind:  # dgds.hpp:31
+    UpToDate, Delta, Full, UnknownGroup = 0, 1, 2, 3
+
+
+@dataclass(frozen=True)
+class FetchReply:  # dgds.hpp:33-37
+    kind: int
+    version: int
+    blob: bytes
+
+
 @dataclass(frozen=True)
 class UpdateReply:
     """rollsim::UpdateReply (dgds.hpp:39-43)."""
@@ -198,6 +209,36 @@ class DraftServer:
         out = C.c_uint64()
         check(lib().dgds_node_count(self._h, C.byref(out)))
         return int(out.value)
+
+    # ---- replica sync (GDX1 blobs, cst.cpp:233-329; fetch_cst, dgds.cpp:53-97) ----
+    def fetch_cst(self, group_ids: Sequence[str], cached_versions: Sequence[int], now: float) -> List[FetchReply]:
+        """DraftServer::fetch_cst: per group UpToDate / Delta / Full / UnknownGroup with the
+        reference's byte-exact blob."""
+        if len(group_ids) != len(cached_versions):
+            raise ValueError("fetch_cst: group_ids and draft_cache_infos must have equal length")
+        n = len(group_ids)
+        if n == 0:
+            return []
+        hs = np.ascontiguousarray(self.group_handles(group_ids), np.int32)
+        cv = np.ascontiguousarray(cached_versions, np.uint64)
+        reps = (_lib.FetchReply * n)()
+        base = C.c_void_p()
+        check(lib().dgds_fetch_cst(self._h, n, _ptr(hs), _ptr(cv), float(now), reps, C.byref(base)))
+        out = []
+        for r in reps:
+            blob = C.string_at(base.value + r.blob_off, r.blob_len) if r.blob_len else b""
+            out.append(FetchReply(int(r.kind), int(r.version), blob))
+        return out
+
+    def compact_group(self, group_id: str, before_version: int):
+        check(lib().dgds_compact_group(self._h, self.group_handle(group_id), int(before_version)))
+
+    def apply_blob(self, group_id: str, blob: bytes, now: float = 0.0) -> int:
+        """GroupDraftIndex::apply_blob on this server's copy of the group (a GPU replica)."""
+        v = C.c_uint64()
+        buf = C.create_string_buffer(bytes(blob), len(blob))
+        check(lib().dgds_apply_blob(self._h, self.group_handle(group_id), buf, len(blob), float(now), C.byref(v)))
+        return int(v.value)
 
     def index_slots(self) -> int:
         out = C.c_uint64()
