@@ -3,7 +3,9 @@
 // Mirrors the reference C++ API so a rollout engine can switch by changing the
 // include and namespace:
 //   rollsim::DraftServer      (proj/include/rollsim/dgds.hpp:51-91)   -> dgds_b200::DraftServer
-//   rollsim::DraftClient      (dgds.hpp:128-162, fetch_period 0 mode) -> dgds_b200::DraftClient
+//   rollsim::DraftClient      (dgds.hpp:128-162)                      -> dgds_b200::DraftClient
+//     fetch_period == 0: always-fresh answers from the server; fetch_period > 0:
+//     periodic fetch_cst into GPU-resident replicas (GDX1 blobs, cst.cpp:233-329)
 //   rollsim::SpeculationSource (engine.hpp:67-74, never implemented
 //                               in the reference)                    -> dgds_b200::GpuSpeculationSource
 //   SpeculationArgs / DraftCandidate / UpdateReply / DgdsParams / SpecQuery
@@ -13,8 +15,10 @@
 // Header-only; link against paper_2511_14617_b200/libdgds_b200.so.
 #pragma once
 
+#include <algorithm>
 #include <cstdint>
 #include <map>
+#include <memory>
 #include <span>
 #include <stdexcept>
 #include <string>
@@ -65,6 +69,19 @@ struct UpdateReply {  // dgds.hpp:39-43
   bool ok = false;
   std::uint64_t version = 0;
   std::uint64_t acked_tokens = 0;
+};
+
+struct DraftCacheInfo {  // dgds.hpp:26-29
+  std::string group_id;
+  std::uint64_t cached_version = 0;  // 0 = no local replica
+};
+
+enum class FetchKind : std::uint8_t { UpToDate = 0, Delta = 1, Full = 2, UnknownGroup = 3 };  // dgds.hpp:31
+
+struct FetchReply {  // dgds.hpp:33-37
+  FetchKind kind = FetchKind::UnknownGroup;
+  std::uint64_t version = 0;
+  std::vector<std::uint8_t> blob;
 };
 
 struct SpecQuery {  // dgds.hpp:118-122
@@ -188,6 +205,40 @@ class DraftServer {
     return out;
   }
 
+  // fetch_cst (dgds.cpp:53-97): UpToDate / Delta / Full / UnknownGroup per group.
+  std::vector<FetchReply> fetch_cst(std::span<const std::string> group_ids, std::span<const DraftCacheInfo> infos,
+                                    SimTime now) {
+    if (group_ids.size() != infos.size())
+      throw std::invalid_argument("fetch_cst: group_ids and draft_cache_infos must have equal length");
+    const std::size_t n = group_ids.size();
+    std::vector<FetchReply> out(n);
+    if (n == 0) return out;
+    std::vector<std::int32_t> hs(n);
+    std::vector<std::uint64_t> cv(n);
+    for (std::size_t i = 0; i < n; ++i) {
+      hs[i] = handle(group_ids[i]);
+      cv[i] = infos[i].cached_version;
+    }
+    std::vector<dgds_fetch_reply> r(n);
+    const std::uint8_t* blobs = nullptr;
+    detail::check(dgds_fetch_cst(s_, static_cast<int64_t>(n), hs.data(), cv.data(), now, r.data(), &blobs));
+    for (std::size_t i = 0; i < n; ++i) {
+      out[i].kind = static_cast<FetchKind>(r[i].kind);
+      out[i].version = r[i].version;
+      if (r[i].blob_len) out[i].blob.assign(blobs + r[i].blob_off, blobs + r[i].blob_off + r[i].blob_len);
+    }
+    return out;
+  }
+  void compact_group(const std::string& group_id, std::uint64_t before_version) {
+    detail::check(dgds_compact_group(s_, handle(group_id), before_version));
+  }
+  // GroupDraftIndex::apply_blob on this server's copy of the group (a replica); returns its version.
+  std::uint64_t apply_blob(const std::string& group_id, std::span<const std::uint8_t> blob, SimTime now = 0.0) {
+    std::uint64_t v = 0;
+    detail::check(dgds_apply_blob(s_, handle(group_id), blob.data(), blob.size(), now, &v));
+    return v;
+  }
+
   int shard_count() const { return params_.shard_count; }
   const DgdsParams& params() const { return params_; }
   bool has_group(const std::string& group_id) {
@@ -227,12 +278,24 @@ class DraftServer {
   std::unordered_map<std::string, std::int32_t> handles_;
 };
 
-// DraftClient in fresh mode (fetch_period 0): note_tokens batches appends per
-// (group, request) and flushes at append_batch_tokens (dgds.cpp:193-217);
-// batch_speculate answers from the always-fresh GPU server.
+// DraftClient (dgds.hpp:128-162, dgds.cpp:186-297). note_tokens batches appends per
+// (group, request) and flushes at append_batch_tokens with the resync rules of
+// push_stream (dgds.cpp:193-217).
+// - fetch_period == 0 (always fresh): batch_speculate first fetches the queried
+//   groups — lazy expiry and TTL refresh as the reference's fresh mode — and then
+//   answers from the server, which is what a just-synced replica would answer.
+// - fetch_period > 0: replicas of the active groups live in a GPU replica server,
+//   synced by fetch_active() with GDX1 delta/full blobs, and batch_speculate answers
+//   from them (stale between fetches, as in the paper's periodic fetch).
 class DraftClient {
  public:
-  DraftClient(DraftServer& server, DgdsParams params) : server_(server), params_(params) {}
+  DraftClient(DraftServer& server, DgdsParams params) : server_(server), params_(params) {
+    if (params_.fetch_period > 0.0) {
+      DgdsParams rp = params_;
+      rp.default_ttl_seconds = 1e300;  // replicas live until dropped or told UnknownGroup
+      replica_ = std::make_unique<DraftServer>(rp);
+    }
+  }
 
   void register_group(const std::string& group_id, double ttl_seconds, SimTime now) {
     server_.register_group(group_id, ttl_seconds, now);
@@ -248,8 +311,65 @@ class DraftClient {
     for (auto& [key, ps] : pending_)
       if (ps.acked < ps.buf.size()) push(key.first, key.second, ps, now);
   }
-  std::vector<std::vector<DraftCandidate>> batch_speculate(std::span<const SpecQuery> queries, SimTime) {
-    return server_.batch_speculate(queries);
+
+  void set_active_groups(std::vector<std::string> group_ids) {  // dgds.cpp:224-228
+    std::sort(group_ids.begin(), group_ids.end());
+    group_ids.erase(std::unique(group_ids.begin(), group_ids.end()), group_ids.end());
+    active_ = std::move(group_ids);
+  }
+  bool fetch_due(SimTime now) const {  // dgds.cpp:230-233
+    if (active_.empty()) return false;
+    return last_fetch_ < 0.0 || now - last_fetch_ >= params_.fetch_period;
+  }
+  void fetch_active(SimTime now) {  // dgds.cpp:265-268
+    fetch_groups(active_, now);
+    last_fetch_ = now;
+  }
+  void drop_replica(const std::string& group_id) {
+    cached_.erase(group_id);
+    if (replica_) replica_->drop_group(group_id);
+  }
+  std::uint64_t cached_version(const std::string& group_id) const {
+    auto it = cached_.find(group_id);
+    return it == cached_.end() ? 0 : it->second;
+  }
+
+  std::vector<std::vector<DraftCandidate>> batch_speculate(std::span<const SpecQuery> queries, SimTime now) {
+    std::vector<std::vector<DraftCandidate>> out(queries.size());
+    if (queries.empty()) return out;
+    if (!replica_) {  // fresh mode: sync (lazy expiry, TTL refresh), then the server answers
+      std::vector<std::string> ids;
+      for (const auto& q : queries) ids.push_back(q.group_id);
+      std::sort(ids.begin(), ids.end());
+      ids.erase(std::unique(ids.begin(), ids.end()), ids.end());
+      std::vector<DraftCacheInfo> infos;
+      for (const auto& g : ids) infos.push_back(DraftCacheInfo{g, server_.group_version(g)});
+      auto reps = server_.fetch_cst(ids, infos, now);
+      std::vector<SpecQuery> live;
+      std::vector<std::size_t> where;
+      for (std::size_t i = 0; i < queries.size(); ++i) {
+        const auto k = std::lower_bound(ids.begin(), ids.end(), queries[i].group_id) - ids.begin();
+        if (reps[k].kind == FetchKind::UnknownGroup) continue;  // no replica -> empty candidates
+        cached_[queries[i].group_id] = reps[k].version;
+        live.push_back(queries[i]);
+        where.push_back(i);
+      }
+      auto got = server_.batch_speculate(live);
+      for (std::size_t j = 0; j < where.size(); ++j) out[where[j]] = std::move(got[j]);
+      for (std::size_t k = 0; k < ids.size(); ++k)
+        if (reps[k].kind == FetchKind::UnknownGroup) cached_.erase(ids[k]);
+      return out;
+    }
+    std::vector<SpecQuery> have;
+    std::vector<std::size_t> where;
+    for (std::size_t i = 0; i < queries.size(); ++i) {
+      if (!cached_.count(queries[i].group_id)) continue;  // no replica -> empty candidates
+      have.push_back(queries[i]);
+      where.push_back(i);
+    }
+    auto got = replica_->batch_speculate(have);
+    for (std::size_t j = 0; j < where.size(); ++j) out[where[j]] = std::move(got[j]);
+    return out;
   }
 
  private:
@@ -257,6 +377,29 @@ class DraftClient {
     TokenSeq buf;
     std::uint64_t acked = 0;
   };
+  void fetch_groups(const std::vector<std::string>& ids, SimTime now) {  // dgds.cpp:235-263
+    if (ids.empty()) return;
+    std::vector<DraftCacheInfo> infos;
+    for (const auto& g : ids) infos.push_back(DraftCacheInfo{g, cached_version(g)});
+    auto reps = server_.fetch_cst(ids, infos, now);
+    for (std::size_t i = 0; i < ids.size(); ++i) {
+      FetchReply& r = reps[i];
+      switch (r.kind) {
+        case FetchKind::UpToDate:
+          break;
+        case FetchKind::UnknownGroup:
+          drop_replica(ids[i]);
+          break;
+        case FetchKind::Delta:
+          if (!cached_.count(ids[i])) throw std::runtime_error("delta for group without replica: " + ids[i]);
+          cached_[ids[i]] = replica_ ? replica_->apply_blob(ids[i], r.blob, now) : r.version;
+          break;
+        case FetchKind::Full:
+          cached_[ids[i]] = replica_ ? replica_->apply_blob(ids[i], r.blob, now) : r.version;
+          break;
+      }
+    }
+  }
   void push(const std::string& gid, int rid, Pending& ps, SimTime now) {  // push_stream, dgds.cpp:193-208
     while (ps.acked < ps.buf.size()) {
       std::span<const Token> chunk(ps.buf.data() + ps.acked, ps.buf.size() - ps.acked);
@@ -274,7 +417,11 @@ class DraftClient {
   }
   DraftServer& server_;
   DgdsParams params_;
+  std::unique_ptr<DraftServer> replica_;  // GPU-resident replicas (fetch_period > 0)
   std::map<std::pair<std::string, int>, Pending> pending_;
+  std::vector<std::string> active_;
+  SimTime last_fetch_ = -1.0;
+  std::map<std::string, std::uint64_t> cached_;
 };
 
 // The engine seam the reference declares but never implements (engine.hpp:67-74).

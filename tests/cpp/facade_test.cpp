@@ -2,6 +2,7 @@
 // rollout engine would use rollsim::DraftServer; answers pinned to SPEC.md.
 #include <cstdio>
 #include <stdexcept>
+#include <string>
 #include <vector>
 
 #include "dgds_b200.hpp"
@@ -40,8 +41,9 @@ int main() {
     threw = true;
   }
   EXPECT(threw);
-  // engine seam: SpeculationSource over a DraftClient (16-token flush)
+  // engine seam: SpeculationSource over an always-fresh DraftClient (16-token flush)
   DgdsParams p;
+  p.fetch_period = 0.0;
   DraftClient client(server, p);
   GpuSpeculationSource src(client);
   TokenSeq emitted;
@@ -52,6 +54,39 @@ int main() {
   auto res = src.batch(qs, 0.0);
   EXPECT(res.size() == 2 && res[1].empty() && res[0].size() == 1 && res[0][0].tokens == (TokenSeq{102, 103, 104, 100}));
   EXPECT(shard_of_group("g00000", 8) == shard_of_group("g00000", 8));
+
+  // replica sync: fetch_cst blobs restore a replica server; periodic client mode
+  std::vector<std::string> ids{"g1"};
+  std::vector<DraftCacheInfo> infos{{"g1", 0}};
+  auto f = server.fetch_cst(ids, infos, 0.0);
+  EXPECT(f.size() == 1 && f[0].kind == FetchKind::Full && f[0].version == 1 && f[0].blob.size() > 4);
+  DraftServer replica(DgdsParams{});
+  EXPECT(replica.apply_blob("g1", f[0].blob) == 1);
+  EXPECT(replica.speculate("g1", TokenSeq{2, 3}, SpeculationArgs{8, 6, 1, 1})[0].tokens == (TokenSeq{4, 5}));
+  infos[0].cached_version = 1;
+  EXPECT(server.fetch_cst(ids, infos, 0.0)[0].kind == FetchKind::UpToDate);
+
+  DgdsParams pp;  // fetch_period 0.2 (reference default): answers from GPU replicas, stale between fetches
+  DraftClient periodic(server, pp);
+  periodic.set_active_groups({"g3", "g2"});
+  EXPECT(periodic.fetch_due(0.0));
+  EXPECT(periodic.batch_speculate(qs, 0.0)[0].empty());  // no replica yet
+  periodic.fetch_active(0.0);
+  EXPECT(!periodic.fetch_due(0.1) && periodic.fetch_due(0.25));
+  EXPECT(periodic.cached_version("g3") == server.group_version("g3"));
+  auto pr = periodic.batch_speculate(qs, 0.1);
+  EXPECT(pr[0].size() == 1 && pr[0][0].tokens == (TokenSeq{102, 103, 104, 100}) && pr[1].empty());
+  TokenSeq more{100, 101, 7, 7, 7, 7, 7, 7, 7, 7, 7, 7, 7, 7, 7, 7};
+  server.update_cst("g3", 1, 0, more, 0.2);  // the server moves on; the replica is stale until fetched
+  auto stale = periodic.batch_speculate(qs, 0.2);
+  EXPECT(stale[0].size() == pr[0].size() && stale[0][0].tokens == pr[0][0].tokens &&
+         stale[0][0].score == pr[0][0].score);
+  periodic.fetch_active(0.3);  // delta
+  auto fresh = periodic.batch_speculate(qs, 0.3);
+  auto direct = server.speculate("g3", TokenSeq{100, 101}, SpeculationArgs{4, 6, 1, 1});
+  EXPECT(fresh[0].size() == direct.size() && fresh[0][0].tokens == direct[0].tokens &&
+         fresh[0][0].score == direct[0].score);
+  EXPECT(periodic.cached_version("g3") == server.group_version("g3"));
   std::printf("facade ok\n");
   return 0;
 }
