@@ -10,6 +10,7 @@
 // missing device is an error.
 
 #include <cuda_runtime.h>
+#include <deque>
 
 #include <algorithm>
 #include <cmath>
@@ -184,11 +185,6 @@ int host_threads() {
   return std::max(1, std::min(8, hc - 1));
 }
 
-struct HistChunk {  // tokens of one accepted append in the history arena
-  uint64_t off;
-  uint32_t len;
-};
-
 struct LogRec {  // GroupDraftIndex::LogEntry (cst.hpp:120-124) + where its tokens live
   uint64_t off;
   uint64_t start;
@@ -197,7 +193,6 @@ struct LogRec {  // GroupDraftIndex::LogEntry (cst.hpp:120-124) + where its toke
 };
 
 struct StreamRec {
-  std::vector<HistChunk> chunks;  // the stream's tokens, in order (full snapshots)
   uint64_t stored = 0;
   uint32_t slot = 0;
   int64_t batch_seg = -1;  // segment index in the batch being built
@@ -258,7 +253,11 @@ struct GroupRec {
   double expires = 0.0;
   uint64_t version = 0;
   StreamTable streams;
-  std::vector<LogRec> log;  // entries of versions log_floor+1 .. version (delta blobs)
+  // Every accepted append of the group, in order (a deque: grows without copying).
+  // Entries [delta_base, end) are versions log_floor+1 .. version (delta blobs);
+  // all entries together hold every stream's tokens (full snapshots).
+  std::deque<LogRec> log;
+  size_t delta_base = 0;
   uint64_t log_floor = 0;
 };
 
@@ -378,6 +377,7 @@ void retire_group(dgds_server* s, GroupRec& g) {
   g.streams.clear();
   g.log.clear();
   g.log.shrink_to_fit();
+  g.delta_base = 0;
   g.log_floor = 0;
   g.alive = false;
   g.version = 0;
@@ -394,6 +394,7 @@ int create_group(dgds_server* s, GroupRec& g, double ttl, double now) {
   g.version = 0;
   g.streams.clear();
   g.log.clear();
+  g.delta_base = 0;
   g.log_floor = 0;
   s->shard_counts[g.shard] += 1;
   return set_root(s, static_cast<int32_t>(&g - s->groups.data()), g.root);
@@ -596,7 +597,6 @@ int plan_updates(dgds_server* s, int64_t n, const int32_t* handles, const int32_
     s->hist_used += cnt;
     pend.push_back(PendingPiece{sr.batch_seg, tstart(i), hoff, static_cast<uint32_t>(cnt)});
     g.log.push_back(LogRec{hoff, sr.stored, static_cast<uint32_t>(cnt), rids[i]});
-    sr.chunks.push_back(HistChunk{hoff, static_cast<uint32_t>(cnt)});
     *worst += worst_windows(sr.stored, cnt, static_cast<uint64_t>(s->D));
     sr.stored += cnt;
     g.version += 1;
@@ -967,12 +967,14 @@ static int update_device_impl(dgds_server* s, int64_t n, const int32_t* handles,
                        dgds_update_reply* rep, void* stream) {
   if (n < 0) return fail(DGDS_EINVAL, "negative batch size");
   if (n == 0) return DGDS_OK;
+  PhaseClock pc("update_device");
   std::lock_guard<std::mutex> lk(s->mu);
   DGDS_CUDA(cudaSetDevice(s->p.device));
   std::vector<dgds::AppendSeg> segs;
   std::vector<dgds::AppendPiece> pieces;
   uint64_t worst = 0;
   if (int rc = plan_updates(s, n, handles, rids, prev, offs, counts, now, rep, segs, pieces, &worst)) return rc;
+  pc.mark("plan");
   if (segs.empty()) return DGDS_OK;
   if (int rc = ensure_capacity(s, worst)) return rc;
   if (int rc = ensure_hist(s)) return rc;
@@ -1753,7 +1755,7 @@ int dgds_fetch_cst(dgds_server* s, int64_t n, const int32_t* handles, const uint
     const uint64_t base = (total + 7) & ~7ull;
     uint64_t pos = base + blob_preamble_bytes(g.gid);
     if (delta) {
-      const size_t first = static_cast<size_t>(c - g.log_floor);
+      const size_t first = g.delta_base + static_cast<size_t>(c - g.log_floor);
       for (size_t k = first; k < g.log.size(); ++k) {
         const LogRec& e = g.log[k];
         pos += 16;
@@ -1762,22 +1764,26 @@ int dgds_fetch_cst(dgds_server* s, int64_t n, const int32_t* handles, const uint
       }
       pre.push_back(Pre{i, kBlobDelta, c, cur, static_cast<uint32_t>(g.log.size() - first)});
     } else {
-      std::vector<std::pair<int32_t, StreamRec*>> st;  // std::map order: request id ascending
-      g.streams.for_each([&](int32_t rid, StreamRec& sr) { st.emplace_back(rid, &sr); });
-      std::sort(st.begin(), st.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
-      for (auto& [rid, sr] : st) {
+      // std::map order: request id ascending; a stream's tokens are its log entries in order
+      std::vector<std::pair<int32_t, uint64_t>> st;  // (rid, stored)
+      g.streams.for_each([&](int32_t rid, StreamRec& sr) { st.emplace_back(rid, sr.stored); });
+      std::sort(st.begin(), st.end());
+      std::vector<uint32_t> order(g.log.size());
+      for (size_t k = 0; k < order.size(); ++k) order[k] = static_cast<uint32_t>(k);
+      std::stable_sort(order.begin(), order.end(),
+                       [&](uint32_t a, uint32_t b) { return g.log[a].rid < g.log[b].rid; });
+      size_t o = 0;
+      for (const auto& [rid, stored] : st) {
         pos += 12;
-        if (sr->chunks.empty()) {
-          pieces.push_back(dgds::BlobPiece{0, pos, 0, 0, static_cast<uint32_t>(rid), 2, 0});
-          continue;
-        }
+        while (o < order.size() && g.log[order[o]].rid < rid) ++o;  // (no stream without a record)
         bool first = true;
-        for (const HistChunk& ch : sr->chunks) {
-          pieces.push_back(dgds::BlobPiece{ch.off, pos, sr->stored, ch.len, static_cast<uint32_t>(rid),
-                                           first ? 2u : 0u, 0});
+        for (; o < order.size() && g.log[order[o]].rid == rid; ++o) {
+          const LogRec& e = g.log[order[o]];
+          pieces.push_back(dgds::BlobPiece{e.off, pos, stored, e.len, static_cast<uint32_t>(rid), first ? 2u : 0u, 0});
           first = false;
-          pos += 4ull * ch.len;
+          pos += 4ull * e.len;
         }
+        if (first) pieces.push_back(dgds::BlobPiece{0, pos, 0, 0, static_cast<uint32_t>(rid), 2, 0});  // empty stream
       }
       pre.push_back(Pre{i, kBlobFull, 0, cur, static_cast<uint32_t>(st.size())});
     }
@@ -1819,7 +1825,7 @@ int dgds_compact_group(dgds_server* s, int32_t h, uint64_t before_version) {  //
   if (!g.alive) return DGDS_OK;
   const uint64_t floor = std::min(before_version, g.version);
   if (floor <= g.log_floor) return DGDS_OK;
-  g.log.erase(g.log.begin(), g.log.begin() + static_cast<std::ptrdiff_t>(floor - g.log_floor));
+  g.delta_base += static_cast<size_t>(floor - g.log_floor);  // the entries stay: full snapshots need them
   g.log_floor = floor;
   return DGDS_OK;
 }
@@ -1913,7 +1919,7 @@ int dgds_apply_blob(dgds_server* s, int32_t h, const uint8_t* blob, uint64_t len
         return rc;
     }
     g.version = to;  // a restored replica owns no history older than the snapshot
-    g.log.clear();
+    g.delta_base = g.log.size();
     g.log_floor = to;
   } else {
     return fail(DGDS_EBLOB, "unknown draft blob kind");
