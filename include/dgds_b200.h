@@ -283,6 +283,19 @@ int dgds_speculate_records_seg(dgds_server* s, int32_t n_seg, int64_t seg_rows, 
                                int32_t max_spec, int32_t* const* seg_out, int32_t origin_field,
                                dgds_query_stats* d_stats, void* stream);
 
+/* The paper's zero-copy batch_speculate (Table 4; the reference SPEC does not
+ * keep it): an engine passes its own device buffers. Request i's pattern is the
+ * last d_pat_len[i] tokens ending (exclusive) at d_pattern_buffer[d_pat_end[i]], read in
+ * place; its reply record (layout reply fields: n_cands, lens[k], scores[k] f64,
+ * supports[k] i64, tokens[k][max_spec]) is written at d_output_buffer + d_out_offsets[i]
+ * (int32 units). No host copies; stream-ordered on `stream`. The engine verifies the drafts
+ * with its target model, so the layout's verify field is ignored. */
+int dgds_batch_speculate_zc(dgds_server* s, int64_t n, const int32_t* d_handles, const int64_t* d_pat_end,
+                            const int32_t* d_pat_len, const int32_t* d_pattern_buffer, const int64_t* d_out_offsets,
+                            int32_t* d_output_buffer, const dgds_query_record_layout* layout,
+                            const dgds_spec_args* d_args, int64_t args_stride, int32_t max_top_k, int32_t max_spec,
+                            dgds_query_stats* d_stats, void* stream);
+
 /* Verification of existing candidates (engine.cpp:115-143), host buffers. */
 int dgds_verify_batch(dgds_server* s, int64_t n, const dgds_candidates* cands, const int32_t* truth_next,
                       int32_t truth_stride, const int32_t* truth_left, const int32_t* limit,

@@ -172,6 +172,8 @@ EXPORTS = {
     "dgds_route_unpack": (C.c_int, [_I64, _P, _I32, _P, _P, _P]),
     "dgds_route_pack_padded": (C.c_int, [_I64, _I32, _P, _P, _I32, _I64, _P, _P, _P, _P]),
     "dgds_speculate_records": (C.c_int, [_P, _I64, _P, C.POINTER(RecordLayout), _P, _I64, _I32, _I32, _P, _P, _P]),
+    "dgds_batch_speculate_zc": (C.c_int, [_P, _I64, _P, _P, _P, _P, _P, _P, C.POINTER(RecordLayout), _P, _I64, _I32,
+                                          _I32, _P, _P]),
     "dgds_fetch_cst": (C.c_int, [_P, _I64, _P, _P, C.c_double, C.POINTER(FetchReply), C.POINTER(C.c_void_p)]),
     "dgds_compact_group": (C.c_int, [_P, _I32, _U64]),
     "dgds_apply_blob": (C.c_int, [_P, _I32, _P, _U64, C.c_double, C.POINTER(_U64)]),

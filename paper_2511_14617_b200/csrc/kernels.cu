@@ -419,7 +419,8 @@ __global__ void __launch_bounds__(kBlock, 4) k_query(QueryLaunch P) {
   const bool fast = start <= 8;
   const int row_len = min(plen, P.pat_stride);
   // row[0..start) = the last `start` pattern tokens; suffix j (length start-j) starts at row + j
-  const int32_t* row = P.patterns + qi * static_cast<int64_t>(P.pat_stride) + (row_len - start);
+  const int32_t* row = P.pat_end ? P.patterns + (P.pat_end[qi] - start)
+                                 : P.patterns + qi * static_cast<int64_t>(P.pat_stride) + (row_len - start);
   int32_t pr[8];
 #pragma unroll
   for (int i = 0; i < 8; ++i) pr[i] = (act && fast && i < start) ? row[i] : 0;
@@ -830,7 +831,7 @@ __global__ void __launch_bounds__(kBlock, 4) k_query(QueryLaunch P) {
       const int64_t row = P.seg_origin ? static_cast<int64_t>(P.seg_origin[q * P.in_qstride]) : q - sg * P.seg_rows;
       R = P.seg_out[sg] + row * P.rec_words_out;
     } else {
-      R = P.rec_out + q * P.rec_words_out;
+      R = P.rec_out + (P.out_off ? P.out_off[q] : q * P.rec_words_out);
     }
     if (P.off_nc >= 0) {
       o_nc = R + P.off_nc;

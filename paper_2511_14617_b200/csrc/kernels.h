@@ -102,6 +102,10 @@ struct QueryLaunch {
   int64_t seg_rows;
   const int32_t* seg_count;
   const int32_t* seg_origin;  // optional: the reply row is seg_origin[q * in_qstride] instead of j
+  // Engine zero-copy: the pattern of query q ends at patterns[pat_end[q]] (exclusive)
+  // in one long token buffer, and its reply record starts at rec_out + out_off[q].
+  const int64_t* pat_end;
+  const int64_t* out_off;
   int32_t* seg_out[kMaxSegments];
 };
 

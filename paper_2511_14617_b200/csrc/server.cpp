@@ -1929,3 +1929,60 @@ int dgds_apply_blob(dgds_server* s, int32_t h, const uint8_t* blob, uint64_t len
 }
 
 }  // extern "C"
+
+extern "C" {
+
+int dgds_batch_speculate_zc(dgds_server* s, int64_t n, const int32_t* d_handles, const int64_t* d_pat_end,
+                            const int32_t* d_pat_len, const int32_t* d_pattern_buffer, const int64_t* d_out_offsets,
+                            int32_t* d_output_buffer, const dgds_query_record_layout* lay,
+                            const dgds_spec_args* d_args, int64_t args_stride, int32_t max_top_k, int32_t max_spec,
+                            dgds_query_stats* d_stats, void* stream) {
+  if (!s || n < 0) return fail(DGDS_EINVAL, "bad batch");
+  if (n == 0) return DGDS_OK;
+  if (!d_handles || !d_pat_end || !d_pat_len || !d_pattern_buffer || !d_out_offsets || !d_output_buffer || !lay ||
+      !d_args)
+    return fail(DGDS_EINVAL, "null argument");
+  if (max_top_k < 1 || max_top_k > DGDS_MAX_TOP_K) return fail(DGDS_EUNSUPPORTED, "max_top_k out of range");
+  if (max_spec <= 0 || max_spec > s->p.max_spec_len) max_spec = std::max(1, s->p.max_spec_len);
+  const dgds_query_record_layout& y = *lay;
+  if (y.reply_words < 1 || (y.off_scores & 1) || (y.off_supports & 1))
+    return fail(DGDS_EINVAL, "bad reply layout (8-byte fields must be even)");
+  std::lock_guard<std::mutex> lk(s->mu);
+  DGDS_CUDA(cudaSetDevice(s->p.device));
+  StreamJoin join(s, stream);
+  dgds::QueryLaunch L{};
+  L.T = s->T;
+  L.root_of = s->d_root_of;
+  L.n_handles = static_cast<int32_t>(s->root_of_cap);
+  L.n = n;
+  L.handles = d_handles;
+  L.pat_len = d_pat_len;
+  L.patterns = d_pattern_buffer;
+  L.pat_end = d_pat_end;
+  L.pat_stride = 0x7FFFFFFF;  // the pattern is read in place: no row clamp
+  L.in_qstride = 1;
+  L.args = d_args;
+  L.args_stride = args_stride;
+  L.k_stride = max_top_k;
+  L.s_stride = max_spec;
+  L.rec_words_out = y.reply_words;
+  L.rec_out = d_output_buffer;
+  L.out_off = d_out_offsets;
+  L.off_nc = y.off_n_cands;
+  L.off_len = y.off_lens;
+  L.off_sc = y.off_scores;
+  L.off_sp = y.off_supports;
+  L.off_tk = y.off_tokens;
+  L.off_v = -1;  // the engine verifies with the target model
+  L.stats = d_stats;
+  L.err_flag = s->d_err;
+  L.stat_part = s->d_stat_part;
+  L.dbg = s->d_dbg;
+  {
+    LaunchTimer lt(s, 1, join.stream());
+    DGDS_CUDA(dgds::launch_query(L, max_top_k, max_spec, join.stream()));
+  }
+  return DGDS_OK;
+}
+
+}  // extern "C"

@@ -210,6 +210,18 @@ class DraftServer:
         check(lib().dgds_node_count(self._h, C.byref(out)))
         return int(out.value)
 
+    def batch_speculate_zc(self, d_handles, d_pat_end, d_pat_len, d_pattern_buffer, d_out_offsets,
+                           d_output_buffer, layout, d_args, args_stride: int, max_top_k: int, max_spec: int,
+                           d_stats=None, stream: int = 0) -> None:
+        """The paper's zero-copy batch_speculate: device tensors in, reply records
+        written into the engine's output buffer at d_out_offsets (dgds_batch_speculate_zc)."""
+        p = lambda t: C.c_void_p(t.data_ptr())  # noqa: E731
+        check(lib().dgds_batch_speculate_zc(self._h, int(d_handles.shape[0]), p(d_handles), p(d_pat_end),
+                                            p(d_pat_len), p(d_pattern_buffer), p(d_out_offsets), p(d_output_buffer),
+                                            C.byref(layout), p(d_args), args_stride, max_top_k, max_spec,
+                                            p(d_stats) if d_stats is not None else None,
+                                            C.c_void_p(stream or None)))
+
     # ---- replica sync (GDX1 blobs, cst.cpp:233-329; fetch_cst, dgds.cpp:53-97) ----
     def fetch_cst(self, group_ids: Sequence[str], cached_versions: Sequence[int], now: float) -> List[FetchReply]:
         """DraftServer::fetch_cst: per group UpToDate / Delta / Full / UnknownGroup with the
