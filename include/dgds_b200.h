@@ -387,6 +387,22 @@ int dgds_compact_group(dgds_server* s, int32_t handle, uint64_t before_version);
 int dgds_apply_blob(dgds_server* s, int32_t handle, const uint8_t* blob, uint64_t len, double now,
                     uint64_t* version);
 
+/* ---- framed wire protocol (dgds_wire.hpp:12-28, dgds_wire.cpp) ----
+ * Frame = u32 BE length + payload; ops 0x01 update_cst, 0x02 fetch_cst, 0x03 register_group,
+ * replies op|0x80, 0x7F error + message; replies byte-identical to the reference's
+ * serve_payload. The TCP service (loopback, thread per connection like TcpDraftService)
+ * hands frames to one dispatcher that applies every waiting update_cst as ONE batch. */
+typedef struct dgds_wire_service dgds_wire_service;
+/* update_cst's steps before the append (dgds.cpp:39-48): auto-register or refresh the expiry. */
+int dgds_touch_group(dgds_server* s, int32_t handle, double now);
+/* One request payload -> reply payload (DGDS_EBUFFER with *out_len set if cap is too small). */
+int dgds_wire_serve_payload(dgds_server* s, const uint8_t* payload, uint64_t len, double now, uint8_t* out,
+                            uint64_t cap, uint64_t* out_len);
+/* port 0 = ephemeral; TTLs use the service's own clock (seconds since start). */
+int dgds_wire_service_start(dgds_server* s, int32_t port, dgds_wire_service** out, int32_t* bound_port);
+int dgds_wire_service_stats(dgds_wire_service* w, uint64_t* requests, uint64_t* batches);
+int dgds_wire_service_stop(dgds_wire_service* w);
+
 /* ---- peer exchange over NVLink / NVSwitch (one process per GPU, CUDA IPC) ----
  * Replaces the all-to-all of the reference's shard routing (dgds.cpp:10-14 routes a
  * group's traffic to shard fnv1a64(gid) % N) with stores straight into the owner's HBM.

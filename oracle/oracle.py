@@ -274,6 +274,21 @@ class RefLib(_Lib):
                                             C.POINTER(C.c_uint64)]
         L.orc_index_apply_blob.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64, C.POINTER(C.c_uint64)]
         L.orc_index_compact.argtypes = [C.c_void_p, C.c_uint64]
+        L.orc_ref_wire_serve.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64, C.c_double, C.c_void_p, C.c_uint64,
+                                         C.POINTER(C.c_uint64)]
+        L.orc_ref_tcp_new.restype = C.c_void_p
+        L.orc_ref_tcp_new.argtypes = [C.c_char_p, C.c_int32]
+        L.orc_ref_tcp_free.argtypes = [C.c_void_p]
+        L.orc_ref_tcp_update.argtypes = [C.c_void_p, C.c_char_p, C.c_int32, C.c_uint64, C.POINTER(C.c_int32),
+                                         C.c_uint64, C.POINTER(C.c_int32), C.POINTER(C.c_uint64),
+                                         C.POINTER(C.c_uint64)]
+        L.orc_ref_tcp_fetch.argtypes = [C.c_void_p, C.c_char_p, C.c_uint64, C.POINTER(C.c_int32),
+                                        C.POINTER(C.c_uint64), C.c_void_p, C.c_uint64, C.POINTER(C.c_uint64)]
+        L.orc_ref_tcp_register.argtypes = [C.c_void_p, C.c_char_p, C.c_double]
+        L.orc_ref_service_new.restype = C.c_void_p
+        L.orc_ref_service_new.argtypes = [C.c_int32]
+        L.orc_ref_service_port.argtypes = [C.c_void_p]
+        L.orc_ref_service_free.argtypes = [C.c_void_p]
         L.orc_ref_workload_new.restype = C.c_void_p
         L.orc_ref_workload_new.argtypes = [C.POINTER(OrcWcfg)]
         L.orc_ref_workload_free.argtypes = [C.c_void_p]
@@ -316,6 +331,11 @@ class RefLib(_Lib):
         blob = self._blob_call(lambda b, c, l: self.L.orc_ref_server_fetch(srv, gid.encode(), cached, now,
                                                                            C.byref(kind), C.byref(ver), b, c, l))
         return int(kind.value), int(ver.value), blob
+
+    def wire_serve(self, srv, payload: bytes, now: float) -> bytes:
+        """wire::serve_payload (dgds_wire.cpp:103-143)."""
+        buf = C.create_string_buffer(bytes(payload), max(1, len(payload)))
+        return self._blob_call(lambda b, c, l: self.L.orc_ref_wire_serve(srv, buf, len(payload), now, b, c, l))
 
     def server_compact(self, srv, gid: str, before: int):
         if self.L.orc_ref_server_compact(srv, gid.encode(), before) != 0:

@@ -24,6 +24,7 @@
 #include "rollsim/detail/bytes.hpp"
 #include "rollsim/detail/rng.hpp"
 #include "rollsim/dgds.hpp"
+#include "rollsim/dgds_wire.hpp"
 #include "rollsim/engine.hpp"
 #include "rollsim/kvpool.hpp"
 #include "rollsim/workload.hpp"
@@ -289,6 +290,73 @@ int orc_index_compact(void* idx, uint64_t before) {
     return 0;
   });
 }
+
+// ---------------------------------------------------------------------------
+// framed wire protocol (dgds_wire.cpp): serve_payload, the TcpTransport client and
+// the TcpDraftService, to check our service and client against the reference.
+
+int orc_ref_wire_serve(void* s, const uint8_t* payload, uint64_t len, double now, uint8_t* out, uint64_t cap,
+                       uint64_t* out_len) {
+  return guarded([&] {
+    auto r = wire::serve_payload(*static_cast<DraftServer*>(s), std::span<const std::uint8_t>(payload, len), now);
+    return copy_blob(r, out, cap, out_len);
+  });
+}
+
+void* orc_ref_tcp_new(const char* host, int32_t port) {
+  try {
+    return new wire::TcpTransport(host, port);
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return nullptr;
+  }
+}
+
+void orc_ref_tcp_free(void* t) { delete static_cast<wire::TcpTransport*>(t); }
+
+int orc_ref_tcp_update(void* t, const char* gid, int32_t rid, uint64_t prev, const int32_t* toks, uint64_t n,
+                       int32_t* ok, uint64_t* version, uint64_t* acked) {
+  return guarded([&] {
+    auto r = static_cast<wire::TcpTransport*>(t)->update_cst(gid, rid, prev, std::span<const Token>(toks, n), 0.0);
+    *ok = r.ok ? 1 : 0;
+    *version = r.version;
+    *acked = r.acked_tokens;
+    return 0;
+  });
+}
+
+int orc_ref_tcp_fetch(void* t, const char* gid, uint64_t cached, int32_t* kind, uint64_t* version, uint8_t* buf,
+                      uint64_t cap, uint64_t* len) {
+  return guarded([&] {
+    std::string id(gid);
+    DraftCacheInfo info{id, cached};
+    auto r = static_cast<wire::TcpTransport*>(t)->fetch_cst(std::span<const std::string>(&id, 1),
+                                                            std::span<const DraftCacheInfo>(&info, 1), 0.0);
+    *kind = static_cast<int32_t>(r[0].kind);
+    *version = r[0].version;
+    return copy_blob(r[0].blob, buf, cap, len);
+  });
+}
+
+int orc_ref_tcp_register(void* t, const char* gid, double ttl) {
+  return guarded([&] {
+    static_cast<wire::TcpTransport*>(t)->register_group(gid, ttl, 0.0);
+    return 0;
+  });
+}
+
+void* orc_ref_service_new(int32_t port) {
+  try {
+    return new wire::TcpDraftService(DgdsParams{}, port);
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return nullptr;
+  }
+}
+
+int32_t orc_ref_service_port(void* sv) { return static_cast<wire::TcpDraftService*>(sv)->port(); }
+
+void orc_ref_service_free(void* sv) { delete static_cast<wire::TcpDraftService*>(sv); }
 
 // ---------------------------------------------------------------------------
 // generate_workload (workload.cpp:51-103)

@@ -174,6 +174,11 @@ EXPORTS = {
     "dgds_speculate_records": (C.c_int, [_P, _I64, _P, C.POINTER(RecordLayout), _P, _I64, _I32, _I32, _P, _P, _P]),
     "dgds_batch_speculate_zc": (C.c_int, [_P, _I64, _P, _P, _P, _P, _P, _P, C.POINTER(RecordLayout), _P, _I64, _I32,
                                           _I32, _P, _P]),
+    "dgds_touch_group": (C.c_int, [_P, _I32, C.c_double]),
+    "dgds_wire_serve_payload": (C.c_int, [_P, _P, _U64, C.c_double, _P, _U64, C.POINTER(_U64)]),
+    "dgds_wire_service_start": (C.c_int, [_P, _I32, C.POINTER(C.c_void_p), C.POINTER(_I32)]),
+    "dgds_wire_service_stats": (C.c_int, [_P, C.POINTER(_U64), C.POINTER(_U64)]),
+    "dgds_wire_service_stop": (C.c_int, [_P]),
     "dgds_fetch_cst": (C.c_int, [_P, _I64, _P, _P, C.c_double, C.POINTER(FetchReply), C.POINTER(C.c_void_p)]),
     "dgds_compact_group": (C.c_int, [_P, _I32, _U64]),
     "dgds_apply_blob": (C.c_int, [_P, _I32, _P, _U64, C.c_double, C.POINTER(_U64)]),

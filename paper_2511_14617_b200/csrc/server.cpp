@@ -1986,3 +1986,14 @@ int dgds_batch_speculate_zc(dgds_server* s, int64_t n, const int32_t* d_handles,
 }
 
 }  // extern "C"
+
+extern "C" int dgds_touch_group(dgds_server* s, int32_t h, double now) {  // update_cst before append (dgds.cpp:39-48)
+  if (!s) return fail(DGDS_EINVAL, "null server");
+  std::lock_guard<std::mutex> lk(s->mu);
+  if (int rc = check_handle(s, h)) return rc;
+  GroupRec& g = s->groups[h];
+  if (!live_entry(s, g, now))
+    if (int rc = create_group(s, g, s->p.default_ttl_seconds, now)) return rc;
+  g.expires = now + g.ttl;
+  return DGDS_OK;
+}
