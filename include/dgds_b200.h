@@ -387,6 +387,18 @@ int dgds_compact_group(dgds_server* s, int32_t handle, uint64_t before_version);
 int dgds_apply_blob(dgds_server* s, int32_t handle, const uint8_t* blob, uint64_t len, double now,
                     uint64_t* version);
 
+/* ---- memory reclamation (TTL expiry / drop) ----
+ * Retired groups' trie slots are dropped by a same-capacity rebuild and their token history
+ * by a compaction of the history arena. dgds_drop_group / dgds_sweep_expired run it once
+ * retired groups hold > 40% of the history; dgds_compact_memory runs it now. */
+typedef struct dgds_memory_stats {
+  uint64_t slots, used_slots;
+  uint64_t history_capacity, history_tokens, dead_history_tokens;
+  uint64_t compactions;
+} dgds_memory_stats;
+int dgds_compact_memory(dgds_server* s);
+int dgds_get_memory_stats(dgds_server* s, dgds_memory_stats* out);
+
 /* ---- framed wire protocol (dgds_wire.hpp:12-28, dgds_wire.cpp) ----
  * Frame = u32 BE length + payload; ops 0x01 update_cst, 0x02 fetch_cst, 0x03 register_group,
  * replies op|0x80, 0x7F error + message; replies byte-identical to the reference's

@@ -80,6 +80,11 @@ class FetchReply(C.Structure):
                 ("blob_len", C.c_uint64)]
 
 
+class MemoryStats(C.Structure):
+    _fields_ = [("slots", C.c_uint64), ("used_slots", C.c_uint64), ("history_capacity", C.c_uint64),
+                ("history_tokens", C.c_uint64), ("dead_history_tokens", C.c_uint64), ("compactions", C.c_uint64)]
+
+
 class QueryStats(C.Structure):
     _fields_ = [
         ("queries", C.c_uint64),
@@ -174,6 +179,8 @@ EXPORTS = {
     "dgds_speculate_records": (C.c_int, [_P, _I64, _P, C.POINTER(RecordLayout), _P, _I64, _I32, _I32, _P, _P, _P]),
     "dgds_batch_speculate_zc": (C.c_int, [_P, _I64, _P, _P, _P, _P, _P, _P, C.POINTER(RecordLayout), _P, _I64, _I32,
                                           _I32, _P, _P]),
+    "dgds_compact_memory": (C.c_int, [_P]),
+    "dgds_get_memory_stats": (C.c_int, [_P, C.POINTER(MemoryStats)]),
     "dgds_touch_group": (C.c_int, [_P, _I32, C.c_double]),
     "dgds_wire_serve_payload": (C.c_int, [_P, _P, _U64, C.c_double, _P, _U64, C.POINTER(_U64)]),
     "dgds_wire_service_start": (C.c_int, [_P, _I32, C.POINTER(C.c_void_p), C.POINTER(_I32)]),

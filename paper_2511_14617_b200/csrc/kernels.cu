@@ -1216,6 +1216,23 @@ cudaError_t launch_verify(int64_t n, int32_t k_stride, int32_t s_stride, const i
   return cudaGetLastError();
 }
 
+__global__ void k_copy_pieces(const CopyPiece* __restrict__ pieces, int64_t n, const int32_t* __restrict__ from,
+                              int32_t* to) {
+  const int lane = lane_id();
+  const int64_t nw = static_cast<int64_t>(gridDim.x) * (blockDim.x / kWarp);
+  for (int64_t w = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / kWarp; w < n; w += nw) {
+    const CopyPiece pc = pieces[w];
+    for (uint32_t i = lane; i < pc.len; i += kWarp) to[pc.dst + i] = from[pc.src + i];
+  }
+}
+
+cudaError_t launch_copy_pieces(const CopyPiece* d_pieces, int64_t n, const int32_t* from, int32_t* to, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  const int64_t blocks = std::min<int64_t>((n + 7) / 8, 148 * 8);
+  k_copy_pieces<<<static_cast<unsigned>(blocks), 256, 0, st>>>(d_pieces, n, from, to);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_blob_fill(const BlobPiece* d_pieces, int64_t n, const int32_t* hist, uint8_t* out,
                              cudaStream_t st) {
   if (n <= 0) return cudaSuccess;

@@ -43,6 +43,11 @@ struct BlobPiece {
   uint32_t hdr_kind;
   uint32_t pad_;
 };
+struct CopyPiece {  // history compaction: len tokens from src to dst
+  uint64_t src, dst;
+  uint32_t len, pad_;
+};
+cudaError_t launch_copy_pieces(const CopyPiece* d_pieces, int64_t n, const int32_t* from, int32_t* to, cudaStream_t st);
 cudaError_t launch_blob_fill(const BlobPiece* d_pieces, int64_t n, const int32_t* hist, uint8_t* out,
                              cudaStream_t st);
 

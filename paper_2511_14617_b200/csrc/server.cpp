@@ -280,6 +280,8 @@ struct dgds_server {
 
   int32_t* d_hist = nullptr;  // append-only token history (GDX1 blobs); K1 fills it
   uint64_t hist_cap = 0, hist_used = 0;
+  uint64_t dead_hist_tokens = 0;  // history of retired groups (reclaimed by compact_memory)
+  uint64_t compactions = 0;
   DevBuf d_blob, d_blob_pieces;
   PinnedBuf h_blob;
 
@@ -373,6 +375,7 @@ int alloc_stream_slot(dgds_server* s, uint32_t* out) {
 
 void retire_group(dgds_server* s, GroupRec& g) {
   if (!g.alive) return;
+  for (const LogRec& e : g.log) s->dead_hist_tokens += e.len;
   g.streams.for_each([&](int32_t, StreamRec& r) { s->free_streams.push_back(r.slot); });
   g.streams.clear();
   g.log.clear();
@@ -837,12 +840,18 @@ int dgds_register_group(dgds_server* s, int32_t h, double ttl, double now) {  //
   return DGDS_OK;
 }
 
+}  // extern "C"
+namespace {
+int maybe_compact(dgds_server* s);  // memory reclamation, below
+}  // namespace
+extern "C" {
+
 int dgds_drop_group(dgds_server* s, int32_t h) {  // dgds.cpp:112-116
   std::lock_guard<std::mutex> lk(s->mu);
   if (int rc = check_handle(s, h)) return rc;
   cudaSetDevice(s->p.device);
   retire_group(s, s->groups[h]);
-  return DGDS_OK;
+  return maybe_compact(s);
 }
 
 int dgds_sweep_expired(dgds_server* s, double now) {  // dgds.cpp:118-128
@@ -850,7 +859,7 @@ int dgds_sweep_expired(dgds_server* s, double now) {  // dgds.cpp:118-128
   cudaSetDevice(s->p.device);
   for (auto& g : s->groups)
     if (g.alive && g.expires < now) retire_group(s, g);
-  return DGDS_OK;
+  return maybe_compact(s);
 }
 
 int dgds_has_group(dgds_server* s, int32_t h, int32_t* out) {
@@ -1997,3 +2006,84 @@ extern "C" int dgds_touch_group(dgds_server* s, int32_t h, double now) {  // upd
   g.expires = now + g.ttl;
   return DGDS_OK;
 }
+
+// ---------------------------------------------------------------------------
+// Memory reclamation: a same-capacity rebuild drops the
+// slots of retired groups (rebuild keeps live roots only), and the history arena is
+// compacted to the live groups' tokens by a gather kernel.
+
+namespace {
+
+int compact_history(dgds_server* s) {
+  std::vector<dgds::CopyPiece> pcs;
+  uint64_t live = 0;
+  for (auto& g : s->groups) {
+    if (!g.alive) continue;
+    for (LogRec& e : g.log) {
+      pcs.push_back(dgds::CopyPiece{e.off, live, e.len, 0});
+      e.off = live;
+      live += e.len;
+    }
+  }
+  const uint64_t cap = std::max<uint64_t>(1ull << 20, live + live / 2);
+  int32_t* nb = nullptr;
+  if (cudaMalloc(&nb, cap * sizeof(int32_t)) != cudaSuccess) return fail(DGDS_ENOMEM, "history arena allocation failed");
+  if (!pcs.empty()) {
+    if (int rc = s->d_blob_pieces.ensure(pcs.size() * sizeof(dgds::CopyPiece))) return rc;
+    DGDS_CUDA(cudaMemcpyAsync(s->d_blob_pieces.p, pcs.data(), pcs.size() * sizeof(dgds::CopyPiece),
+                              cudaMemcpyHostToDevice, s->st));
+    DGDS_CUDA(dgds::launch_copy_pieces(static_cast<const dgds::CopyPiece*>(s->d_blob_pieces.p),
+                                       static_cast<int64_t>(pcs.size()), s->d_hist, nb, s->st));
+  }
+  DGDS_CUDA(cudaStreamSynchronize(s->st));
+  cudaFree(s->d_hist);
+  s->d_hist = nb;
+  s->T.hist = nb;
+  s->hist_cap = cap;
+  s->hist_used = live;
+  s->dead_hist_tokens = 0;
+  return DGDS_OK;
+}
+
+int compact_memory(dgds_server* s) {
+  DGDS_CUDA(cudaStreamSynchronize(s->st));
+  if (int rc = rebuild(s, s->T.cap)) return rc;
+  if (int rc = compact_history(s)) return rc;
+  s->compactions += 1;
+  return DGDS_OK;
+}
+
+// after explicit retirements: compact once retired groups hold > 40% of the history
+int maybe_compact(dgds_server* s) {
+  if (s->dead_hist_tokens < (1ull << 12) || s->dead_hist_tokens * 10 < s->hist_used * 4) return DGDS_OK;
+  return compact_memory(s);
+}
+
+}  // namespace
+
+extern "C" {
+
+int dgds_compact_memory(dgds_server* s) {
+  if (!s) return fail(DGDS_EINVAL, "null server");
+  std::lock_guard<std::mutex> lk(s->mu);
+  DGDS_CUDA(cudaSetDevice(s->p.device));
+  return compact_memory(s);
+}
+
+int dgds_get_memory_stats(dgds_server* s, dgds_memory_stats* out) {
+  if (!s || !out) return fail(DGDS_EINVAL, "null argument");
+  std::lock_guard<std::mutex> lk(s->mu);
+  DGDS_CUDA(cudaSetDevice(s->p.device));
+  uint64_t used = 0;
+  if (int rc = read_used(s, &used)) return rc;
+  s->used_ub = used;
+  out->slots = s->T.cap;
+  out->used_slots = used;
+  out->history_capacity = s->hist_cap;
+  out->history_tokens = s->hist_used;
+  out->dead_history_tokens = s->dead_hist_tokens;
+  out->compactions = s->compactions;
+  return DGDS_OK;
+}
+
+}  // extern "C"

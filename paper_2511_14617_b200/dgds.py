@@ -252,6 +252,15 @@ class DraftServer:
         check(lib().dgds_apply_blob(self._h, self.group_handle(group_id), buf, len(blob), float(now), C.byref(v)))
         return int(v.value)
 
+    def compact_memory(self):
+        """Reclaim retired groups' slots (same-capacity rebuild) and history (dgds_compact_memory)."""
+        check(lib().dgds_compact_memory(self._h))
+
+    def memory_stats(self) -> dict:
+        m = _lib.MemoryStats()
+        check(lib().dgds_get_memory_stats(self._h, C.byref(m)))
+        return {k: int(getattr(m, k)) for k, _ in m._fields_}
+
     def index_slots(self) -> int:
         out = C.c_uint64()
         check(lib().dgds_index_slots(self._h, C.byref(out)))
