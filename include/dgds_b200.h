@@ -314,6 +314,8 @@ typedef struct dgds_profile {
 } dgds_profile;
 int dgds_profile_enable(dgds_server* s, int32_t on);
 /* Debug: record per-query phase cycles of later device-API query launches into d_buf[n][8] (NULL = off). */
+/* Debug (DGDS_APPEND_DBG set at create): per-warp [start, end] globaltimer ns of the last K1 launch. */
+int dgds_debug_append_timing(dgds_server* s, uint64_t* out, int64_t n_warps);
 int dgds_debug_query_timing(dgds_server* s, void* d_buf);
 /* Device->host bytes moved by the last host-buffer query call (results are compacted on device). */
 int dgds_last_transfer(dgds_server* s, uint64_t* d2h_bytes);

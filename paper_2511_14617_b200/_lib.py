@@ -179,6 +179,7 @@ EXPORTS = {
     "dgds_speculate_records": (C.c_int, [_P, _I64, _P, C.POINTER(RecordLayout), _P, _I64, _I32, _I32, _P, _P, _P]),
     "dgds_batch_speculate_zc": (C.c_int, [_P, _I64, _P, _P, _P, _P, _P, _P, C.POINTER(RecordLayout), _P, _I64, _I32,
                                           _I32, _P, _P]),
+    "dgds_debug_append_timing": (C.c_int, [_P, _P, _I64]),
     "dgds_compact_memory": (C.c_int, [_P]),
     "dgds_get_memory_stats": (C.c_int, [_P, C.POINTER(MemoryStats)]),
     "dgds_touch_group": (C.c_int, [_P, _I32, C.c_double]),

@@ -27,6 +27,12 @@ namespace {
 
 constexpr unsigned kFull = 0xFFFFFFFFu;
 constexpr int kBlock = 256;
+#ifndef DGDS_APPEND_OCC
+#define DGDS_APPEND_OCC 4  // resident blocks per SM the register budget is sized for
+#endif
+#ifndef DGDS_QUERY_OCC
+#define DGDS_QUERY_OCC 4
+#endif
 constexpr int kWarpsPerBlock = kBlock / kWarp;
 
 __device__ __forceinline__ int lane_id() { return threadIdx.x & (kWarp - 1); }
@@ -136,7 +142,7 @@ __device__ __forceinline__ void claim_cas(const DevTrie& T, unsigned long long h
   }
 }
 
-__global__ void __launch_bounds__(kBlock, 4) k_append(DevTrie T, const AppendSeg* __restrict__ segs, int64_t nseg,
+__global__ void __launch_bounds__(kBlock, DGDS_APPEND_OCC) k_append(DevTrie T, const AppendSeg* __restrict__ segs, int64_t nseg,
                                                    const AppendPiece* __restrict__ pieces,
                                                    const int32_t* __restrict__ tokens) {
   const int lane = lane_id();
@@ -149,6 +155,8 @@ __global__ void __launch_bounds__(kBlock, 4) k_append(DevTrie T, const AppendSeg
   __shared__ int32_t stage[kWarpsPerBlock][kStage];
   int32_t* stage_w = stage[threadIdx.x / kWarp];
 
+  unsigned long long t_start = 0;
+  if (T.dbg) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
   for (int64_t sg = warp; sg < nseg; sg += nwarps) {
     const AppendSeg g = segs[sg];
     const uint64_t len0 = g.start;
@@ -247,6 +255,12 @@ __global__ void __launch_bounds__(kBlock, 4) k_append(DevTrie T, const AppendSeg
     }
     if (link_pending) store_link(T.slots + link_slot, link_prev, g.root);
     if (lane < D && static_cast<uint64_t>(lane) < len) act_row[lane] = a;
+  }
+  if (T.dbg && lane == 0 && warp < 65536) {
+    unsigned long long t_end;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+    T.dbg[2 * warp] = t_start;
+    T.dbg[2 * warp + 1] = t_end;
   }
   // one RED per warp into a partition of the occupancy counter (no block barrier)
   const unsigned long long ins_warp = __reduce_add_sync(kFull, static_cast<unsigned>(inserted_total));
@@ -377,7 +391,7 @@ __device__ __forceinline__ uint32_t resolve_content(const DevTrie& T, unsigned l
 }
 
 template <int G, int S>
-__global__ void __launch_bounds__(kBlock, 4) k_query(QueryLaunch P) {
+__global__ void __launch_bounds__(kBlock, DGDS_QUERY_OCC) k_query(QueryLaunch P) {
   constexpr int kTiles = kBlock / G;
   __shared__ GroupScratch<G, S> scratch[kTiles];
   const int lane = lane_id();

@@ -756,6 +756,11 @@ int dgds_create(const dgds_params* params, dgds_server** out) {
   s->T.lim_spec = p.max_spec_len;
   s->T.ahead = 0;  // the bulk L2 prefetch measured slower than the register preload alone
   if (const char* e = std::getenv("DGDS_PREFETCH_AHEAD")) s->T.ahead = std::max(0, std::atoi(e));
+  s->T.dbg = nullptr;
+  if (std::getenv("DGDS_APPEND_DBG")) {  // debug: per-warp K1 timing, read with dgds_debug_append_timing
+    DGDS_CUDA(cudaMalloc(&s->T.dbg, 65536 * 2 * sizeof(unsigned long long)));
+    DGDS_CUDA(cudaMemset(s->T.dbg, 0, 65536 * 2 * sizeof(unsigned long long)));
+  }
   s->T.claim_cas = 1;  // CAS-first claim (measured faster: fewer random accesses per insert)
   if (const char* e = std::getenv("DGDS_CLAIM")) s->T.claim_cas = std::strcmp(e, "load") == 0 ? 0 : 1;
   DGDS_CUDA(cudaMalloc(&s->T.slots, cap * sizeof(dgds::Slot)));
@@ -2087,3 +2092,12 @@ int dgds_get_memory_stats(dgds_server* s, dgds_memory_stats* out) {
 }
 
 }  // extern "C"
+
+extern "C" int dgds_debug_append_timing(dgds_server* s, uint64_t* out, int64_t n_warps) {  // [n][2] start, end (ns)
+  if (!s || !out) return fail(DGDS_EINVAL, "null argument");
+  if (!s->T.dbg) return fail(DGDS_ESTATE, "set DGDS_APPEND_DBG before dgds_create");
+  std::lock_guard<std::mutex> lk(s->mu);
+  DGDS_CUDA(cudaStreamSynchronize(s->st));
+  DGDS_CUDA(cudaMemcpy(out, s->T.dbg, std::min<int64_t>(n_warps, 65536) * 16, cudaMemcpyDeviceToHost));
+  return DGDS_OK;
+}

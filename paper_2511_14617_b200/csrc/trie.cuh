@@ -70,6 +70,7 @@ struct DevTrie {
   int32_t ahead;             // append look-ahead (tokens) of the L2 prefetch; 0 = off
   int32_t claim_cas;         // append claim: 1 = CAS-first, 0 = read the window first
   int32_t* hist;             // append-only token history (replica sync blobs); K1 copies every token
+  unsigned long long* dbg;   // optional (debug): per-warp [start, end] globaltimer of K1
 };
 
 __host__ __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
@@ -138,7 +139,11 @@ __device__ __forceinline__ void load_key_nc(const Slot* p, unsigned long long& k
 }
 
 __device__ __forceinline__ void prefetch_l2_window(const void* p) {  // one probe window
+#ifdef DGDS_BULK_PREFETCH
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "n"(kWindow * 32) : "memory");
+#else
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));  // per-thread: no TMA-unit queue
+#endif
 }
 __device__ __forceinline__ void prefetch_l1(const void* p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
 
