@@ -487,6 +487,11 @@ def main_b200(args):
 
         host_step(host_steps[0])  # warm-up: pinned staging buffers reach their steady size
         torch.cuda.synchronize()
+        tp = None
+        if os.environ.get("DGDS_E2E_TRACE"):  # debug only: device timeline of the e2e steps (numbers then invalid)
+            from torch.profiler import ProfilerActivity, profile
+            tp = profile(activities=[ProfilerActivity.CPU, ProfilerActivity.CUDA])
+            tp.__enter__()
         t0 = time.perf_counter()
         for hs_ in host_steps[1:]:
             a_, b_ = host_step(hs_)
@@ -494,6 +499,10 @@ def main_b200(args):
             d2h += b_
         torch.cuda.synchronize()
         t1 = time.perf_counter()
+        if tp is not None:
+            tp.__exit__(None, None, None)
+            os.makedirs("gpurun_out", exist_ok=True)
+            tp.export_chrome_trace("gpurun_out/e2e_bench_trace.json")
         E = len(host_steps) - 1
         e2e = {"value": Q * E / (t1 - t0), "unit": "queries/s", "h2d_bytes_per_step": h2d // E,
                "d2h_bytes_per_step": d2h // E, "steps": E,

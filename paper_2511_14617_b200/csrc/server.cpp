@@ -10,6 +10,7 @@
 // missing device is an error.
 
 #include <cuda_runtime.h>
+#include <emmintrin.h>
 #include <deque>
 
 #include <algorithm>
@@ -263,6 +264,23 @@ struct GroupRec {
 
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
+// Copy into pinned staging memory with non-temporal (streaming) stores. A staging block
+// written by several threads with normal stores, then read by the device (DMA or a pull
+// kernel), measured 8 GB/s on the GPU box instead of 52 GB/s: the device reads snoop
+// lines still dirty in the writers' caches (tools/h2d_dirty.cu). The caller fences.
+void nt_copy(void* dst, const void* src, size_t n) {
+  char* d = static_cast<char*>(dst);
+  const char* sp = static_cast<const char*>(src);
+  const size_t head = std::min<size_t>(n, (16 - (reinterpret_cast<uintptr_t>(d) & 15)) & 15);
+  std::memcpy(d, sp, head);
+  d += head;
+  sp += head;
+  n -= head;
+  for (; n >= 16; n -= 16, d += 16, sp += 16)
+    _mm_stream_si128(reinterpret_cast<__m128i*>(d), _mm_loadu_si128(reinterpret_cast<const __m128i*>(sp)));
+  std::memcpy(d, sp, n);
+}
+
 }  // namespace
 
 struct dgds_server {
@@ -302,7 +320,7 @@ struct dgds_server {
   DevBuf d_stage, d_out;
   PinnedBuf hq_stage;  // mapped: the copy-in kernel reads it over PCIe
   DevBuf dq_stage;
-  bool h2d_kernel = true;  // DGDS_H2D=dma: copy-engine H2D instead
+  bool h2d_kernel = false;  // copy-engine H2D (no SMs taken from K1); DGDS_H2D=kernel: a pull kernel
   int h2d_blocks = 148;    // one CTA per SM (measured best); DGDS_H2D_BLOCKS
   std::unique_ptr<WorkerPool> pool;
   WorkerPool& workers() {
@@ -736,7 +754,7 @@ int dgds_create(const dgds_params* params, dgds_server** out) {
   s->p = p;
   s->h_out.flags = cudaHostAllocMapped;
   s->hq_stage.flags = cudaHostAllocMapped;
-  if (const char* e = std::getenv("DGDS_H2D")) s->h2d_kernel = std::strcmp(e, "dma") != 0;
+  if (const char* e = std::getenv("DGDS_H2D")) s->h2d_kernel = std::strcmp(e, "kernel") == 0;
   cudaDeviceGetAttribute(&s->h2d_blocks, cudaDevAttrMultiProcessorCount, p.device);
   if (const char* e = std::getenv("DGDS_H2D_BLOCKS")) s->h2d_blocks = std::max(1, std::atoi(e));
   s->D = p.max_pattern_len + p.max_spec_len;
@@ -948,10 +966,11 @@ static int update_batch_locked(dgds_server* s, int64_t n, const int32_t* handles
   if (int rc = s->h_stage.ensure(total)) return rc;
   if (int rc = s->d_stage.ensure(total)) return rc;
   char* h = static_cast<char*>(s->h_stage.p);
-  std::memcpy(h, segs.data(), b_seg);
   for (auto& pc : pieces) pc.tok_off -= offs[0];
-  std::memcpy(h + o_piece, pieces.data(), b_piece);
-  std::memcpy(h + o_tok, tokens + offs[0], ntok * sizeof(int32_t));
+  nt_copy(h, segs.data(), b_seg);
+  nt_copy(h + o_piece, pieces.data(), b_piece);
+  nt_copy(h + o_tok, tokens + offs[0], ntok * sizeof(int32_t));
+  _mm_sfence();
   char* d = static_cast<char*>(s->d_stage.p);
   pc.mark("stage");
   DGDS_CUDA(cudaMemcpyAsync(d, h, total, cudaMemcpyHostToDevice, s->st));
@@ -1000,8 +1019,9 @@ static int update_device_impl(dgds_server* s, int64_t n, const int32_t* handles,
   if (int rc = s->h_stage.ensure(total)) return rc;
   if (int rc = s->d_stage.ensure(total)) return rc;
   char* h = static_cast<char*>(s->h_stage.p);
-  std::memcpy(h, segs.data(), b_seg);
-  std::memcpy(h + o_piece, pieces.data(), pieces.size() * sizeof(dgds::AppendPiece));
+  nt_copy(h, segs.data(), b_seg);
+  nt_copy(h + o_piece, pieces.data(), pieces.size() * sizeof(dgds::AppendPiece));
+  _mm_sfence();
   char* d = static_cast<char*>(s->d_stage.p);
   DGDS_CUDA(cudaMemcpyAsync(d, h, total, cudaMemcpyHostToDevice, join.stream()));
   DGDS_CUDA(cudaEventRecord(s->staging_free, join.stream()));
@@ -1134,23 +1154,29 @@ int speculate_host(dgds_server* s, int64_t n, const int32_t* handles, const uint
   pool.run(tasks, [&](int t) {
     const int64_t q0 = t * chunk, q1 = std::min<int64_t>(n, q0 + chunk);
     if (q0 >= q1) return;
+    thread_local std::vector<int32_t> lens, rows;  // built in cache, then streamed out
+    lens.resize(q1 - q0);
+    rows.assign(static_cast<size_t>(q1 - q0) * P, 0);
     for (int64_t i = q0; i < q1; ++i) {
       const int32_t hd = handles[i];
       if ((hd < 0 || static_cast<size_t>(hd) >= ngroups || pat_offs[i + 1] < pat_offs[i]) && bad[t] < 0) bad[t] = i;
       const uint64_t L = pat_offs[i + 1] - pat_offs[i];
-      hl[i] = static_cast<int32_t>(std::min<uint64_t>(L, 0x7FFFFFFF));
+      lens[i - q0] = static_cast<int32_t>(std::min<uint64_t>(L, 0x7FFFFFFF));
       const uint64_t keep = std::min<uint64_t>(L, static_cast<uint64_t>(P));
       const int32_t* src = patterns + pat_offs[i + 1] - keep;
-      int32_t* dst = hp + i * P;
+      int32_t* dst = rows.data() + (i - q0) * P;
       for (uint64_t k = 0; k < keep; ++k) dst[k] = src[k];
     }
-    std::memcpy(h + q0 * 4, handles + q0, (q1 - q0) * 4);
+    nt_copy(hl + q0, lens.data(), (q1 - q0) * 4);
+    nt_copy(hp + q0 * P, rows.data(), rows.size() * 4);
+    nt_copy(h + q0 * 4, handles + q0, (q1 - q0) * 4);
     if (verify) {
-      std::memcpy(h + o_tr + static_cast<size_t>(q0) * truth_stride * 4, truth + q0 * truth_stride,
-                  static_cast<size_t>(q1 - q0) * truth_stride * 4);
-      std::memcpy(h + o_tl + q0 * 4, truth_left + q0, (q1 - q0) * 4);
-      std::memcpy(h + o_lm + q0 * 4, limit + q0, (q1 - q0) * 4);
+      nt_copy(h + o_tr + static_cast<size_t>(q0) * truth_stride * 4, truth + q0 * truth_stride,
+              static_cast<size_t>(q1 - q0) * truth_stride * 4);
+      nt_copy(h + o_tl + q0 * 4, truth_left + q0, (q1 - q0) * 4);
+      nt_copy(h + o_lm + q0 * 4, limit + q0, (q1 - q0) * 4);
     }
+    _mm_sfence();  // streaming stores globally visible before the copy is issued
   });
   for (int t = 0; t < tasks; ++t) {
     if (bad[t] >= 0) {
