@@ -140,7 +140,7 @@ def run_multi(args, world, rank, local, dev):
     side = torch.cuda.Stream(dev)
     side_q = torch.cuda.Stream(dev)  # early query sends (px)
     q_sent = set()
-    ev_side = torch.cuda.Event()
+    ev_side = torch.cuda.Event()  # spin-waited: blocking events cost 1-3 ms of wakeup per tick here
     meta_h = torch.empty((world * capa, 5), dtype=torch.int32).pin_memory()
     mq = world * capq
     # reply record: n_cands | lens[k] | pad | scores[k] f64 | supports[k] i64 | tokens[k][dl] | verify[3] | pad
@@ -231,9 +231,29 @@ def run_multi(args, world, rank, local, dev):
             px.send("q", inp["q_owner"], inp["q"], s + 1, origin_word=QRY_W - 1, want_slot=False, stream=side_q)
         q_sent.add(s)
 
-    def step(s, stats):
-        """One tick in engine order (engine.cpp:88-161): draft queries (+ verify) on the
-        current index, then the appends of the tick's emitted tokens."""
+    plans = {}  # tick -> plan, or a future of one (planned on a helper thread)
+    planner = None
+    if use_px:
+        from concurrent.futures import ThreadPoolExecutor
+        planner = ThreadPoolExecutor(max_workers=1)  # ctypes and event waits release the GIL
+    run_until = [0]  # ticks < run_until[0] will run in the current loop: only those are planned ahead
+
+    def make_plan(s, k):
+        """Host half of tick s's appends (dgds_update_plan_routed): waits for the tick's routed
+        metadata, does the bookkeeping, returns the plan to launch after tick s's queries."""
+        ev_bufs[k].synchronize()
+        nrej = C.c_int64()
+        plan = C.c_void_p()
+        _lib.check(L.dgds_update_plan_routed(srv.handle, world, capa, C.c_void_p(cnt_bufs[k].data_ptr()),
+                                             C.c_void_p(meta_bufs[k].data_ptr()), 5,
+                                             C.c_void_p(px.slab_ptr("a", s + 1)), APP_W, 0.0, C.byref(nrej),
+                                             C.byref(plan)))
+        if nrej.value:
+            raise RuntimeError("routed append out of order")
+        return plan
+
+    def q_part(s, stats):
+        """Tick s, first half (engine.cpp:88-143): draft queries (+ fused verify) on the current index."""
         nonlocal overflow
         inp = steps_in[s]
         main = torch.cuda.current_stream(dev)
@@ -265,50 +285,82 @@ def run_multi(args, world, rank, local, dev):
                                                 C.c_void_p(main.cuda_stream)))
             t0 = mark("q_kernel", t0)
             back, ovq = router.reverse(replies, st_q)
+            overflow = overflow | ovq
             t0 = mark("q_rev", t0)
-        # (3) the tick's appends: metadata arrived during the previous tick; bookkeeping, then K1
-        ra, ova, k = inflight.pop(s)
-        ev_bufs[k].synchronize()
-        t0 = mark("meta_wait", t0)
-        if use_px:
-            main.wait_event(ev_bufs[k])
-            t0 = mark("meta_np", t0)
-            nrej = C.c_int64()
-            _lib.check(L.dgds_update_batch_routed(srv.handle, world, capa, C.c_void_p(cnt_bufs[k].data_ptr()),
-                                                  C.c_void_p(meta_bufs[k].data_ptr()), 5,
-                                                  C.c_void_p(px.slab_ptr("a", seq)), APP_W, 0.0, C.byref(nrej),
-                                                  C.c_void_p(main.cuda_stream)))
-            if nrej.value:
-                raise RuntimeError("routed append out of order")
-            if stats:
-                app_alg_owner[0] += own_alg[s]
-        else:
-            meta = meta_bufs[k].numpy()
-            rows = np.nonzero(meta[:, 0] >= 0)[0]
-            if len(rows):
-                m = meta[rows]
-                n = m[:, 4].astype(np.uint64)
-                prev = m[:, 2].view(np.uint32).astype(np.uint64) | (m[:, 3].astype(np.uint64) << np.uint64(32))
-                starts = rows.astype(np.uint64) * np.uint64(APP_W) + np.uint64(5)
-                main.wait_event(ev_bufs[k])
-                rep = srv.update_device_strided(m[:, 0].copy(), m[:, 1].copy(), prev, starts, n, ra.data_ptr(), 0.0,
-                                                main.cuda_stream)
-                if not rep["ok"].all():
-                    raise RuntimeError("routed append out of order")
-            if stats:
-                app_alg_owner[0] += own_alg[s]
-        if not use_px:
-            overflow = overflow | ovq | ova
-        t0 = mark("append_call", t0)
-        # (4) route the next tick's appends now, so their metadata is home by then
-        route_appends(s + 1)
-        t0 = mark("route_next", t0)
-        send_queries(s + 1)
-        mark("send_next", t0)
         return back
 
-    for s in range(W):
-        step(s, False)
+    def a_part(s, stats, pipeline=False):
+        """Tick s, second half (engine.cpp:144-161): the appends of the tick's emitted tokens,
+        planned on the host during the previous tick (px), launched after the tick's queries.
+        With pipeline, tick s+1's queries are enqueued before tick s+1 is planned, so the GPU
+        has work queued while the host plans. Returns tick s+1's reply view when enqueued."""
+        nonlocal overflow
+        main = torch.cuda.current_stream(dev)
+        t0 = time.perf_counter()
+        ra, ova, k = inflight.pop(s)
+        if use_px:
+            # tick s+1's exchanges first: they need only tick s's replies (ev_rep), and their kernels
+            # get SMs before K1 fills them; the helper thread plans tick s+1 as its metadata lands
+            if s not in plans:  # the planner is FIFO: tick s must be planned before tick s+1
+                plans[s] = planner.submit(make_plan, s, k)
+            route_appends(s + 1)
+            if s + 1 < run_until[0] and (s + 1) in inflight and (s + 1) not in plans:
+                plans[s + 1] = planner.submit(make_plan, s + 1, inflight[s + 1][2])
+            send_queries(s + 1)
+            t0 = mark("route_next", t0)
+            plan = plans.pop(s).result()
+            t0 = mark("meta_np", t0)
+            main.wait_event(ev_bufs[k])  # K1 reads the slab rows delivered on the side stream
+            _lib.check(L.dgds_update_launch(srv.handle, plan, C.c_void_p(main.cuda_stream)))
+            if stats:
+                app_alg_owner[0] += own_alg[s]
+            t0 = mark("append_call", t0)
+            nxt = None
+            if pipeline and s + 1 < run_until[0]:
+                nxt = q_part(s + 1, stats)
+            mark("send_next", t0)
+            return nxt
+        ev_bufs[k].synchronize()
+        t0 = mark("meta_wait", t0)
+        meta = meta_bufs[k].numpy()
+        rows = np.nonzero(meta[:, 0] >= 0)[0]
+        if len(rows):
+            m = meta[rows]
+            n = m[:, 4].astype(np.uint64)
+            prev = m[:, 2].view(np.uint32).astype(np.uint64) | (m[:, 3].astype(np.uint64) << np.uint64(32))
+            starts = rows.astype(np.uint64) * np.uint64(APP_W) + np.uint64(5)
+            main.wait_event(ev_bufs[k])
+            rep = srv.update_device_strided(m[:, 0].copy(), m[:, 1].copy(), prev, starts, n, ra.data_ptr(), 0.0,
+                                            main.cuda_stream)
+            if not rep["ok"].all():
+                raise RuntimeError("routed append out of order")
+        if stats:
+            app_alg_owner[0] += own_alg[s]
+        overflow = overflow | ova
+        t0 = mark("append_call", t0)
+        route_appends(s + 1)  # the next tick's appends (NCCL route), one tick ahead
+        mark("route_next", t0)
+        return None
+
+    def run_ticks(a, b, stats):
+        """Ticks [a, b) back to back, pipelined (px) or in order (nccl)."""
+        run_until[0] = b
+        back = q_part(a, stats)
+        for s in range(a, b):
+            nxt = a_part(s, stats, pipeline=use_px)
+            if not use_px and s + 1 < b:
+                nxt = q_part(s + 1, stats)
+            back = nxt if nxt is not None else back
+        return back
+
+    def step(s, stats):
+        """One tick, unpipelined (the e2e loop)."""
+        run_until[0] = max(run_until[0], s + 1)
+        back = q_part(s, stats)
+        a_part(s, stats)
+        return back
+
+    run_ticks(0, W, False)
     torch.cuda.synchronize()
     prof = _lib.Profile()
     _lib.check(L.dgds_profile_enable(srv.handle, 1))
@@ -325,8 +377,7 @@ def run_multi(args, world, rank, local, dev):
         tp.__enter__()
     with ClockSampler(local) as clk:
         e0.record()
-        for s in range(W, W + K):
-            step(s, True)
+        run_ticks(W, W + K, True)
         e1.record()
         torch.cuda.synchronize()
     if tp is not None:
@@ -362,13 +413,19 @@ def run_multi(args, world, rank, local, dev):
         t0 = time.perf_counter()
         d2h = 0
         base_s = len(steps_in)
+        run_until[0] = base_s + E
+        back_h = None
         for j, hin in enumerate(host_in):
             d_in = {k: hin[k].to(dev, non_blocking=True) for k in ("app", "app_owner", "q", "q_owner")}
             d_in["ready"] = torch.cuda.Event()
             d_in["ready"].record(torch.cuda.current_stream(dev))
             steps_in.append(d_in)
-            back = step(base_s + j, False).cpu()
-            d2h += back.nbytes
+            back = step(base_s + j, False)
+            if back_h is None:
+                back_h = torch.empty(back.shape, dtype=back.dtype).pin_memory()  # the step's replies land here
+            back_h.copy_(back, non_blocking=True)
+            torch.cuda.current_stream(dev).synchronize()
+            d2h += back_h.nbytes
         torch.cuda.synchronize()
         dt = torch.tensor([time.perf_counter() - t0], device=dev)
         dist.all_reduce(dt, op=dist.ReduceOp.MAX)
@@ -419,6 +476,8 @@ def run_multi(args, world, rank, local, dev):
         print(json.dumps(line))
     dist.barrier()
     torch.cuda.synchronize()
+    if planner is not None:
+        planner.shutdown(wait=True)
     if use_px:
         px.close()  # every rank is past its last exchange (barrier above)
     srv.close()

@@ -241,6 +241,17 @@ int dgds_speculate_records(dgds_server* s, int64_t n, const int32_t* d_records, 
 int dgds_update_batch_routed(dgds_server* s, int32_t n_seg, int64_t seg_rows, const int32_t* h_counts,
                              const int32_t* h_meta, int32_t meta_stride, const int32_t* d_rows, int32_t row_words,
                              double now, int64_t* n_rejected, void* stream);
+/* Two-phase form of dgds_update_batch_routed: the plan call does all host work (validation,
+ * replies, versions, history log, capacity) and returns a plan; dgds_update_launch later
+ * enqueues the device part (H2D of the segment tables + the append kernel) on `stream` and
+ * frees the plan. Lets a driver plan tick s+1 while the GPU runs tick s. Plans must be
+ * launched in the order they were made (DGDS_ESTATE otherwise); d_rows must stay valid
+ * until the launched kernel has run. */
+typedef struct dgds_update_plan dgds_update_plan;
+int dgds_update_plan_routed(dgds_server* s, int32_t n_seg, int64_t seg_rows, const int32_t* h_counts,
+                            const int32_t* h_meta, int32_t meta_stride, const int32_t* d_rows, int32_t row_words,
+                            double now, int64_t* n_rejected, dgds_update_plan** out);
+int dgds_update_launch(dgds_server* s, dgds_update_plan* plan, void* stream);
 /* Strided device -> host copy (cudaMemcpy2DAsync): `rows` rows of `width` bytes. */
 int dgds_copy_rows_d2h(void* h_dst, int64_t dst_pitch, const void* d_src, int64_t src_pitch, int64_t width,
                        int64_t rows, void* stream);
