@@ -66,6 +66,8 @@ def parse():
     ap.add_argument("--cpu-groups", type=int, default=32, help="groups in the bounded CPU sample")
     ap.add_argument("--cpu-steps", type=int, default=8)
     ap.add_argument("--seed", type=int, default=1234)
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="N>1: replicate the config's group set per GPU (weak) or shard it (strong, e.g. C4)")
     ap.add_argument("--route", default="px", choices=["px", "nccl"],
                     help="N>1 owner routing: NVLink peer-memory exchange fused into the kernels (px) "
                          "or NCCL all_to_all_single (nccl, the library baseline)")

@@ -34,7 +34,11 @@ def run_multi(args, world, rank, local, dev):
     from paper_2511_14617_b200.workload import CONFIGS, generate_workload, group_id
 
     base = CONFIGS[args.config]
-    cfg = replace(base, num_groups=base.num_groups * world)
+    strong = args.scaling == "strong"
+    # weak: the group set is replicated N times (per-GPU work fixed); strong: the config's own
+    # group set is sharded over the N GPUs (total work fixed; e.g. C4, the Kimi-K2 shape, which
+    # does not fit one GPU)
+    cfg = base if strong else replace(base, num_groups=base.num_groups * world)
     tr = generate_workload(cfg)
     G, R = cfg.num_groups, cfg.group_size
     S = G * R
@@ -50,6 +54,8 @@ def run_multi(args, world, rank, local, dev):
     my_streams = (mine[:, None] * R + np.arange(R)[None, :]).reshape(-1)
     K, W = args.steps, args.warmup
     Q, kq, dl = args.queries, args.top_k, args.draft_len
+    if strong:
+        Q = max(1, Q // world)  # the config's query batch, split over the ranks
     E = max(0, args.e2e_steps)
     assert dl <= 8, "query records carry 8 truth tokens"
     idx_tokens = int(prefill[my_streams].sum()) + len(my_streams) * rt * (K + W + E) * world
@@ -455,17 +461,20 @@ def run_multi(args, world, rank, local, dev):
             "avg_launch_ms": us / 1e3 / max(1, n), "peak_kind": peak_kind, "per_gpu": True}
         line = {
             "metric": "draft_queries_per_s", "value": world * Q * K / T, "unit": "queries/s", "n_gpus": world,
-            "steps": K, "warmup": W, "ms_per_step": 1e3 * T / K, "higher_is_better": True, "scaling": "weak",
+            "steps": K, "warmup": W, "ms_per_step": 1e3 * T / K, "higher_is_better": True,
+            "scaling": "strong" if strong else "weak",
             "vs_baseline": None, "dtype": "i32+f64", "data": "synthetic",
             "append_tokens_per_s": ntok_all / T,
-            "config": {"workload": f"{args.config}: {CONFIG_NAMES[args.config]} (group set replicated x{world})",
+            "config": {"workload": f"{args.config}: {CONFIG_NAMES[args.config]} " + (
+                           f"(group set sharded over {world} GPUs)" if strong else f"(group set replicated x{world})"),
                        "queries_per_step": world * Q, "queries_per_rank": Q, "record_tokens": rt, "top_k": kq,
                        "draft_len": dl, "prefill": args.prefill, "groups": G,
                        "routing": ("fnv1a64(gid) % N owner; NVLink peer-memory exchange: k_px_send stores rows "
                                    "into the owner's slab, K2+K3 stores replies into the sender's slab (no collectives)"
                                    if use_px else
                                    "fnv1a64(gid) % N owner; NCCL all_to_all_single (counts, payload, replies)"),
-                       "l2": "inputs larger than L2 (per-GPU index ~ the N=1 index)",
+                       "l2": ("inputs larger than L2 (per-GPU index = 1/N of the config's index)" if strong else
+                              "inputs larger than L2 (per-GPU index ~ the N=1 index)"),
                        "parallelism": f"group-sharded dp{world}"},
             "roofline": roof("k_query (K2+K3)", q_ach, q_alg_all, qus_all, K * world) if dom_q else roof(
                 "k_append (K1)", a_ach, a_alg_all, aus_all, K * world),
