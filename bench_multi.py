@@ -25,7 +25,21 @@ APP_W = 21  # append record: [local handle, request id, prev lo, prev hi, n, tok
 QRY_W = 21  # query record: [local handle, pat_len, pattern[8], truth_left, limit, truth[8], pad]
 
 
+def _pin_rank_cores(world, local):
+    """Give each rank its own slice of the host cores (threads created later inherit it), so
+    the ranks' host paths do not preempt each other (the tick waits on every rank's host)."""
+    try:
+        cores = sorted(os.sched_getaffinity(0))
+        per = len(cores) // world
+        if per >= 2:
+            os.sched_setaffinity(0, set(cores[local * per:(local + 1) * per]))
+    except (AttributeError, OSError):
+        pass
+
+
 def run_multi(args, world, rank, local, dev):
+    if os.environ.get("DGDS_PIN_CORES", "1") == "1":
+        _pin_rank_cores(world, local)
     from bench import CONFIG_NAMES, RANDOM_CEILING_GBS, ClockSampler, append_alg_bytes, peaks
     from paper_2511_14617_b200 import _lib
     from paper_2511_14617_b200.dgds import DgdsParams, DraftServer, SpeculationArgs, args_array, shard_of_group
