@@ -61,7 +61,7 @@ def parse():
     ap.add_argument("--top-k", type=int, default=4)
     ap.add_argument("--draft-len", type=int, default=8)
     ap.add_argument("--prefill", type=float, default=0.5)
-    ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--e2e-steps", type=int, default=30)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-groups", type=int, default=32, help="groups in the bounded CPU sample")
     ap.add_argument("--cpu-steps", type=int, default=8)
@@ -316,7 +316,7 @@ def main_b200(args):
     tr = sched.tr
     S = sched.S
     # ---- server + untimed prefill (host API, 16-token records, round-robin) ----
-    idx_tokens = int(sched.prefill.sum()) + S * args.record_tokens * (args.steps + args.warmup + args.e2e_steps)
+    idx_tokens = int(sched.prefill.sum()) + S * args.record_tokens * (args.steps + args.warmup + 2 * args.e2e_steps + 4)
     srv = DraftServer(DgdsParams(), device=local, expected_nodes=min(idx_tokens * 24, 1_900_000_000),
                       expected_streams=S)
     handles_of_stream = np.repeat(srv.group_handles(sched.gids), sched.R).astype(np.int32)
@@ -446,71 +446,109 @@ def main_b200(args):
     # ---- e2e: same tick through the host C ABI (host buffers, H2D/D2H inside) ----
     e2e = None
     if args.e2e_steps > 0:
-        E = args.e2e_steps + 1  # + one warm-up step
-        host_steps = []
-        for s in range(E):
-            live = np.nonzero(spos < tr.lengths)[0]
-            ns = np.minimum(args.record_tokens, tr.lengths[live] - spos[live])
-            offs = np.zeros(len(live) + 1, np.uint64)
-            offs[1:] = np.cumsum(ns)
-            g0 = tr.offsets[live] + spos[live]
-            idx = np.repeat(g0, ns) + (np.arange(int(offs[-1])) - np.repeat(offs[:-1].astype(np.int64), ns))
-            toks = np.ascontiguousarray(tr.tokens[idx])
-            prev = spos[live].astype(np.uint64)
-            spos[live] += ns
-            st, qpos = sched.queries(Q)
-            base = tr.offsets[st] + qpos
-            pat = np.stack([tr.tokens[base - 6 + j] for j in range(6)], 1).astype(np.int32).reshape(-1)
-            poff = np.arange(0, 6 * Q + 1, 6, dtype=np.uint64)
-            tl = (tr.lengths[st] - qpos).astype(np.int32)
-            tru = np.zeros((Q, dl), np.int32)
-            for j in range(dl):
-                ok = j < tl
-                tru[ok, j] = tr.tokens[(base + j)[ok]]
-            host_steps.append((handles_of_stream[live], rid_of_stream[live], prev, offs, toks,
-                               handles_of_stream[st].copy(), poff, pat, tru, tl))
+        WE = 2  # warm-up steps per mode: both result slots' pinned buffers reach their steady size
+        E = args.e2e_steps + WE
+
+        def make_steps(count):
+            out = []
+            for _ in range(count):
+                live = np.nonzero(spos < tr.lengths)[0]
+                ns = np.minimum(args.record_tokens, tr.lengths[live] - spos[live])
+                offs = np.zeros(len(live) + 1, np.uint64)
+                offs[1:] = np.cumsum(ns)
+                g0 = tr.offsets[live] + spos[live]
+                idx = np.repeat(g0, ns) + (np.arange(int(offs[-1])) - np.repeat(offs[:-1].astype(np.int64), ns))
+                toks = np.ascontiguousarray(tr.tokens[idx])
+                prev = spos[live].astype(np.uint64)
+                spos[live] += ns
+                st, qpos = sched.queries(Q)
+                base = tr.offsets[st] + qpos
+                pat = np.stack([tr.tokens[base - 6 + j] for j in range(6)], 1).astype(np.int32).reshape(-1)
+                poff = np.arange(0, 6 * Q + 1, 6, dtype=np.uint64)
+                tl = (tr.lengths[st] - qpos).astype(np.int32)
+                tru = np.zeros((Q, dl), np.int32)
+                for j in range(dl):
+                    ok = j < tl
+                    tru[ok, j] = tr.tokens[(base + j)[ok]]
+                out.append((handles_of_stream[live], rid_of_stream[live], prev, offs, toks,
+                            handles_of_stream[st].copy(), poff, pat, tru, tl))
+            return out
+
         view = _lib.ResultView()
         em_sum = [0]
-        h2d = d2h = 0
         last = C.c_uint64()
+        ticket = C.c_uint64()
 
-        def host_step(hs_):
-            (h, r, prev, offs, toks, qh, poff, pat, tru, tl) = hs_
+        def update(hs_):
+            (h, r, prev, offs, toks) = hs_[:5]
             srv.update_arrays(h, r, prev, offs, toks, 0.0)
-            # compact results (CSR) in the server's pinned block: the public zero-copy query call
-            _lib.check(L.dgds_speculate_verify_view(
-                srv.handle, Q, qh.ctypes.data, poff.ctypes.data, pat.ctypes.data, sp_args.ctypes.data, 0,
-                tru.ctypes.data, dl, tl.ctypes.data, tl.ctypes.data, C.byref(view)))
+
+        def submit(hs_):
+            (qh, poff, pat, tru, tl) = hs_[5:]
+            _lib.check(L.dgds_speculate_submit(srv.handle, Q, qh.ctypes.data, poff.ctypes.data, pat.ctypes.data,
+                                               sp_args.ctypes.data, 0, tru.ctypes.data, dl, tl.ctypes.data,
+                                               tl.ctypes.data, C.byref(ticket)))
+            return int(ticket.value)
+
+        def consume(t):
+            # compact results (CSR) in the server's pinned block; the step reads every emitted count
+            _lib.check(L.dgds_speculate_wait(srv.handle, t, C.byref(view)))
             em_sum[0] += int(np.ctypeslib.as_array(C.cast(view.emitted, C.POINTER(C.c_int32)), shape=(Q,)).sum())
             _lib.check(L.dgds_last_transfer(srv.handle, C.byref(last)))
+            return int(last.value)
+
+        def h2d_bytes(hs_):
             # bytes actually staged: tokens + segment table (32 B/record) + pieces (16 B/record);
             # patterns (8 int32 rows), pattern lengths, handles, truth rows, truth_left, limit, args
-            return (toks.nbytes + len(h) * (32 + 16) + Q * (4 + 4 + 8 * 4 + dl * 4 + 4 + 4) + 32, int(last.value))
+            return hs_[4].nbytes + len(hs_[0]) * (32 + 16) + Q * (4 + 4 + 8 * 4 + dl * 4 + 4 + 4) + 32
 
-        host_step(host_steps[0])  # warm-up: pinned staging buffers reach their steady size
-        torch.cuda.synchronize()
+        def run(steps, pipelined):
+            """serial: update, query, read results, next tick. pipelined: tick s+1's host work
+            (update plan + K1 launch, query staging + launch) is issued before tick s's results
+            are read, so it overlaps tick s's device work (two result slots)."""
+            d2h, pend = 0, None
+            for hs_ in steps:
+                update(hs_)
+                t = submit(hs_)
+                if not pipelined:
+                    d2h += consume(t)
+                    continue
+                if pend is not None:
+                    d2h += consume(pend)
+                pend = t
+            if pend is not None:
+                d2h += consume(pend)
+            return d2h
+
+        res = {}
         tp = None
-        if os.environ.get("DGDS_E2E_TRACE"):  # debug only: device timeline of the e2e steps (numbers then invalid)
-            from torch.profiler import ProfilerActivity, profile
-            tp = profile(activities=[ProfilerActivity.CPU, ProfilerActivity.CUDA])
-            tp.__enter__()
-        t0 = time.perf_counter()
-        for hs_ in host_steps[1:]:
-            a_, b_ = host_step(hs_)
-            h2d += a_
-            d2h += b_
-        torch.cuda.synchronize()
-        t1 = time.perf_counter()
+        for mode in ("serial", "pipelined"):
+            steps = make_steps(E)
+            run(steps[:WE], mode == "pipelined")
+            torch.cuda.synchronize()
+            if mode == "pipelined" and os.environ.get("DGDS_E2E_TRACE"):  # debug only (numbers then invalid)
+                from torch.profiler import ProfilerActivity, profile
+                tp = profile(activities=[ProfilerActivity.CPU, ProfilerActivity.CUDA])
+                tp.__enter__()
+            t0 = time.perf_counter()
+            d2h = run(steps[WE:], mode == "pipelined")
+            torch.cuda.synchronize()
+            t1 = time.perf_counter()
+            n_e = len(steps) - WE
+            res[mode] = {"value": Q * n_e / (t1 - t0), "unit": "queries/s",
+                         "h2d_bytes_per_step": sum(h2d_bytes(x) for x in steps[WE:]) // n_e,
+                         "d2h_bytes_per_step": d2h // n_e, "steps": n_e,
+                         "append_tokens_per_s": sum(x[4].size for x in steps[WE:]) / (t1 - t0)}
         if tp is not None:
             tp.__exit__(None, None, None)
             os.makedirs("gpurun_out", exist_ok=True)
             tp.export_chrome_trace("gpurun_out/e2e_bench_trace.json")
-        E = len(host_steps) - 1
-        e2e = {"value": Q * E / (t1 - t0), "unit": "queries/s", "h2d_bytes_per_step": h2d // E,
-               "d2h_bytes_per_step": d2h // E, "steps": E,
-               "append_tokens_per_s": sum(x[4].size for x in host_steps[1:]) / (t1 - t0),
-               "path": "dgds_update_batch + dgds_speculate_verify_view (host buffers in, compact pinned results "
-                       "out; the step reads every query's emitted count)"}
+        e2e = dict(res["pipelined"])
+        e2e["path"] = ("per tick: dgds_update_batch + dgds_speculate_submit, then dgds_speculate_wait on the "
+                       "previous tick's ticket (host buffers in, compact pinned results out; every emitted count "
+                       "read); the next tick's host work overlaps this tick's device work")
+        e2e["serial"] = res["serial"]
+        e2e["serial"]["path"] = "per tick: dgds_update_batch + dgds_speculate_submit + dgds_speculate_wait"
 
     # ---- CPU baseline (reference, bounded sample, all host cores) ----
     cpu = None

@@ -257,7 +257,7 @@ int dgds_copy_rows_d2h(void* h_dst, int64_t dst_pitch, const void* d_src, int64_
                        int64_t rows, void* stream);
 
 /* Zero-copy host results: compact per-query candidate lists (CSR) in a pinned block owned
- * by the server, valid until the next query call on `s`. Candidates of query q are
+ * by the server, valid until the second-next host query batch on `s` (two result slots). Candidates of query q are
  * cands[cand_off[q] .. cand_off[q+1]) in candidate_before order (cst.cpp:29-35); the tokens
  * of candidate c are tokens[tok_off[c] .. tok_off[c+1]). Verification (engine.cpp:115-143)
  * runs when truth != NULL. Same inputs and validation as dgds_speculate_verify_batch. */
@@ -281,6 +281,20 @@ int dgds_speculate_verify_view(dgds_server* s, int64_t n, const int32_t* handles
                                const int32_t* patterns, const dgds_spec_args* args, int64_t args_stride,
                                const int32_t* truth, int32_t truth_stride, const int32_t* truth_left,
                                const int32_t* limit, dgds_result_view* out);
+
+/* Asynchronous dgds_speculate_verify_view. submit validates and stages the batch, queues its
+ * H2D, query (+ verify) and copy-out behind every update already launched, and returns a
+ * ticket without waiting; wait blocks for that batch and fills `out`. Two batches can be in
+ * flight: submitting a batch reuses the result slot of the batch submitted two before it
+ * (waiting for it on the device if needed), after which waiting on that older ticket fails
+ * with DGDS_EINVAL. So a caller overlaps the next tick's host work (dgds_update_batch plan,
+ * query staging) with this tick's device work. Updates made after a submit are not seen by
+ * it (stream order). Nothing is launched unless the whole batch validates. */
+int dgds_speculate_submit(dgds_server* s, int64_t n, const int32_t* handles, const uint64_t* pat_offs,
+                          const int32_t* patterns, const dgds_spec_args* args, int64_t args_stride,
+                          const int32_t* truth, int32_t truth_stride, const int32_t* truth_left,
+                          const int32_t* limit, uint64_t* ticket);
+int dgds_speculate_wait(dgds_server* s, uint64_t ticket, dgds_result_view* out);
 
 /* Segmented form for owner routing: rows arrive as n_seg sender segments of seg_rows rows
  * (row j of segment s valid while j < d_seg_count[s]); the reply of row j of segment s is

@@ -1350,12 +1350,16 @@ __global__ void k_cmp_count(int64_t n, int32_t K, const int32_t* __restrict__ n_
   }
 }
 
-__global__ void __launch_bounds__(kCmpBlock) k_cmp_scan(int64_t nblocks, long long* block_sums, long long* totals) {
+__global__ void __launch_bounds__(kCmpBlock) k_cmp_scan(int64_t nblocks, long long* block_sums, long long* totals,
+                                                        const long long* __restrict__ carry_in) {
   // exclusive scan of the per-block (candidates, tokens) sums, one block, kCmpBlock at a time
   using BS = cub::BlockScan<long long, kCmpBlock>;
   __shared__ typename BS::TempStorage tmp;
   __shared__ long long carry[2];
-  if (threadIdx.x == 0) carry[0] = carry[1] = 0;
+  if (threadIdx.x == 0) {
+    carry[0] = carry_in ? carry_in[0] : 0;
+    carry[1] = carry_in ? carry_in[1] : 0;
+  }
   __syncthreads();
   for (int64_t b0 = 0; b0 < nblocks; b0 += kCmpBlock) {
     const int64_t b = b0 + threadIdx.x;
@@ -1412,19 +1416,30 @@ __global__ void k_cmp_scatter(int64_t n, int32_t K, int32_t S, const int32_t* __
 }
 
 // Device -> (mapped) host copy of regions whose sizes are only known on the device:
-// region r holds totals[idx] elements of elem_bytes. Coalesced 16-B stores (PCIe-friendly).
+// 4-B head up to 16-B alignment, coalesced 16-B body (PCIe-friendly), 4-B tail.
 __global__ void k_copy_out(const long long* __restrict__ totals, CopyOutRegions R) {
   const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int64_t nth = static_cast<int64_t>(gridDim.x) * blockDim.x;
   for (int r = 0; r < R.n; ++r) {
-    const int64_t bytes = R.total_idx[r] < 0 ? R.fixed_bytes[r] : totals[R.total_idx[r]] * R.elem_bytes[r];
-    const int64_t n16 = bytes / 16;
-    const uint4* src = reinterpret_cast<const uint4*>(R.src[r]);
-    uint4* dst = reinterpret_cast<uint4*>(R.dst[r]);
-    for (int64_t i = tid; i < n16; i += nth) dst[i] = src[i];
-    const int64_t tail = bytes - n16 * 16;  // multiple of 4
-    if (tid < tail / 4)
-      reinterpret_cast<uint32_t*>(R.dst[r] + n16 * 16)[tid] = reinterpret_cast<const uint32_t*>(R.src[r] + n16 * 16)[tid];
+    int64_t b0 = 0, b1 = R.fixed_bytes[r];
+    if (R.total_idx[r] >= 0) {
+      b1 = totals[R.total_idx[r]] * R.elem_bytes[r];
+      if (R.begin_idx[r] >= 0) b0 = totals[R.begin_idx[r]] * R.elem_bytes[r];
+    }
+    if (b1 <= b0) continue;
+    const char* src = R.src[r];
+    char* dst = R.dst[r];
+    const int64_t mis = static_cast<int64_t>((reinterpret_cast<uintptr_t>(src) + b0) & 15);
+    const int64_t a0 = b0 + ((16 - mis) & 15) < b1 ? b0 + ((16 - mis) & 15) : b1;
+    const int64_t body = (b1 - a0) & ~int64_t{15};
+    const int64_t a1 = a0 + body;
+    if (tid < (a0 - b0) / 4)
+      reinterpret_cast<uint32_t*>(dst + b0)[tid] = reinterpret_cast<const uint32_t*>(src + b0)[tid];
+    const uint4* s16 = reinterpret_cast<const uint4*>(src + a0);
+    uint4* d16 = reinterpret_cast<uint4*>(dst + a0);
+    for (int64_t i = tid; i < body / 16; i += nth) d16[i] = s16[i];
+    if (tid < (b1 - a1) / 4)
+      reinterpret_cast<uint32_t*>(dst + a1)[tid] = reinterpret_cast<const uint32_t*>(src + a1)[tid];
   }
 }
 
@@ -1433,11 +1448,11 @@ __global__ void k_copy_out(const long long* __restrict__ totals, CopyOutRegions 
 cudaError_t launch_compact(int64_t n, int32_t K, int32_t S, const int32_t* n_cands, const int32_t* lens,
                            const double* scores, const int64_t* supports, const int32_t* tokens,
                            long long* block_sums, long long* totals, CandMeta* meta, int32_t* tok_out,
-                           int64_t* cand_off, int64_t* tok_off, cudaStream_t st) {
+                           int64_t* cand_off, int64_t* tok_off, const long long* carry_in, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
   const int64_t nb = (n + kCmpBlock - 1) / kCmpBlock;
   k_cmp_count<<<static_cast<unsigned>(nb), kCmpBlock, 0, st>>>(n, K, n_cands, lens, block_sums);
-  k_cmp_scan<<<1, kCmpBlock, 0, st>>>(nb, block_sums, totals);
+  k_cmp_scan<<<1, kCmpBlock, 0, st>>>(nb, block_sums, totals, carry_in);
   k_cmp_scatter<<<static_cast<unsigned>(nb), kCmpBlock, 0, st>>>(n, K, S, n_cands, lens, scores, supports, tokens,
                                                                   block_sums, meta, tok_out, cand_off, tok_off);
   return cudaGetLastError();

@@ -151,27 +151,29 @@ struct CandMeta {
   int32_t len;
   int32_t pad;
 };
-constexpr int kMaxCopyRegions = 6;
+constexpr int kMaxCopyRegions = 8;
 struct CopyOutRegions {
   int32_t n;
   int32_t total_idx[kMaxCopyRegions];   // < 0: fixed size fixed_bytes[r]
+  int32_t begin_idx[kMaxCopyRegions];   // >= 0 (sized regions): start at element totals[begin_idx[r]]
   int32_t elem_bytes[kMaxCopyRegions];
   int64_t fixed_bytes[kMaxCopyRegions];
-  const char* src[kMaxCopyRegions];  // 16-B aligned
-  char* dst[kMaxCopyRegions];        // 16-B aligned; typically mapped pinned host memory
+  const char* src[kMaxCopyRegions];  // src[r] and dst[r] congruent mod 16
+  char* dst[kMaxCopyRegions];        // typically mapped pinned host memory
 };
-// Copies region r = totals[total_idx[r]] * elem_bytes[r] (or fixed_bytes[r]) bytes, a multiple
-// of 4; max_bytes sizes the grid.
+// Copies bytes [b0, b1) of region r: b1 = totals[total_idx[r]] * elem_bytes[r] (b0 from begin_idx)
+// or [0, fixed_bytes[r]); sizes are multiples of 4. max_bytes sizes the grid.
 cudaError_t launch_copy_out(const long long* totals, const CopyOutRegions& R, int64_t max_bytes, cudaStream_t st,
                             int max_blocks = 592);
 
-// block_sums: 2 * ceil(n / 256) scratch; totals[0] = candidates, totals[1] = tokens.
-// Outputs may live in mapped pinned host memory (written over PCIe by the kernel).
+// block_sums: 2 * ceil(n / 256) scratch; totals[0] = candidates, totals[1] = tokens, both
+// counted from carry_in (optional: the totals of an earlier chunk, so chunks of one batch
+// compact into one CSR). Outputs may live in mapped pinned host memory.
 // cand_off[q] (optional) = first candidate of query q; tok_off[c] (optional) = first token of c.
 cudaError_t launch_compact(int64_t n, int32_t K, int32_t S, const int32_t* n_cands, const int32_t* lens,
                            const double* scores, const int64_t* supports, const int32_t* tokens,
                            long long* block_sums, long long* totals, CandMeta* meta, int32_t* tok_out,
-                           int64_t* cand_off, int64_t* tok_off, cudaStream_t st);
+                           int64_t* cand_off, int64_t* tok_off, const long long* carry_in, cudaStream_t st);
 
 cudaError_t launch_route_pack(int64_t n, int32_t world, const int32_t* owner, const uint32_t* records,
                               int32_t rec_words, uint32_t* out, int64_t* counts, int64_t* perm, void* scratch,

@@ -307,6 +307,9 @@ void nt_copy(void* dst, const void* src, size_t n) {
 
 }  // namespace
 
+struct dgds_server;
+static void free_plan_pool(dgds_server* s);  // after dgds_update_plan is complete
+
 struct dgds_server {
   dgds_params p{};
   int32_t D = 0;
@@ -315,7 +318,28 @@ struct dgds_server {
   // host-path query inputs: own staging pair and copy stream, so their H2D overlaps the
   // append kernel queued before them on `st`
   cudaStream_t copy_st = nullptr;
-  cudaEvent_t q_staging_free = nullptr, q_h2d_done = nullptr;
+  // Host-path query batches in flight (dgds_speculate_submit / _wait): each owns a slot with
+  // its staging, device outputs and mapped result block, so the next batch is staged while
+  // this one runs. Copy-outs run on out_st, beside the next batch's append and query kernels.
+  static constexpr int kQSlots = 2;
+  struct QSlot {
+    PinnedBuf hq, ho;  // mapped: the pull kernel reads hq, the copy-out kernel writes ho
+    DevBuf dq, dout;
+    cudaEvent_t done = nullptr;  // the batch's last copy-out finished
+    uint64_t ticket = 0;         // 0: never used
+    int64_t n = 0;
+    bool verify = false;
+    size_t h_coff = 0, h_v = 0, h_meta = 0, h_toff = 0, h_tok = 0;
+  } qslot[kQSlots];
+  uint64_t last_ticket = 0;
+  cudaStream_t out_st = nullptr;
+  // optional chunking of one batch (DGDS_Q_CHUNKS, batches of >= 32K queries): chunk c's H2D
+  // beside chunk c+1's staging, its copy-out beside chunk c+1's query kernel. Off by default:
+  // the query kernel's fixed latency tail makes 4 x 16K queries slower than 1 x 64K.
+  static constexpr int kMaxQChunks = 16;
+  cudaEvent_t ev_h2d[kMaxQChunks] = {}, ev_cmp[kMaxQChunks] = {};
+  int q_chunks = 1;
+  int out_blocks = 148;  // copy-out grid when chunked; DGDS_OUT_BLOCKS
   dgds::DevTrie T{};
   unsigned long long* d_used = nullptr;
   uint64_t used_ub = 0;  // upper bound on occupied slots since the last exact read
@@ -340,10 +364,8 @@ struct dgds_server {
   std::vector<uint64_t> shard_counts;
   uint64_t batch_stamp = 0;
 
-  PinnedBuf h_stage, h_out;  // h_out is mapped: the copy-out kernel stores results into it
+  PinnedBuf h_stage, h_out;  // update staging; dgds_verify_batch results
   DevBuf d_stage, d_out;
-  PinnedBuf hq_stage;  // mapped: the copy-in kernel reads it over PCIe
-  DevBuf dq_stage;
   bool h2d_kernel = false;  // copy-engine H2D (no SMs taken from K1); DGDS_H2D=kernel: a pull kernel
   int h2d_blocks = 148;    // one CTA per SM (measured best); DGDS_H2D_BLOCKS
   std::unique_ptr<WorkerPool> pool;
@@ -845,8 +867,7 @@ int dgds_create(const dgds_params* params, dgds_server** out) {
   DGDS_CUDA(cudaSetDevice(p.device));
   auto s = std::make_unique<dgds_server>();
   s->p = p;
-  s->h_out.flags = cudaHostAllocMapped;
-  s->hq_stage.flags = cudaHostAllocMapped;
+  for (auto& q : s->qslot) q.hq.flags = q.ho.flags = cudaHostAllocMapped;
   if (const char* e = std::getenv("DGDS_H2D")) s->h2d_kernel = std::strcmp(e, "kernel") == 0;
   cudaDeviceGetAttribute(&s->h2d_blocks, cudaDevAttrMultiProcessorCount, p.device);
   if (const char* e = std::getenv("DGDS_H2D_BLOCKS")) s->h2d_blocks = std::max(1, std::atoi(e));
@@ -855,8 +876,16 @@ int dgds_create(const dgds_params* params, dgds_server** out) {
   DGDS_CUDA(cudaStreamCreateWithFlags(&s->st, cudaStreamNonBlocking));
   DGDS_CUDA(cudaEventCreateWithFlags(&s->staging_free, cudaEventDisableTiming));
   DGDS_CUDA(cudaStreamCreateWithFlags(&s->copy_st, cudaStreamNonBlocking));
-  DGDS_CUDA(cudaEventCreateWithFlags(&s->q_staging_free, cudaEventDisableTiming));
-  DGDS_CUDA(cudaEventCreateWithFlags(&s->q_h2d_done, cudaEventDisableTiming));
+  DGDS_CUDA(cudaStreamCreateWithFlags(&s->out_st, cudaStreamNonBlocking));
+  for (auto& q : s->qslot) DGDS_CUDA(cudaEventCreateWithFlags(&q.done, cudaEventDisableTiming));
+  for (int c = 0; c < dgds_server::kMaxQChunks; ++c) {
+    DGDS_CUDA(cudaEventCreateWithFlags(&s->ev_h2d[c], cudaEventDisableTiming));
+    DGDS_CUDA(cudaEventCreateWithFlags(&s->ev_cmp[c], cudaEventDisableTiming));
+  }
+  if (const char* e = std::getenv("DGDS_Q_CHUNKS"))
+    s->q_chunks = std::min(dgds_server::kMaxQChunks, std::max(1, std::atoi(e)));
+  s->out_blocks = s->h2d_blocks;
+  if (const char* e = std::getenv("DGDS_OUT_BLOCKS")) s->out_blocks = std::max(1, std::atoi(e));
   const uint64_t nodes = p.expected_nodes ? p.expected_nodes : (1ull << 20);
   double init_load = 0.35;  // expected_nodes is an upper bound, so the real load starts lower
   if (const char* e = std::getenv("DGDS_INIT_LOAD")) init_load = std::min(0.9, std::max(0.05, std::atof(e)));
@@ -909,11 +938,16 @@ int dgds_destroy(dgds_server* s) {
   cudaFree(s->d_err);
   cudaFree(s->d_stat_part);
   cudaFree(s->d_hist);
-  for (auto* pl : s->plan_pool) delete pl;
+  free_plan_pool(s);
   if (s->staging_free) cudaEventDestroy(s->staging_free);
-  if (s->q_staging_free) cudaEventDestroy(s->q_staging_free);
-  if (s->q_h2d_done) cudaEventDestroy(s->q_h2d_done);
+  for (auto& q : s->qslot)
+    if (q.done) cudaEventDestroy(q.done);
   if (s->copy_st) cudaStreamDestroy(s->copy_st);
+  for (int c = 0; c < dgds_server::kMaxQChunks; ++c) {
+    if (s->ev_h2d[c]) cudaEventDestroy(s->ev_h2d[c]);
+    if (s->ev_cmp[c]) cudaEventDestroy(s->ev_cmp[c]);
+  }
+  if (s->out_st) cudaStreamDestroy(s->out_st);
   for (auto e : s->ev_pool) cudaEventDestroy(e);
   for (auto& v : s->ev_pending)
     for (auto& pr : v) {
@@ -1040,8 +1074,11 @@ static int update_batch_locked(dgds_server* s, int64_t n, const int32_t* handles
   PhaseClock pc("update_batch");
   DGDS_CUDA(cudaSetDevice(s->p.device));
   const uint64_t ntok = offs[n] - offs[0];
-  for (uint64_t i = offs[0]; i < offs[n]; ++i)
-    if (tokens[i] < 0) return fail(DGDS_EINVAL, "negative token");
+  {
+    int32_t any = 0;  // branch-free sign scan (vectorised)
+    for (uint64_t i = offs[0]; i < offs[n]; ++i) any |= tokens[i];
+    if (any < 0) return fail(DGDS_EINVAL, "negative token");
+  }
   std::vector<dgds::AppendSeg>& segs = s->scratch.segs;
   std::vector<dgds::AppendPiece>& pieces = s->scratch.pieces;
   uint64_t worst = 0;
@@ -1098,6 +1135,11 @@ struct dgds_update_plan {
   const int32_t* d_tokens = nullptr;
   uint64_t seq = 0;
 };
+
+static void free_plan_pool(dgds_server* s) {
+  for (auto* pl : s->plan_pool) delete pl;
+  s->plan_pool.clear();
+}
 
 // Host half: validation, bookkeeping (replies, versions, history log), capacity. Plans must be
 // launched in the order they were made (K1 of a later plan reads the stream rows K1 of an
@@ -1315,8 +1357,8 @@ int dgds_copy_rows_d2h(void* h_dst, int64_t dst_pitch, const void* d_src, int64_
 
 namespace {
 
-// One host-buffer query batch: its results live in the mapped pinned block s->h_out
-// (valid until the next host-path call on the server).
+// One host-buffer query batch: its results live in the mapped pinned block of its slot
+// (valid until the batch submitted kQSlots later reuses the slot).
 struct HostResult {
   int64_t n = 0, ncand = 0, ntok = 0;
   const int64_t* cand_off = nullptr;  // [n + 1]
@@ -1327,13 +1369,13 @@ struct HostResult {
 };
 
 // Validate + stage (in parallel on the worker pool), H2D, K2 (+ fused K3), compaction into
-// device memory, one copy-out kernel into the mapped host block, one stream sync.
-// Caller holds s->mu. Nothing is launched unless the whole batch validates.
-int speculate_host(dgds_server* s, int64_t n, const int32_t* handles, const uint64_t* pat_offs,
-                   const int32_t* patterns, const dgds_spec_args* args, int64_t args_stride, const int32_t* truth,
-                   int32_t truth_stride, const int32_t* truth_left, const int32_t* limit, bool verify,
-                   HostResult* r) {
-  PhaseClock pc("speculate_host");
+// device memory, one copy-out kernel into the slot's mapped host block; returns without
+// waiting. Caller holds s->mu. Nothing is launched unless the whole batch validates.
+int speculate_submit(dgds_server* s, int64_t n, const int32_t* handles, const uint64_t* pat_offs,
+                     const int32_t* patterns, const dgds_spec_args* args, int64_t args_stride, const int32_t* truth,
+                     int32_t truth_stride, const int32_t* truth_left, const int32_t* limit, bool verify,
+                     uint64_t* ticket) {
+  PhaseClock pc("speculate_submit");
   const int64_t nargs = args_stride ? n : 1;
   int32_t max_k = 1, max_s = 1;
   for (int64_t i = 0; i < nargs; ++i) {
@@ -1345,61 +1387,110 @@ int speculate_host(dgds_server* s, int64_t n, const int32_t* handles, const uint
   if (verify && (!truth || !truth_left || !limit || truth_stride < 0))
     return fail(DGDS_EINVAL, "verify needs truth inputs");
   const int32_t P = s->p.max_pattern_len;  // only the last max_pattern_len tokens can matter
-  // staging: handles | pat_len | patterns | args | truth | truth_left | limit
-  const size_t o_len = align_up(n * 4, 256);
-  const size_t o_pat = align_up(o_len + n * 4, 256);
-  const size_t o_args = align_up(o_pat + static_cast<size_t>(n) * P * 4, 256);
-  const size_t o_tr = align_up(o_args + nargs * sizeof(dgds_spec_args), 256);
-  const size_t o_tl = align_up(o_tr + (verify ? static_cast<size_t>(n) * truth_stride * 4 : 0), 256);
-  const size_t o_lm = align_up(o_tl + (verify ? n * 4 : 0), 256);
-  const size_t in_all = o_lm + (verify ? n * 4 : 0);
-  DGDS_CUDA(cudaEventSynchronize(s->q_staging_free));
-  pc.mark("staging_wait");
-  if (int rc = s->hq_stage.ensure(align_up(in_all, 16))) return rc;  // the copy-in kernel moves 16-B units
-  if (int rc = s->dq_stage.ensure(align_up(in_all, 16))) return rc;
-  char* h = static_cast<char*>(s->hq_stage.p);
-  int32_t* hl = reinterpret_cast<int32_t*>(h + o_len);
-  int32_t* hp = reinterpret_cast<int32_t*>(h + o_pat);
+  // Chunks of the batch are staged, copied in and queried in order. Chunk c's H2D runs while
+  // chunk c+1 is staged, and chunk c's copy-out (PCIe-bound, out_st) while chunk c+1 is queried.
+  // The query kernels are launched only after the whole batch validated.
+  int nch = n >= 32768 ? s->q_chunks : 1;
+  const int64_t per = static_cast<int64_t>(align_up((n + nch - 1) / nch, 256));
+  nch = static_cast<int>((n + per - 1) / per);
+  // per-chunk input block: handles | pat_len | patterns | args | truth | truth_left | limit
+  struct InBlock {
+    int64_t q0, m;
+    size_t base, o_len, o_pat, o_args, o_tr, o_tl, o_lm, bytes;
+  };
+  InBlock blk[dgds_server::kMaxQChunks];
+  size_t in_all = 0;
+  for (int c = 0; c < nch; ++c) {
+    InBlock& b = blk[c];
+    b.q0 = c * per;
+    b.m = std::min<int64_t>(per, n - b.q0);
+    b.base = in_all;
+    b.o_len = align_up(b.m * 4, 256);
+    b.o_pat = align_up(b.o_len + b.m * 4, 256);
+    b.o_args = align_up(b.o_pat + static_cast<size_t>(b.m) * P * 4, 256);
+    b.o_tr = align_up(b.o_args + (args_stride ? b.m : 1) * sizeof(dgds_spec_args), 256);
+    b.o_tl = align_up(b.o_tr + (verify ? static_cast<size_t>(b.m) * truth_stride * 4 : 0), 256);
+    b.o_lm = align_up(b.o_tl + (verify ? b.m * 4 : 0), 256);
+    b.bytes = align_up(b.o_lm + (verify ? b.m * 4 : 0), 16);  // the copy-in kernel moves 16-B units
+    in_all = align_up(b.base + b.bytes, 256);
+  }
+  const uint64_t tk = s->last_ticket + 1;
+  dgds_server::QSlot& slot = s->qslot[tk % dgds_server::kQSlots];
+  DGDS_CUDA(cudaEventSynchronize(slot.done));  // the slot's previous batch is complete
+  slot.ticket = 0;  // its results are gone from here on
+  pc.mark("slot_wait");
+  if (int rc = slot.hq.ensure(in_all)) return rc;
+  if (int rc = slot.dq.ensure(in_all)) return rc;
+  char* h = static_cast<char*>(slot.hq.p);
+  char* d = static_cast<char*>(slot.dq.p);
   const size_t ngroups = s->groups.size();
   WorkerPool& pool = s->workers();
-  const int tasks = n >= 8192 ? 4 * pool.threads() : 1;
-  const int64_t chunk = (n + tasks - 1) / tasks;
-  std::vector<int64_t> bad(tasks, -1);  // first invalid query of each chunk
-  pool.run(tasks, [&](int t) {
-    const int64_t q0 = t * chunk, q1 = std::min<int64_t>(n, q0 + chunk);
-    if (q0 >= q1) return;
-    thread_local std::vector<int32_t> lens, rows;  // built in cache, then streamed out
-    lens.resize(q1 - q0);
-    rows.assign(static_cast<size_t>(q1 - q0) * P, 0);
-    for (int64_t i = q0; i < q1; ++i) {
-      const int32_t hd = handles[i];
-      if ((hd < 0 || static_cast<size_t>(hd) >= ngroups || pat_offs[i + 1] < pat_offs[i]) && bad[t] < 0) bad[t] = i;
-      const uint64_t L = pat_offs[i + 1] - pat_offs[i];
-      lens[i - q0] = static_cast<int32_t>(std::min<uint64_t>(L, 0x7FFFFFFF));
-      const uint64_t keep = std::min<uint64_t>(L, static_cast<uint64_t>(P));
-      const int32_t* src = patterns + pat_offs[i + 1] - keep;
-      int32_t* dst = rows.data() + (i - q0) * P;
-      for (uint64_t k = 0; k < keep; ++k) dst[k] = src[k];
+  const int tasks = n >= 8192 ? std::max(1, 4 * pool.threads() / nch) : 1;
+  std::vector<int64_t> bad(tasks, -1);  // first invalid query of each task
+  for (int c = 0; c < nch; ++c) {
+    const InBlock& b = blk[c];
+    char* hb = h + b.base;
+    int32_t* hl = reinterpret_cast<int32_t*>(hb + b.o_len);
+    int32_t* hp = reinterpret_cast<int32_t*>(hb + b.o_pat);
+    const int64_t chunk = (b.m + tasks - 1) / tasks;
+    std::fill(bad.begin(), bad.end(), -1);
+    pool.run(tasks, [&](int t) {
+      const int64_t j0 = t * chunk, j1 = std::min<int64_t>(b.m, j0 + chunk);  // chunk-relative
+      if (j0 >= j1) return;
+      const int64_t q0 = b.q0 + j0;
+      thread_local std::vector<int32_t> lens, rows;  // built in cache, then streamed out
+      lens.resize(j1 - j0);
+      rows.assign(static_cast<size_t>(j1 - j0) * P, 0);
+      for (int64_t j = j0; j < j1; ++j) {
+        const int64_t i = b.q0 + j;
+        const int32_t hd = handles[i];
+        if ((hd < 0 || static_cast<size_t>(hd) >= ngroups || pat_offs[i + 1] < pat_offs[i]) && bad[t] < 0) bad[t] = i;
+        const uint64_t L = pat_offs[i + 1] - pat_offs[i];
+        lens[j - j0] = static_cast<int32_t>(std::min<uint64_t>(L, 0x7FFFFFFF));
+        const uint64_t keep = std::min<uint64_t>(L, static_cast<uint64_t>(P));
+        const int32_t* src = patterns + pat_offs[i + 1] - keep;
+        int32_t* dst = rows.data() + (j - j0) * P;
+        for (uint64_t k = 0; k < keep; ++k) dst[k] = src[k];
+      }
+      nt_copy(hl + j0, lens.data(), (j1 - j0) * 4);
+      nt_copy(hp + j0 * P, rows.data(), rows.size() * 4);
+      nt_copy(hb + j0 * 4, handles + q0, (j1 - j0) * 4);
+      if (verify) {
+        nt_copy(hb + b.o_tr + static_cast<size_t>(j0) * truth_stride * 4, truth + q0 * truth_stride,
+                static_cast<size_t>(j1 - j0) * truth_stride * 4);
+        nt_copy(hb + b.o_tl + j0 * 4, truth_left + q0, (j1 - j0) * 4);
+        nt_copy(hb + b.o_lm + j0 * 4, limit + q0, (j1 - j0) * 4);
+      }
+      _mm_sfence();  // streaming stores globally visible before the copy is issued
+    });
+    auto* ha = reinterpret_cast<dgds_spec_args*>(hb + b.o_args);
+    if (!args_stride) ha[0] = args[0];
+    else
+      for (int64_t j = 0; j < b.m; ++j) ha[j] = args[(b.q0 + j) * args_stride];
+    for (int t = 0; t < tasks; ++t) {
+      if (bad[t] >= 0) {
+        DGDS_CUDA(cudaEventRecord(slot.done, s->copy_st));  // chunks already in flight read hq
+        const int64_t i = bad[t];
+        if (int rc = check_handle(s, handles[i])) return rc;
+        return fail(DGDS_EINVAL, "pattern offsets must be nondecreasing");
+      }
     }
-    nt_copy(hl + q0, lens.data(), (q1 - q0) * 4);
-    nt_copy(hp + q0 * P, rows.data(), rows.size() * 4);
-    nt_copy(h + q0 * 4, handles + q0, (q1 - q0) * 4);
-    if (verify) {
-      nt_copy(h + o_tr + static_cast<size_t>(q0) * truth_stride * 4, truth + q0 * truth_stride,
-              static_cast<size_t>(q1 - q0) * truth_stride * 4);
-      nt_copy(h + o_tl + q0 * 4, truth_left + q0, (q1 - q0) * 4);
-      nt_copy(h + o_lm + q0 * 4, limit + q0, (q1 - q0) * 4);
+    // the copy stream runs the H2D under the append kernel already queued on st
+    if (s->h2d_kernel) {  // the GPU pulls the mapped staging block
+      dgds::CopyOutRegions Rin{};
+      Rin.n = 1;
+      Rin.total_idx[0] = -1;
+      Rin.begin_idx[0] = -1;
+      Rin.fixed_bytes[0] = static_cast<int64_t>(b.bytes);
+      Rin.src[0] = hb;
+      Rin.dst[0] = d + b.base;
+      // a narrow grid: enough reads in flight for PCIe, SMs left to the append kernel running beside it
+      DGDS_CUDA(dgds::launch_copy_out(nullptr, Rin, Rin.fixed_bytes[0], s->copy_st, s->h2d_blocks));
+    } else {
+      DGDS_CUDA(cudaMemcpyAsync(d + b.base, hb, b.bytes, cudaMemcpyHostToDevice, s->copy_st));
     }
-    _mm_sfence();  // streaming stores globally visible before the copy is issued
-  });
-  for (int t = 0; t < tasks; ++t) {
-    if (bad[t] >= 0) {
-      const int64_t i = bad[t];
-      if (int rc = check_handle(s, handles[i])) return rc;
-      return fail(DGDS_EINVAL, "pattern offsets must be nondecreasing");
-    }
+    DGDS_CUDA(cudaEventRecord(s->ev_h2d[c], s->copy_st));
   }
-  std::memcpy(h + o_args, args, nargs * sizeof(dgds_spec_args));
   pc.mark("validate_stage");
   // device outputs (internal strides) + compaction scratch
   const int32_t K = max_k, Sx = max_s;
@@ -1410,117 +1501,146 @@ int speculate_host(dgds_server* s, int64_t n, const int32_t* handles, const uint
   const size_t o_ln = align_up(o_nc + n * 4, 256);
   const size_t o_tk = align_up(o_ln + nk * 4, 256);
   const size_t o_v = align_up(o_tk + static_cast<size_t>(nk) * Sx * 4, 256);
-  const int64_t nblk = (n + 255) / 256;
+  const int64_t nblk = (per + 255) / 256;
   const size_t o_bs = align_up(o_v + (verify ? static_cast<size_t>(n) * 12 : 0), 256);
-  const size_t o_cmeta = align_up(o_bs + static_cast<size_t>(nblk) * 16 + 16, 256);
+  const size_t o_tot = align_up(o_bs + static_cast<size_t>(nblk) * 16, 256);
+  const size_t o_cmeta = align_up(o_tot + static_cast<size_t>(nch) * 16, 256);
   const size_t o_ctoff = align_up(o_cmeta + nk * sizeof(dgds::CandMeta), 256);
   const size_t o_ccoff = align_up(o_ctoff + nk * 8, 256);
   const size_t o_ctok = align_up(o_ccoff + (n + 1) * 8, 256);
   const size_t dev_total = o_ctok + static_cast<size_t>(nk) * Sx * 4;
-  if (int rc = s->d_out.ensure(dev_total)) return rc;
+  if (int rc = slot.dout.ensure(dev_total)) return rc;
   // mapped host block: totals | cand_off | verify | meta | tok_off | tokens
   const size_t h_coff = 256;
   const size_t h_v = align_up(h_coff + (n + 1) * 8, 256);
   const size_t h_meta = align_up(h_v + (verify ? n * 12 : 0), 256);
   const size_t h_toff = align_up(h_meta + nk * sizeof(dgds::CandMeta), 256);
   const size_t h_tok = align_up(h_toff + (nk + 1) * 8, 256);
-  if (int rc = s->h_out.ensure(h_tok + static_cast<size_t>(nk) * Sx * 4)) return rc;
-  char* d = static_cast<char*>(s->dq_stage.p);
-  char* dout = static_cast<char*>(s->d_out.p);
-  char* ho = static_cast<char*>(s->h_out.p);
-  // the copy stream runs the H2D under the append kernel already queued on st; the query
-  // kernel waits for both (dq_stage is free: the previous query call synchronised)
-  if (s->h2d_kernel) {  // the GPU pulls the mapped staging block (steadier than the copy engine here)
-    dgds::CopyOutRegions Rin{};
-    Rin.n = 1;
-    Rin.total_idx[0] = -1;
-    Rin.fixed_bytes[0] = static_cast<int64_t>(align_up(in_all, 16));
-    Rin.src[0] = h;
-    Rin.dst[0] = d;
-    // a narrow grid: enough reads in flight for PCIe, SMs left to the append kernel running beside it
-    DGDS_CUDA(dgds::launch_copy_out(nullptr, Rin, Rin.fixed_bytes[0], s->copy_st, s->h2d_blocks));
-  } else {
-    DGDS_CUDA(cudaMemcpyAsync(d, h, in_all, cudaMemcpyHostToDevice, s->copy_st));
-  }
-  DGDS_CUDA(cudaEventRecord(s->q_staging_free, s->copy_st));
-  DGDS_CUDA(cudaEventRecord(s->q_h2d_done, s->copy_st));
-  DGDS_CUDA(cudaStreamWaitEvent(s->st, s->q_h2d_done, 0));
-  dgds::QueryLaunch L{};
-  L.T = s->T;
-  L.root_of = s->d_root_of;
-  L.n_handles = static_cast<int32_t>(s->root_of_cap);
-  L.n = n;
-  L.handles = reinterpret_cast<const int32_t*>(d);
-  L.pat_len = reinterpret_cast<const int32_t*>(d + o_len);
-  L.patterns = reinterpret_cast<const int32_t*>(d + o_pat);
-  L.pat_stride = P;
-  L.args = reinterpret_cast<const dgds_spec_args*>(d + o_args);
-  L.args_stride = args_stride ? 1 : 0;
-  L.k_stride = K;
-  L.s_stride = Sx;
-  dgds::soa_strides(L);
-  L.scores = reinterpret_cast<double*>(dout + o_sc);
-  L.supports = reinterpret_cast<int64_t*>(dout + o_sp);
-  L.n_cands = reinterpret_cast<int32_t*>(dout + o_nc);
-  L.lens = reinterpret_cast<int32_t*>(dout + o_ln);
-  L.tokens = reinterpret_cast<int32_t*>(dout + o_tk);
-  L.err_flag = s->d_err;
-  L.stat_part = s->d_stat_part;
-  if (verify) {
-    L.truth = reinterpret_cast<const int32_t*>(d + o_tr);
-    L.truth_stride = truth_stride;
-    L.truth_left = reinterpret_cast<const int32_t*>(d + o_tl);
-    L.limit = reinterpret_cast<const int32_t*>(d + o_lm);
-    L.v_drafted = reinterpret_cast<int32_t*>(dout + o_v);
-    L.v_accepted = L.v_drafted + n;
-    L.v_emitted = L.v_drafted + 2 * n;
-  }
-  {
-    LaunchTimer lt(s, 1, s->st);
-    DGDS_CUDA(dgds::launch_query(L, max_k, max_s, s->st));
-  }
+  if (int rc = slot.ho.ensure(h_tok + static_cast<size_t>(nk) * Sx * 4)) return rc;
+  char* dout = static_cast<char*>(slot.dout.p);
+  char* ho = static_cast<char*>(slot.ho.p);
   long long* d_bs = reinterpret_cast<long long*>(dout + o_bs);
-  long long* d_tot = d_bs + 2 * nblk;
+  long long* d_tot = reinterpret_cast<long long*>(dout + o_tot);  // [chunk][candidates, tokens], cumulative
   auto* d_meta = reinterpret_cast<dgds::CandMeta*>(dout + o_cmeta);
   auto* d_toff = reinterpret_cast<int64_t*>(dout + o_ctoff);
   auto* d_coff = reinterpret_cast<int64_t*>(dout + o_ccoff);
   int32_t* d_ctok = reinterpret_cast<int32_t*>(dout + o_ctok);
-  DGDS_CUDA(dgds::launch_compact(n, K, Sx, L.n_cands, L.lens, L.scores, L.supports, L.tokens, d_bs, d_tot, d_meta,
-                                 d_ctok, d_coff, d_toff, s->st));
-  dgds::CopyOutRegions R{};
-  auto region = [&](const void* src, size_t dst_off, int idx, int elem, int64_t fixed) {
-    const int i = R.n++;
-    R.src[i] = static_cast<const char*>(src);
-    R.dst[i] = ho + dst_off;
-    R.total_idx[i] = idx;
-    R.elem_bytes[i] = elem;
-    R.fixed_bytes[i] = fixed;
-  };
-  region(d_tot, 0, -1, 0, 16);
-  region(d_coff, h_coff, -1, 0, n * 8);
-  if (verify) region(dout + o_v, h_v, -1, 0, n * 12);
-  region(d_meta, h_meta, 0, sizeof(dgds::CandMeta), 0);
-  region(d_toff, h_toff, 0, 8, 0);
-  region(d_ctok, h_tok, 1, 4, 0);
-  DGDS_CUDA(dgds::launch_copy_out(d_tot, R, static_cast<int64_t>(nk) * (sizeof(dgds::CandMeta) + 8 + Sx * 4),
-                                  s->st));
+  for (int c = 0; c < nch; ++c) {
+    const InBlock& b = blk[c];
+    const char* db = d + b.base;
+    const int64_t q0 = b.q0, m = b.m;
+    DGDS_CUDA(cudaStreamWaitEvent(s->st, s->ev_h2d[c], 0));
+    dgds::QueryLaunch L{};
+    L.T = s->T;
+    L.root_of = s->d_root_of;
+    L.n_handles = static_cast<int32_t>(s->root_of_cap);
+    L.n = m;
+    L.handles = reinterpret_cast<const int32_t*>(db);
+    L.pat_len = reinterpret_cast<const int32_t*>(db + b.o_len);
+    L.patterns = reinterpret_cast<const int32_t*>(db + b.o_pat);
+    L.pat_stride = P;
+    L.args = reinterpret_cast<const dgds_spec_args*>(db + b.o_args);
+    L.args_stride = args_stride ? 1 : 0;
+    L.k_stride = K;
+    L.s_stride = Sx;
+    dgds::soa_strides(L);
+    L.scores = reinterpret_cast<double*>(dout + o_sc) + q0 * K;
+    L.supports = reinterpret_cast<int64_t*>(dout + o_sp) + q0 * K;
+    L.n_cands = reinterpret_cast<int32_t*>(dout + o_nc) + q0;
+    L.lens = reinterpret_cast<int32_t*>(dout + o_ln) + q0 * K;
+    L.tokens = reinterpret_cast<int32_t*>(dout + o_tk) + q0 * K * Sx;
+    L.err_flag = s->d_err;
+    L.stat_part = s->d_stat_part;
+    int32_t* d_v = reinterpret_cast<int32_t*>(dout + o_v);
+    if (verify) {
+      L.truth = reinterpret_cast<const int32_t*>(db + b.o_tr);
+      L.truth_stride = truth_stride;
+      L.truth_left = reinterpret_cast<const int32_t*>(db + b.o_tl);
+      L.limit = reinterpret_cast<const int32_t*>(db + b.o_lm);
+      L.v_drafted = d_v + q0;
+      L.v_accepted = d_v + n + q0;
+      L.v_emitted = d_v + 2 * n + q0;
+    }
+    {
+      LaunchTimer lt(s, 1, s->st);
+      DGDS_CUDA(dgds::launch_query(L, max_k, max_s, s->st));
+    }
+    DGDS_CUDA(dgds::launch_compact(m, K, Sx, L.n_cands, L.lens, L.scores, L.supports, L.tokens, d_bs, d_tot + 2 * c,
+                                   d_meta, d_ctok, d_coff + q0, d_toff, c ? d_tot + 2 * (c - 1) : nullptr, s->st));
+    DGDS_CUDA(cudaEventRecord(s->ev_cmp[c], s->st));
+    DGDS_CUDA(cudaStreamWaitEvent(s->out_st, s->ev_cmp[c], 0));
+    dgds::CopyOutRegions R{};
+    auto region = [&](const void* src, char* dst, int tot, int begin, int elem, int64_t fixed) {
+      const int i = R.n++;
+      R.src[i] = static_cast<const char*>(src);
+      R.dst[i] = dst;
+      R.total_idx[i] = tot;
+      R.begin_idx[i] = begin;
+      R.elem_bytes[i] = elem;
+      R.fixed_bytes[i] = fixed;
+    };
+    const int tc = 2 * c, tb = c ? 2 * (c - 1) : -1;
+    region(d_coff + q0, ho + h_coff + q0 * 8, -1, -1, 0, m * 8);
+    if (verify)
+      for (int k = 0; k < 3; ++k)
+        region(d_v + k * n + q0, ho + h_v + (k * n + q0) * 4, -1, -1, 0, m * 4);
+    region(d_meta, ho + h_meta, tc, tb, sizeof(dgds::CandMeta), 0);
+    region(d_toff, ho + h_toff, tc, tb, 8, 0);
+    region(d_ctok, ho + h_tok, tc + 1, c ? tb + 1 : -1, 4, 0);
+    if (c == nch - 1) region(d_tot + tc, ho, -1, -1, 0, 16);
+    DGDS_CUDA(dgds::launch_copy_out(d_tot, R, m * K * static_cast<int64_t>(sizeof(dgds::CandMeta) + 8 + Sx * 4),
+                                    s->out_st, nch > 1 ? s->out_blocks : 592));
+  }
+  DGDS_CUDA(cudaEventRecord(slot.done, s->out_st));  // after st's work (out_st waited on it)
   pc.mark("launch");
-  DGDS_CUDA(cudaStreamSynchronize(s->st));
-  pc.mark("device_wait");
+  slot.ticket = tk;
+  slot.n = n;
+  slot.verify = verify;
+  slot.h_coff = h_coff;
+  slot.h_v = h_v;
+  slot.h_meta = h_meta;
+  slot.h_toff = h_toff;
+  slot.h_tok = h_tok;
+  s->last_ticket = tk;
+  *ticket = tk;
+  return DGDS_OK;
+}
+
+// Waits for a submitted batch and describes its results. Caller holds s->mu.
+int speculate_finish(dgds_server* s, uint64_t ticket, HostResult* r) {
+  if (ticket == 0 || ticket > s->last_ticket) return fail(DGDS_EINVAL, "unknown query ticket");
+  dgds_server::QSlot& slot = s->qslot[ticket % dgds_server::kQSlots];
+  if (slot.ticket != ticket) return fail(DGDS_EINVAL, "query ticket expired (its result slot was reused)");
+  DGDS_CUDA(cudaEventSynchronize(slot.done));
+  char* ho = static_cast<char*>(slot.ho.p);
+  const int64_t n = slot.n;
   r->n = n;
   r->ncand = reinterpret_cast<const long long*>(ho)[0];
   r->ntok = reinterpret_cast<const long long*>(ho)[1];
-  auto* coff = reinterpret_cast<int64_t*>(ho + h_coff);
-  auto* toff = reinterpret_cast<int64_t*>(ho + h_toff);
+  auto* coff = reinterpret_cast<int64_t*>(ho + slot.h_coff);
+  auto* toff = reinterpret_cast<int64_t*>(ho + slot.h_toff);
   coff[n] = r->ncand;
   toff[r->ncand] = r->ntok;
   r->cand_off = coff;
-  r->meta = reinterpret_cast<const dgds::CandMeta*>(ho + h_meta);
+  r->meta = reinterpret_cast<const dgds::CandMeta*>(ho + slot.h_meta);
   r->tok_off = toff;
-  r->tokens = reinterpret_cast<const int32_t*>(ho + h_tok);
-  r->verify = verify ? reinterpret_cast<const int32_t*>(ho + h_v) : nullptr;
-  s->last_d2h_bytes = 16 + (n + 1) * 8 + (verify ? n * 12 : 0) + r->ncand * (sizeof(dgds::CandMeta) + 8) + r->ntok * 4;
+  r->tokens = reinterpret_cast<const int32_t*>(ho + slot.h_tok);
+  r->verify = slot.verify ? reinterpret_cast<const int32_t*>(ho + slot.h_v) : nullptr;
+  s->last_d2h_bytes =
+      16 + (n + 1) * 8 + (slot.verify ? n * 12 : 0) + r->ncand * (sizeof(dgds::CandMeta) + 8) + r->ntok * 4;
   return DGDS_OK;
+}
+
+int speculate_host(dgds_server* s, int64_t n, const int32_t* handles, const uint64_t* pat_offs,
+                   const int32_t* patterns, const dgds_spec_args* args, int64_t args_stride, const int32_t* truth,
+                   int32_t truth_stride, const int32_t* truth_left, const int32_t* limit, bool verify,
+                   HostResult* r) {
+  uint64_t t = 0;
+  if (int rc = speculate_submit(s, n, handles, pat_offs, patterns, args, args_stride, truth, truth_stride,
+                                truth_left, limit, verify, &t))
+    return rc;
+  PhaseClock pc("speculate_wait");
+  return speculate_finish(s, t, r);
 }
 
 }  // namespace
@@ -1579,6 +1699,25 @@ int dgds_speculate_verify_batch(dgds_server* s, int64_t n, const int32_t* handle
   return DGDS_OK;
 }
 
+}  // extern "C"
+
+static void fill_view(const HostResult& r, dgds_result_view* out) {
+  out->n_queries = r.n;
+  out->n_cands = r.ncand;
+  out->n_tokens = r.ntok;
+  out->cand_off = r.cand_off;
+  out->cands = reinterpret_cast<const dgds_cand_meta*>(r.meta);
+  out->tok_off = r.tok_off;
+  out->tokens = r.tokens;
+  if (r.verify) {
+    out->drafted = r.verify;
+    out->accepted = r.verify + r.n;
+    out->emitted = r.verify + 2 * r.n;
+  }
+}
+
+extern "C" {
+
 int dgds_speculate_verify_view(dgds_server* s, int64_t n, const int32_t* handles, const uint64_t* pat_offs,
                                const int32_t* patterns, const dgds_spec_args* args, int64_t args_stride,
                                const int32_t* truth, int32_t truth_stride, const int32_t* truth_left,
@@ -1593,18 +1732,30 @@ int dgds_speculate_verify_view(dgds_server* s, int64_t n, const int32_t* handles
   if (int rc = speculate_host(s, n, handles, pat_offs, patterns, args, args_stride, truth, truth_stride, truth_left,
                               limit, truth != nullptr, &r))
     return rc;
-  out->n_queries = n;
-  out->n_cands = r.ncand;
-  out->n_tokens = r.ntok;
-  out->cand_off = r.cand_off;
-  out->cands = reinterpret_cast<const dgds_cand_meta*>(r.meta);
-  out->tok_off = r.tok_off;
-  out->tokens = r.tokens;
-  if (r.verify) {
-    out->drafted = r.verify;
-    out->accepted = r.verify + n;
-    out->emitted = r.verify + 2 * n;
-  }
+  fill_view(r, out);
+  return DGDS_OK;
+}
+
+int dgds_speculate_submit(dgds_server* s, int64_t n, const int32_t* handles, const uint64_t* pat_offs,
+                          const int32_t* patterns, const dgds_spec_args* args, int64_t args_stride,
+                          const int32_t* truth, int32_t truth_stride, const int32_t* truth_left,
+                          const int32_t* limit, uint64_t* ticket) {
+  if (!s || !ticket) return fail(DGDS_EINVAL, "null argument");
+  if (n <= 0) return fail(DGDS_EINVAL, "submit needs a non-empty batch");
+  std::lock_guard<std::mutex> lk(s->mu);
+  DGDS_CUDA(cudaSetDevice(s->p.device));
+  return speculate_submit(s, n, handles, pat_offs, patterns, args, args_stride, truth, truth_stride, truth_left,
+                          limit, truth != nullptr, ticket);
+}
+
+int dgds_speculate_wait(dgds_server* s, uint64_t ticket, dgds_result_view* out) {
+  if (!s || !out) return fail(DGDS_EINVAL, "null argument");
+  *out = dgds_result_view{};
+  std::lock_guard<std::mutex> lk(s->mu);
+  DGDS_CUDA(cudaSetDevice(s->p.device));
+  HostResult r;
+  if (int rc = speculate_finish(s, ticket, &r)) return rc;
+  fill_view(r, out);
   return DGDS_OK;
 }
 

@@ -394,6 +394,35 @@ class DraftServer:
                                                    _ptr(args), args_stride, None, 0, None, None, C.byref(v)))
         return ResultView(v)
 
+    def speculate_submit(self, handles: np.ndarray, pat_offsets: np.ndarray, patterns: np.ndarray, args: np.ndarray,
+                         args_stride: int, truth: Optional[np.ndarray] = None,
+                         truth_left: Optional[np.ndarray] = None, limit: Optional[np.ndarray] = None) -> int:
+        """Asynchronous speculate_view (dgds_speculate_submit): stages and launches the batch,
+        returns a ticket for speculate_wait. Two batches can be in flight."""
+        n = len(handles)
+        handles = np.ascontiguousarray(handles, np.int32)
+        pat_offsets = np.ascontiguousarray(pat_offsets, np.uint64)
+        patterns = np.ascontiguousarray(patterns, np.int32)
+        args = np.ascontiguousarray(args, ARGS_DTYPE)
+        t = _lib._U64()
+        if truth is not None:
+            truth = np.ascontiguousarray(truth, np.int32).reshape(n, -1)
+            tl = np.ascontiguousarray(truth_left, np.int32)
+            lm = np.ascontiguousarray(limit, np.int32)
+            check(lib().dgds_speculate_submit(self._h, n, _ptr(handles), _ptr(pat_offsets), _ptr(patterns),
+                                              _ptr(args), args_stride, _ptr(truth), truth.shape[1], _ptr(tl),
+                                              _ptr(lm), C.byref(t)))
+        else:
+            check(lib().dgds_speculate_submit(self._h, n, _ptr(handles), _ptr(pat_offsets), _ptr(patterns),
+                                              _ptr(args), args_stride, None, 0, None, None, C.byref(t)))
+        return int(t.value)
+
+    def speculate_wait(self, ticket: int) -> "ResultView":
+        """Results of a submitted batch (zero-copy views, valid until two batches later)."""
+        v = _lib.ResultView()
+        check(lib().dgds_speculate_wait(self._h, ticket, C.byref(v)))
+        return ResultView(v)
+
     def verify_batch(self, cands: "CandidateBatch", truth: np.ndarray, truth_left: np.ndarray, limit: np.ndarray):
         """Instance::decode_step verification (engine.cpp:115-143) on the GPU."""
         n = cands.n
