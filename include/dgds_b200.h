@@ -282,14 +282,19 @@ int dgds_speculate_verify_view(dgds_server* s, int64_t n, const int32_t* handles
                                const int32_t* truth, int32_t truth_stride, const int32_t* truth_left,
                                const int32_t* limit, dgds_result_view* out);
 
-/* Asynchronous dgds_speculate_verify_view. submit validates and stages the batch, queues its
- * H2D, query (+ verify) and copy-out behind every update already launched, and returns a
- * ticket without waiting; wait blocks for that batch and fills `out`. Two batches can be in
- * flight: submitting a batch reuses the result slot of the batch submitted two before it
- * (waiting for it on the device if needed), after which waiting on that older ticket fails
- * with DGDS_EINVAL. So a caller overlaps the next tick's host work (dgds_update_batch plan,
- * query staging) with this tick's device work. Updates made after a submit are not seen by
- * it (stream order). Nothing is launched unless the whole batch validates. */
+/* Asynchronous dgds_speculate_verify_view. submit checks the arguments, starts staging the batch
+ * on the server's host workers and returns a ticket without waiting; the last worker queues the
+ * H2D, and the query (+ verify) kernels and the
+ * copy-out are launched before any later call on `s` touches the device. So the caller's next
+ * host work — typically the next tick's dgds_update_batch planning — overlaps this batch's
+ * staging, and its device work overlaps the next tick's host work. The batch sees exactly the
+ * updates made before the submit (stream order). wait blocks for the batch and fills `out`.
+ * The host input arrays are read asynchronously: keep them valid and unchanged until wait
+ * returns for this ticket. Two batches can be in flight: submitting a batch reuses the result
+ * slot of the batch submitted two before it, after which waiting on that ticket fails with
+ * DGDS_EINVAL. A bad group handle or decreasing pattern offsets fail the whole batch (nothing
+ * of it is launched): reported by submit for batches staged in the call (< 8192 queries),
+ * else by wait. */
 int dgds_speculate_submit(dgds_server* s, int64_t n, const int32_t* handles, const uint64_t* pat_offs,
                           const int32_t* patterns, const dgds_spec_args* args, int64_t args_stride,
                           const int32_t* truth, int32_t truth_stride, const int32_t* truth_left,

@@ -124,6 +124,7 @@ class WorkerPool {
   int threads() const { return static_cast<int>(th_.size()) + 1; }
   // fn(i) for i in [0, tasks), returns when all are done
   void run(int tasks, const std::function<void(int)>& fn) {
+    join();
     if (tasks <= 1 || th_.empty()) {
       for (int i = 0; i < tasks; ++i) fn(i);
       return;
@@ -141,6 +142,32 @@ class WorkerPool {
     std::unique_lock<std::mutex> lk(mu_);
     done_cv_.wait(lk, [this] { return pending_ == 0; });
     fn_ = nullptr;
+  }
+  // fn(i) for i in [0, tasks) on the workers alone; returns at once, join() waits
+  void post(int tasks, std::function<void(int)> fn) {
+    join();
+    if (th_.empty()) {
+      for (int i = 0; i < tasks; ++i) fn(i);
+      return;
+    }
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      owned_ = std::move(fn);
+      fn_ = &owned_;
+      tasks_ = tasks;
+      next_.store(0);
+      pending_ = tasks;
+      posted_ = true;
+      ++gen_;
+    }
+    cv_.notify_all();
+  }
+  void join() {
+    std::unique_lock<std::mutex> lk(mu_);
+    if (!posted_) return;
+    done_cv_.wait(lk, [this] { return pending_ == 0; });
+    fn_ = nullptr;
+    posted_ = false;
   }
 
  private:
@@ -173,6 +200,8 @@ class WorkerPool {
   std::mutex mu_;
   std::condition_variable cv_, done_cv_;
   const std::function<void(int)>* fn_ = nullptr;
+  std::function<void(int)> owned_;  // a posted job
+  bool posted_ = false;
   int tasks_ = 0;
   int pending_ = 0;
   std::atomic<int> next_{0};
@@ -309,6 +338,19 @@ void nt_copy(void* dst, const void* src, size_t n) {
 
 struct dgds_server;
 static void free_plan_pool(dgds_server* s);  // after dgds_update_plan is complete
+namespace {
+int flush_pending(dgds_server* s);  // launches a submitted query batch; before any later device work
+int launch_batch(dgds_server* s, bool timed);
+// one chunk of a staged host query batch: handles | pat_len | patterns | args | truth | truth_left | limit
+struct QInBlock {
+  int64_t q0 = 0, m = 0;
+  size_t base = 0, o_len = 0, o_pat = 0, o_args = 0, o_tr = 0, o_tl = 0, o_lm = 0, bytes = 0;
+};
+// device outputs of a host query batch (internal strides) + compaction scratch
+struct QOutLayout {
+  size_t sc = 0, sp = 0, nc = 0, ln = 0, tk = 0, v = 0, bs = 0, tot = 0, cmeta = 0, ctoff = 0, ccoff = 0, ctok = 0;
+};
+}  // namespace
 
 struct dgds_server {
   dgds_params p{};
@@ -329,6 +371,8 @@ struct dgds_server {
     uint64_t ticket = 0;         // 0: never used
     int64_t n = 0;
     bool verify = false;
+    int err = DGDS_OK;  // the batch failed validation (nothing launched)
+    std::string err_msg;
     size_t h_coff = 0, h_v = 0, h_meta = 0, h_toff = 0, h_tok = 0;
   } qslot[kQSlots];
   uint64_t last_ticket = 0;
@@ -340,6 +384,28 @@ struct dgds_server {
   cudaEvent_t ev_h2d[kMaxQChunks] = {}, ev_cmp[kMaxQChunks] = {};
   int q_chunks = 1;
   int out_blocks = 148;  // copy-out grid when chunked; DGDS_OUT_BLOCKS
+  // the submitted batch whose staging may still run on the workers (kernels not yet launched)
+  struct PendingQuery {
+    bool active = false;
+    uint64_t ticket = 0;
+    int64_t n = 0, args_stride = 0;
+    int nch = 1;
+    int32_t K = 1, Sx = 1, truth_stride = 0;
+    bool verify = false;
+    QInBlock blk[kMaxQChunks];
+    QOutLayout out;
+    std::atomic<int> left{0};           // staging tasks still running
+    std::atomic<int64_t> bad{0};        // first invalid query (INT64_MAX: none)
+    const int32_t* handles = nullptr;   // the caller's, for the error message
+    int64_t ng = 0;                     // groups at submit
+    std::atomic<cudaError_t> h2d_err{cudaSuccess};  // set by the last stager
+    bool stager_launch = true;          // the last stager also launches the kernels
+    bool launched = false;
+    int launch_rc = DGDS_OK;
+    std::string launch_msg;
+  } pq;
+  int stage_tasks = 8;  // workers of an asynchronous stage; DGDS_STAGE_TASKS
+  bool async_stage = true;  // DGDS_ASYNC_STAGE=0: submit stages synchronously
   dgds::DevTrie T{};
   unsigned long long* d_used = nullptr;
   uint64_t used_ub = 0;  // upper bound on occupied slots since the last exact read
@@ -398,6 +464,7 @@ struct dgds_server {
 namespace {
 
 int set_root(dgds_server* s, int32_t handle, uint32_t root) {
+  if (int rc = flush_pending(s)) return rc;  // a submitted query reads root_of as it was
   if (static_cast<size_t>(handle) >= s->root_of_cap) {
     size_t nc = std::max<size_t>(1024, s->root_of_cap * 2);
     while (nc <= static_cast<size_t>(handle)) nc *= 2;
@@ -423,6 +490,7 @@ int alloc_stream_slot(dgds_server* s, uint32_t* out) {
     return DGDS_OK;
   }
   if (s->next_stream >= s->stream_cap) {
+    if (int rc = flush_pending(s)) return rc;  // T.active / T.tail change under a staged batch's launch
     uint64_t nc = std::max<uint64_t>(1024, s->stream_cap * 2);
     uint32_t* na = nullptr;
     int32_t* nt = nullptr;
@@ -568,6 +636,7 @@ int rebuild(dgds_server* s, uint64_t new_cap) {
 }
 
 int ensure_capacity(dgds_server* s, uint64_t worst_new) {
+  if (int rc = flush_pending(s)) return rc;  // a submitted query reads the table as it was
   const double limit = kMaxLoad * static_cast<double>(s->T.cap);
   if (static_cast<double>(s->used_ub + worst_new) <= limit) return DGDS_OK;
   int rc = read_used(s, &s->used_ub);
@@ -601,6 +670,7 @@ struct PendingPiece {
 // Grow the history arena to hold hist_used tokens (stream-ordered copy; rare).
 int ensure_hist(dgds_server* s) {
   if (s->hist_used <= s->hist_cap) return DGDS_OK;
+  if (int rc = flush_pending(s)) return rc;  // T.hist changes under a staged batch's launch
   uint64_t nc = std::max<uint64_t>(s->hist_used, s->hist_cap * 2);
   int32_t* nb = nullptr;
   if (cudaMalloc(&nb, nc * sizeof(int32_t)) != cudaSuccess) return fail(DGDS_ENOMEM, "history arena allocation failed");
@@ -886,6 +956,8 @@ int dgds_create(const dgds_params* params, dgds_server** out) {
     s->q_chunks = std::min(dgds_server::kMaxQChunks, std::max(1, std::atoi(e)));
   s->out_blocks = s->h2d_blocks;
   if (const char* e = std::getenv("DGDS_OUT_BLOCKS")) s->out_blocks = std::max(1, std::atoi(e));
+  if (const char* e = std::getenv("DGDS_ASYNC_STAGE")) s->async_stage = std::atoi(e) != 0;
+  if (const char* e = std::getenv("DGDS_STAGE_TASKS")) s->stage_tasks = std::max(1, std::atoi(e));
   const uint64_t nodes = p.expected_nodes ? p.expected_nodes : (1ull << 20);
   double init_load = 0.35;  // expected_nodes is an upper bound, so the real load starts lower
   if (const char* e = std::getenv("DGDS_INIT_LOAD")) init_load = std::min(0.9, std::max(0.05, std::atof(e)));
@@ -929,7 +1001,10 @@ int dgds_create(const dgds_params* params, dgds_server** out) {
 int dgds_destroy(dgds_server* s) {
   if (!s) return DGDS_OK;
   cudaSetDevice(s->p.device);
+  flush_pending(s);  // a staged batch: its workers finish, its kernels run
   if (s->st) cudaStreamSynchronize(s->st);
+  if (s->out_st) cudaStreamSynchronize(s->out_st);
+  if (s->copy_st) cudaStreamSynchronize(s->copy_st);
   cudaFree(s->T.slots);
   cudaFree(s->T.active);
   cudaFree(s->T.tail);
@@ -963,6 +1038,7 @@ void* dgds_cuda_stream(dgds_server* s) { return s ? static_cast<void*>(s->st) : 
 
 int dgds_intern(dgds_server* s, const char* gid, size_t len, int32_t* handle) {
   std::lock_guard<std::mutex> lk(s->mu);
+  // host state only: no flush
   std::string key(gid, len);
   auto it = s->intern.find(key);
   if (it != s->intern.end()) {
@@ -981,6 +1057,7 @@ int dgds_intern(dgds_server* s, const char* gid, size_t len, int32_t* handle) {
 
 int dgds_register_group(dgds_server* s, int32_t h, double ttl, double now) {  // dgds.cpp:99-110
   std::lock_guard<std::mutex> lk(s->mu);
+  if (int rc_ = flush_pending(s)) return rc_;
   if (int rc = check_handle(s, h)) return rc;
   if (!(ttl > 0.0)) return fail(DGDS_EINVAL, "register_group: ttl_seconds must be > 0");
   cudaSetDevice(s->p.device);
@@ -999,6 +1076,7 @@ extern "C" {
 
 int dgds_drop_group(dgds_server* s, int32_t h) {  // dgds.cpp:112-116
   std::lock_guard<std::mutex> lk(s->mu);
+  if (int rc_ = flush_pending(s)) return rc_;
   if (int rc = check_handle(s, h)) return rc;
   cudaSetDevice(s->p.device);
   retire_group(s, s->groups[h]);
@@ -1007,6 +1085,7 @@ int dgds_drop_group(dgds_server* s, int32_t h) {  // dgds.cpp:112-116
 
 int dgds_sweep_expired(dgds_server* s, double now) {  // dgds.cpp:118-128
   std::lock_guard<std::mutex> lk(s->mu);
+  if (int rc_ = flush_pending(s)) return rc_;
   cudaSetDevice(s->p.device);
   for (auto& g : s->groups)
     if (g.alive && g.expires < now) retire_group(s, g);
@@ -1015,6 +1094,7 @@ int dgds_sweep_expired(dgds_server* s, double now) {  // dgds.cpp:118-128
 
 int dgds_has_group(dgds_server* s, int32_t h, int32_t* out) {
   std::lock_guard<std::mutex> lk(s->mu);
+  // host state only: no flush
   if (int rc = check_handle(s, h)) return rc;
   *out = s->groups[h].alive ? 1 : 0;
   return DGDS_OK;
@@ -1022,6 +1102,7 @@ int dgds_has_group(dgds_server* s, int32_t h, int32_t* out) {
 
 int dgds_group_version(dgds_server* s, int32_t h, uint64_t* out) {
   std::lock_guard<std::mutex> lk(s->mu);
+  // host state only: no flush
   if (int rc = check_handle(s, h)) return rc;
   *out = s->groups[h].alive ? s->groups[h].version : 0;
   return DGDS_OK;
@@ -1029,6 +1110,7 @@ int dgds_group_version(dgds_server* s, int32_t h, uint64_t* out) {
 
 int dgds_stored_tokens(dgds_server* s, int32_t h, int32_t rid, uint64_t* out) {
   std::lock_guard<std::mutex> lk(s->mu);
+  // host state only: no flush
   if (int rc = check_handle(s, h)) return rc;
   GroupRec& g = s->groups[h];
   StreamRec* r = g.streams.find(rid);
@@ -1038,6 +1120,7 @@ int dgds_stored_tokens(dgds_server* s, int32_t h, int32_t rid, uint64_t* out) {
 
 int dgds_shard_group_count(dgds_server* s, int32_t shard, uint64_t* out) {
   std::lock_guard<std::mutex> lk(s->mu);
+  // host state only: no flush
   if (shard < 0 || shard >= s->p.shard_count) return fail(DGDS_EINVAL, "bad shard");
   *out = s->shard_counts[shard];
   return DGDS_OK;
@@ -1046,12 +1129,14 @@ int dgds_shard_group_count(dgds_server* s, int32_t shard, uint64_t* out) {
 int dgds_index_slots(dgds_server* s, uint64_t* slots) {
   if (!s || !slots) return fail(DGDS_EINVAL, "null argument");
   std::lock_guard<std::mutex> lk(s->mu);
+  // host state only: no flush
   *slots = s->T.cap;
   return DGDS_OK;
 }
 
 int dgds_node_count(dgds_server* s, uint64_t* out) {
   std::lock_guard<std::mutex> lk(s->mu);
+  if (int rc_ = flush_pending(s)) return rc_;
   cudaSetDevice(s->p.device);
   uint64_t u = 0;
   if (int rc = read_used(s, &u)) return rc;
@@ -1104,6 +1189,7 @@ static int update_batch_locked(dgds_server* s, int64_t n, const int32_t* handles
   _mm_sfence();
   char* d = static_cast<char*>(s->d_stage.p);
   pc.mark("stage");
+  if (int rc = flush_pending(s)) return rc;  // K1 after the query batch submitted before it
   DGDS_CUDA(cudaMemcpyAsync(d, h, total, cudaMemcpyHostToDevice, s->st));
   DGDS_CUDA(cudaEventRecord(s->staging_free, s->st));
   {
@@ -1120,7 +1206,7 @@ extern "C" int dgds_update_batch(dgds_server* s, int64_t n, const int32_t* handl
                                  const uint64_t* prev, const uint64_t* offs, const int32_t* tokens, double now,
                                  dgds_update_reply* rep) {
   if (!s) return fail(DGDS_EINVAL, "null server");
-  std::lock_guard<std::mutex> lk(s->mu);
+  std::lock_guard<std::mutex> lk(s->mu);  // a pending query batch is flushed at the first device work
   return update_batch_locked(s, n, handles, rids, prev, offs, tokens, now, rep);
 }
 
@@ -1198,6 +1284,7 @@ static int update_device_impl(dgds_server* s, int64_t n, const int32_t* handles,
   if (n == 0) return DGDS_OK;
   PhaseClock pc("update_device");
   std::lock_guard<std::mutex> lk(s->mu);
+  if (int rc_ = flush_pending(s)) return rc_;
   DGDS_CUDA(cudaSetDevice(s->p.device));
   thread_local dgds_update_plan plan;
   plan.segs.clear();
@@ -1304,6 +1391,7 @@ int dgds_update_plan_routed(dgds_server* s, int32_t n_seg, int64_t seg_rows, con
   std::unique_ptr<dgds_update_plan> plan;
   {
     std::lock_guard<std::mutex> lk(s->mu);
+    if (int rc_ = flush_pending(s)) return rc_;
     if (!s->plan_pool.empty()) {
       plan.reset(s->plan_pool.back());
       s->plan_pool.pop_back();
@@ -1318,6 +1406,7 @@ int dgds_update_plan_routed(dgds_server* s, int32_t n_seg, int64_t seg_rows, con
     thread_local RoutedScratch r;
     if (int rc = fill_routed(r, n, n_seg, seg_rows, h_counts, h_meta, meta_stride, row_words)) return rc;
     std::lock_guard<std::mutex> lk(s->mu);
+    if (int rc_ = flush_pending(s)) return rc_;
     DGDS_CUDA(cudaSetDevice(s->p.device));
     if (int rc = plan_device(s, n, r.handles.data(), r.rids.data(), r.prev.data(), r.starts.data(), r.counts.data(),
                              d_rows, now, r.rep.data(), plan.get()))
@@ -1336,6 +1425,7 @@ int dgds_update_launch(dgds_server* s, dgds_update_plan* plan, void* stream) {
   if (!s || !plan) return fail(DGDS_EINVAL, "null argument");
   PhaseClock pc("update_launch");
   std::lock_guard<std::mutex> lk(s->mu);
+  if (int rc_ = flush_pending(s)) return rc_;
   const cudaError_t e = cudaSetDevice(s->p.device);
   const int rc = e == cudaSuccess ? launch_plan(s, plan, stream, pc)
                                   : fail(DGDS_ECUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(e));
@@ -1368,14 +1458,85 @@ struct HostResult {
   const int32_t* verify = nullptr;    // [3][n] drafted | accepted | emitted, or null
 };
 
-// Validate + stage (in parallel on the worker pool), H2D, K2 (+ fused K3), compaction into
-// device memory, one copy-out kernel into the slot's mapped host block; returns without
-// waiting. Caller holds s->mu. Nothing is launched unless the whole batch validates.
+// Stage queries [j0, j1) of chunk b (chunk-relative) into its pinned block: pattern rows are
+// built in cache, then streamed out with non-temporal stores.
+// Returns the first query of the range with a bad handle (>= ng) or decreasing offsets, or -1.
+int64_t stage_rows(const QInBlock& b, char* hb, int64_t j0, int64_t j1, int32_t P, int64_t ng, const int32_t* handles,
+                   const uint64_t* pat_offs, const int32_t* patterns, const int32_t* truth, int32_t truth_stride,
+                   const int32_t* truth_left, const int32_t* limit, bool verify) {
+  if (j0 >= j1) return -1;
+  int64_t bad = -1;
+  const int64_t q0 = b.q0 + j0;
+  int32_t* hl = reinterpret_cast<int32_t*>(hb + b.o_len);
+  int32_t* hp = reinterpret_cast<int32_t*>(hb + b.o_pat);
+  thread_local std::vector<int32_t> lens, rows;
+  lens.resize(j1 - j0);
+  rows.assign(static_cast<size_t>(j1 - j0) * P, 0);
+  for (int64_t j = j0; j < j1; ++j) {
+    const int64_t i = b.q0 + j;
+    const int32_t hd = handles[i];
+    if ((hd < 0 || hd >= ng || pat_offs[i + 1] < pat_offs[i]) && bad < 0) bad = i;
+    const uint64_t L = pat_offs[i + 1] - pat_offs[i];
+    lens[j - j0] = static_cast<int32_t>(std::min<uint64_t>(L, 0x7FFFFFFF));
+    const uint64_t keep = std::min<uint64_t>(L, static_cast<uint64_t>(P));
+    const int32_t* src = patterns + pat_offs[i + 1] - keep;
+    int32_t* dst = rows.data() + (j - j0) * P;
+    for (uint64_t k = 0; k < keep; ++k) dst[k] = src[k];
+  }
+  nt_copy(hl + j0, lens.data(), (j1 - j0) * 4);
+  nt_copy(hp + j0 * P, rows.data(), rows.size() * 4);
+  nt_copy(hb + j0 * 4, handles + q0, (j1 - j0) * 4);
+  if (verify) {
+    nt_copy(hb + b.o_tr + static_cast<size_t>(j0) * truth_stride * 4, truth + q0 * truth_stride,
+            static_cast<size_t>(j1 - j0) * truth_stride * 4);
+    nt_copy(hb + b.o_tl + j0 * 4, truth_left + q0, (j1 - j0) * 4);
+    nt_copy(hb + b.o_lm + j0 * 4, limit + q0, (j1 - j0) * 4);
+  }
+  _mm_sfence();  // streaming stores globally visible before the copy is issued
+  return bad;
+}
+
+// Issue the H2D of every chunk of the pending batch (from the worker that staged last).
+// The batch's H2D, one copy per chunk block (per-row copies queued by each stager measured
+// slower: many small copies from several threads), from the worker that staged last; then the
+// per-chunk events the query launches wait on.
+cudaError_t issue_h2d(dgds_server* s) {
+  dgds_server::PendingQuery& pq = s->pq;
+  dgds_server::QSlot& slot = s->qslot[pq.ticket % dgds_server::kQSlots];
+  char* h = static_cast<char*>(slot.hq.p);
+  char* d = static_cast<char*>(slot.dq.p);
+  cudaError_t e = cudaSetDevice(s->p.device);
+  for (int c = 0; c < pq.nch && e == cudaSuccess; ++c) {
+    const QInBlock& b = pq.blk[c];
+    if (s->h2d_kernel) {  // the GPU pulls the mapped staging block
+      dgds::CopyOutRegions Rin{};
+      Rin.n = 1;
+      Rin.total_idx[0] = -1;
+      Rin.begin_idx[0] = -1;
+      Rin.fixed_bytes[0] = static_cast<int64_t>(b.bytes);
+      Rin.src[0] = h + b.base;
+      Rin.dst[0] = d + b.base;
+      // a narrow grid: enough reads in flight for PCIe, SMs left to the append kernel running beside it
+      e = dgds::launch_copy_out(nullptr, Rin, Rin.fixed_bytes[0], s->copy_st, s->h2d_blocks);
+    } else {
+      e = cudaMemcpyAsync(d + b.base, h + b.base, b.bytes, cudaMemcpyHostToDevice, s->copy_st);
+    }
+    if (e == cudaSuccess) e = cudaEventRecord(s->ev_h2d[c], s->copy_st);
+  }
+  return e;
+}
+
+// Check the arguments, then stage (and validate handles / offsets) on the worker pool without
+// waiting: the caller's next host work (typically the next tick's dgds_update_batch planning)
+// overlaps the staging. The worker that stages last issues the H2D and launches the kernels;
+// any later call that touches the device first joins it (flush_pending), so every batch sees
+// exactly the updates launched before it. Caller holds s->mu.
 int speculate_submit(dgds_server* s, int64_t n, const int32_t* handles, const uint64_t* pat_offs,
                      const int32_t* patterns, const dgds_spec_args* args, int64_t args_stride, const int32_t* truth,
                      int32_t truth_stride, const int32_t* truth_left, const int32_t* limit, bool verify,
                      uint64_t* ticket) {
   PhaseClock pc("speculate_submit");
+  if (int rc = flush_pending(s)) return rc;
   const int64_t nargs = args_stride ? n : 1;
   int32_t max_k = 1, max_s = 1;
   for (int64_t i = 0; i < nargs; ++i) {
@@ -1386,22 +1547,16 @@ int speculate_submit(dgds_server* s, int64_t n, const int32_t* handles, const ui
   }
   if (verify && (!truth || !truth_left || !limit || truth_stride < 0))
     return fail(DGDS_EINVAL, "verify needs truth inputs");
+  pc.mark("args");
   const int32_t P = s->p.max_pattern_len;  // only the last max_pattern_len tokens can matter
-  // Chunks of the batch are staged, copied in and queried in order. Chunk c's H2D runs while
-  // chunk c+1 is staged, and chunk c's copy-out (PCIe-bound, out_st) while chunk c+1 is queried.
-  // The query kernels are launched only after the whole batch validated.
+  dgds_server::PendingQuery& pq = s->pq;
+  // optional chunks of the batch (DGDS_Q_CHUNKS): chunk c's copy-out beside chunk c+1's query
   int nch = n >= 32768 ? s->q_chunks : 1;
   const int64_t per = static_cast<int64_t>(align_up((n + nch - 1) / nch, 256));
   nch = static_cast<int>((n + per - 1) / per);
-  // per-chunk input block: handles | pat_len | patterns | args | truth | truth_left | limit
-  struct InBlock {
-    int64_t q0, m;
-    size_t base, o_len, o_pat, o_args, o_tr, o_tl, o_lm, bytes;
-  };
-  InBlock blk[dgds_server::kMaxQChunks];
   size_t in_all = 0;
-  for (int c = 0; c < nch; ++c) {
-    InBlock& b = blk[c];
+  for (int c = 0; c < nch; ++c) {  // per-chunk block: handles | pat_len | patterns | args | truth | truth_left | limit
+    QInBlock& b = pq.blk[c];
     b.q0 = c * per;
     b.m = std::min<int64_t>(per, n - b.q0);
     b.base = in_all;
@@ -1419,114 +1574,140 @@ int speculate_submit(dgds_server* s, int64_t n, const int32_t* handles, const ui
   DGDS_CUDA(cudaEventSynchronize(slot.done));  // the slot's previous batch is complete
   slot.ticket = 0;  // its results are gone from here on
   pc.mark("slot_wait");
+  // device outputs (internal strides) + compaction scratch; mapped result block
+  const int32_t K = max_k, Sx = max_s;
+  const int64_t nk = static_cast<int64_t>(n) * K;
+  QOutLayout& o = pq.out;
+  o.sc = 0;
+  o.sp = align_up(o.sc + nk * 8, 256);
+  o.nc = align_up(o.sp + nk * 8, 256);
+  o.ln = align_up(o.nc + n * 4, 256);
+  o.tk = align_up(o.ln + nk * 4, 256);
+  o.v = align_up(o.tk + static_cast<size_t>(nk) * Sx * 4, 256);
+  o.bs = align_up(o.v + (verify ? static_cast<size_t>(n) * 12 : 0), 256);
+  o.tot = align_up(o.bs + static_cast<size_t>((per + 255) / 256) * 16, 256);
+  o.cmeta = align_up(o.tot + static_cast<size_t>(nch) * 16, 256);
+  o.ctoff = align_up(o.cmeta + nk * sizeof(dgds::CandMeta), 256);
+  o.ccoff = align_up(o.ctoff + nk * 8, 256);
+  o.ctok = align_up(o.ccoff + (n + 1) * 8, 256);
+  const size_t dev_total = o.ctok + static_cast<size_t>(nk) * Sx * 4;
+  slot.h_coff = 256;  // totals | cand_off | verify | meta | tok_off | tokens
+  slot.h_v = align_up(slot.h_coff + (n + 1) * 8, 256);
+  slot.h_meta = align_up(slot.h_v + (verify ? n * 12 : 0), 256);
+  slot.h_toff = align_up(slot.h_meta + nk * sizeof(dgds::CandMeta), 256);
+  slot.h_tok = align_up(slot.h_toff + (nk + 1) * 8, 256);
   if (int rc = slot.hq.ensure(in_all)) return rc;
   if (int rc = slot.dq.ensure(in_all)) return rc;
+  if (int rc = slot.dout.ensure(dev_total)) return rc;
+  if (int rc = slot.ho.ensure(slot.h_tok + static_cast<size_t>(nk) * Sx * 4)) return rc;
   char* h = static_cast<char*>(slot.hq.p);
-  char* d = static_cast<char*>(slot.dq.p);
-  const size_t ngroups = s->groups.size();
-  WorkerPool& pool = s->workers();
-  const int tasks = n >= 8192 ? std::max(1, 4 * pool.threads() / nch) : 1;
-  std::vector<int64_t> bad(tasks, -1);  // first invalid query of each task
-  for (int c = 0; c < nch; ++c) {
-    const InBlock& b = blk[c];
-    char* hb = h + b.base;
-    int32_t* hl = reinterpret_cast<int32_t*>(hb + b.o_len);
-    int32_t* hp = reinterpret_cast<int32_t*>(hb + b.o_pat);
-    const int64_t chunk = (b.m + tasks - 1) / tasks;
-    std::fill(bad.begin(), bad.end(), -1);
-    pool.run(tasks, [&](int t) {
-      const int64_t j0 = t * chunk, j1 = std::min<int64_t>(b.m, j0 + chunk);  // chunk-relative
-      if (j0 >= j1) return;
-      const int64_t q0 = b.q0 + j0;
-      thread_local std::vector<int32_t> lens, rows;  // built in cache, then streamed out
-      lens.resize(j1 - j0);
-      rows.assign(static_cast<size_t>(j1 - j0) * P, 0);
-      for (int64_t j = j0; j < j1; ++j) {
-        const int64_t i = b.q0 + j;
-        const int32_t hd = handles[i];
-        if ((hd < 0 || static_cast<size_t>(hd) >= ngroups || pat_offs[i + 1] < pat_offs[i]) && bad[t] < 0) bad[t] = i;
-        const uint64_t L = pat_offs[i + 1] - pat_offs[i];
-        lens[j - j0] = static_cast<int32_t>(std::min<uint64_t>(L, 0x7FFFFFFF));
-        const uint64_t keep = std::min<uint64_t>(L, static_cast<uint64_t>(P));
-        const int32_t* src = patterns + pat_offs[i + 1] - keep;
-        int32_t* dst = rows.data() + (j - j0) * P;
-        for (uint64_t k = 0; k < keep; ++k) dst[k] = src[k];
-      }
-      nt_copy(hl + j0, lens.data(), (j1 - j0) * 4);
-      nt_copy(hp + j0 * P, rows.data(), rows.size() * 4);
-      nt_copy(hb + j0 * 4, handles + q0, (j1 - j0) * 4);
-      if (verify) {
-        nt_copy(hb + b.o_tr + static_cast<size_t>(j0) * truth_stride * 4, truth + q0 * truth_stride,
-                static_cast<size_t>(j1 - j0) * truth_stride * 4);
-        nt_copy(hb + b.o_tl + j0 * 4, truth_left + q0, (j1 - j0) * 4);
-        nt_copy(hb + b.o_lm + j0 * 4, limit + q0, (j1 - j0) * 4);
-      }
-      _mm_sfence();  // streaming stores globally visible before the copy is issued
-    });
-    auto* ha = reinterpret_cast<dgds_spec_args*>(hb + b.o_args);
+  for (int c = 0; c < nch; ++c) {  // args: tiny, copied here
+    const QInBlock& b = pq.blk[c];
+    auto* ha = reinterpret_cast<dgds_spec_args*>(h + b.base + b.o_args);
     if (!args_stride) ha[0] = args[0];
     else
       for (int64_t j = 0; j < b.m; ++j) ha[j] = args[(b.q0 + j) * args_stride];
-    for (int t = 0; t < tasks; ++t) {
-      if (bad[t] >= 0) {
-        DGDS_CUDA(cudaEventRecord(slot.done, s->copy_st));  // chunks already in flight read hq
-        const int64_t i = bad[t];
-        if (int rc = check_handle(s, handles[i])) return rc;
-        return fail(DGDS_EINVAL, "pattern offsets must be nondecreasing");
+  }
+  pq.n = n;
+  pq.nch = nch;
+  pq.K = K;
+  pq.Sx = Sx;
+  pq.args_stride = args_stride;
+  pq.truth_stride = truth_stride;
+  pq.verify = verify;
+  pq.ticket = tk;
+  pq.h2d_err = cudaSuccess;
+  pq.handles = handles;
+  pq.ng = static_cast<int64_t>(s->groups.size());
+  pq.stager_launch = !s->profiling;  // LaunchTimer state belongs to the caller's thread
+  pq.launched = false;
+  pq.launch_rc = DGDS_OK;
+  slot.ticket = tk;
+  slot.err = DGDS_OK;
+  slot.n = n;
+  slot.verify = verify;
+  s->last_ticket = tk;
+  *ticket = tk;
+  // stage (and validate) on the workers; tasks cover [0, n) and split at chunk boundaries. An
+  // asynchronous stage uses a few workers: it overlaps the caller's next host work, which
+  // would otherwise be starved of memory bandwidth.
+  WorkerPool& pool = s->workers();
+  const bool async = s->async_stage && n >= 8192 && pool.threads() > 1;
+  const int tasks = n < 8192 ? 1 : async ? std::min(s->stage_tasks, pool.threads() - 1) : 4 * pool.threads();
+  const int64_t span = (n + tasks - 1) / tasks;
+  const int64_t ng = static_cast<int64_t>(s->groups.size());
+  pq.left.store(tasks);
+  pq.bad.store(INT64_MAX);
+  auto job = [s, h, span, n, per, P, ng, handles, pat_offs, patterns, truth, truth_stride, truth_left, limit,
+              verify](int t) {
+    const int64_t i0 = t * span, i1 = std::min<int64_t>(n, i0 + span);
+    int64_t first_bad = INT64_MAX;
+    for (int64_t i = i0; i < i1;) {
+      const int c = static_cast<int>(i / per);
+      const QInBlock& b = s->pq.blk[c];
+      const int64_t e = std::min<int64_t>(i1, b.q0 + b.m);
+      const int64_t bad = stage_rows(b, h + b.base, i - b.q0, e - b.q0, P, ng, handles, pat_offs, patterns, truth,
+                                     truth_stride, truth_left, limit, verify);
+      if (bad >= 0 && bad < first_bad) first_bad = bad;
+      i = e;
+    }
+    if (first_bad != INT64_MAX) {
+      int64_t cur = s->pq.bad.load();
+      while (first_bad < cur && !s->pq.bad.compare_exchange_weak(cur, first_bad)) {
       }
     }
-    // the copy stream runs the H2D under the append kernel already queued on st
-    if (s->h2d_kernel) {  // the GPU pulls the mapped staging block
-      dgds::CopyOutRegions Rin{};
-      Rin.n = 1;
-      Rin.total_idx[0] = -1;
-      Rin.begin_idx[0] = -1;
-      Rin.fixed_bytes[0] = static_cast<int64_t>(b.bytes);
-      Rin.src[0] = hb;
-      Rin.dst[0] = d + b.base;
-      // a narrow grid: enough reads in flight for PCIe, SMs left to the append kernel running beside it
-      DGDS_CUDA(dgds::launch_copy_out(nullptr, Rin, Rin.fixed_bytes[0], s->copy_st, s->h2d_blocks));
-    } else {
-      DGDS_CUDA(cudaMemcpyAsync(d + b.base, hb, b.bytes, cudaMemcpyHostToDevice, s->copy_st));
+    if (s->pq.left.fetch_sub(1) == 1 && s->pq.bad.load() == INT64_MAX) {  // the last stager
+      dgds_server::PendingQuery& q = s->pq;  // (nothing is launched for an invalid batch)
+      if (q.h2d_err == cudaSuccess) q.h2d_err = issue_h2d(s);
+      if (q.h2d_err == cudaSuccess && q.stager_launch) {
+        q.launch_rc = launch_batch(s, false);
+        if (q.launch_rc) q.launch_msg = dgds_last_error();
+        q.launched = true;
+      }
     }
-    DGDS_CUDA(cudaEventRecord(s->ev_h2d[c], s->copy_st));
+  };
+  pq.active = true;
+  if (async) {
+    pool.post(tasks, job);  // a bad handle / offset is reported by the batch's wait
+  } else {
+    pool.run(tasks, job);
+    if (pq.bad.load() != INT64_MAX) {  // staged here: report at submit, nothing was queued
+      const int64_t i = pq.bad.load();
+      pq.active = false;
+      slot.ticket = 0;
+      s->last_ticket = tk - 1;
+      if (int rc = check_handle(s, handles[i])) return rc;
+      return fail(DGDS_EINVAL, "pattern offsets must be nondecreasing");
+    }
   }
-  pc.mark("validate_stage");
-  // device outputs (internal strides) + compaction scratch
-  const int32_t K = max_k, Sx = max_s;
-  const int64_t nk = static_cast<int64_t>(n) * K;
-  const size_t o_sc = 0;
-  const size_t o_sp = align_up(o_sc + nk * 8, 256);
-  const size_t o_nc = align_up(o_sp + nk * 8, 256);
-  const size_t o_ln = align_up(o_nc + n * 4, 256);
-  const size_t o_tk = align_up(o_ln + nk * 4, 256);
-  const size_t o_v = align_up(o_tk + static_cast<size_t>(nk) * Sx * 4, 256);
-  const int64_t nblk = (per + 255) / 256;
-  const size_t o_bs = align_up(o_v + (verify ? static_cast<size_t>(n) * 12 : 0), 256);
-  const size_t o_tot = align_up(o_bs + static_cast<size_t>(nblk) * 16, 256);
-  const size_t o_cmeta = align_up(o_tot + static_cast<size_t>(nch) * 16, 256);
-  const size_t o_ctoff = align_up(o_cmeta + nk * sizeof(dgds::CandMeta), 256);
-  const size_t o_ccoff = align_up(o_ctoff + nk * 8, 256);
-  const size_t o_ctok = align_up(o_ccoff + (n + 1) * 8, 256);
-  const size_t dev_total = o_ctok + static_cast<size_t>(nk) * Sx * 4;
-  if (int rc = slot.dout.ensure(dev_total)) return rc;
-  // mapped host block: totals | cand_off | verify | meta | tok_off | tokens
-  const size_t h_coff = 256;
-  const size_t h_v = align_up(h_coff + (n + 1) * 8, 256);
-  const size_t h_meta = align_up(h_v + (verify ? n * 12 : 0), 256);
-  const size_t h_toff = align_up(h_meta + nk * sizeof(dgds::CandMeta), 256);
-  const size_t h_tok = align_up(h_toff + (nk + 1) * 8, 256);
-  if (int rc = slot.ho.ensure(h_tok + static_cast<size_t>(nk) * Sx * 4)) return rc;
+  pc.mark("post");
+  return DGDS_OK;
+}
+
+// Launch a staged batch's kernels (its H2D issued): query (+ verify), compaction, copy-out.
+// Run by the worker that staged last, or by flush_pending when that worker could not (profiling
+// timers are main-thread state). Reads server state that every main-thread mutation of it
+// (root table, index table, stream and history arrays) first flushes, i.e. joins the worker.
+int launch_batch(dgds_server* s, bool timed) {
+  dgds_server::PendingQuery& pq = s->pq;
+  dgds_server::QSlot& slot = s->qslot[pq.ticket % dgds_server::kQSlots];
+  const QOutLayout& o = pq.out;
+  const int64_t n = pq.n;
+  const int32_t K = pq.K, Sx = pq.Sx, P = s->p.max_pattern_len;
+  const bool verify = pq.verify;
+  const int nch = pq.nch;
+  char* d = static_cast<char*>(slot.dq.p);
   char* dout = static_cast<char*>(slot.dout.p);
   char* ho = static_cast<char*>(slot.ho.p);
-  long long* d_bs = reinterpret_cast<long long*>(dout + o_bs);
-  long long* d_tot = reinterpret_cast<long long*>(dout + o_tot);  // [chunk][candidates, tokens], cumulative
-  auto* d_meta = reinterpret_cast<dgds::CandMeta*>(dout + o_cmeta);
-  auto* d_toff = reinterpret_cast<int64_t*>(dout + o_ctoff);
-  auto* d_coff = reinterpret_cast<int64_t*>(dout + o_ccoff);
-  int32_t* d_ctok = reinterpret_cast<int32_t*>(dout + o_ctok);
+  long long* d_bs = reinterpret_cast<long long*>(dout + o.bs);
+  long long* d_tot = reinterpret_cast<long long*>(dout + o.tot);  // [chunk][candidates, tokens], cumulative
+  auto* d_meta = reinterpret_cast<dgds::CandMeta*>(dout + o.cmeta);
+  auto* d_toff = reinterpret_cast<int64_t*>(dout + o.ctoff);
+  auto* d_coff = reinterpret_cast<int64_t*>(dout + o.ccoff);
+  int32_t* d_ctok = reinterpret_cast<int32_t*>(dout + o.ctok);
+  int32_t* d_v = reinterpret_cast<int32_t*>(dout + o.v);
   for (int c = 0; c < nch; ++c) {
-    const InBlock& b = blk[c];
+    const QInBlock& b = pq.blk[c];
     const char* db = d + b.base;
     const int64_t q0 = b.q0, m = b.m;
     DGDS_CUDA(cudaStreamWaitEvent(s->st, s->ev_h2d[c], 0));
@@ -1540,30 +1721,31 @@ int speculate_submit(dgds_server* s, int64_t n, const int32_t* handles, const ui
     L.patterns = reinterpret_cast<const int32_t*>(db + b.o_pat);
     L.pat_stride = P;
     L.args = reinterpret_cast<const dgds_spec_args*>(db + b.o_args);
-    L.args_stride = args_stride ? 1 : 0;
+    L.args_stride = pq.args_stride ? 1 : 0;
     L.k_stride = K;
     L.s_stride = Sx;
     dgds::soa_strides(L);
-    L.scores = reinterpret_cast<double*>(dout + o_sc) + q0 * K;
-    L.supports = reinterpret_cast<int64_t*>(dout + o_sp) + q0 * K;
-    L.n_cands = reinterpret_cast<int32_t*>(dout + o_nc) + q0;
-    L.lens = reinterpret_cast<int32_t*>(dout + o_ln) + q0 * K;
-    L.tokens = reinterpret_cast<int32_t*>(dout + o_tk) + q0 * K * Sx;
+    L.scores = reinterpret_cast<double*>(dout + o.sc) + q0 * K;
+    L.supports = reinterpret_cast<int64_t*>(dout + o.sp) + q0 * K;
+    L.n_cands = reinterpret_cast<int32_t*>(dout + o.nc) + q0;
+    L.lens = reinterpret_cast<int32_t*>(dout + o.ln) + q0 * K;
+    L.tokens = reinterpret_cast<int32_t*>(dout + o.tk) + q0 * K * Sx;
     L.err_flag = s->d_err;
     L.stat_part = s->d_stat_part;
-    int32_t* d_v = reinterpret_cast<int32_t*>(dout + o_v);
     if (verify) {
       L.truth = reinterpret_cast<const int32_t*>(db + b.o_tr);
-      L.truth_stride = truth_stride;
+      L.truth_stride = pq.truth_stride;
       L.truth_left = reinterpret_cast<const int32_t*>(db + b.o_tl);
       L.limit = reinterpret_cast<const int32_t*>(db + b.o_lm);
       L.v_drafted = d_v + q0;
       L.v_accepted = d_v + n + q0;
       L.v_emitted = d_v + 2 * n + q0;
     }
-    {
+    if (timed) {
       LaunchTimer lt(s, 1, s->st);
-      DGDS_CUDA(dgds::launch_query(L, max_k, max_s, s->st));
+      DGDS_CUDA(dgds::launch_query(L, K, Sx, s->st));
+    } else {
+      DGDS_CUDA(dgds::launch_query(L, K, Sx, s->st));
     }
     DGDS_CUDA(dgds::launch_compact(m, K, Sx, L.n_cands, L.lens, L.scores, L.supports, L.tokens, d_bs, d_tot + 2 * c,
                                    d_meta, d_ctok, d_coff + q0, d_toff, c ? d_tot + 2 * (c - 1) : nullptr, s->st));
@@ -1580,35 +1762,58 @@ int speculate_submit(dgds_server* s, int64_t n, const int32_t* handles, const ui
       R.fixed_bytes[i] = fixed;
     };
     const int tc = 2 * c, tb = c ? 2 * (c - 1) : -1;
-    region(d_coff + q0, ho + h_coff + q0 * 8, -1, -1, 0, m * 8);
+    region(d_coff + q0, ho + slot.h_coff + q0 * 8, -1, -1, 0, m * 8);
     if (verify)
       for (int k = 0; k < 3; ++k)
-        region(d_v + k * n + q0, ho + h_v + (k * n + q0) * 4, -1, -1, 0, m * 4);
-    region(d_meta, ho + h_meta, tc, tb, sizeof(dgds::CandMeta), 0);
-    region(d_toff, ho + h_toff, tc, tb, 8, 0);
-    region(d_ctok, ho + h_tok, tc + 1, c ? tb + 1 : -1, 4, 0);
+        region(d_v + k * n + q0, ho + slot.h_v + (k * n + q0) * 4, -1, -1, 0, m * 4);
+    region(d_meta, ho + slot.h_meta, tc, tb, sizeof(dgds::CandMeta), 0);
+    region(d_toff, ho + slot.h_toff, tc, tb, 8, 0);
+    region(d_ctok, ho + slot.h_tok, tc + 1, c ? tb + 1 : -1, 4, 0);
     if (c == nch - 1) region(d_tot + tc, ho, -1, -1, 0, 16);
     DGDS_CUDA(dgds::launch_copy_out(d_tot, R, m * K * static_cast<int64_t>(sizeof(dgds::CandMeta) + 8 + Sx * 4),
                                     s->out_st, nch > 1 ? s->out_blocks : 592));
   }
   DGDS_CUDA(cudaEventRecord(slot.done, s->out_st));  // after st's work (out_st waited on it)
-  pc.mark("launch");
-  slot.ticket = tk;
-  slot.n = n;
-  slot.verify = verify;
-  slot.h_coff = h_coff;
-  slot.h_v = h_v;
-  slot.h_meta = h_meta;
-  slot.h_toff = h_toff;
-  slot.h_tok = h_tok;
-  s->last_ticket = tk;
-  *ticket = tk;
   return DGDS_OK;
+}
+
+// Completes the pending batch: joins its staging workers and, unless the last of them did,
+// launches its kernels. Runs before any later call on the server touches the device.
+// Caller holds s->mu.
+int flush_pending(dgds_server* s) {
+  dgds_server::PendingQuery& pq = s->pq;
+  if (!pq.active) return DGDS_OK;
+  PhaseClock pc("flush_pending");
+  s->workers().join();
+  pq.active = false;
+  pc.mark("join");
+  dgds_server::QSlot& slot = s->qslot[pq.ticket % dgds_server::kQSlots];
+  if (pq.bad.load() != INT64_MAX) {  // reported by the batch's wait, not by the call that flushed
+    const int64_t i = pq.bad.load();
+    const int32_t hd = pq.handles[i];
+    slot.err = DGDS_EINVAL;
+    slot.err_msg = (hd < 0 || hd >= pq.ng) ? "bad group handle" : "pattern offsets must be nondecreasing";
+    return DGDS_OK;
+  }
+  if (pq.h2d_err.load() != cudaSuccess) return fail(DGDS_ECUDA, cudaGetErrorString(pq.h2d_err.load()));
+  if (pq.launched) {
+    if (pq.launch_rc) return fail(pq.launch_rc, pq.launch_msg);
+    return DGDS_OK;
+  }
+  const int rc = launch_batch(s, true);
+  pc.mark("launch");
+  return rc;
 }
 
 // Waits for a submitted batch and describes its results. Caller holds s->mu.
 int speculate_finish(dgds_server* s, uint64_t ticket, HostResult* r) {
   if (ticket == 0 || ticket > s->last_ticket) return fail(DGDS_EINVAL, "unknown query ticket");
+  if (s->pq.active && s->pq.ticket == ticket)  // waiting on the batch still being staged
+    if (int rc = flush_pending(s)) return rc;
+  {
+    const dgds_server::QSlot& sl = s->qslot[ticket % dgds_server::kQSlots];
+    if (sl.ticket == ticket && sl.err) return fail(sl.err, sl.err_msg);
+  }
   dgds_server::QSlot& slot = s->qslot[ticket % dgds_server::kQSlots];
   if (slot.ticket != ticket) return fail(DGDS_EINVAL, "query ticket expired (its result slot was reused)");
   DGDS_CUDA(cudaEventSynchronize(slot.done));
@@ -1655,6 +1860,7 @@ int dgds_speculate_verify_batch(dgds_server* s, int64_t n, const int32_t* handle
   if (n == 0) return DGDS_OK;
   if (!out) return fail(DGDS_EINVAL, "null output");
   std::lock_guard<std::mutex> lk(s->mu);
+  if (int rc_ = flush_pending(s)) return rc_;
   DGDS_CUDA(cudaSetDevice(s->p.device));
   {
     const int64_t nargs = args_stride ? n : 1;
@@ -1727,6 +1933,7 @@ int dgds_speculate_verify_view(dgds_server* s, int64_t n, const int32_t* handles
   *out = dgds_result_view{};
   if (n == 0) return DGDS_OK;
   std::lock_guard<std::mutex> lk(s->mu);
+  if (int rc_ = flush_pending(s)) return rc_;
   DGDS_CUDA(cudaSetDevice(s->p.device));
   HostResult r;
   if (int rc = speculate_host(s, n, handles, pat_offs, patterns, args, args_stride, truth, truth_stride, truth_left,
@@ -1743,6 +1950,7 @@ int dgds_speculate_submit(dgds_server* s, int64_t n, const int32_t* handles, con
   if (!s || !ticket) return fail(DGDS_EINVAL, "null argument");
   if (n <= 0) return fail(DGDS_EINVAL, "submit needs a non-empty batch");
   std::lock_guard<std::mutex> lk(s->mu);
+  if (int rc_ = flush_pending(s)) return rc_;
   DGDS_CUDA(cudaSetDevice(s->p.device));
   return speculate_submit(s, n, handles, pat_offs, patterns, args, args_stride, truth, truth_stride, truth_left,
                           limit, truth != nullptr, ticket);
@@ -1752,6 +1960,7 @@ int dgds_speculate_wait(dgds_server* s, uint64_t ticket, dgds_result_view* out) 
   if (!s || !out) return fail(DGDS_EINVAL, "null argument");
   *out = dgds_result_view{};
   std::lock_guard<std::mutex> lk(s->mu);
+  // host state only: no flush
   DGDS_CUDA(cudaSetDevice(s->p.device));
   HostResult r;
   if (int rc = speculate_finish(s, ticket, &r)) return rc;
@@ -1780,6 +1989,7 @@ int dgds_speculate_device(dgds_server* s, int64_t n, const int32_t* d_handles, c
   if (d_out && (d_out->k_stride < max_top_k || d_out->s_stride < 1)) return fail(DGDS_EBUFFER, "bad output strides");
   if (d_vout && (!d_truth || !d_truth_left || !d_limit)) return fail(DGDS_EINVAL, "verify needs truth inputs");
   std::lock_guard<std::mutex> lk(s->mu);
+  if (int rc_ = flush_pending(s)) return rc_;
   DGDS_CUDA(cudaSetDevice(s->p.device));
   StreamJoin join(s, stream);
   dgds::QueryLaunch L{};
@@ -1842,6 +2052,7 @@ static int speculate_records_impl(dgds_server* s, int64_t n, const int32_t* d_re
   if (y.rec_words - y.off_pattern < s->p.max_pattern_len)
     return fail(DGDS_EINVAL, "query record pattern field shorter than max_pattern_len");
   std::lock_guard<std::mutex> lk(s->mu);
+  if (int rc_ = flush_pending(s)) return rc_;
   DGDS_CUDA(cudaSetDevice(s->p.device));
   StreamJoin join(s, stream);
   dgds::QueryLaunch L{};
@@ -1916,6 +2127,7 @@ int dgds_verify_batch(dgds_server* s, int64_t n, const dgds_candidates* c, const
   if (n < 0) return fail(DGDS_EINVAL, "negative batch size");
   if (n == 0) return DGDS_OK;
   std::lock_guard<std::mutex> lk(s->mu);
+  if (int rc_ = flush_pending(s)) return rc_;
   DGDS_CUDA(cudaSetDevice(s->p.device));
   const int K = c->k_stride, Sx = c->s_stride;
   const size_t o_ln = align_up(n * 4, 256);
@@ -1963,6 +2175,7 @@ int32_t dgds_draft_len(int32_t sd_enabled, int32_t adaptive, int32_t cap, int32_
 // Debug: record per-query phase cycles of device-API query launches into d_buf[n][8].
 int dgds_debug_query_timing(dgds_server* s, void* d_buf) {
   std::lock_guard<std::mutex> lk(s->mu);
+  // host state only: no flush
   s->d_dbg = static_cast<long long*>(d_buf);
   return DGDS_OK;
 }
@@ -1974,12 +2187,14 @@ int dgds_last_transfer(dgds_server* s, uint64_t* d2h_bytes) {
 
 int dgds_profile_enable(dgds_server* s, int32_t on) {
   std::lock_guard<std::mutex> lk(s->mu);
+  // host state only: no flush
   s->profiling = on != 0;
   return DGDS_OK;
 }
 
 int dgds_profile_read(dgds_server* s, dgds_profile* out, int32_t reset) {
   std::lock_guard<std::mutex> lk(s->mu);
+  if (int rc_ = flush_pending(s)) return rc_;
   DGDS_CUDA(cudaSetDevice(s->p.device));
   for (int k = 0; k < 2; ++k) {
     for (auto& pr : s->ev_pending[k]) {
@@ -2125,6 +2340,7 @@ int dgds_fetch_cst(dgds_server* s, int64_t n, const int32_t* handles, const uint
                    dgds_fetch_reply* rep, const uint8_t** blobs) {
   if (!s || n < 0 || (n > 0 && (!handles || !cached || !rep || !blobs))) return fail(DGDS_EINVAL, "null argument");
   std::lock_guard<std::mutex> lk(s->mu);
+  if (int rc_ = flush_pending(s)) return rc_;
   DGDS_CUDA(cudaSetDevice(s->p.device));
   for (int64_t i = 0; i < n; ++i)
     if (int rc = check_handle(s, handles[i])) return rc;
@@ -2225,6 +2441,7 @@ int dgds_fetch_cst(dgds_server* s, int64_t n, const int32_t* handles, const uint
 int dgds_compact_group(dgds_server* s, int32_t h, uint64_t before_version) {  // dgds.cpp:153-158, cst.cpp:324-329
   if (!s) return fail(DGDS_EINVAL, "null server");
   std::lock_guard<std::mutex> lk(s->mu);
+  if (int rc_ = flush_pending(s)) return rc_;
   if (int rc = check_handle(s, h)) return rc;
   GroupRec& g = s->groups[h];
   if (!g.alive) return DGDS_OK;
@@ -2238,6 +2455,7 @@ int dgds_compact_group(dgds_server* s, int32_t h, uint64_t before_version) {  //
 int dgds_apply_blob(dgds_server* s, int32_t h, const uint8_t* blob, uint64_t len, double now, uint64_t* version) {
   if (!s || (!blob && len)) return fail(DGDS_EINVAL, "null argument");
   std::lock_guard<std::mutex> lk(s->mu);
+  if (int rc_ = flush_pending(s)) return rc_;
   if (int rc = check_handle(s, h)) return rc;
   GroupRec& g = s->groups[h];
   BlobReader r{blob, blob + len};
@@ -2353,6 +2571,7 @@ int dgds_batch_speculate_zc(dgds_server* s, int64_t n, const int32_t* d_handles,
   if (y.reply_words < 1 || (y.off_scores & 1) || (y.off_supports & 1))
     return fail(DGDS_EINVAL, "bad reply layout (8-byte fields must be even)");
   std::lock_guard<std::mutex> lk(s->mu);
+  if (int rc_ = flush_pending(s)) return rc_;
   DGDS_CUDA(cudaSetDevice(s->p.device));
   StreamJoin join(s, stream);
   dgds::QueryLaunch L{};
@@ -2395,6 +2614,7 @@ int dgds_batch_speculate_zc(dgds_server* s, int64_t n, const int32_t* d_handles,
 extern "C" int dgds_touch_group(dgds_server* s, int32_t h, double now) {  // update_cst before append (dgds.cpp:39-48)
   if (!s) return fail(DGDS_EINVAL, "null server");
   std::lock_guard<std::mutex> lk(s->mu);
+  if (int rc_ = flush_pending(s)) return rc_;
   if (int rc = check_handle(s, h)) return rc;
   GroupRec& g = s->groups[h];
   if (!live_entry(s, g, now))
@@ -2462,6 +2682,7 @@ extern "C" {
 int dgds_compact_memory(dgds_server* s) {
   if (!s) return fail(DGDS_EINVAL, "null server");
   std::lock_guard<std::mutex> lk(s->mu);
+  if (int rc_ = flush_pending(s)) return rc_;
   DGDS_CUDA(cudaSetDevice(s->p.device));
   return compact_memory(s);
 }
@@ -2469,6 +2690,7 @@ int dgds_compact_memory(dgds_server* s) {
 int dgds_get_memory_stats(dgds_server* s, dgds_memory_stats* out) {
   if (!s || !out) return fail(DGDS_EINVAL, "null argument");
   std::lock_guard<std::mutex> lk(s->mu);
+  if (int rc_ = flush_pending(s)) return rc_;
   DGDS_CUDA(cudaSetDevice(s->p.device));
   uint64_t used = 0;
   if (int rc = read_used(s, &used)) return rc;
@@ -2488,6 +2710,7 @@ extern "C" int dgds_debug_append_timing(dgds_server* s, uint64_t* out, int64_t n
   if (!s || !out) return fail(DGDS_EINVAL, "null argument");
   if (!s->T.dbg) return fail(DGDS_ESTATE, "set DGDS_APPEND_DBG before dgds_create");
   std::lock_guard<std::mutex> lk(s->mu);
+  if (int rc_ = flush_pending(s)) return rc_;
   DGDS_CUDA(cudaStreamSynchronize(s->st));
   DGDS_CUDA(cudaMemcpy(out, s->T.dbg, std::min<int64_t>(n_warps, 65536) * 16, cudaMemcpyDeviceToHost));
   return DGDS_OK;

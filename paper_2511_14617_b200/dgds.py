@@ -397,8 +397,9 @@ class DraftServer:
     def speculate_submit(self, handles: np.ndarray, pat_offsets: np.ndarray, patterns: np.ndarray, args: np.ndarray,
                          args_stride: int, truth: Optional[np.ndarray] = None,
                          truth_left: Optional[np.ndarray] = None, limit: Optional[np.ndarray] = None) -> int:
-        """Asynchronous speculate_view (dgds_speculate_submit): stages and launches the batch,
-        returns a ticket for speculate_wait. Two batches can be in flight."""
+        """Asynchronous speculate_view (dgds_speculate_submit): validates, starts staging and
+        returns a ticket for speculate_wait. Two batches can be in flight. The input arrays are
+        read asynchronously; this object keeps them alive until the ticket is waited on."""
         n = len(handles)
         handles = np.ascontiguousarray(handles, np.int32)
         pat_offsets = np.ascontiguousarray(pat_offsets, np.uint64)
@@ -415,12 +416,19 @@ class DraftServer:
         else:
             check(lib().dgds_speculate_submit(self._h, n, _ptr(handles), _ptr(pat_offsets), _ptr(patterns),
                                               _ptr(args), args_stride, None, 0, None, None, C.byref(t)))
-        return int(t.value)
+            tl = lm = None
+        tk = int(t.value)
+        inflight = self.__dict__.setdefault("_inflight", {})
+        for old in [k for k in inflight if k <= tk - 2]:  # their slots are reused: inputs long read
+            del inflight[old]
+        inflight[tk] = (handles, pat_offsets, patterns, args, truth, tl, lm)
+        return tk
 
     def speculate_wait(self, ticket: int) -> "ResultView":
         """Results of a submitted batch (zero-copy views, valid until two batches later)."""
         v = _lib.ResultView()
         check(lib().dgds_speculate_wait(self._h, ticket, C.byref(v)))
+        self.__dict__.get("_inflight", {}).pop(ticket, None)
         return ResultView(v)
 
     def verify_batch(self, cands: "CandidateBatch", truth: np.ndarray, truth_left: np.ndarray, limit: np.ndarray):
