@@ -294,6 +294,8 @@ def run_multi(args, world, rank, local, dev):
             ev_rep[k].record(main)
             t0 = mark("q_rev", t0)
         else:
+            if "ready" in inp:  # e2e: inputs copied in on the copy stream
+                main.wait_event(inp["ready"])
             # (1) queries -> owners (static splits, no host sync)
             rq, st_q = router.forward(inp["q_owner"], inp["q"], capq)
             t0 = mark("q_fwd", t0)
@@ -373,13 +375,6 @@ def run_multi(args, world, rank, local, dev):
             back = nxt if nxt is not None else back
         return back
 
-    def step(s, stats):
-        """One tick, unpipelined (the e2e loop)."""
-        run_until[0] = max(run_until[0], s + 1)
-        back = q_part(s, stats)
-        a_part(s, stats)
-        return back
-
     run_ticks(0, W, False)
     torch.cuda.synchronize()
     prof = _lib.Profile()
@@ -428,30 +423,80 @@ def run_multi(args, world, rank, local, dev):
         host_in = [{k: (v.cpu().pin_memory() if torch.is_tensor(v) else v) for k, v in steps_in[s].items()}
                    for s in range(W + K, W + K + E)]
         h2d = sum(x["app"].nbytes + x["app_owner"].nbytes + x["q"].nbytes + x["q_owner"].nbytes for x in host_in)
+        cp = torch.cuda.Stream(dev)  # input H2D beside the kernels
+        main = torch.cuda.current_stream(dev)
+        keys = ("app", "app_owner", "q", "q_owner")
+        # device input sets and pinned reply buffers, double-buffered and allocated up front (an
+        # allocation inside the loop is a device-synchronising cudaMalloc / cudaHostAlloc)
+        d_sets = [{k: torch.empty((max(x[k].shape[0] for x in host_in),) + tuple(host_in[0][k].shape[1:]),
+                                  dtype=host_in[0][k].dtype, device=dev) for k in keys} for _ in range(2)]
+        ev_in_free = [torch.cuda.Event(), torch.cuda.Event()]
+        back_h = [torch.empty((Q, rep_w), dtype=torch.int32).pin_memory() for _ in range(2)]
+        ev_back = [torch.cuda.Event(), torch.cuda.Event()]
+        emitted = [0]
+        col_em = off_v + 2  # verify words: drafted | accepted | emitted
+
+        def issue_inputs(j):
+            buf = d_sets[j % 2]
+            with torch.cuda.stream(cp):
+                if j >= 2:  # set j%2 was read by tick j-2's exchanges, all done before its K1 was queued
+                    cp.wait_event(ev_in_free[j % 2])
+                d_in = {}
+                for k in keys:
+                    v = buf[k][:host_in[j][k].shape[0]]
+                    v.copy_(host_in[j][k], non_blocking=True)
+                    d_in[k] = v
+                d_in["ready"] = torch.cuda.Event()
+                d_in["ready"].record(cp)
+            steps_in.append(d_in)
+
+        def d2h_replies(j, back):
+            # enqueued right after the tick's reply wait on the main stream: the owners' replies of
+            # tick j+2 reuse this slab parity only after that stream passes tick j+1's reply wait
+            back_h[j % 2].copy_(back, non_blocking=True)
+            ev_back[j % 2].record(main)
+            return back_h[j % 2].nbytes
+
+        def consume(j):
+            ev_back[j % 2].synchronize()
+            emitted[0] += int(back_h[j % 2][:, col_em].sum())
+
         dist.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         d2h = 0
         base_s = len(steps_in)
         run_until[0] = base_s + E
-        back_h = None
-        for j, hin in enumerate(host_in):
-            d_in = {k: hin[k].to(dev, non_blocking=True) for k in ("app", "app_owner", "q", "q_owner")}
-            d_in["ready"] = torch.cuda.Event()
-            d_in["ready"].record(torch.cuda.current_stream(dev))
-            steps_in.append(d_in)
-            back = step(base_s + j, False)
-            if back_h is None:
-                back_h = torch.empty(back.shape, dtype=back.dtype).pin_memory()  # the step's replies land here
-            back_h.copy_(back, non_blocking=True)
-            torch.cuda.current_stream(dev).synchronize()
-            d2h += back_h.nbytes
+        # pipelined like the single-GPU e2e loop: tick j+1's inputs, exchanges and queries are
+        # queued before tick j's replies are read on the host
+        issue_inputs(0)
+        d2h += d2h_replies(0, q_part(base_s, False))
+        e2e_trace = [] if os.environ.get("DGDS_MULTI_E2E_TRACE") == "1" else None  # host µs per phase (debug)
+        for j in range(E):
+            ta = time.perf_counter()
+            if j + 1 < E:
+                issue_inputs(j + 1)
+            tb = time.perf_counter()
+            nxt = a_part(base_s + j, False, pipeline=use_px)
+            ev_in_free[j % 2].record(main)  # after tick j's K1 was queued behind its exchanges
+            if not use_px and j + 1 < E:
+                nxt = q_part(base_s + j + 1, False)
+            tc = time.perf_counter()
+            if nxt is not None:
+                d2h += d2h_replies(j + 1, nxt)
+            td = time.perf_counter()
+            consume(j)
+            if e2e_trace is not None:
+                e2e_trace.append([round(1e6 * x) for x in (tb - ta, tc - tb, td - tc, time.perf_counter() - td)])
+        if e2e_trace is not None:
+            print(f"rank {rank} e2e inputs|a_part|d2h|consume us:", e2e_trace, flush=True)
         torch.cuda.synchronize()
         dt = torch.tensor([time.perf_counter() - t0], device=dev)
         dist.all_reduce(dt, op=dist.ReduceOp.MAX)
         e2e = {"value": world * Q * E / dt.item(), "unit": "queries/s", "h2d_bytes_per_step": h2d // E,
                "d2h_bytes_per_step": d2h // E, "steps": E,
-               "path": "routed step, pinned host records in / replies out (rank-local view)"}
+               "path": ("routed ticks, pinned host records in (copy stream) / reply records out, every emitted "
+                        "count read; tick j+1 is queued before tick j's replies are read")}
 
     if dbg or host_t:
         print(f"rank {rank} breakdown (s, all steps):",
