@@ -21,6 +21,7 @@ from __future__ import annotations
 
 import argparse
 import ctypes as C
+import gc
 import json
 import os
 import statistics
@@ -109,6 +110,10 @@ class ClockSampler:
             time.sleep(0.002)
 
     def __enter__(self):
+        # the timed region runs without the cyclic GC (a collection is a multi-ms host stall,
+        # and at N>1 one rank's stall holds every rank at the next exchange); callers collect
+        # before their barrier, so the ranks enter the region together
+        gc.disable()
         if self.nv:
             self._t = threading.Thread(target=self._run, daemon=True)
             self._t.start()
@@ -118,6 +123,7 @@ class ClockSampler:
         self._stop.set()
         if self._t:
             self._t.join()
+        gc.enable()
 
     def summary(self):
         return {"sm_mhz": statistics.median(self.samples) if self.samples else None, "sm_max_mhz": self.max_mhz,
@@ -407,6 +413,7 @@ def main_b200(args):
     _lib.check(L.dgds_profile_enable(srv.handle, 1))
     _lib.check(L.dgds_profile_read(srv.handle, C.byref(prof), 1))
     d_stats.zero_()
+    gc.collect()
     torch.cuda.synchronize()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)

@@ -12,6 +12,7 @@ inverse all-to-all. Timing: CUDA events on the step stream, max over ranks.
 from __future__ import annotations
 
 import ctypes as C
+import gc
 import json
 import os
 import time
@@ -382,6 +383,7 @@ def run_multi(args, world, rank, local, dev):
     _lib.check(L.dgds_profile_read(srv.handle, C.byref(prof), 1))
     d_stats.zero_()
     px_l0 = px.status()[1] if use_px else 0
+    gc.collect()
     dist.barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
