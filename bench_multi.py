@@ -433,10 +433,10 @@ def run_multi(args, world, rank, local, dev):
         d_sets = [{k: torch.empty((max(x[k].shape[0] for x in host_in),) + tuple(host_in[0][k].shape[1:]),
                                   dtype=host_in[0][k].dtype, device=dev) for k in keys} for _ in range(2)]
         ev_in_free = [torch.cuda.Event(), torch.cuda.Event()]
-        back_h = [torch.empty((Q, rep_w), dtype=torch.int32).pin_memory() for _ in range(2)]
-        ev_back = [torch.cuda.Event(), torch.cuda.Event()]
         emitted = [0]
-        col_em = off_v + 2  # verify words: drafted | accepted | emitted
+        tickets = {}
+        view = _lib.ResultView()
+        last = C.c_uint64()
 
         def issue_inputs(j):
             buf = d_sets[j % 2]
@@ -453,16 +453,26 @@ def run_multi(args, world, rank, local, dev):
             steps_in.append(d_in)
 
         def d2h_replies(j, back):
-            # enqueued right after the tick's reply wait on the main stream: the owners' replies of
-            # tick j+2 reuse this slab parity only after that stream passes tick j+1's reply wait
-            back_h[j % 2].copy_(back, non_blocking=True)
-            ev_back[j % 2].record(main)
-            return back_h[j % 2].nbytes
+            # the tick's reply records, compacted on the main stream right after its reply wait (the
+            # owners' replies of tick j+2 reuse this slab parity only after that stream passes tick
+            # j+1's reply wait), then copied out over PCIe into the server's next result slot
+            tk = C.c_uint64()
+            _lib.check(L.dgds_replies_submit(srv.handle, back.shape[0], C.c_void_p(back.data_ptr()),
+                                             C.byref(layout), kq, dl, C.c_void_p(main.cuda_stream), C.byref(tk)))
+            tickets[j] = int(tk.value)
 
         def consume(j):
-            ev_back[j % 2].synchronize()
-            emitted[0] += int(back_h[j % 2][:, col_em].sum())
+            _lib.check(L.dgds_speculate_wait(srv.handle, tickets.pop(j), C.byref(view)))
+            emitted[0] += int(np.ctypeslib.as_array(C.cast(view.emitted, C.POINTER(C.c_int32)), shape=(Q,)).sum())
+            _lib.check(L.dgds_last_transfer(srv.handle, C.byref(last)))
+            return int(last.value)
 
+        warm = torch.zeros((Q, rep_w), dtype=torch.int32, device=dev)  # both result slots reach their size
+        for j in range(2):
+            d2h_replies(-1 - j, warm)
+            consume(-1 - j)
+        emitted[0] = 0
+        gc.collect()
         dist.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
@@ -472,7 +482,7 @@ def run_multi(args, world, rank, local, dev):
         # pipelined like the single-GPU e2e loop: tick j+1's inputs, exchanges and queries are
         # queued before tick j's replies are read on the host
         issue_inputs(0)
-        d2h += d2h_replies(0, q_part(base_s, False))
+        d2h_replies(0, q_part(base_s, False))
         e2e_trace = [] if os.environ.get("DGDS_MULTI_E2E_TRACE") == "1" else None  # host µs per phase (debug)
         for j in range(E):
             ta = time.perf_counter()
@@ -485,9 +495,9 @@ def run_multi(args, world, rank, local, dev):
                 nxt = q_part(base_s + j + 1, False)
             tc = time.perf_counter()
             if nxt is not None:
-                d2h += d2h_replies(j + 1, nxt)
+                d2h_replies(j + 1, nxt)
             td = time.perf_counter()
-            consume(j)
+            d2h += consume(j)
             if e2e_trace is not None:
                 e2e_trace.append([round(1e6 * x) for x in (tb - ta, tc - tb, td - tc, time.perf_counter() - td)])
         if e2e_trace is not None:
@@ -497,8 +507,9 @@ def run_multi(args, world, rank, local, dev):
         dist.all_reduce(dt, op=dist.ReduceOp.MAX)
         e2e = {"value": world * Q * E / dt.item(), "unit": "queries/s", "h2d_bytes_per_step": h2d // E,
                "d2h_bytes_per_step": d2h // E, "steps": E,
-               "path": ("routed ticks, pinned host records in (copy stream) / reply records out, every emitted "
-                        "count read; tick j+1 is queued before tick j's replies are read")}
+               "path": ("routed ticks, pinned host records in (copy stream); each tick's reply records compacted "
+                        "into a CSR result view in pinned memory (dgds_replies_submit / dgds_speculate_wait), every "
+                        "emitted count read; tick j+1 is queued before tick j's replies are read")}
 
     if dbg or host_t:
         print(f"rank {rank} breakdown (s, all steps):",

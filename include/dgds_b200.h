@@ -301,6 +301,14 @@ int dgds_speculate_submit(dgds_server* s, int64_t n, const int32_t* handles, con
                           const int32_t* limit, uint64_t* ticket);
 int dgds_speculate_wait(dgds_server* s, uint64_t ticket, dgds_result_view* out);
 
+/* Compact n reply records (dgds_query_record_layout; e.g. the routed replies a sender
+ * gathers in peer memory) into the same CSR result view, in the server's next result slot:
+ * compaction on `stream` after the records are complete, then a PCIe copy-out into mapped
+ * pinned memory. Returns a ticket for dgds_speculate_wait; max_spec is the reply's token row
+ * stride. The records may be overwritten once the work queued on `stream` here has run. */
+int dgds_replies_submit(dgds_server* s, int64_t n, const int32_t* d_replies, const dgds_query_record_layout* lay,
+                        int32_t max_top_k, int32_t max_spec, void* stream, uint64_t* ticket);
+
 /* Segmented form for owner routing: rows arrive as n_seg sender segments of seg_rows rows
  * (row j of segment s valid while j < d_seg_count[s]); the reply of row j of segment s is
  * written to seg_out[s] + r * reply_words with r = j, or with origin_field >= 0 r = the

@@ -1330,13 +1330,12 @@ namespace {
 
 constexpr int kCmpBlock = 256;
 
-__global__ void k_cmp_count(int64_t n, int32_t K, const int32_t* __restrict__ n_cands,
-                            const int32_t* __restrict__ lens, long long* block_sums) {
+__global__ void k_cmp_count(int64_t n, CmpIn in, long long* block_sums) {
   const int64_t q = static_cast<int64_t>(blockIdx.x) * kCmpBlock + threadIdx.x;
   int c = 0, t = 0;
   if (q < n) {
-    c = n_cands[q];
-    for (int j = 0; j < c; ++j) t += lens[q * K + j];
+    c = in.n_cands[q * in.qs_nc];
+    for (int j = 0; j < c; ++j) t += in.lens[q * in.qs_len + j];
   }
   using BS = cub::BlockScan<int, kCmpBlock>;
   __shared__ typename BS::TempStorage tmp;
@@ -1385,16 +1384,13 @@ __global__ void __launch_bounds__(kCmpBlock) k_cmp_scan(int64_t nblocks, long lo
   }
 }
 
-__global__ void k_cmp_scatter(int64_t n, int32_t K, int32_t S, const int32_t* __restrict__ n_cands,
-                              const int32_t* __restrict__ lens, const double* __restrict__ scores,
-                              const int64_t* __restrict__ supports, const int32_t* __restrict__ tokens,
-                              const long long* __restrict__ block_sums, CandMeta* meta, int32_t* tok_out,
-                              int64_t* cand_off, int64_t* tok_off) {
+__global__ void k_cmp_scatter(int64_t n, CmpIn in, const long long* __restrict__ block_sums, CandMeta* meta,
+                              int32_t* tok_out, int64_t* cand_off, int64_t* tok_off, int32_t* v_out) {
   const int64_t q = static_cast<int64_t>(blockIdx.x) * kCmpBlock + threadIdx.x;
   int c = 0, t = 0;
   if (q < n) {
-    c = n_cands[q];
-    for (int j = 0; j < c; ++j) t += lens[q * K + j];
+    c = in.n_cands[q * in.qs_nc];
+    for (int j = 0; j < c; ++j) t += in.lens[q * in.qs_len + j];
   }
   using BS = cub::BlockScan<int, kCmpBlock>;
   __shared__ typename BS::TempStorage tmp;
@@ -1406,13 +1402,15 @@ __global__ void k_cmp_scatter(int64_t n, int32_t K, int32_t S, const int32_t* __
   long long cb = block_sums[2 * blockIdx.x] + co, tb = block_sums[2 * blockIdx.x + 1] + to;
   if (cand_off) cand_off[q] = cb;
   for (int j = 0; j < c; ++j) {
-    const int64_t si = q * K + j;
-    const int L = lens[si];
-    meta[cb + j] = CandMeta{scores[si], supports[si], L, 0};
+    const int L = in.lens[q * in.qs_len + j];
+    meta[cb + j] = CandMeta{in.scores[q * in.qs_sc + j], in.supports[q * in.qs_sp + j], L, 0};
     if (tok_off) tok_off[cb + j] = tb;
-    for (int i = 0; i < L; ++i) tok_out[tb + i] = tokens[si * S + i];
+    const int32_t* src = in.tokens + q * in.qs_tok + static_cast<int64_t>(j) * in.cs_tok;
+    for (int i = 0; i < L; ++i) tok_out[tb + i] = src[i];
     tb += L;
   }
+  if (in.verify && v_out)  // drafted | accepted | emitted -> [3][n]
+    for (int k = 0; k < 3; ++k) v_out[k * n + q] = in.verify[q * in.qs_v + k];
 }
 
 // Device -> (mapped) host copy of regions whose sizes are only known on the device:
@@ -1445,17 +1443,35 @@ __global__ void k_copy_out(const long long* __restrict__ totals, CopyOutRegions 
 
 }  // namespace
 
+cudaError_t launch_compact_in(int64_t n, const CmpIn& in, long long* block_sums, long long* totals, CandMeta* meta,
+                              int32_t* tok_out, int64_t* cand_off, int64_t* tok_off, int32_t* v_out,
+                              const long long* carry_in, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  const int64_t nb = (n + kCmpBlock - 1) / kCmpBlock;
+  k_cmp_count<<<static_cast<unsigned>(nb), kCmpBlock, 0, st>>>(n, in, block_sums);
+  k_cmp_scan<<<1, kCmpBlock, 0, st>>>(nb, block_sums, totals, carry_in);
+  k_cmp_scatter<<<static_cast<unsigned>(nb), kCmpBlock, 0, st>>>(n, in, block_sums, meta, tok_out, cand_off, tok_off,
+                                                                  v_out);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_compact(int64_t n, int32_t K, int32_t S, const int32_t* n_cands, const int32_t* lens,
                            const double* scores, const int64_t* supports, const int32_t* tokens,
                            long long* block_sums, long long* totals, CandMeta* meta, int32_t* tok_out,
                            int64_t* cand_off, int64_t* tok_off, const long long* carry_in, cudaStream_t st) {
-  if (n <= 0) return cudaSuccess;
-  const int64_t nb = (n + kCmpBlock - 1) / kCmpBlock;
-  k_cmp_count<<<static_cast<unsigned>(nb), kCmpBlock, 0, st>>>(n, K, n_cands, lens, block_sums);
-  k_cmp_scan<<<1, kCmpBlock, 0, st>>>(nb, block_sums, totals, carry_in);
-  k_cmp_scatter<<<static_cast<unsigned>(nb), kCmpBlock, 0, st>>>(n, K, S, n_cands, lens, scores, supports, tokens,
-                                                                  block_sums, meta, tok_out, cand_off, tok_off);
-  return cudaGetLastError();
+  CmpIn in{};  // the query kernel's internal SoA outputs
+  in.n_cands = n_cands;
+  in.qs_nc = 1;
+  in.lens = lens;
+  in.qs_len = K;
+  in.scores = scores;
+  in.qs_sc = K;
+  in.supports = supports;
+  in.qs_sp = K;
+  in.tokens = tokens;
+  in.qs_tok = static_cast<int64_t>(K) * S;
+  in.cs_tok = S;
+  return launch_compact_in(n, in, block_sums, totals, meta, tok_out, cand_off, tok_off, nullptr, carry_in, st);
 }
 
 cudaError_t launch_copy_out(const long long* totals, const CopyOutRegions& R, int64_t max_bytes, cudaStream_t st,

@@ -166,6 +166,27 @@ struct CopyOutRegions {
 cudaError_t launch_copy_out(const long long* totals, const CopyOutRegions& R, int64_t max_bytes, cudaStream_t st,
                             int max_blocks = 592);
 
+// Compaction input: per-query candidate fields at query strides (elements), e.g. the query
+// kernel's SoA outputs or fixed-size reply records.
+struct CmpIn {
+  const int32_t* n_cands;
+  int64_t qs_nc;
+  const int32_t* lens;  // lens[q * qs_len + j]
+  int64_t qs_len;
+  const double* scores;
+  int64_t qs_sc;
+  const int64_t* supports;
+  int64_t qs_sp;
+  const int32_t* tokens;  // tokens[q * qs_tok + j * cs_tok + i]
+  int64_t qs_tok;
+  int32_t cs_tok;
+  const int32_t* verify;  // optional: drafted, accepted, emitted at verify[q * qs_v + 0..2]
+  int64_t qs_v;
+};
+cudaError_t launch_compact_in(int64_t n, const CmpIn& in, long long* block_sums, long long* totals, CandMeta* meta,
+                              int32_t* tok_out, int64_t* cand_off, int64_t* tok_off, int32_t* v_out,
+                              const long long* carry_in, cudaStream_t st);
+
 // block_sums: 2 * ceil(n / 256) scratch; totals[0] = candidates, totals[1] = tokens, both
 // counted from carry_in (optional: the totals of an earlier chunk, so chunks of one batch
 // compact into one CSR). Outputs may live in mapped pinned host memory.

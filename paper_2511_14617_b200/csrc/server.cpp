@@ -1968,6 +1968,100 @@ int dgds_speculate_wait(dgds_server* s, uint64_t ticket, dgds_result_view* out) 
   return DGDS_OK;
 }
 
+int dgds_replies_submit(dgds_server* s, int64_t n, const int32_t* d_replies, const dgds_query_record_layout* lay,
+                        int32_t max_top_k, int32_t max_spec, void* stream, uint64_t* ticket) {
+  if (!s || !lay || !d_replies || !ticket) return fail(DGDS_EINVAL, "null argument");
+  if (n <= 0) return fail(DGDS_EINVAL, "submit needs a non-empty batch");
+  if (max_top_k < 1 || max_top_k > DGDS_MAX_TOP_K) return fail(DGDS_EUNSUPPORTED, "max_top_k out of range");
+  if (max_spec < 1) return fail(DGDS_EINVAL, "max_spec must be >= 1");
+  const dgds_query_record_layout& y = *lay;
+  if (y.reply_words < 1 || (y.reply_words & 1) || (y.off_scores & 1) || (y.off_supports & 1))
+    return fail(DGDS_EINVAL, "bad record layout (reply words and 8-byte fields must be even)");
+  std::lock_guard<std::mutex> lk(s->mu);
+  if (int rc = flush_pending(s)) return rc;
+  DGDS_CUDA(cudaSetDevice(s->p.device));
+  StreamJoin join(s, stream);
+  const cudaStream_t js = join.stream();
+  const uint64_t tk = s->last_ticket + 1;
+  dgds_server::QSlot& slot = s->qslot[tk % dgds_server::kQSlots];
+  DGDS_CUDA(cudaEventSynchronize(slot.done));  // the slot's previous batch is complete
+  slot.ticket = 0;
+  const bool verify = y.off_verify >= 0;
+  const int32_t K = max_top_k, Sx = max_spec;
+  const int64_t nk = n * K;
+  // device: block sums | totals | meta | tok_off | cand_off | tokens | verify [3][n]
+  const int64_t nblk = (n + 255) / 256;
+  const size_t o_bs = 0;
+  const size_t o_tot = align_up(o_bs + static_cast<size_t>(nblk) * 16, 256);
+  const size_t o_cmeta = align_up(o_tot + 16, 256);
+  const size_t o_ctoff = align_up(o_cmeta + nk * sizeof(dgds::CandMeta), 256);
+  const size_t o_ccoff = align_up(o_ctoff + nk * 8, 256);
+  const size_t o_ctok = align_up(o_ccoff + (n + 1) * 8, 256);
+  const size_t o_v = align_up(o_ctok + static_cast<size_t>(nk) * Sx * 4, 256);
+  const size_t dev_total = o_v + (verify ? n * 12 : 0);
+  slot.h_coff = 256;  // totals | cand_off | verify | meta | tok_off | tokens
+  slot.h_v = align_up(slot.h_coff + (n + 1) * 8, 256);
+  slot.h_meta = align_up(slot.h_v + (verify ? n * 12 : 0), 256);
+  slot.h_toff = align_up(slot.h_meta + nk * sizeof(dgds::CandMeta), 256);
+  slot.h_tok = align_up(slot.h_toff + (nk + 1) * 8, 256);
+  if (int rc = slot.dout.ensure(dev_total)) return rc;
+  if (int rc = slot.ho.ensure(slot.h_tok + static_cast<size_t>(nk) * Sx * 4)) return rc;
+  char* dout = static_cast<char*>(slot.dout.p);
+  char* ho = static_cast<char*>(slot.ho.p);
+  long long* d_bs = reinterpret_cast<long long*>(dout + o_bs);
+  long long* d_tot = reinterpret_cast<long long*>(dout + o_tot);
+  auto* d_meta = reinterpret_cast<dgds::CandMeta*>(dout + o_cmeta);
+  auto* d_toff = reinterpret_cast<int64_t*>(dout + o_ctoff);
+  auto* d_coff = reinterpret_cast<int64_t*>(dout + o_ccoff);
+  int32_t* d_ctok = reinterpret_cast<int32_t*>(dout + o_ctok);
+  int32_t* d_v = reinterpret_cast<int32_t*>(dout + o_v);
+  dgds::CmpIn in{};  // reply records: int32 fields at stride reply_words, 8-byte fields at reply_words / 2
+  in.n_cands = d_replies + y.off_n_cands;
+  in.qs_nc = y.reply_words;
+  in.lens = d_replies + y.off_lens;
+  in.qs_len = y.reply_words;
+  in.scores = reinterpret_cast<const double*>(d_replies + y.off_scores);
+  in.qs_sc = y.reply_words / 2;
+  in.supports = reinterpret_cast<const int64_t*>(d_replies + y.off_supports);
+  in.qs_sp = y.reply_words / 2;
+  in.tokens = d_replies + y.off_tokens;
+  in.qs_tok = y.reply_words;
+  in.cs_tok = max_spec;
+  in.verify = verify ? d_replies + y.off_verify : nullptr;
+  in.qs_v = y.reply_words;
+  DGDS_CUDA(dgds::launch_compact_in(n, in, d_bs, d_tot, d_meta, d_ctok, d_coff, d_toff, verify ? d_v : nullptr,
+                                    nullptr, js));
+  // the copy-out (PCIe-bound) runs on out_st, so the caller's stream moves on
+  DGDS_CUDA(cudaEventRecord(s->ev_cmp[0], js));
+  DGDS_CUDA(cudaStreamWaitEvent(s->out_st, s->ev_cmp[0], 0));
+  dgds::CopyOutRegions R{};
+  auto region = [&](const void* src, char* dst, int tot, int elem, int64_t fixed) {
+    const int i = R.n++;
+    R.src[i] = static_cast<const char*>(src);
+    R.dst[i] = dst;
+    R.total_idx[i] = tot;
+    R.begin_idx[i] = -1;
+    R.elem_bytes[i] = elem;
+    R.fixed_bytes[i] = fixed;
+  };
+  region(d_coff, ho + slot.h_coff, -1, 0, n * 8);
+  if (verify) region(d_v, ho + slot.h_v, -1, 0, n * 12);
+  region(d_meta, ho + slot.h_meta, 0, sizeof(dgds::CandMeta), 0);
+  region(d_toff, ho + slot.h_toff, 0, 8, 0);
+  region(d_ctok, ho + slot.h_tok, 1, 4, 0);
+  region(d_tot, ho, -1, 0, 16);
+  DGDS_CUDA(dgds::launch_copy_out(d_tot, R, nk * static_cast<int64_t>(sizeof(dgds::CandMeta) + 8 + Sx * 4),
+                                  s->out_st));
+  DGDS_CUDA(cudaEventRecord(slot.done, s->out_st));
+  slot.ticket = tk;
+  slot.n = n;
+  slot.verify = verify;
+  slot.err = DGDS_OK;
+  s->last_ticket = tk;
+  *ticket = tk;
+  return DGDS_OK;
+}
+
 int dgds_speculate_batch(dgds_server* s, int64_t n, const int32_t* handles, const uint64_t* pat_offs,
                          const int32_t* patterns, const dgds_spec_args* args, int64_t args_stride,
                          dgds_candidates* out) {
