@@ -735,6 +735,7 @@ int plan_updates(dgds_server* s, int64_t n, const int32_t* handles, const int32_
   }
   std::mutex gmu;
   std::atomic<uint64_t> hist_at{s->hist_used};
+  uint64_t hist_one = s->hist_used;
   auto work = [&](int w) {
     Part& P = parts[w];
     if (W > 1) cudaSetDevice(s->p.device);
@@ -786,7 +787,13 @@ int plan_updates(dgds_server* s, int64_t n, const int32_t* handles, const int32_
         sg.start = sr.stored;
         P.segs.push_back(sg);
       }
-      const uint64_t hoff = hist_at.fetch_add(cnt, std::memory_order_relaxed);
+      uint64_t hoff;
+      if (W == 1) {  // single planner: no locked read-modify-write per record
+        hoff = hist_one;
+        hist_one += cnt;
+      } else {
+        hoff = hist_at.fetch_add(cnt, std::memory_order_relaxed);
+      }
       P.pend.push_back(PendingPiece{sr.batch_seg, tstart(i), hoff, static_cast<uint32_t>(cnt)});
       g.log.push_back(LogRec{hoff, sr.stored, static_cast<uint32_t>(cnt), rids[i]});
       P.worst += worst_windows(sr.stored, cnt, static_cast<uint64_t>(s->D));
@@ -799,7 +806,7 @@ int plan_updates(dgds_server* s, int64_t n, const int32_t* handles, const int32_
   if (W > 1) pool.run(W, work);
   else work(0);
   pcl.mark("records");
-  s->hist_used = hist_at.load();
+  s->hist_used = W == 1 ? hist_one : hist_at.load();
   for (const Part& P : parts)
     if (P.rc) return fail(P.rc, P.msg);
   // merge the workers' segments; group pieces by segment, keeping call order inside a segment
