@@ -481,8 +481,9 @@ def main_b200(args):
                 for j in range(dl):
                     ok = j < tl
                     tru[ok, j] = tr.tokens[(base + j)[ok]]
-                out.append((handles_of_stream[live], rid_of_stream[live], prev, offs, toks,
-                            handles_of_stream[st].copy(), poff, pat, tru, tl))
+                out.append((np.ascontiguousarray(handles_of_stream[live]), np.ascontiguousarray(rid_of_stream[live]),
+                            prev, offs, toks.astype(np.int32, copy=False), handles_of_stream[st].copy(), poff, pat,
+                            tru, tl))
             return out
 
         view = _lib.ResultView()
@@ -490,9 +491,12 @@ def main_b200(args):
         last = C.c_uint64()
         ticket = C.c_uint64()
 
+        reply_buf = np.zeros(len(handles_of_stream), srv.REPLY_DTYPE)  # reused by every tick
+
         def update(hs_):
             (h, r, prev, offs, toks) = hs_[:5]
-            srv.update_arrays(h, r, prev, offs, toks, 0.0)
+            _lib.check(L.dgds_update_batch(srv.handle, len(h), h.ctypes.data, r.ctypes.data, prev.ctypes.data,
+                                           offs.ctypes.data, toks.ctypes.data, 0.0, reply_buf.ctypes.data))
 
         def submit(hs_):
             (qh, poff, pat, tru, tl) = hs_[5:]
