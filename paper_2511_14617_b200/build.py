@@ -14,7 +14,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libdgds_b200.so")
-SOURCES = ["kernels.cu", "peer.cu", "server.cpp", "workload.cpp", "wire.cpp"]
+SOURCES = ["kernels.cu", "peer.cu", "server.cpp", "host_query.cpp", "replica.cpp", "workload.cpp", "wire.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
