@@ -266,12 +266,8 @@ int plan_updates(dgds_server* s, int64_t n, const int32_t* handles, const int32_
   // Measured: the pool wake-up and cross-core traffic on group/stream records cost more than
   // the planning saves at bench sizes (4096 records: 0.34 -> 0.61 ms per step), so the parallel
   // path is opt-in (DGDS_PARALLEL_PLAN=<min records>).
-  static const int64_t par_min = [] {
-    const char* e = std::getenv("DGDS_PARALLEL_PLAN");
-    return e ? std::max<int64_t>(1, std::atoll(e)) : INT64_MAX;
-  }();
   WorkerPool& pool = s->workers();
-  const int W = (n >= par_min && pool.threads() > 1) ? pool.threads() : 1;
+  const int W = (n >= s->par_plan_min && pool.threads() > 1) ? pool.threads() : 1;
   struct Part {
     std::vector<dgds::AppendSeg> segs;
     std::vector<PendingPiece> pend;
@@ -279,7 +275,10 @@ int plan_updates(dgds_server* s, int64_t n, const int32_t* handles, const int32_
     int rc = DGDS_OK;
     std::string msg;
   };
-  thread_local std::vector<Part> parts;  // kept across calls: capacity persists
+  thread_local std::vector<Part> tl_parts;  // kept across calls: capacity persists
+  // the workers must use the CALLER's instance: a thread_local named inside the lambda would
+  // resolve to each worker's own (empty) one
+  std::vector<Part>& parts = tl_parts;
   parts.resize(W);
   for (Part& P : parts) {
     P.segs.clear();
@@ -471,6 +470,7 @@ int dgds_create(const dgds_params* params, dgds_server** out) {
   if (const char* e = std::getenv("DGDS_OUT_BLOCKS")) s->out_blocks = std::max(1, std::atoi(e));
   if (const char* e = std::getenv("DGDS_ASYNC_STAGE")) s->async_stage = std::atoi(e) != 0;
   if (const char* e = std::getenv("DGDS_STAGE_TASKS")) s->stage_tasks = std::max(1, std::atoi(e));
+  if (const char* e = std::getenv("DGDS_PARALLEL_PLAN")) s->par_plan_min = std::max<int64_t>(1, std::atoll(e));
   const uint64_t nodes = p.expected_nodes ? p.expected_nodes : (1ull << 20);
   double init_load = 0.35;  // expected_nodes is an upper bound, so the real load starts lower
   if (const char* e = std::getenv("DGDS_INIT_LOAD")) init_load = std::min(0.9, std::max(0.05, std::atof(e)));

@@ -401,6 +401,7 @@ struct dgds_server {
     std::string launch_msg;
   } pq;
   int stage_tasks = 8;  // workers of an asynchronous stage; DGDS_STAGE_TASKS
+  int64_t par_plan_min = INT64_MAX;  // DGDS_PARALLEL_PLAN=<min records>: plan by group partition on the workers
   bool async_stage = true;  // DGDS_ASYNC_STAGE=0: submit stages synchronously
   dgds::DevTrie T{};
   unsigned long long* d_used = nullptr;
