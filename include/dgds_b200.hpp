@@ -205,6 +205,58 @@ class DraftServer {
     return out;
   }
 
+  // Asynchronous batch_speculate (dgds_speculate_submit / dgds_speculate_wait): the batch is
+  // staged on the server's host workers and queued behind every update made before the call;
+  // speculate_wait returns its results. The PendingBatch owns the flattened inputs the staging
+  // reads, so it must outlive the wait; two batches can be in flight.
+  class PendingBatch {
+   public:
+    std::uint64_t ticket() const { return ticket_; }
+    std::size_t size() const { return in_ ? in_->hs.size() : 0; }
+
+   private:
+    friend class DraftServer;
+    struct Inputs {
+      std::vector<std::int32_t> hs;
+      std::vector<std::uint64_t> offs;
+      TokenSeq flat;
+      std::vector<dgds_spec_args> args;
+    };
+    std::unique_ptr<Inputs> in_;  // stable addresses while the server stages them
+    std::uint64_t ticket_ = 0;
+  };
+
+  PendingBatch speculate_submit(std::span<const SpecQuery> queries) {
+    if (queries.empty()) throw std::invalid_argument("speculate_submit: empty batch");
+    PendingBatch b;
+    b.in_ = std::make_unique<PendingBatch::Inputs>();
+    auto& in = *b.in_;
+    const std::size_t n = queries.size();
+    in.hs.resize(n);
+    in.offs.assign(n + 1, 0);
+    in.args.resize(n);
+    for (std::size_t i = 0; i < n; ++i) {
+      in.hs[i] = handle(queries[i].group_id);
+      in.offs[i + 1] = in.offs[i] + queries[i].pattern.size();
+      in.flat.insert(in.flat.end(), queries[i].pattern.begin(), queries[i].pattern.end());
+      in.args[i] = detail::c_args(queries[i].args);
+    }
+    detail::check(dgds_speculate_submit(s_, static_cast<int64_t>(n), in.hs.data(), in.offs.data(), in.flat.data(),
+                                        in.args.data(), 1, nullptr, 0, nullptr, nullptr, &b.ticket_));
+    return b;
+  }
+
+  std::vector<std::vector<DraftCandidate>> speculate_wait(const PendingBatch& b) {
+    dgds_result_view v{};
+    detail::check(dgds_speculate_wait(s_, b.ticket_, &v));
+    std::vector<std::vector<DraftCandidate>> out(static_cast<std::size_t>(v.n_queries));
+    for (int64_t q = 0; q < v.n_queries; ++q)
+      for (int64_t c = v.cand_off[q]; c < v.cand_off[q + 1]; ++c)
+        out[q].push_back(DraftCandidate{TokenSeq(v.tokens + v.tok_off[c], v.tokens + v.tok_off[c + 1]),
+                                        v.cands[c].score, static_cast<long long>(v.cands[c].support)});
+    return out;
+  }
+
   // fetch_cst (dgds.cpp:53-97): UpToDate / Delta / Full / UnknownGroup per group.
   std::vector<FetchReply> fetch_cst(std::span<const std::string> group_ids, std::span<const DraftCacheInfo> infos,
                                     SimTime now) {

@@ -87,6 +87,21 @@ int main() {
   EXPECT(fresh[0].size() == direct.size() && fresh[0][0].tokens == direct[0].tokens &&
          fresh[0][0].score == direct[0].score);
   EXPECT(periodic.cached_version("g3") == server.group_version("g3"));
+  // asynchronous batches see exactly the updates made before their submit
+  DraftServer as;
+  as.update_cst("ga", 0, 0, TokenSeq{1, 2, 3, 4, 5}, 0.0);
+  std::vector<SpecQuery> aq{{"ga", TokenSeq{1, 2}, SpeculationArgs{4, 6, 1, 2}}};
+  auto b1 = as.speculate_submit(aq);
+  as.update_cst("ga", 1, 0, TokenSeq{1, 2, 9}, 0.0);
+  auto b2 = as.speculate_submit(aq);
+  auto r2 = as.speculate_wait(b2);
+  auto r1 = as.speculate_wait(b1);
+  EXPECT(r1[0].size() == 1 && r1[0][0].tokens == (TokenSeq{3, 4, 5}) && r1[0][0].score == 1.0);
+  auto now = as.batch_speculate(aq);
+  EXPECT(r2[0].size() == 2 && now[0].size() == 2);
+  for (int j = 0; j < 2; ++j)
+    EXPECT(r2[0][j].tokens == now[0][j].tokens && r2[0][j].score == now[0][j].score &&
+           r2[0][j].support == now[0][j].support);
   std::printf("facade ok\n");
   return 0;
 }
