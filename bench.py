@@ -403,13 +403,15 @@ def main_b200(args):
 
     def step(s, stats):
         app, qd = steps_in[s]
-        srv.update_device(app["h"], app["r"], app["prev"], app["offs"], app["d_tok"].data_ptr(), 0.0, 0)
+        # on the server's own stream (dgds_cuda_stream): no cross-stream joins per call
+        srv.update_device(app["h"], app["r"], app["prev"], app["offs"], app["d_tok"].data_ptr(), 0.0, sstream)
         _lib.check(L.dgds_speculate_device(
             srv.handle, Q, C.c_void_p(qd["h"].data_ptr()), C.c_void_p(qd["pl"].data_ptr()),
             C.c_void_p(qd["pat"].data_ptr()), 8, C.c_void_p(d_args.data_ptr()), 0, kq, dl, C.byref(cand),
             C.c_void_p(qd["tru"].data_ptr()), dl, C.c_void_p(qd["tl"].data_ptr()), C.c_void_p(qd["lim"].data_ptr()),
-            C.byref(vo), C.c_void_p(d_stats.data_ptr()) if stats else None, None))
+            C.byref(vo), C.c_void_p(d_stats.data_ptr()) if stats else None, C.c_void_p(sstream)))
 
+    torch.cuda.synchronize()  # inputs were built on torch's stream; the steps run on the server's
     for s in range(W):
         step(s, False)
     torch.cuda.synchronize()
@@ -421,6 +423,11 @@ def main_b200(args):
     torch.cuda.synchronize()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
+    tp = None
+    if os.environ.get("DGDS_DEVICE_TRACE"):  # debug only: device timeline of the timed steps (numbers then invalid)
+        from torch.profiler import ProfilerActivity, profile
+        tp = profile(activities=[ProfilerActivity.CPU, ProfilerActivity.CUDA])
+        tp.__enter__()
     with ClockSampler(local) as clk:
         torch.cuda.synchronize()
         w0 = time.perf_counter()
@@ -430,6 +437,10 @@ def main_b200(args):
         e1.record(ext)
         torch.cuda.synchronize()
         w1 = time.perf_counter()
+    if tp is not None:
+        tp.__exit__(None, None, None)
+        os.makedirs("gpurun_out", exist_ok=True)
+        tp.export_chrome_trace("gpurun_out/device_trace.json")
     dev_ms = e0.elapsed_time(e1)
     _lib.check(L.dgds_profile_read(srv.handle, C.byref(prof), 1))
     _lib.check(L.dgds_profile_enable(srv.handle, 0))

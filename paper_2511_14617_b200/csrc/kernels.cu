@@ -392,6 +392,9 @@ __device__ __forceinline__ uint32_t resolve_content(const DevTrie& T, unsigned l
 
 template <int G, int S>
 __global__ void __launch_bounds__(kBlock, DGDS_QUERY_OCC) k_query(QueryLaunch P) {
+  // Programmatic dependent launch: the blocks may be resident before the previous kernel in
+  // the stream (typically K1) has finished; nothing is read until it has.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   constexpr int kTiles = kBlock / G;
   __shared__ GroupScratch<G, S> scratch[kTiles];
   const int lane = lane_id();
@@ -1186,8 +1189,19 @@ template <int G, int S>
 cudaError_t launch_query_gs(const QueryLaunch& L, cudaStream_t st) {
   const int per_block = kBlock / G;
   const int64_t blocks = (L.n + per_block - 1) / per_block;
-  k_query<G, S><<<static_cast<unsigned>(blocks), kBlock, 0, st>>>(L);
-  return cudaGetLastError();
+  // launched with programmatic stream serialization: the launch overlaps the previous
+  // kernel's tail (k_query waits for its completion in griddepcontrol.wait)
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>(blocks));
+  cfg.blockDim = dim3(kBlock);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k_query<G, S>, L);
 }
 
 template <int G>
