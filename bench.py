@@ -612,8 +612,8 @@ def main_b200(args):
         "roofline": roof_q if dom_q else roof_a,
         "roofline_query": roof_q, "roofline_append": roof_a,
         "cpu_baseline": cpu, "e2e": e2e,
-        # K1 and K2+K3 launches (server profile) + one counter-fold kernel per counted query launch
-        "gpu_launches": int(prof.append_launches + 2 * prof.query_launches),
+        # K1 and K2+K3 launches (server profile); K2 folds its counters in its last block
+        "gpu_launches": int(prof.append_launches + prof.query_launches),
         "wall_ms_per_step": 1e3 * (w1 - w0) / K,
         "clocks": clk.summary(),
     }

@@ -414,7 +414,7 @@ def run_multi(args, world, rank, local, dev):
     route_launches = (px.status()[1] - px_l0) if use_px else 0
     tot = torch.tensor([sum(steps_in[s]["ntok"] for s in range(W, W + K)), int(d_stats[7].item()),
                         app_alg_owner[0], prof.query_ms * 1e3, prof.append_ms * 1e3,
-                        2 * prof.query_launches + prof.append_launches + route_launches], dtype=torch.float64,
+                        prof.query_launches + prof.append_launches + route_launches], dtype=torch.float64,
                        device=dev)
     dist.all_reduce(tot)
     ntok_all, q_alg_all, a_alg_all, qus_all, aus_all, launches_all = tot.tolist()

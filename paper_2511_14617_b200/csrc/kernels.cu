@@ -924,7 +924,7 @@ __global__ void __launch_bounds__(kBlock, DGDS_QUERY_OCC) k_query(QueryLaunch P)
   }
   if (P.stats) {
     // tile leaders' counters -> warp sums (redux) -> one RED per counter per warp into one of
-    // kStatParts partitions: no block barrier, no same-address storm (k_stats_fold sums them)
+    // kStatParts partitions: no same-address storm (the last block sums them)
     const int ctoks = tile.sum(gl < nf ? sm.f.len[gl] : 0);
     const bool lead = valid && gl == 0;
     const uint32_t B = lead ? static_cast<uint32_t>(4ull * plen + 32ull + 32ull * st_lookups + 32ull * st_exp +
@@ -942,19 +942,28 @@ __global__ void __launch_bounds__(kBlock, DGDS_QUERY_OCC) k_query(QueryLaunch P)
       for (int k = 0; k < 8; ++k)
         if (v[k]) atomicAdd(P.stat_part + part * 8 + k, static_cast<unsigned long long>(v[k]));
     }
+    // The last block to finish folds the partitions into P.stats (no separate fold launch):
+    // the barrier + fence order this block's counter atomics before its ticket.
+    __shared__ bool last_block;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      unsigned long long* ticket = P.stat_part + kStatParts * 8;
+      last_block = atomicAdd(ticket, 1ull) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (last_block) {
+      __threadfence();
+      if (threadIdx.x < 8) {
+        unsigned long long t = 0;
+        for (int p = 0; p < kStatParts; ++p) t += atomicExch(P.stat_part + p * 8 + threadIdx.x, 0ull);
+        reinterpret_cast<unsigned long long*>(P.stats)[threadIdx.x] += t;
+      }
+      if (threadIdx.x == 0) P.stat_part[kStatParts * 8] = 0ull;
+    }
   }
 }
 
-__global__ void k_stats_fold(unsigned long long* part, dgds_query_stats* out) {
-  const int k = threadIdx.x;
-  if (k >= 8) return;
-  unsigned long long t = 0;
-  for (int p = 0; p < kStatParts; ++p) {
-    t += part[p * 8 + k];
-    part[p * 8 + k] = 0ull;
-  }
-  reinterpret_cast<unsigned long long*>(out)[k] += t;
-}
 
 // ---------------------------------------------------------------------------
 // standalone verify (engine.cpp:115-143), one thread per request
@@ -1228,9 +1237,7 @@ cudaError_t launch_query(const QueryLaunch& L, int32_t max_k, int32_t max_s, cud
   if (max_k <= 4) e = launch_query_g<4>(L, max_s, st);
   else if (max_k <= 8) e = launch_query_g<8>(L, max_s, st);
   else e = launch_query_g<32>(L, max_s, st);
-  if (e != cudaSuccess || !L.stats) return e;
-  k_stats_fold<<<1, 32, 0, st>>>(L.stat_part, L.stats);
-  return cudaGetLastError();
+  return e;  // the counters are folded by k_query's last block
 }
 
 cudaError_t launch_verify(int64_t n, int32_t k_stride, int32_t s_stride, const int32_t* n_cands, const int32_t* lens,

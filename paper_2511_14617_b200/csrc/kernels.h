@@ -85,8 +85,8 @@ struct QueryLaunch {
   int32_t* v_drafted;
   int32_t* v_accepted;
   int32_t* v_emitted;
-  dgds_query_stats* stats;          // optional: counters added here (after k_stats_fold)
-  unsigned long long* stat_part;    // server scratch [kStatParts][8], zero between launches
+  dgds_query_stats* stats;          // optional: counters added here (by the last block)
+  unsigned long long* stat_part;    // server scratch [kStatParts][8] + a block ticket, zero between launches
   int32_t* err_flag;  // set to 1 by any query with invalid args (device API)
   long long* dbg;     // optional per-query phase timing [n][8] (debug)
   // Per-query strides (elements). SoA buffers: in_qstride 1, out_qstride = out_qstride8 = k_stride,

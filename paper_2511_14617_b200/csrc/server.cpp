@@ -501,8 +501,9 @@ int dgds_create(const dgds_params* params, dgds_server** out) {
   s->hist_cap = std::max<uint64_t>(1ull << 20, nodes / 20);  // ~ tokens (nodes per token ~ 17-24)
   DGDS_CUDA(cudaMalloc(&s->d_hist, s->hist_cap * sizeof(int32_t)));
   s->T.hist = s->d_hist;
-  DGDS_CUDA(cudaMalloc(&s->d_stat_part, dgds::kStatParts * 8 * sizeof(unsigned long long)));
-  DGDS_CUDA(cudaMemsetAsync(s->d_stat_part, 0, dgds::kStatParts * 8 * sizeof(unsigned long long), s->st));
+  // [kStatParts][8] counter partitions + the ticket of k_query's last-block fold
+  DGDS_CUDA(cudaMalloc(&s->d_stat_part, (dgds::kStatParts * 8 + 1) * sizeof(unsigned long long)));
+  DGDS_CUDA(cudaMemsetAsync(s->d_stat_part, 0, (dgds::kStatParts * 8 + 1) * sizeof(unsigned long long), s->st));
   s->root_of_cap = 1024;
   DGDS_CUDA(cudaMalloc(&s->d_root_of, s->root_of_cap * sizeof(uint32_t)));
   DGDS_CUDA(cudaMemsetAsync(s->d_root_of, 0, s->root_of_cap * sizeof(uint32_t), s->st));
