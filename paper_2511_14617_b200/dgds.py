@@ -375,7 +375,8 @@ class DraftServer:
                        limit: Optional[np.ndarray] = None) -> "ResultView":
         """Batch query (+ fused verification when `truth` is given) returning compact per-query
         candidate lists as zero-copy views of the server's pinned result block
-        (dgds_speculate_verify_view) — valid until the next query call on this server."""
+        (dgds_speculate_verify_view) — valid until the second-next host query batch on this server
+        (two result slots)."""
         n = len(handles)
         handles = np.ascontiguousarray(handles, np.int32)
         pat_offsets = np.ascontiguousarray(pat_offsets, np.uint64)
