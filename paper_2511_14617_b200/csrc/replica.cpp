@@ -110,6 +110,7 @@ int dgds_fetch_cst(dgds_server* s, int64_t n, const int32_t* handles, const uint
   if (!s || n < 0 || (n > 0 && (!handles || !cached || !rep || !blobs))) return fail(DGDS_EINVAL, "null argument");
   std::lock_guard<std::mutex> lk(s->mu);
   if (int rc_ = flush_pending(s)) return rc_;
+  materialize_logs(s);  // pending plans' history-log records first
   DGDS_CUDA(cudaSetDevice(s->p.device));
   for (int64_t i = 0; i < n; ++i)
     if (int rc = check_handle(s, handles[i])) return rc;
@@ -211,6 +212,7 @@ int dgds_compact_group(dgds_server* s, int32_t h, uint64_t before_version) {  //
   if (!s) return fail(DGDS_EINVAL, "null server");
   std::lock_guard<std::mutex> lk(s->mu);
   if (int rc_ = flush_pending(s)) return rc_;
+  materialize_logs(s);  // pending plans' history-log records first
   if (int rc = check_handle(s, h)) return rc;
   GroupRec& g = s->groups[h];
   if (!g.alive) return DGDS_OK;
@@ -225,6 +227,7 @@ int dgds_apply_blob(dgds_server* s, int32_t h, const uint8_t* blob, uint64_t len
   if (!s || (!blob && len)) return fail(DGDS_EINVAL, "null argument");
   std::lock_guard<std::mutex> lk(s->mu);
   if (int rc_ = flush_pending(s)) return rc_;
+  materialize_logs(s);  // pending plans' history-log records first
   if (int rc = check_handle(s, h)) return rc;
   GroupRec& g = s->groups[h];
   BlobReader r{blob, blob + len};
@@ -324,6 +327,7 @@ int dgds_compact_memory(dgds_server* s) {
   if (!s) return fail(DGDS_EINVAL, "null server");
   std::lock_guard<std::mutex> lk(s->mu);
   if (int rc_ = flush_pending(s)) return rc_;
+  materialize_logs(s);  // pending plans' history-log records first
   DGDS_CUDA(cudaSetDevice(s->p.device));
   return compact_memory(s);
 }

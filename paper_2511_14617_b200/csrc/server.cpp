@@ -69,6 +69,7 @@ int alloc_stream_slot(dgds_server* s, uint32_t* out) {
 
 void retire_group(dgds_server* s, GroupRec& g) {
   if (!g.alive) return;
+  materialize_logs(s);
   for (const LogRec& e : g.log) s->dead_hist_tokens += e.len;
   g.streams.for_each([&](int32_t, StreamRec& r) { s->free_streams.push_back(r.slot); });
   g.streams.clear();
@@ -83,6 +84,7 @@ void retire_group(dgds_server* s, GroupRec& g) {
 }
 
 int create_group(dgds_server* s, GroupRec& g, double ttl, double now) {
+  materialize_logs(s);
   if (s->next_root_index >= kRootCap) return fail(DGDS_EUNSUPPORTED, "group root ids exhausted");
   g.root = dgds::kRootTop - s->next_root_index++;
   g.alive = true;
@@ -245,7 +247,8 @@ int ensure_hist(dgds_server* s) {
 // Record i's tokens are tokens[tok_start(i) .. tok_start(i) + tok_count(i)).
 int plan_updates(dgds_server* s, int64_t n, const int32_t* handles, const int32_t* rids, const uint64_t* prev,
                  const uint64_t* offs, const uint64_t* counts, double now, dgds_update_reply* rep,
-                 std::vector<dgds::AppendSeg>& segs, std::vector<dgds::AppendPiece>& pieces, uint64_t* worst) {
+                 std::vector<dgds::AppendSeg>& segs, std::vector<dgds::AppendPiece>& pieces, uint64_t* worst,
+                 std::vector<DeferredLog>* defer = nullptr) {
   // offs[n+1] cumulative (counts == nullptr), or offs[n] starts + counts[n]
   auto tstart = [&](int64_t i) { return offs[i]; };
   auto tcount = [&](int64_t i) { return counts ? counts[i] : offs[i + 1] - offs[i]; };
@@ -268,6 +271,7 @@ int plan_updates(dgds_server* s, int64_t n, const int32_t* handles, const int32_
   // path is opt-in (DGDS_PARALLEL_PLAN=<min records>).
   WorkerPool& pool = s->workers();
   const int W = (n >= s->par_plan_min && pool.threads() > 1) ? pool.threads() : 1;
+  if (!defer || W > 1) materialize_logs(s);  // this plan appends to the group logs directly
   struct Part {
     std::vector<dgds::AppendSeg> segs;
     std::vector<PendingPiece> pend;
@@ -348,7 +352,10 @@ int plan_updates(dgds_server* s, int64_t n, const int32_t* handles, const int32_
         hoff = hist_at.fetch_add(cnt, std::memory_order_relaxed);
       }
       P.pend.push_back(PendingPiece{sr.batch_seg, tstart(i), hoff, static_cast<uint32_t>(cnt)});
-      g.log.push_back(LogRec{hoff, sr.stored, static_cast<uint32_t>(cnt), rids[i]});
+      if (defer && W == 1)  // appended to the group log after the plan's K1 launch
+        defer->push_back(DeferredLog{handles[i], LogRec{hoff, sr.stored, static_cast<uint32_t>(cnt), rids[i]}});
+      else
+        g.log.push_back(LogRec{hoff, sr.stored, static_cast<uint32_t>(cnt), rids[i]});
       P.worst += worst_windows(sr.stored, cnt, static_cast<uint64_t>(s->D));
       sr.stored += cnt;
       g.version += 1;
@@ -724,9 +731,20 @@ extern "C" int dgds_update_batch(dgds_server* s, int64_t n, const int32_t* handl
 struct dgds_update_plan {
   std::vector<dgds::AppendSeg> segs;
   std::vector<dgds::AppendPiece> pieces;
+  std::vector<DeferredLog> logs;  // history-log records, appended after the launch
   const int32_t* d_tokens = nullptr;
   uint64_t seq = 0;
 };
+
+namespace dgds_host {
+void materialize_logs(dgds_server* s) {
+  for (dgds_update_plan* p : s->log_pending) {
+    for (const DeferredLog& d : p->logs) s->groups[d.handle].log.push_back(d.rec);
+    p->logs.clear();
+  }
+  s->log_pending.clear();
+}
+}  // namespace dgds_host
 
 static void free_plan_pool(dgds_server* s) {
   for (auto* pl : s->plan_pool) delete pl;
@@ -740,8 +758,10 @@ static int plan_device(dgds_server* s, int64_t n, const int32_t* handles, const 
                        const uint64_t* offs, const uint64_t* counts, const int32_t* d_tokens, double now,
                        dgds_update_reply* rep, dgds_update_plan* plan) {
   uint64_t worst = 0;
-  if (int rc = plan_updates(s, n, handles, rids, prev, offs, counts, now, rep, plan->segs, plan->pieces, &worst))
-    return rc;
+  const int prc = plan_updates(s, n, handles, rids, prev, offs, counts, now, rep, plan->segs, plan->pieces, &worst,
+                               &plan->logs);
+  if (!plan->logs.empty()) s->log_pending.push_back(plan);  // accepted records, even on a later error
+  if (prc) return prc;
   if (plan->segs.empty()) return DGDS_OK;
   if (int rc = ensure_capacity(s, worst)) return rc;
   if (int rc = ensure_hist(s)) return rc;
@@ -795,9 +815,14 @@ static int update_device_impl(dgds_server* s, int64_t n, const int32_t* handles,
   thread_local dgds_update_plan plan;
   plan.segs.clear();
   plan.pieces.clear();
-  if (int rc = plan_device(s, n, handles, rids, prev, offs, counts, d_tokens, now, rep, &plan)) return rc;
+  if (int rc = plan_device(s, n, handles, rids, prev, offs, counts, d_tokens, now, rep, &plan)) {
+    materialize_logs(s);
+    return rc;
+  }
   pc.mark("plan");
-  return launch_plan(s, &plan, stream, pc);
+  const int rc = launch_plan(s, &plan, stream, pc);
+  materialize_logs(s);  // after K1 is queued
+  return rc;
 }
 
 extern "C" {
@@ -906,6 +931,7 @@ int dgds_update_plan_routed(dgds_server* s, int32_t n_seg, int64_t seg_rows, con
   if (!plan) plan = std::make_unique<dgds_update_plan>();
   plan->segs.clear();
   plan->pieces.clear();
+  plan->logs.clear();
   plan->d_tokens = nullptr;
   plan->seq = 0;
   if (n > 0) {
@@ -915,8 +941,10 @@ int dgds_update_plan_routed(dgds_server* s, int32_t n_seg, int64_t seg_rows, con
     if (int rc_ = flush_pending(s)) return rc_;
     DGDS_CUDA(cudaSetDevice(s->p.device));
     if (int rc = plan_device(s, n, r.handles.data(), r.rids.data(), r.prev.data(), r.starts.data(), r.counts.data(),
-                             d_rows, now, r.rep.data(), plan.get()))
+                             d_rows, now, r.rep.data(), plan.get())) {
+      materialize_logs(s);  // before the plan (holding accepted records' logs) is destroyed
       return rc;
+    }
     if (n_rejected) {
       int64_t bad = 0;
       for (int64_t k = 0; k < n; ++k) bad += r.rep[k].ok ? 0 : 1;
@@ -935,6 +963,7 @@ int dgds_update_launch(dgds_server* s, dgds_update_plan* plan, void* stream) {
   const cudaError_t e = cudaSetDevice(s->p.device);
   const int rc = e == cudaSuccess ? launch_plan(s, plan, stream, pc)
                                   : fail(DGDS_ECUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(e));
+  materialize_logs(s);  // the plan's history-log records, now that its K1 is queued
   s->plan_pool.push_back(plan);  // recycled (the staging copy above does not keep references)
   return rc;
 }

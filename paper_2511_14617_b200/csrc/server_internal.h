@@ -336,6 +336,11 @@ namespace dgds_host {
 int flush_pending(dgds_server* s);  // launches a submitted query batch; before any later device work
 int launch_batch(dgds_server* s, bool timed);
 // one chunk of a staged host query batch: handles | pat_len | patterns | args | truth | truth_left | limit
+// a history-log record planned but not yet appended to its group's log (materialize_logs)
+struct DeferredLog {
+  int32_t handle;
+  LogRec rec;
+};
 struct QInBlock {
   int64_t q0 = 0, m = 0;
   size_t base = 0, o_len = 0, o_pat = 0, o_args = 0, o_tr = 0, o_tl = 0, o_lm = 0, bytes = 0;
@@ -401,6 +406,9 @@ struct dgds_server {
     std::string launch_msg;
   } pq;
   int stage_tasks = 8;  // workers of an asynchronous stage; DGDS_STAGE_TASKS
+  // plans whose history-log records are not yet in their groups' logs (device / routed update
+  // plans append them after their K1 launch, off the routed critical path); creation order
+  std::vector<struct dgds_update_plan*> log_pending;
   int64_t par_plan_min = INT64_MAX;  // DGDS_PARALLEL_PLAN=<min records>: plan by group partition on the workers
   bool async_stage = true;  // DGDS_ASYNC_STAGE=0: submit stages synchronously
   dgds::DevTrie T{};
@@ -468,6 +476,9 @@ void retire_group(dgds_server* s, GroupRec& g);
 int create_group(dgds_server* s, GroupRec& g, double ttl, double now);
 bool live_entry(dgds_server* s, GroupRec& g, double now);
 int check_handle(dgds_server* s, int32_t h);
+// appends every pending plan's history-log records to the group logs, in plan order; anything
+// that reads or resets group logs calls it first
+void materialize_logs(dgds_server* s);
 int check_args(const dgds_spec_args& a);
 int read_used(dgds_server* s, uint64_t* out);
 int rebuild(dgds_server* s, uint64_t new_cap);

@@ -166,3 +166,79 @@ def test_apply_blob_errors_match_reference(reference):
         other.apply_blob("g2", full)
     assert rep.apply_blob("g1", full) == src.group_version("g1")
     assert rep.fetch_cst(["g1"], [0], 0.0)[0].blob == full
+
+
+def test_device_and_routed_updates_keep_replica_logs():
+    """Device-buffer updates (dgds_update_batch_device) and two-phase routed updates
+    (dgds_update_plan_routed, then dgds_update_launch; the next plan is made before the previous
+    launch) append their history-log records after the K1 launch. fetch_cst blobs (full and
+    delta) stay byte-identical to a host-path twin fed the same records."""
+    import ctypes as C
+    import torch
+    from paper_2511_14617_b200 import _lib
+    dev = torch.device("cuda:0")
+    L = _lib.lib()
+    host = D.DraftServer(D.DgdsParams(), expected_nodes=1 << 16)
+    devs = D.DraftServer(D.DgdsParams(), expected_nodes=1 << 16)
+    routed = D.DraftServer(D.DgdsParams(), expected_nodes=1 << 16)
+    rng = np.random.default_rng(12)
+    groups = ["ga", "gb", "gc"]
+    stored = {}
+    RW = 5 + 16  # routed row: handle, rid, prev lo, prev hi, count, 16 tokens
+    pending = None  # routed plan made but not yet launched
+    versions = {}
+    for rnd in range(8):
+        gids, rids, prevs, toks = [], [], [], []
+        for _ in range(int(rng.integers(4, 30))):
+            g = groups[int(rng.integers(3))]
+            r = int(rng.integers(4))
+            t = rng.integers(0, 9, int(rng.integers(1, 17))).tolist()
+            if any(g == a and r == b for a, b in zip(gids, rids)):
+                continue  # one record per stream per batch keeps the twins' batches identical
+            gids.append(g)
+            rids.append(r)
+            prevs.append(stored.get((g, r), 0))
+            toks.append(t)
+            stored[(g, r)] = stored.get((g, r), 0) + len(t)
+        now = float(rnd)
+        rh = host.update_batch(gids, rids, prevs, toks, now)
+        # device-buffer path
+        hd = devs.group_handles(gids)
+        offs = np.zeros(len(toks) + 1, np.uint64)
+        offs[1:] = np.cumsum([len(t) for t in toks])
+        d_tok = torch.tensor(np.concatenate(toks).astype(np.int32), device=dev)
+        rd = devs.update_device(hd, np.array(rids, np.int32), np.array(prevs, np.uint64), offs, d_tok.data_ptr(), now)
+        assert [(x.ok, x.version, x.acked_tokens) for x in rh] == [(bool(a), int(b), int(c)) for a, _, b, c in rd]
+        # routed path: plan this round; launch the previous round's plan after it
+        hr = routed.group_handles(gids)
+        n = len(gids)
+        meta = np.zeros((n, 5), np.int32)
+        rows = np.zeros((n, RW), np.int32)
+        for i in range(n):
+            meta[i] = [hr[i], rids[i], prevs[i] & 0xFFFFFFFF, prevs[i] >> 32, len(toks[i])]
+            rows[i, :5] = meta[i]
+            rows[i, 5:5 + len(toks[i])] = toks[i]
+        d_rows = torch.from_numpy(rows).to(dev)
+        counts = np.array([n], np.int32)
+        nrej = C.c_int64()
+        plan = C.c_void_p()
+        _lib.check(L.dgds_update_plan_routed(routed.handle, 1, n, counts.ctypes.data, meta.ctypes.data, 5,
+                                             C.c_void_p(d_rows.data_ptr()), RW, now, C.byref(nrej), C.byref(plan)))
+        assert nrej.value == 0
+        if pending is not None:
+            _lib.check(L.dgds_update_launch(routed.handle, pending[0], None))
+        pending = (plan, d_rows)
+        for g in set(gids):
+            versions.setdefault(g, []).append(host.group_version(g))
+        if rnd % 3 == 2:
+            _lib.check(L.dgds_update_launch(routed.handle, pending[0], None))
+            pending = None
+            torch.cuda.synchronize()
+            for g in groups:
+                if g not in versions:
+                    continue
+                for cached in sorted({0, versions[g][0], versions[g][-1] // 2}):
+                    want = host.fetch_cst([g], [cached], now)[0]
+                    for other in (devs, routed):
+                        got = other.fetch_cst([g], [cached], now)[0]
+                        assert (got.kind, got.version, got.blob) == (want.kind, want.version, want.blob), (g, cached)
