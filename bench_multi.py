@@ -26,11 +26,36 @@ APP_W = 21  # append record: [local handle, request id, prev lo, prev hi, n, tok
 QRY_W = 21  # query record: [local handle, pat_len, pattern[8], truth_left, limit, truth[8], pad]
 
 
+def _gpu_local_cpus(local):
+    """CPUs local to visible GPU `local` (NVML affinity), or None."""
+    try:
+        import pynvml
+        pynvml.nvmlInit()
+        uuid = str(torch.cuda.get_device_properties(local).uuid)
+        h = pynvml.nvmlDeviceGetHandleByUUID(uuid if uuid.startswith("GPU-") else "GPU-" + uuid)
+        words = (os.cpu_count() + 63) // 64
+        mask = pynvml.nvmlDeviceGetCpuAffinity(h, words)
+        return {64 * w + b for w, m in enumerate(mask) for b in range(64) if (m >> b) & 1}
+    except Exception:
+        return None
+
+
 def _pin_rank_cores(world, local):
     """Give each rank its own slice of the host cores (threads created later inherit it), so
-    the ranks' host paths do not preempt each other (the tick waits on every rank's host)."""
+    the ranks' host paths do not preempt each other (the tick waits on every rank's host).
+    The slice is taken from the cores local to the rank's GPU (NVML affinity; ranks whose GPUs
+    share those cores split them), so its pinned staging and host round trips stay on-socket."""
     try:
         cores = sorted(os.sched_getaffinity(0))
+        near = [_gpu_local_cpus(g) for g in range(world)]
+        if all(n is not None for n in near):
+            mine = sorted(set(cores) & near[local])
+            peers = [g for g in range(world) if near[g] == near[local]]  # ranks on the same CPU set
+            per = len(mine) // len(peers)
+            if per >= 2:
+                k = peers.index(local)
+                os.sched_setaffinity(0, set(mine[k * per:(k + 1) * per]))
+                return
         per = len(cores) // world
         if per >= 2:
             os.sched_setaffinity(0, set(cores[local * per:(local + 1) * per]))
@@ -41,6 +66,9 @@ def _pin_rank_cores(world, local):
 def run_multi(args, world, rank, local, dev):
     if os.environ.get("DGDS_PIN_CORES", "1") == "1":
         _pin_rank_cores(world, local)
+        if os.environ.get("DGDS_TICK_TRACE") == "1":
+            print(f"rank {local} cores {sorted(os.sched_getaffinity(0))} near {sorted(_gpu_local_cpus(local) or [])[:4]}...",
+                  flush=True)
     from bench import CONFIG_NAMES, RANDOM_CEILING_GBS, ClockSampler, append_alg_bytes, peaks
     from paper_2511_14617_b200 import _lib
     from paper_2511_14617_b200.dgds import DgdsParams, DraftServer, SpeculationArgs, args_array, shard_of_group
@@ -257,7 +285,11 @@ def run_multi(args, world, rank, local, dev):
     if use_px:
         from concurrent.futures import ThreadPoolExecutor
         planner = ThreadPoolExecutor(max_workers=1)  # ctypes and event waits release the GIL
-    run_until = [0]  # ticks < run_until[0] will run in the current loop: only those are planned ahead
+    run_until = [0]  # ticks < run_until[0] run in the current loop (their queries may be issued ahead)
+    # ticks < plan_until[0] may be planned ahead (host bookkeeping of their routed appends): the
+    # warm-up plans the first timed tick, so the timed region starts with a full pipeline, as
+    # every later tick does; a tick that will not run is never planned
+    plan_until = [0]
 
     def make_plan(s, k):
         """Host half of tick s's appends (dgds_update_plan_routed): waits for the tick's routed
@@ -327,7 +359,7 @@ def run_multi(args, world, rank, local, dev):
             if s not in plans:  # the planner is FIFO: tick s must be planned before tick s+1
                 plans[s] = planner.submit(make_plan, s, k)
             route_appends(s + 1)
-            if s + 1 < run_until[0] and (s + 1) in inflight and (s + 1) not in plans:
+            if s + 1 < plan_until[0] and (s + 1) in inflight and (s + 1) not in plans:
                 plans[s + 1] = planner.submit(make_plan, s + 1, inflight[s + 1][2])
             send_queries(s + 1)
             t0 = mark("route_next", t0)
@@ -365,18 +397,26 @@ def run_multi(args, world, rank, local, dev):
         mark("route_next", t0)
         return None
 
-    def run_ticks(a, b, stats):
-        """Ticks [a, b) back to back, pipelined (px) or in order (nccl)."""
+    tick_ev = [] if os.environ.get("DGDS_TICK_TRACE") == "1" else None  # debug: per-tick device times
+
+    def run_ticks(a, b, stats, plan_to=None):
+        """Ticks [a, b) back to back, pipelined (px) or in order (nccl); ticks < plan_to (default b)
+        may be planned ahead."""
         run_until[0] = b
+        plan_until[0] = b if plan_to is None else plan_to
         back = q_part(a, stats)
         for s in range(a, b):
+            if tick_ev is not None and stats:
+                ev = torch.cuda.Event(enable_timing=True)
+                ev.record(torch.cuda.current_stream(dev))
+                tick_ev.append(ev)
             nxt = a_part(s, stats, pipeline=use_px)
             if not use_px and s + 1 < b:
                 nxt = q_part(s + 1, stats)
             back = nxt if nxt is not None else back
         return back
 
-    run_ticks(0, W, False)
+    run_ticks(0, W, False, plan_to=W + 1)  # the first timed tick is planned during the warm-up
     torch.cuda.synchronize()
     prof = _lib.Profile()
     _lib.check(L.dgds_profile_enable(srv.handle, 1))
@@ -404,6 +444,9 @@ def run_multi(args, world, rank, local, dev):
         if rank == 0:
             print(tp.key_averages().table(sort_by="cuda_time_total", row_limit=22), flush=True)
             print(tp.key_averages().table(sort_by="cpu_time_total", row_limit=22), flush=True)
+    if tick_ev:
+        print(f"rank {rank} tick us:", [round(1e3 * tick_ev[i].elapsed_time(tick_ev[i + 1]))
+                                        for i in range(len(tick_ev) - 1)], flush=True)
     dist.barrier()
     ms = torch.tensor([e0.elapsed_time(e1)], device=dev)
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
@@ -479,6 +522,7 @@ def run_multi(args, world, rank, local, dev):
         d2h = 0
         base_s = len(steps_in)
         run_until[0] = base_s + E
+        plan_until[0] = base_s + E
         # pipelined like the single-GPU e2e loop: tick j+1's inputs, exchanges and queries are
         # queued before tick j's replies are read on the host
         issue_inputs(0)
