@@ -556,10 +556,13 @@ def main_b200(args):
                 from torch.profiler import ProfilerActivity, profile
                 tp = profile(activities=[ProfilerActivity.CPU, ProfilerActivity.CUDA])
                 tp.__enter__()
+            gc.collect()
+            gc.disable()  # like the device-timed region: no cyclic-GC pause inside the timed ticks
             t0 = time.perf_counter()
             d2h = run(steps[WE:], mode == "pipelined")
             torch.cuda.synchronize()
             t1 = time.perf_counter()
+            gc.enable()
             n_e = len(steps) - WE
             res[mode] = {"value": Q * n_e / (t1 - t0), "unit": "queries/s",
                          "h2d_bytes_per_step": sum(h2d_bytes(x) for x in steps[WE:]) // n_e,

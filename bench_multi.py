@@ -523,6 +523,7 @@ def run_multi(args, world, rank, local, dev):
         gc.collect()
         dist.barrier()
         torch.cuda.synchronize()
+        gc.disable()  # no cyclic-GC pause inside the timed ticks
         t0 = time.perf_counter()
         d2h = 0
         base_s = len(steps_in)
@@ -553,6 +554,7 @@ def run_multi(args, world, rank, local, dev):
             print(f"rank {rank} e2e inputs|a_part|d2h|consume us:", e2e_trace, flush=True)
         torch.cuda.synchronize()
         dt = torch.tensor([time.perf_counter() - t0], device=dev)
+        gc.enable()
         dist.all_reduce(dt, op=dist.ReduceOp.MAX)
         e2e = {"value": world * Q * E / dt.item(), "unit": "queries/s", "h2d_bytes_per_step": h2d // E,
                "d2h_bytes_per_step": d2h // E, "steps": E,
