@@ -296,6 +296,30 @@ def run_multi(args, world, rank, local, dev):
     # every later tick does; a tick that will not run is never planned
     plan_until = [0]
 
+    native_planner = use_px and os.environ.get("DGDS_NATIVE_PLANNER", "1") == "1"
+
+    def submit_plan(s, k):
+        """Tick s's routed plan, made off the main thread: the server's C++ planner thread
+        (waits for the metadata event, no GIL), or the Python helper thread."""
+        if native_planner:
+            job = C.c_uint64()
+            _lib.check(L.dgds_update_plan_routed_async(
+                srv.handle, C.c_void_p(ev_bufs[k].cuda_event), world, capa, C.c_void_p(cnt_bufs[k].data_ptr()),
+                C.c_void_p(meta_bufs[k].data_ptr()), 5, C.c_void_p(px.slab_ptr("a", s + 1)), APP_W, 0.0,
+                C.byref(job)))
+            return job.value
+        return planner.submit(make_plan, s, k)
+
+    def take_plan(h):
+        if not native_planner:
+            return h.result()
+        nrej = C.c_int64()
+        plan = C.c_void_p()
+        _lib.check(L.dgds_update_plan_take(srv.handle, h, C.byref(nrej), C.byref(plan)))
+        if nrej.value:
+            raise RuntimeError("routed append out of order")
+        return plan
+
     def make_plan(s, k):
         """Host half of tick s's appends (dgds_update_plan_routed): waits for the tick's routed
         metadata, does the bookkeeping, returns the plan to launch after tick s's queries."""
@@ -362,13 +386,13 @@ def run_multi(args, world, rank, local, dev):
             # tick s+1's exchanges first: they need only tick s's replies (ev_rep), and their kernels
             # get SMs before K1 fills them; the helper thread plans tick s+1 as its metadata lands
             if s not in plans:  # the planner is FIFO: tick s must be planned before tick s+1
-                plans[s] = planner.submit(make_plan, s, k)
+                plans[s] = submit_plan(s, k)
             route_appends(s + 1)
             if s + 1 < plan_until[0] and (s + 1) in inflight and (s + 1) not in plans:
-                plans[s + 1] = planner.submit(make_plan, s + 1, inflight[s + 1][2])
+                plans[s + 1] = submit_plan(s + 1, inflight[s + 1][2])
             send_queries(s + 1)
             t0 = mark("route_next", t0)
-            plan = plans.pop(s).result()
+            plan = take_plan(plans.pop(s))
             t0 = mark("meta_np", t0)
             main.wait_event(ev_bufs[k])  # K1 reads the slab rows delivered on the side stream
             _lib.check(L.dgds_update_launch(srv.handle, plan, C.c_void_p(main.cuda_stream)))

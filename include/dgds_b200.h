@@ -252,6 +252,17 @@ int dgds_update_plan_routed(dgds_server* s, int32_t n_seg, int64_t seg_rows, con
                             const int32_t* h_meta, int32_t meta_stride, const int32_t* d_rows, int32_t row_words,
                             double now, int64_t* n_rejected, dgds_update_plan** out);
 int dgds_update_launch(dgds_server* s, dgds_update_plan* plan, void* stream);
+
+/* Asynchronous dgds_update_plan_routed on a server-owned planner thread: the job waits for
+ * `ready_event` (a cudaEvent_t recorded after the metadata rows reached h_meta / h_counts, or
+ * NULL), then plans exactly like dgds_update_plan_routed. Jobs run in submission order, so
+ * plans come out in the order dgds_update_launch needs. The host buffers must stay unchanged
+ * until dgds_update_plan_take returns for the job; take blocks until the job is planned and
+ * hands over its plan (and the number of rejected records). */
+int dgds_update_plan_routed_async(dgds_server* s, void* ready_event, int32_t n_seg, int64_t seg_rows,
+                                  const int32_t* h_counts, const int32_t* h_meta, int32_t meta_stride,
+                                  const int32_t* d_rows, int32_t row_words, double now, uint64_t* job);
+int dgds_update_plan_take(dgds_server* s, uint64_t job, int64_t* n_rejected, dgds_update_plan** out);
 /* Strided device -> host copy (cudaMemcpy2DAsync): `rows` rows of `width` bytes. */
 int dgds_copy_rows_d2h(void* h_dst, int64_t dst_pitch, const void* d_src, int64_t src_pitch, int64_t width,
                        int64_t rows, void* stream);

@@ -195,6 +195,9 @@ EXPORTS = {
     "dgds_update_plan_routed": (C.c_int, [_P, _I32, _I64, _P, _P, _I32, _P, _I32, C.c_double, C.POINTER(_I64),
                                           C.POINTER(C.c_void_p)]),
     "dgds_update_launch": (C.c_int, [_P, _P, _P]),
+    "dgds_update_plan_routed_async": (C.c_int, [_P, _P, _I32, _I64, _P, _P, _I32, _P, _I32, C.c_double,
+                                                C.POINTER(_U64)]),
+    "dgds_update_plan_take": (C.c_int, [_P, _U64, C.POINTER(_I64), C.POINTER(_P)]),
     "dgds_copy_rows_d2h": (C.c_int, [_P, _I64, _P, _I64, _I64, _I64, _P]),
     "dgds_speculate_verify_view": (C.c_int, [_P, _I64, _P, _P, _P, _P, _I64, _P, _I32, _P, _P, C.POINTER(ResultView)]),
     "dgds_speculate_submit": (C.c_int, [_P, _I64, _P, _P, _P, _P, _I64, _P, _I32, _P, _P, C.POINTER(_U64)]),

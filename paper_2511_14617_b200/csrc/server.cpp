@@ -14,6 +14,7 @@
 #include "server_internal.h"
 
 static void free_plan_pool(dgds_server* s);  // after dgds_update_plan is complete
+static void stop_planner(dgds_server* s);    // asynchronous routed planning, below
 
 namespace dgds_host {
 
@@ -521,6 +522,7 @@ int dgds_create(const dgds_params* params, dgds_server** out) {
 
 int dgds_destroy(dgds_server* s) {
   if (!s) return DGDS_OK;
+  stop_planner(s);  // jobs still queued are planned first (their inputs are the caller's)
   cudaSetDevice(s->p.device);
   flush_pending(s);  // a staged batch: its workers finish, its kernels run
   if (s->st) cudaStreamSynchronize(s->st);
@@ -952,6 +954,108 @@ int dgds_update_plan_routed(dgds_server* s, int32_t n_seg, int64_t seg_rows, con
     }
   }
   *out = plan.release();
+  return DGDS_OK;
+}
+
+}  // extern "C"
+
+struct dgds_server::PlanJob {
+  cudaEvent_t ready = nullptr;
+  int32_t n_seg = 0;
+  int64_t seg_rows = 0;
+  const int32_t* h_counts = nullptr;
+  const int32_t* h_meta = nullptr;
+  int32_t meta_stride = 0;
+  const int32_t* d_rows = nullptr;
+  int32_t row_words = 0;
+  double now = 0.0;
+  bool done = false;
+  int rc = DGDS_OK;
+  std::string msg;
+  int64_t n_rejected = 0;
+  dgds_update_plan* plan = nullptr;
+};
+
+static void planner_loop(dgds_server* s) {
+  cudaSetDevice(s->p.device);
+  for (;;) {
+    std::shared_ptr<dgds_server::PlanJob> j;
+    {
+      std::unique_lock<std::mutex> lk(s->pj_mu);
+      s->pj_cv.wait(lk, [&] { return s->pj_stop || !s->pj_queue.empty(); });
+      if (s->pj_queue.empty()) return;  // stopping
+      j = s->pj_queue.front();
+      s->pj_queue.pop_front();
+    }
+    int rc = DGDS_OK;
+    if (j->ready && cudaEventSynchronize(j->ready) != cudaSuccess)
+      rc = fail(DGDS_ECUDA, "metadata event of a routed plan failed");
+    if (rc == DGDS_OK)
+      rc = dgds_update_plan_routed(s, j->n_seg, j->seg_rows, j->h_counts, j->h_meta, j->meta_stride, j->d_rows,
+                                   j->row_words, j->now, &j->n_rejected, &j->plan);
+    {
+      std::lock_guard<std::mutex> lk(s->pj_mu);
+      j->rc = rc;
+      if (rc) j->msg = dgds_last_error();
+      j->done = true;
+    }
+    s->pj_done_cv.notify_all();
+  }
+}
+
+static void stop_planner(dgds_server* s) {
+  {
+    std::lock_guard<std::mutex> lk(s->pj_mu);
+    s->pj_stop = true;
+  }
+  s->pj_cv.notify_all();
+  if (s->planner.joinable()) s->planner.join();
+  for (auto& kv : s->pj_jobs) delete kv.second->plan;  // planned but never taken
+  s->pj_jobs.clear();
+}
+
+extern "C" {
+
+int dgds_update_plan_routed_async(dgds_server* s, void* ready_event, int32_t n_seg, int64_t seg_rows,
+                                  const int32_t* h_counts, const int32_t* h_meta, int32_t meta_stride,
+                                  const int32_t* d_rows, int32_t row_words, double now, uint64_t* job) {
+  if (!s || !job || !d_rows) return fail(DGDS_EINVAL, "bad routed append arguments");
+  auto j = std::make_shared<dgds_server::PlanJob>();
+  j->ready = static_cast<cudaEvent_t>(ready_event);
+  j->n_seg = n_seg;
+  j->seg_rows = seg_rows;
+  j->h_counts = h_counts;
+  j->h_meta = h_meta;
+  j->meta_stride = meta_stride;
+  j->d_rows = d_rows;
+  j->row_words = row_words;
+  j->now = now;
+  {
+    std::lock_guard<std::mutex> lk(s->pj_mu);
+    if (!s->planner.joinable()) s->planner = std::thread(planner_loop, s);
+    *job = ++s->pj_next;
+    s->pj_jobs[*job] = j;
+    s->pj_queue.push_back(j);
+  }
+  s->pj_cv.notify_one();
+  return DGDS_OK;
+}
+
+int dgds_update_plan_take(dgds_server* s, uint64_t job, int64_t* n_rejected, dgds_update_plan** out) {
+  if (!s || !out) return fail(DGDS_EINVAL, "null argument");
+  *out = nullptr;
+  std::shared_ptr<dgds_server::PlanJob> j;
+  {
+    std::unique_lock<std::mutex> lk(s->pj_mu);
+    auto it = s->pj_jobs.find(job);
+    if (it == s->pj_jobs.end()) return fail(DGDS_EINVAL, "unknown plan job");
+    j = it->second;
+    s->pj_done_cv.wait(lk, [&] { return j->done; });
+    s->pj_jobs.erase(it);
+  }
+  if (n_rejected) *n_rejected = j->n_rejected;
+  if (j->rc) return fail(j->rc, j->msg);
+  *out = j->plan;
   return DGDS_OK;
 }
 

@@ -406,6 +406,16 @@ struct dgds_server {
     std::string launch_msg;
   } pq;
   int stage_tasks = 8;  // workers of an asynchronous stage; DGDS_STAGE_TASKS
+  // asynchronous routed planning (dgds_update_plan_routed_async / _take): one server-owned
+  // planner thread runs the jobs in submission order, each after its metadata-ready event
+  struct PlanJob;
+  std::thread planner;
+  std::mutex pj_mu;
+  std::condition_variable pj_cv, pj_done_cv;
+  std::deque<std::shared_ptr<PlanJob>> pj_queue;
+  std::map<uint64_t, std::shared_ptr<PlanJob>> pj_jobs;
+  uint64_t pj_next = 0;
+  bool pj_stop = false;
   // plans whose history-log records are not yet in their groups' logs (device / routed update
   // plans append them after their K1 launch, off the routed critical path); creation order
   std::vector<struct dgds_update_plan*> log_pending;

@@ -170,8 +170,9 @@ def test_apply_blob_errors_match_reference(reference):
 
 def test_device_and_routed_updates_keep_replica_logs():
     """Device-buffer updates (dgds_update_batch_device) and two-phase routed updates
-    (dgds_update_plan_routed, then dgds_update_launch; the next plan is made before the previous
-    launch) append their history-log records after the K1 launch. fetch_cst blobs (full and
+    (dgds_update_plan_routed, or the planner thread's _async / _take, then dgds_update_launch;
+    the next plan is made before the previous launch) append their history-log records after
+    the K1 launch. fetch_cst blobs (full and
     delta) stay byte-identical to a host-path twin fed the same records."""
     import ctypes as C
     import torch
@@ -222,8 +223,16 @@ def test_device_and_routed_updates_keep_replica_logs():
         counts = np.array([n], np.int32)
         nrej = C.c_int64()
         plan = C.c_void_p()
-        _lib.check(L.dgds_update_plan_routed(routed.handle, 1, n, counts.ctypes.data, meta.ctypes.data, 5,
-                                             C.c_void_p(d_rows.data_ptr()), RW, now, C.byref(nrej), C.byref(plan)))
+        if rnd % 2:  # the server's planner thread (dgds_update_plan_routed_async / _take)
+            job = C.c_uint64()
+            _lib.check(L.dgds_update_plan_routed_async(routed.handle, None, 1, n, counts.ctypes.data,
+                                                       meta.ctypes.data, 5, C.c_void_p(d_rows.data_ptr()), RW, now,
+                                                       C.byref(job)))
+            _lib.check(L.dgds_update_plan_take(routed.handle, job.value, C.byref(nrej), C.byref(plan)))
+        else:
+            _lib.check(L.dgds_update_plan_routed(routed.handle, 1, n, counts.ctypes.data, meta.ctypes.data, 5,
+                                                 C.c_void_p(d_rows.data_ptr()), RW, now, C.byref(nrej),
+                                                 C.byref(plan)))
         assert nrej.value == 0
         if pending is not None:
             _lib.check(L.dgds_update_launch(routed.handle, pending[0], None))
