@@ -588,7 +588,8 @@ def run_multi(args, world, rank, local, dev):
 
     if dbg or host_t:
         print(f"rank {rank} breakdown (s, all steps):",
-              {k: (round(v, 4) if isinstance(v, float) else v) for k, v in prof_host.items()}, flush=True)
+              dict({k: (round(v, 4) if isinstance(v, float) else v) for k, v in prof_host.items()
+                    if k != "route_cur_each_us"}, rank=rank, cores=sorted(os.sched_getaffinity(0))), flush=True)
     if use_px:
         timed_out, _ = px.status()
         if timed_out:
