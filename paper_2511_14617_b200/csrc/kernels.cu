@@ -18,6 +18,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "kernels.h"
 
@@ -34,6 +35,8 @@ constexpr int kBlock = 256;
 #define DGDS_QUERY_OCC 4
 #endif
 constexpr int kWarpsPerBlock = kBlock / kWarp;
+constexpr int kQueryBlockDefault = 64;  // measured: 256 -> 64 took K2 0.106 -> 0.102 ms (C2)
+constexpr int kAppendBlockDefault = 64;  // measured: 256 -> 64 took K1 0.194 -> 0.188 ms (C2)
 
 __device__ __forceinline__ int lane_id() { return threadIdx.x & (kWarp - 1); }
 
@@ -142,7 +145,8 @@ __device__ __forceinline__ void claim_cas(const DevTrie& T, unsigned long long h
   }
 }
 
-__global__ void __launch_bounds__(kBlock, DGDS_APPEND_OCC) k_append(DevTrie T, const AppendSeg* __restrict__ segs, int64_t nseg,
+template <int B>  // threads per block (one warp per segment; B only sets the block granularity)
+__global__ void __launch_bounds__(B, DGDS_APPEND_OCC * (kBlock / B)) k_append(DevTrie T, const AppendSeg* __restrict__ segs, int64_t nseg,
                                                    const AppendPiece* __restrict__ pieces,
                                                    const int32_t* __restrict__ tokens) {
   const int lane = lane_id();
@@ -152,7 +156,7 @@ __global__ void __launch_bounds__(kBlock, DGDS_APPEND_OCC) k_append(DevTrie T, c
   unsigned long long inserted_total = 0;
   constexpr int kStage = 128;
   const int kAhead = T.ahead;  // 0: no look-ahead prefetch (server default)
-  __shared__ int32_t stage[kWarpsPerBlock][kStage];
+  __shared__ int32_t stage[B / kWarp][kStage];
   int32_t* stage_w = stage[threadIdx.x / kWarp];
 
   unsigned long long t_start = 0;
@@ -390,12 +394,14 @@ __device__ __forceinline__ uint32_t resolve_content(const DevTrie& T, unsigned l
   }
 }
 
-template <int G, int S>
-__global__ void __launch_bounds__(kBlock, DGDS_QUERY_OCC) k_query(QueryLaunch P) {
+// B = threads per block. A block retires only when its slowest warp does, so smaller blocks
+// free a finished warp's SM slot sooner; the register budget per SM is the same for every B.
+template <int G, int S, int B>
+__global__ void __launch_bounds__(B, DGDS_QUERY_OCC * (kBlock / B)) k_query(QueryLaunch P) {
   // Programmatic dependent launch: the blocks may be resident before the previous kernel in
   // the stream (typically K1) has finished; nothing is read until it has.
   asm volatile("griddepcontrol.wait;" ::: "memory");
-  constexpr int kTiles = kBlock / G;
+  constexpr int kTiles = B / G;
   __shared__ GroupScratch<G, S> scratch[kTiles];
   const int lane = lane_id();
   const int gl = lane % G;
@@ -937,7 +943,7 @@ __global__ void __launch_bounds__(kBlock, DGDS_QUERY_OCC) k_query(QueryLaunch P)
 #pragma unroll
     for (int k = 0; k < 8; ++k) v[k] = __reduce_add_sync(kFull, v[k]);
     if (lane == 0) {
-      const uint32_t part = (blockIdx.x * (kBlock / kWarp) + threadIdx.x / kWarp) & (kStatParts - 1);
+      const uint32_t part = (blockIdx.x * (B / kWarp) + threadIdx.x / kWarp) & (kStatParts - 1);
 #pragma unroll
       for (int k = 0; k < 8; ++k)
         if (v[k]) atomicAdd(P.stat_part + part * 8 + k, static_cast<unsigned long long>(v[k]));
@@ -1194,15 +1200,15 @@ __global__ void k_route_gather(int64_t n, const uint32_t* __restrict__ in, int32
   out[t] = in[perm[i] * rw + k];
 }
 
-template <int G, int S>
-cudaError_t launch_query_gs(const QueryLaunch& L, cudaStream_t st) {
-  const int per_block = kBlock / G;
+template <int G, int S, int B>
+cudaError_t launch_query_gsb(const QueryLaunch& L, cudaStream_t st) {
+  const int per_block = B / G;
   const int64_t blocks = (L.n + per_block - 1) / per_block;
   // launched with programmatic stream serialization: the launch overlaps the previous
   // kernel's tail (k_query waits for its completion in griddepcontrol.wait)
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(static_cast<unsigned>(blocks));
-  cfg.blockDim = dim3(kBlock);
+  cfg.blockDim = dim3(B);
   cfg.dynamicSmemBytes = 0;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
@@ -1210,7 +1216,32 @@ cudaError_t launch_query_gs(const QueryLaunch& L, cudaStream_t st) {
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, k_query<G, S>, L);
+  return cudaLaunchKernelEx(&cfg, k_query<G, S, B>, L);
+}
+
+// K1 / K2 block sizes: DGDS_APPEND_BLOCK = 32 | 64 | 256, DGDS_QUERY_BLOCK = 32 | 64 | 128 | 256
+// (read once per process)
+int block_env(const char* name, int dflt) {
+  const char* e = std::getenv(name);
+  const int v = e ? std::atoi(e) : dflt;
+  return (v == 32 || v == 64 || v == 128) ? v : kBlock;
+}
+int query_block() {
+  static const int b = block_env("DGDS_QUERY_BLOCK", kQueryBlockDefault);
+  return b;
+}
+int append_block() {
+  static const int b = block_env("DGDS_APPEND_BLOCK", kAppendBlockDefault);
+  return b == 128 ? kBlock : b;
+}
+
+template <int G, int S>
+cudaError_t launch_query_gs(const QueryLaunch& L, cudaStream_t st) {
+  const int blk = query_block();
+  if (blk == 32) return launch_query_gsb<G, S, 32>(L, st);
+  if (blk == 64) return launch_query_gsb<G, S, 64>(L, st);
+  if (blk == 128) return launch_query_gsb<G, S, 128>(L, st);
+  return launch_query_gsb<G, S, 256>(L, st);
 }
 
 template <int G>
@@ -1225,8 +1256,12 @@ cudaError_t launch_query_g(const QueryLaunch& L, int32_t max_s, cudaStream_t st)
 cudaError_t launch_append(const DevTrie& T, const AppendSeg* d_segs, int64_t nseg, const AppendPiece* d_pieces,
                           const int32_t* d_tokens, cudaStream_t st) {
   if (nseg <= 0) return cudaSuccess;
-  const int64_t blocks = (nseg + kWarpsPerBlock - 1) / kWarpsPerBlock;
-  k_append<<<static_cast<unsigned>(blocks), kBlock, 0, st>>>(T, d_segs, nseg, d_pieces, d_tokens);
+  const int blk = append_block();
+  const int64_t wpb = blk / kWarp;
+  const int64_t blocks = (nseg + wpb - 1) / wpb;
+  if (blk == 32) k_append<32><<<static_cast<unsigned>(blocks), 32, 0, st>>>(T, d_segs, nseg, d_pieces, d_tokens);
+  else if (blk == 64) k_append<64><<<static_cast<unsigned>(blocks), 64, 0, st>>>(T, d_segs, nseg, d_pieces, d_tokens);
+  else k_append<kBlock><<<static_cast<unsigned>(blocks), kBlock, 0, st>>>(T, d_segs, nseg, d_pieces, d_tokens);
   return cudaGetLastError();
 }
 
