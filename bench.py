@@ -40,8 +40,8 @@ DEFAULT_CONFIG = "C2"
 RANDOM_CEILING_GBS = 1155.0
 # dram__bytes_read.sum + dram__bytes_write.sum per launch, from one
 # `ncu --set full` capture of the same step (profiles/r1_summary.md).
-QUERY_TRAFFIC = 165634560 + 11755520   # prof_query_r1k (k_query<4,8>, timed step)
-APPEND_TRAFFIC = 157042432 + 76937472  # prof_append_r1k (k_append, timed step)
+QUERY_TRAFFIC = 165623808 + 12307456   # prof_query_r1m (k_query<4,8,64>, timed step)
+APPEND_TRAFFIC = 157086720 + 74619648  # prof_append_r1m (k_append<64>, timed step)
 CONFIG_NAMES = {
     "C1": "single group 16 x 4K, vocab 32K",
     "C2": "Moonlight-shaped 256 groups x 16 responses <=32K tokens, vocab 163840",
