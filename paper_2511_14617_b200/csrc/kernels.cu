@@ -31,10 +31,12 @@ constexpr int kBlock = 256;
 #ifndef DGDS_APPEND_OCC
 #define DGDS_APPEND_OCC 4  // resident blocks per SM the register budget is sized for
 #endif
+#ifndef DGDS_K1_PDL_TRIGGER
+#define DGDS_K1_PDL_TRIGGER 0  // measured flat on C2 (profiles/r1_pdl_trigger.txt)
+#endif
 #ifndef DGDS_QUERY_OCC
 #define DGDS_QUERY_OCC 4
 #endif
-constexpr int kWarpsPerBlock = kBlock / kWarp;
 constexpr int kQueryBlockDefault = 64;  // measured: 256 -> 64 took K2 0.106 -> 0.102 ms (C2)
 constexpr int kAppendBlockDefault = 64;  // measured: 256 -> 64 took K1 0.194 -> 0.188 ms (C2)
 
@@ -149,6 +151,13 @@ template <int B>  // threads per block (one warp per segment; B only sets the bl
 __global__ void __launch_bounds__(B, DGDS_APPEND_OCC * (kBlock / B)) k_append(DevTrie T, const AppendSeg* __restrict__ segs, int64_t nseg,
                                                    const AppendPiece* __restrict__ pieces,
                                                    const int32_t* __restrict__ tokens) {
+#if DGDS_K1_PDL_TRIGGER
+  // Let a programmatic dependent (K2) launch now: its blocks take the SM slots K1's single wave
+  // leaves free and sit in griddepcontrol.wait until K1 has completed and flushed, so K2's launch
+  // and ramp hide under K1's tail. Every K1 block triggers before dependents can launch, so they
+  // never hold slots K1 still needs.
+  asm volatile("griddepcontrol.launch_dependents;");
+#endif
   const int lane = lane_id();
   const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / kWarp;
   const int64_t nwarps = static_cast<int64_t>(gridDim.x) * blockDim.x / kWarp;
@@ -933,13 +942,13 @@ __global__ void __launch_bounds__(B, DGDS_QUERY_OCC * (kBlock / B)) k_query(Quer
     // kStatParts partitions: no same-address storm (the last block sums them)
     const int ctoks = tile.sum(gl < nf ? sm.f.len[gl] : 0);
     const bool lead = valid && gl == 0;
-    const uint32_t B = lead ? static_cast<uint32_t>(4ull * plen + 32ull + 32ull * st_lookups + 32ull * st_exp +
-                                                    32ull * st_csec + 4ull * ctoks + 16ull * nf)
-                            : 0u;
+    const uint32_t qbytes = lead ? static_cast<uint32_t>(4ull * plen + 32ull + 32ull * st_lookups + 32ull * st_exp +
+                                                         32ull * st_csec + 4ull * ctoks + 16ull * nf)
+                                 : 0u;
     uint32_t v[8] = {lead ? 1u : 0u, lead ? static_cast<uint32_t>(plen) : 0u,
                      lead ? static_cast<uint32_t>(st_lookups) : 0u, lead ? static_cast<uint32_t>(st_exp) : 0u,
                      lead ? static_cast<uint32_t>(st_csec) : 0u, lead ? static_cast<uint32_t>(nf) : 0u,
-                     lead ? static_cast<uint32_t>(ctoks) : 0u, B};
+                     lead ? static_cast<uint32_t>(ctoks) : 0u, qbytes};
 #pragma unroll
     for (int k = 0; k < 8; ++k) v[k] = __reduce_add_sync(kFull, v[k]);
     if (lane == 0) {
