@@ -149,8 +149,16 @@ int dgds_has_group(dgds_server* s, int32_t handle, int32_t* out);
 int dgds_group_version(dgds_server* s, int32_t handle, uint64_t* out);
 int dgds_stored_tokens(dgds_server* s, int32_t handle, int32_t request_id, uint64_t* out);
 int dgds_shard_group_count(dgds_server* s, int32_t shard, uint64_t* out);
-/* Device-side trie size: nodes in use (synchronises). */
+/* Device-side trie size: the reference's node count (nodes_.size(), root included) summed over
+ * live groups; counts entries plus the implicit count-1 chains below leaves (synchronises). */
 int dgds_node_count(dgds_server* s, uint64_t* out);
+/* Table entries in use (materialised windows: nodes with count >= 2 and leaves). */
+int dgds_entry_count(dgds_server* s, uint64_t* out);
+/* Reads and clears the device error flags (synchronises): bit 0 a device-API query with invalid
+ * arguments (it returned no candidates), bit 1 a negative token in a device-path update batch
+ * (that batch and every later one inserted nothing; its replies were already returned), bits
+ * 2-4 internal invariants (never expected). Returns DGDS_OK with *flags = 0 when clean. */
+int dgds_device_error(dgds_server* s, int32_t* flags);
 /* Slots of the open-addressing node table (load factor = stored nodes / slots). */
 int dgds_index_slots(dgds_server* s, uint64_t* slots);
 
@@ -365,6 +373,10 @@ int dgds_profile_enable(dgds_server* s, int32_t on);
 /* Debug: record per-query phase cycles of later device-API query launches into d_buf[n][8] (NULL = off). */
 /* Debug (DGDS_APPEND_DBG set at create): per-warp [start, end] globaltimer ns of the last K1 launch. */
 int dgds_debug_append_timing(dgds_server* s, uint64_t* out, int64_t n_warps);
+/* Debug: copies device state into out (host), at most `bytes`: which 0 = slot table (32 B slots,
+ * csrc/trie.cuh), 1 = stream table, 2 = active rows, 3 = ov rows, 4 = stream-history arena,
+ * 5 = conversion-event queue. */
+int dgds_debug_dump(dgds_server* s, int32_t which, void* out, uint64_t bytes);
 int dgds_debug_query_timing(dgds_server* s, void* d_buf);
 /* Device->host bytes moved by the last host-buffer query call (results are compacted on device). */
 int dgds_last_transfer(dgds_server* s, uint64_t* d2h_bytes);

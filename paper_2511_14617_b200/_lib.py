@@ -157,6 +157,8 @@ EXPORTS = {
     "dgds_stored_tokens": (C.c_int, [_P, _I32, _I32, C.POINTER(_U64)]),
     "dgds_shard_group_count": (C.c_int, [_P, _I32, C.POINTER(_U64)]),
     "dgds_node_count": (C.c_int, [_P, C.POINTER(_U64)]),
+    "dgds_entry_count": (C.c_int, [_P, C.POINTER(_U64)]),
+    "dgds_device_error": (C.c_int, [_P, C.POINTER(C.c_int32)]),
     "dgds_index_slots": (C.c_int, [_P, C.POINTER(_U64)]),
     "dgds_update_batch": (C.c_int, [_P, _I64, _P, _P, _P, _P, _P, _D, _P]),
     "dgds_update_batch_device": (C.c_int, [_P, _I64, _P, _P, _P, _P, _P, _D, _P, _P]),
@@ -180,6 +182,7 @@ EXPORTS = {
     "dgds_batch_speculate_zc": (C.c_int, [_P, _I64, _P, _P, _P, _P, _P, _P, C.POINTER(RecordLayout), _P, _I64, _I32,
                                           _I32, _P, _P]),
     "dgds_debug_append_timing": (C.c_int, [_P, _P, _I64]),
+    "dgds_debug_dump": (C.c_int, [_P, C.c_int32, _P, _U64]),
     "dgds_compact_memory": (C.c_int, [_P]),
     "dgds_get_memory_stats": (C.c_int, [_P, C.POINTER(MemoryStats)]),
     "dgds_touch_group": (C.c_int, [_P, _I32, C.c_double]),

@@ -18,7 +18,9 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
+#include <unistd.h>
 
 #include "kernels.h"
 
@@ -43,27 +45,67 @@ constexpr int kAppendBlockDefault = 64;  // measured: 256 -> 64 took K1 0.194 ->
 __device__ __forceinline__ int lane_id() { return threadIdx.x & (kWarp - 1); }
 
 // ---------------------------------------------------------------------------
-// K1: append
-//
-// One warp per stream segment. Lane i owns window length i+1 (Stream::active[i],
-// cst.hpp:115-118). Per token t, lanes i < min(depth_cap, len+1) claim-or-find
-// the window that ends at t: key {hash, parent = active[i-1] of the previous
-// token (group root for lane 0), t}, then count it — insert_token's loop
-// (cst.cpp:105-116) with the depth levels in parallel.
-//
-// The claim chain is inherently sequential (a token's parents are the previous
-// token's nodes), but its ADDRESSES are not: home buckets depend on window
-// content only, so a look-ahead hash prefetches them into L2 a few tokens
-// ahead and the chain's line reads / CASes hit L2 instead of DRAM.
+// k_stage: every record's tokens from the batch buffer into the history arena
+// (record order; replica blobs) and into its stream's extent, and the stream
+// table row {extent, stored length after the batch, root}. It runs before K1,
+// so K1's conversion walks (below) read every stream of the batch at its final
+// length. A negative token (possible only on the device paths; the host path
+// rejects it before planning) sets err bit 1, and K1 then inserts nothing.
 
-// 16-byte key of a slot through L2 (coherent with the CASes of other warps).
-__device__ __forceinline__ void load_key_cg(const Slot* p, unsigned long long& k0, unsigned long long& k1) {
-  asm volatile("ld.global.cg.v2.u64 {%0,%1}, [%2];" : "=l"(k0), "=l"(k1) : "l"(p));
+__global__ void k_stage(DevTrie T, const AppendSeg* __restrict__ segs, int64_t nseg,
+                        const AppendPiece* __restrict__ pieces, int64_t npieces, const int32_t* __restrict__ tokens) {
+  const int lane = lane_id();
+  const int64_t gt = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t nth = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t s = gt; s < nseg; s += nth) {
+    const AppendSeg g = segs[s];
+    T.sinfo[g.stream] = StreamInfo{g.sh_base, static_cast<uint32_t>(g.start + g.n), g.root};
+  }
+  int32_t any = 0;
+  for (int64_t w = gt / kWarp; w < npieces; w += nth / kWarp) {
+    const AppendPiece pc = pieces[w];
+    for (uint32_t k = lane; k < pc.n; k += kWarp) {
+      const int32_t v = tokens[pc.tok_off + k];
+      any |= v;
+      T.hist[pc.hist_off + k] = v;
+      T.shist[pc.sh_off + k] = v;
+    }
+  }
+  if (__any_sync(kFull, any < 0) && lane == 0) atomicOr(T.err, 2);
 }
 
-__device__ __forceinline__ void cas128(Slot* s, unsigned long long h, unsigned long long pt, unsigned long long& o0,
+// ---------------------------------------------------------------------------
+// K1: append (GroupDraftIndex::append / insert_token / ensure_child, cst.cpp:90-133)
+//
+// One warp per stream segment. Lane i owns the window of length i+1 ending at
+// the current token (Stream::active[i], cst.hpp:115-118); its parent is lane
+// i-1's window at the previous token. Per token, a lane ADDS one occurrence of
+// its window only when the parent is a node (count >= 2) or the group root:
+//   - absent  -> a new LEAF holding this occurrence; the window's continuation
+//                (all longer windows on this diagonal) is implicit from here on;
+//   - a leaf  -> it becomes a node (count 2); the leaf's own occurrence must now
+//                continue explicitly: a CONVERSION WALK (below) is queued;
+//   - a node  -> count + 1.
+// A lane whose parent is implicit does nothing: its window has count 1 and is
+// the stream's own continuation below a leaf. Counts are order-free sums and a
+// leaf converts exactly once (the atomic that takes its counter from 0), so
+// concurrent streams of one group reach exactly the reference's trie.
+//
+// Conversion walk (K1b, one thread per event queued by K1): the displaced
+// occurrence (stream s, window ending at e) continues with the windows ending
+// at e+1, e+2, ... on the same diagonal, which nobody counted (s's owner
+// treated them as implicit). The walk adds them one by one from s's extent
+// (final for this batch: k_stage ran first) until it creates a leaf, reaches
+// the depth cap or the end of s. Converting another leaf on the way also
+// continues that leaf's own occurrence (a DFS stack; depths strictly increase,
+// so it holds < 32 frames). A walk that reaches the end of s leaves the node
+// it holds in ov[s][depth-1]; s's next segment takes it as that lane's state.
+// K1b runs after K1 has finished, so no segment of this batch reads ov while a
+// walk writes it.
+
+__device__ __forceinline__ void cas128(Slot* s, unsigned long long n0, unsigned long long n1, unsigned long long& o0,
                                        unsigned long long& o1) {
-  // {h, parent|token}: empty -> ours (claim), else returns the occupant
+  // {key, occ}: empty (all zero) -> ours, else returns the occupant
   asm volatile(
       "{\n\t.reg .b128 c, v, o;\n\t"
       "mov.b128 c, {%2, %3};\n\t"
@@ -71,202 +113,222 @@ __device__ __forceinline__ void cas128(Slot* s, unsigned long long h, unsigned l
       "atom.global.cas.b128 o, [%6], c, v;\n\t"
       "mov.b128 {%0, %1}, o;\n\t}"
       : "=l"(o0), "=l"(o1)
-      : "l"(0ull), "l"(0ull), "l"(h), "l"(pt), "l"(s)
+      : "l"(0ull), "l"(0ull), "l"(n0), "l"(n1), "l"(s)
       : "memory");
 }
 
-// {next_sibling, root} of a new node in one 64-bit store
-__device__ __forceinline__ void store_link(Slot* s, uint32_t next_sibling, uint32_t root) {
-  *reinterpret_cast<unsigned long long*>(&s->next_sibling) =
-      static_cast<unsigned long long>(next_sibling) | (static_cast<unsigned long long>(root) << 32);
+// {h32, next_sibling} of a new entry in one 64-bit store
+__device__ __forceinline__ void store_link(Slot* s, uint32_t h32, uint32_t next_sibling) {
+  *reinterpret_cast<unsigned long long*>(&s->h32) =
+      static_cast<unsigned long long>(h32) | (static_cast<unsigned long long>(next_sibling) << 32);
 }
 
-// Claim-or-find of window {h, parent, token} (ensure_child, cst.cpp:90-103):
-// read the bucket's 4 keys in one line read; a match only bumps the count,
-// otherwise ONE CAS claims the first empty slot (a single CAS site keeps the
-// lanes of the warp convergent). A lost race re-reads the same bucket.
-__device__ __forceinline__ void claim(const DevTrie& T, unsigned long long h, uint32_t parent, int32_t token,
-                                      uint32_t& id, bool& inserted) {
-  const unsigned long long pt = pack_pt(parent, token);
+// One occurrence of window (parent, token): CAS-first over the probe sequence. Slots fill in
+// probe order and are never freed between rebuilds, so the CAS's old value settles the case:
+// 0 = our new leaf; our key = present (count it); another key = probe on.
+// Returns the entry id; created = a new leaf; old = its counter before (0: it was a leaf and is
+// now a node, whose first occurrence is returned in occ_old).
+__device__ __forceinline__ uint32_t add_occurrence(const DevTrie& T, uint32_t h32, uint32_t parent, int32_t token,
+                                                   unsigned long long occ, bool& created, uint32_t& old,
+                                                   unsigned long long& occ_old) {
+  const unsigned long long key = pack_key(parent, token);
   const uint64_t cap = T.cap;
-  const uint64_t nb = cap / kBucket;
-  uint64_t b = home_bucket(h, nb);
-  while (true) {
-    unsigned long long k0[kWindow], k1[kWindow];
-#pragma unroll
-    for (int s = 0; s < kWindow; ++s) load_key_cg(T.slots + window_slot(b, s, cap), k0[s], k1[s]);
-    int found = -1, empty = -1;
-#pragma unroll
-    for (int s = kWindow - 1; s >= 0; --s) {  // first match / first empty in probe order
-      if (k0[s] == h && k1[s] == pt) found = s;
-      if (k0[s] == 0ull) {
-        empty = s;
-        found = found > s ? -1 : found;  // nothing valid lies beyond an empty slot
-      }
+  uint64_t i = home_bucket(h32, cap / kBucket) * kBucket;
+  for (uint64_t probes = 0;; ++probes) {
+    if (probes > 65536) {  // defensive: probe runs are short below the rebuild load
+      atomicOr(T.err, 8);
+      created = false;
+      old = 1;
+      occ_old = 0;
+      return 0;
     }
-    bool ins = false;
-    if (found < 0 && empty >= 0) {
-      unsigned long long o0, o1;
-      cas128(T.slots + window_slot(b, empty, cap), h, pt, o0, o1);
-      ins = o0 == 0ull;
-      if (ins || (o0 == h && o1 == pt)) found = empty;
-      else continue;  // lost the slot to another key: re-read this window
-    }
-    if (found >= 0) {
-      const uint64_t i = window_slot(b, found, cap);
-      if (!ins) atomicAdd(&T.slots[i].count, 1u);  // RED; an insert's occurrence is implicit
-      inserted = ins;
-      id = static_cast<uint32_t>(i + 1);
-      return;
-    }
-    b += kWindow / kBucket;  // window full without a match
-    if (b >= nb) b -= nb;
-  }
-}
-
-// CAS-first claim: no read before the first atomic. Slots fill in probe order and are never
-// freed between rebuilds, so walking the probe sequence with CAS(empty -> key) either finds
-// the key (the CAS returns it), claims the first empty slot (returns 0), or passes an
-// occupant — the same slot the load-first claim would pick, with one random access instead
-// of a window read followed by the CAS on an insert, the common case at depth.
-__device__ __forceinline__ void claim_cas(const DevTrie& T, unsigned long long h, uint32_t parent, int32_t token,
-                                          uint32_t& id, bool& inserted) {
-  const unsigned long long pt = pack_pt(parent, token);
-  const uint64_t cap = T.cap;
-  uint64_t i = home_bucket(h, cap / kBucket) * kBucket;
-  while (true) {
     unsigned long long o0, o1;
-    cas128(T.slots + i, h, pt, o0, o1);
-    if (o0 == 0ull || (o0 == h && o1 == pt)) {
-      inserted = o0 == 0ull;
-      if (!inserted) atomicAdd(&T.slots[i].count, 1u);  // RED; an insert's occurrence is implicit
-      id = static_cast<uint32_t>(i + 1);
-      return;
+    cas128(T.slots + i, key, occ, o0, o1);
+    if (o0 == 0ull) {
+      created = true;
+      old = 0;
+      occ_old = 0;
+      return static_cast<uint32_t>(i + 1);
+    }
+    if (o0 == key) {
+      created = false;
+      occ_old = o1;
+      old = atomicAdd(&T.slots[i].count, 1u);
+      return static_cast<uint32_t>(i + 1);
     }
     if (++i == cap) i = 0;
   }
 }
 
+__device__ void conversion_walk(const DevTrie& T, WalkEvent e, unsigned long long& inserted) {
+  struct Frame {
+    unsigned long long h;
+    uint32_t id, depth, stream, pos;
+  };
+  Frame stk[DGDS_MAX_DEPTH];
+  int sp = 0;
+  Frame cur{e.h, e.id, e.depth, e.stream, e.pos};
+  const uint32_t D = static_cast<uint32_t>(T.depth_cap);
+  for (int guard = 0;; ++guard) {
+    if (guard > (1 << 16)) {  // defensive: a walk is bounded by its conversions
+      atomicOr(T.err, 16);
+      return;
+    }
+    const StreamInfo si = T.sinfo[cur.stream];
+    const uint32_t p = cur.pos + 1;
+    if (p == si.len) T.ov[static_cast<uint64_t>(cur.stream) * kWarp + cur.depth - 1] = cur.id;
+    if (cur.depth < D && p < si.len) {
+      const int32_t x = T.shist[si.base + p];
+      const unsigned long long h2 = hash_step(cur.h, x);
+      const uint32_t hh = hash32(h2);
+      bool created;
+      uint32_t old;
+      unsigned long long oo;
+      const uint32_t id = add_occurrence(T, hh, cur.id, x, pack_occ(cur.stream, cur.depth + 1, p), created, old, oo);
+      if (created) {  // a new leaf: the rest of this occurrence is implicit below it
+        ++inserted;
+        store_link(T.slots + (id - 1), hh, atomicExch(&T.slots[cur.id - 1].first_child, id));
+      } else {
+        const Frame nxt{h2, id, cur.depth + 1, cur.stream, p};
+        if (old == 0u && sp == DGDS_MAX_DEPTH) atomicOr(T.err, 4);  // cannot happen: depths increase
+        if (old == 0u && sp < DGDS_MAX_DEPTH) {  // another leaf converted: its occurrence continues too
+          stk[sp++] = nxt;
+          cur = Frame{h2, id, cur.depth + 1, occ_stream(static_cast<uint32_t>(oo)), static_cast<uint32_t>(oo >> 32)};
+        } else {
+          cur = nxt;
+        }
+        continue;
+      }
+    }
+    if (sp == 0) break;
+    cur = stk[--sp];
+  }
+}
+
+__global__ void k_walks(DevTrie T) {
+  const unsigned long long n = __ldcg(T.ev_count);
+  unsigned long long inserted = 0;
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
+    conversion_walk(T, T.ev[i], inserted);
+  const unsigned long long w = __reduce_add_sync(kFull, static_cast<unsigned>(inserted));
+  const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / kWarp;
+  if (lane_id() == 0 && w) atomicAdd(T.used + ((warp & (kUsedParts - 1)) * 8), w);
+  // the last block to finish resets the event queue for the next batch
+  __shared__ bool last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(T.ev_count + 1, 1ull) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (last && threadIdx.x == 0) {
+    T.ev_count[0] = 0;
+    T.ev_count[1] = 0;
+  }
+}
+
 template <int B>  // threads per block (one warp per segment; B only sets the block granularity)
-__global__ void __launch_bounds__(B, DGDS_APPEND_OCC * (kBlock / B)) k_append(DevTrie T, const AppendSeg* __restrict__ segs, int64_t nseg,
-                                                   const AppendPiece* __restrict__ pieces,
-                                                   const int32_t* __restrict__ tokens) {
-#if DGDS_K1_PDL_TRIGGER
-  // Let a programmatic dependent (K2) launch now: its blocks take the SM slots K1's single wave
-  // leaves free and sit in griddepcontrol.wait until K1 has completed and flushed, so K2's launch
-  // and ramp hide under K1's tail. Every K1 block triggers before dependents can launch, so they
-  // never hold slots K1 still needs.
-  asm volatile("griddepcontrol.launch_dependents;");
-#endif
+__global__ void __launch_bounds__(B, DGDS_APPEND_OCC * (kBlock / B))
+    k_append(DevTrie T, const AppendSeg* __restrict__ segs, int64_t nseg) {
+  if (__ldcg(T.err) & 2) return;  // k_stage found a negative token: the batch inserts nothing
   const int lane = lane_id();
   const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / kWarp;
   const int64_t nwarps = static_cast<int64_t>(gridDim.x) * blockDim.x / kWarp;
   const int D = T.depth_cap;
   unsigned long long inserted_total = 0;
-  constexpr int kStage = 128;
-  const int kAhead = T.ahead;  // 0: no look-ahead prefetch (server default)
-  __shared__ int32_t stage[B / kWarp][kStage];
-  int32_t* stage_w = stage[threadIdx.x / kWarp];
 
   unsigned long long t_start = 0;
   if (T.dbg) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
   for (int64_t sg = warp; sg < nseg; sg += nwarps) {
     const AppendSeg g = segs[sg];
     const uint64_t len0 = g.start;
-    uint32_t* act_row = T.active + static_cast<uint64_t>(g.stream) * kWarp;
-    int32_t* tail_row = T.tail + static_cast<uint64_t>(g.stream) * kWarp;
+    const uint32_t stream = g.stream;
+    uint32_t* act_row = T.active + static_cast<uint64_t>(stream) * kWarp;
+    uint32_t* ov_row = T.ov + static_cast<uint64_t>(stream) * kWarp;
+    const int32_t* ext = T.shist + g.sh_base;
     const unsigned long long hr = root_hash(g.root);
 
-    // hashes of the windows ending at the last stored token, from the tail ring
-    unsigned long long h_init = 0;
+    // hashes of the windows ending at the last stored token, from the stream's extent
+    unsigned long long h = 0;
     {
       const int have = static_cast<int>(min(static_cast<uint64_t>(D), len0));
-      const int32_t mytail = tail_row[lane];
-      for (int k = have; k > 0; --k) {  // positions len0-k .. len0-1
-        const int32_t t = __shfl_sync(kFull, mytail, static_cast<int>((len0 - k) & 31));
-        const unsigned long long up = __shfl_up_sync(kFull, h_init, 1);
-        h_init = hash_step(lane == 0 ? hr : up, t);
+      const int32_t mine = lane < have ? ext[len0 - have + lane] : 0;
+      for (int k = 0; k < have; ++k) {
+        const int32_t t = __shfl_sync(kFull, mine, k);
+        const unsigned long long up = __shfl_up_sync(kFull, h, 1);
+        h = hash_step(lane == 0 ? hr : up, t);
       }
     }
-
-    // The segment's tokens are staged through shared memory kStage at a time.
-    // Optionally (T.ahead > 0) a second rolling hash runs ahead of the claim
-    // chain and prefetches those windows' home buckets into L2. Measured on
-    // C2 it is slower than none (the kernel is bound by random DRAM accesses,
-    // not by the chain's latency), so the server leaves it off by default.
-    uint64_t len = len0;
-    unsigned long long h = h_init, hp = h_init;
-    uint64_t lenp = len0;
-    uint32_t a = (lane < D && static_cast<uint64_t>(lane) < len0) ? act_row[lane] : 0u;
-    uint32_t link_slot = 0, link_prev = 0;
-    bool link_pending = false;
-    uint32_t p = 0, poff = 0;
-    while (p < g.npieces) {
-      int filled = 0;  // stage the next <= kStage tokens (coalesced)
-      while (filled < kStage && p < g.npieces) {
-        const AppendPiece pc = pieces[g.piece0 + p];
-        const uint32_t take = min(static_cast<uint32_t>(kStage - filled), pc.n - poff);
-        for (uint32_t k = lane; k < take; k += kWarp) {
-          const int32_t v = tokens[pc.tok_off + poff + k];
-          stage_w[filled + k] = v;
-          T.hist[pc.hist_off + poff + k] = v;  // history arena (coalesced)
-        }
-        filled += static_cast<int>(take);
-        poff += take;
-        if (poff == pc.n) {
-          ++p;
-          poff = 0;
-        }
+    const bool stored_lane = lane < D && static_cast<uint64_t>(lane) < len0;
+    uint32_t a = stored_lane ? act_row[lane] : 0u;
+    {
+      const uint32_t o = ov_row[lane];  // a conversion walk made this lane's window a node
+      if (o) {
+        ov_row[lane] = 0u;
+        if (stored_lane) a = o;
       }
-      __syncwarp();
-      auto advance_ahead = [&](int j) {
-        const int32_t t = stage_w[j];
-        const unsigned long long up = __shfl_up_sync(kFull, hp, 1);
-        hp = hash_step(lane == 0 ? hr : up, t);
-        if (static_cast<uint64_t>(lane) < min(static_cast<uint64_t>(D), lenp + 1))
-          prefetch_l2_window(T.slots + home_bucket(key_hash(hp), T.cap / kBucket) * kBucket);
-        ++lenp;
-      };
-      const int ahead = min(kAhead, filled);
-      for (int j = 0; j < ahead; ++j) advance_ahead(j);
-      for (int j = 0; j < filled; ++j) {
-        if (kAhead > 0 && j + kAhead < filled) advance_ahead(j + kAhead);
-        const int32_t t = stage_w[j];
+    }
+    uint64_t len = len0;
+    uint32_t link_slot = 0, link_prev = 0, link_h = 0;
+    bool link_pending = false;
+    for (uint32_t j0 = 0; j0 < g.n; j0 += kWarp) {
+      const int chunk = static_cast<int>(min(static_cast<uint32_t>(kWarp), g.n - j0));
+      const int32_t tv = lane < chunk ? ext[len0 + j0 + lane] : 0;  // coalesced
+      for (int jj = 0; jj < chunk; ++jj) {
+        const int32_t t = __shfl_sync(kFull, tv, jj);
         const int newsize = static_cast<int>(min(static_cast<uint64_t>(D), len + 1));
         const unsigned long long hup = __shfl_up_sync(kFull, h, 1);
         h = hash_step(lane == 0 ? hr : hup, t);
-        uint32_t parent = __shfl_up_sync(kFull, a, 1);
-        if (lane == 0) parent = g.root;
-        if (lane < newsize) {
-          uint32_t id;
-          bool ins;
-          if (T.claim_cas) claim_cas(T, key_hash(h), parent, t, id, ins);
-          else claim(T, key_hash(h), parent, t, id, ins);
-          if (link_pending) {  // {next_sibling, root} of the node created at the previous token
-            store_link(T.slots + link_slot, link_prev, g.root);
+        const uint32_t pm = __shfl_up_sync(kFull, a, 1);
+        const uint32_t parent = lane == 0 ? g.root : pm;
+        uint32_t na = 0;
+        bool ev = false;
+        uint32_t ev_stream = 0, ev_pos = 0;
+        if (lane < newsize && parent != 0u) {
+          const uint32_t hh = hash32(h);
+          bool created;
+          uint32_t old;
+          unsigned long long oo;
+          const uint32_t id = add_occurrence(T, hh, parent, t, pack_occ(stream, static_cast<uint32_t>(lane) + 1u,
+                                                                        static_cast<uint32_t>(len)),
+                                             created, old, oo);
+          if (link_pending) {  // {h32, next_sibling} of the leaf created at the previous token
+            store_link(T.slots + link_slot, link_h, link_prev);
             link_pending = false;
           }
-          if (ins) {
+          if (created) {
             ++inserted_total;
             if (!is_root_id(parent, T.cap)) {  // root child lists are never enumerated
               link_prev = atomicExch(&T.slots[parent - 1].first_child, id);
               link_slot = id - 1;
+              link_h = hh;
               link_pending = true;
             } else {
-              store_link(T.slots + (id - 1), 0u, g.root);
+              store_link(T.slots + (id - 1), hh, 0u);
+            }
+          } else {
+            na = id;
+            if (old == 0u) {
+              ev = true;
+              ev_stream = occ_stream(static_cast<uint32_t>(oo));
+              ev_pos = static_cast<uint32_t>(oo >> 32);
             }
           }
-          a = id;
         }
-        if (lane == static_cast<int>(len & 31)) tail_row[lane] = t;  // ring of the last 32 tokens
+        a = na;
+        const unsigned m = __ballot_sync(kFull, ev);
+        if (m) {  // queue the conversion walks for K1b (one atomic per warp)
+          unsigned long long at = 0;
+          if (lane == __ffs(m) - 1) at = atomicAdd(T.ev_count, static_cast<unsigned long long>(__popc(m)));
+          at = __shfl_sync(kFull, at, __ffs(m) - 1);
+          if (ev) T.ev[at + __popc(m & ((1u << lane) - 1u))] = WalkEvent{h, a, static_cast<uint32_t>(lane) + 1u,
+                                                                          ev_stream, ev_pos};
+        }
         ++len;
       }
-      // the look-ahead hash restarts from the claim chain at the next stage
-      hp = h;
-      lenp = len;
-      __syncwarp();
     }
-    if (link_pending) store_link(T.slots + link_slot, link_prev, g.root);
+    if (link_pending) store_link(T.slots + link_slot, link_h, link_prev);
     if (lane < D && static_cast<uint64_t>(lane) < len) act_row[lane] = a;
   }
   if (T.dbg && lane == 0 && warp < 65536) {
@@ -374,15 +436,10 @@ struct Tile {
   }
 };
 
-__device__ __forceinline__ unsigned long long ld_nc_u64(const unsigned long long* p) {
-  unsigned long long v;
-  asm("ld.global.nc.u64 %0, [%1];" : "=l"(v) : "l"(p));
-  return v;
-}
-
-// Resolve a content probe whose first probe window (hb[]) is already loaded.
-__device__ __forceinline__ uint32_t resolve_content(const DevTrie& T, unsigned long long h, int32_t token, uint64_t b,
-                                                    const unsigned long long (&hb)[kWindow], SlotView& rec) {
+// Resolve a content probe (h32, token) whose first probe window (hb[]: the slots' h32) is
+// already loaded. A match on (h32, token) is a candidate; the caller checks its parent.
+__device__ __forceinline__ uint32_t resolve_content(const DevTrie& T, uint32_t h, int32_t token, uint64_t b,
+                                                    const uint32_t (&hb)[kWindow], SlotView& rec) {
   const uint64_t cap = T.cap;
   const uint64_t nb = cap / kBucket;
   bool first = true;
@@ -390,17 +447,32 @@ __device__ __forceinline__ uint32_t resolve_content(const DevTrie& T, unsigned l
 #pragma unroll
     for (int s = 0; s < kWindow; ++s) {
       const uint64_t i = window_slot(b, s, cap);
-      const unsigned long long hs = first ? hb[s] : ld_nc_u64(&T.slots[i].h);
+      const uint32_t hs = first ? hb[s] : hash_word(T.slots + i);
       if (hs == h) {
         rec = load_slot_nc(T.slots + i);  // same sector as the hash: an L1 hit
         if (rec.token == token) return static_cast<uint32_t>(i + 1);
       }
-      if (hs == 0ull) return 0;
+      if (hs == 0u) return 0;
     }
     first = false;
     b += kWindow / kBucket;
     if (b >= nb) b -= nb;
   }
+}
+
+// Implicit path state (a count-1 window below a leaf): bit 63 set, bits 32-62 = continuation
+// tokens still available below it (depth cap, stream end), bits 0-31 = the shist offset of
+// the window's last token. 0 = an entry path (children in the entry's child list).
+__device__ __forceinline__ unsigned long long make_imp(uint64_t abs, uint32_t rem) {
+  return (1ull << 63) | (static_cast<unsigned long long>(rem) << 32) | static_cast<uint32_t>(abs);
+}
+__device__ __forceinline__ uint32_t imp_rem(unsigned long long v) { return static_cast<uint32_t>(v >> 32) & 0x7FFFFFFFu; }
+__device__ __forceinline__ uint32_t imp_abs(unsigned long long v) { return static_cast<uint32_t>(v); }
+// the implicit continuation below leaf r (a window of `depth` tokens)
+__device__ __forceinline__ unsigned long long leaf_imp(const DevTrie& T, const SlotView& r, int depth) {
+  const StreamInfo si = T.sinfo[occ_stream(r.occ_stream)];
+  const uint32_t rem = min(static_cast<uint32_t>(T.depth_cap - depth), si.len - 1u - r.occ_pos);
+  return make_imp(si.base + r.occ_pos, rem);
 }
 
 // B = threads per block. A block retires only when its slowest warp does, so smaller blocks
@@ -464,12 +536,12 @@ __global__ void __launch_bounds__(B, DGDS_QUERY_OCC * (kBlock / B)) k_query(Quer
     return (act && !fast) ? row[x] : v;
   };
   const unsigned long long h0 = root_hash(root);
-  auto hash_prefix = [&](int j, int i) {  // hash of row[j .. j+i)
+  auto hash_prefix = [&](int j, int i) {  // content hash of row[j .. j+i)
     unsigned long long h = h0;
 #pragma unroll
     for (int t = 0; t < 8; ++t)
       if (t < i) h = hash_step(h, tok_at(j + t));
-    return key_hash(h);
+    return hash32(h);
   };
   auto b0 = [&](int j) { return j * start - j * (j - 1) / 2; };  // first window of suffix j
 
@@ -478,6 +550,7 @@ __global__ void __launch_bounds__(B, DGDS_QUERY_OCC * (kBlock / B)) k_query(Quer
   int it_child = 0, it_merge = 0, it_depth = 0;
   int winner = -1;
   uint32_t locus_cnt = 0, locus_fc = 0;
+  unsigned long long locus_imp = 0;  // nonzero: the locus is a count-1 window (implicit path)
   const uint64_t nbk = T.cap / kBucket;
 
   // ---------------- phase A ----------------
@@ -504,18 +577,17 @@ __global__ void __launch_bounds__(B, DGDS_QUERY_OCC * (kBlock / B)) k_query(Quer
         t2 = pr[i - 1];
       }
     }
-    h1 = key_hash(h1);
-    h2 = key_hash(h2);
-    const uint64_t bk1 = home_bucket(h1, nbk), bk2 = home_bucket(h2, nbk);
-    unsigned long long x[kWindow], y[kWindow];
+    const uint32_t k1 = hash32(h1), k2 = hash32(h2);
+    const uint64_t bk1 = home_bucket(k1, nbk), bk2 = home_bucket(k2, nbk);
+    uint32_t x[kWindow], y[kWindow];
 #pragma unroll
     for (int s = 0; s < kWindow; ++s) {
-      x[s] = d1 ? ld_nc_u64(&T.slots[window_slot(bk1, s, T.cap)].h) : 0ull;
-      y[s] = d2 ? ld_nc_u64(&T.slots[window_slot(bk2, s, T.cap)].h) : 0ull;
+      x[s] = d1 ? hash_word(T.slots + window_slot(bk1, s, T.cap)) : 0u;
+      y[s] = d2 ? hash_word(T.slots + window_slot(bk2, s, T.cap)) : 0u;
     }
     if (d1) {
       SlotView r;
-      const uint32_t id = resolve_content(T, h1, t1, bk1, x, r);
+      const uint32_t id = resolve_content(T, k1, t1, bk1, x, r);
       sm.a.wid[i1 - 1] = id;
       sm.a.wpar[i1 - 1] = id ? r.parent : 0u;
       if (i1 == start) {
@@ -525,7 +597,7 @@ __global__ void __launch_bounds__(B, DGDS_QUERY_OCC * (kBlock / B)) k_query(Quer
     }
     if (d2) {
       SlotView r;
-      const uint32_t id = resolve_content(T, h2, t2, bk2, y, r);
+      const uint32_t id = resolve_content(T, k2, t2, bk2, y, r);
       sm.a.wid[i2 - 1] = id;
       sm.a.wpar[i2 - 1] = id ? r.parent : 0u;
       if (i2 == start) {
@@ -535,8 +607,18 @@ __global__ void __launch_bounds__(B, DGDS_QUERY_OCC * (kBlock / B)) k_query(Quer
     }
     __syncwarp();
   }
-  // check the chain of suffix j from the probe records (exact fallback on mismatch)
-  auto check_suffix = [&](int j, int& looks, uint32_t& cnt, uint32_t& fc) -> bool {
+  // The window of L tokens ending in entry `last` (its own record r) is the locus: a node
+  // keeps its child list; a leaf (one occurrence) continues implicitly in its stream.
+  auto locus_of = [&](const SlotView& r, int L, uint32_t& cnt, uint32_t& fc, unsigned long long& imp) {
+    cnt = occurrences(r.count);
+    fc = r.first_child;
+    imp = r.count == 0u ? leaf_imp(T, r, L) : 0ull;
+  };
+  // Suffix j from the probe records (exact fallback on a parent mismatch). Windows past the
+  // deepest entry of the suffix are count-1 windows below a leaf: they exist iff the leaf's
+  // occurrence continues with the suffix's remaining tokens (one lookup per window, as the
+  // reference's walk counts them).
+  auto check_suffix = [&](int j, int& looks, uint32_t& cnt, uint32_t& fc, unsigned long long& imp) -> bool {
     const int L = start - j;
     const int bj = b0(j);
     uint32_t prev = root;
@@ -546,30 +628,39 @@ __global__ void __launch_bounds__(B, DGDS_QUERY_OCC * (kBlock / B)) k_query(Quer
       const int32_t tk = tok_at(j + i - 1);
       h = hash_step(h, tk);
       uint32_t id;
+      SlotView r;
       if (fast && sm.a.wid[bj + i - 1] != 0u && sm.a.wpar[bj + i - 1] == prev) {
         id = sm.a.wid[bj + i - 1];
-        if (i == L) {
-          cnt = sm.a.scnt[j];
-          fc = sm.a.sfc[j];
-        }
       } else if (fast && sm.a.wid[bj + i - 1] == 0u) {
-        id = 0;  // no slot with this content at all: the window is absent
+        id = 0;  // no entry with this content at all
       } else {   // hash collision or long pattern: exact (parent, token) probe
-        SlotView r;
-        id = find_exact(T, key_hash(h), prev, tk, r);
-        if (id && i == L) {
-          cnt = occurrences(r.count);
-          fc = r.first_child;
-        }
+        id = find_exact(T, hash32(h), prev, tk, r);
       }
-      if (id == 0u) return false;
+      if (id == 0u) {
+        if (i == 1) return false;
+        const SlotView lr = load_slot_nc(T.slots + (prev - 1));
+        if (lr.count != 0u) return false;  // a node: every child of a node is an entry
+        const StreamInfo si = T.sinfo[occ_stream(lr.occ_stream)];
+        uint32_t e = lr.occ_pos;
+        for (int m = i; m <= L; ++m) {
+          if (m > i) ++looks;
+          ++e;
+          if (e >= si.len || T.shist[si.base + e] != tok_at(j + m - 1)) return false;
+        }
+        cnt = 1;
+        fc = 0;
+        imp = make_imp(si.base + e, min(static_cast<uint32_t>(T.depth_cap - L), si.len - 1u - e));
+        return true;
+      }
       prev = id;
     }
+    locus_of(load_slot_nc(T.slots + (prev - 1)), L, cnt, fc, imp);
     return true;
   };
   {
     int looks = 0;
     uint32_t cnt = 0, fc = 0;
+    unsigned long long imp = 0;
     bool ok = false;
     if (act && gl == 0) {
       // fast check of the longest suffix from the probe records
@@ -580,27 +671,35 @@ __global__ void __launch_bounds__(B, DGDS_QUERY_OCC * (kBlock / B)) k_query(Quer
         if (fast && i <= start && !dead && !slow) {
           ++looks;
           const uint32_t id = sm.a.wid[i - 1];
-          if (id == 0u) dead = true;
-          else if (sm.a.wpar[i - 1] != prev) slow = true;  // hash collision: exact walk below
-          else prev = id;
+          if (id == 0u) {
+            if (i == 1) dead = true;
+            else slow = true;  // maybe the implicit continuation of a leaf: checked below
+          } else if (sm.a.wpar[i - 1] != prev) {
+            slow = true;  // hash collision: exact walk below
+          } else {
+            prev = id;
+          }
         }
       }
       if (fast && !slow) {
         ok = !dead;
         cnt = sm.a.scnt[0];
         fc = sm.a.sfc[0];
+        if (ok && cnt == 1u) locus_of(load_slot_nc(T.slots + (prev - 1)), start, cnt, fc, imp);
       } else {
         looks = 0;
-        ok = check_suffix(0, looks, cnt, fc);
+        ok = check_suffix(0, looks, cnt, fc, imp);
       }
     }
     st_lookups = tile.shfl(looks, 0);
     const bool ok0 = tile.shfl(static_cast<int>(ok), 0) != 0;
     const uint32_t c0 = tile.shfl(cnt, 0), f0 = tile.shfl(fc, 0);
+    const unsigned long long i0 = tile.shfl(imp, 0);
     if (ok0) {
       winner = 0;
       locus_cnt = c0;
       locus_fc = f0;
+      locus_imp = i0;
     }
   }
   // (2) only when the longest suffix is absent: the shorter ones, in order
@@ -622,11 +721,11 @@ __global__ void __launch_bounds__(B, DGDS_QUERY_OCC * (kBlock / B)) k_query(Quer
         uint32_t id = 0;
         SlotView r;
         if (dw) {
-          const unsigned long long h = hash_prefix(j, i);
-          unsigned long long hb[kWindow];
+          const uint32_t h = hash_prefix(j, i);
+          uint32_t hb[kWindow];
           const uint64_t bk = home_bucket(h, nbk);
 #pragma unroll
-          for (int s = 0; s < kWindow; ++s) hb[s] = ld_nc_u64(&T.slots[window_slot(bk, s, T.cap)].h);
+          for (int s = 0; s < kWindow; ++s) hb[s] = hash_word(T.slots + window_slot(bk, s, T.cap));
           id = resolve_content(T, h, tok_at(j + i - 1), bk, hb, r);
           sm.a.wid[w] = id;
           sm.a.wpar[w] = id ? r.parent : 0u;
@@ -645,19 +744,22 @@ __global__ void __launch_bounds__(B, DGDS_QUERY_OCC * (kBlock / B)) k_query(Quer
       const int j = 1 + u * G + gl;
       int looks = 0;
       uint32_t cnt = 0, fc = 0;
-      const bool ok = !done && j < nlen && check_suffix(j, looks, cnt, fc);
+      unsigned long long imp = 0;
+      const bool ok = !done && j < nlen && check_suffix(j, looks, cnt, fc, imp);
       const unsigned m = tile.ballot(ok);
       const int w = m ? __ffs(m) - 1 : G - 1;
       // collectives at one call site for every lane (tiles that are done add 0)
       const int add = tile.sum((!done && gl <= w) ? looks : 0);
       const uint32_t wc = tile.shfl(cnt, w);
       const uint32_t wf = tile.shfl(fc, w);
+      const unsigned long long wi = tile.shfl(imp, w);
       if (!done) {
         st_lookups += add;
         if (m) {
           winner = 1 + u * G + w;
           locus_cnt = wc;
           locus_fc = wf;
+          locus_imp = wi;
           done = true;
         }
       }
@@ -673,6 +775,8 @@ __global__ void __launch_bounds__(B, DGDS_QUERY_OCC * (kBlock / B)) k_query(Quer
   for (int i = 0; i < S; ++i) tok[i] = 0;
   int nb = winner >= 0 ? 1 : 0;
   uint32_t b_fc = locus_fc;
+  unsigned long long b_imp = locus_imp;  // nonzero: an implicit path (one continuation token in shist)
+  const int locus_len = start - winner;  // depth of the locus (tile-uniform when nb > 0)
   double b_score = 1.0;
   long long b_sup = static_cast<long long>(locus_cnt);
   int b_lex = 0;
@@ -733,16 +837,32 @@ __global__ void __launch_bounds__(B, DGDS_QUERY_OCC * (kBlock / B)) k_query(Quer
     int p_lex = 0, p_src = 0;
     int32_t p_tok = 0;
     uint32_t p_fc = 0;
+    unsigned long long p_imp = 0;
     int np = 0;
-    uint32_t c = (live && gl < nb) ? b_fc : 0u;
+    // an entry path enumerates its child list; an implicit path has at most one child, the
+    // next token of its occurrence (count 1)
+    uint32_t c = (live && gl < nb && b_imp == 0ull) ? b_fc : 0u;
+    bool impc = live && gl < nb && b_imp != 0ull && imp_rem(b_imp) > 0u;
+    const int child_depth = locus_len + d + 1;
     bool grew = false;
     int nchild = 0;
     ++it_depth;
-    while (__any_sync(kFull, c != 0u)) {
+    while (__any_sync(kFull, c != 0u || impc)) {
       ++it_child;
       SlotView r{};
-      const bool have = c != 0u;
-      if (have) r = load_slot_nc(T.slots + (c - 1));
+      const bool have = c != 0u || impc;
+      unsigned long long cimp = 0;
+      if (c != 0u) {
+        r = load_slot_nc(T.slots + (c - 1));
+        if (r.count == 0u) cimp = leaf_imp(T, r, child_depth);  // a leaf: implicit below it
+      } else if (impc) {
+        const uint32_t at = imp_abs(b_imp) + 1u;
+        r.token = T.shist[at];
+        r.count = 0u;
+        r.first_child = 0u;
+        r.next_sibling = 0u;
+        cimp = make_imp(at, imp_rem(b_imp) - 1u);
+      }
       bool qual = false;
       double sc = 0.0;
       const long long cnt = have ? static_cast<long long>(occurrences(r.count)) : 0ll;
@@ -767,6 +887,7 @@ __global__ void __launch_bounds__(B, DGDS_QUERY_OCC * (kBlock / B)) k_query(Quer
         const int cl = tile.shfl(b_lex, b);
         const int32_t ct = tile.shfl(r.token, b);
         const uint32_t cfc = tile.shfl(r.first_child, b);
+        const unsigned long long cim = tile.shfl(cimp, b);
         const bool before = has && gl < np &&
                             (p_score != cs ? p_score > cs
                              : p_sup != cp ? p_sup > cp
@@ -780,6 +901,7 @@ __global__ void __launch_bounds__(B, DGDS_QUERY_OCC * (kBlock / B)) k_query(Quer
         const int usrc = tile.shfl_up(p_src, 1);
         const int32_t ut = tile.shfl_up(p_tok, 1);
         const uint32_t ufc = tile.shfl_up(p_fc, 1);
+        const unsigned long long uim = tile.shfl_up(p_imp, 1);
         if (ins && gl > pos && gl <= np) {
           p_score = us;
           p_sup = up;
@@ -787,6 +909,7 @@ __global__ void __launch_bounds__(B, DGDS_QUERY_OCC * (kBlock / B)) k_query(Quer
           p_src = usrc;
           p_tok = ut;
           p_fc = ufc;
+          p_imp = uim;
         }
         if (ins && gl == pos) {
           p_score = cs;
@@ -795,10 +918,12 @@ __global__ void __launch_bounds__(B, DGDS_QUERY_OCC * (kBlock / B)) k_query(Quer
           p_src = b;
           p_tok = ct;
           p_fc = cfc;
+          p_imp = cim;
         }
         if (ins) np = min(np + 1, kq);
       }
-      c = have ? r.next_sibling : 0u;
+      c = c != 0u ? r.next_sibling : 0u;
+      impc = false;
     }
     if (live) {
       st_exp += nb;
@@ -828,6 +953,7 @@ __global__ void __launch_bounds__(B, DGDS_QUERY_OCC * (kBlock / B)) k_query(Quer
       for (int i = 0; i < S; ++i) tok[i] = nt[i];
       set_tok<S>(tok, d, p_tok);
       b_fc = p_fc;
+      b_imp = p_imp;
       b_score = p_score;
       b_sup = p_sup;
       b_lex = lex;
@@ -1051,24 +1177,19 @@ __global__ void k_rebuild_place(DevTrie from, DevTrie to, const uint32_t* __rest
   for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < from.cap; i += stride) {
     const Slot s = from.slots[i];
     remap[i] = 0;
-    if (s.h == 0ull) continue;
-    const uint32_t ridx = kRootTop - s.root;
+    if (s.parent == 0u) continue;
+    const uint32_t ridx = kRootTop - from.sinfo[occ_stream(s.occ_stream)].root;  // the entry's group
     if (!((root_alive[ridx >> 5] >> (ridx & 31)) & 1u)) continue;
     const uint64_t nbk = to.cap / kBucket;
-    uint64_t bk = home_bucket(s.h, nbk);
-    uint64_t j = 0;
-    for (bool done = false; !done;) {
-      for (int q = 0; q < kBucket && !done; ++q) {
-        j = bk * kBucket + q;
-        done = atomicCAS(&to.slots[j].h, 0ull, s.h) == 0ull;
-      }
-      if (!done) bk = (bk + 1 == nbk) ? 0 : bk + 1;
-    }
+    const unsigned long long key = pack_key(s.parent, s.token);  // keys are unique: any empty slot will do
+    uint64_t j = home_bucket(s.h32, nbk) * kBucket;
+    while (atomicCAS(reinterpret_cast<unsigned long long*>(to.slots + j), 0ull, key) != 0ull)
+      if (++j == to.cap) j = 0;
     Slot* d = to.slots + j;
-    d->parent = s.parent;  // old id until pass 2
-    d->token = s.token;
+    d->occ_stream = s.occ_stream;  // parent: old id until pass 2
+    d->occ_pos = s.occ_pos;
     d->count = s.count;
-    d->root = s.root;
+    d->h32 = s.h32;
     remap[i] = static_cast<uint32_t>(j + 1);
     atomicAdd(to.used + ((i & (kUsedParts - 1)) * 8), 1ull);
   }
@@ -1078,25 +1199,42 @@ __global__ void k_rebuild_link(DevTrie to, const uint32_t* __restrict__ remap) {
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
   for (uint64_t j = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < to.cap; j += stride) {
     Slot* d = to.slots + j;
-    if (d->h == 0ull) continue;
     const uint32_t op = d->parent;
-    if (op == d->root) continue;  // depth 1: parent is the group root
+    if (op == 0u || op >= kMinRootId) continue;  // empty, or depth 1 (parent = group root)
     const uint32_t np = remap[op - 1];
     d->parent = np;
     d->next_sibling = atomicExch(&to.slots[np - 1].first_child, static_cast<uint32_t>(j + 1));
   }
 }
 
-__global__ void k_remap_active(uint32_t* active, const uint32_t* __restrict__ streams,
-                               const uint32_t* __restrict__ sizes, int64_t ns, const uint32_t* __restrict__ remap) {
+// active / ov rows through the old -> new id map (ids of dropped groups map to 0)
+__global__ void k_remap_active(uint32_t* active, uint32_t* ov, const uint32_t* __restrict__ streams, int64_t ns,
+                               const uint32_t* __restrict__ remap, uint64_t from_cap) {
   const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int64_t s = t / kWarp;
   const int l = static_cast<int>(t % kWarp);
   if (s >= ns) return;
-  if (static_cast<uint32_t>(l) >= sizes[s]) return;
-  uint32_t* row = active + static_cast<uint64_t>(streams[s]) * kWarp;
-  const uint32_t v = row[l];
-  row[l] = v ? remap[v - 1] : 0u;
+  const uint64_t at = static_cast<uint64_t>(streams[s]) * kWarp + l;
+  const uint32_t v = active[at], o = ov[at];
+  active[at] = (v && v <= from_cap) ? remap[v - 1] : 0u;
+  ov[at] = (o && o <= from_cap) ? remap[o - 1] : 0u;
+}
+
+// logical trie nodes: every entry, plus the count-1 chain below each leaf
+__global__ void k_node_count(DevTrie T, unsigned long long* out) {
+  unsigned long long n = 0;
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < T.cap; i += stride) {
+    const Slot s = T.slots[i];
+    if (s.parent == 0u) continue;
+    n += 1;
+    if (s.count == 0u) {
+      const StreamInfo si = T.sinfo[occ_stream(s.occ_stream)];
+      n += min(static_cast<uint32_t>(T.depth_cap) - occ_depth(s.occ_stream), si.len - 1u - s.occ_pos);
+    }
+  }
+  n = __reduce_add_sync(kFull, static_cast<unsigned>(n));  // < 2^32 per warp
+  if (lane_id() == 0 && n) atomicAdd(out, n);
 }
 
 // ---------------------------------------------------------------------------
@@ -1244,6 +1382,24 @@ int append_block() {
   return b == 128 ? kBlock : b;
 }
 
+// DGDS_DEBUG_SYNC=1: wait for each append kernel with a deadline and name the one that does not
+// finish (debug builds of a new kernel; off by default).
+void debug_sync(cudaStream_t st, const char* what) {
+  static const bool on = std::getenv("DGDS_DEBUG_SYNC") != nullptr;
+  if (!on) return;
+  for (int i = 0; i < 5000; ++i) {
+    const cudaError_t e = cudaStreamQuery(st);
+    if (e == cudaSuccess) return;
+    if (e != cudaErrorNotReady) {
+      std::fprintf(stderr, "[dgds debug] %s failed: %s\n", what, cudaGetErrorString(e));
+      std::abort();
+    }
+    usleep(1000);
+  }
+  std::fprintf(stderr, "[dgds debug] %s did not finish within 5 s\n", what);
+  std::abort();
+}
+
 template <int G, int S>
 cudaError_t launch_query_gs(const QueryLaunch& L, cudaStream_t st) {
   const int blk = query_block();
@@ -1263,14 +1419,28 @@ cudaError_t launch_query_g(const QueryLaunch& L, int32_t max_s, cudaStream_t st)
 }  // namespace
 
 cudaError_t launch_append(const DevTrie& T, const AppendSeg* d_segs, int64_t nseg, const AppendPiece* d_pieces,
-                          const int32_t* d_tokens, cudaStream_t st) {
+                          int64_t npieces, const int32_t* d_tokens, const CopyPiece* d_grow, int64_t ngrow,
+                          cudaStream_t st) {
   if (nseg <= 0) return cudaSuccess;
+  if (ngrow > 0) {  // moved extents: the stored tokens into the new, larger extent
+    cudaError_t e = launch_copy_pieces(d_grow, ngrow, T.shist, T.shist, st);
+    if (e != cudaSuccess) return e;
+  }
+  {
+    const int64_t work = std::max<int64_t>(nseg, npieces * kWarp);
+    const int64_t blocks = std::min<int64_t>((work + 255) / 256, 148 * 8);
+    k_stage<<<static_cast<unsigned>(blocks), 256, 0, st>>>(T, d_segs, nseg, d_pieces, npieces, d_tokens);
+  }
+  debug_sync(st, "k_stage");
   const int blk = append_block();
   const int64_t wpb = blk / kWarp;
   const int64_t blocks = (nseg + wpb - 1) / wpb;
-  if (blk == 32) k_append<32><<<static_cast<unsigned>(blocks), 32, 0, st>>>(T, d_segs, nseg, d_pieces, d_tokens);
-  else if (blk == 64) k_append<64><<<static_cast<unsigned>(blocks), 64, 0, st>>>(T, d_segs, nseg, d_pieces, d_tokens);
-  else k_append<kBlock><<<static_cast<unsigned>(blocks), kBlock, 0, st>>>(T, d_segs, nseg, d_pieces, d_tokens);
+  if (blk == 32) k_append<32><<<static_cast<unsigned>(blocks), 32, 0, st>>>(T, d_segs, nseg);
+  else if (blk == 64) k_append<64><<<static_cast<unsigned>(blocks), 64, 0, st>>>(T, d_segs, nseg);
+  else k_append<kBlock><<<static_cast<unsigned>(blocks), kBlock, 0, st>>>(T, d_segs, nseg);
+  debug_sync(st, "k_append");
+  k_walks<<<148 * 2, 128, 0, st>>>(T);
+  debug_sync(st, "k_walks");
   return cudaGetLastError();
 }
 
@@ -1334,12 +1504,17 @@ cudaError_t launch_rebuild(const DevTrie& from, const DevTrie& to, const uint32_
   return cudaGetLastError();
 }
 
-cudaError_t launch_remap_active(uint32_t* active, const uint32_t* streams, const uint32_t* sizes, int64_t nstreams,
-                                const uint32_t* remap, cudaStream_t st) {
+cudaError_t launch_remap_active(const DevTrie& T, const uint32_t* streams, int64_t nstreams, const uint32_t* remap,
+                                cudaStream_t st, uint64_t from_cap) {
   if (nstreams <= 0) return cudaSuccess;
   const int64_t threads = nstreams * kWarp;
-  k_remap_active<<<static_cast<unsigned>((threads + 255) / 256), 256, 0, st>>>(active, streams, sizes, nstreams,
-                                                                                 remap);
+  k_remap_active<<<static_cast<unsigned>((threads + 255) / 256), 256, 0, st>>>(T.active, T.ov, streams, nstreams,
+                                                                                 remap, from_cap);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_node_count(const DevTrie& T, unsigned long long* out, cudaStream_t st) {
+  k_node_count<<<148 * 8, 256, 0, st>>>(T, out);
   return cudaGetLastError();
 }
 

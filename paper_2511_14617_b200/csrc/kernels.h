@@ -12,23 +12,26 @@
 namespace dgds {
 
 // One warp per segment: all records of one request stream inside one batch, in
-// call order, as `npieces` token runs starting at stream position `start`.
+// call order: n tokens at stream positions start .. start + n, read from the
+// stream's history extent (staged there by k_stage).
 struct AppendSeg {
-  uint32_t stream;  // stream slot (row of DevTrie::active)
-  uint32_t root;    // group root id
-  uint64_t start;   // tokens stored for the stream before this batch
-  uint32_t piece0;
-  uint32_t npieces;
-  uint64_t pad_;
+  uint32_t stream;    // stream slot (row of DevTrie::active)
+  uint32_t root;      // group root id
+  uint64_t start;     // tokens stored for the stream before this batch
+  uint64_t sh_base;   // the stream's extent in DevTrie::shist (after any growth)
+  uint32_t n;         // tokens appended in this batch
+  uint32_t pad_;
 };
 static_assert(sizeof(AppendSeg) == 32, "AppendSeg is 32 B");
 
-struct AppendPiece {
+struct AppendPiece {  // one record's tokens: batch buffer -> history arena + stream extent
   uint64_t tok_off;   // into the batch token buffer
-  uint64_t hist_off;  // where K1 copies the tokens in the history arena (DevTrie::hist)
+  uint64_t hist_off;  // history arena (record order, replica blobs)
+  uint64_t sh_off;    // stream extent position (DevTrie::shist)
   uint32_t n;
   uint32_t pad_;
 };
+static_assert(sizeof(AppendPiece) == 32, "AppendPiece is 32 B");
 
 // One piece of a GDX1 blob (cst.cpp:233-269), serialised big-endian on the device:
 // an optional header right before `dst` — kind 1: delta record {u32 rid, u64 start, u32 len}
@@ -51,8 +54,11 @@ cudaError_t launch_copy_pieces(const CopyPiece* d_pieces, int64_t n, const int32
 cudaError_t launch_blob_fill(const BlobPiece* d_pieces, int64_t n, const int32_t* hist, uint8_t* out,
                              cudaStream_t st);
 
+// k_stage (tokens -> history arena + stream extents, stream table rows) then K1. Extent growth
+// copies (grow, ngrow: old extent -> new extent, within shist) run first.
 cudaError_t launch_append(const DevTrie& T, const AppendSeg* d_segs, int64_t nseg, const AppendPiece* d_pieces,
-                          const int32_t* d_tokens, cudaStream_t st);
+                          int64_t npieces, const int32_t* d_tokens, const CopyPiece* d_grow, int64_t ngrow,
+                          cudaStream_t st);
 
 int set_error(int code, const std::string& msg);  // dgds_last_error() message (server.cpp)
 
@@ -141,8 +147,12 @@ cudaError_t launch_set_u32(uint32_t* dst, uint32_t value, cudaStream_t st);
 // root indices.
 cudaError_t launch_rebuild(const DevTrie& from, const DevTrie& to, const uint32_t* root_alive, uint32_t* remap,
                            cudaStream_t st);
-cudaError_t launch_remap_active(uint32_t* active, const uint32_t* streams, const uint32_t* sizes, int64_t nstreams,
-                                const uint32_t* remap, cudaStream_t st);
+// active / ov rows of the given streams through the old->new id map
+cudaError_t launch_remap_active(const DevTrie& T, const uint32_t* streams, int64_t nstreams, const uint32_t* remap,
+                                cudaStream_t st, uint64_t from_cap);
+// Logical trie nodes of the arena (the reference's node count without roots): entries plus the
+// implicit chain below every leaf. out[0] += total (one u64).
+cudaError_t launch_node_count(const DevTrie& T, unsigned long long* out, cudaStream_t st);
 
 // Dense per-candidate record of the host path's compacted results.
 struct CandMeta {

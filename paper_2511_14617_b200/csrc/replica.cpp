@@ -85,10 +85,54 @@ int compact_history(dgds_server* s) {
   return DGDS_OK;
 }
 
+// Pack the live streams' token extents (moved and retired extents are dropped) and rewrite
+// the device stream table. Runs after the rebuild, so no entry names a retired stream.
+int compact_streams(dgds_server* s) {
+  std::vector<dgds::CopyPiece> pcs;
+  std::vector<dgds::StreamInfo> rows(s->stream_cap, dgds::StreamInfo{0, 0, 0});
+  uint64_t live = 0;
+  for (auto& g : s->groups) {
+    if (!g.alive) continue;
+    g.streams.for_each([&](int32_t, StreamRec& r) {
+      const uint64_t nc = r.stored ? (std::max<uint64_t>(64, r.stored + r.stored / 4) + 7) / 8 * 8 : 0;
+      if (r.stored) pcs.push_back(dgds::CopyPiece{r.sh_base, live, static_cast<uint32_t>(r.stored), 0});
+      r.sh_base = live;
+      r.sh_cap = nc;
+      rows[r.slot] = dgds::StreamInfo{live, static_cast<uint32_t>(r.stored), g.root};
+      live += nc;
+    });
+  }
+  const uint64_t cap = std::max<uint64_t>(1ull << 20, live + live / 2);
+  if (cap >= (1ull << 32)) return fail(DGDS_ENOMEM, "stream-history arena exceeds 2^32 tokens");
+  int32_t* nb = nullptr;
+  if (cudaMalloc(&nb, cap * sizeof(int32_t)) != cudaSuccess) return fail(DGDS_ENOMEM, "stream-history allocation failed");
+  if (!pcs.empty()) {
+    if (int rc = s->d_blob_pieces.ensure(pcs.size() * sizeof(dgds::CopyPiece))) return rc;
+    DGDS_CUDA(cudaMemcpyAsync(s->d_blob_pieces.p, pcs.data(), pcs.size() * sizeof(dgds::CopyPiece),
+                              cudaMemcpyHostToDevice, s->st));
+    DGDS_CUDA(dgds::launch_copy_pieces(static_cast<const dgds::CopyPiece*>(s->d_blob_pieces.p),
+                                       static_cast<int64_t>(pcs.size()), s->d_shist, nb, s->st));
+  }
+  DGDS_CUDA(cudaMemcpyAsync(s->T.sinfo, rows.data(), rows.size() * sizeof(dgds::StreamInfo), cudaMemcpyHostToDevice,
+                            s->st));
+  DGDS_CUDA(cudaStreamSynchronize(s->st));
+  cudaFree(s->d_shist);
+  s->d_shist = nb;
+  s->T.shist = nb;
+  s->shist_cap = cap;
+  s->shist_used = live;
+  s->dead_shist_tokens = 0;
+  return DGDS_OK;
+}
+
 int compact_memory(dgds_server* s) {
+  // planned-but-unlaunched device updates hold arena offsets and have not written their tokens
+  if (s->plans_made != s->plans_launched) return fail(DGDS_ESTATE, "memory compaction with update plans outstanding");
+  materialize_logs(s);
   DGDS_CUDA(cudaStreamSynchronize(s->st));
   if (int rc = rebuild(s, s->T.cap)) return rc;
   if (int rc = compact_history(s)) return rc;
+  if (int rc = compact_streams(s)) return rc;
   s->compactions += 1;
   return DGDS_OK;
 }
@@ -110,6 +154,8 @@ int dgds_fetch_cst(dgds_server* s, int64_t n, const int32_t* handles, const uint
   if (!s || n < 0 || (n > 0 && (!handles || !cached || !rep || !blobs))) return fail(DGDS_EINVAL, "null argument");
   std::lock_guard<std::mutex> lk(s->mu);
   if (int rc_ = flush_pending(s)) return rc_;
+  // a planned-but-unlaunched device update has bumped versions but not yet written its tokens
+  if (s->plans_made != s->plans_launched) return fail(DGDS_ESTATE, "fetch_cst with update plans outstanding");
   materialize_logs(s);  // pending plans' history-log records first
   DGDS_CUDA(cudaSetDevice(s->p.device));
   for (int64_t i = 0; i < n; ++i)
@@ -272,7 +318,7 @@ int dgds_apply_blob(dgds_server* s, int32_t h, const uint8_t* blob, uint64_t len
         const StreamRec* sr = g.streams.find(rid);
         it = stored.emplace(rid, sr ? sr->stored : 0).first;
       }
-      if (n > 0 && start != it->second) {  // append() would reply ok=false
+      if (start != it->second) {  // append() would reply ok=false (checked before its empty-token return)
         toks.resize(offs.back());
         bad = true;
         break;

@@ -38,6 +38,37 @@ int set_root(dgds_server* s, int32_t handle, uint32_t root) {
   return DGDS_OK;
 }
 
+// Stream tables (active, ov: [stream][32] entry ids; sinfo: extent + length + root), zeroed
+// beyond the old capacity: ids of never-written lanes read as 0 (remapped safely by a rebuild).
+int grow_streams(dgds_server* s, uint64_t nc) {
+  if (nc > static_cast<uint64_t>(dgds::kStreamMask) + 1) return fail(DGDS_EUNSUPPORTED, "request streams exhausted (2^24)");
+  uint32_t *na = nullptr, *no = nullptr;
+  dgds::StreamInfo* ni = nullptr;
+  DGDS_CUDA(cudaMalloc(&na, nc * dgds::kWarp * sizeof(uint32_t)));
+  DGDS_CUDA(cudaMalloc(&no, nc * dgds::kWarp * sizeof(uint32_t)));
+  DGDS_CUDA(cudaMalloc(&ni, nc * sizeof(dgds::StreamInfo)));
+  DGDS_CUDA(cudaMemsetAsync(na, 0, nc * dgds::kWarp * sizeof(uint32_t), s->st));
+  DGDS_CUDA(cudaMemsetAsync(no, 0, nc * dgds::kWarp * sizeof(uint32_t), s->st));
+  DGDS_CUDA(cudaMemsetAsync(ni, 0, nc * sizeof(dgds::StreamInfo), s->st));
+  if (s->T.active) {
+    DGDS_CUDA(cudaMemcpyAsync(na, s->T.active, s->stream_cap * dgds::kWarp * sizeof(uint32_t),
+                              cudaMemcpyDeviceToDevice, s->st));
+    DGDS_CUDA(cudaMemcpyAsync(no, s->T.ov, s->stream_cap * dgds::kWarp * sizeof(uint32_t), cudaMemcpyDeviceToDevice,
+                              s->st));
+    DGDS_CUDA(cudaMemcpyAsync(ni, s->T.sinfo, s->stream_cap * sizeof(dgds::StreamInfo), cudaMemcpyDeviceToDevice,
+                              s->st));
+    DGDS_CUDA(cudaStreamSynchronize(s->st));
+    cudaFree(s->T.active);
+    cudaFree(s->T.ov);
+    cudaFree(s->T.sinfo);
+  }
+  s->T.active = na;
+  s->T.ov = no;
+  s->T.sinfo = ni;
+  s->stream_cap = nc;
+  return DGDS_OK;
+}
+
 int alloc_stream_slot(dgds_server* s, uint32_t* out) {
   if (!s->free_streams.empty()) {
     *out = s->free_streams.back();
@@ -45,24 +76,8 @@ int alloc_stream_slot(dgds_server* s, uint32_t* out) {
     return DGDS_OK;
   }
   if (s->next_stream >= s->stream_cap) {
-    if (int rc = flush_pending(s)) return rc;  // T.active / T.tail change under a staged batch's launch
-    uint64_t nc = std::max<uint64_t>(1024, s->stream_cap * 2);
-    uint32_t* na = nullptr;
-    int32_t* nt = nullptr;
-    DGDS_CUDA(cudaMalloc(&na, nc * dgds::kWarp * sizeof(uint32_t)));
-    DGDS_CUDA(cudaMalloc(&nt, nc * dgds::kWarp * sizeof(int32_t)));
-    if (s->T.active) {
-      DGDS_CUDA(cudaMemcpyAsync(na, s->T.active, s->stream_cap * dgds::kWarp * sizeof(uint32_t),
-                                cudaMemcpyDeviceToDevice, s->st));
-      DGDS_CUDA(cudaMemcpyAsync(nt, s->T.tail, s->stream_cap * dgds::kWarp * sizeof(int32_t),
-                                cudaMemcpyDeviceToDevice, s->st));
-      DGDS_CUDA(cudaStreamSynchronize(s->st));
-      cudaFree(s->T.active);
-      cudaFree(s->T.tail);
-    }
-    s->T.active = na;
-    s->T.tail = nt;
-    s->stream_cap = nc;
+    if (int rc = flush_pending(s)) return rc;  // the stream tables change under a staged batch's launch
+    if (int rc = grow_streams(s, std::max<uint64_t>(1024, s->stream_cap * 2))) return rc;
   }
   *out = s->next_stream++;
   return DGDS_OK;
@@ -72,7 +87,10 @@ void retire_group(dgds_server* s, GroupRec& g) {
   if (!g.alive) return;
   materialize_logs(s);
   for (const LogRec& e : g.log) s->dead_hist_tokens += e.len;
-  g.streams.for_each([&](int32_t, StreamRec& r) { s->free_streams.push_back(r.slot); });
+  g.streams.for_each([&](int32_t, StreamRec& r) {
+    s->retired_streams.push_back(r.slot);
+    s->dead_shist_tokens += r.sh_cap;
+  });
   g.streams.clear();
   g.log.clear();
   g.log.shrink_to_fit();
@@ -155,45 +173,56 @@ int rebuild(dgds_server* s, uint64_t new_cap) {
   DGDS_CUDA(cudaMemsetAsync(d_used_new, 0, dgds::kUsedParts * 8 * sizeof(unsigned long long), s->st));
   to.used = d_used_new;
   std::vector<uint32_t> alive((kRootCap + 31) / 32, 0);
-  std::vector<uint32_t> live_slots, live_sizes;
+  std::vector<uint32_t> rows;  // stream rows to remap: live streams, and retired ones (-> 0)
   for (auto& g : s->groups) {
     if (!g.alive) continue;
     const uint32_t r = dgds::kRootTop - g.root;
     alive[r >> 5] |= 1u << (r & 31);
-    g.streams.for_each([&](int32_t, StreamRec& r) {
-      live_slots.push_back(r.slot);
-      live_sizes.push_back(static_cast<uint32_t>(std::min<uint64_t>(r.stored, s->D)));
-    });
+    g.streams.for_each([&](int32_t, StreamRec& r) { rows.push_back(r.slot); });
   }
-  uint32_t *d_alive = nullptr, *d_remap = nullptr, *d_ls = nullptr;
+  rows.insert(rows.end(), s->retired_streams.begin(), s->retired_streams.end());
+  uint32_t *d_alive = nullptr, *d_remap = nullptr, *d_rows = nullptr;
   DGDS_CUDA(cudaMalloc(&d_alive, alive.size() * 4));
   DGDS_CUDA(cudaMalloc(&d_remap, s->T.cap * 4));
-  DGDS_CUDA(cudaMalloc(&d_ls, std::max<size_t>(1, live_slots.size()) * 8));
+  DGDS_CUDA(cudaMalloc(&d_rows, std::max<size_t>(1, rows.size()) * 4));
   DGDS_CUDA(cudaMemcpyAsync(d_alive, alive.data(), alive.size() * 4, cudaMemcpyHostToDevice, s->st));
   DGDS_CUDA(cudaMemsetAsync(d_remap, 0, s->T.cap * 4, s->st));
-  if (!live_slots.empty()) {
-    DGDS_CUDA(cudaMemcpyAsync(d_ls, live_slots.data(), live_slots.size() * 4, cudaMemcpyHostToDevice, s->st));
-    DGDS_CUDA(cudaMemcpyAsync(d_ls + live_slots.size(), live_sizes.data(), live_sizes.size() * 4,
-                              cudaMemcpyHostToDevice, s->st));
-  }
+  if (!rows.empty())
+    DGDS_CUDA(cudaMemcpyAsync(d_rows, rows.data(), rows.size() * 4, cudaMemcpyHostToDevice, s->st));
   DGDS_CUDA(dgds::launch_rebuild(s->T, to, d_alive, d_remap, s->st));
-  DGDS_CUDA(dgds::launch_remap_active(s->T.active, d_ls, d_ls + live_slots.size(),
-                                      static_cast<int64_t>(live_slots.size()), d_remap, s->st));
+  DGDS_CUDA(dgds::launch_remap_active(s->T, d_rows, static_cast<int64_t>(rows.size()), d_remap, s->st, s->T.cap));
   DGDS_CUDA(cudaStreamSynchronize(s->st));  // host vectors above must outlive the copies
   cudaFree(d_alive);
   cudaFree(d_remap);
-  cudaFree(d_ls);
+  cudaFree(d_rows);
   cudaFree(s->T.slots);
   cudaFree(s->d_used);
   s->T.slots = to.slots;
   s->T.cap = new_cap;
   s->T.used = d_used_new;
   s->d_used = d_used_new;
+  // retired streams' entries are gone: their slots may now serve new streams
+  s->free_streams.insert(s->free_streams.end(), s->retired_streams.begin(), s->retired_streams.end());
+  s->retired_streams.clear();
   return read_used(s, &s->used_ub);
+}
+
+// K1's conversion-event queue holds at most one event per window occurrence of the batch.
+int ensure_events(dgds_server* s, uint64_t worst_new) {
+  if (worst_new <= s->ev_cap) return DGDS_OK;
+  const uint64_t nc = std::max<uint64_t>(worst_new, s->ev_cap * 2);
+  dgds::WalkEvent* nb = nullptr;
+  DGDS_CUDA(cudaStreamSynchronize(s->st));  // a launch in flight may still use the old queue
+  if (cudaMalloc(&nb, nc * sizeof(dgds::WalkEvent)) != cudaSuccess) return fail(DGDS_ENOMEM, "event queue allocation failed");
+  cudaFree(s->T.ev);
+  s->T.ev = nb;
+  s->ev_cap = nc;
+  return DGDS_OK;
 }
 
 int ensure_capacity(dgds_server* s, uint64_t worst_new) {
   if (int rc = flush_pending(s)) return rc;  // a submitted query reads the table as it was
+  if (int rc = ensure_events(s, worst_new)) return rc;
   const double limit = kMaxLoad * static_cast<double>(s->T.cap);
   if (static_cast<double>(s->used_ub + worst_new) <= limit) return DGDS_OK;
   int rc = read_used(s, &s->used_ub);
@@ -221,6 +250,7 @@ struct PendingPiece {
   int64_t seg;
   uint64_t tok_off;
   uint64_t hist_off;
+  uint64_t pos;  // stream position of the record's first token
   uint32_t n;
 };
 
@@ -242,14 +272,34 @@ int ensure_hist(dgds_server* s) {
   return DGDS_OK;
 }
 
+// Grow the stream-history arena to hold shist_used tokens. Offsets are kept (the old arena is
+// copied whole), so extents planned but not yet staged stay valid.
+int ensure_shist(dgds_server* s) {
+  if (s->shist_used <= s->shist_cap) return DGDS_OK;
+  if (s->shist_used >= (1ull << 32)) return fail(DGDS_ENOMEM, "stream-history arena exceeds 2^32 tokens");
+  if (int rc = flush_pending(s)) return rc;  // T.shist changes under a staged batch's launch
+  const uint64_t nc = std::min<uint64_t>(std::max<uint64_t>(s->shist_used, s->shist_cap * 2), (1ull << 32) - 1);
+  int32_t* nb = nullptr;
+  if (cudaMalloc(&nb, nc * sizeof(int32_t)) != cudaSuccess) return fail(DGDS_ENOMEM, "stream-history allocation failed");
+  if (s->d_shist) {
+    DGDS_CUDA(cudaStreamSynchronize(s->st));  // appends in flight finish writing the old arena
+    DGDS_CUDA(cudaMemcpy(nb, s->d_shist, s->shist_cap * sizeof(int32_t), cudaMemcpyDeviceToDevice));
+    cudaFree(s->d_shist);
+  }
+  s->d_shist = nb;
+  s->shist_cap = nc;
+  s->T.shist = nb;
+  return DGDS_OK;
+}
+
 // Shared host logic of update_batch / update_batch_device: replies in call
 // order (DraftServer::update_cst, dgds.cpp:36-51 -> GroupDraftIndex::append,
 // cst.cpp:118-133), plus the device segment table.
 // Record i's tokens are tokens[tok_start(i) .. tok_start(i) + tok_count(i)).
 int plan_updates(dgds_server* s, int64_t n, const int32_t* handles, const int32_t* rids, const uint64_t* prev,
                  const uint64_t* offs, const uint64_t* counts, double now, dgds_update_reply* rep,
-                 std::vector<dgds::AppendSeg>& segs, std::vector<dgds::AppendPiece>& pieces, uint64_t* worst,
-                 std::vector<DeferredLog>* defer = nullptr) {
+                 std::vector<dgds::AppendSeg>& segs, std::vector<dgds::AppendPiece>& pieces,
+                 std::vector<dgds::CopyPiece>& grow, uint64_t* worst, std::vector<DeferredLog>* defer = nullptr) {
   // offs[n+1] cumulative (counts == nullptr), or offs[n] starts + counts[n]
   auto tstart = [&](int64_t i) { return offs[i]; };
   auto tcount = [&](int64_t i) { return counts ? counts[i] : offs[i + 1] - offs[i]; };
@@ -262,6 +312,7 @@ int plan_updates(dgds_server* s, int64_t n, const int32_t* handles, const int32_
   PhaseClock pcl("plan_updates");
   const uint64_t stamp = ++s->batch_stamp;
   segs.clear();
+  grow.clear();
   *worst = 0;
   // Records of different groups are independent (version, streams and log are per group), so
   // large batches are planned in parallel with the groups partitioned over the host workers;
@@ -275,6 +326,8 @@ int plan_updates(dgds_server* s, int64_t n, const int32_t* handles, const int32_
   if (!defer || W > 1) materialize_logs(s);  // this plan appends to the group logs directly
   struct Part {
     std::vector<dgds::AppendSeg> segs;
+    std::vector<std::pair<int32_t, int32_t>> srec;  // (group handle, request id) of each segment
+    std::vector<dgds::CopyPiece> grow;
     std::vector<PendingPiece> pend;
     uint64_t worst = 0;
     int rc = DGDS_OK;
@@ -287,6 +340,8 @@ int plan_updates(dgds_server* s, int64_t n, const int32_t* handles, const int32_
   parts.resize(W);
   for (Part& P : parts) {
     P.segs.clear();
+    P.srec.clear();
+    P.grow.clear();
     P.pend.clear();
     P.worst = 0;
     P.rc = DGDS_OK;
@@ -294,6 +349,8 @@ int plan_updates(dgds_server* s, int64_t n, const int32_t* handles, const int32_
   std::mutex gmu;
   std::atomic<uint64_t> hist_at{s->hist_used};
   uint64_t hist_one = s->hist_used;
+  std::atomic<uint64_t> shist_at{s->shist_used};
+  std::atomic<uint64_t> shist_dead{0};
   auto work = [&](int w) {
     Part& P = parts[w];
     if (W > 1) cudaSetDevice(s->p.device);
@@ -344,6 +401,7 @@ int plan_updates(dgds_server* s, int64_t n, const int32_t* handles, const int32_
         sg.root = g.root;
         sg.start = sr.stored;
         P.segs.push_back(sg);
+        P.srec.emplace_back(handles[i], rids[i]);  // not &sr: a later insert may move it
       }
       uint64_t hoff;
       if (W == 1) {  // single planner: no locked read-modify-write per record
@@ -352,7 +410,7 @@ int plan_updates(dgds_server* s, int64_t n, const int32_t* handles, const int32_
       } else {
         hoff = hist_at.fetch_add(cnt, std::memory_order_relaxed);
       }
-      P.pend.push_back(PendingPiece{sr.batch_seg, tstart(i), hoff, static_cast<uint32_t>(cnt)});
+      P.pend.push_back(PendingPiece{sr.batch_seg, tstart(i), hoff, sr.stored, static_cast<uint32_t>(cnt)});
       if (defer && W == 1)  // appended to the group log after the plan's K1 launch
         defer->push_back(DeferredLog{handles[i], LogRec{hoff, sr.stored, static_cast<uint32_t>(cnt), rids[i]}});
       else
@@ -362,56 +420,61 @@ int plan_updates(dgds_server* s, int64_t n, const int32_t* handles, const int32_
       g.version += 1;
       rep[i] = dgds_update_reply{1, 0, g.version, sr.stored};
     }
+    // each segment's stream extent: a full one moves to one twice as large (its stored tokens
+    // are copied on the device before the batch is staged)
+    for (size_t k = 0; k < P.segs.size(); ++k) {
+      dgds::AppendSeg& sg = P.segs[k];
+      StreamRec& sr = *s->groups[P.srec[k].first].streams.find(P.srec[k].second);
+      sg.n = static_cast<uint32_t>(sr.stored - sg.start);
+      if (sr.stored > sr.sh_cap) {
+        const uint64_t nc = (std::max<uint64_t>({sr.stored, sr.sh_cap * 2, 64}) + 7) / 8 * 8;
+        const uint64_t nb = shist_at.fetch_add(nc, std::memory_order_relaxed);
+        if (sg.start > 0) P.grow.push_back(dgds::CopyPiece{sr.sh_base, nb, static_cast<uint32_t>(sg.start), 0});
+        shist_dead.fetch_add(sr.sh_cap, std::memory_order_relaxed);
+        sr.sh_base = nb;
+        sr.sh_cap = nc;
+      }
+      sg.sh_base = sr.sh_base;
+    }
   };
   pcl.mark("validate_setup");
   if (W > 1) pool.run(W, work);
   else work(0);
   pcl.mark("records");
   s->hist_used = W == 1 ? hist_one : hist_at.load();
+  s->shist_used = shist_at.load();
+  s->dead_shist_tokens += shist_dead.load();
   for (const Part& P : parts)
     if (P.rc) return fail(P.rc, P.msg);
-  // merge the workers' segments; group pieces by segment, keeping call order inside a segment
-  if (W == 1 && parts[0].pend.size() == parts[0].segs.size()) {  // one piece per segment: no grouping
+  for (const Part& P : parts) grow.insert(grow.end(), P.grow.begin(), P.grow.end());
+  // merge the workers' segments (pieces are independent copies: k_stage)
+  if (W == 1) {
     Part& P = parts[0];
     segs.assign(P.segs.begin(), P.segs.end());  // copy: both vectors keep their capacity
     *worst = P.worst;
     pieces.resize(P.pend.size());
     for (size_t k = 0; k < P.pend.size(); ++k) {
       const PendingPiece& pp = P.pend[k];
-      segs[pp.seg].piece0 = static_cast<uint32_t>(k);
-      segs[pp.seg].npieces = 1;
-      pieces[k] = dgds::AppendPiece{pp.tok_off, pp.hist_off, pp.n, 0};
+      pieces[k] = dgds::AppendPiece{pp.tok_off, pp.hist_off, segs[pp.seg].sh_base + pp.pos, pp.n, 0};
     }
-    pcl.mark("pieces_fast");
+    pcl.mark("pieces");
     return DGDS_OK;
   }
   std::vector<int64_t> base(W + 1, 0);
   for (int w = 0; w < W; ++w) base[w + 1] = base[w] + static_cast<int64_t>(parts[w].segs.size());
   segs.reserve(base[W]);
   for (int w = 0; w < W; ++w) segs.insert(segs.end(), parts[w].segs.begin(), parts[w].segs.end());
-  std::vector<uint32_t>& cnt = s->scratch.cnt;
-  cnt.assign(segs.size() + 1, 0);
   size_t npend = 0;
   for (int w = 0; w < W; ++w) {
     *worst += parts[w].worst;
-    for (const auto& pp : parts[w].pend) cnt[base[w] + pp.seg + 1]++;
     npend += parts[w].pend.size();
   }
-  for (size_t k = 0; k < segs.size(); ++k) {
-    segs[k].piece0 = cnt[k];
-    segs[k].npieces = cnt[k + 1];
-    cnt[k + 1] += cnt[k];
-  }
-  pieces.assign(npend, dgds::AppendPiece{});
-  std::vector<uint32_t>& fill = s->scratch.fill;
-  fill.assign(segs.size(), 0);
-  for (int w = 0; w < W; ++w) {
-    for (const auto& pp : parts[w].pend) {
-      const int64_t sg = base[w] + pp.seg;
-      const uint32_t at = segs[sg].piece0 + fill[sg]++;
-      pieces[at] = dgds::AppendPiece{pp.tok_off, pp.hist_off, pp.n, 0};
-    }
-  }
+  // pieces are independent copies (k_stage); K1 reads each segment from its stream extent
+  pieces.resize(npend);
+  size_t at = 0;
+  for (int w = 0; w < W; ++w)
+    for (const auto& pp : parts[w].pend)
+      pieces[at++] = dgds::AppendPiece{pp.tok_off, pp.hist_off, segs[base[w] + pp.seg].sh_base + pp.pos, pp.n, 0};
   return DGDS_OK;
 }
 
@@ -487,28 +550,28 @@ int dgds_create(const dgds_params* params, dgds_server** out) {
   s->T.depth_cap = s->D;
   s->T.lim_pattern = p.max_pattern_len;
   s->T.lim_spec = p.max_spec_len;
-  s->T.ahead = 0;  // the bulk L2 prefetch measured slower than the register preload alone
-  if (const char* e = std::getenv("DGDS_PREFETCH_AHEAD")) s->T.ahead = std::max(0, std::atoi(e));
   s->T.dbg = nullptr;
   if (std::getenv("DGDS_APPEND_DBG")) {  // debug: per-warp K1 timing, read with dgds_debug_append_timing
     DGDS_CUDA(cudaMalloc(&s->T.dbg, 65536 * 2 * sizeof(unsigned long long)));
     DGDS_CUDA(cudaMemset(s->T.dbg, 0, 65536 * 2 * sizeof(unsigned long long)));
   }
-  s->T.claim_cas = 1;  // CAS-first claim (measured faster: fewer random accesses per insert)
-  if (const char* e = std::getenv("DGDS_CLAIM")) s->T.claim_cas = std::strcmp(e, "load") == 0 ? 0 : 1;
   DGDS_CUDA(cudaMalloc(&s->T.slots, cap * sizeof(dgds::Slot)));
   DGDS_CUDA(cudaMemsetAsync(s->T.slots, 0, cap * sizeof(dgds::Slot), s->st));
   DGDS_CUDA(cudaMalloc(&s->d_used, dgds::kUsedParts * 8 * sizeof(unsigned long long)));
   DGDS_CUDA(cudaMemsetAsync(s->d_used, 0, dgds::kUsedParts * 8 * sizeof(unsigned long long), s->st));
   s->T.used = s->d_used;
-  s->stream_cap = std::max<uint64_t>(p.expected_streams ? p.expected_streams : 4096, 64);
-  DGDS_CUDA(cudaMalloc(&s->T.active, s->stream_cap * dgds::kWarp * sizeof(uint32_t)));
-  DGDS_CUDA(cudaMalloc(&s->T.tail, s->stream_cap * dgds::kWarp * sizeof(int32_t)));
+  if (int rc = grow_streams(s.get(), std::max<uint64_t>(p.expected_streams ? p.expected_streams : 4096, 64))) return rc;
   DGDS_CUDA(cudaMalloc(&s->d_err, sizeof(int32_t)));
   DGDS_CUDA(cudaMemsetAsync(s->d_err, 0, sizeof(int32_t), s->st));
-  s->hist_cap = std::max<uint64_t>(1ull << 20, nodes / 20);  // ~ tokens (nodes per token ~ 17-24)
+  s->T.err = s->d_err;
+  DGDS_CUDA(cudaMalloc(&s->T.ev_count, 2 * sizeof(unsigned long long)));
+  DGDS_CUDA(cudaMemsetAsync(s->T.ev_count, 0, 2 * sizeof(unsigned long long), s->st));
+  s->hist_cap = std::max<uint64_t>(1ull << 20, nodes / 2);  // ~ tokens (entries per token ~ 1-3)
   DGDS_CUDA(cudaMalloc(&s->d_hist, s->hist_cap * sizeof(int32_t)));
   s->T.hist = s->d_hist;
+  s->shist_cap = s->hist_cap * 2;  // extents: up to 2x their streams' lengths
+  DGDS_CUDA(cudaMalloc(&s->d_shist, s->shist_cap * sizeof(int32_t)));
+  s->T.shist = s->d_shist;
   // [kStatParts][8] counter partitions + the ticket of k_query's last-block fold
   DGDS_CUDA(cudaMalloc(&s->d_stat_part, (dgds::kStatParts * 8 + 1) * sizeof(unsigned long long)));
   DGDS_CUDA(cudaMemsetAsync(s->d_stat_part, 0, (dgds::kStatParts * 8 + 1) * sizeof(unsigned long long), s->st));
@@ -530,7 +593,11 @@ int dgds_destroy(dgds_server* s) {
   if (s->copy_st) cudaStreamSynchronize(s->copy_st);
   cudaFree(s->T.slots);
   cudaFree(s->T.active);
-  cudaFree(s->T.tail);
+  cudaFree(s->T.ov);
+  cudaFree(s->T.sinfo);
+  cudaFree(s->d_shist);
+  cudaFree(s->T.ev);
+  cudaFree(s->T.ev_count);
   cudaFree(s->d_used);
   cudaFree(s->d_root_of);
   cudaFree(s->d_err);
@@ -660,10 +727,39 @@ int dgds_node_count(dgds_server* s, uint64_t* out) {
   uint64_t u = 0;
   if (int rc = read_used(s, &u)) return rc;
   s->used_ub = u;
-  // + group roots, matching nodes_.size() (root counted) per live group
+  // entries + the count-1 chains below leaves (k_node_count) + group roots, matching
+  // nodes_.size() (root counted) per live group
+  DevBuf& tmp = s->d_count;
+  if (int rc = tmp.ensure(sizeof(unsigned long long))) return rc;
+  DGDS_CUDA(cudaMemsetAsync(tmp.p, 0, sizeof(unsigned long long), s->st));
+  DGDS_CUDA(dgds::launch_node_count(s->T, static_cast<unsigned long long*>(tmp.p), s->st));
+  unsigned long long nodes = 0;
+  DGDS_CUDA(cudaMemcpyAsync(&nodes, tmp.p, sizeof(nodes), cudaMemcpyDeviceToHost, s->st));
+  DGDS_CUDA(cudaStreamSynchronize(s->st));
   uint64_t roots = 0;
   for (const auto& g : s->groups) roots += g.alive ? 1 : 0;
-  *out = u + roots;
+  *out = nodes + roots;
+  return DGDS_OK;
+}
+
+int dgds_entry_count(dgds_server* s, uint64_t* out) {
+  if (!s || !out) return fail(DGDS_EINVAL, "null argument");
+  std::lock_guard<std::mutex> lk(s->mu);
+  if (int rc_ = flush_pending(s)) return rc_;
+  cudaSetDevice(s->p.device);
+  if (int rc = read_used(s, out)) return rc;
+  s->used_ub = *out;
+  return DGDS_OK;
+}
+
+int dgds_device_error(dgds_server* s, int32_t* flags) {
+  if (!s || !flags) return fail(DGDS_EINVAL, "null argument");
+  std::lock_guard<std::mutex> lk(s->mu);
+  if (int rc_ = flush_pending(s)) return rc_;
+  DGDS_CUDA(cudaSetDevice(s->p.device));
+  DGDS_CUDA(cudaMemcpyAsync(flags, s->d_err, sizeof(int32_t), cudaMemcpyDeviceToHost, s->st));
+  DGDS_CUDA(cudaMemsetAsync(s->d_err, 0, sizeof(int32_t), s->st));
+  DGDS_CUDA(cudaStreamSynchronize(s->st));
   return DGDS_OK;
 }
 
@@ -685,17 +781,21 @@ int update_batch_locked(dgds_server* s, int64_t n, const int32_t* handles, const
   }
   std::vector<dgds::AppendSeg>& segs = s->scratch.segs;
   std::vector<dgds::AppendPiece>& pieces = s->scratch.pieces;
+  std::vector<dgds::CopyPiece>& grow = s->scratch.grow;
   uint64_t worst = 0;
-  if (int rc = plan_updates(s, n, handles, rids, prev, offs, nullptr, now, rep, segs, pieces, &worst)) return rc;
+  if (int rc = plan_updates(s, n, handles, rids, prev, offs, nullptr, now, rep, segs, pieces, grow, &worst)) return rc;
   pc.mark("plan");
   if (segs.empty()) return DGDS_OK;
   if (int rc = ensure_capacity(s, worst)) return rc;
   if (int rc = ensure_hist(s)) return rc;
-  // one pinned staging block -> one H2D copy: segs | pieces | tokens
+  if (int rc = ensure_shist(s)) return rc;
+  // one pinned staging block -> one H2D copy: segs | pieces | extent moves | tokens
   const size_t b_seg = segs.size() * sizeof(dgds::AppendSeg);
   const size_t o_piece = align_up(b_seg, 256);
   const size_t b_piece = pieces.size() * sizeof(dgds::AppendPiece);
-  const size_t o_tok = align_up(o_piece + b_piece, 256);
+  const size_t o_grow = align_up(o_piece + b_piece, 256);
+  const size_t b_grow = grow.size() * sizeof(dgds::CopyPiece);
+  const size_t o_tok = align_up(o_grow + b_grow, 256);
   const size_t total = o_tok + ntok * sizeof(int32_t);
   DGDS_CUDA(cudaEventSynchronize(s->staging_free));
   if (int rc = s->h_stage.ensure(total)) return rc;
@@ -704,6 +804,7 @@ int update_batch_locked(dgds_server* s, int64_t n, const int32_t* handles, const
   for (auto& pc : pieces) pc.tok_off -= offs[0];
   nt_copy(h, segs.data(), b_seg);
   nt_copy(h + o_piece, pieces.data(), b_piece);
+  nt_copy(h + o_grow, grow.data(), b_grow);
   nt_copy(h + o_tok, tokens + offs[0], ntok * sizeof(int32_t));
   _mm_sfence();
   char* d = static_cast<char*>(s->d_stage.p);
@@ -715,7 +816,9 @@ int update_batch_locked(dgds_server* s, int64_t n, const int32_t* handles, const
     LaunchTimer lt(s, 0, s->st);
     DGDS_CUDA(dgds::launch_append(s->T, reinterpret_cast<const dgds::AppendSeg*>(d),
                                   static_cast<int64_t>(segs.size()), reinterpret_cast<const dgds::AppendPiece*>(d + o_piece),
-                                  reinterpret_cast<const int32_t*>(d + o_tok), s->st));
+                                  static_cast<int64_t>(pieces.size()), reinterpret_cast<const int32_t*>(d + o_tok),
+                                  reinterpret_cast<const dgds::CopyPiece*>(d + o_grow),
+                                  static_cast<int64_t>(grow.size()), s->st));
   }
   s->used_ub += worst;
   return DGDS_OK;
@@ -733,6 +836,7 @@ extern "C" int dgds_update_batch(dgds_server* s, int64_t n, const int32_t* handl
 struct dgds_update_plan {
   std::vector<dgds::AppendSeg> segs;
   std::vector<dgds::AppendPiece> pieces;
+  std::vector<dgds::CopyPiece> grow;  // stream extents moved by this plan
   std::vector<DeferredLog> logs;  // history-log records, appended after the launch
   const int32_t* d_tokens = nullptr;
   uint64_t seq = 0;
@@ -760,13 +864,14 @@ static int plan_device(dgds_server* s, int64_t n, const int32_t* handles, const 
                        const uint64_t* offs, const uint64_t* counts, const int32_t* d_tokens, double now,
                        dgds_update_reply* rep, dgds_update_plan* plan) {
   uint64_t worst = 0;
-  const int prc = plan_updates(s, n, handles, rids, prev, offs, counts, now, rep, plan->segs, plan->pieces, &worst,
-                               &plan->logs);
+  const int prc = plan_updates(s, n, handles, rids, prev, offs, counts, now, rep, plan->segs, plan->pieces,
+                               plan->grow, &worst, &plan->logs);
   if (!plan->logs.empty()) s->log_pending.push_back(plan);  // accepted records, even on a later error
   if (prc) return prc;
   if (plan->segs.empty()) return DGDS_OK;
   if (int rc = ensure_capacity(s, worst)) return rc;
   if (int rc = ensure_hist(s)) return rc;
+  if (int rc = ensure_shist(s)) return rc;
   s->used_ub += worst;  // at plan time: a later plan's capacity check must see pending inserts
   plan->d_tokens = d_tokens;
   plan->seq = ++s->plans_made;
@@ -781,7 +886,8 @@ static int launch_plan(dgds_server* s, dgds_update_plan* plan, void* stream, Pha
   StreamJoin join(s, stream);
   const size_t b_seg = plan->segs.size() * sizeof(dgds::AppendSeg);
   const size_t o_piece = align_up(b_seg, 256);
-  const size_t total = o_piece + plan->pieces.size() * sizeof(dgds::AppendPiece);
+  const size_t o_grow = align_up(o_piece + plan->pieces.size() * sizeof(dgds::AppendPiece), 256);
+  const size_t total = o_grow + plan->grow.size() * sizeof(dgds::CopyPiece);
   DGDS_CUDA(cudaEventSynchronize(s->staging_free));
   pc.mark("staging_wait");
   if (int rc = s->h_stage.ensure(total)) return rc;
@@ -789,6 +895,7 @@ static int launch_plan(dgds_server* s, dgds_update_plan* plan, void* stream, Pha
   char* h = static_cast<char*>(s->h_stage.p);
   nt_copy(h, plan->segs.data(), b_seg);
   nt_copy(h + o_piece, plan->pieces.data(), plan->pieces.size() * sizeof(dgds::AppendPiece));
+  nt_copy(h + o_grow, plan->grow.data(), plan->grow.size() * sizeof(dgds::CopyPiece));
   _mm_sfence();
   pc.mark("stage");
   char* d = static_cast<char*>(s->d_stage.p);
@@ -798,8 +905,10 @@ static int launch_plan(dgds_server* s, dgds_update_plan* plan, void* stream, Pha
     LaunchTimer lt(s, 0, join.stream());
     DGDS_CUDA(dgds::launch_append(s->T, reinterpret_cast<const dgds::AppendSeg*>(d),
                                   static_cast<int64_t>(plan->segs.size()),
-                                  reinterpret_cast<const dgds::AppendPiece*>(d + o_piece), plan->d_tokens,
-                                  join.stream()));
+                                  reinterpret_cast<const dgds::AppendPiece*>(d + o_piece),
+                                  static_cast<int64_t>(plan->pieces.size()), plan->d_tokens,
+                                  reinterpret_cast<const dgds::CopyPiece*>(d + o_grow),
+                                  static_cast<int64_t>(plan->grow.size()), join.stream()));
   }
   pc.mark("copy_launch");
   return DGDS_OK;
@@ -817,6 +926,7 @@ static int update_device_impl(dgds_server* s, int64_t n, const int32_t* handles,
   thread_local dgds_update_plan plan;
   plan.segs.clear();
   plan.pieces.clear();
+  plan.grow.clear();
   if (int rc = plan_device(s, n, handles, rids, prev, offs, counts, d_tokens, now, rep, &plan)) {
     materialize_logs(s);
     return rc;
@@ -933,6 +1043,7 @@ int dgds_update_plan_routed(dgds_server* s, int32_t n_seg, int64_t seg_rows, con
   if (!plan) plan = std::make_unique<dgds_update_plan>();
   plan->segs.clear();
   plan->pieces.clear();
+  plan->grow.clear();
   plan->logs.clear();
   plan->d_tokens = nullptr;
   plan->seq = 0;
@@ -1219,6 +1330,28 @@ extern "C" int dgds_touch_group(dgds_server* s, int32_t h, double now) {  // upd
 // Memory reclamation: a same-capacity rebuild drops the
 // slots of retired groups (rebuild keeps live roots only), and the history arena is
 // compacted to the live groups' tokens by a gather kernel.
+
+// Debug: copy device state into out (host): which 0 = slot table, 1 = stream table (StreamInfo),
+// 2 = active rows, 3 = ov rows, 4 = the stream-history arena, 5 = event queue. At most `bytes`.
+extern "C" int dgds_debug_dump(dgds_server* s, int32_t which, void* out, uint64_t bytes) {
+  if (!s || !out) return fail(DGDS_EINVAL, "null argument");
+  std::lock_guard<std::mutex> lk(s->mu);
+  if (int rc_ = flush_pending(s)) return rc_;
+  DGDS_CUDA(cudaStreamSynchronize(s->st));
+  const void* src = nullptr;
+  uint64_t have = 0;
+  switch (which) {
+    case 0: src = s->T.slots; have = s->T.cap * sizeof(dgds::Slot); break;
+    case 1: src = s->T.sinfo; have = s->stream_cap * sizeof(dgds::StreamInfo); break;
+    case 2: src = s->T.active; have = s->stream_cap * dgds::kWarp * 4; break;
+    case 3: src = s->T.ov; have = s->stream_cap * dgds::kWarp * 4; break;
+    case 4: src = s->d_shist; have = s->shist_cap * 4; break;
+    case 5: src = s->T.ev; have = s->ev_cap * sizeof(dgds::WalkEvent); break;
+    default: return fail(DGDS_EINVAL, "bad dump selector");
+  }
+  DGDS_CUDA(cudaMemcpy(out, src, std::min(bytes, have), cudaMemcpyDeviceToHost));
+  return DGDS_OK;
+}
 
 extern "C" int dgds_debug_append_timing(dgds_server* s, uint64_t* out, int64_t n_warps) {  // [n][2] start, end (ns)
   if (!s || !out) return fail(DGDS_EINVAL, "null argument");

@@ -219,6 +219,8 @@ struct LogRec {  // GroupDraftIndex::LogEntry (cst.hpp:120-124) + where its toke
 
 struct StreamRec {
   uint64_t stored = 0;
+  uint64_t sh_base = 0;  // token extent in the stream-history arena (dgds_server::d_shist)
+  uint64_t sh_cap = 0;   // its capacity (tokens); a full extent moves to one twice as large
   uint32_t slot = 0;
   int64_t batch_seg = -1;  // segment index in the batch being built
   uint64_t batch_stamp = 0;
@@ -425,8 +427,12 @@ struct dgds_server {
   unsigned long long* d_used = nullptr;
   uint64_t used_ub = 0;  // upper bound on occupied slots since the last exact read
 
-  int32_t* d_hist = nullptr;  // append-only token history (GDX1 blobs); K1 fills it
+  int32_t* d_hist = nullptr;  // append-only token history (GDX1 blobs); k_stage fills it
   uint64_t hist_cap = 0, hist_used = 0;
+  // per-stream token extents (queries and K1's conversion walks read continuations there)
+  int32_t* d_shist = nullptr;
+  uint64_t shist_cap = 0, shist_used = 0;
+  uint64_t dead_shist_tokens = 0;  // extents that were moved or whose stream was retired
   uint64_t dead_hist_tokens = 0;  // history of retired groups (reclaimed by compact_memory)
   uint64_t compactions = 0;
   DevBuf d_blob, d_blob_pieces;
@@ -439,6 +445,9 @@ struct dgds_server {
   uint64_t stream_cap = 0;
   uint32_t next_stream = 0;
   std::vector<uint32_t> free_streams;
+  // slots of retired streams: reusable only after a rebuild has dropped their groups' entries
+  // (entries name their stream; a reused slot would make a dead entry look alive)
+  std::vector<uint32_t> retired_streams;
 
   std::unordered_map<std::string, int32_t> intern;
   std::vector<GroupRec> groups;
@@ -456,6 +465,7 @@ struct dgds_server {
   struct PlanScratch {
     std::vector<dgds::AppendSeg> segs;
     std::vector<dgds::AppendPiece> pieces;
+    std::vector<dgds::CopyPiece> grow;
     std::vector<uint32_t> cnt, fill;
   } scratch;
   WorkerPool& workers() {
@@ -463,6 +473,8 @@ struct dgds_server {
     return *pool;
   }
   int32_t* d_err = nullptr;
+  DevBuf d_count;  // node-count reduction
+  uint64_t ev_cap = 0;  // K1 conversion-event queue (T.ev)
   unsigned long long* d_stat_part = nullptr;  // [kStatParts][8] query-counter partitions
   std::mutex mu;  // calls on one handle are serialized
 
@@ -494,6 +506,7 @@ int read_used(dgds_server* s, uint64_t* out);
 int rebuild(dgds_server* s, uint64_t new_cap);
 int ensure_capacity(dgds_server* s, uint64_t worst_new);
 int ensure_hist(dgds_server* s);
+int ensure_shist(dgds_server* s);
 // replica.cpp
 int compact_memory(dgds_server* s);
 int maybe_compact(dgds_server* s);

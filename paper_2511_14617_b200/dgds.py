@@ -210,6 +210,18 @@ class DraftServer:
         check(lib().dgds_node_count(self._h, C.byref(out)))
         return int(out.value)
 
+    def entry_count(self) -> int:
+        """Table entries in use (nodes with count >= 2 and leaves)."""
+        out = C.c_uint64()
+        check(lib().dgds_entry_count(self._h, C.byref(out)))
+        return out.value
+
+    def device_error(self) -> int:
+        """Reads and clears the device error flags (0 = clean); see dgds_device_error."""
+        out = C.c_int32()
+        check(lib().dgds_device_error(self._h, C.byref(out)))
+        return out.value
+
     def batch_speculate_zc(self, d_handles, d_pat_end, d_pat_len, d_pattern_buffer, d_out_offsets,
                            d_output_buffer, layout, d_args, args_stride: int, max_top_k: int, max_spec: int,
                            d_stats=None, stream: int = 0) -> None:
