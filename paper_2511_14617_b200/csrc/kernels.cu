@@ -53,7 +53,8 @@ __device__ __forceinline__ int lane_id() { return threadIdx.x & (kWarp - 1); }
 // rejects it before planning) sets err bit 1, and K1 then inserts nothing.
 
 __global__ void k_stage(DevTrie T, const AppendSeg* __restrict__ segs, int64_t nseg,
-                        const AppendPiece* __restrict__ pieces, int64_t npieces, const int32_t* __restrict__ tokens) {
+                        const AppendPiece* __restrict__ pieces, int64_t npieces, const int32_t* __restrict__ tokens,
+                        const CopyPiece* __restrict__ grow, int64_t ngrow) {
   const int lane = lane_id();
   const int64_t gt = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int64_t nth = static_cast<int64_t>(gridDim.x) * blockDim.x;
@@ -71,6 +72,11 @@ __global__ void k_stage(DevTrie T, const AppendSeg* __restrict__ segs, int64_t n
       T.shist[pc.sh_off + k] = v;
     }
   }
+  // moved stream extents: the stored tokens into the new extent (disjoint from the pieces above)
+  for (int64_t w = gt / kWarp; w < ngrow; w += nth / kWarp) {
+    const CopyPiece pc = grow[w];
+    for (uint32_t k = lane; k < pc.len; k += kWarp) T.shist[pc.dst + k] = T.shist[pc.src + k];
+  }
   if (__any_sync(kFull, any < 0) && lane == 0) atomicOr(T.err, 2);
 }
 
@@ -83,25 +89,39 @@ __global__ void k_stage(DevTrie T, const AppendSeg* __restrict__ segs, int64_t n
 // its window only when the parent is a node (count >= 2) or the group root:
 //   - absent  -> a new LEAF holding this occurrence; the window's continuation
 //                (all longer windows on this diagonal) is implicit from here on;
-//   - a leaf  -> it becomes a node (count 2); the leaf's own occurrence must now
-//                continue explicitly: a CONVERSION WALK (below) is queued;
+//   - a leaf  -> it becomes a node (count 2); the leaf's own occurrence (the
+//                DISPLACED occurrence) must now continue explicitly;
 //   - a node  -> count + 1.
 // A lane whose parent is implicit does nothing: its window has count 1 and is
 // the stream's own continuation below a leaf. Counts are order-free sums and a
 // leaf converts exactly once (the atomic that takes its counter from 0), so
 // concurrent streams of one group reach exactly the reference's trie.
 //
-// Conversion walk (K1b, one thread per event queued by K1): the displaced
-// occurrence (stream s, window ending at e) continues with the windows ending
-// at e+1, e+2, ... on the same diagonal, which nobody counted (s's owner
-// treated them as implicit). The walk adds them one by one from s's extent
-// (final for this batch: k_stage ran first) until it creates a leaf, reaches
-// the depth cap or the end of s. Converting another leaf on the way also
-// continues that leaf's own occurrence (a DFS stack; depths strictly increase,
-// so it holds < 32 frames). A walk that reaches the end of s leaves the node
-// it holds in ov[s][depth-1]; s's next segment takes it as that lane's state.
-// K1b runs after K1 has finished, so no segment of this batch reads ov while a
-// walk writes it.
+// Riders. A displaced occurrence usually continues with the same tokens as the
+// occurrence that displaced it (responses of a group share long runs). The lane
+// that converted the leaf therefore carries the displaced occurrence down its
+// own diagonal as a RIDER: at each next token it compares the rider's next
+// token (from the rider stream's extent, staged by k_stage) with its own; equal
+// tokens mean the same window, counted twice in one atomic. The first mismatch,
+// the rider stream's end, or the end of the segment hands the rider to K1b as an
+// event. A second displaced occurrence while a rider is aboard is queued too.
+//
+// Node marks. A converted leaf gets occ_pos = kNodeMark, and a window created
+// with two occurrences (a lane and its rider) is born marked, so a claim that
+// returns a marked entry knows it is a node: its count is a fire-and-forget RED
+// instead of a returning atomic on the token's critical path.
+//
+// Conversion walk (K1b, one thread per event): the event's occurrence (stream
+// s, window ending at e) continues with the windows ending at e+1, e+2, ... on
+// the same diagonal, which nobody counted (s's owner treated them as implicit).
+// The walk adds them one by one from s's extent (final for this batch: k_stage
+// ran first) until it creates a leaf, reaches the depth cap or the end of s,
+// with the same rider scheme; other displaced occurrences go on a DFS stack. A
+// walk that reaches the end of s leaves the node it holds in ov[s][depth-1];
+// s's next segment takes it as that lane's state. K1b runs after K1 has
+// finished, so no segment of this batch reads ov while a walk writes it.
+
+constexpr uint32_t kNodeMark = 0xFFFFFFFFu;  // occ_pos of an entry known to be a node
 
 __device__ __forceinline__ void cas128(Slot* s, unsigned long long n0, unsigned long long n1, unsigned long long& o0,
                                        unsigned long long& o1) {
@@ -123,41 +143,63 @@ __device__ __forceinline__ void store_link(Slot* s, uint32_t h32, uint32_t next_
       static_cast<unsigned long long>(h32) | (static_cast<unsigned long long>(next_sibling) << 32);
 }
 
-// One occurrence of window (parent, token): CAS-first over the probe sequence. Slots fill in
-// probe order and are never freed between rebuilds, so the CAS's old value settles the case:
-// 0 = our new leaf; our key = present (count it); another key = probe on.
-// Returns the entry id; created = a new leaf; old = its counter before (0: it was a leaf and is
-// now a node, whose first occurrence is returned in occ_old).
-__device__ __forceinline__ uint32_t add_occurrence(const DevTrie& T, uint32_t h32, uint32_t parent, int32_t token,
-                                                   unsigned long long occ, bool& created, uint32_t& old,
-                                                   unsigned long long& occ_old) {
+struct AddResult {
+  uint32_t id;
+  bool created;
+  bool converted;     // a leaf became a node: its occurrence (d_stream, d_pos) is displaced
+  uint32_t d_stream;
+  uint32_t d_pos;
+};
+
+// Add inc (1 or 2) occurrences of window (parent, token) at depth `depth`, one of them ending at
+// `pos` of `stream`. CAS-first over the probe sequence: slots fill in probe order and are never
+// freed between rebuilds, so the CAS's old value settles the case: 0 = created (a leaf holding
+// this occurrence, or a marked node when inc = 2); our key = present; another key = probe on.
+__device__ __forceinline__ AddResult add_window(const DevTrie& T, uint32_t h32, uint32_t parent, int32_t token,
+                                                uint32_t stream, uint32_t depth, uint32_t pos, uint32_t inc) {
   const unsigned long long key = pack_key(parent, token);
+  const unsigned long long occ = pack_occ(stream, depth, inc == 2u ? kNodeMark : pos);
   const uint64_t cap = T.cap;
   uint64_t i = home_bucket(h32, cap / kBucket) * kBucket;
+  AddResult r{0, false, false, 0, 0};
   for (uint64_t probes = 0;; ++probes) {
     if (probes > 65536) {  // defensive: probe runs are short below the rebuild load
       atomicOr(T.err, 8);
-      created = false;
-      old = 1;
-      occ_old = 0;
-      return 0;
+      return r;
     }
     unsigned long long o0, o1;
     cas128(T.slots + i, key, occ, o0, o1);
     if (o0 == 0ull) {
-      created = true;
-      old = 0;
-      occ_old = 0;
-      return static_cast<uint32_t>(i + 1);
+      r.id = static_cast<uint32_t>(i + 1);
+      r.created = true;
+      if (inc == 2u) atomicAdd(&T.slots[i].count, 1u);  // born a node: the second occurrence
+      return r;
     }
     if (o0 == key) {
-      created = false;
-      occ_old = o1;
-      old = atomicAdd(&T.slots[i].count, 1u);
-      return static_cast<uint32_t>(i + 1);
+      r.id = static_cast<uint32_t>(i + 1);
+      if (static_cast<uint32_t>(o1 >> 32) == kNodeMark) {
+        atomicAdd(&T.slots[i].count, inc);  // a node: no conversion possible (RED)
+      } else if (atomicAdd(&T.slots[i].count, inc) == 0u) {
+        r.converted = true;
+        r.d_stream = occ_stream(static_cast<uint32_t>(o1));
+        r.d_pos = static_cast<uint32_t>(o1 >> 32);
+        T.slots[i].occ_pos = kNodeMark;
+      }
+      return r;
     }
     if (++i == cap) i = 0;
   }
+}
+
+// A rider: a displaced occurrence travelling down a diagonal with the occurrence that holds it.
+struct Rider {
+  uint32_t stream, pos;  // its window ends at `pos` of `stream`
+  uint32_t abs, end;     // shist offsets of that token and of the stream's end
+};
+
+__device__ __forceinline__ Rider make_rider(const DevTrie& T, uint32_t stream, uint32_t pos) {
+  const StreamInfo si = T.sinfo[stream];
+  return Rider{stream, pos, static_cast<uint32_t>(si.base + pos), static_cast<uint32_t>(si.base + si.len)};
 }
 
 __device__ void conversion_walk(const DevTrie& T, WalkEvent e, unsigned long long& inserted) {
@@ -165,9 +207,18 @@ __device__ void conversion_walk(const DevTrie& T, WalkEvent e, unsigned long lon
     unsigned long long h;
     uint32_t id, depth, stream, pos;
   };
-  Frame stk[DGDS_MAX_DEPTH];
+  // Pushes happen at the current depth (a rider leaving) or one deeper (a conversion with a
+  // rider aboard), and a popped frame carries no rider, so the stack is non-decreasing in depth
+  // with at most two frames per depth.
+  Frame stk[2 * DGDS_MAX_DEPTH];
   int sp = 0;
+  auto push = [&](const Frame& f) {
+    if (sp < 2 * DGDS_MAX_DEPTH) stk[sp++] = f;
+    else atomicOr(T.err, 4);  // cannot happen (see above)
+  };
   Frame cur{e.h, e.id, e.depth, e.stream, e.pos};
+  bool ron = false;
+  Rider rd{};
   const uint32_t D = static_cast<uint32_t>(T.depth_cap);
   for (int guard = 0;; ++guard) {
     if (guard > (1 << 16)) {  // defensive: a walk is bounded by its conversions
@@ -177,29 +228,45 @@ __device__ void conversion_walk(const DevTrie& T, WalkEvent e, unsigned long lon
     const StreamInfo si = T.sinfo[cur.stream];
     const uint32_t p = cur.pos + 1;
     if (p == si.len) T.ov[static_cast<uint64_t>(cur.stream) * kWarp + cur.depth - 1] = cur.id;
+    if (ron && rd.abs + 1u >= rd.end) {  // the rider's stream ends at this window
+      T.ov[static_cast<uint64_t>(rd.stream) * kWarp + cur.depth - 1] = cur.id;
+      ron = false;
+    }
     if (cur.depth < D && p < si.len) {
       const int32_t x = T.shist[si.base + p];
+      uint32_t inc = 1;
+      if (ron) {
+        if (T.shist[rd.abs + 1u] == x) {
+          inc = 2;
+        } else {
+          push(Frame{cur.h, cur.id, cur.depth, rd.stream, rd.pos});
+          ron = false;
+        }
+      }
       const unsigned long long h2 = hash_step(cur.h, x);
       const uint32_t hh = hash32(h2);
-      bool created;
-      uint32_t old;
-      unsigned long long oo;
-      const uint32_t id = add_occurrence(T, hh, cur.id, x, pack_occ(cur.stream, cur.depth + 1, p), created, old, oo);
-      if (created) {  // a new leaf: the rest of this occurrence is implicit below it
+      const AddResult r = add_window(T, hh, cur.id, x, cur.stream, cur.depth + 1, p, inc);
+      if (r.created) {
         ++inserted;
-        store_link(T.slots + (id - 1), hh, atomicExch(&T.slots[cur.id - 1].first_child, id));
-      } else {
-        const Frame nxt{h2, id, cur.depth + 1, cur.stream, p};
-        if (old == 0u && sp == DGDS_MAX_DEPTH) atomicOr(T.err, 4);  // cannot happen: depths increase
-        if (old == 0u && sp < DGDS_MAX_DEPTH) {  // another leaf converted: its occurrence continues too
-          stk[sp++] = nxt;
-          cur = Frame{h2, id, cur.depth + 1, occ_stream(static_cast<uint32_t>(oo)), static_cast<uint32_t>(oo >> 32)};
-        } else {
-          cur = nxt;
+        store_link(T.slots + (r.id - 1), hh, atomicExch(&T.slots[cur.id - 1].first_child, r.id));
+      }
+      if (!r.created || inc == 2u) {  // a node now: this occurrence (and its rider) continue
+        if (inc == 2u) rd = Rider{rd.stream, rd.pos + 1, rd.abs + 1, rd.end};
+        if (r.converted) {
+          if (!ron) {
+            rd = make_rider(T, r.d_stream, r.d_pos);
+            ron = true;
+          } else {
+            push(Frame{h2, r.id, cur.depth + 1, r.d_stream, r.d_pos});
+          }
         }
+        cur = Frame{h2, r.id, cur.depth + 1, cur.stream, p};
         continue;
       }
+    } else if (ron && cur.depth < D) {  // this stream ends here; the rider's continues
+      push(Frame{cur.h, cur.id, cur.depth, rd.stream, rd.pos});
     }
+    ron = false;
     if (sp == 0) break;
     cur = stk[--sp];
   }
@@ -237,6 +304,16 @@ __global__ void __launch_bounds__(B, DGDS_APPEND_OCC * (kBlock / B))
   const int64_t nwarps = static_cast<int64_t>(gridDim.x) * blockDim.x / kWarp;
   const int D = T.depth_cap;
   unsigned long long inserted_total = 0;
+  // warp-collective: queue the lanes' events for K1b with one queue atomic
+  auto queue = [&](bool ev, unsigned long long eh, uint32_t eid, uint32_t edepth, uint32_t es, uint32_t ep) {
+    const unsigned m = __ballot_sync(kFull, ev);
+    if (m) {
+      unsigned long long at = 0;
+      if (lane == __ffs(m) - 1) at = atomicAdd(T.ev_count, static_cast<unsigned long long>(__popc(m)));
+      at = __shfl_sync(kFull, at, __ffs(m) - 1);
+      if (ev) T.ev[at + __popc(m & ((1u << lane) - 1u))] = WalkEvent{eh, eid, edepth, es, ep};
+    }
+  };
 
   unsigned long long t_start = 0;
   if (T.dbg) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
@@ -269,6 +346,8 @@ __global__ void __launch_bounds__(B, DGDS_APPEND_OCC * (kBlock / B))
         if (stored_lane) a = o;
       }
     }
+    bool ron = false;  // this lane's window carries a rider
+    Rider rd{};
     uint64_t len = len0;
     uint32_t link_slot = 0, link_prev = 0, link_h = 0;
     bool link_pending = false;
@@ -281,53 +360,68 @@ __global__ void __launch_bounds__(B, DGDS_APPEND_OCC * (kBlock / B))
         const unsigned long long hup = __shfl_up_sync(kFull, h, 1);
         h = hash_step(lane == 0 ? hr : hup, t);
         const uint32_t pm = __shfl_up_sync(kFull, a, 1);
+        bool pron = __shfl_up_sync(kFull, ron, 1);
+        Rider prd;
+        prd.stream = __shfl_up_sync(kFull, rd.stream, 1);
+        prd.pos = __shfl_up_sync(kFull, rd.pos, 1);
+        prd.abs = __shfl_up_sync(kFull, rd.abs, 1);
+        prd.end = __shfl_up_sync(kFull, rd.end, 1);
         const uint32_t parent = lane == 0 ? g.root : pm;
+        const bool act = lane < newsize && parent != 0u;
+        pron = pron && act && lane > 0;
+        // the parent's rider: same next token = same window (counted twice); otherwise, or at
+        // the rider stream's end, it continues in K1b from the parent window
+        uint32_t inc = 1;
+        bool ev1 = false;
+        if (pron) {
+          if (prd.abs + 1u < prd.end && T.shist[prd.abs + 1u] == t) inc = 2;
+          else ev1 = true;
+        }
+        queue(ev1, hup, pm, static_cast<uint32_t>(lane), prd.stream, prd.pos);
         uint32_t na = 0;
-        bool ev = false;
-        uint32_t ev_stream = 0, ev_pos = 0;
-        if (lane < newsize && parent != 0u) {
+        bool nron = false, ev2 = false;
+        AddResult r{0, false, false, 0, 0};
+        if (act) {
           const uint32_t hh = hash32(h);
-          bool created;
-          uint32_t old;
-          unsigned long long oo;
-          const uint32_t id = add_occurrence(T, hh, parent, t, pack_occ(stream, static_cast<uint32_t>(lane) + 1u,
-                                                                        static_cast<uint32_t>(len)),
-                                             created, old, oo);
-          if (link_pending) {  // {h32, next_sibling} of the leaf created at the previous token
+          r = add_window(T, hh, parent, t, stream, static_cast<uint32_t>(lane) + 1u, static_cast<uint32_t>(len), inc);
+          if (link_pending) {  // {h32, next_sibling} of the entry created at the previous token
             store_link(T.slots + link_slot, link_h, link_prev);
             link_pending = false;
           }
-          if (created) {
+          if (r.created) {
             ++inserted_total;
             if (!is_root_id(parent, T.cap)) {  // root child lists are never enumerated
-              link_prev = atomicExch(&T.slots[parent - 1].first_child, id);
-              link_slot = id - 1;
+              link_prev = atomicExch(&T.slots[parent - 1].first_child, r.id);
+              link_slot = r.id - 1;
               link_h = hh;
               link_pending = true;
             } else {
-              store_link(T.slots + (id - 1), hh, 0u);
+              store_link(T.slots + (r.id - 1), hh, 0u);
             }
-          } else {
-            na = id;
-            if (old == 0u) {
-              ev = true;
-              ev_stream = occ_stream(static_cast<uint32_t>(oo));
-              ev_pos = static_cast<uint32_t>(oo >> 32);
+          }
+          if (!r.created || inc == 2u) {
+            na = r.id;  // a node
+            if (inc == 2u) {
+              nron = true;
+              rd = Rider{prd.stream, prd.pos + 1, prd.abs + 1, prd.end};
+            }
+            if (r.converted) {
+              if (!nron) {
+                nron = true;
+                rd = make_rider(T, r.d_stream, r.d_pos);
+              } else {
+                ev2 = true;
+              }
             }
           }
         }
+        queue(ev2, h, r.id, static_cast<uint32_t>(lane) + 1u, r.d_stream, r.d_pos);
         a = na;
-        const unsigned m = __ballot_sync(kFull, ev);
-        if (m) {  // queue the conversion walks for K1b (one atomic per warp)
-          unsigned long long at = 0;
-          if (lane == __ffs(m) - 1) at = atomicAdd(T.ev_count, static_cast<unsigned long long>(__popc(m)));
-          at = __shfl_sync(kFull, at, __ffs(m) - 1);
-          if (ev) T.ev[at + __popc(m & ((1u << lane) - 1u))] = WalkEvent{h, a, static_cast<uint32_t>(lane) + 1u,
-                                                                          ev_stream, ev_pos};
-        }
+        ron = nron && lane + 1 < D;  // at the depth cap a rider has no continuation
         ++len;
       }
     }
+    queue(ron, h, a, static_cast<uint32_t>(lane) + 1u, rd.stream, rd.pos);  // riders left at the segment end
     if (link_pending) store_link(T.slots + link_slot, link_h, link_prev);
     if (lane < D && static_cast<uint64_t>(lane) < len) act_row[lane] = a;
   }
@@ -1422,14 +1516,11 @@ cudaError_t launch_append(const DevTrie& T, const AppendSeg* d_segs, int64_t nse
                           int64_t npieces, const int32_t* d_tokens, const CopyPiece* d_grow, int64_t ngrow,
                           cudaStream_t st) {
   if (nseg <= 0) return cudaSuccess;
-  if (ngrow > 0) {  // moved extents: the stored tokens into the new, larger extent
-    cudaError_t e = launch_copy_pieces(d_grow, ngrow, T.shist, T.shist, st);
-    if (e != cudaSuccess) return e;
-  }
   {
-    const int64_t work = std::max<int64_t>(nseg, npieces * kWarp);
+    const int64_t work = std::max<int64_t>(nseg, (npieces + ngrow) * kWarp);
     const int64_t blocks = std::min<int64_t>((work + 255) / 256, 148 * 8);
-    k_stage<<<static_cast<unsigned>(blocks), 256, 0, st>>>(T, d_segs, nseg, d_pieces, npieces, d_tokens);
+    k_stage<<<static_cast<unsigned>(blocks), 256, 0, st>>>(T, d_segs, nseg, d_pieces, npieces, d_tokens, d_grow,
+                                                             ngrow);
   }
   debug_sync(st, "k_stage");
   const int blk = append_block();
@@ -1439,7 +1530,7 @@ cudaError_t launch_append(const DevTrie& T, const AppendSeg* d_segs, int64_t nse
   else if (blk == 64) k_append<64><<<static_cast<unsigned>(blocks), 64, 0, st>>>(T, d_segs, nseg);
   else k_append<kBlock><<<static_cast<unsigned>(blocks), kBlock, 0, st>>>(T, d_segs, nseg);
   debug_sync(st, "k_append");
-  k_walks<<<148 * 2, 128, 0, st>>>(T);
+  k_walks<<<148 * 16, 128, 0, st>>>(T);  // ~1 thread per event: walks are latency chains
   debug_sync(st, "k_walks");
   return cudaGetLastError();
 }

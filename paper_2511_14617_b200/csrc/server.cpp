@@ -429,7 +429,8 @@ int plan_updates(dgds_server* s, int64_t n, const int32_t* handles, const int32_
       if (sr.stored > sr.sh_cap) {
         const uint64_t nc = (std::max<uint64_t>({sr.stored, sr.sh_cap * 2, 64}) + 7) / 8 * 8;
         const uint64_t nb = shist_at.fetch_add(nc, std::memory_order_relaxed);
-        if (sg.start > 0) P.grow.push_back(dgds::CopyPiece{sr.sh_base, nb, static_cast<uint32_t>(sg.start), 0});
+        for (uint64_t c = 0; c < sg.start; c += 512)  // 512-token chunks: one warp each in k_stage
+          P.grow.push_back(dgds::CopyPiece{sr.sh_base + c, nb + c, static_cast<uint32_t>(std::min<uint64_t>(512, sg.start - c)), 0});
         shist_dead.fetch_add(sr.sh_cap, std::memory_order_relaxed);
         sr.sh_base = nb;
         sr.sh_cap = nc;

@@ -30,18 +30,23 @@ class Model:
         self.ov = {}
         self.events = []
 
-    def add(self, parent, tok, occ):
+    def add(self, parent, tok, occ, inc=1):
+        """add_window: returns (id, created, converted, displaced occ)."""
         k = (parent, tok)
         e = self.slots.get(k)
         if e is None:
-            e = dict(id=self.next_id, count=0, occ=occ, key=k)
+            e = dict(id=self.next_id, count=inc - 1, occ=occ if inc == 1 else (occ[0], occ[1], "mark"), key=k)
             self.next_id += 1
             self.slots[k] = e
             self.byid[e["id"]] = e
-            return e["id"], True, 0, None
+            return e["id"], True, False, None
         old = e["count"]
-        e["count"] += 1
-        return e["id"], False, old, e["occ"]
+        e["count"] += inc
+        if e["occ"][2] != "mark" and old == 0:
+            d = e["occ"]
+            e["occ"] = (d[0], d[1], "mark")
+            return e["id"], False, True, d
+        return e["id"], False, False, None
 
     def append_batch(self, recs, order=None):
         """recs: list of (stream, tokens) in call order; one segment per stream."""
@@ -56,8 +61,8 @@ class Model:
         items = list(segs.items())
         if order:
             random.Random(order).shuffle(items)
+        D = self.D
         for s, toks in items:  # K1, one segment at a time
-            D = self.D
             len0 = start[s]
             a = [self.active[s][l] if (l < D and l < len0) else 0 for l in range(32)]
             for l in range(32):
@@ -66,21 +71,42 @@ class Model:
                     self.ov[s][l] = 0
                     if l < D and l < len0:
                         a[l] = o
+            rider = [None] * 32  # (stream, pos)
             ln = len0
             for t in toks:
                 newsize = min(D, ln + 1)
                 na = [0] * 32
+                nr = [None] * 32
                 for l in range(newsize):
-                    parent = ("root", s_root(s)) if l == 0 else a[l - 1]
+                    parent = ("root", 0) if l == 0 else a[l - 1]
                     if parent == 0:
                         continue
-                    id_, created, old, oo = self.add(parent, t, (s, l + 1, ln))
-                    if not created:
+                    prd = rider[l - 1] if l > 0 else None
+                    inc = 1
+                    if prd is not None:
+                        rs, rp = prd
+                        if rp + 1 < len(self.hist[rs]) and self.hist[rs][rp + 1] == t:
+                            inc = 2
+                        else:
+                            self.events.append((parent, l, rs, rp))
+                    id_, created, conv, d = self.add(parent, t, (s, l + 1, ln), inc)
+                    if not created or inc == 2:
                         na[l] = id_
-                        if old == 0:
-                            self.events.append((id_, l + 1, oo[0], oo[2]))
-                a = na
+                        if inc == 2:
+                            nr[l] = (prd[0], prd[1] + 1)
+                        if conv:
+                            if nr[l] is None:
+                                nr[l] = (d[0], d[2])
+                            else:
+                                self.events.append((id_, l + 1, d[0], d[2]))
+                for l in range(32):
+                    if nr[l] is not None and l + 1 >= D:
+                        nr[l] = None
+                a, rider = na, nr
                 ln += 1
+            for l in range(32):
+                if rider[l] is not None:
+                    self.events.append((a[l], l + 1, rider[l][0], rider[l][1]))
             for l in range(32):
                 if l < D and l < ln:
                     self.active[s][l] = a[l]
@@ -92,23 +118,39 @@ class Model:
     def walk(self, id_, depth, stream, pos):
         stk = []
         cur = (id_, depth, stream, pos)
+        rider = None
         while True:
             cid, d, s, p0 = cur
             L = len(self.hist[s])
             p = p0 + 1
             if p == L:
                 self.ov[s][d - 1] = cid
+            if rider is not None and rider[1] + 1 >= len(self.hist[rider[0]]):
+                self.ov[rider[0]][d - 1] = cid
+                rider = None
             if d < self.D and p < L:
                 x = self.hist[s][p]
-                nid, created, old, oo = self.add(cid, x, (s, d + 1, p))
-                if not created:
-                    nxt = (nid, d + 1, s, p)
-                    if old == 0:
-                        stk.append(nxt)
-                        cur = (nid, d + 1, oo[0], oo[2])
+                inc = 1
+                if rider is not None:
+                    if self.hist[rider[0]][rider[1] + 1] == x:
+                        inc = 2
                     else:
-                        cur = nxt
+                        stk.append((cid, d, rider[0], rider[1]))
+                        rider = None
+                nid, created, conv, dd = self.add(cid, x, (s, d + 1, p), inc)
+                if not created or inc == 2:
+                    if inc == 2:
+                        rider = (rider[0], rider[1] + 1)
+                    if conv:
+                        if rider is None:
+                            rider = (dd[0], dd[2])
+                        else:
+                            stk.append((nid, d + 1, dd[0], dd[2]))
+                    cur = (nid, d + 1, s, p)
                     continue
+            elif rider is not None and d < self.D:
+                stk.append((cid, d, rider[0], rider[1]))
+            rider = None
             if not stk:
                 break
             cur = stk.pop()
@@ -129,7 +171,7 @@ class Model:
         for e in self.slots.values():
             w = window(e)
             out[w] += e["count"] + 1
-            if e["count"] == 0:
+            if e["count"] == 0 and e["occ"][2] != "mark":
                 s, d, p = e["occ"]
                 h = self.hist[s]
                 k = 1
