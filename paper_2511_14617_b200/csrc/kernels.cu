@@ -563,8 +563,25 @@ __device__ __forceinline__ unsigned long long make_imp(uint64_t abs, uint32_t re
 __device__ __forceinline__ uint32_t imp_rem(unsigned long long v) { return static_cast<uint32_t>(v >> 32) & 0x7FFFFFFFu; }
 __device__ __forceinline__ uint32_t imp_abs(unsigned long long v) { return static_cast<uint32_t>(v); }
 // the implicit continuation below leaf r (a window of `depth` tokens)
+__device__ __forceinline__ StreamInfo load_sinfo(const DevTrie& T, uint32_t stream) {
+  unsigned long long a, b;
+  asm("ld.global.nc.v2.u64 {%0,%1}, [%2];" : "=l"(a), "=l"(b) : "l"(T.sinfo + stream));
+  return StreamInfo{a, static_cast<uint32_t>(b), static_cast<uint32_t>(b >> 32)};
+}
+// A leaf child in the beam pool keeps its raw occurrence (bit 62) until it becomes a beam path:
+// most leaf children do not qualify, and resolving one costs a stream-table load.
+constexpr unsigned long long kImpRaw = 1ull << 62;
+__device__ __forceinline__ unsigned long long raw_imp(const SlotView& r) {
+  return (1ull << 63) | kImpRaw | (static_cast<unsigned long long>(occ_stream(r.occ_stream)) << 32) | r.occ_pos;
+}
+__device__ __forceinline__ unsigned long long resolve_imp(const DevTrie& T, unsigned long long v, int depth) {
+  const uint32_t pos = static_cast<uint32_t>(v);
+  const StreamInfo si = load_sinfo(T, static_cast<uint32_t>(v >> 32) & kStreamMask);
+  const uint32_t rem = min(static_cast<uint32_t>(T.depth_cap - depth), si.len - 1u - pos);
+  return make_imp(si.base + pos, rem);
+}
 __device__ __forceinline__ unsigned long long leaf_imp(const DevTrie& T, const SlotView& r, int depth) {
-  const StreamInfo si = T.sinfo[occ_stream(r.occ_stream)];
+  const StreamInfo si = load_sinfo(T, occ_stream(r.occ_stream));
   const uint32_t rem = min(static_cast<uint32_t>(T.depth_cap - depth), si.len - 1u - r.occ_pos);
   return make_imp(si.base + r.occ_pos, rem);
 }
@@ -734,12 +751,12 @@ __global__ void __launch_bounds__(B, DGDS_QUERY_OCC * (kBlock / B)) k_query(Quer
         if (i == 1) return false;
         const SlotView lr = load_slot_nc(T.slots + (prev - 1));
         if (lr.count != 0u) return false;  // a node: every child of a node is an entry
-        const StreamInfo si = T.sinfo[occ_stream(lr.occ_stream)];
+        const StreamInfo si = load_sinfo(T, occ_stream(lr.occ_stream));
         uint32_t e = lr.occ_pos;
         for (int m = i; m <= L; ++m) {
           if (m > i) ++looks;
           ++e;
-          if (e >= si.len || T.shist[si.base + e] != tok_at(j + m - 1)) return false;
+          if (e >= si.len || __ldg(T.shist + si.base + e) != tok_at(j + m - 1)) return false;
         }
         cnt = 1;
         fc = 0;
@@ -948,10 +965,10 @@ __global__ void __launch_bounds__(B, DGDS_QUERY_OCC * (kBlock / B)) k_query(Quer
       unsigned long long cimp = 0;
       if (c != 0u) {
         r = load_slot_nc(T.slots + (c - 1));
-        if (r.count == 0u) cimp = leaf_imp(T, r, child_depth);  // a leaf: implicit below it
+        if (r.count == 0u) cimp = raw_imp(r);  // a leaf: implicit below it (resolved if it is kept)
       } else if (impc) {
         const uint32_t at = imp_abs(b_imp) + 1u;
-        r.token = T.shist[at];
+        r.token = __ldg(T.shist + at);
         r.count = 0u;
         r.first_child = 0u;
         r.next_sibling = 0u;
@@ -1047,7 +1064,7 @@ __global__ void __launch_bounds__(B, DGDS_QUERY_OCC * (kBlock / B)) k_query(Quer
       for (int i = 0; i < S; ++i) tok[i] = nt[i];
       set_tok<S>(tok, d, p_tok);
       b_fc = p_fc;
-      b_imp = p_imp;
+      b_imp = (p_imp & kImpRaw) && gl < np ? resolve_imp(T, p_imp, child_depth) : p_imp;
       b_score = p_score;
       b_sup = p_sup;
       b_lex = lex;
@@ -1177,24 +1194,23 @@ __global__ void __launch_bounds__(B, DGDS_QUERY_OCC * (kBlock / B)) k_query(Quer
       for (int k = 0; k < 8; ++k)
         if (v[k]) atomicAdd(P.stat_part + part * 8 + k, static_cast<unsigned long long>(v[k]));
     }
-    // The last block to finish folds the partitions into P.stats (no separate fold launch):
-    // the barrier + fence order this block's counter atomics before its ticket.
-    __shared__ bool last_block;
-    __syncthreads();
-    if (threadIdx.x == 0) {
+    // The last warp to finish folds the partitions into P.stats (no separate fold launch, and
+    // no block barrier holding finished warps' SM slots): the fence orders this warp's counter
+    // atomics before its ticket.
+    bool last = false;
+    if (lane == 0) {
       __threadfence();
       unsigned long long* ticket = P.stat_part + kStatParts * 8;
-      last_block = atomicAdd(ticket, 1ull) == gridDim.x - 1;
+      last = atomicAdd(ticket, 1ull) == static_cast<unsigned long long>(gridDim.x) * (B / kWarp) - 1;
     }
-    __syncthreads();
-    if (last_block) {
+    if (__shfl_sync(kFull, last, 0)) {
       __threadfence();
-      if (threadIdx.x < 8) {
+      if (lane < 8) {
         unsigned long long t = 0;
-        for (int p = 0; p < kStatParts; ++p) t += atomicExch(P.stat_part + p * 8 + threadIdx.x, 0ull);
-        reinterpret_cast<unsigned long long*>(P.stats)[threadIdx.x] += t;
+        for (int p = 0; p < kStatParts; ++p) t += atomicExch(P.stat_part + p * 8 + lane, 0ull);
+        reinterpret_cast<unsigned long long*>(P.stats)[lane] += t;
       }
-      if (threadIdx.x == 0) P.stat_part[kStatParts * 8] = 0ull;
+      if (lane == 0) P.stat_part[kStatParts * 8] = 0ull;
     }
   }
 }
