@@ -303,6 +303,15 @@ class RefLib(_Lib):
         L.orc_ref_workload_output.argtypes = [C.c_void_p, C.c_int32, C.c_int32]
         L.orc_ref_workload_fingerprint.restype = C.c_uint64
         L.orc_ref_workload_fingerprint.argtypes = [C.c_void_p]
+        L.orc_ref_gset_new.restype = C.c_void_p
+        L.orc_ref_gset_new.argtypes = [C.c_int32, C.POINTER(C.c_char_p), C.c_int32, C.c_int32]
+        L.orc_ref_gset_free.argtypes = [C.c_void_p]
+        L.orc_ref_gset_append.argtypes = [C.c_void_p, C.c_int64] + [C.c_void_p] * 5 + [C.c_int32] + [C.c_void_p] * 3
+        L.orc_ref_gset_speculate.argtypes = ([C.c_void_p, C.c_int64] + [C.c_void_p] * 4 + [C.c_int32, C.c_int32,
+                                                                                          C.c_int32]
+                                             + [C.c_void_p] * 5)
+        L.orc_ref_gset_node_count.restype = C.c_uint64
+        L.orc_ref_gset_node_count.argtypes = [C.c_void_p]
         L.orc_ref_replay.restype = C.c_int64
         L.orc_ref_replay.argtypes = [C.c_void_p, C.POINTER(OrcReplayCfg), C.POINTER(C.c_int32), C.c_int64,
                                      C.POINTER(C.c_int32), C.c_int64, C.POINTER(C.c_int64),
@@ -310,6 +319,10 @@ class RefLib(_Lib):
 
     def shard_of_group(self, gid: str, n: int) -> int:
         return int(self.L.orc_ref_shard_of_group(gid.encode(), n))
+
+    # ---- many GroupDraftIndex objects in bulk (scale parity tests) ----
+    def group_set(self, gids, max_pattern_len=8, max_spec_len=16) -> "GroupSet":
+        return GroupSet(self, gids, max_pattern_len, max_spec_len)
 
     # ---- replica sync (GDX1 blobs) ----
     def _blob_call(self, fn, *args):
@@ -399,6 +412,62 @@ class RefLib(_Lib):
         finally:
             self.L.orc_ref_workload_free(h)
         return sb[:steps].copy(), rec[:4 * nrec.value].reshape(-1, 4).copy(), int(nq.value)
+
+
+class GroupSet:
+    """The reference GroupDraftIndex for many groups, appended and queried in bulk on host
+    threads split by group (oracle/ref_capi.cpp orc_ref_gset_*). TEST INFRASTRUCTURE ONLY."""
+
+    def __init__(self, lib: "RefLib", gids, max_pattern_len, max_spec_len):
+        import numpy as np
+        self.lib, self.np = lib, np
+        arr = (C.c_char_p * len(gids))(*[g.encode() for g in gids])
+        self.h = lib.L.orc_ref_gset_new(len(gids), arr, max_pattern_len, max_spec_len)
+        if not self.h:
+            raise OracleError(lib.err())
+        self.threads = os.cpu_count() or 8
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.lib.L.orc_ref_gset_free(self.h)
+            self.h = None
+
+    def append(self, group, rid, prev, offs, tokens):
+        np = self.np
+        n = len(group)
+        group, rid = np.ascontiguousarray(group, np.int32), np.ascontiguousarray(rid, np.int32)
+        prev, offs = np.ascontiguousarray(prev, np.uint64), np.ascontiguousarray(offs, np.uint64)
+        tokens = np.ascontiguousarray(tokens, np.int32)
+        ok = np.zeros(n, np.int32)
+        ver = np.zeros(n, np.uint64)
+        ack = np.zeros(n, np.uint64)
+        p = lambda a: a.ctypes.data_as(C.c_void_p)  # noqa: E731
+        if self.lib.L.orc_ref_gset_append(self.h, n, p(group), p(rid), p(prev), p(offs), p(tokens), self.threads,
+                                          p(ok), p(ver), p(ack)):
+            raise OracleError(self.lib.err())
+        return ok, ver, ack
+
+    def speculate(self, group, pat_offs, pats, args, k_cap, s_cap):
+        """args: one OrcArgs per query (ctypes array). Returns n_cands, lens, scores, supports, tokens
+        shaped [n], [n,k], [n,k], [n,k], [n,k,s]."""
+        np = self.np
+        n = len(group)
+        group = np.ascontiguousarray(group, np.int32)
+        pat_offs = np.ascontiguousarray(pat_offs, np.uint64)
+        pats = np.ascontiguousarray(pats, np.int32)
+        nc = np.zeros(n, np.int32)
+        ln = np.zeros((n, k_cap), np.int32)
+        sc = np.zeros((n, k_cap), np.float64)
+        sp = np.zeros((n, k_cap), np.int64)
+        tk = np.zeros((n, k_cap, s_cap), np.int32)
+        p = lambda a: a.ctypes.data_as(C.c_void_p)  # noqa: E731
+        if self.lib.L.orc_ref_gset_speculate(self.h, n, p(group), p(pat_offs), p(pats), C.cast(args, C.c_void_p),
+                                             self.threads, k_cap, s_cap, p(nc), p(ln), p(sc), p(sp), p(tk)):
+            raise OracleError(self.lib.err())
+        return nc, ln, sc, sp, tk
+
+    def node_count(self) -> int:
+        return int(self.lib.L.orc_ref_gset_node_count(self.h))
 
 
 def wcfg(num_groups=1, group_size=16, length_family=0, vocab_size=32000, location=4096.0, scale=0.0,

@@ -74,6 +74,19 @@ int orc_oracle_speculate(const int32_t* toks, const uint64_t* offsets, uint64_t 
 int orc_index_speculate_stats(const void* idx, const int32_t* pattern, uint64_t plen,
                               const orc_args* args, orc_cands* out, orc_qstats* stats);
 
+/* ---- reference-only: many indexes driven in bulk, threads split by group (scale parity) ---- */
+void* orc_ref_gset_new(int32_t ngroups, const char* const* gids, int32_t max_pattern_len, int32_t max_spec_len);
+void orc_ref_gset_free(void* gset);
+int orc_ref_gset_append(void* gset, int64_t n, const int32_t* group, const int32_t* rid, const uint64_t* prev,
+                        const uint64_t* offs, const int32_t* tokens, int32_t threads, int32_t* ok,
+                        uint64_t* version, uint64_t* acked);
+/* candidates of query i at [i][k_cap][s_cap] (tokens) / [i][k_cap] (lens, scores, supports) */
+int orc_ref_gset_speculate(void* gset, int64_t n, const int32_t* group, const uint64_t* pat_offs,
+                           const int32_t* pats, const orc_args* args, int32_t threads, int32_t k_cap,
+                           int32_t s_cap, int32_t* n_cands, int32_t* lens, double* scores, int64_t* supports,
+                           int32_t* tokens);
+uint64_t orc_ref_gset_node_count(const void* gset);
+
 #ifdef __cplusplus
 }
 #endif

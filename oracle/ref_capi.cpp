@@ -75,6 +75,25 @@ int guarded(F&& f) {
 
 }  // namespace
 
+namespace {
+struct GroupSet {
+  std::vector<std::unique_ptr<GroupDraftIndex>> idx;
+};
+
+template <class F>
+void for_groups(int64_t n, const int32_t* group, int32_t ngroups, int32_t threads, F&& f) {
+  const int T = std::max(1, std::min<int32_t>(threads, ngroups));
+  std::vector<std::thread> th;
+  for (int t = 0; t < T; ++t)
+    th.emplace_back([&, t] {
+      for (int64_t i = 0; i < n; ++i)
+        if (group[i] % T == t) f(i);
+    });
+  for (auto& x : th) x.join();
+}
+
+}  // namespace
+
 extern "C" {
 
 const char* orc_last_error(void) { return g_err.c_str(); }
@@ -138,6 +157,80 @@ int orc_oracle_speculate(const int32_t* toks, const uint64_t* offsets, uint64_t 
 int orc_index_speculate_stats(const void*, const int32_t*, uint64_t, const orc_args*, orc_cands*, orc_qstats*) {
   g_err = "speculate_stats is provided by liboracle.so only";
   return -1;
+}
+
+// ---------------------------------------------------------------------------
+// A set of GroupDraftIndex objects driven in bulk (scale parity tests): records and queries
+// of different groups are independent, so they are split over threads by group; inside a
+// group the records apply in array order, exactly as sequential append calls would.
+
+void* orc_ref_gset_new(int32_t ngroups, const char* const* gids, int32_t max_pattern_len, int32_t max_spec_len) {
+  try {
+    auto* g = new GroupSet;
+    GroupDraftIndex::Limits lim;
+    lim.max_pattern_len = max_pattern_len;
+    lim.max_spec_len = max_spec_len;
+    for (int32_t i = 0; i < ngroups; ++i) g->idx.push_back(std::make_unique<GroupDraftIndex>(gids[i], lim));
+    return g;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return nullptr;
+  }
+}
+
+void orc_ref_gset_free(void* g) { delete static_cast<GroupSet*>(g); }
+
+int orc_ref_gset_append(void* gs, int64_t n, const int32_t* group, const int32_t* rid, const uint64_t* prev,
+                        const uint64_t* offs, const int32_t* tokens, int32_t threads, int32_t* ok,
+                        uint64_t* version, uint64_t* acked) {
+  auto* g = static_cast<GroupSet*>(gs);
+  std::atomic<int> bad{0};
+  for_groups(n, group, static_cast<int32_t>(g->idx.size()), threads, [&](int64_t i) {
+    try {
+      auto r = g->idx[group[i]]->append(rid[i], prev[i], std::span<const Token>(tokens + offs[i], offs[i + 1] - offs[i]));
+      ok[i] = r.ok ? 1 : 0;
+      version[i] = r.version;
+      acked[i] = r.acked_tokens;
+    } catch (const std::exception&) {
+      bad = 1;
+    }
+  });
+  if (bad) {
+    g_err = "reference append threw";
+    return -1;
+  }
+  return 0;
+}
+
+int orc_ref_gset_speculate(void* gs, int64_t n, const int32_t* group, const uint64_t* pat_offs, const int32_t* pats,
+                           const orc_args* args, int32_t threads, int32_t k_cap, int32_t s_cap, int32_t* n_cands,
+                           int32_t* lens, double* scores, int64_t* supports, int32_t* tokens) {
+  auto* g = static_cast<GroupSet*>(gs);
+  std::atomic<int> bad{0};
+  for_groups(n, group, static_cast<int32_t>(g->idx.size()), threads, [&](int64_t i) {
+    try {
+      auto c = g->idx[group[i]]->speculate(std::span<const Token>(pats + pat_offs[i], pat_offs[i + 1] - pat_offs[i]),
+                                            to_args(args + i));
+      orc_cands out{tokens + i * static_cast<int64_t>(k_cap) * s_cap, lens + i * static_cast<int64_t>(k_cap),
+                    scores + i * static_cast<int64_t>(k_cap), supports + i * static_cast<int64_t>(k_cap), k_cap,
+                    s_cap, 0};
+      if (write_cands(c, &out)) bad = 1;
+      n_cands[i] = out.n;
+    } catch (const std::exception&) {
+      bad = 1;
+    }
+  });
+  if (bad) {
+    g_err = "reference speculate threw or overflowed the candidate buffer";
+    return -1;
+  }
+  return 0;
+}
+
+uint64_t orc_ref_gset_node_count(const void* gs) {
+  uint64_t n = 0;
+  for (const auto& x : static_cast<const GroupSet*>(gs)->idx) n += x->node_count();
+  return n;
 }
 
 // ---------------------------------------------------------------------------

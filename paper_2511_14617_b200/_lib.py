@@ -9,7 +9,9 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libdgds_b200.so")
+# DGDS_LIB_VARIANT=<name> loads a test-only build variant (build.py VARIANTS), e.g. hash10
+LIB_PATH = os.path.join(HERE, "libdgds_b200%s.so" % ("_" + os.environ["DGDS_LIB_VARIANT"]
+                                                       if os.environ.get("DGDS_LIB_VARIANT") else ""))
 
 DGDS_OK = 0
 DGDS_EINVAL = -1
@@ -231,7 +233,7 @@ def lib():
         if not os.path.exists(LIB_PATH):
             from . import build as _b
 
-            _b.build()
+            _b.build(variant=os.environ.get("DGDS_LIB_VARIANT") or None)
         L = C.CDLL(LIB_PATH)
         for name, (res, args) in EXPORTS.items():
             fn = getattr(L, name)

@@ -25,22 +25,35 @@ def nvcc() -> str:
     raise RuntimeError("nvcc not found")
 
 
-def _stale() -> bool:
-    if not os.path.exists(LIB):
+# Test-only variants: the same sources with a compile-time switch, loaded when the environment
+# names them (DGDS_LIB_VARIANT, see _lib.py). "hash10" truncates the stored content hash to 10
+# bits, so content probes collide constantly and every exact-key fallback and long probe run in
+# K1 / K2 is exercised by the parity tests.
+VARIANTS = {"hash10": ["-DDGDS_TEST_HASH_BITS=10"]}
+
+
+def lib_path(variant: str | None = None) -> str:
+    return LIB if not variant else os.path.join(HERE, "libdgds_b200_%s.so" % variant)
+
+
+def _stale(lib: str = LIB) -> bool:
+    if not os.path.exists(lib):
         return True
-    t = os.path.getmtime(LIB)
+    t = os.path.getmtime(lib)
     deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)]
     deps.append(os.path.join(HERE, "..", "include", "dgds_b200.h"))
     deps.append(os.path.abspath(__file__))
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
-        return LIB
+def build(force: bool = False, verbose: bool = False, variant: str | None = None) -> str:
+    lib = lib_path(variant)
+    if not force and not _stale(lib):
+        return lib
     objs = []
     common = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O3"] + ARCH
-    outdir = os.path.join(HERE, "_build")
+    common += VARIANTS[variant] if variant else []
+    outdir = os.path.join(HERE, "_build" + ("_" + variant if variant else ""))
     os.makedirs(outdir, exist_ok=True)
     for src in SOURCES:
         obj = os.path.join(outdir, os.path.splitext(src)[0] + ".o")
@@ -50,11 +63,14 @@ def build(force: bool = False, verbose: bool = False) -> str:
             cmd += ["-Xptxas", "-v"]
         subprocess.run(cmd, check=True)
         objs.append(obj)
-    tmp = LIB + ".tmp"
+    tmp = lib + ".tmp"
     subprocess.run([nvcc()] + ARCH + ["-shared", "-cudart", "static", "-o", tmp] + objs, check=True)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
     print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    for v in VARIANTS:
+        if "--variants" in sys.argv:
+            print(build(force="--force" in sys.argv, variant=v))
