@@ -4,6 +4,16 @@
 // reply-record compaction, and host-buffer verification (cst.cpp:153-228, engine.cpp:115-143).
 #include "server_internal.h"
 
+namespace {
+// K2a -> K2b queue of queries whose locus is a node: one entry per query of the launch.
+int set_cplx(dgds_server* s, dgds::QueryLaunch& L) {
+  if (int rc = s->d_cplx.ensure(std::max<int64_t>(1, L.n) * sizeof(dgds::CplxRec))) return rc;
+  L.cplx = static_cast<dgds::CplxRec*>(s->d_cplx.p);
+  L.cplx_count = s->d_cplx_count;
+  return DGDS_OK;
+}
+}  // namespace
+
 namespace dgds_host {
 
 // One host-buffer query batch: its results live in the mapped pinned block of its slot
@@ -291,6 +301,7 @@ int launch_batch(dgds_server* s, bool timed) {
     L.tokens = reinterpret_cast<int32_t*>(dout + o.tk) + q0 * K * Sx;
     L.err_flag = s->d_err;
     L.stat_part = s->d_stat_part;
+  if (int rc = set_cplx(s, L)) return rc;
     if (verify) {
       L.truth = reinterpret_cast<const int32_t*>(db + b.o_tr);
       L.truth_stride = pq.truth_stride;
@@ -479,6 +490,7 @@ static int speculate_records_impl(dgds_server* s, int64_t n, const int32_t* d_re
   L.stats = d_stats;
   L.err_flag = s->d_err;
   L.stat_part = s->d_stat_part;
+  if (int rc = set_cplx(s, L)) return rc;
   L.dbg = s->d_dbg;
   {
     LaunchTimer lt(s, 1, join.stream());
@@ -743,6 +755,7 @@ int dgds_speculate_device(dgds_server* s, int64_t n, const int32_t* d_handles, c
   L.stats = d_stats;
   L.err_flag = s->d_err;
   L.stat_part = s->d_stat_part;
+  if (int rc = set_cplx(s, L)) return rc;
   L.dbg = s->d_dbg;
   {
     LaunchTimer lt(s, 1, join.stream());
@@ -862,6 +875,7 @@ int dgds_batch_speculate_zc(dgds_server* s, int64_t n, const int32_t* d_handles,
   L.stats = d_stats;
   L.err_flag = s->d_err;
   L.stat_part = s->d_stat_part;
+  if (int rc = set_cplx(s, L)) return rc;
   L.dbg = s->d_dbg;
   {
     LaunchTimer lt(s, 1, join.stream());

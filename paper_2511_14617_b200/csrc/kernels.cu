@@ -470,6 +470,7 @@ struct __align__(16) GroupScratch {
       uint32_t wpar[36];
       uint32_t scnt[8];
       uint32_t sfc[8];
+      int32_t pat[8];  // the last `start` pattern tokens (tok_at)
     } a;
     struct {
       double score[G];
@@ -588,25 +589,26 @@ __device__ __forceinline__ unsigned long long leaf_imp(const DevTrie& T, const S
 
 // B = threads per block. A block retires only when its slowest warp does, so smaller blocks
 // free a finished warp's SM slot sooner; the register budget per SM is the same for every B.
-template <int G, int S, int B>
-__global__ void __launch_bounds__(B, DGDS_QUERY_OCC * (kBlock / B)) k_query(QueryLaunch P) {
-  // Programmatic dependent launch: the blocks may be resident before the previous kernel in
-  // the stream (typically K1) has finished; nothing is read until it has.
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-  constexpr int kTiles = B / G;
-  __shared__ GroupScratch<G, S> scratch[kTiles];
+// K2 runs in one of three modes (template parameter M):
+//   0  whole query per tile (phase A + phase B) — the fallback without a complex-query queue;
+//   1  K2a: phase A for every query. A query whose locus is a count-1 window (a leaf or the
+//      chain below one) has a determined answer — the single path of its stream's
+//      continuation, score 1.0 (every step 1/1), support 1 — written here with its
+//      verification; a query whose locus is a node is queued for K2b;
+//   2  K2b: phase B for the queued queries only, so its warps hold only branching queries.
+// Results, counters and verification are identical in every mode.
+
+template <int G, int S, int B, int M>
+__device__ __forceinline__ void query_tile(const QueryLaunch& P, GroupScratch<G, S>& sm, const int64_t q, bool valid,
+                                           const CplxRec& cr, uint32_t (&sv)[8]) {
   const int lane = lane_id();
   const int gl = lane % G;
   const Tile<G> tile{lane - gl};
-  const int gib = threadIdx.x / G;
-  const int64_t q = static_cast<int64_t>(blockIdx.x) * kTiles + gib;
-  bool valid = q < P.n;  // invalid tiles stay (convergence) but do nothing
   if (P.seg_rows > 0 && valid) {  // routed segments: rows past the sender's count are padding
     const int64_t sg = q / P.seg_rows;
     valid = q - sg * P.seg_rows < P.seg_count[sg];
   }
   const int64_t qi = valid ? q : 0;
-  GroupScratch<G, S>& sm = scratch[gib];
   const DevTrie& T = P.T;
 
   const dgds_spec_args a = P.args[qi * P.args_stride];
@@ -626,7 +628,7 @@ __global__ void __launch_bounds__(B, DGDS_QUERY_OCC * (kBlock / B)) k_query(Quer
   const bool bad_args = a.pattern_lookup_min < 1 || a.pattern_lookup_min > a.pattern_lookup_max ||
                         a.max_spec_tokens < 0 || a.top_k < 1 || a.top_k > G || !(a.min_step_freq >= 0.0) ||
                         a.min_support < 0 || eff_smax > S;
-  if (valid && bad_args && gl == 0 && P.err_flag) atomicExch(P.err_flag, 1);
+  if (valid && bad_args && gl == 0 && P.err_flag) atomicOr(P.err_flag, 1);
 
   const int start = max(0, min(eff_pmax, plen));
   const int nlen = start - a.pattern_lookup_min + 1;
@@ -639,13 +641,11 @@ __global__ void __launch_bounds__(B, DGDS_QUERY_OCC * (kBlock / B)) k_query(Quer
   int32_t pr[8];
 #pragma unroll
   for (int i = 0; i < 8; ++i) pr[i] = (act && fast && i < start) ? row[i] : 0;
-  auto tok_at = [&](int x) -> int32_t {
-    int32_t v = 0;
-#pragma unroll
-    for (int i = 0; i < 8; ++i)
-      if (i == x) v = pr[i];
-    return (act && !fast) ? row[x] : v;
-  };
+  if constexpr (M != 2) {
+    for (int i = gl; i < 8; i += G) sm.a.pat[i] = (act && fast && i < start) ? row[i] : 0;
+    __syncwarp();
+  }
+  auto tok_at = [&](int x) -> int32_t { return (act && !fast) ? row[x] : sm.a.pat[x]; };
   const unsigned long long h0 = root_hash(root);
   auto hash_prefix = [&](int j, int i) {  // content hash of row[j .. j+i)
     unsigned long long h = h0;
@@ -664,6 +664,12 @@ __global__ void __launch_bounds__(B, DGDS_QUERY_OCC * (kBlock / B)) k_query(Quer
   unsigned long long locus_imp = 0;  // nonzero: the locus is a count-1 window (implicit path)
   const uint64_t nbk = T.cap / kBucket;
 
+  if constexpr (M == 2) {  // the locus was found by K2a
+    winner = valid ? cr.winner : -1;
+    locus_cnt = cr.cnt;
+    locus_fc = cr.fc;
+    st_lookups = valid ? cr.lookups : 0;
+  } else {
   // ---------------- phase A ----------------
   // (1) the longest suffix: windows i = gl+1 and gl+1+G, both probes in flight.
   // Its windows are prefixes of row[0..start): hash them once with static indexing.
@@ -876,6 +882,7 @@ __global__ void __launch_bounds__(B, DGDS_QUERY_OCC * (kBlock / B)) k_query(Quer
       }
     }
   }
+  }  // M != 2
   __syncwarp();  // phase-A scratch is dead from here (reused for finals)
 
   long long tB = P.dbg ? clock64() : 0;
@@ -885,6 +892,38 @@ __global__ void __launch_bounds__(B, DGDS_QUERY_OCC * (kBlock / B)) k_query(Quer
 #pragma unroll
   for (int i = 0; i < S; ++i) tok[i] = 0;
   int nb = winner >= 0 ? 1 : 0;
+  if constexpr (M == 1) {
+    const bool cplx = valid && act && winner >= 0 && locus_imp == 0ull;  // the locus is a node: K2b
+    const unsigned cm = __ballot_sync(kFull, cplx && gl == 0);
+    if (cm) {
+      unsigned long long at = 0;
+      if (lane == __ffs(cm) - 1) at = atomicAdd(P.cplx_count, static_cast<unsigned long long>(__popc(cm)));
+      at = __shfl_sync(kFull, at, __ffs(cm) - 1);
+      if (cplx && gl == 0)
+        P.cplx[at + __popc(cm & ((1u << lane) - 1u))] = CplxRec{q, locus_fc, locus_cnt, winner, st_lookups};
+    }
+    if (cplx) valid = false;  // answered (and counted) by K2b
+    // a count-1 locus: one path along its occurrence's continuation (cst.cpp:196-215 with one
+    // child per step, step = 1/1), expanded min(rem + 1, eff_smax) times; it qualifies unless the
+    // query's min_step_freq > 1 or min_support > 1
+    const bool imp = valid && winner >= 0 && locus_imp != 0ull;
+    const int rem = imp ? static_cast<int>(imp_rem(locus_imp)) : 0;
+    const bool qual = !(1.0 < a.min_step_freq) && !(1ll < a.min_support);
+    const int k = (imp && qual && eff_smax > 0) ? min(rem, eff_smax) : 0;
+    if (imp && eff_smax > 0) {
+      st_exp = qual ? min(rem + 1, eff_smax) : 1;
+      st_csec = qual ? k : (rem > 0 ? 1 : 0);
+    }
+    if (gl < k) sm.f.tok[0][gl] = __ldg(T.shist + imp_abs(locus_imp) + 1u + gl);
+    for (int i = gl + G; i < k; i += G) sm.f.tok[0][i] = __ldg(T.shist + imp_abs(locus_imp) + 1u + i);
+    if (k > 0 && gl == 0) {
+      sm.f.len[0] = k;
+      sm.f.score[0] = 1.0;
+      sm.f.sup[0] = 1;
+    }
+    nf = k > 0 ? 1 : 0;  // written directly (a count-1 locus)
+    nb = 0;
+  }
   uint32_t b_fc = locus_fc;
   unsigned long long b_imp = locus_imp;  // nonzero: an implicit path (one continuation token in shist)
   const int locus_len = start - winner;  // depth of the locus (tile-uniform when nb > 0)
@@ -1175,33 +1214,68 @@ __global__ void __launch_bounds__(B, DGDS_QUERY_OCC * (kBlock / B)) k_query(Quer
     o[7] = nf;
   }
   if (P.stats) {
-    // tile leaders' counters -> warp sums (redux) -> one RED per counter per warp into one of
-    // kStatParts partitions: no same-address storm (the last block sums them)
     const int ctoks = tile.sum(gl < nf ? sm.f.len[gl] : 0);
     const bool lead = valid && gl == 0;
-    const uint32_t qbytes = lead ? static_cast<uint32_t>(4ull * plen + 32ull + 32ull * st_lookups + 32ull * st_exp +
-                                                         32ull * st_csec + 4ull * ctoks + 16ull * nf)
-                                 : 0u;
-    uint32_t v[8] = {lead ? 1u : 0u, lead ? static_cast<uint32_t>(plen) : 0u,
-                     lead ? static_cast<uint32_t>(st_lookups) : 0u, lead ? static_cast<uint32_t>(st_exp) : 0u,
-                     lead ? static_cast<uint32_t>(st_csec) : 0u, lead ? static_cast<uint32_t>(nf) : 0u,
-                     lead ? static_cast<uint32_t>(ctoks) : 0u, qbytes};
+    if (lead) {
+      sv[0] += 1u;
+      sv[1] += static_cast<uint32_t>(plen);
+      sv[2] += static_cast<uint32_t>(st_lookups);
+      sv[3] += static_cast<uint32_t>(st_exp);
+      sv[4] += static_cast<uint32_t>(st_csec);
+      sv[5] += static_cast<uint32_t>(nf);
+      sv[6] += static_cast<uint32_t>(ctoks);
+      sv[7] += static_cast<uint32_t>(4ull * plen + 32ull + 32ull * st_lookups + 32ull * st_exp + 32ull * st_csec +
+                                     4ull * ctoks + 16ull * nf);
+    }
+  }
+}
+
+// K2b holds only branching queries and loops over them: 3 blocks of 256 per SM (85 registers)
+// instead of 4 (64), which removes its spills.
+template <int G, int S, int B, int M>
+__global__ void __launch_bounds__(B, (M == 2 ? 3 : DGDS_QUERY_OCC) * (kBlock / B)) k_query(QueryLaunch P) {
+  // Programmatic dependent launch: the blocks may be resident before the previous kernel in
+  // the stream (K1, or K2a for K2b) has finished; nothing is read until it has.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  constexpr int kTiles = B / G;
+  __shared__ GroupScratch<G, S> scratch[kTiles];
+  const int lane = lane_id();
+  const int gib = threadIdx.x / G;
+  uint32_t sv[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  if constexpr (M != 2) {
+    const int64_t q = static_cast<int64_t>(blockIdx.x) * kTiles + gib;
+    query_tile<G, S, B, M>(P, scratch[gib], q, q < P.n, CplxRec{}, sv);  // invalid tiles stay, idle
+  } else {
+    const unsigned long long cnt = __ldcg(P.cplx_count);
+    const int64_t tiles = static_cast<int64_t>(gridDim.x) * kTiles;
+    for (int64_t r = static_cast<int64_t>(blockIdx.x) * kTiles + gib;
+         __any_sync(kFull, r < static_cast<int64_t>(cnt)); r += tiles) {
+      const bool has = r < static_cast<int64_t>(cnt);
+      const CplxRec cr = has ? P.cplx[r] : CplxRec{0, 0, 0, -1, 0};
+      query_tile<G, S, B, M>(P, scratch[gib], has ? cr.q : 0, has, cr, sv);
+      __syncwarp();
+    }
+  }
+  const int64_t nwarps = static_cast<int64_t>(gridDim.x) * (B / kWarp);
+  if (P.stats) {
+    // tile leaders' counters -> warp sums (redux) -> one RED per counter per warp into one of
+    // kStatParts partitions: no same-address storm
 #pragma unroll
-    for (int k = 0; k < 8; ++k) v[k] = __reduce_add_sync(kFull, v[k]);
+    for (int k = 0; k < 8; ++k) sv[k] = __reduce_add_sync(kFull, sv[k]);
     if (lane == 0) {
       const uint32_t part = (blockIdx.x * (B / kWarp) + threadIdx.x / kWarp) & (kStatParts - 1);
 #pragma unroll
       for (int k = 0; k < 8; ++k)
-        if (v[k]) atomicAdd(P.stat_part + part * 8 + k, static_cast<unsigned long long>(v[k]));
+        if (sv[k]) atomicAdd(P.stat_part + part * 8 + k, static_cast<unsigned long long>(sv[k]));
     }
     // The last warp to finish folds the partitions into P.stats (no separate fold launch, and
     // no block barrier holding finished warps' SM slots): the fence orders this warp's counter
-    // atomics before its ticket.
+    // atomics before its ticket. K2a leaves its counters in the partitions for K2b's fold.
     bool last = false;
-    if (lane == 0) {
+    if (M != 1 && lane == 0) {
       __threadfence();
       unsigned long long* ticket = P.stat_part + kStatParts * 8;
-      last = atomicAdd(ticket, 1ull) == static_cast<unsigned long long>(gridDim.x) * (B / kWarp) - 1;
+      last = atomicAdd(ticket, 1ull) == static_cast<unsigned long long>(nwarps) - 1;
     }
     if (__shfl_sync(kFull, last, 0)) {
       __threadfence();
@@ -1213,8 +1287,13 @@ __global__ void __launch_bounds__(B, DGDS_QUERY_OCC * (kBlock / B)) k_query(Quer
       if (lane == 0) P.stat_part[kStatParts * 8] = 0ull;
     }
   }
+  if constexpr (M == 2) {  // the last warp resets the queue for the next batch
+    if (lane == 0 && atomicAdd(P.cplx_count + 1, 1ull) == static_cast<unsigned long long>(nwarps) - 1) {
+      P.cplx_count[0] = 0;
+      P.cplx_count[1] = 0;
+    }
+  }
 }
-
 
 // ---------------------------------------------------------------------------
 // standalone verify (engine.cpp:115-143), one thread per request
@@ -1457,10 +1536,8 @@ __global__ void k_route_gather(int64_t n, const uint32_t* __restrict__ in, int32
   out[t] = in[perm[i] * rw + k];
 }
 
-template <int G, int S, int B>
-cudaError_t launch_query_gsb(const QueryLaunch& L, cudaStream_t st) {
-  const int per_block = B / G;
-  const int64_t blocks = (L.n + per_block - 1) / per_block;
+template <int G, int S, int B, int M>
+cudaError_t launch_query_gsbm(const QueryLaunch& L, cudaStream_t st, int64_t blocks) {
   // launched with programmatic stream serialization: the launch overlaps the previous
   // kernel's tail (k_query waits for its completion in griddepcontrol.wait)
   cudaLaunchConfig_t cfg{};
@@ -1473,7 +1550,31 @@ cudaError_t launch_query_gsb(const QueryLaunch& L, cudaStream_t st) {
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, k_query<G, S, B>, L);
+  return cudaLaunchKernelEx(&cfg, k_query<G, S, B, M>, L);
+}
+
+// K2b's grid: the blocks that fit the GPU at once (it loops over its queue)
+template <int G, int S, int B>
+int64_t resident_blocks() {
+  static const int64_t n = [] {
+    int per_sm = 0, sms = 148, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_query<G, S, B, 2>, B, 0);
+    return static_cast<int64_t>(std::max(1, per_sm)) * sms;
+  }();
+  return n;
+}
+
+template <int G, int S, int B>
+cudaError_t launch_query_gsb(const QueryLaunch& L, cudaStream_t st) {
+  const int per_block = B / G;
+  const int64_t blocks = (L.n + per_block - 1) / per_block;
+  if (!L.cplx || !L.cplx_count) return launch_query_gsbm<G, S, B, 0>(L, st, blocks);
+  cudaError_t e = launch_query_gsbm<G, S, B, 1>(L, st, blocks);
+  if (e != cudaSuccess) return e;
+  // K2b: a grid-stride pass over the queued queries (their number is known only on the device)
+  return launch_query_gsbm<G, S, B, 2>(L, st, std::min<int64_t>(blocks, resident_blocks<G, S, B>()));
 }
 
 // K1 / K2 block sizes: DGDS_APPEND_BLOCK = 32 | 64 | 256, DGDS_QUERY_BLOCK = 32 | 64 | 128 | 256

@@ -65,6 +65,12 @@ int set_error(int code, const std::string& msg);  // dgds_last_error() message (
 constexpr int kMaxSegments = 8;
 constexpr int kStatParts = 64;  // partitions of the query counters (spreads the REDs)  // senders of a segmented query launch (ranks of one node)
 
+struct CplxRec {  // a query whose locus is a node (K2a -> K2b)
+  int64_t q;
+  uint32_t fc, cnt;
+  int32_t winner, lookups;
+};
+
 struct QueryLaunch {
   DevTrie T;
   const uint32_t* root_of;
@@ -118,6 +124,10 @@ struct QueryLaunch {
   const int64_t* pat_end;
   const int64_t* out_off;
   int32_t* seg_out[kMaxSegments];
+  // K2a -> K2b queue of queries whose locus is a node (null: one whole-query kernel), and
+  // [0] its length, [1] K2b's warp ticket; server scratch of n entries, zero between launches
+  CplxRec* cplx;
+  unsigned long long* cplx_count;
 };
 
 // SoA strides for a QueryLaunch whose outputs are [n][k_stride][s_stride] buffers.

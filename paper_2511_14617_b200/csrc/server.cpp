@@ -566,6 +566,8 @@ int dgds_create(const dgds_params* params, dgds_server** out) {
   DGDS_CUDA(cudaMemsetAsync(s->d_err, 0, sizeof(int32_t), s->st));
   s->T.err = s->d_err;
   DGDS_CUDA(cudaMalloc(&s->T.ev_count, 2 * sizeof(unsigned long long)));
+  DGDS_CUDA(cudaMalloc(&s->d_cplx_count, 2 * sizeof(unsigned long long)));
+  DGDS_CUDA(cudaMemsetAsync(s->d_cplx_count, 0, 2 * sizeof(unsigned long long), s->st));
   DGDS_CUDA(cudaMemsetAsync(s->T.ev_count, 0, 2 * sizeof(unsigned long long), s->st));
   s->hist_cap = std::max<uint64_t>(1ull << 20, nodes / 2);  // ~ tokens (entries per token ~ 1-3)
   DGDS_CUDA(cudaMalloc(&s->d_hist, s->hist_cap * sizeof(int32_t)));
@@ -599,6 +601,7 @@ int dgds_destroy(dgds_server* s) {
   cudaFree(s->d_shist);
   cudaFree(s->T.ev);
   cudaFree(s->T.ev_count);
+  cudaFree(s->d_cplx_count);
   cudaFree(s->d_used);
   cudaFree(s->d_root_of);
   cudaFree(s->d_err);
