@@ -38,10 +38,12 @@ DEFAULT_CONFIG = "C2"
 # Measured random 32-B access ceiling of this pool's B200 (tools/chase.cu,
 # profiles/r1_microbench.md): 36.1 G accesses/s = 1155 GB/s of useful sectors.
 RANDOM_CEILING_GBS = 1155.0
-# dram__bytes_read.sum + dram__bytes_write.sum per launch, from one
-# `ncu --set full` capture of the same step (profiles/r1_summary.md).
-QUERY_TRAFFIC = 165623808 + 12307456   # prof_query_r1m (k_query<4,8,64>, timed step)
-APPEND_TRAFFIC = 157086720 + 74619648  # prof_append_r1m (k_append<64>, timed step)
+# dram__bytes_read.sum + dram__bytes_write.sum per launch, from one `ncu --set full` capture of
+# the same command (profiles/r2_summary.md); a capture constant, not measured in this run.
+QUERY_TRAFFIC = {"value": 63527168 + 1750272 + 28469248 + 0, "source": "ncu prof_query_r2c: K2a + K2b (K2b write "
+                 "not captured in the summary; reads only)"}
+APPEND_TRAFFIC = {"value": 24080384 + 1123840 + 4267520 + 256, "source": "ncu prof_append_r2b + prof_walks_r2b: "
+                  "K1 + K1b (k_stage not captured)"}
 CONFIG_NAMES = {
     "C1": "single group 16 x 4K, vocab 32K",
     "C2": "Moonlight-shaped 256 groups x 16 responses <=32K tokens, vocab 163840",
@@ -53,7 +55,7 @@ CONFIG_NAMES = {
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default=DEFAULT_CONFIG, choices=sorted(CONFIG_NAMES))
@@ -62,9 +64,11 @@ def parse():
     ap.add_argument("--top-k", type=int, default=4)
     ap.add_argument("--draft-len", type=int, default=8)
     ap.add_argument("--prefill", type=float, default=0.5)
-    ap.add_argument("--e2e-steps", type=int, default=30)
+    ap.add_argument("--e2e-steps", type=int, default=50)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-groups", type=int, default=32, help="groups in the bounded CPU sample")
+    ap.add_argument("--cpu-groups", type=int, default=0,
+                    help="groups in the bounded CPU sample (0: 8 per host thread, at most all)")
+    ap.add_argument("--no-lines", action="store_true", help="skip the c5_sweep / c3_adaptive / c2_full lines")
     ap.add_argument("--cpu-steps", type=int, default=8)
     ap.add_argument("--seed", type=int, default=1234)
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
@@ -259,6 +263,13 @@ def cpu_model():
     return "unknown"
 
 
+def cpu_sample_groups(args, sched) -> int:
+    """Whole groups in the bounded CPU sample: 8 per host thread (thread-per-shard balance), or
+    --cpu-groups, at most the whole trace."""
+    threads = os.cpu_count() or 1
+    return min(args.cpu_groups or 8 * threads, sched.G)
+
+
 def main_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -272,7 +283,7 @@ def main_reference(args):
     threads = os.cpu_count() or 1
     # step = the same tick as our arm, on a bounded sample of whole groups; queries
     # scale with the sample so the queries:appended-tokens mix matches
-    ng = min(args.cpu_groups, sched.G)
+    ng = cpu_sample_groups(args, sched)
     frac = ng / sched.G
     q = max(1, int(args.queries * frac))
     r = run_reference_cpu(args, sched, ng, args.steps + args.warmup, q, threads)
@@ -455,13 +466,15 @@ def main_b200(args):
     q_ach = q_alg / (prof.query_ms / 1e3) / 1e9 if prof.query_ms > 0 else 0.0
     a_ach = app_alg / (prof.append_ms / 1e3) / 1e9 if prof.append_ms > 0 else 0.0
     dom_q = prof.query_ms >= prof.append_ms
-    roof_q = {"kernel": "k_query<4> (K2+K3)", "bound": "hbm", "achieved": q_ach, "peak": peak, "unit": "GB/s",
-              "frac": q_ach / peak, "frac_random_ceiling": q_ach / RANDOM_CEILING_GBS,
-              "traffic": QUERY_TRAFFIC, "alg_bytes_per_launch": q_alg / K,
+    roof_q = {"kernel": "query: k_query K2a + K2b (+K3 fused)", "bound": "hbm", "achieved": q_ach, "peak": peak,
+              "unit": "GB/s", "frac": q_ach / peak, "frac_random_ceiling": q_ach / RANDOM_CEILING_GBS,
+              "traffic": QUERY_TRAFFIC["value"], "traffic_source": QUERY_TRAFFIC["source"],
+              "alg_bytes_per_launch": q_alg / K,
               "avg_launch_ms": prof.query_ms / max(1, prof.query_launches), "peak_kind": peak_kind}
-    roof_a = {"kernel": "k_append (K1)", "bound": "hbm", "achieved": a_ach, "peak": peak, "unit": "GB/s",
-              "frac": a_ach / peak, "frac_random_ceiling": a_ach / RANDOM_CEILING_GBS,
-              "traffic": APPEND_TRAFFIC, "alg_bytes_per_launch": app_alg / K,
+    roof_a = {"kernel": "append: k_stage + k_append (K1) + k_walks (K1b)", "bound": "hbm", "achieved": a_ach,
+              "peak": peak, "unit": "GB/s", "frac": a_ach / peak, "frac_random_ceiling": a_ach / RANDOM_CEILING_GBS,
+              "traffic": APPEND_TRAFFIC["value"], "traffic_source": APPEND_TRAFFIC["source"],
+              "alg_bytes_per_launch": app_alg / K,
               "avg_launch_ms": prof.append_ms / max(1, prof.append_launches), "peak_kind": peak_kind}
     nodes = srv.node_count()
     entries = srv.entry_count()
@@ -585,7 +598,7 @@ def main_b200(args):
     cpu = None
     if not args.no_cpu_baseline:
         try:
-            ng = min(args.cpu_groups, sched.G)
+            ng = cpu_sample_groups(args, sched)
             qn = max(1, int(Q * ng / sched.G))
             threads = os.cpu_count() or 1
             r = run_reference_cpu(args, sched, ng, args.cpu_steps, qn, threads)
@@ -622,8 +635,21 @@ def main_b200(args):
         "wall_ms_per_step": 1e3 * (w1 - w0) / K,
         "clocks": clk.summary(),
     }
-    print(json.dumps(line))
     srv.close()
+    # ---- extra lines: engine-shaped C5 sweep on C4, C3 with adaptive draft length, C2 full index ----
+    if not args.no_lines:
+        import bench_lines
+        torch.cuda.synchronize()
+        gc.collect()
+        for key, fn in (("c5_sweep", bench_lines.c5_sweep), ("c3_adaptive", bench_lines.c3_adaptive),
+                        ("c2_full", bench_lines.c2_full)):
+            try:
+                line[key] = fn(dev, local, peak)
+            except Exception as e:  # an extra line must never break the headline
+                line[key] = {"unavailable": repr(e)}
+            gc.collect()
+            torch.cuda.empty_cache()
+    print(json.dumps(line))
 
 
 def main():
