@@ -205,6 +205,38 @@ int dgds_speculate_device(dgds_server* s, int64_t n, const int32_t* d_handles, c
                           const int32_t* d_limit, const dgds_verify_out* d_vout, dgds_query_stats* d_stats,
                           void* stream);
 
+/* The draft-budget policy of the engine (AdaptiveSpecPolicy + SpecConfig::sd_enabled,
+ * engine.hpp:28-40). feedback 0 = the reference policy, d = min(cap, budget / n_running)
+ * (engine.cpp:78-85), which has no acceptance feedback (the paper claims one);
+ * feedback 1 = an acceptance-scaled extension: d_next = min(d_reference, ceil(mean accepted) + 1). */
+typedef struct dgds_spec_policy {
+  int32_t sd_enabled;
+  int32_t adaptive;
+  int32_t batch_token_budget;
+  int32_t per_request_cap;
+  int32_t multi_path_k;
+  int32_t feedback;
+} dgds_spec_policy;
+
+/* Instance::decode_step's draft path for one step of n running requests, entirely on the device
+ * (engine.cpp:69-143): per request, spec_len = min(d, limit - 1), pat_len = min(pattern_lookup_max,
+ * generated), no query when spec_len <= 0 or pat_len < pattern_lookup_min; top_k =
+ * max(1, multi_path_k); the draft query; verification against the next truth tokens
+ * (d_vout: drafted / accepted / emitted). d is *d_draft_len (device scalar, e.g. the previous step's
+ * d_next_draft_len) or, when that is NULL, draft_len. d_ctx rows (ctx_stride >= max_pattern_len)
+ * hold each request's last min(generated, ctx_stride) tokens, left-aligned. The step's last warp
+ * writes d_next_draft_len (the policy over the requests still running after this step, i.e.
+ * limit - emitted > 0) and d_totals[4] = {still running, drafted, accepted, emitted} (both
+ * optional, device memory). args: lookup bounds and cutoffs (max_spec_tokens / top_k are set per
+ * request). Stream-ordered like dgds_speculate_device. */
+int dgds_decode_step_device(dgds_server* s, int64_t n, const int32_t* d_handles, const int32_t* d_ctx,
+                            int32_t ctx_stride, const int32_t* d_generated, const int32_t* d_limit,
+                            const int32_t* d_truth, int32_t truth_stride, const int32_t* d_truth_left,
+                            const dgds_spec_args* args, const dgds_spec_policy* policy,
+                            const int32_t* d_draft_len, int32_t draft_len, const dgds_candidates* d_out,
+                            const dgds_verify_out* d_vout, int32_t* d_next_draft_len, int64_t* d_totals,
+                            void* stream);
+
 /* dgds_speculate_batch + fused verification (engine.cpp:115-143) in one host call:
  * truth_next[q*truth_stride ..], truth_left[q], limit[q] -> vout (host buffers). */
 int dgds_speculate_verify_batch(dgds_server* s, int64_t n, const int32_t* handles, const uint64_t* pat_offsets,

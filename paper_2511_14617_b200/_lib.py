@@ -67,6 +67,11 @@ class Candidates(C.Structure):
     ]
 
 
+class SpecPolicy(C.Structure):  # dgds_spec_policy (AdaptiveSpecPolicy, engine.hpp:28-33)
+    _fields_ = [("sd_enabled", C.c_int32), ("adaptive", C.c_int32), ("batch_token_budget", C.c_int32),
+                ("per_request_cap", C.c_int32), ("multi_path_k", C.c_int32), ("feedback", C.c_int32)]
+
+
 class VerifyOut(C.Structure):
     _fields_ = [("drafted", C.c_void_p), ("accepted", C.c_void_p), ("emitted", C.c_void_p)]
 
@@ -166,6 +171,9 @@ EXPORTS = {
     "dgds_update_batch_device": (C.c_int, [_P, _I64, _P, _P, _P, _P, _P, _D, _P, _P]),
     "dgds_update_batch_device_strided": (C.c_int, [_P, _I64, _P, _P, _P, _P, _P, _P, _D, _P, _P]),
     "dgds_speculate_batch": (C.c_int, [_P, _I64, _P, _P, _P, _P, _I64, C.POINTER(Candidates)]),
+    "dgds_decode_step_device": (C.c_int, [_P, _I64, _P, _P, _I32, _P, _P, _P, _I32, _P, C.POINTER(SpecArgs),
+                                          C.POINTER(SpecPolicy), _P, _I32, C.POINTER(Candidates),
+                                          C.POINTER(VerifyOut), _P, _P, _P]),
     "dgds_speculate_device": (C.c_int, [_P, _I64, _P, _P, _P, _I32, _P, _I64, _I32, _I32, C.POINTER(Candidates), _P,
                                         _I32,
                                         _P, _P, C.POINTER(VerifyOut), _P, _P]),

@@ -703,6 +703,84 @@ int dgds_speculate_batch(dgds_server* s, int64_t n, const int32_t* handles, cons
                                      nullptr, out, nullptr);
 }
 
+int dgds_decode_step_device(dgds_server* s, int64_t n, const int32_t* d_handles, const int32_t* d_ctx,
+                            int32_t ctx_stride, const int32_t* d_generated, const int32_t* d_limit,
+                            const int32_t* d_truth, int32_t truth_stride, const int32_t* d_truth_left,
+                            const dgds_spec_args* args, const dgds_spec_policy* policy,
+                            const int32_t* d_draft_len, int32_t draft_len, const dgds_candidates* d_out,
+                            const dgds_verify_out* d_vout, int32_t* d_next_draft_len, int64_t* d_totals,
+                            void* stream) {
+  if (!s || !args || !policy || !d_vout || !d_truth || !d_truth_left || !d_limit || !d_generated || !d_ctx ||
+      !d_handles)
+    return fail(DGDS_EINVAL, "null argument");
+  if (n < 0) return fail(DGDS_EINVAL, "negative batch size");
+  if (n == 0) return DGDS_OK;
+  if (int rc = check_args(dgds_spec_args{0, args->pattern_lookup_max, args->pattern_lookup_min, 1,
+                                         args->min_step_freq, args->min_support}))
+    return rc;
+  const int32_t k = std::max(1, policy->multi_path_k);
+  if (k > DGDS_MAX_TOP_K) return fail(DGDS_EUNSUPPORTED, "multi_path_k above DGDS_MAX_TOP_K");
+  if (ctx_stride < s->p.max_pattern_len) return fail(DGDS_EINVAL, "ctx_stride must be >= max_pattern_len");
+  if (d_out && (d_out->k_stride < k || d_out->s_stride < 1)) return fail(DGDS_EBUFFER, "bad output strides");
+  const int32_t max_spec = std::max(1, std::min(std::max(policy->per_request_cap, 1), s->p.max_spec_len));
+  if (truth_stride < max_spec) return fail(DGDS_EINVAL, "truth_stride below the draft length cap");
+  std::lock_guard<std::mutex> lk(s->mu);
+  if (int rc_ = flush_pending(s)) return rc_;
+  DGDS_CUDA(cudaSetDevice(s->p.device));
+  StreamJoin join(s, stream);
+  if (int rc = s->d_step_args.ensure(sizeof(dgds_spec_args))) return rc;
+  DGDS_CUDA(cudaMemcpyAsync(s->d_step_args.p, args, sizeof(dgds_spec_args), cudaMemcpyHostToDevice, join.stream()));
+  dgds::QueryLaunch L{};
+  L.T = s->T;
+  L.root_of = s->d_root_of;
+  L.n_handles = static_cast<int32_t>(s->root_of_cap);
+  L.n = n;
+  L.handles = d_handles;
+  L.pat_len = nullptr;
+  L.patterns = d_ctx;
+  L.pat_stride = ctx_stride;
+  L.args = static_cast<const dgds_spec_args*>(s->d_step_args.p);
+  L.args_stride = 0;
+  if (d_out) {
+    L.k_stride = d_out->k_stride;
+    L.s_stride = d_out->s_stride;
+    dgds::soa_strides(L);
+    L.n_cands = d_out->n_cands;
+    L.lens = d_out->lens;
+    L.scores = d_out->scores;
+    L.supports = d_out->supports;
+    L.tokens = d_out->tokens;
+  } else {
+    L.k_stride = k;
+    L.s_stride = max_spec;
+  }
+  L.in_qstride = 1;
+  L.v_qstride = 1;
+  L.truth = d_truth;
+  L.truth_stride = truth_stride;
+  L.truth_left = d_truth_left;
+  L.limit = d_limit;
+  L.v_drafted = d_vout->drafted;
+  L.v_accepted = d_vout->accepted;
+  L.v_emitted = d_vout->emitted;
+  L.err_flag = s->d_err;
+  L.stat_part = s->d_stat_part;
+  if (int rc = set_cplx(s, L)) return rc;
+  L.engine = 1;
+  L.draft_len = draft_len;
+  L.draft_len_dev = d_draft_len;
+  L.gen = d_generated;
+  L.policy = *policy;
+  L.step_acc = s->d_step_acc;
+  L.next_draft_len = d_next_draft_len;
+  L.step_totals = reinterpret_cast<long long*>(d_totals);
+  {
+    LaunchTimer lt(s, 1, join.stream());
+    DGDS_CUDA(dgds::launch_query(L, k, max_spec, join.stream()));
+  }
+  return DGDS_OK;
+}
+
 int dgds_speculate_device(dgds_server* s, int64_t n, const int32_t* d_handles, const int32_t* d_pat_len,
                           const int32_t* d_patterns, int32_t pat_stride, const dgds_spec_args* d_args,
                           int64_t args_stride, int32_t max_top_k, int32_t max_spec, const dgds_candidates* d_out,

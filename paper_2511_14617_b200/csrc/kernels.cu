@@ -600,7 +600,7 @@ __device__ __forceinline__ unsigned long long leaf_imp(const DevTrie& T, const S
 
 template <int G, int S, int B, int M>
 __device__ __forceinline__ void query_tile(const QueryLaunch& P, GroupScratch<G, S>& sm, const int64_t q, bool valid,
-                                           const CplxRec& cr, uint32_t (&sv)[8]) {
+                                           const CplxRec& cr, uint32_t (&sv)[12]) {
   const int lane = lane_id();
   const int gl = lane % G;
   const Tile<G> tile{lane - gl};
@@ -611,10 +611,26 @@ __device__ __forceinline__ void query_tile(const QueryLaunch& P, GroupScratch<G,
   const int64_t qi = valid ? q : 0;
   const DevTrie& T = P.T;
 
-  const dgds_spec_args a = P.args[qi * P.args_stride];
+  dgds_spec_args a = P.args[qi * P.args_stride];
   const int64_t qin = qi * P.in_qstride;  // per-query scalars: SoA (stride 1) or routed records
   const int32_t hdl = P.handles[qin];
-  const int plen = P.pat_len[qin];
+  int plen = P.pat_len ? P.pat_len[qin] : 0;
+  int row_valid = min(plen, P.pat_stride);  // pattern tokens present in the row (left-aligned)
+  if (P.engine) {
+    // Instance::decode_step's query rules (engine.cpp:88-99): spec_len = min(d, limit - 1),
+    // pat_len = min(pattern_lookup_max, generated); no query when spec_len <= 0 or pat_len <
+    // pattern_lookup_min (or drafting is off); top_k = max(1, multi_path_k). The row holds the
+    // last min(generated, pat_stride) context tokens.
+    const int g = P.gen[qin];
+    const int d = P.draft_len_dev ? __ldcg(P.draft_len_dev) : P.draft_len;
+    const int spec_len = min(d, P.limit[qin] - 1);
+    const int pat_len = min(a.pattern_lookup_max, g);
+    const bool skip = !(P.policy.sd_enabled && d > 0) || spec_len <= 0 || pat_len < a.pattern_lookup_min;
+    a.max_spec_tokens = max(spec_len, 0);
+    a.top_k = max(1, P.policy.multi_path_k);
+    plen = skip ? 0 : pat_len;
+    row_valid = min(g, P.pat_stride);
+  }
   int32_t tleft = 0, lim = 0;
   const bool verify = P.v_emitted != nullptr || (P.rec_words_out > 0 && P.off_v >= 0);
   if (verify) {
@@ -634,7 +650,7 @@ __device__ __forceinline__ void query_tile(const QueryLaunch& P, GroupScratch<G,
   const int nlen = start - a.pattern_lookup_min + 1;
   const bool act = valid && !bad_args && root != 0u && plen > 0 && a.pattern_lookup_min <= eff_pmax && nlen > 0;
   const bool fast = start <= 8;
-  const int row_len = min(plen, P.pat_stride);
+  const int row_len = row_valid;
   // row[0..start) = the last `start` pattern tokens; suffix j (length start-j) starts at row + j
   const int32_t* row = P.pat_end ? P.patterns + (P.pat_end[qi] - start)
                                  : P.patterns + qi * static_cast<int64_t>(P.pat_stride) + (row_len - start);
@@ -1190,6 +1206,12 @@ __device__ __forceinline__ void query_tile(const QueryLaunch& P, GroupScratch<G,
     match = tile.max(match);
     if (valid && gl == 0) {
       const int emitted = min(match + 1, lim);
+      if (P.engine) {  // the step's totals and the requests still running after it
+        sv[8] += lim - emitted > 0 ? 1u : 0u;
+        sv[9] += static_cast<uint32_t>(drafted);
+        sv[10] += static_cast<uint32_t>(emitted - 1);
+        sv[11] += static_cast<uint32_t>(emitted);
+      }
       if (P.rec_words_out > 0) {
         o_v[0] = drafted;
         o_v[1] = emitted - 1;
@@ -1241,7 +1263,7 @@ __global__ void __launch_bounds__(B, (M == 2 ? 3 : DGDS_QUERY_OCC) * (kBlock / B
   __shared__ GroupScratch<G, S> scratch[kTiles];
   const int lane = lane_id();
   const int gib = threadIdx.x / G;
-  uint32_t sv[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  uint32_t sv[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
   if constexpr (M != 2) {
     const int64_t q = static_cast<int64_t>(blockIdx.x) * kTiles + gib;
     query_tile<G, S, B, M>(P, scratch[gib], q, q < P.n, CplxRec{}, sv);  // invalid tiles stay, idle
@@ -1257,20 +1279,23 @@ __global__ void __launch_bounds__(B, (M == 2 ? 3 : DGDS_QUERY_OCC) * (kBlock / B
     }
   }
   const int64_t nwarps = static_cast<int64_t>(gridDim.x) * (B / kWarp);
-  if (P.stats) {
+  if (P.stats || P.engine) {
     // tile leaders' counters -> warp sums (redux) -> one RED per counter per warp into one of
     // kStatParts partitions: no same-address storm
 #pragma unroll
-    for (int k = 0; k < 8; ++k) sv[k] = __reduce_add_sync(kFull, sv[k]);
+    for (int k = 0; k < 12; ++k) sv[k] = __reduce_add_sync(kFull, sv[k]);
     if (lane == 0) {
       const uint32_t part = (blockIdx.x * (B / kWarp) + threadIdx.x / kWarp) & (kStatParts - 1);
 #pragma unroll
       for (int k = 0; k < 8; ++k)
-        if (sv[k]) atomicAdd(P.stat_part + part * 8 + k, static_cast<unsigned long long>(sv[k]));
+        if (P.stats && sv[k]) atomicAdd(P.stat_part + part * 8 + k, static_cast<unsigned long long>(sv[k]));
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (P.engine && sv[8 + k]) atomicAdd(P.step_acc + k, static_cast<unsigned long long>(sv[8 + k]));
     }
-    // The last warp to finish folds the partitions into P.stats (no separate fold launch, and
-    // no block barrier holding finished warps' SM slots): the fence orders this warp's counter
-    // atomics before its ticket. K2a leaves its counters in the partitions for K2b's fold.
+    // The last warp to finish folds the partitions into P.stats and settles the engine step (no
+    // separate launch, and no block barrier holding finished warps' SM slots): the fence orders
+    // this warp's atomics before its ticket. K2a leaves its counters for K2b's fold.
     bool last = false;
     if (M != 1 && lane == 0) {
       __threadfence();
@@ -1279,10 +1304,29 @@ __global__ void __launch_bounds__(B, (M == 2 ? 3 : DGDS_QUERY_OCC) * (kBlock / B
     }
     if (__shfl_sync(kFull, last, 0)) {
       __threadfence();
-      if (lane < 8) {
+      if (P.stats && lane < 8) {
         unsigned long long t = 0;
         for (int p = 0; p < kStatParts; ++p) t += atomicExch(P.stat_part + p * 8 + lane, 0ull);
         reinterpret_cast<unsigned long long*>(P.stats)[lane] += t;
+      }
+      if (P.engine && lane == 0) {
+        unsigned long long tot[4];
+        for (int k = 0; k < 4; ++k) tot[k] = atomicExch(P.step_acc + k, 0ull);
+        // next step's draft length (engine.cpp:78-85) over the requests still running
+        const long long n_next = static_cast<long long>(tot[0]);
+        int d = 0;
+        if (P.policy.sd_enabled && n_next > 0)
+          d = P.policy.adaptive ? static_cast<int>(min(static_cast<long long>(P.policy.per_request_cap),
+                                                       P.policy.batch_token_budget / n_next))
+                                : P.policy.per_request_cap;
+        d = max(d, 0);
+        if (P.policy.feedback == 1 && P.n > 0) {  // extension: acceptance-scaled (not in the reference)
+          const long long mean_acc = (static_cast<long long>(tot[2]) + P.n - 1) / P.n;
+          d = static_cast<int>(min(static_cast<long long>(d), mean_acc + 1));
+        }
+        if (P.next_draft_len) *P.next_draft_len = d;
+        if (P.step_totals)
+          for (int k = 0; k < 4; ++k) P.step_totals[k] = static_cast<long long>(tot[k]);
       }
       if (lane == 0) P.stat_part[kStatParts * 8] = 0ull;
     }

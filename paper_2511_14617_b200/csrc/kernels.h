@@ -128,6 +128,17 @@ struct QueryLaunch {
   // [0] its length, [1] K2b's warp ticket; server scratch of n entries, zero between launches
   CplxRec* cplx;
   unsigned long long* cplx_count;
+  // Engine decode step (dgds_decode_step_device): the query's args, pattern length and the
+  // no-query rule are derived per request on the device from its generated-token count and
+  // limit; the last warp settles the step (totals, next draft length).
+  int32_t engine;
+  int32_t draft_len;              // this step's d when draft_len_dev is null
+  const int32_t* draft_len_dev;   // device scalar d (e.g. the previous step's next_draft_len)
+  const int32_t* gen;             // generated tokens per request
+  dgds_spec_policy policy;
+  unsigned long long* step_acc;   // server scratch [4], zero between launches
+  int32_t* next_draft_len;        // out (device scalar), optional
+  long long* step_totals;         // out [4]: still running, drafted, accepted, emitted; optional
 };
 
 // SoA strides for a QueryLaunch whose outputs are [n][k_stride][s_stride] buffers.

@@ -567,6 +567,8 @@ int dgds_create(const dgds_params* params, dgds_server** out) {
   s->T.err = s->d_err;
   DGDS_CUDA(cudaMalloc(&s->T.ev_count, 2 * sizeof(unsigned long long)));
   DGDS_CUDA(cudaMalloc(&s->d_cplx_count, 2 * sizeof(unsigned long long)));
+  DGDS_CUDA(cudaMalloc(&s->d_step_acc, 4 * sizeof(unsigned long long)));
+  DGDS_CUDA(cudaMemsetAsync(s->d_step_acc, 0, 4 * sizeof(unsigned long long), s->st));
   DGDS_CUDA(cudaMemsetAsync(s->d_cplx_count, 0, 2 * sizeof(unsigned long long), s->st));
   DGDS_CUDA(cudaMemsetAsync(s->T.ev_count, 0, 2 * sizeof(unsigned long long), s->st));
   s->hist_cap = std::max<uint64_t>(1ull << 20, nodes / 2);  // ~ tokens (entries per token ~ 1-3)
@@ -602,6 +604,7 @@ int dgds_destroy(dgds_server* s) {
   cudaFree(s->T.ev);
   cudaFree(s->T.ev_count);
   cudaFree(s->d_cplx_count);
+  cudaFree(s->d_step_acc);
   cudaFree(s->d_used);
   cudaFree(s->d_root_of);
   cudaFree(s->d_err);

@@ -476,6 +476,8 @@ struct dgds_server {
   DevBuf d_count;  // node-count reduction
   DevBuf d_cplx;   // K2a -> K2b queue (dgds::CplxRec per query of a launch)
   unsigned long long* d_cplx_count = nullptr;  // [0] queue length, [1] K2b warp ticket
+  unsigned long long* d_step_acc = nullptr;    // engine decode step accumulators [4]
+  DevBuf d_step_args;                          // dgds_decode_step_device's lookup args
   uint64_t ev_cap = 0;  // K1 conversion-event queue (T.ev)
   unsigned long long* d_stat_part = nullptr;  // [kStatParts][8] query-counter partitions
   std::mutex mu;  // calls on one handle are serialized

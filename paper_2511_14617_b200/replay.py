@@ -179,3 +179,102 @@ def replay(trace: Trace, cfg: ReplayConfig, server: DraftServer = None, record: 
         running = keep
         step += 1
     return step_batch, np.asarray(recs, np.int64).reshape(-1, 4), nq
+
+
+def replay_device(trace: Trace, cfg: ReplayConfig, server: DraftServer = None, feedback: int = 0):
+    """The same staggered replay with each decode step's draft path on the device
+    (dgds_decode_step_device): the draft length d, per-request spec_len / pat_len / no-query rule,
+    the queries and the verification all run in the step's kernels. The host keeps the request
+    states and the append buffer. Returns (step_batch, records, d_sequence, device_next_d, admitted)
+    where device_next_d[i] is the step kernel's d for step i+1 (exact when step i+1 admitted nobody)."""
+    import ctypes as C
+
+    import torch
+
+    from . import _lib
+    args = cfg.args or SpeculationArgs()
+    G, R = trace.cfg.num_groups, trace.cfg.group_size
+    if server is None:
+        server = DraftServer(DgdsParams(append_batch_tokens=cfg.append_batch_tokens, fetch_period=0.0),
+                             expected_nodes=max(1 << 16, int(trace.tokens.size) * 3))
+    client = _ClientBuffer(server, cfg.append_batch_tokens)
+    gids = [group_id(g) for g in range(G)]
+    n = G * R
+    lens = trace.lengths.astype(np.int64)
+    offs = trace.offsets
+    generated = np.zeros(n, np.int64)
+    state = np.zeros(n, np.int8)
+    running: List[int] = []
+    step_batch, recs, ds, dev_next, admitted = [], [], [], [], []
+    now, step, finished = 0.0, 0, 0
+    k = max(1, cfg.multi_path_k)
+    P = server.params
+    S = max(1, min(cfg.per_request_cap, P.max_spec_len))
+    W = P.max_pattern_len
+    dev = torch.device("cuda", server.device)
+    pol = _lib.SpecPolicy(1, 1 if cfg.adaptive else 0, cfg.batch_token_budget, cfg.per_request_cap, k, feedback)
+    sa = _lib.SpecArgs(0, args.pattern_lookup_max, args.pattern_lookup_min, 1, args.min_step_freq, args.min_support)
+    d_next = torch.zeros(1, dtype=torch.int32, device=dev)
+    handles_all = server.group_handles(gids)
+    L = _lib.lib()
+    while finished < n and step < cfg.max_steps:
+        adm = 0
+        for s in range(n):
+            if state[s] == 0 and (s % R) * cfg.stagger == step:
+                state[s] = 1
+                running.append(s)
+                adm += 1
+        if not running:
+            step += 1
+            step_batch.append(0)
+            continue
+        nr = len(running)
+        d = max(min(cfg.per_request_cap, cfg.batch_token_budget // nr) if cfg.adaptive else cfg.per_request_cap, 0)
+        ds.append(d)
+        admitted.append(adm)
+        run = np.asarray(running, np.int64)
+        rem = (lens[run] - generated[run]).astype(np.int32)
+        ctx = np.zeros((nr, W), np.int32)
+        truth = np.zeros((nr, S), np.int32)
+        for i in range(nr):
+            s = int(run[i])
+            g0 = offs[s] + generated[s]
+            c = int(min(generated[s], W))
+            ctx[i, :c] = trace.tokens[g0 - c:g0]
+            m = min(S, int(rem[i]))
+            truth[i, :m] = trace.tokens[g0:g0 + m]
+        t = {name: torch.from_numpy(np.ascontiguousarray(x)).to(dev) for name, x in (
+            ("h", handles_all[run // R].astype(np.int32)), ("ctx", ctx), ("gen", generated[run].astype(np.int32)),
+            ("lim", rem), ("tru", truth), ("tl", rem))}
+        v = torch.zeros((3, nr), dtype=torch.int32, device=dev)
+        vo = _lib.VerifyOut(v[0].data_ptr(), v[1].data_ptr(), v[2].data_ptr())
+        p = lambda x: C.c_void_p(x.data_ptr())  # noqa: E731
+        _lib.check(L.dgds_decode_step_device(server.handle, nr, p(t["h"]), p(t["ctx"]), W, p(t["gen"]), p(t["lim"]),
+                                             p(t["tru"]), S, p(t["tl"]), C.byref(sa), C.byref(pol), None, d, None,
+                                             C.byref(vo), p(d_next), None, C.c_void_p(server.cuda_stream)))
+        torch.cuda.synchronize()
+        drafted, accepted, emitted = (x.cpu().numpy() for x in v)
+        dev_next.append(int(d_next.item()))
+        step_batch.append(nr)
+        for i in range(nr):
+            recs.append((int(run[i] // R) * R + int(run[i] % R), int(drafted[i]), int(accepted[i]), int(emitted[i])))
+        duration = cfg.t_base + cfg.t_tok * float(np.sum(1 + drafted.astype(np.int64)))
+        flushes = []
+        for i in range(nr):
+            s = int(run[i])
+            e = int(emitted[i])
+            g0 = offs[s] + generated[s]
+            client.note(gids[s // R], s % R, trace.tokens[g0:g0 + e], flushes)
+            generated[s] += e
+        client.push(flushes, now)
+        now += duration
+        keep = []
+        for s in running:
+            if generated[s] >= lens[s]:
+                state[s] = 2
+                finished += 1
+            else:
+                keep.append(s)
+        running = keep
+        step += 1
+    return step_batch, np.asarray(recs, np.int64).reshape(-1, 4), ds, dev_next, admitted
