@@ -28,8 +28,9 @@ def nvcc() -> str:
 # Test-only variants: the same sources with a compile-time switch, loaded when the environment
 # names them (DGDS_LIB_VARIANT, see _lib.py). "hash10" truncates the stored content hash to 10
 # bits, so content probes collide constantly and every exact-key fallback and long probe run in
-# K1 / K2 is exercised by the parity tests.
-VARIANTS = {"hash10": ["-DDGDS_TEST_HASH_BITS=10"]}
+# K1 / K2 is exercised by the parity tests. "checked" adds device bounds checks (DGDS_CHECK in
+# trie.cuh) that flag any index outside its arena (compute-sanitizer is unavailable on the pool).
+VARIANTS = {"hash10": ["-DDGDS_TEST_HASH_BITS=10"], "checked": ["-DDGDS_CHECKED"]}
 
 
 def lib_path(variant: str | None = None) -> str:

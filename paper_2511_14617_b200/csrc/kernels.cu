@@ -60,11 +60,13 @@ __global__ void k_stage(DevTrie T, const AppendSeg* __restrict__ segs, int64_t n
   const int64_t nth = static_cast<int64_t>(gridDim.x) * blockDim.x;
   for (int64_t s = gt; s < nseg; s += nth) {
     const AppendSeg g = segs[s];
+    DGDS_CHECK(T, g.stream < T.stream_cap && g.sh_base + g.start + g.n <= T.shist_cap);
     T.sinfo[g.stream] = StreamInfo{g.sh_base, static_cast<uint32_t>(g.start + g.n), g.root};
   }
   int32_t any = 0;
   for (int64_t w = gt / kWarp; w < npieces; w += nth / kWarp) {
     const AppendPiece pc = pieces[w];
+    DGDS_CHECK(T, pc.hist_off + pc.n <= T.hist_cap && pc.sh_off + pc.n <= T.shist_cap);
     for (uint32_t k = lane; k < pc.n; k += kWarp) {
       const int32_t v = tokens[pc.tok_off + k];
       any |= v;
@@ -75,6 +77,7 @@ __global__ void k_stage(DevTrie T, const AppendSeg* __restrict__ segs, int64_t n
   // moved stream extents: the stored tokens into the new extent (disjoint from the pieces above)
   for (int64_t w = gt / kWarp; w < ngrow; w += nth / kWarp) {
     const CopyPiece pc = grow[w];
+    DGDS_CHECK(T, pc.src + pc.len <= T.shist_cap && pc.dst + pc.len <= T.shist_cap);
     for (uint32_t k = lane; k < pc.len; k += kWarp) T.shist[pc.dst + k] = T.shist[pc.src + k];
   }
   if (__any_sync(kFull, any < 0) && lane == 0) atomicOr(T.err, 2);
@@ -168,6 +171,7 @@ __device__ __forceinline__ AddResult add_window(const DevTrie& T, uint32_t h32, 
       return r;
     }
     unsigned long long o0, o1;
+    DGDS_CHECK(T, i < cap && (parent <= cap || parent >= kMinRootId));
     cas128(T.slots + i, key, occ, o0, o1);
     if (o0 == 0ull) {
       r.id = static_cast<uint32_t>(i + 1);
@@ -225,8 +229,11 @@ __device__ void conversion_walk(const DevTrie& T, WalkEvent e, unsigned long lon
       atomicOr(T.err, 16);
       return;
     }
+    DGDS_CHECK(T, cur.stream < T.stream_cap && cur.id >= 1 && cur.id <= T.cap && cur.depth >= 1 &&
+                      cur.depth <= static_cast<uint32_t>(T.depth_cap));
     const StreamInfo si = T.sinfo[cur.stream];
     const uint32_t p = cur.pos + 1;
+    DGDS_CHECK(T, si.base + si.len <= T.shist_cap && (!ron || (rd.stream < T.stream_cap && rd.end <= T.shist_cap)));
     if (p == si.len) T.ov[static_cast<uint64_t>(cur.stream) * kWarp + cur.depth - 1] = cur.id;
     if (ron && rd.abs + 1u >= rd.end) {  // the rider's stream ends at this window
       T.ov[static_cast<uint64_t>(rd.stream) * kWarp + cur.depth - 1] = cur.id;
@@ -311,6 +318,7 @@ __global__ void __launch_bounds__(B, DGDS_APPEND_OCC * (kBlock / B))
       unsigned long long at = 0;
       if (lane == __ffs(m) - 1) at = atomicAdd(T.ev_count, static_cast<unsigned long long>(__popc(m)));
       at = __shfl_sync(kFull, at, __ffs(m) - 1);
+      DGDS_CHECK(T, at + __popc(m) <= T.ev_cap);
       if (ev) T.ev[at + __popc(m & ((1u << lane) - 1u))] = WalkEvent{eh, eid, edepth, es, ep};
     }
   };
@@ -321,6 +329,7 @@ __global__ void __launch_bounds__(B, DGDS_APPEND_OCC * (kBlock / B))
     const AppendSeg g = segs[sg];
     const uint64_t len0 = g.start;
     const uint32_t stream = g.stream;
+    DGDS_CHECK(T, stream < T.stream_cap && g.sh_base + g.start + g.n <= T.shist_cap);
     uint32_t* act_row = T.active + static_cast<uint64_t>(stream) * kWarp;
     uint32_t* ov_row = T.ov + static_cast<uint64_t>(stream) * kWarp;
     const int32_t* ext = T.shist + g.sh_base;
@@ -367,6 +376,7 @@ __global__ void __launch_bounds__(B, DGDS_APPEND_OCC * (kBlock / B))
         prd.abs = __shfl_up_sync(kFull, rd.abs, 1);
         prd.end = __shfl_up_sync(kFull, rd.end, 1);
         const uint32_t parent = lane == 0 ? g.root : pm;
+        DGDS_CHECK(T, lane == 0 || pm <= T.cap);
         const bool act = lane < newsize && parent != 0u;
         pron = pron && act && lane > 0;
         // the parent's rider: same next token = same window (counted twice); otherwise, or at
@@ -565,6 +575,7 @@ __device__ __forceinline__ uint32_t imp_rem(unsigned long long v) { return stati
 __device__ __forceinline__ uint32_t imp_abs(unsigned long long v) { return static_cast<uint32_t>(v); }
 // the implicit continuation below leaf r (a window of `depth` tokens)
 __device__ __forceinline__ StreamInfo load_sinfo(const DevTrie& T, uint32_t stream) {
+  DGDS_CHECK(T, stream < T.stream_cap);
   unsigned long long a, b;
   asm("ld.global.nc.v2.u64 {%0,%1}, [%2];" : "=l"(a), "=l"(b) : "l"(T.sinfo + stream));
   return StreamInfo{a, static_cast<uint32_t>(b), static_cast<uint32_t>(b >> 32)};
@@ -1019,10 +1030,12 @@ __device__ __forceinline__ void query_tile(const QueryLaunch& P, GroupScratch<G,
       const bool have = c != 0u || impc;
       unsigned long long cimp = 0;
       if (c != 0u) {
+        DGDS_CHECK(T, c <= T.cap);
         r = load_slot_nc(T.slots + (c - 1));
         if (r.count == 0u) cimp = raw_imp(r);  // a leaf: implicit below it (resolved if it is kept)
       } else if (impc) {
         const uint32_t at = imp_abs(b_imp) + 1u;
+        DGDS_CHECK(T, at < T.shist_cap);
         r.token = __ldg(T.shist + at);
         r.count = 0u;
         r.first_child = 0u;

@@ -80,6 +80,7 @@ int compact_history(dgds_server* s) {
   s->d_hist = nb;
   s->T.hist = nb;
   s->hist_cap = cap;
+  s->T.hist_cap = cap;
   s->hist_used = live;
   s->dead_hist_tokens = 0;
   return DGDS_OK;
@@ -120,6 +121,7 @@ int compact_streams(dgds_server* s) {
   s->d_shist = nb;
   s->T.shist = nb;
   s->shist_cap = cap;
+  s->T.shist_cap = cap;
   s->shist_used = live;
   s->dead_shist_tokens = 0;
   return DGDS_OK;

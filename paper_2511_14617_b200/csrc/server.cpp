@@ -66,6 +66,7 @@ int grow_streams(dgds_server* s, uint64_t nc) {
   s->T.ov = no;
   s->T.sinfo = ni;
   s->stream_cap = nc;
+  s->T.stream_cap = nc;
   return DGDS_OK;
 }
 
@@ -217,6 +218,7 @@ int ensure_events(dgds_server* s, uint64_t worst_new) {
   cudaFree(s->T.ev);
   s->T.ev = nb;
   s->ev_cap = nc;
+  s->T.ev_cap = nc;
   return DGDS_OK;
 }
 
@@ -268,6 +270,7 @@ int ensure_hist(dgds_server* s) {
   }
   s->d_hist = nb;
   s->hist_cap = nc;
+  s->T.hist_cap = nc;
   s->T.hist = nb;
   return DGDS_OK;
 }
@@ -288,6 +291,7 @@ int ensure_shist(dgds_server* s) {
   }
   s->d_shist = nb;
   s->shist_cap = nc;
+  s->T.shist_cap = nc;
   s->T.shist = nb;
   return DGDS_OK;
 }
@@ -575,6 +579,8 @@ int dgds_create(const dgds_params* params, dgds_server** out) {
   DGDS_CUDA(cudaMalloc(&s->d_hist, s->hist_cap * sizeof(int32_t)));
   s->T.hist = s->d_hist;
   s->shist_cap = s->hist_cap * 2;  // extents: up to 2x their streams' lengths
+  s->T.hist_cap = s->hist_cap;
+  s->T.shist_cap = s->shist_cap;
   DGDS_CUDA(cudaMalloc(&s->d_shist, s->shist_cap * sizeof(int32_t)));
   s->T.shist = s->d_shist;
   // [kStatParts][8] counter partitions + the ticket of k_query's last-block fold

@@ -97,8 +97,23 @@ struct DevTrie {
   int32_t* err;              // device error flags (bit 1: negative token in a device-path batch)
   WalkEvent* ev;             // conversion events of the batch being appended (capacity: its window count)
   unsigned long long* ev_count;  // [0] events queued, [1] k_walks block ticket
+  // capacities, for the bounds checks of the test-only "checked" build (DGDS_CHECK)
+  uint64_t stream_cap, shist_cap, hist_cap, ev_cap;
   unsigned long long* dbg;   // optional (debug): per-warp [start, end] globaltimer of K1
 };
+
+// Test-only bounds checks (build variant "checked", -DDGDS_CHECKED): a violated invariant sets err
+// bit 5 (dgds_device_error), so a parity run under that build also proves every index in range.
+#ifdef DGDS_CHECKED
+#define DGDS_CHECK(T, cond)                          \
+  do {                                               \
+    if (!(cond)) atomicOr((T).err, 32);              \
+  } while (0)
+#else
+#define DGDS_CHECK(T, cond) \
+  do {                      \
+  } while (0)
+#endif
 
 __host__ __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
   x += 0x9E3779B97F4A7C15ull;

@@ -13,6 +13,7 @@ Every call runs on the GPU through libdgds_b200.so; there is no CPU path.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass, field
 from typing import Iterable, List, Optional, Sequence
 
@@ -142,8 +143,15 @@ class DraftServer:
 
     def close(self):
         if getattr(self, "_h", None) is not None and self._h.value:
+            flags = 0
+            if os.environ.get("DGDS_ASSERT_CLEAN"):  # test runs: device error flags must stay clear
+                out = C.c_int32()
+                check(lib().dgds_device_error(self._h, C.byref(out)))
+                flags = out.value
             lib().dgds_destroy(self._h)
             self._h = None
+            if flags:
+                raise RuntimeError("device error flags 0x%x at close (dgds_device_error)" % flags)
 
     def __del__(self):
         try:
