@@ -78,7 +78,18 @@ __global__ void k_stage(DevTrie T, const AppendSeg* __restrict__ segs, int64_t n
   for (int64_t w = gt / kWarp; w < ngrow; w += nth / kWarp) {
     const CopyPiece pc = grow[w];
     DGDS_CHECK(T, pc.src + pc.len <= T.shist_cap && pc.dst + pc.len <= T.shist_cap);
-    for (uint32_t k = lane; k < pc.len; k += kWarp) T.shist[pc.dst + k] = T.shist[pc.src + k];
+    int32_t v[4];  // <= 128 tokens: all loads in flight before the stores
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint32_t k = lane + u * kWarp;
+      v[u] = k < pc.len ? T.shist[pc.src + k] : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint32_t k = lane + u * kWarp;
+      if (k < pc.len) T.shist[pc.dst + k] = v[u];
+    }
+    for (uint32_t k = lane + 4 * kWarp; k < pc.len; k += kWarp) T.shist[pc.dst + k] = T.shist[pc.src + k];
   }
   if (__any_sync(kFull, any < 0) && lane == 0) atomicOr(T.err, 2);
 }
@@ -224,7 +235,8 @@ __device__ void conversion_walk(const DevTrie& T, WalkEvent e, unsigned long lon
   bool ron = false;
   Rider rd{};
   const uint32_t D = static_cast<uint32_t>(T.depth_cap);
-  for (int guard = 0;; ++guard) {
+  int guard = 0;
+  for (;; ++guard) {
     if (guard > (1 << 16)) {  // defensive: a walk is bounded by its conversions
       atomicOr(T.err, 16);
       return;
@@ -277,6 +289,11 @@ __device__ void conversion_walk(const DevTrie& T, WalkEvent e, unsigned long lon
     if (sp == 0) break;
     cur = stk[--sp];
   }
+  if (T.k1_stats) {
+    atomicAdd(T.k1_stats + 5, static_cast<unsigned long long>(guard + 1));
+    atomicMax(T.k1_stats + 6, static_cast<unsigned long long>(guard + 1));
+    atomicAdd(T.k1_stats + 7, 1ull);
+  }
 }
 
 __global__ void k_walks(DevTrie T) {
@@ -316,7 +333,10 @@ __global__ void __launch_bounds__(B, DGDS_APPEND_OCC * (kBlock / B))
     const unsigned m = __ballot_sync(kFull, ev);
     if (m) {
       unsigned long long at = 0;
-      if (lane == __ffs(m) - 1) at = atomicAdd(T.ev_count, static_cast<unsigned long long>(__popc(m)));
+      if (lane == __ffs(m) - 1) {
+        at = atomicAdd(T.ev_count, static_cast<unsigned long long>(__popc(m)));
+        if (T.k1_stats) atomicAdd(T.k1_stats + 4, static_cast<unsigned long long>(__popc(m)));
+      }
       at = __shfl_sync(kFull, at, __ffs(m) - 1);
       DGDS_CHECK(T, at + __popc(m) <= T.ev_cap);
       if (ev) T.ev[at + __popc(m & ((1u << lane) - 1u))] = WalkEvent{eh, eid, edepth, es, ep};
@@ -394,6 +414,12 @@ __global__ void __launch_bounds__(B, DGDS_APPEND_OCC * (kBlock / B))
         if (act) {
           const uint32_t hh = hash32(h);
           r = add_window(T, hh, parent, t, stream, static_cast<uint32_t>(lane) + 1u, static_cast<uint32_t>(len), inc);
+          if (T.k1_stats) {
+            atomicAdd(T.k1_stats + 0, 1ull);
+            if (r.created) atomicAdd(T.k1_stats + 1, 1ull);
+            if (r.converted) atomicAdd(T.k1_stats + 2, 1ull);
+            if (inc == 2u) atomicAdd(T.k1_stats + 3, 1ull);
+          }
           if (link_pending) {  // {h32, next_sibling} of the entry created at the previous token
             store_link(T.slots + link_slot, link_h, link_prev);
             link_pending = false;

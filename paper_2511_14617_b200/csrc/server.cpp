@@ -433,8 +433,8 @@ int plan_updates(dgds_server* s, int64_t n, const int32_t* handles, const int32_
       if (sr.stored > sr.sh_cap) {
         const uint64_t nc = (std::max<uint64_t>({sr.stored, sr.sh_cap * 2, 64}) + 7) / 8 * 8;
         const uint64_t nb = shist_at.fetch_add(nc, std::memory_order_relaxed);
-        for (uint64_t c = 0; c < sg.start; c += 512)  // 512-token chunks: one warp each in k_stage
-          P.grow.push_back(dgds::CopyPiece{sr.sh_base + c, nb + c, static_cast<uint32_t>(std::min<uint64_t>(512, sg.start - c)), 0});
+        for (uint64_t c = 0; c < sg.start; c += 128)  // 128-token chunks: one warp each, one pass, in k_stage
+          P.grow.push_back(dgds::CopyPiece{sr.sh_base + c, nb + c, static_cast<uint32_t>(std::min<uint64_t>(128, sg.start - c)), 0});
         shist_dead.fetch_add(sr.sh_cap, std::memory_order_relaxed);
         sr.sh_base = nb;
         sr.sh_cap = nc;
@@ -572,6 +572,10 @@ int dgds_create(const dgds_params* params, dgds_server** out) {
   DGDS_CUDA(cudaMalloc(&s->T.ev_count, 2 * sizeof(unsigned long long)));
   DGDS_CUDA(cudaMalloc(&s->d_cplx_count, 2 * sizeof(unsigned long long)));
   DGDS_CUDA(cudaMalloc(&s->d_step_acc, 4 * sizeof(unsigned long long)));
+  if (std::getenv("DGDS_K1_STATS")) {  // debug: append-path counters, read with dgds_debug_dump(6)
+    DGDS_CUDA(cudaMalloc(&s->T.k1_stats, 8 * sizeof(unsigned long long)));
+    DGDS_CUDA(cudaMemsetAsync(s->T.k1_stats, 0, 8 * sizeof(unsigned long long), s->st));
+  }
   DGDS_CUDA(cudaMemsetAsync(s->d_step_acc, 0, 4 * sizeof(unsigned long long), s->st));
   DGDS_CUDA(cudaMemsetAsync(s->d_cplx_count, 0, 2 * sizeof(unsigned long long), s->st));
   DGDS_CUDA(cudaMemsetAsync(s->T.ev_count, 0, 2 * sizeof(unsigned long long), s->st));
@@ -611,6 +615,7 @@ int dgds_destroy(dgds_server* s) {
   cudaFree(s->T.ev_count);
   cudaFree(s->d_cplx_count);
   cudaFree(s->d_step_acc);
+  if (s->T.k1_stats) cudaFree(s->T.k1_stats);
   cudaFree(s->d_used);
   cudaFree(s->d_root_of);
   cudaFree(s->d_err);
@@ -1360,6 +1365,7 @@ extern "C" int dgds_debug_dump(dgds_server* s, int32_t which, void* out, uint64_
     case 3: src = s->T.ov; have = s->stream_cap * dgds::kWarp * 4; break;
     case 4: src = s->d_shist; have = s->shist_cap * 4; break;
     case 5: src = s->T.ev; have = s->ev_cap * sizeof(dgds::WalkEvent); break;
+    case 6: src = s->T.k1_stats; have = s->T.k1_stats ? 8 * sizeof(unsigned long long) : 0; break;
     default: return fail(DGDS_EINVAL, "bad dump selector");
   }
   DGDS_CUDA(cudaMemcpy(out, src, std::min(bytes, have), cudaMemcpyDeviceToHost));

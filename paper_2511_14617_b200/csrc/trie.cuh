@@ -100,6 +100,9 @@ struct DevTrie {
   // capacities, for the bounds checks of the test-only "checked" build (DGDS_CHECK)
   uint64_t stream_cap, shist_cap, hist_cap, ev_cap;
   unsigned long long* dbg;   // optional (debug): per-warp [start, end] globaltimer of K1
+  // optional (debug, DGDS_K1_STATS): [0] K1 claims, [1] K1 leaves created, [2] K1 conversions,
+  // [3] K1 rider matches, [4] events queued, [5] walk steps, [6] longest walk (steps), [7] walks
+  unsigned long long* k1_stats;
 };
 
 // Test-only bounds checks (build variant "checked", -DDGDS_CHECKED): a violated invariant sets err
