@@ -431,28 +431,6 @@ int dgds_route_pack_padded(int64_t n, int32_t world, const int32_t* d_owner, con
 int dgds_route_unpack(int64_t n, const uint32_t* d_in, int32_t rec_words, const int64_t* d_perm, uint32_t* d_out,
                       void* stream);
 
-/* ---- synthetic grouped-rollout traces (generate_workload, workload.cpp:51-103) ---- */
-typedef struct dgds_workload_cfg {
-  int32_t num_groups;
-  int32_t group_size;
-  int32_t length_family; /* 0 lognormal, 1 pareto (workload.hpp:19-25) */
-  int32_t vocab_size;
-  double location;
-  double scale;
-  double group_correlation;
-  double noise_base;
-  double pattern_similarity;
-  double prompt_mean;
-  double prompt_spread;
-  int32_t max_tokens;
-  int32_t reserved0;
-  uint64_t seed;
-} dgds_workload_cfg;
-
-/* Pass 1 (tokens == NULL): fills lengths[num_groups*group_size] and prompt_lens[num_groups] (may be NULL).
- * Pass 2: also writes all outputs back to back (group-major, request-minor) into tokens. */
-int dgds_generate_workload(const dgds_workload_cfg* cfg, int64_t* lengths, int32_t* prompt_lens, int32_t* tokens);
-
 /* ---- replica sync: GDX1 blobs (cst.cpp:233-329) and DraftServer::fetch_cst (dgds.cpp:53-97) ----
  * Blobs are byte-identical to the reference's: "GDX1", kind (1 delta, 2 full), u16+group id,
  * u64 from, u64 to, u32 count, then delta records {u32 rid, u64 start, u32 len, i32 tokens[len]}

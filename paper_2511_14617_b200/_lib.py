@@ -218,7 +218,6 @@ EXPORTS = {
     "dgds_replies_submit": (C.c_int, [_P, _I64, _P, C.POINTER(RecordLayout), _I32, _I32, _P, C.POINTER(_U64)]),
     "dgds_speculate_records_seg": (C.c_int, [_P, _I32, _I64, _P, _P, C.POINTER(RecordLayout), _P, _I64, _I32, _I32,
                                              C.POINTER(C.c_void_p), _I32, _P, _P]),
-    "dgds_generate_workload": (C.c_int, [C.POINTER(WorkloadCfg), _P, _P, _P]),
     "dgds_px_create": (C.c_int, [_I32, _I32, _I32, _U64, C.POINTER(C.c_void_p), _P]),
     "dgds_px_connect": (C.c_int, [_P, _P]),
     "dgds_px_connect_local": (C.c_int, [C.POINTER(C.c_void_p), _I32]),

@@ -1,7 +1,8 @@
 """Build the native library libdgds_b200.so in-tree (sm_100a only).
 
 nvcc -gencode arch=compute_100a,code=sm_100a -lineinfo -O3 over csrc/*.cu + the
-host C++ (server.cpp, workload.cpp) -> paper_2511_14617_b200/libdgds_b200.so.
+host C++ (server.cpp, host_query.cpp, replica.cpp, wire.cpp) -> paper_2511_14617_b200/libdgds_b200.so.
+The bench/test trace generator is a separate host library (tools/workload, build_workload).
 The built .so is git-ignored but travels to the GPU box with the snapshot.
 """
 from __future__ import annotations
@@ -14,7 +15,16 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libdgds_b200.so")
-SOURCES = ["kernels.cu", "peer.cu", "server.cpp", "host_query.cpp", "replica.cpp", "workload.cpp", "wire.cpp"]
+SOURCES = ["kernels.cu", "peer.cu", "server.cpp", "host_query.cpp", "replica.cpp", "wire.cpp"]
+# the trace generator of the bench / tests: a separate host-only tools library
+WORKLOAD_SRC = os.path.join(HERE, "..", "tools", "workload", "workload_gen.cpp")
+WORKLOAD_LIB = os.path.join(HERE, "..", "tools", "workload", "libdgds_workload.so")
+
+
+def build_workload(force: bool = False) -> str:
+    if force or not os.path.exists(WORKLOAD_LIB) or os.path.getmtime(WORKLOAD_SRC) > os.path.getmtime(WORKLOAD_LIB):
+        subprocess.run(["g++", "-std=c++17", "-O2", "-fPIC", "-shared", "-o", WORKLOAD_LIB, WORKLOAD_SRC], check=True)
+    return WORKLOAD_LIB
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -48,6 +58,7 @@ def _stale(lib: str = LIB) -> bool:
 
 
 def build(force: bool = False, verbose: bool = False, variant: str | None = None) -> str:
+    build_workload(force)
     lib = lib_path(variant)
     if not force and not _stale(lib):
         return lib

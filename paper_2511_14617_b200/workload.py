@@ -1,7 +1,8 @@
 """Synthetic grouped-rollout traces (generate_workload, proj/src/workload.cpp:51-103).
 
-Generated natively (csrc/workload.cpp) so the GPU box can build the exact
-reference inputs without the reference. The config table is BASELINE.md §3.
+Generated natively by a tools library (tools/workload/workload_gen.cpp -> libdgds_workload.so,
+separate from the draft-server library) so the GPU box can build the exact reference inputs
+without the reference. The config table is BASELINE.md §3.
 """
 from __future__ import annotations
 
@@ -10,8 +11,31 @@ from dataclasses import dataclass, asdict
 
 import numpy as np
 
+import os
+
 from . import _lib
-from ._lib import lib
+
+_WL = None
+
+
+def lib():
+    """tools/workload/libdgds_workload.so (built with the library by build.py)."""
+    global _WL
+    if _WL is None:
+        from . import build as _b
+        path = _b.WORKLOAD_LIB
+        if not os.path.exists(path):
+            _b.build_workload()
+        L = C.CDLL(path)
+        L.dgds_generate_workload.restype = C.c_int
+        L.dgds_generate_workload.argtypes = [C.POINTER(_lib.WorkloadCfg), C.c_void_p, C.c_void_p, C.c_void_p]
+        _WL = L
+    return _WL
+
+
+def _check(rc):
+    if rc != 0:
+        raise ValueError("invalid workload configuration")
 
 
 @dataclass(frozen=True)
@@ -84,7 +108,7 @@ def lengths_only(cfg: WorkloadConfig):
     lengths = np.zeros(n, np.int64)
     plens = np.zeros(cfg.num_groups, np.int32)
     c = cfg.c()
-    _lib.check(lib().dgds_generate_workload(C.byref(c), lengths.ctypes.data_as(C.c_void_p),
+    _check(lib().dgds_generate_workload(C.byref(c), lengths.ctypes.data_as(C.c_void_p),
                                             plens.ctypes.data_as(C.c_void_p), None))
     return lengths, plens
 
@@ -93,6 +117,6 @@ def generate_workload(cfg: WorkloadConfig) -> Trace:
     lengths, plens = lengths_only(cfg)
     tokens = np.zeros(int(lengths.sum()), np.int32)
     c = cfg.c()
-    _lib.check(lib().dgds_generate_workload(C.byref(c), lengths.ctypes.data_as(C.c_void_p),
+    _check(lib().dgds_generate_workload(C.byref(c), lengths.ctypes.data_as(C.c_void_p),
                                             plens.ctypes.data_as(C.c_void_p), tokens.ctypes.data_as(C.c_void_p)))
     return Trace(cfg, lengths, plens, tokens)

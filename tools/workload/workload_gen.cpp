@@ -1,4 +1,5 @@
-// workload.cpp — synthetic grouped-rollout traces for the benchmark.
+// workload_gen.cpp — synthetic grouped-rollout traces for the benchmark and the tests (a tools
+// library, not part of the draft server: tools/workload/libdgds_workload.so).
 //
 // Restates generate_workload (proj/src/workload.cpp:51-103) and the
 // self-contained splitmix64 Rng it draws from (proj/include/rollsim/detail/
@@ -15,7 +16,7 @@
 #include <string>
 #include <vector>
 
-#include "../../include/dgds_b200.h"
+#include "workload_gen.h"
 
 namespace {
 
@@ -82,7 +83,7 @@ bool valid(const dgds_workload_cfg& c) {  // validate_config (workload.cpp:21-39
 
 extern "C" int dgds_generate_workload(const dgds_workload_cfg* cfg, int64_t* lengths, int32_t* prompt_lens,
                                       int32_t* tokens) {
-  if (!cfg || !lengths || !valid(*cfg)) return DGDS_EINVAL;
+  if (!cfg || !lengths || !valid(*cfg)) return -1;
   const dgds_workload_cfg& c = *cfg;
   int64_t out_off = 0;
   std::vector<int> len(c.group_size);
@@ -114,5 +115,5 @@ extern "C" int dgds_generate_workload(const dgds_workload_cfg* cfg, int64_t* len
       out_off += len[i];
     }
   }
-  return DGDS_OK;
+  return 0;
 }
