@@ -3,9 +3,10 @@
 // Mirrors the reference C++ API so a rollout engine can switch by changing the
 // include and namespace:
 //   rollsim::DraftServer      (proj/include/rollsim/dgds.hpp:51-91)   -> dgds_b200::DraftServer
+//   rollsim::DraftTransport / LocalTransport (dgds.hpp:93-116)      -> same names
 //   rollsim::DraftClient      (dgds.hpp:128-162)                      -> dgds_b200::DraftClient
-//     fetch_period == 0: always-fresh answers from the server; fetch_period > 0:
-//     periodic fetch_cst into GPU-resident replicas (GDX1 blobs, cst.cpp:233-329)
+//     DraftClient(DraftTransport&, DgdsParams) as in the reference; replicas of the queried /
+//     active groups are GPU-resident (GDX1 blobs, cst.cpp:233-329)
 //   rollsim::SpeculationSource (engine.hpp:67-74, never implemented
 //                               in the reference)                    -> dgds_b200::GpuSpeculationSource
 //   SpeculationArgs / DraftCandidate / UpdateReply / DgdsParams / SpecQuery
@@ -330,27 +331,70 @@ class DraftServer {
   std::unordered_map<std::string, std::int32_t> handles_;
 };
 
-// DraftClient (dgds.hpp:128-162, dgds.cpp:186-297). note_tokens batches appends per
-// (group, request) and flushes at append_batch_tokens with the resync rules of
-// push_stream (dgds.cpp:193-217).
-// - fetch_period == 0 (always fresh): batch_speculate first fetches the queried
-//   groups — lazy expiry and TTL refresh as the reference's fresh mode — and then
-//   answers from the server, which is what a just-synced replica would answer.
-// - fetch_period > 0: replicas of the active groups live in a GPU replica server,
-//   synced by fetch_active() with GDX1 delta/full blobs, and batch_speculate answers
-//   from them (stale between fetches, as in the paper's periodic fetch).
+// Transport seam between DraftClient and the server (dgds.hpp:93-116): in-process calls
+// (LocalTransport) or any other implementation (e.g. the framed wire protocol).
+class DraftTransport {
+ public:
+  virtual ~DraftTransport() = default;
+  virtual UpdateReply update_cst(const std::string& group_id, int request_id, std::uint64_t prev_token_count,
+                                 std::span<const Token> new_tokens, SimTime now) = 0;
+  virtual std::vector<FetchReply> fetch_cst(std::span<const std::string> group_ids,
+                                            std::span<const DraftCacheInfo> infos, SimTime now) = 0;
+  virtual void register_group(const std::string& group_id, double ttl_seconds, SimTime now) = 0;
+};
+
+class LocalTransport final : public DraftTransport {  // dgds.hpp:105-116
+ public:
+  explicit LocalTransport(DraftServer& server) : server_(server) {}
+  UpdateReply update_cst(const std::string& group_id, int request_id, std::uint64_t prev_token_count,
+                         std::span<const Token> new_tokens, SimTime now) override {
+    return server_.update_cst(group_id, request_id, prev_token_count, new_tokens, now);
+  }
+  std::vector<FetchReply> fetch_cst(std::span<const std::string> group_ids, std::span<const DraftCacheInfo> infos,
+                                    SimTime now) override {
+    return server_.fetch_cst(group_ids, infos, now);
+  }
+  void register_group(const std::string& group_id, double ttl_seconds, SimTime now) override {
+    server_.register_group(group_id, ttl_seconds, now);
+  }
+  DraftServer& server() { return server_; }
+
+ private:
+  DraftServer& server_;
+};
+
+// DraftClient (dgds.hpp:128-162, dgds.cpp:186-297) over a DraftTransport. note_tokens batches
+// appends per (group, request) and flushes at append_batch_tokens with the resync rules of
+// push_stream (dgds.cpp:193-217). batch_speculate answers from replicas of the queried groups,
+// kept in a GPU replica server and synced with GDX1 delta / full blobs (cst.cpp:233-329):
+// - fetch_period == 0 (always fresh): the queried groups are fetched first on every call;
+// - fetch_period > 0: fetch_active() syncs the active groups (stale between fetches, as in the
+//   paper's periodic fetch).
+// Over a LocalTransport in fresh mode the just-fetched replica would equal the server's own
+// index, so the server answers directly (same results, no blob round trip).
 class DraftClient {
  public:
-  DraftClient(DraftServer& server, DgdsParams params) : server_(server), params_(params) {
-    if (params_.fetch_period > 0.0) {
+  DraftClient(DraftTransport& transport, DgdsParams params) : transport_(transport), params_(params) {
+    local_ = dynamic_cast<LocalTransport*>(&transport_);
+    if (params_.fetch_period > 0.0 || !local_) {
       DgdsParams rp = params_;
       rp.default_ttl_seconds = 1e300;  // replicas live until dropped or told UnknownGroup
       replica_ = std::make_unique<DraftServer>(rp);
     }
   }
+  // Convenience: a client of a server in this process (owns its LocalTransport).
+  DraftClient(DraftServer& server, DgdsParams params)
+      : own_(std::make_unique<LocalTransport>(server)), transport_(*own_), params_(params) {
+    local_ = own_.get();
+    if (params_.fetch_period > 0.0) {
+      DgdsParams rp = params_;
+      rp.default_ttl_seconds = 1e300;
+      replica_ = std::make_unique<DraftServer>(rp);
+    }
+  }
 
   void register_group(const std::string& group_id, double ttl_seconds, SimTime now) {
-    server_.register_group(group_id, ttl_seconds, now);
+    transport_.register_group(group_id, ttl_seconds, now);
   }
   void note_tokens(const std::string& group_id, int request_id, std::span<const Token> tokens, SimTime now) {
     if (tokens.empty()) return;
@@ -385,32 +429,36 @@ class DraftClient {
     auto it = cached_.find(group_id);
     return it == cached_.end() ? 0 : it->second;
   }
+  const DgdsParams& params() const { return params_; }
 
   std::vector<std::vector<DraftCandidate>> batch_speculate(std::span<const SpecQuery> queries, SimTime now) {
     std::vector<std::vector<DraftCandidate>> out(queries.size());
     if (queries.empty()) return out;
-    if (!replica_) {  // fresh mode: sync (lazy expiry, TTL refresh), then the server answers
+    if (params_.fetch_period <= 0.0) {  // fresh mode: sync the queried groups first (dgds.cpp:277-282)
       std::vector<std::string> ids;
       for (const auto& q : queries) ids.push_back(q.group_id);
       std::sort(ids.begin(), ids.end());
       ids.erase(std::unique(ids.begin(), ids.end()), ids.end());
-      std::vector<DraftCacheInfo> infos;
-      for (const auto& g : ids) infos.push_back(DraftCacheInfo{g, server_.group_version(g)});
-      auto reps = server_.fetch_cst(ids, infos, now);
-      std::vector<SpecQuery> live;
-      std::vector<std::size_t> where;
-      for (std::size_t i = 0; i < queries.size(); ++i) {
-        const auto k = std::lower_bound(ids.begin(), ids.end(), queries[i].group_id) - ids.begin();
-        if (reps[k].kind == FetchKind::UnknownGroup) continue;  // no replica -> empty candidates
-        cached_[queries[i].group_id] = reps[k].version;
-        live.push_back(queries[i]);
-        where.push_back(i);
+      if (local_ && !replica_) {  // the server's own index is what the replica would hold
+        std::vector<DraftCacheInfo> infos;
+        for (const auto& g : ids) infos.push_back(DraftCacheInfo{g, local_->server().group_version(g)});
+        auto reps = local_->fetch_cst(ids, infos, now);  // lazy expiry + TTL refresh, no blob (up to date)
+        std::vector<SpecQuery> live;
+        std::vector<std::size_t> where;
+        for (std::size_t i = 0; i < queries.size(); ++i) {
+          const auto k = std::lower_bound(ids.begin(), ids.end(), queries[i].group_id) - ids.begin();
+          if (reps[k].kind == FetchKind::UnknownGroup) continue;  // no replica -> empty candidates
+          cached_[queries[i].group_id] = reps[k].version;
+          live.push_back(queries[i]);
+          where.push_back(i);
+        }
+        auto got = local_->server().batch_speculate(live);
+        for (std::size_t j = 0; j < where.size(); ++j) out[where[j]] = std::move(got[j]);
+        for (std::size_t k = 0; k < ids.size(); ++k)
+          if (reps[k].kind == FetchKind::UnknownGroup) cached_.erase(ids[k]);
+        return out;
       }
-      auto got = server_.batch_speculate(live);
-      for (std::size_t j = 0; j < where.size(); ++j) out[where[j]] = std::move(got[j]);
-      for (std::size_t k = 0; k < ids.size(); ++k)
-        if (reps[k].kind == FetchKind::UnknownGroup) cached_.erase(ids[k]);
-      return out;
+      fetch_groups(ids, now);
     }
     std::vector<SpecQuery> have;
     std::vector<std::size_t> where;
@@ -433,7 +481,7 @@ class DraftClient {
     if (ids.empty()) return;
     std::vector<DraftCacheInfo> infos;
     for (const auto& g : ids) infos.push_back(DraftCacheInfo{g, cached_version(g)});
-    auto reps = server_.fetch_cst(ids, infos, now);
+    auto reps = transport_.fetch_cst(ids, infos, now);
     for (std::size_t i = 0; i < ids.size(); ++i) {
       FetchReply& r = reps[i];
       switch (r.kind) {
@@ -455,7 +503,7 @@ class DraftClient {
   void push(const std::string& gid, int rid, Pending& ps, SimTime now) {  // push_stream, dgds.cpp:193-208
     while (ps.acked < ps.buf.size()) {
       std::span<const Token> chunk(ps.buf.data() + ps.acked, ps.buf.size() - ps.acked);
-      UpdateReply rep = server_.update_cst(gid, rid, ps.acked, chunk, now);
+      UpdateReply rep = transport_.update_cst(gid, rid, ps.acked, chunk, now);
       if (rep.ok) {
         ps.acked = rep.acked_tokens;
       } else if (rep.acked_tokens > ps.acked && rep.acked_tokens <= ps.buf.size()) {
@@ -467,9 +515,11 @@ class DraftClient {
       }
     }
   }
-  DraftServer& server_;
+  std::unique_ptr<LocalTransport> own_;  // the DraftServer& constructor's transport
+  DraftTransport& transport_;
+  LocalTransport* local_ = nullptr;
   DgdsParams params_;
-  std::unique_ptr<DraftServer> replica_;  // GPU-resident replicas (fetch_period > 0)
+  std::unique_ptr<DraftServer> replica_;  // GPU-resident replicas
   std::map<std::pair<std::string, int>, Pending> pending_;
   std::vector<std::string> active_;
   SimTime last_fetch_ = -1.0;
