@@ -40,10 +40,11 @@ DEFAULT_CONFIG = "C2"
 RANDOM_CEILING_GBS = 1155.0
 # dram__bytes_read.sum + dram__bytes_write.sum per launch, from one `ncu --set full` capture of
 # the same command (profiles/r2_summary.md); a capture constant, not measured in this run.
-QUERY_TRAFFIC = {"value": 63527168 + 1750272 + 28469248 + 0, "source": "ncu prof_query_r2c: K2a + K2b (K2b write "
-                 "not captured in the summary; reads only)"}
-APPEND_TRAFFIC = {"value": 24080384 + 1123840 + 4267520 + 256, "source": "ncu prof_append_r2b + prof_walks_r2b: "
-                  "K1 + K1b (k_stage not captured)"}
+QUERY_TRAFFIC = {"value": 63553536 + 1948672 + 28480768 + 273664,
+                 "source": "capture constant: ncu --set full prof_query_r2e (K2a + K2b, read + write), profiles/r2_summary.md"}
+APPEND_TRAFFIC = {"value": 903936 + 24150272 + 882944 + 4275200 + 512,
+                  "source": "capture constant: ncu --set full prof_append_r2e (k_stage + K1 + K1b, read + write), "
+                            "profiles/r2_summary.md"}
 CONFIG_NAMES = {
     "C1": "single group 16 x 4K, vocab 32K",
     "C2": "Moonlight-shaped 256 groups x 16 responses <=32K tokens, vocab 163840",

@@ -25,11 +25,17 @@ import numpy as np
 REC = 16
 
 
-def build_index(cfg_name, prefill, device, extra_tokens_per_stream=0, seed=1234):
-    """Server + untimed prefill of the first `prefill` of every response (16-token records)."""
+def build_index(cfg_name, prefill, device, extra_tokens_per_stream=0, seed=1234, num_groups=None):
+    """Server + untimed prefill of the first `prefill` of every response (16-token records).
+    num_groups: a larger group set of the same shape (the generator draws each group from its own
+    substream, so the first groups are the config's own)."""
+    import dataclasses
+
     from paper_2511_14617_b200.dgds import DgdsParams, DraftServer
     from paper_2511_14617_b200.workload import CONFIGS, generate_workload, group_id
     cfg = CONFIGS[cfg_name]
+    if num_groups:
+        cfg = dataclasses.replace(cfg, num_groups=num_groups)
     tr = generate_workload(cfg)
     G, R = cfg.num_groups, cfg.group_size
     S = G * R
@@ -183,14 +189,18 @@ def _append_inputs(tr, live, pos, handles, rids, dev):
 
 
 def c5_sweep(dev, device, peak, Bs=(1024, 2048, 4096, 8192, 16384), ticks=40, warmup=5, seed=5):
-    """Engine-shaped ticks on the C4 trace at 50% prefill: B running requests."""
+    """Engine-shaped ticks on the C4-shaped trace at 50% prefill: B running requests. C4 has 8,192
+    streams, so the trace is the C4 shape with 1,024 groups (16,384 streams; its first 512 groups are
+    C4's own) to reach B = 16K."""
     from paper_2511_14617_b200.dgds import SpeculationArgs, args_array
-    ix = build_index("C4", 0.5, device, extra_tokens_per_stream=REC * (ticks + warmup) * len(Bs))
+    ix = build_index("C4", 0.5, device, extra_tokens_per_stream=REC * (ticks + warmup) * 2, num_groups=1024)
     tr, rng = ix["tr"], np.random.default_rng(seed)
     args = args_array([SpeculationArgs(8, 6, 1, 4, 0.25, 1)])
     rows = []
     for B in Bs:
         live_all = np.nonzero(ix["pos"] + REC * (ticks + warmup) <= tr.lengths)[0]
+        if len(live_all) < B:  # short responses: take the longest-remaining ones
+            live_all = np.argsort(ix["pos"] - tr.lengths)[:B]
         run = np.sort(rng.choice(live_all, size=min(B, len(live_all)), replace=False))
         tk = []
         for _ in range(ticks + warmup):
@@ -203,7 +213,8 @@ def c5_sweep(dev, device, peak, Bs=(1024, 2048, 4096, 8192, 16384), ticks=40, wa
         del tk
     entries, nodes = ix["srv"].entry_count(), ix["srv"].node_count()
     ix["srv"].close()
-    return {"workload": "C4 trace (512 groups x 16, <=64K tokens, V 163840) at 50% prefill on ONE GPU; per tick "
+    return {"workload": "C4-shaped trace (1024 groups x 16, <=64K tokens, V 163840; the first 512 groups are C4) at 50% "
+                        "prefill on ONE GPU; per tick "
                         "each of B running requests appends its next 16-token record and issues one query "
                         "(pattern = its own context's last 6 tokens, top-4, draft 8, fused verify)",
             "index_entries": entries, "index_nodes": nodes, "points": rows}
