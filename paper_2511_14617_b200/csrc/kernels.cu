@@ -136,6 +136,7 @@ __global__ void k_stage(DevTrie T, const AppendSeg* __restrict__ segs, int64_t n
 // finished, so no segment of this batch reads ov while a walk writes it.
 
 constexpr uint32_t kNodeMark = 0xFFFFFFFFu;  // occ_pos of an entry known to be a node
+constexpr int kEvChunk = 32;                 // K1 event-queue slots a warp takes per counter atomic
 
 __device__ __forceinline__ void cas128(Slot* s, unsigned long long n0, unsigned long long n1, unsigned long long& o0,
                                        unsigned long long& o1) {
@@ -300,8 +301,10 @@ __global__ void k_walks(DevTrie T) {
   const unsigned long long n = __ldcg(T.ev_count);
   unsigned long long inserted = 0;
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
-    conversion_walk(T, T.ev[i], inserted);
+  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const WalkEvent e = T.ev[i];
+    if (e.id) conversion_walk(T, e, inserted);  // id 0: an unused slot of a warp's chunk
+  }
   const unsigned long long w = __reduce_add_sync(kFull, static_cast<unsigned>(inserted));
   const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / kWarp;
   if (lane_id() == 0 && w) atomicAdd(T.used + ((warp & (kUsedParts - 1)) * 8), w);
@@ -328,18 +331,31 @@ __global__ void __launch_bounds__(B, DGDS_APPEND_OCC * (kBlock / B))
   const int64_t nwarps = static_cast<int64_t>(gridDim.x) * blockDim.x / kWarp;
   const int D = T.depth_cap;
   unsigned long long inserted_total = 0;
-  // warp-collective: queue the lanes' events for K1b with one queue atomic
+  // Warp-collective event queueing for K1b. A warp takes queue slots in chunks of kEvChunk (one
+  // atomic on the shared counter per chunk instead of one per event batch: that counter is a
+  // single L2 address every warp of the launch hits); unused slots of a chunk are marked empty
+  // (id 0). Slots used <= 2 x events + kEvChunk x warps (the host sizes the queue for it).
+  unsigned long long ev_base = 0;
+  int ev_fill = kEvChunk;  // warp-uniform; no chunk yet
+  auto close_chunk = [&]() {
+    if (ev_fill < kEvChunk && ev_fill + lane < kEvChunk) T.ev[ev_base + ev_fill + lane].id = 0u;
+    ev_fill = kEvChunk;
+  };
   auto queue = [&](bool ev, unsigned long long eh, uint32_t eid, uint32_t edepth, uint32_t es, uint32_t ep) {
     const unsigned m = __ballot_sync(kFull, ev);
     if (m) {
-      unsigned long long at = 0;
-      if (lane == __ffs(m) - 1) {
-        at = atomicAdd(T.ev_count, static_cast<unsigned long long>(__popc(m)));
-        if (T.k1_stats) atomicAdd(T.k1_stats + 4, static_cast<unsigned long long>(__popc(m)));
+      const int c = __popc(m);
+      if (ev_fill + c > kEvChunk) {
+        close_chunk();
+        unsigned long long at = 0;
+        if (lane == 0) at = atomicAdd(T.ev_count, static_cast<unsigned long long>(kEvChunk));
+        ev_base = __shfl_sync(kFull, at, 0);
+        ev_fill = 0;
+        DGDS_CHECK(T, ev_base + kEvChunk <= T.ev_cap);
       }
-      at = __shfl_sync(kFull, at, __ffs(m) - 1);
-      DGDS_CHECK(T, at + __popc(m) <= T.ev_cap);
-      if (ev) T.ev[at + __popc(m & ((1u << lane) - 1u))] = WalkEvent{eh, eid, edepth, es, ep};
+      if (lane == 0 && T.k1_stats) atomicAdd(T.k1_stats + 4, static_cast<unsigned long long>(c));
+      if (ev) T.ev[ev_base + ev_fill + __popc(m & ((1u << lane) - 1u))] = WalkEvent{eh, eid, edepth, es, ep};
+      ev_fill += c;
     }
   };
 
@@ -461,6 +477,7 @@ __global__ void __launch_bounds__(B, DGDS_APPEND_OCC * (kBlock / B))
     if (link_pending) store_link(T.slots + link_slot, link_h, link_prev);
     if (lane < D && static_cast<uint64_t>(lane) < len) act_row[lane] = a;
   }
+  close_chunk();
   if (T.dbg && lane == 0 && warp < 65536) {
     unsigned long long t_end;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));

@@ -208,10 +208,12 @@ int rebuild(dgds_server* s, uint64_t new_cap) {
   return read_used(s, &s->used_ub);
 }
 
-// K1's conversion-event queue holds at most one event per window occurrence of the batch.
-int ensure_events(dgds_server* s, uint64_t worst_new) {
-  if (worst_new <= s->ev_cap) return DGDS_OK;
-  const uint64_t nc = std::max<uint64_t>(worst_new, s->ev_cap * 2);
+// K1's conversion-event queue: at most one event per window occurrence of the batch; warps take
+// slots in chunks of 32, so the slots used are <= 2 x events + 32 x warps (kernels.cu, K1 queue).
+int ensure_events(dgds_server* s, uint64_t worst_new, uint64_t nseg) {
+  const uint64_t need = 2 * worst_new + 32 * (nseg + 64);
+  if (need <= s->ev_cap) return DGDS_OK;
+  const uint64_t nc = std::max<uint64_t>(need, s->ev_cap * 2);
   dgds::WalkEvent* nb = nullptr;
   DGDS_CUDA(cudaStreamSynchronize(s->st));  // a launch in flight may still use the old queue
   if (cudaMalloc(&nb, nc * sizeof(dgds::WalkEvent)) != cudaSuccess) return fail(DGDS_ENOMEM, "event queue allocation failed");
@@ -222,9 +224,9 @@ int ensure_events(dgds_server* s, uint64_t worst_new) {
   return DGDS_OK;
 }
 
-int ensure_capacity(dgds_server* s, uint64_t worst_new) {
+int ensure_capacity(dgds_server* s, uint64_t worst_new, uint64_t nseg) {
   if (int rc = flush_pending(s)) return rc;  // a submitted query reads the table as it was
-  if (int rc = ensure_events(s, worst_new)) return rc;
+  if (int rc = ensure_events(s, worst_new, nseg)) return rc;
   const double limit = kMaxLoad * static_cast<double>(s->T.cap);
   if (static_cast<double>(s->used_ub + worst_new) <= limit) return DGDS_OK;
   int rc = read_used(s, &s->used_ub);
@@ -804,7 +806,7 @@ int update_batch_locked(dgds_server* s, int64_t n, const int32_t* handles, const
   if (int rc = plan_updates(s, n, handles, rids, prev, offs, nullptr, now, rep, segs, pieces, grow, &worst)) return rc;
   pc.mark("plan");
   if (segs.empty()) return DGDS_OK;
-  if (int rc = ensure_capacity(s, worst)) return rc;
+  if (int rc = ensure_capacity(s, worst, segs.size())) return rc;
   if (int rc = ensure_hist(s)) return rc;
   if (int rc = ensure_shist(s)) return rc;
   // one pinned staging block -> one H2D copy: segs | pieces | extent moves | tokens
@@ -887,7 +889,7 @@ static int plan_device(dgds_server* s, int64_t n, const int32_t* handles, const 
   if (!plan->logs.empty()) s->log_pending.push_back(plan);  // accepted records, even on a later error
   if (prc) return prc;
   if (plan->segs.empty()) return DGDS_OK;
-  if (int rc = ensure_capacity(s, worst)) return rc;
+  if (int rc = ensure_capacity(s, worst, plan->segs.size())) return rc;
   if (int rc = ensure_hist(s)) return rc;
   if (int rc = ensure_shist(s)) return rc;
   s->used_ub += worst;  // at plan time: a later plan's capacity check must see pending inserts

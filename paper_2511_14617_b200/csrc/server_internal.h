@@ -508,7 +508,7 @@ void materialize_logs(dgds_server* s);
 int check_args(const dgds_spec_args& a);
 int read_used(dgds_server* s, uint64_t* out);
 int rebuild(dgds_server* s, uint64_t new_cap);
-int ensure_capacity(dgds_server* s, uint64_t worst_new);
+int ensure_capacity(dgds_server* s, uint64_t worst_new, uint64_t nseg = 0);
 int ensure_hist(dgds_server* s);
 int ensure_shist(dgds_server* s);
 // replica.cpp

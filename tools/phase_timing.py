@@ -51,3 +51,9 @@ for i, name in enumerate(["phaseA_cyc", "phaseB_cyc", "out_cyc", "depth_it", "ch
     v = d[:, i]
     print(f"{name:12s} mean {v.mean():10.1f} p50 {np.percentile(v, 50):10.1f} p90 {np.percentile(v, 90):10.1f} "
           f"max {v.max()}")
+cx = d[d[:, 3] > 0]  # phase B ran: the branching queries (K2b)
+print("branching queries:", len(cx), "of", len(d))
+for i, name in enumerate(["phaseA_cyc", "phaseB_cyc", "out_cyc", "depth_it", "child_it", "merge_it", "winner", "nf"]):
+    v = cx[:, i]
+    print(f"  {name:12s} mean {v.mean():10.1f} p50 {np.percentile(v, 50):10.1f} p90 {np.percentile(v, 90):10.1f} "
+          f"p99 {np.percentile(v, 99):10.1f} max {v.max()}")
