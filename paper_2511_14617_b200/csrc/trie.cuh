@@ -134,8 +134,11 @@ __device__ __forceinline__ unsigned long long hash_step(unsigned long long h, in
 }
 // Stored 32-bit content hash (never 0). DGDS_TEST_HASH_BITS (test builds only) truncates it so
 // that content probes collide constantly and every exact-key fallback path runs.
+// One xor-shift and one multiply: the rolling hash is linear in the tokens, and the finaliser only
+// has to spread it over 32 bits (keys are exact; a collision costs a probe, never a result).
 __device__ __forceinline__ uint32_t hash32(unsigned long long h) {
-  uint32_t v = static_cast<uint32_t>(splitmix64(h) >> 32);
+  h ^= h >> 32;
+  uint32_t v = static_cast<uint32_t>((h * 0xD6E8FEB86659FD93ull) >> 32);
 #ifdef DGDS_TEST_HASH_BITS
   v &= (1u << DGDS_TEST_HASH_BITS) - 1u;
 #endif
@@ -163,9 +166,14 @@ __device__ __forceinline__ uint64_t window_slot(uint64_t b, int k, uint64_t cap)
   return i < cap ? i : i - cap;
 }
 
-// Home bucket from the stored hash alone (a rebuild re-places entries without their windows).
+// Home bucket from the stored hash alone (a rebuild re-places entries without their windows):
+// fast-range of the 32-bit hash. Test builds that truncate the hash spread it again first.
 __host__ __device__ __forceinline__ uint64_t home_bucket(uint32_t h32, uint64_t nbuckets) {
+#ifdef DGDS_TEST_HASH_BITS
   return (static_cast<uint64_t>(splitmix64(h32) >> 32) * nbuckets) >> 32;
+#else
+  return (static_cast<uint64_t>(h32) * nbuckets) >> 32;
+#endif
 }
 
 // occurrences of a window from its stored counter (see Slot::count)
