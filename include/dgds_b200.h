@@ -431,6 +431,39 @@ int dgds_route_pack_padded(int64_t n, int32_t world, const int32_t* d_owner, con
 int dgds_route_unpack(int64_t n, const uint32_t* d_in, int32_t rec_words, const int64_t* d_perm, uint32_t* d_out,
                       void* stream);
 
+/* ---- N GPUs behind one server (DraftServer's shard routing, dgds.cpp:10-51) ----
+ * One server per device; group g is owned by GPU fnv1a64(g) % n_gpus (shard_of_group). Batch
+ * calls split records / queries by owner (stable: call order per group is kept), run the owners'
+ * batches concurrently (one host thread per GPU) and return replies / results in call order, so
+ * a cluster call equals the same call on one server holding every group. Handles are cluster
+ * handles (dgds_cluster_intern). devices: n_gpus ordinals (NULL = 0..n_gpus-1; repeats allowed,
+ * e.g. several shards on one GPU); params->device is ignored. */
+typedef struct dgds_cluster dgds_cluster;
+int dgds_cluster_create(const dgds_params* params, int32_t n_gpus, const int32_t* devices, dgds_cluster** out);
+int dgds_cluster_destroy(dgds_cluster* c);
+int32_t dgds_cluster_size(dgds_cluster* c);
+dgds_server* dgds_cluster_server(dgds_cluster* c, int32_t gpu); /* member server (NULL if out of range) */
+int dgds_cluster_intern(dgds_cluster* c, const char* group_id, size_t len, int32_t* handle);
+int dgds_cluster_owner(dgds_cluster* c, int32_t handle, int32_t* gpu);
+int dgds_cluster_register_group(dgds_cluster* c, int32_t handle, double ttl_seconds, double now);
+int dgds_cluster_drop_group(dgds_cluster* c, int32_t handle);
+int dgds_cluster_sweep_expired(dgds_cluster* c, double now);
+int dgds_cluster_has_group(dgds_cluster* c, int32_t handle, int32_t* out);
+int dgds_cluster_group_version(dgds_cluster* c, int32_t handle, uint64_t* out);
+int dgds_cluster_stored_tokens(dgds_cluster* c, int32_t handle, int32_t request_id, uint64_t* out);
+int dgds_cluster_shard_group_count(dgds_cluster* c, int32_t shard, uint64_t* out);
+int dgds_cluster_node_count(dgds_cluster* c, uint64_t* out);
+/* dgds_update_batch over the cluster (host buffers). */
+int dgds_cluster_update_batch(dgds_cluster* c, int64_t n, const int32_t* handles, const int32_t* request_ids,
+                              const uint64_t* prev_counts, const uint64_t* tok_offsets, const int32_t* tokens,
+                              double now, dgds_update_reply* replies);
+/* dgds_speculate_verify_batch over the cluster (host buffers; vout and the truth inputs optional). */
+int dgds_cluster_speculate_verify_batch(dgds_cluster* c, int64_t n, const int32_t* handles,
+                                        const uint64_t* pat_offsets, const int32_t* patterns,
+                                        const dgds_spec_args* args, int64_t args_stride, const int32_t* truth_next,
+                                        int32_t truth_stride, const int32_t* truth_left, const int32_t* limit,
+                                        dgds_candidates* out, dgds_verify_out* vout);
+
 /* ---- replica sync: GDX1 blobs (cst.cpp:233-329) and DraftServer::fetch_cst (dgds.cpp:53-97) ----
  * Blobs are byte-identical to the reference's: "GDX1", kind (1 delta, 2 full), u16+group id,
  * u64 from, u64 to, u32 count, then delta records {u32 rid, u64 start, u32 len, i32 tokens[len]}

@@ -299,6 +299,11 @@ class DraftServer {
     detail::check(dgds_has_group(s_, handle(group_id), &r));
     return r != 0;
   }
+  std::uint64_t node_count() {  // the reference's node count over live groups (roots included)
+    std::uint64_t v = 0;
+    detail::check(dgds_node_count(s_, &v));
+    return v;
+  }
   std::uint64_t group_version(const std::string& group_id) {
     std::uint64_t v = 0;
     detail::check(dgds_group_version(s_, handle(group_id), &v));
@@ -328,6 +333,117 @@ class DraftServer {
 
   DgdsParams params_;
   dgds_server* s_ = nullptr;
+  std::unordered_map<std::string, std::int32_t> handles_;
+};
+
+// N GPUs behind one DraftServer API: the reference's shards (dgds.cpp:10-51) as GPUs
+// (dgds_cluster_*). Group g lives on GPU shard_of_group(g, n); batch calls run the GPUs
+// concurrently and keep call order. Drop-in for rollsim::DraftServer's update / speculate /
+// group calls with shard_count = the number of GPUs.
+class ClusterServer {
+ public:
+  ClusterServer(DgdsParams params, std::vector<int> devices) : params_(params) {
+    dgds_params p{};
+    p.shard_count = params.shard_count;
+    p.append_batch_tokens = params.append_batch_tokens;
+    p.fetch_period = params.fetch_period;
+    p.default_ttl_seconds = params.default_ttl_seconds;
+    p.max_pattern_len = params.limits.max_pattern_len;
+    p.max_spec_len = params.limits.max_spec_len;
+    p.expected_nodes = params.expected_nodes;
+    p.expected_streams = params.expected_streams;
+    detail::check(dgds_cluster_create(&p, static_cast<std::int32_t>(devices.size()), devices.data(), &c_));
+  }
+  ~ClusterServer() { dgds_cluster_destroy(c_); }
+  ClusterServer(const ClusterServer&) = delete;
+  ClusterServer& operator=(const ClusterServer&) = delete;
+
+  std::int32_t handle(const std::string& group_id) {
+    auto it = handles_.find(group_id);
+    if (it != handles_.end()) return it->second;
+    std::int32_t h = 0;
+    detail::check(dgds_cluster_intern(c_, group_id.data(), group_id.size(), &h));
+    handles_.emplace(group_id, h);
+    return h;
+  }
+  int owner_gpu(const std::string& group_id) {
+    std::int32_t g = 0;
+    detail::check(dgds_cluster_owner(c_, handle(group_id), &g));
+    return g;
+  }
+  UpdateReply update_cst(const std::string& group_id, int request_id, std::uint64_t prev_token_count,
+                         std::span<const Token> new_tokens, SimTime now) {
+    const std::int32_t h = handle(group_id);
+    const std::uint64_t offs[2] = {0, new_tokens.size()};
+    dgds_update_reply r{};
+    detail::check(dgds_cluster_update_batch(c_, 1, &h, &request_id, &prev_token_count, offs, new_tokens.data(), now,
+                                            &r));
+    return UpdateReply{r.ok != 0, r.version, r.acked_tokens};
+  }
+  void register_group(const std::string& group_id, double ttl_seconds, SimTime now) {
+    detail::check(dgds_cluster_register_group(c_, handle(group_id), ttl_seconds, now));
+  }
+  void drop_group(const std::string& group_id) { detail::check(dgds_cluster_drop_group(c_, handle(group_id))); }
+  void sweep_expired(SimTime now) { detail::check(dgds_cluster_sweep_expired(c_, now)); }
+  bool has_group(const std::string& group_id) {
+    std::int32_t v = 0;
+    detail::check(dgds_cluster_has_group(c_, handle(group_id), &v));
+    return v != 0;
+  }
+  std::uint64_t group_version(const std::string& group_id) {
+    std::uint64_t v = 0;
+    detail::check(dgds_cluster_group_version(c_, handle(group_id), &v));
+    return v;
+  }
+  std::vector<DraftCandidate> speculate(const std::string& group_id, std::span<const Token> pattern,
+                                        const SpeculationArgs& args) {
+    SpecQuery q{group_id, TokenSeq(pattern.begin(), pattern.end()), args};
+    return batch_speculate(std::span<const SpecQuery>(&q, 1))[0];
+  }
+  std::vector<std::vector<DraftCandidate>> batch_speculate(std::span<const SpecQuery> queries) {
+    const std::size_t n = queries.size();
+    std::vector<std::vector<DraftCandidate>> out(n);
+    if (n == 0) return out;
+    std::vector<std::int32_t> hs(n);
+    std::vector<std::uint64_t> offs(n + 1, 0);
+    std::vector<Token> pats;
+    std::vector<dgds_spec_args> args(n);
+    int K = 1, S = 1;
+    for (std::size_t i = 0; i < n; ++i) {
+      hs[i] = handle(queries[i].group_id);
+      pats.insert(pats.end(), queries[i].pattern.begin(), queries[i].pattern.end());
+      offs[i + 1] = pats.size();
+      args[i] = detail::c_args(queries[i].args);
+      K = std::max(K, queries[i].args.top_k);
+      S = std::max(S, std::min(queries[i].args.max_spec_tokens, params_.limits.max_spec_len));
+    }
+    std::vector<std::int32_t> nc(n), lens(n * K), toks(n * K * S);
+    std::vector<double> sc(n * K);
+    std::vector<std::int64_t> sp(n * K);
+    dgds_candidates c{K, S, nc.data(), lens.data(), sc.data(), sp.data(), toks.data()};
+    detail::check(dgds_cluster_speculate_verify_batch(c_, static_cast<std::int64_t>(n), hs.data(), offs.data(),
+                                                      pats.data(), args.data(), 1, nullptr, 0, nullptr, nullptr, &c,
+                                                      nullptr));
+    for (std::size_t i = 0; i < n; ++i)
+      for (int j = 0; j < nc[i]; ++j) {
+        const std::size_t at = i * K + j;
+        DraftCandidate d;
+        d.tokens.assign(toks.begin() + at * S, toks.begin() + at * S + lens[at]);
+        d.score = sc[at];
+        d.support = sp[at];
+        out[i].push_back(std::move(d));
+      }
+    return out;
+  }
+  std::uint64_t node_count() {
+    std::uint64_t v = 0;
+    detail::check(dgds_cluster_node_count(c_, &v));
+    return v;
+  }
+
+ private:
+  DgdsParams params_;
+  dgds_cluster* c_ = nullptr;
   std::unordered_map<std::string, std::int32_t> handles_;
 };
 

@@ -171,6 +171,23 @@ EXPORTS = {
     "dgds_update_batch_device": (C.c_int, [_P, _I64, _P, _P, _P, _P, _P, _D, _P, _P]),
     "dgds_update_batch_device_strided": (C.c_int, [_P, _I64, _P, _P, _P, _P, _P, _P, _D, _P, _P]),
     "dgds_speculate_batch": (C.c_int, [_P, _I64, _P, _P, _P, _P, _I64, C.POINTER(Candidates)]),
+    "dgds_cluster_create": (C.c_int, [_P, C.c_int32, _P, C.POINTER(_P)]),
+    "dgds_cluster_destroy": (C.c_int, [_P]),
+    "dgds_cluster_size": (C.c_int32, [_P]),
+    "dgds_cluster_server": (_P, [_P, C.c_int32]),
+    "dgds_cluster_intern": (C.c_int, [_P, C.c_char_p, C.c_size_t, C.POINTER(C.c_int32)]),
+    "dgds_cluster_owner": (C.c_int, [_P, C.c_int32, C.POINTER(C.c_int32)]),
+    "dgds_cluster_register_group": (C.c_int, [_P, C.c_int32, C.c_double, C.c_double]),
+    "dgds_cluster_drop_group": (C.c_int, [_P, C.c_int32]),
+    "dgds_cluster_sweep_expired": (C.c_int, [_P, C.c_double]),
+    "dgds_cluster_has_group": (C.c_int, [_P, C.c_int32, C.POINTER(C.c_int32)]),
+    "dgds_cluster_group_version": (C.c_int, [_P, C.c_int32, C.POINTER(_U64)]),
+    "dgds_cluster_stored_tokens": (C.c_int, [_P, C.c_int32, C.c_int32, C.POINTER(_U64)]),
+    "dgds_cluster_shard_group_count": (C.c_int, [_P, C.c_int32, C.POINTER(_U64)]),
+    "dgds_cluster_node_count": (C.c_int, [_P, C.POINTER(_U64)]),
+    "dgds_cluster_update_batch": (C.c_int, [_P, _I64, _P, _P, _P, _P, _P, C.c_double, _P]),
+    "dgds_cluster_speculate_verify_batch": (C.c_int, [_P, _I64, _P, _P, _P, _P, _I64, _P, _I32, _P, _P,
+                                                      C.POINTER(Candidates), _P]),
     "dgds_decode_step_device": (C.c_int, [_P, _I64, _P, _P, _I32, _P, _P, _P, _I32, _P, C.POINTER(SpecArgs),
                                           C.POINTER(SpecPolicy), _P, _I32, C.POINTER(Candidates),
                                           C.POINTER(VerifyOut), _P, _P, _P]),

@@ -28,38 +28,54 @@ struct HostResult {
 };
 
 // Stage queries [j0, j1) of chunk b (chunk-relative) into its pinned block: pattern rows are
-// built in cache, then streamed out with non-temporal stores.
+// built in cache, then streamed out with non-temporal stores. With idx, query i of the batch
+// reads row idx[i] of the caller's pattern / truth / limit arrays (a cluster owner's share of
+// a batch, staged without an intermediate gather); handles are always the batch's own.
 // Returns the first query of the range with a bad handle (>= ng) or decreasing offsets, or -1.
 int64_t stage_rows(const QInBlock& b, char* hb, int64_t j0, int64_t j1, int32_t P, int64_t ng, const int32_t* handles,
-                   const uint64_t* pat_offs, const int32_t* patterns, const int32_t* truth, int32_t truth_stride,
-                   const int32_t* truth_left, const int32_t* limit, bool verify) {
+                   const int64_t* idx, const uint64_t* pat_offs, const int32_t* patterns, const int32_t* truth,
+                   int32_t truth_stride, const int32_t* truth_left, const int32_t* limit, bool verify) {
   if (j0 >= j1) return -1;
   int64_t bad = -1;
-  const int64_t q0 = b.q0 + j0;
+  const int64_t q0 = b.q0 + j0, m = j1 - j0;
   int32_t* hl = reinterpret_cast<int32_t*>(hb + b.o_len);
   int32_t* hp = reinterpret_cast<int32_t*>(hb + b.o_pat);
-  thread_local std::vector<int32_t> lens, rows;
-  lens.resize(j1 - j0);
-  rows.assign(static_cast<size_t>(j1 - j0) * P, 0);
+  thread_local std::vector<int32_t> lens, rows, tr, tl, lm;
+  lens.resize(m);
+  rows.assign(static_cast<size_t>(m) * P, 0);
   for (int64_t j = j0; j < j1; ++j) {
-    const int64_t i = b.q0 + j;
+    const int64_t i = b.q0 + j, r = idx ? idx[i] : i;
     const int32_t hd = handles[i];
-    if ((hd < 0 || hd >= ng || pat_offs[i + 1] < pat_offs[i]) && bad < 0) bad = i;
-    const uint64_t L = pat_offs[i + 1] - pat_offs[i];
+    if ((hd < 0 || hd >= ng || pat_offs[r + 1] < pat_offs[r]) && bad < 0) bad = i;
+    const uint64_t L = pat_offs[r + 1] - pat_offs[r];
     lens[j - j0] = static_cast<int32_t>(std::min<uint64_t>(L, 0x7FFFFFFF));
     const uint64_t keep = std::min<uint64_t>(L, static_cast<uint64_t>(P));
-    const int32_t* src = patterns + pat_offs[i + 1] - keep;
+    const int32_t* src = patterns + pat_offs[r + 1] - keep;
     int32_t* dst = rows.data() + (j - j0) * P;
     for (uint64_t k = 0; k < keep; ++k) dst[k] = src[k];
   }
-  nt_copy(hl + j0, lens.data(), (j1 - j0) * 4);
+  nt_copy(hl + j0, lens.data(), m * 4);
   nt_copy(hp + j0 * P, rows.data(), rows.size() * 4);
-  nt_copy(hb + j0 * 4, handles + q0, (j1 - j0) * 4);
+  nt_copy(hb + j0 * 4, handles + q0, m * 4);
   if (verify) {
-    nt_copy(hb + b.o_tr + static_cast<size_t>(j0) * truth_stride * 4, truth + q0 * truth_stride,
-            static_cast<size_t>(j1 - j0) * truth_stride * 4);
-    nt_copy(hb + b.o_tl + j0 * 4, truth_left + q0, (j1 - j0) * 4);
-    nt_copy(hb + b.o_lm + j0 * 4, limit + q0, (j1 - j0) * 4);
+    const int32_t *vtr = truth + q0 * truth_stride, *vtl = truth_left + q0, *vlm = limit + q0;
+    if (idx) {
+      tr.resize(static_cast<size_t>(m) * truth_stride);
+      tl.resize(m);
+      lm.resize(m);
+      for (int64_t j = 0; j < m; ++j) {
+        const int64_t r = idx[q0 + j];
+        std::memcpy(tr.data() + j * truth_stride, truth + r * truth_stride, truth_stride * 4);
+        tl[j] = truth_left[r];
+        lm[j] = limit[r];
+      }
+      vtr = tr.data();
+      vtl = tl.data();
+      vlm = lm.data();
+    }
+    nt_copy(hb + b.o_tr + static_cast<size_t>(j0) * truth_stride * 4, vtr, static_cast<size_t>(m) * truth_stride * 4);
+    nt_copy(hb + b.o_tl + j0 * 4, vtl, m * 4);
+    nt_copy(hb + b.o_lm + j0 * 4, vlm, m * 4);
   }
   _mm_sfence();  // streaming stores globally visible before the copy is issued
   return bad;
@@ -103,13 +119,13 @@ cudaError_t issue_h2d(dgds_server* s) {
 int speculate_submit(dgds_server* s, int64_t n, const int32_t* handles, const uint64_t* pat_offs,
                      const int32_t* patterns, const dgds_spec_args* args, int64_t args_stride, const int32_t* truth,
                      int32_t truth_stride, const int32_t* truth_left, const int32_t* limit, bool verify,
-                     uint64_t* ticket) {
+                     uint64_t* ticket, const int64_t* idx = nullptr) {
   PhaseClock pc("speculate_submit");
   if (int rc = flush_pending(s)) return rc;
   const int64_t nargs = args_stride ? n : 1;
   int32_t max_k = 1, max_s = 1;
   for (int64_t i = 0; i < nargs; ++i) {
-    const dgds_spec_args& a = args[i * args_stride];
+    const dgds_spec_args& a = args[(idx && args_stride ? idx[i] : i) * args_stride];
     if (int rc = check_args(a)) return rc;
     max_k = std::max(max_k, a.top_k);
     max_s = std::max(max_s, std::min(a.max_spec_tokens, s->p.max_spec_len));
@@ -175,7 +191,7 @@ int speculate_submit(dgds_server* s, int64_t n, const int32_t* handles, const ui
     auto* ha = reinterpret_cast<dgds_spec_args*>(h + b.base + b.o_args);
     if (!args_stride) ha[0] = args[0];
     else
-      for (int64_t j = 0; j < b.m; ++j) ha[j] = args[(b.q0 + j) * args_stride];
+      for (int64_t j = 0; j < b.m; ++j) ha[j] = args[(idx ? idx[b.q0 + j] : b.q0 + j) * args_stride];
   }
   pq.n = n;
   pq.nch = nch;
@@ -207,7 +223,7 @@ int speculate_submit(dgds_server* s, int64_t n, const int32_t* handles, const ui
   const int64_t ng = static_cast<int64_t>(s->groups.size());
   pq.left.store(tasks);
   pq.bad.store(INT64_MAX);
-  auto job = [s, h, span, n, per, P, ng, handles, pat_offs, patterns, truth, truth_stride, truth_left, limit,
+  auto job = [s, h, span, n, per, P, ng, handles, idx, pat_offs, patterns, truth, truth_stride, truth_left, limit,
               verify](int t) {
     const int64_t i0 = t * span, i1 = std::min<int64_t>(n, i0 + span);
     int64_t first_bad = INT64_MAX;
@@ -215,7 +231,7 @@ int speculate_submit(dgds_server* s, int64_t n, const int32_t* handles, const ui
       const int c = static_cast<int>(i / per);
       const QInBlock& b = s->pq.blk[c];
       const int64_t e = std::min<int64_t>(i1, b.q0 + b.m);
-      const int64_t bad = stage_rows(b, h + b.base, i - b.q0, e - b.q0, P, ng, handles, pat_offs, patterns, truth,
+      const int64_t bad = stage_rows(b, h + b.base, i - b.q0, e - b.q0, P, ng, handles, idx, pat_offs, patterns, truth,
                                      truth_stride, truth_left, limit, verify);
       if (bad >= 0 && bad < first_bad) first_bad = bad;
       i = e;
@@ -226,10 +242,13 @@ int speculate_submit(dgds_server* s, int64_t n, const int32_t* handles, const ui
       }
     }
     if (s->pq.left.fetch_sub(1) == 1 && s->pq.bad.load() == INT64_MAX) {  // the last stager
+      PhaseClock lpc("stager_launch");
       dgds_server::PendingQuery& q = s->pq;  // (nothing is launched for an invalid batch)
       if (q.h2d_err == cudaSuccess) q.h2d_err = issue_h2d(s);
+      lpc.mark("h2d");
       if (q.h2d_err == cudaSuccess && q.stager_launch) {
         q.launch_rc = launch_batch(s, false);
+        lpc.mark("launch");
         if (q.launch_rc) q.launch_msg = dgds_last_error();
         q.launched = true;
       }
@@ -409,16 +428,37 @@ int speculate_finish(dgds_server* s, uint64_t ticket, HostResult* r) {
 int speculate_host(dgds_server* s, int64_t n, const int32_t* handles, const uint64_t* pat_offs,
                    const int32_t* patterns, const dgds_spec_args* args, int64_t args_stride, const int32_t* truth,
                    int32_t truth_stride, const int32_t* truth_left, const int32_t* limit, bool verify,
-                   HostResult* r) {
+                   HostResult* r, const int64_t* idx = nullptr) {
   uint64_t t = 0;
   if (int rc = speculate_submit(s, n, handles, pat_offs, patterns, args, args_stride, truth, truth_stride,
-                                truth_left, limit, verify, &t))
+                                truth_left, limit, verify, &t, idx))
     return rc;
   PhaseClock pc("speculate_wait");
   return speculate_finish(s, t, r);
 }
 
-static void fill_view(const HostResult& r, dgds_result_view* out) {
+void fill_view(const HostResult& r, dgds_result_view* out);
+
+// dgds_speculate_verify_view over rows idx[0..n) of the caller's arrays (handles: n server
+// handles, one per query): a cluster owner's share of a batch (cluster.cpp).
+int speculate_view_indexed(dgds_server* s, int64_t n, const int64_t* idx, const int32_t* handles,
+                           const uint64_t* pat_offs, const int32_t* patterns, const dgds_spec_args* args,
+                           int64_t args_stride, const int32_t* truth, int32_t truth_stride, const int32_t* truth_left,
+                           const int32_t* limit, dgds_result_view* out) {
+  *out = dgds_result_view{};
+  if (n == 0) return DGDS_OK;
+  std::lock_guard<std::mutex> lk(s->mu);
+  if (int rc = flush_pending(s)) return rc;
+  DGDS_CUDA(cudaSetDevice(s->p.device));
+  HostResult r;
+  if (int rc = speculate_host(s, n, handles, pat_offs, patterns, args, args_stride, truth, truth_stride, truth_left,
+                              limit, truth != nullptr, &r, idx))
+    return rc;
+  fill_view(r, out);
+  return DGDS_OK;
+}
+
+void fill_view(const HostResult& r, dgds_result_view* out) {
   out->n_queries = r.n;
   out->n_cands = r.ncand;
   out->n_tokens = r.ntok;

@@ -5,6 +5,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <sys/resource.h>
 #include <emmintrin.h>
 #include <deque>
 
@@ -60,6 +61,15 @@ constexpr double kTargetLoad = 0.35;  // load right after a rebuild
 constexpr uint32_t kRootCap = 1u << 22;
 constexpr uint64_t kMaxCap = (0xFFFFFFFFull - kRootCap - 2) / 4 * 4;
 
+// Capacity for a growing staging buffer: 2x, and 25% headroom over the request. Batch sizes
+// vary a little from call to call (a cluster splits each batch by owner), and every regrowth
+// costs a cudaFreeHost / cudaFree (device-synchronizing) plus pinning or mapping fresh pages
+// (measured: 30-80 ms per 18 MB pinned block on the 4-GPU box, i.e. 10x a tick).
+inline size_t grown_cap(size_t bytes, size_t cap) {
+  const size_t c = std::max<size_t>(bytes + bytes / 4, cap * 2);
+  return (c + 65535) & ~size_t(65535);
+}
+
 struct PinnedBuf {
   void* p = nullptr;
   size_t cap = 0;
@@ -71,8 +81,9 @@ struct PinnedBuf {
     if (bytes <= cap) return DGDS_OK;
     if (p) cudaFreeHost(p);
     p = nullptr;
-    size_t c = std::max<size_t>(bytes, cap * 2);
+    const size_t c = grown_cap(bytes, cap);
     if (cudaHostAlloc(&p, c, flags) != cudaSuccess) {
+      p = nullptr;
       cap = 0;
       return fail(DGDS_ENOMEM, "cudaHostAlloc failed");
     }
@@ -91,7 +102,7 @@ struct DevBuf {
     if (bytes <= cap) return DGDS_OK;
     if (p) cudaFree(p);
     p = nullptr;
-    size_t c = std::max<size_t>(bytes, cap * 2);
+    const size_t c = grown_cap(bytes, cap);
     if (cudaMalloc(&p, c) != cudaSuccess) {
       cap = 0;
       return fail(DGDS_ENOMEM, "cudaMalloc failed");
@@ -291,26 +302,38 @@ struct GroupRec {
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 // Debug: DGDS_HOST_TIMING=1 prints the host-path phases of each call to stderr.
-struct PhaseClock {
+struct PhaseClock {  // DGDS_HOST_TIMING: per-phase wall time (us) and the thread's minor faults
   bool on;
   const char* name;
   std::chrono::steady_clock::time_point t0, last;
+  long flt0 = 0, flt = 0;
   std::string line;
+  static long faults() {
+    rusage u{};
+    getrusage(RUSAGE_THREAD, &u);
+    return u.ru_minflt;
+  }
   explicit PhaseClock(const char* n) : on(std::getenv("DGDS_HOST_TIMING") != nullptr), name(n) {
-    if (on) t0 = last = std::chrono::steady_clock::now();
+    if (on) {
+      t0 = last = std::chrono::steady_clock::now();
+      flt0 = flt = faults();
+    }
   }
   void mark(const char* phase) {
     if (!on) return;
     auto t = std::chrono::steady_clock::now();
+    const long f = faults();
     line += std::string(" ") + phase + "=" +
             std::to_string(std::chrono::duration<double, std::micro>(t - last).count()).substr(0, 7);
+    if (f != flt) line += "(" + std::to_string(f - flt) + "f)";
     last = t;
+    flt = f;
   }
   ~PhaseClock() {
     if (on)
-      std::fprintf(stderr, "[%s] total=%.1fus%s\n", name,
+      std::fprintf(stderr, "[%s] total=%.1fus faults=%ld%s\n", name,
                    std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count(),
-                   line.c_str());
+                   faults() - flt0, line.c_str());
   }
 };
 
@@ -335,6 +358,10 @@ inline void nt_copy(void* dst, const void* src, size_t n) {
 
 struct dgds_server;
 namespace dgds_host {
+int speculate_view_indexed(dgds_server* s, int64_t n, const int64_t* idx, const int32_t* handles,
+                           const uint64_t* pat_offs, const int32_t* patterns, const dgds_spec_args* args,
+                           int64_t args_stride, const int32_t* truth, int32_t truth_stride, const int32_t* truth_left,
+                           const int32_t* limit, dgds_result_view* out);
 int flush_pending(dgds_server* s);  // launches a submitted query batch; before any later device work
 int launch_batch(dgds_server* s, bool timed);
 // one chunk of a staged host query batch: handles | pat_len | patterns | args | truth | truth_left | limit
@@ -459,6 +486,7 @@ struct dgds_server {
   bool h2d_kernel = false;  // copy-engine H2D (no SMs taken from K1); DGDS_H2D=kernel: a pull kernel
   int h2d_blocks = 148;    // one CTA per SM (measured best); DGDS_H2D_BLOCKS
   std::unique_ptr<WorkerPool> pool;
+  int pool_threads = 0;  // host workers incl. the caller; 0 = host_threads() (a cluster splits the cores)
   uint64_t plans_made = 0, plans_launched = 0;  // two-phase device updates (plan now, launch later)
   std::vector<struct dgds_update_plan*> plan_pool;  // recycled plans: their vectors keep capacity
   // planning scratch, reused across calls (per-call vectors of 16-130 KB were page-faulting)
@@ -469,7 +497,7 @@ struct dgds_server {
     std::vector<uint32_t> cnt, fill;
   } scratch;
   WorkerPool& workers() {
-    if (!pool) pool = std::make_unique<WorkerPool>(host_threads() - 1);
+    if (!pool) pool = std::make_unique<WorkerPool>((pool_threads > 0 ? pool_threads : host_threads()) - 1);
     return *pool;
   }
   int32_t* d_err = nullptr;

@@ -532,3 +532,100 @@ class CandidateBatch:
 
     def to_lists(self) -> List[List[DraftCandidate]]:
         return [self.query(q) for q in range(self.n)]
+
+
+class DraftCluster:
+    """N GPUs behind one draft server (dgds_cluster_*): group g lives on GPU fnv1a64(g) % n, the
+    reference's shard_of_group (dgds.cpp:10-14); batch calls split by owner and run the GPUs
+    concurrently, returning results in call order."""
+
+    def __init__(self, params: Optional[DgdsParams] = None, devices: Sequence[int] = (0,), expected_nodes: int = 0,
+                 expected_streams: int = 0):
+        self.params = params or DgdsParams()
+        p = self.params
+        cp = _lib.Params(p.shard_count, p.append_batch_tokens, p.fetch_period, p.default_ttl_seconds,
+                         p.max_pattern_len, p.max_spec_len, 0, 0, expected_nodes, expected_streams)
+        devs = (C.c_int32 * len(devices))(*devices)
+        h = C.c_void_p()
+        check(lib().dgds_cluster_create(C.byref(cp), len(devices), devs, C.byref(h)))
+        self._h = h
+        self._handles = {}
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            lib().dgds_cluster_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def size(self) -> int:
+        return int(lib().dgds_cluster_size(self._h))
+
+    def group_handles(self, group_ids: Iterable[str]) -> np.ndarray:
+        out = []
+        for g in group_ids:
+            h = self._handles.get(g)
+            if h is None:
+                v = C.c_int32()
+                b = g.encode()
+                check(lib().dgds_cluster_intern(self._h, b, len(b), C.byref(v)))
+                h = self._handles[g] = v.value
+            out.append(h)
+        return np.asarray(out, np.int32)
+
+    def owner(self, group_id: str) -> int:
+        v = C.c_int32()
+        check(lib().dgds_cluster_owner(self._h, int(self.group_handles([group_id])[0]), C.byref(v)))
+        return v.value
+
+    def update_batch(self, group_ids, request_ids, prev_counts, token_lists, now: float) -> List[UpdateReply]:
+        n = len(group_ids)
+        if n == 0:
+            return []
+        handles = self.group_handles(group_ids)
+        toks = [np.asarray(t, dtype=np.int64) for t in token_lists]
+        offs = np.zeros(n + 1, np.uint64)
+        offs[1:] = np.cumsum([len(t) for t in toks])
+        flat = np.concatenate(toks).astype(np.int32) if offs[-1] else np.zeros(0, np.int32)
+        rids = np.ascontiguousarray(request_ids, np.int32)
+        prev = np.ascontiguousarray(prev_counts, np.uint64)
+        rep = np.zeros(n, DraftServer.REPLY_DTYPE)
+        check(lib().dgds_cluster_update_batch(self._h, n, _ptr(handles), _ptr(rids), _ptr(prev), _ptr(offs),
+                                              _ptr(flat), float(now), _ptr(rep)))
+        return [UpdateReply(bool(r["ok"]), int(r["version"]), int(r["acked"])) for r in rep]
+
+    def speculate_batch(self, group_ids, patterns, args) -> List[List[DraftCandidate]]:
+        n = len(group_ids)
+        if n == 0:
+            return []
+        handles = self.group_handles(group_ids)
+        pats = [np.asarray(p, dtype=np.int64) for p in patterns]
+        offs = np.zeros(n + 1, np.uint64)
+        offs[1:] = np.cumsum([len(p) for p in pats])
+        flat = (np.concatenate(pats) if offs[-1] else np.zeros(0, np.int64)).astype(np.int32)
+        if isinstance(args, SpeculationArgs):
+            arr, stride = args_array([args]), 0
+        else:
+            arr, stride = args_array(list(args)), 1
+        a = arr if stride else arr[:1]
+        k = max(1, int(a["top_k"].max()))
+        s = max(1, int(np.minimum(a["max_spec_tokens"], self.params.max_spec_len).max()))
+        out = CandidateBatch(n, k, s)
+        check(lib().dgds_cluster_speculate_verify_batch(self._h, n, _ptr(handles), _ptr(offs), _ptr(flat), _ptr(arr),
+                                                        stride, None, 0, None, None, C.byref(out.c()), None))
+        return out.to_lists()
+
+    def node_count(self) -> int:
+        out = C.c_uint64()
+        check(lib().dgds_cluster_node_count(self._h, C.byref(out)))
+        return int(out.value)
+
+    def group_version(self, group_id: str) -> int:
+        out = C.c_uint64()
+        check(lib().dgds_cluster_group_version(self._h, int(self.group_handles([group_id])[0]), C.byref(out)))
+        return int(out.value)

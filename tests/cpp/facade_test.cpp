@@ -102,6 +102,50 @@ int main() {
   for (int j = 0; j < 2; ++j)
     EXPECT(r2[0][j].tokens == now[0][j].tokens && r2[0][j].score == now[0][j].score &&
            r2[0][j].support == now[0][j].support);
+  // the cluster form (shards as GPUs; here three shards on device 0) answers like one server
+  ClusterServer cl(DgdsParams{}, std::vector<int>{0, 0, 0});
+  DraftServer one;
+  for (int g = 0; g < 6; ++g) {
+    const std::string gid = "k" + std::to_string(g);
+    for (int r = 0; r < 3; ++r) {
+      TokenSeq t{1, 2, 3 + (r + g) % 3, 4, 5 + r};
+      EXPECT(cl.update_cst(gid, r, 0, t, 0.0).version == one.update_cst(gid, r, 0, t, 0.0).version);
+    }
+    EXPECT(cl.owner_gpu(gid) == shard_of_group(gid, 3));
+  }
+  std::vector<SpecQuery> cq;
+  for (int g = 0; g < 6; ++g) cq.push_back({"k" + std::to_string(g), TokenSeq{1, 2}, SpeculationArgs{4, 6, 1, 3}});
+  auto x = cl.batch_speculate(cq);
+  auto y = one.batch_speculate(cq);
+  for (std::size_t i = 0; i < cq.size(); ++i) {
+    EXPECT(x[i].size() == y[i].size());
+    for (std::size_t j = 0; j < x[i].size(); ++j)
+      EXPECT(x[i][j].tokens == y[i][j].tokens && x[i][j].score == y[i][j].score && x[i][j].support == y[i][j].support);
+  }
+  EXPECT(cl.node_count() == one.node_count());
+  // DraftClient over a transport that is not local: GPU replicas synced by blobs
+  struct Fwd final : DraftTransport {
+    LocalTransport& t;
+    explicit Fwd(LocalTransport& x) : t(x) {}
+    UpdateReply update_cst(const std::string& g, int r, std::uint64_t p, std::span<const Token> v, SimTime n) override {
+      return t.update_cst(g, r, p, v, n);
+    }
+    std::vector<FetchReply> fetch_cst(std::span<const std::string> ids, std::span<const DraftCacheInfo> in,
+                                      SimTime n) override {
+      return t.fetch_cst(ids, in, n);
+    }
+    void register_group(const std::string& g, double ttl, SimTime n) override { t.register_group(g, ttl, n); }
+  };
+  LocalTransport lt(one);
+  Fwd fwd(lt);
+  DgdsParams fresh_p;
+  fresh_p.fetch_period = 0.0;
+  DraftClient rc(fwd, fresh_p);
+  auto z = rc.batch_speculate(cq, 1.0);
+  for (std::size_t i = 0; i < cq.size(); ++i) {
+    EXPECT(z[i].size() == y[i].size());
+    for (std::size_t j = 0; j < z[i].size(); ++j) EXPECT(z[i][j].tokens == y[i][j].tokens && z[i][j].score == y[i][j].score);
+  }
   std::printf("facade ok\n");
   return 0;
 }

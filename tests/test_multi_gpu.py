@@ -190,3 +190,13 @@ def test_two_gpu_routed_parity(tmp_path):
     except Exception:
         msgs = [open(errfile + f".{r}").read() for r in range(2) if os.path.exists(errfile + f".{r}")]
         raise AssertionError("\n".join(msgs) or "worker failed")
+
+
+def test_cluster_on_two_gpus(restatement):
+    """dgds_cluster_* with one shard per GPU (devices 0 and 1): the same differential as the
+    one-GPU cluster test, so groups really live on different devices."""
+    import torch
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs two GPUs")
+    import test_gpu_parity as T
+    T.test_cluster_routes_by_shard_and_matches_oracle(restatement, (0, 1))
