@@ -557,6 +557,39 @@ int dgds_px_status(dgds_px* px, int32_t* timed_out, uint64_t* launches);
 int dgds_px_set_timeout(dgds_px* px, uint64_t timeout_ns);
 int dgds_px_destroy(dgds_px* px);
 
+/* The routed tick loop of one rank in C++ (bench_multi.py's pipeline without the interpreter):
+ * per tick s, the rank's append rows go to their owners (side stream; their metadata rows come
+ * back to pinned memory for the server's planner thread), its query rows go to their owners
+ * once tick s-1's replies are home (second side stream), and on the main stream the owner runs
+ * K2 + fused K3 on the queries it received (replies into the senders' shared reply slab, row =
+ * q_origin_word), waits for its own replies, then launches K1 with tick s's routed plan.
+ * Channels are described exactly as laid out in the px regions (identical on every rank). */
+typedef struct dgds_px_channel_desc {
+  int32_t rows, words;     /* rows per sender (shared: of the whole slab), int32 words per row */
+  int32_t shared, pad;     /* shared: one slab addressed by row (replies) */
+  uint64_t flag_off;
+  uint64_t count_off[2];   /* by parity seq % 2 */
+  uint64_t slab_off[2];
+} dgds_px_channel_desc;
+typedef struct dgds_px_tick {  /* one tick's device-resident rows produced by this rank */
+  int64_t n_q, n_a;
+  const int32_t* q_owner;  /* [n_q] owner rank */
+  const int32_t* q;        /* [n_q][q.words] query records (dgds_query_record_layout) */
+  const int32_t* a_owner;  /* [n_a] */
+  const int32_t* a;        /* [n_a][a.words]: handle | request id | prev lo | prev hi | count | tokens */
+} dgds_px_tick;
+typedef struct dgds_px_driver dgds_px_driver;
+int dgds_px_driver_create(dgds_server* s, dgds_px* px, int32_t world, int32_t rank, const dgds_px_channel_desc* q,
+                          const dgds_px_channel_desc* rep, const dgds_px_channel_desc* a, int32_t q_origin_word,
+                          const dgds_query_record_layout* layout, const dgds_spec_args* d_args, int32_t max_top_k,
+                          int32_t max_spec, int32_t* d_overflow, const dgds_px_tick* ticks, int64_t n_ticks,
+                          void* main_stream, dgds_px_driver** out);
+/* Ticks [first, last) on the main stream (returns once enqueued); ticks < plan_to (0: last) may
+ * be planned ahead — e.g. a warm-up run plans the first tick of the next run. */
+int dgds_px_driver_run(dgds_px_driver* d, int64_t first, int64_t last, int64_t plan_to, dgds_query_stats* d_stats);
+/* Launches any tick planned ahead but not run, waits for the driver's streams, frees it. */
+int dgds_px_driver_destroy(dgds_px_driver* d);
+
 #ifdef __cplusplus
 }
 #endif

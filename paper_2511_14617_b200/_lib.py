@@ -105,6 +105,16 @@ class QueryStats(C.Structure):
     ]
 
 
+class PxChannelDesc(C.Structure):  # dgds_px_channel_desc
+    _fields_ = [("rows", C.c_int32), ("words", C.c_int32), ("shared", C.c_int32), ("pad", C.c_int32),
+                ("flag_off", C.c_uint64), ("count_off", C.c_uint64 * 2), ("slab_off", C.c_uint64 * 2)]
+
+
+class PxTick(C.Structure):  # dgds_px_tick
+    _fields_ = [("n_q", C.c_int64), ("n_a", C.c_int64), ("q_owner", C.c_void_p), ("q", C.c_void_p),
+                ("a_owner", C.c_void_p), ("a", C.c_void_p)]
+
+
 class RecordLayout(C.Structure):
     _fields_ = [(n, C.c_int32) for n in ("rec_words", "off_handle", "off_pat_len", "off_pattern", "off_truth_left",
                                          "off_limit", "off_truth", "reply_words", "off_n_cands", "off_lens",
@@ -245,6 +255,10 @@ EXPORTS = {
     "dgds_px_status": (C.c_int, [_P, C.POINTER(_I32), C.POINTER(_U64)]),
     "dgds_px_set_timeout": (C.c_int, [_P, _U64]),
     "dgds_px_destroy": (C.c_int, [_P]),
+    "dgds_px_driver_create": (C.c_int, [_P, _P, _I32, _I32, _P, _P, _P, _I32, _P, _P, _I32, _I32, _P, _P, _I64, _P,
+                                        C.POINTER(C.c_void_p)]),
+    "dgds_px_driver_run": (C.c_int, [_P, _I64, _I64, _I64, _P]),
+    "dgds_px_driver_destroy": (C.c_int, [_P]),
 }
 
 _lib = None

@@ -15,7 +15,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libdgds_b200.so")
-SOURCES = ["kernels.cu", "peer.cu", "server.cpp", "host_query.cpp", "replica.cpp", "wire.cpp", "cluster.cpp"]
+SOURCES = ["kernels.cu", "peer.cu", "server.cpp", "host_query.cpp", "replica.cpp", "wire.cpp", "cluster.cpp", "px_driver.cpp"]
 # the trace generator of the bench / tests: a separate host-only tools library
 WORKLOAD_SRC = os.path.join(HERE, "..", "tools", "workload", "workload_gen.cpp")
 WORKLOAD_LIB = os.path.join(HERE, "..", "tools", "workload", "libdgds_workload.so")

@@ -192,6 +192,136 @@ def test_two_gpu_routed_parity(tmp_path):
         raise AssertionError("\n".join(msgs) or "worker failed")
 
 
+def _driver_worker(rank, world, port, errfile):
+    try:
+        _run_driver(rank, world, port)
+    except Exception:
+        with open(errfile + f".{rank}", "w") as f:
+            f.write(traceback.format_exc())
+        raise
+
+
+def _run_driver(rank, world, port):
+    """The C++ tick loop (dgds_px_driver_*): T routed ticks of appends + queries enqueued in one
+    call; the replies of the last two ticks (still in their slab parities) must equal the oracle
+    fed every earlier tick's appends, i.e. each tick's queries saw exactly the ticks before it."""
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(rank)
+    dev = torch.device("cuda", rank)
+    from oracle import oracle as O
+    from paper_2511_14617_b200 import _lib
+    from paper_2511_14617_b200 import dgds as D
+    from paper_2511_14617_b200.peer import PeerExchange
+    from paper_2511_14617_b200.workload import CONFIGS, generate_workload, group_id
+
+    cfg = replace(CONFIGS["C1"], num_groups=8, group_size=4, location=400.0, max_tokens=400, vocab_size=40)
+    tr = generate_workload(cfg)
+    G, R = cfg.num_groups, cfg.group_size
+    S = G * R
+    owner_g = np.array([D.shard_of_group(group_id(g), world) for g in range(G)], np.int32)
+    local_h = np.zeros(G, np.int32)
+    for o in range(world):
+        gs = np.nonzero(owner_g == o)[0]
+        local_h[gs] = np.arange(len(gs), dtype=np.int32)
+    srv = D.DraftServer(D.DgdsParams(), device=rank, expected_nodes=1 << 20, expected_streams=S)
+    mine = np.nonzero(owner_g == rank)[0]
+    assert (srv.group_handles([group_id(int(g)) for g in mine]) == np.arange(len(mine))).all()
+    Q, T = 600, 12
+    px = PeerExchange(world, rank, rank, {"a": (S, APP_W), "q": (Q, QRY_W), "rep": (Q, RW, "shared")})
+    px.set_timeout(20.0)
+    L = _lib.lib()
+    ora = O.restatement()
+    oidx = {g: ora.index(group_id=group_id(g)) for g in range(G)}
+    oargs = O.make_args(DL, 6, 1, KQ, 0.1, 1)
+    rng = np.random.default_rng(300 + rank)
+    produced = np.arange(rank, S, world)
+    pos = np.zeros(S, np.int64)
+    keep, expected = [], {}
+    for t in range(T):
+        # queries of tick t see the appends of ticks < t (K2 of a tick runs before its K1)
+        st = rng.choice(np.nonzero(pos >= 2)[0], Q) if t > 0 else rng.integers(0, S, Q)
+        qr = np.zeros((Q, QRY_W), np.int32)
+        pats = []
+        for i, s_ in enumerate(st):
+            p = int(rng.integers(0, pos[s_] + 1))
+            pat = tr.stream(s_)[max(0, p - int(rng.integers(0, 9))):p]
+            pats.append(pat)
+            truth = tr.stream(s_)[p:p + DL]
+            qr[i, 0], qr[i, 1] = local_h[s_ // R], len(pat)
+            qr[i, 2:2 + len(pat)] = pat
+            qr[i, 10] = qr[i, 11] = max(1, tr.lengths[s_] - p)
+            qr[i, 12:12 + len(truth)] = truth
+        if t >= T - 2:
+            expected[t] = [[c.key() for c in oidx[s_ // R].speculate(pat, oargs)] for s_, pat in zip(st, pats)]
+        live = [s_ for s_ in range(S) if pos[s_] < tr.lengths[s_]]
+        mine_live = [s_ for s_ in live if s_ % world == rank]
+        rec = np.zeros((max(1, len(mine_live)), APP_W), np.int32)
+        own = np.full(len(rec), -1, np.int32)
+        for i, s_ in enumerate(mine_live):
+            n = int(min(16, tr.lengths[s_] - pos[s_]))
+            rec[i, :5] = [local_h[s_ // R], s_ % R, pos[s_] & 0xFFFFFFFF, pos[s_] >> 32, n]
+            rec[i, 5:5 + n] = tr.stream(s_)[pos[s_]:pos[s_] + n]
+            own[i] = owner_g[s_ // R]
+        for s_ in live:  # every rank feeds the oracle every stream (the schedule is known to all)
+            n = int(min(16, tr.lengths[s_] - pos[s_]))
+            assert oidx[s_ // R].append(s_ % R, int(pos[s_]), tr.stream(s_)[pos[s_]:pos[s_] + n])[0]
+            pos[s_] += n
+        tensors = [torch.from_numpy(x).to(dev) for x in (owner_g[st // R].astype(np.int32), qr, own, rec)]
+        keep.append(tensors)
+    ticks = (_lib.PxTick * T)(*[_lib.PxTick(Q, x[3].shape[0], x[0].data_ptr(), x[1].data_ptr(), x[2].data_ptr(),
+                                            x[3].data_ptr()) for x in keep])
+
+    def desc(name):
+        c = px.ch[name]
+        d = _lib.PxChannelDesc()
+        d.rows, d.words, d.shared, d.flag_off = c.rows, c.words, 1 if c.shared else 0, c.flag_off
+        d.count_off[0], d.count_off[1] = c.count_off
+        d.slab_off[0], d.slab_off[1] = c.slab_off
+        return d
+    dq, drep, da = desc("q"), desc("rep"), desc("a")
+    lay = _lib.RecordLayout(QRY_W, 0, 1, 2, 10, 11, 12, RW, 0, 1, 6, 14, 22, 54)
+    d_args = torch.from_numpy(D.args_array([D.SpeculationArgs(DL, 6, 1, KQ, 0.1, 1)]).view(np.uint8)).to(dev)
+    drv = C.c_void_p()
+    main = torch.cuda.current_stream(dev)
+    _lib.check(L.dgds_px_driver_create(srv.handle, px.h, world, rank, C.byref(dq), C.byref(drep), C.byref(da),
+                                       QRY_W - 1, C.byref(lay), C.c_void_p(d_args.data_ptr()), KQ, DL,
+                                       C.c_void_p(px.overflow.data_ptr()), ticks, T, C.c_void_p(main.cuda_stream),
+                                       C.byref(drv)))
+    _lib.check(L.dgds_px_driver_run(drv, 0, T - 3, T - 2, None))  # a first run that plans ahead
+    _lib.check(L.dgds_px_driver_run(drv, T - 3, T, 0, None))
+    torch.cuda.synchronize()
+    assert px.status()[0] is False and px.overflow.item() == 0
+    for t in (T - 2, T - 1):
+        back = px.slab("rep", t + 1)[:Q].cpu().numpy()
+        bad = [i for i in range(Q) if _decode(back[i]) != expected[t][i]]
+        assert not bad, f"rank {rank} tick {t}: {len(bad)} of {Q} replies differ from the oracle (first {bad[0]})"
+    assert sum(int(r[0]) for r in back) > Q // 2
+    dist.barrier()
+    _lib.check(L.dgds_px_driver_destroy(drv))
+    assert srv.node_count() == sum(oidx[int(g)].node_count for g in mine)
+    dist.barrier()
+    px.close()
+    srv.close()
+    dist.destroy_process_group()
+
+
+def test_two_gpu_native_tick_driver(tmp_path):
+    import torch
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs two GPUs")
+    import torch.multiprocessing as mp
+    errfile = str(tmp_path / "err")
+    try:
+        mp.spawn(_driver_worker, args=(2, _free_port(), errfile), nprocs=2, join=True)
+    except Exception:
+        msgs = [open(errfile + f".{r}").read() for r in range(2) if os.path.exists(errfile + f".{r}")]
+        raise AssertionError("\n".join(msgs) or "worker failed")
+
+
 def test_cluster_on_two_gpus(restatement):
     """dgds_cluster_* with one shard per GPU (devices 0 and 1): the same differential as the
     one-GPU cluster test, so groups really live on different devices."""
