@@ -444,10 +444,12 @@ def main_b200(args):
     with ClockSampler(local) as clk:
         torch.cuda.synchronize()
         w0 = time.perf_counter()
+        kl0 = L.dgds_kernel_launches()
         e0.record(ext)
         for s in range(W, W + K):
             step(s, True)
         e1.record(ext)
+        kl1 = L.dgds_kernel_launches()
         torch.cuda.synchronize()
         w1 = time.perf_counter()
     if tp is not None:
@@ -631,8 +633,9 @@ def main_b200(args):
         "roofline": roof_q if dom_q else roof_a,
         "roofline_query": roof_q, "roofline_append": roof_a,
         "cpu_baseline": cpu, "e2e": e2e,
-        # K1 and K2+K3 launches (server profile); K2 folds its counters in its last block
-        "gpu_launches": int(prof.append_launches + prof.query_launches),
+        # our kernels enqueued in the timed region (k_stage + K1 + K1b + K2a + K2b per tick;
+        # K2 folds its counters in its last block)
+        "gpu_launches": int(kl1 - kl0),
         "wall_ms_per_step": 1e3 * (w1 - w0) / K,
         "clocks": clk.summary(),
     }

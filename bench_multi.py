@@ -491,9 +491,11 @@ def run_multi(args, world, rank, local, dev):
         tp = profile(activities=[ProfilerActivity.CPU, ProfilerActivity.CUDA])
         tp.__enter__()
     with ClockSampler(local) as clk:
+        kl0 = L.dgds_kernel_launches()
         e0.record()
         run_ticks(W, W + K, True)
         e1.record()
+        kl1 = L.dgds_kernel_launches()
         torch.cuda.synchronize()
     if tp is not None:
         tp.__exit__(None, None, None)
@@ -515,7 +517,7 @@ def run_multi(args, world, rank, local, dev):
     route_launches = (px.status()[1] - px_l0) if use_px else 0
     tot = torch.tensor([sum(steps_in[s]["ntok"] for s in range(W, W + K)), int(d_stats[7].item()),
                         app_alg_owner[0], prof.query_ms * 1e3, prof.append_ms * 1e3,
-                        prof.query_launches + prof.append_launches + route_launches], dtype=torch.float64,
+                        (kl1 - kl0) + route_launches], dtype=torch.float64,
                        device=dev)
     dist.all_reduce(tot)
     ntok_all, q_alg_all, a_alg_all, qus_all, aus_all, launches_all = tot.tolist()

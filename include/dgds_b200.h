@@ -129,6 +129,9 @@ typedef struct dgds_query_stats {
 } dgds_query_stats;
 
 const char* dgds_last_error(void);
+/* Index / query / compaction kernels this process has enqueued (append: k_stage + K1 + K1b;
+ * query: K2a + K2b or K2; compaction; copy-out; verify) — bench.py's gpu_launches. */
+uint64_t dgds_kernel_launches(void);
 const char* dgds_version_string(void);
 
 uint64_t dgds_fnv1a64(const void* data, size_t n); /* detail::fnv1a64 (bytes.hpp:89-96) */

@@ -255,6 +255,7 @@ EXPORTS = {
     "dgds_px_status": (C.c_int, [_P, C.POINTER(_I32), C.POINTER(_U64)]),
     "dgds_px_set_timeout": (C.c_int, [_P, _U64]),
     "dgds_px_destroy": (C.c_int, [_P]),
+    "dgds_kernel_launches": (_U64, []),
     "dgds_px_driver_create": (C.c_int, [_P, _P, _I32, _I32, _P, _P, _P, _I32, _P, _P, _I32, _I32, _P, _P, _I64, _P,
                                         C.POINTER(C.c_void_p)]),
     "dgds_px_driver_run": (C.c_int, [_P, _I64, _I64, _I64, _P]),

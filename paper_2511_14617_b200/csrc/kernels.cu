@@ -1650,6 +1650,7 @@ cudaError_t launch_query_gsbm(const QueryLaunch& L, cudaStream_t st, int64_t blo
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
   return cudaLaunchKernelEx(&cfg, k_query<G, S, B, M>, L);
 }
 
@@ -1729,6 +1730,8 @@ cudaError_t launch_query_g(const QueryLaunch& L, int32_t max_s, cudaStream_t st)
 
 }  // namespace
 
+std::atomic<unsigned long long> g_kernel_launches{0};
+
 cudaError_t launch_append(const DevTrie& T, const AppendSeg* d_segs, int64_t nseg, const AppendPiece* d_pieces,
                           int64_t npieces, const int32_t* d_tokens, const CopyPiece* d_grow, int64_t ngrow,
                           cudaStream_t st) {
@@ -1749,6 +1752,7 @@ cudaError_t launch_append(const DevTrie& T, const AppendSeg* d_segs, int64_t nse
   debug_sync(st, "k_append");
   k_walks<<<148 * 16, 128, 0, st>>>(T);  // ~1 thread per event: walks are latency chains
   debug_sync(st, "k_walks");
+  g_kernel_launches.fetch_add(3, std::memory_order_relaxed);
   return cudaGetLastError();
 }
 
@@ -1767,6 +1771,7 @@ cudaError_t launch_verify(int64_t n, int32_t k_stride, int32_t s_stride, const i
                           const int32_t* limit, int32_t* drafted, int32_t* accepted, int32_t* emitted,
                           cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
+  g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
   k_verify<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(n, k_stride, s_stride, n_cands, lens, tokens,
                                                                       truth, truth_stride, truth_left, limit, drafted,
                                                                       accepted, emitted);
@@ -1996,6 +2001,7 @@ cudaError_t launch_compact_in(int64_t n, const CmpIn& in, long long* block_sums,
                               const long long* carry_in, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
   const int64_t nb = (n + kCmpBlock - 1) / kCmpBlock;
+  g_kernel_launches.fetch_add(3, std::memory_order_relaxed);
   k_cmp_count<<<static_cast<unsigned>(nb), kCmpBlock, 0, st>>>(n, in, block_sums);
   k_cmp_scan<<<1, kCmpBlock, 0, st>>>(nb, block_sums, totals, carry_in);
   k_cmp_scatter<<<static_cast<unsigned>(nb), kCmpBlock, 0, st>>>(n, in, block_sums, meta, tok_out, cand_off, tok_off,
@@ -2026,6 +2032,7 @@ cudaError_t launch_copy_out(const long long* totals, const CopyOutRegions& R, in
                             int max_blocks) {
   if (R.n == 0 || max_bytes <= 0) return cudaSuccess;
   const int64_t blocks = std::min<int64_t>(max_blocks, (max_bytes / 16 + 255) / 256 + 1);
+  g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
   k_copy_out<<<static_cast<unsigned>(blocks), 256, 0, st>>>(totals, R);
   return cudaGetLastError();
 }

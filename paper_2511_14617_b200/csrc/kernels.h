@@ -6,10 +6,15 @@
 #include <string>
 #include <cuda_runtime.h>
 
+#include <atomic>
+
 #include "../../include/dgds_b200.h"
 #include "trie.cuh"
 
 namespace dgds {
+
+// Kernels enqueued by the launch helpers below (process-wide; dgds_kernel_launches)
+extern std::atomic<unsigned long long> g_kernel_launches;
 
 // One warp per segment: all records of one request stream inside one batch, in
 // call order: n tokens at stream positions start .. start + n, read from the

@@ -508,6 +508,8 @@ extern "C" {
 const char* dgds_last_error(void) { return g_err.c_str(); }
 const char* dgds_version_string(void) { return "dgds-b200 0.1 (sm_100a)"; }
 
+uint64_t dgds_kernel_launches(void) { return dgds::g_kernel_launches.load(std::memory_order_relaxed); }
+
 uint64_t dgds_fnv1a64(const void* data, size_t n) { return fnv1a64(data, n); }
 
 int32_t dgds_shard_of_group(const char* gid, size_t len, int32_t shard_count) {  // dgds.cpp:10-14
