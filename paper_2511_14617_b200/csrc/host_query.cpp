@@ -918,12 +918,12 @@ int dgds_verify_batch(dgds_server* s, int64_t n, const dgds_candidates* c, const
   const size_t o_tl = align_up(o_tr + static_cast<size_t>(n) * truth_stride * 4, 256);
   const size_t o_lm = align_up(o_tl + n * 4, 256);
   const size_t in_total = o_lm + n * 4;
-  DGDS_CUDA(cudaEventSynchronize(s->staging_free));
-  if (int rc = s->h_stage.ensure(in_total)) return rc;
+  char* h = nullptr;
+  cudaEvent_t ev_free = nullptr;
+  if (int rc = next_stage(s, in_total, &h, &ev_free)) return rc;
   if (int rc = s->d_stage.ensure(in_total)) return rc;
   if (int rc = s->h_out.ensure(n * 12)) return rc;
   if (int rc = s->d_out.ensure(n * 12)) return rc;
-  char* h = static_cast<char*>(s->h_stage.p);
   std::memcpy(h, c->n_cands, n * 4);
   std::memcpy(h + o_ln, c->lens, n * K * 4);
   std::memcpy(h + o_tk, c->tokens, static_cast<size_t>(n) * K * Sx * 4);
@@ -933,7 +933,7 @@ int dgds_verify_batch(dgds_server* s, int64_t n, const dgds_candidates* c, const
   char* d = static_cast<char*>(s->d_stage.p);
   int32_t* dv = static_cast<int32_t*>(s->d_out.p);
   DGDS_CUDA(cudaMemcpyAsync(d, h, in_total, cudaMemcpyHostToDevice, s->st));
-  DGDS_CUDA(cudaEventRecord(s->staging_free, s->st));
+  DGDS_CUDA(cudaEventRecord(ev_free, s->st));
   DGDS_CUDA(dgds::launch_verify(n, K, Sx, reinterpret_cast<const int32_t*>(d), reinterpret_cast<const int32_t*>(d + o_ln),
                                 reinterpret_cast<const int32_t*>(d + o_tk), reinterpret_cast<const int32_t*>(d + o_tr),
                                 truth_stride, reinterpret_cast<const int32_t*>(d + o_tl),

@@ -458,7 +458,7 @@ int plan_updates(dgds_server* s, int64_t n, const int32_t* handles, const int32_
   // merge the workers' segments (pieces are independent copies: k_stage)
   if (W == 1) {
     Part& P = parts[0];
-    segs.assign(P.segs.begin(), P.segs.end());  // copy: both vectors keep their capacity
+    segs.swap(P.segs);  // P.segs is cleared before its next use; both buffers keep their capacity
     *worst = P.worst;
     pieces.resize(P.pend.size());
     for (size_t k = 0; k < P.pend.size(); ++k) {
@@ -537,7 +537,9 @@ int dgds_create(const dgds_params* params, dgds_server** out) {
   s->D = p.max_pattern_len + p.max_spec_len;
   s->shard_counts.assign(p.shard_count, 0);
   DGDS_CUDA(cudaStreamCreateWithFlags(&s->st, cudaStreamNonBlocking));
-  DGDS_CUDA(cudaEventCreateWithFlags(&s->staging_free, cudaEventDisableTiming));
+  for (auto& e : s->staging_free) DGDS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  for (auto& e : s->plan_ready) DGDS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  for (auto& e : s->plan_free) DGDS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   DGDS_CUDA(cudaStreamCreateWithFlags(&s->copy_st, cudaStreamNonBlocking));
   DGDS_CUDA(cudaStreamCreateWithFlags(&s->out_st, cudaStreamNonBlocking));
   for (auto& q : s->qslot) DGDS_CUDA(cudaEventCreateWithFlags(&q.done, cudaEventDisableTiming));
@@ -628,7 +630,12 @@ int dgds_destroy(dgds_server* s) {
   cudaFree(s->d_stat_part);
   cudaFree(s->d_hist);
   free_plan_pool(s);
-  if (s->staging_free) cudaEventDestroy(s->staging_free);
+  for (auto e : s->staging_free)
+    if (e) cudaEventDestroy(e);
+  for (auto e : s->plan_ready)
+    if (e) cudaEventDestroy(e);
+  for (auto e : s->plan_free)
+    if (e) cudaEventDestroy(e);
   for (auto& q : s->qslot)
     if (q.done) cudaEventDestroy(q.done);
   if (s->copy_st) cudaStreamDestroy(s->copy_st);
@@ -821,10 +828,10 @@ int update_batch_locked(dgds_server* s, int64_t n, const int32_t* handles, const
   const size_t b_grow = grow.size() * sizeof(dgds::CopyPiece);
   const size_t o_tok = align_up(o_grow + b_grow, 256);
   const size_t total = o_tok + ntok * sizeof(int32_t);
-  DGDS_CUDA(cudaEventSynchronize(s->staging_free));
-  if (int rc = s->h_stage.ensure(total)) return rc;
+  char* h = nullptr;
+  cudaEvent_t ev_free = nullptr;
+  if (int rc = next_stage(s, total, &h, &ev_free)) return rc;
   if (int rc = s->d_stage.ensure(total)) return rc;
-  char* h = static_cast<char*>(s->h_stage.p);
   for (auto& pc : pieces) pc.tok_off -= offs[0];
   nt_copy(h, segs.data(), b_seg);
   nt_copy(h + o_piece, pieces.data(), b_piece);
@@ -835,7 +842,7 @@ int update_batch_locked(dgds_server* s, int64_t n, const int32_t* handles, const
   pc.mark("stage");
   if (int rc = flush_pending(s)) return rc;  // K1 after the query batch submitted before it
   DGDS_CUDA(cudaMemcpyAsync(d, h, total, cudaMemcpyHostToDevice, s->st));
-  DGDS_CUDA(cudaEventRecord(s->staging_free, s->st));
+  DGDS_CUDA(cudaEventRecord(ev_free, s->st));
   {
     LaunchTimer lt(s, 0, s->st);
     DGDS_CUDA(dgds::launch_append(s->T, reinterpret_cast<const dgds::AppendSeg*>(d),
@@ -906,12 +913,14 @@ static void free_plan_pool(dgds_server* s) {
 // Host half: validation, bookkeeping (replies, versions, history log), capacity. Plans must be
 // launched in the order they were made (K1 of a later plan reads the stream rows K1 of an
 // earlier one writes), which dgds_update_launch checks.
+// defer_logs = false (a plan launched within the same locked call): history-log records go
+// straight to the group logs instead of through the plan.
 static int plan_device(dgds_server* s, int64_t n, const int32_t* handles, const int32_t* rids, const uint64_t* prev,
                        const uint64_t* offs, const uint64_t* counts, const int32_t* d_tokens, double now,
-                       dgds_update_reply* rep, dgds_update_plan* plan) {
+                       dgds_update_reply* rep, dgds_update_plan* plan, bool defer_logs = true) {
   uint64_t worst = 0;
   const int prc = plan_updates(s, n, handles, rids, prev, offs, counts, now, rep, plan->segs, plan->pieces,
-                               plan->grow, &worst, &plan->logs);
+                               plan->grow, &worst, defer_logs ? &plan->logs : nullptr);
   if (!plan->logs.empty()) s->log_pending.push_back(plan);  // accepted records, even on a later error
   if (prc) return prc;
   if (plan->segs.empty()) return DGDS_OK;
@@ -934,19 +943,23 @@ static int launch_plan(dgds_server* s, dgds_update_plan* plan, void* stream, Pha
   const size_t o_piece = align_up(b_seg, 256);
   const size_t o_grow = align_up(o_piece + plan->pieces.size() * sizeof(dgds::AppendPiece), 256);
   const size_t total = o_grow + plan->grow.size() * sizeof(dgds::CopyPiece);
-  DGDS_CUDA(cudaEventSynchronize(s->staging_free));
+  char* h = nullptr;
+  cudaEvent_t ev_free = nullptr;
+  if (int rc = next_stage(s, total, &h, &ev_free)) return rc;
   pc.mark("staging_wait");
-  if (int rc = s->h_stage.ensure(total)) return rc;
-  if (int rc = s->d_stage.ensure(total)) return rc;
-  char* h = static_cast<char*>(s->h_stage.p);
+  const int k = s->stage_k;  // the parity next_stage chose
+  if (int rc = s->d_plan[k].ensure(total)) return rc;  // growth: cudaFree waits for the device
   nt_copy(h, plan->segs.data(), b_seg);
   nt_copy(h + o_piece, plan->pieces.data(), plan->pieces.size() * sizeof(dgds::AppendPiece));
   nt_copy(h + o_grow, plan->grow.data(), plan->grow.size() * sizeof(dgds::CopyPiece));
   _mm_sfence();
   pc.mark("stage");
-  char* d = static_cast<char*>(s->d_stage.p);
-  DGDS_CUDA(cudaMemcpyAsync(d, h, total, cudaMemcpyHostToDevice, join.stream()));
-  DGDS_CUDA(cudaEventRecord(s->staging_free, join.stream()));
+  char* d = static_cast<char*>(s->d_plan[k].p);
+  DGDS_CUDA(cudaStreamWaitEvent(s->copy_st, s->plan_free[k], 0));  // its last readers were enqueued
+  DGDS_CUDA(cudaMemcpyAsync(d, h, total, cudaMemcpyHostToDevice, s->copy_st));
+  DGDS_CUDA(cudaEventRecord(ev_free, s->copy_st));
+  DGDS_CUDA(cudaEventRecord(s->plan_ready[k], s->copy_st));
+  DGDS_CUDA(cudaStreamWaitEvent(join.stream(), s->plan_ready[k], 0));
   {
     LaunchTimer lt(s, 0, join.stream());
     DGDS_CUDA(dgds::launch_append(s->T, reinterpret_cast<const dgds::AppendSeg*>(d),
@@ -956,6 +969,7 @@ static int launch_plan(dgds_server* s, dgds_update_plan* plan, void* stream, Pha
                                   reinterpret_cast<const dgds::CopyPiece*>(d + o_grow),
                                   static_cast<int64_t>(plan->grow.size()), join.stream()));
   }
+  DGDS_CUDA(cudaEventRecord(s->plan_free[k], join.stream()));
   pc.mark("copy_launch");
   return DGDS_OK;
 }
@@ -973,7 +987,7 @@ static int update_device_impl(dgds_server* s, int64_t n, const int32_t* handles,
   plan.segs.clear();
   plan.pieces.clear();
   plan.grow.clear();
-  if (int rc = plan_device(s, n, handles, rids, prev, offs, counts, d_tokens, now, rep, &plan)) {
+  if (int rc = plan_device(s, n, handles, rids, prev, offs, counts, d_tokens, now, rep, &plan, false)) {
     materialize_logs(s);
     return rc;
   }

@@ -386,7 +386,7 @@ struct dgds_server {
   dgds_params p{};
   int32_t D = 0;
   cudaStream_t st = nullptr;
-  cudaEvent_t staging_free = nullptr;
+  cudaEvent_t staging_free[2] = {nullptr, nullptr};  // h_stage[k]'s last H2D is done
   // host-path query inputs: own staging pair and copy stream, so their H2D overlaps the
   // append kernel queued before them on `st`
   cudaStream_t copy_st = nullptr;
@@ -481,7 +481,15 @@ struct dgds_server {
   std::vector<uint64_t> shard_counts;
   uint64_t batch_stamp = 0;
 
-  PinnedBuf h_stage, h_out;  // update staging; dgds_verify_batch results
+  // update / verify staging, double-buffered so the host can plan a batch ahead of the last
+  // one's H2D (the single buffer made tick s+1's plan wait for tick s's copy)
+  PinnedBuf h_stage[2], h_out;  // h_out: dgds_verify_batch results
+  int stage_k = 0;
+  // device update plans (segment / piece tables), by h_stage parity: copied in on copy_st as
+  // soon as staged, so the H2D runs under the previous batch's kernels instead of between them
+  DevBuf d_plan[2];
+  cudaEvent_t plan_ready[2] = {nullptr, nullptr};  // d_plan[k] copied in
+  cudaEvent_t plan_free[2] = {nullptr, nullptr};   // K1 of the last plan in d_plan[k] enqueued before this
   DevBuf d_stage, d_out;
   bool h2d_kernel = false;  // copy-engine H2D (no SMs taken from K1); DGDS_H2D=kernel: a pull kernel
   int h2d_blocks = 148;    // one CTA per SM (measured best); DGDS_H2D_BLOCKS
@@ -544,6 +552,17 @@ int compact_memory(dgds_server* s);
 int maybe_compact(dgds_server* s);
 
 // Brackets one kernel launch with events on its stream when profiling is on.
+// The next host staging buffer (alternating): waits for its previous H2D, sizes it; the caller
+// records *ev on the stream of its copy out of it.
+inline int next_stage(dgds_server* s, size_t bytes, char** h, cudaEvent_t* ev) {
+  const int k = s->stage_k ^= 1;
+  DGDS_CUDA(cudaEventSynchronize(s->staging_free[k]));
+  if (int rc = s->h_stage[k].ensure(bytes)) return rc;
+  *h = static_cast<char*>(s->h_stage[k].p);
+  *ev = s->staging_free[k];
+  return DGDS_OK;
+}
+
 struct LaunchTimer {
   dgds_server* s;
   int kind;
