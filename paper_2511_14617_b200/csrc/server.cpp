@@ -831,18 +831,23 @@ int update_batch_locked(dgds_server* s, int64_t n, const int32_t* handles, const
   char* h = nullptr;
   cudaEvent_t ev_free = nullptr;
   if (int rc = next_stage(s, total, &h, &ev_free)) return rc;
-  if (int rc = s->d_stage.ensure(total)) return rc;
+  const int k = s->stage_k;  // the parity next_stage chose (d_plan protocol: launch_plan)
+  if (int rc = s->d_plan[k].ensure(total)) return rc;
   for (auto& pc : pieces) pc.tok_off -= offs[0];
   nt_copy(h, segs.data(), b_seg);
   nt_copy(h + o_piece, pieces.data(), b_piece);
   nt_copy(h + o_grow, grow.data(), b_grow);
   nt_copy(h + o_tok, tokens + offs[0], ntok * sizeof(int32_t));
   _mm_sfence();
-  char* d = static_cast<char*>(s->d_stage.p);
+  char* d = static_cast<char*>(s->d_plan[k].p);
   pc.mark("stage");
   if (int rc = flush_pending(s)) return rc;  // K1 after the query batch submitted before it
-  DGDS_CUDA(cudaMemcpyAsync(d, h, total, cudaMemcpyHostToDevice, s->st));
-  DGDS_CUDA(cudaEventRecord(ev_free, s->st));
+  // the copy runs on copy_st under the kernels already queued; K1 waits for it
+  DGDS_CUDA(cudaStreamWaitEvent(s->copy_st, s->plan_free[k], 0));
+  DGDS_CUDA(cudaMemcpyAsync(d, h, total, cudaMemcpyHostToDevice, s->copy_st));
+  DGDS_CUDA(cudaEventRecord(ev_free, s->copy_st));
+  DGDS_CUDA(cudaEventRecord(s->plan_ready[k], s->copy_st));
+  DGDS_CUDA(cudaStreamWaitEvent(s->st, s->plan_ready[k], 0));
   {
     LaunchTimer lt(s, 0, s->st);
     DGDS_CUDA(dgds::launch_append(s->T, reinterpret_cast<const dgds::AppendSeg*>(d),
@@ -851,6 +856,7 @@ int update_batch_locked(dgds_server* s, int64_t n, const int32_t* handles, const
                                   reinterpret_cast<const dgds::CopyPiece*>(d + o_grow),
                                   static_cast<int64_t>(grow.size()), s->st));
   }
+  DGDS_CUDA(cudaEventRecord(s->plan_free[k], s->st));
   s->used_ub += worst;
   return DGDS_OK;
 }
