@@ -298,6 +298,7 @@ __device__ void conversion_walk(const DevTrie& T, WalkEvent e, unsigned long lon
 }
 
 __global__ void k_walks(DevTrie T) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // PDL launch: K1 is complete
   const unsigned long long n = __ldcg(T.ev_count);
   unsigned long long inserted = 0;
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
@@ -325,6 +326,7 @@ __global__ void k_walks(DevTrie T) {
 template <int B>  // threads per block (one warp per segment; B only sets the block granularity)
 __global__ void __launch_bounds__(B, DGDS_APPEND_OCC * (kBlock / B))
     k_append(DevTrie T, const AppendSeg* __restrict__ segs, int64_t nseg) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // PDL launch: k_stage is complete
   if (__ldcg(T.err) & 2) return;  // k_stage found a negative token: the batch inserts nothing
   const int lane = lane_id();
   const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / kWarp;
@@ -1732,6 +1734,24 @@ cudaError_t launch_query_g(const QueryLaunch& L, int32_t max_s, cudaStream_t st)
 
 std::atomic<unsigned long long> g_kernel_launches{0};
 
+namespace {
+// Launch with programmatic stream serialization: the launch overlaps the previous kernel's
+// tail; the kernel's first instruction (griddepcontrol.wait) waits for that kernel's completion.
+template <class... P, class... A>
+cudaError_t launch_pdl(void (*kernel)(P...), int64_t blocks, int threads, cudaStream_t st, A&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>(blocks));
+  cfg.blockDim = dim3(threads);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<A>(args)...);
+}
+}  // namespace
+
 cudaError_t launch_append(const DevTrie& T, const AppendSeg* d_segs, int64_t nseg, const AppendPiece* d_pieces,
                           int64_t npieces, const int32_t* d_tokens, const CopyPiece* d_grow, int64_t ngrow,
                           cudaStream_t st) {
@@ -1746,11 +1766,13 @@ cudaError_t launch_append(const DevTrie& T, const AppendSeg* d_segs, int64_t nse
   const int blk = append_block();
   const int64_t wpb = blk / kWarp;
   const int64_t blocks = (nseg + wpb - 1) / wpb;
-  if (blk == 32) k_append<32><<<static_cast<unsigned>(blocks), 32, 0, st>>>(T, d_segs, nseg);
-  else if (blk == 64) k_append<64><<<static_cast<unsigned>(blocks), 64, 0, st>>>(T, d_segs, nseg);
-  else k_append<kBlock><<<static_cast<unsigned>(blocks), kBlock, 0, st>>>(T, d_segs, nseg);
+  cudaError_t e;
+  if (blk == 32) e = launch_pdl(k_append<32>, blocks, 32, st, T, d_segs, nseg);
+  else if (blk == 64) e = launch_pdl(k_append<64>, blocks, 64, st, T, d_segs, nseg);
+  else e = launch_pdl(k_append<kBlock>, blocks, kBlock, st, T, d_segs, nseg);
+  if (e != cudaSuccess) return e;
   debug_sync(st, "k_append");
-  k_walks<<<148 * 16, 128, 0, st>>>(T);  // ~1 thread per event: walks are latency chains
+  if ((e = launch_pdl(k_walks, 148 * 16, 128, st, T)) != cudaSuccess) return e;  // ~1 thread per event
   debug_sync(st, "k_walks");
   g_kernel_launches.fetch_add(3, std::memory_order_relaxed);
   return cudaGetLastError();
