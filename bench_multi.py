@@ -431,34 +431,19 @@ def run_multi(args, world, rank, local, dev):
     # The px tick loop runs in C++ (dgds_px_driver_*, csrc/px_driver.cpp) unless
     # DGDS_PX_DRIVER=python: same pipeline, no interpreter on the per-tick critical path.
     native_driver = use_px and os.environ.get("DGDS_PX_DRIVER", "native") == "native"
-    drv = C.c_void_p()
+    drv = None
     if native_driver:
-        def chan_desc(name):
-            c = px.ch[name]
-            d = _lib.PxChannelDesc()
-            d.rows, d.words, d.shared, d.flag_off = c.rows, c.words, 1 if c.shared else 0, c.flag_off
-            d.count_off[0], d.count_off[1] = c.count_off
-            d.slab_off[0], d.slab_off[1] = c.slab_off
-            return d
-        descs = [chan_desc(n) for n in ("q", "rep", "a")]
+        from paper_2511_14617_b200.peer import TickDriver
         n_drv = W + K  # the device-resident ticks; the e2e loop below runs in Python after a sync
-        drv_ticks = (_lib.PxTick * n_drv)()
-        for s_ in range(n_drv):
-            x = steps_in[s_]
-            drv_ticks[s_] = _lib.PxTick(x["q"].shape[0], x["app"].shape[0], x["q_owner"].data_ptr(),
-                                        x["q"].data_ptr(), x["app_owner"].data_ptr(), x["app"].data_ptr())
-        _lib.check(L.dgds_px_driver_create(srv.handle, px.h, world, rank, C.byref(descs[0]), C.byref(descs[1]),
-                                           C.byref(descs[2]), QRY_W - 1, C.byref(layout),
-                                           C.c_void_p(sp_args.data_ptr()), kq, dl,
-                                           C.c_void_p(px.overflow.data_ptr()), drv_ticks, n_drv,
-                                           C.c_void_p(torch.cuda.current_stream(dev).cuda_stream), C.byref(drv)))
+        drv = TickDriver(srv, px, layout, sp_args, kq, dl,
+                         [(steps_in[i]["q_owner"], steps_in[i]["q"], steps_in[i]["app_owner"], steps_in[i]["app"])
+                          for i in range(n_drv)], QRY_W - 1, stream=torch.cuda.current_stream(dev))
 
     def run_ticks(a, b, stats, plan_to=None):
         """Ticks [a, b) back to back, pipelined (px) or in order (nccl); ticks < plan_to (default b)
         may be planned ahead."""
         if native_driver:
-            _lib.check(L.dgds_px_driver_run(drv, a, b, plan_to or 0,
-                                            C.c_void_p(d_stats.data_ptr()) if stats else None))
+            drv.run(a, b, plan_to or 0, d_stats if stats else None)
             return None
         run_until[0] = b
         plan_until[0] = b if plan_to is None else plan_to
@@ -668,8 +653,8 @@ def run_multi(args, world, rank, local, dev):
     torch.cuda.synchronize()
     if planner is not None:
         planner.shutdown(wait=True)
-    if drv:
-        _lib.check(L.dgds_px_driver_destroy(drv))
+    if drv is not None:
+        drv.close()
     if use_px:
         px.close()  # every rank is past its last exchange (barrier above)
     srv.close()

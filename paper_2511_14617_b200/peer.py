@@ -209,3 +209,50 @@ def speculate_routed(srv, px: PeerExchange, q_ch: str, rep_ch: str, seq: int, la
         max_spec, px.seg_out(rep_ch, seq), origin_field, C.c_void_p(stats.data_ptr()) if stats is not None else None,
         C.c_void_p(st.cuda_stream)))
     px.signal(rep_ch, seq, st)
+
+
+class TickDriver:
+    """The routed tick loop in C++ (``dgds_px_driver_*``, csrc/px_driver.cpp) for one rank.
+
+    ``ticks`` is a list of (q_owner, q_records, a_owner, a_records) device tensors, one per tick
+    (int32, contiguous; query rows carry ``q_origin_word``, append rows the layout
+    handle | request id | prev lo | prev hi | count | tokens). ``run(first, last)`` enqueues
+    ticks [first, last) on ``stream``: queries to their owners, the owner's K2 + K3 with replies
+    into the senders' shared ``rep`` slab, appends to their owners planned on the server's
+    planner thread and launched after each tick's queries."""
+
+    def __init__(self, srv, px: PeerExchange, layout, d_args: torch.Tensor, max_top_k: int, max_spec: int,
+                 ticks: Sequence[Tuple[torch.Tensor, torch.Tensor, torch.Tensor, torch.Tensor]],
+                 q_origin_word: int, stream=None, q: str = "q", rep: str = "rep", a: str = "a"):
+        L = _lib.lib()
+        self._keep = [t for tick in ticks for t in tick]  # the driver reads them until it is destroyed
+        descs = [self._desc(px.ch[n]) for n in (q, rep, a)]
+        arr = (_lib.PxTick * len(ticks))(*[_lib.PxTick(qr.shape[0], ar.shape[0], qo.data_ptr(), qr.data_ptr(),
+                                                       ao.data_ptr(), ar.data_ptr()) for qo, qr, ao, ar in ticks])
+        st = stream if stream is not None else torch.cuda.current_stream(px.device)
+        self.h = C.c_void_p()
+        _lib.check(L.dgds_px_driver_create(srv.handle, px.h, px.world, px.rank, C.byref(descs[0]), C.byref(descs[1]),
+                                           C.byref(descs[2]), q_origin_word, C.byref(layout),
+                                           C.c_void_p(d_args.data_ptr()), max_top_k, max_spec,
+                                           C.c_void_p(px.overflow.data_ptr()), arr, len(ticks),
+                                           C.c_void_p(st.cuda_stream), C.byref(self.h)))
+
+    @staticmethod
+    def _desc(c: Channel):
+        d = _lib.PxChannelDesc()
+        d.rows, d.words, d.shared, d.flag_off = c.rows, c.words, 1 if c.shared else 0, c.flag_off
+        d.count_off[0], d.count_off[1] = c.count_off
+        d.slab_off[0], d.slab_off[1] = c.slab_off
+        return d
+
+    def run(self, first: int, last: int, plan_to: int = 0, stats: Optional[torch.Tensor] = None) -> None:
+        """Ticks [first, last); ticks < plan_to (0: last) may be planned ahead."""
+        _lib.check(_lib.lib().dgds_px_driver_run(self.h, first, last, plan_to,
+                                                 C.c_void_p(stats.data_ptr()) if stats is not None else None))
+
+    def close(self) -> None:
+        """Launches any tick planned ahead but not run, then frees the driver."""
+        if self.h:
+            _lib.check(_lib.lib().dgds_px_driver_destroy(self.h))
+            self.h = C.c_void_p()
+

@@ -215,7 +215,7 @@ def _run_driver(rank, world, port):
     from oracle import oracle as O
     from paper_2511_14617_b200 import _lib
     from paper_2511_14617_b200 import dgds as D
-    from paper_2511_14617_b200.peer import PeerExchange
+    from paper_2511_14617_b200.peer import PeerExchange, TickDriver
     from paper_2511_14617_b200.workload import CONFIGS, generate_workload, group_id
 
     cfg = replace(CONFIGS["C1"], num_groups=8, group_size=4, location=400.0, max_tokens=400, vocab_size=40)
@@ -233,7 +233,6 @@ def _run_driver(rank, world, port):
     Q, T = 600, 12
     px = PeerExchange(world, rank, rank, {"a": (S, APP_W), "q": (Q, QRY_W), "rep": (Q, RW, "shared")})
     px.set_timeout(20.0)
-    L = _lib.lib()
     ora = O.restatement()
     oidx = {g: ora.index(group_id=group_id(g)) for g in range(G)}
     oargs = O.make_args(DL, 6, 1, KQ, 0.1, 1)
@@ -272,27 +271,11 @@ def _run_driver(rank, world, port):
             pos[s_] += n
         tensors = [torch.from_numpy(x).to(dev) for x in (owner_g[st // R].astype(np.int32), qr, own, rec)]
         keep.append(tensors)
-    ticks = (_lib.PxTick * T)(*[_lib.PxTick(Q, x[3].shape[0], x[0].data_ptr(), x[1].data_ptr(), x[2].data_ptr(),
-                                            x[3].data_ptr()) for x in keep])
-
-    def desc(name):
-        c = px.ch[name]
-        d = _lib.PxChannelDesc()
-        d.rows, d.words, d.shared, d.flag_off = c.rows, c.words, 1 if c.shared else 0, c.flag_off
-        d.count_off[0], d.count_off[1] = c.count_off
-        d.slab_off[0], d.slab_off[1] = c.slab_off
-        return d
-    dq, drep, da = desc("q"), desc("rep"), desc("a")
     lay = _lib.RecordLayout(QRY_W, 0, 1, 2, 10, 11, 12, RW, 0, 1, 6, 14, 22, 54)
     d_args = torch.from_numpy(D.args_array([D.SpeculationArgs(DL, 6, 1, KQ, 0.1, 1)]).view(np.uint8)).to(dev)
-    drv = C.c_void_p()
-    main = torch.cuda.current_stream(dev)
-    _lib.check(L.dgds_px_driver_create(srv.handle, px.h, world, rank, C.byref(dq), C.byref(drep), C.byref(da),
-                                       QRY_W - 1, C.byref(lay), C.c_void_p(d_args.data_ptr()), KQ, DL,
-                                       C.c_void_p(px.overflow.data_ptr()), ticks, T, C.c_void_p(main.cuda_stream),
-                                       C.byref(drv)))
-    _lib.check(L.dgds_px_driver_run(drv, 0, T - 3, T - 2, None))  # a first run that plans ahead
-    _lib.check(L.dgds_px_driver_run(drv, T - 3, T, 0, None))
+    drv = TickDriver(srv, px, lay, d_args, KQ, DL, keep, QRY_W - 1)
+    drv.run(0, T - 3, T - 2)  # a first run that plans ahead
+    drv.run(T - 3, T)
     torch.cuda.synchronize()
     assert px.status()[0] is False and px.overflow.item() == 0
     for t in (T - 2, T - 1):
@@ -301,7 +284,7 @@ def _run_driver(rank, world, port):
         assert not bad, f"rank {rank} tick {t}: {len(bad)} of {Q} replies differ from the oracle (first {bad[0]})"
     assert sum(int(r[0]) for r in back) > Q // 2
     dist.barrier()
-    _lib.check(L.dgds_px_driver_destroy(drv))
+    drv.close()
     assert srv.node_count() == sum(oidx[int(g)].node_count for g in mine)
     dist.barrier()
     px.close()
