@@ -36,6 +36,11 @@ constexpr int kBlock = 256;
 #ifndef DGDS_K1_PDL_TRIGGER
 #define DGDS_K1_PDL_TRIGGER 0  // measured flat on C2 (profiles/r1_pdl_trigger.txt)
 #endif
+#ifndef DGDS_K2B_OCC
+// K2b (M = 2): resident blocks per SM (x kBlock / B). 2 gives K2b 128 registers and no stack;
+// 3 (80 registers + 112 B of stack) and 4 spilled and were 5-13% slower, 1 starved it (25%)
+#define DGDS_K2B_OCC 2
+#endif
 #ifndef DGDS_QUERY_OCC
 #define DGDS_QUERY_OCC 4
 #endif
@@ -1313,7 +1318,7 @@ __device__ __forceinline__ void query_tile(const QueryLaunch& P, GroupScratch<G,
 // K2b holds only branching queries and loops over them: 3 blocks of 256 per SM (85 registers)
 // instead of 4 (64), which removes its spills.
 template <int G, int S, int B, int M>
-__global__ void __launch_bounds__(B, (M == 2 ? 3 : DGDS_QUERY_OCC) * (kBlock / B)) k_query(QueryLaunch P) {
+__global__ void __launch_bounds__(B, (M == 2 ? DGDS_K2B_OCC : DGDS_QUERY_OCC) * (kBlock / B)) k_query(QueryLaunch P) {
   // Programmatic dependent launch: the blocks may be resident before the previous kernel in
   // the stream (K1, or K2a for K2b) has finished; nothing is read until it has.
   asm volatile("griddepcontrol.wait;" ::: "memory");
