@@ -40,8 +40,8 @@ DEFAULT_CONFIG = "C2"
 RANDOM_CEILING_GBS = 1155.0
 # dram__bytes_read.sum + dram__bytes_write.sum per launch, from one `ncu --set full` capture of
 # the same command (profiles/r2_summary.md); a capture constant, not measured in this run.
-QUERY_TRAFFIC = {"value": 63553536 + 1948672 + 28480768 + 273664,
-                 "source": "capture constant: ncu --set full prof_query_r2e (K2a + K2b, read + write), profiles/r2_summary.md"}
+QUERY_TRAFFIC = {"value": 63374336 + 1956864 + 28820736 + 26624,
+                 "source": "capture constant: ncu --set full prof_query_r2f (K2a + K2b, read + write), profiles/r2_summary.md"}
 APPEND_TRAFFIC = {"value": 903936 + 24150272 + 882944 + 4275200 + 512,
                   "source": "capture constant: ncu --set full prof_append_r2e (k_stage + K1 + K1b, read + write), "
                             "profiles/r2_summary.md"}
