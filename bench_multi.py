@@ -69,7 +69,9 @@ def run_multi(args, world, rank, local, dev):
     # bytecode (measured: fewer slow runs at 0.1 ms)
     import sys
     sys.setswitchinterval(float(os.environ.get("DGDS_SWITCH_INTERVAL", "0.0001")))
-    if os.environ.get("DGDS_PIN_CORES", "1") == "1":
+    # measured on a 4-GPU box: pinning each rank to 8 cores cost 10-15% at N=4 (0.347-0.368 vs
+    # 0.313-0.317 ms per tick unpinned), so it is opt-in
+    if os.environ.get("DGDS_PIN_CORES", "0") == "1":
         _pin_rank_cores(world, local)
         if os.environ.get("DGDS_TICK_TRACE") == "1":
             print(f"rank {local} cores {sorted(os.sched_getaffinity(0))} near {sorted(_gpu_local_cpus(local) or [])[:4]}...",
