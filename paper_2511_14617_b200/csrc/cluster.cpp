@@ -17,7 +17,7 @@ namespace {
 // One persistent host thread per GPU; run(f) calls f(g) for every GPU in parallel.
 class GpuThreads {
  public:
-  explicit GpuThreads(const std::vector<int>& devices) : dev_(devices), job_(devices.size(), 0) {
+  explicit GpuThreads(const std::vector<int>& devices) : dev_(devices) {
     for (size_t g = 0; g < dev_.size(); ++g) th_.emplace_back([this, g] { loop(static_cast<int>(g)); });
   }
   ~GpuThreads() {
@@ -57,7 +57,6 @@ class GpuThreads {
     }
   }
   std::vector<int> dev_;
-  std::vector<uint64_t> job_;
   std::vector<std::thread> th_;
   std::mutex mu_;
   std::condition_variable cv_, done_;
@@ -152,7 +151,7 @@ int partition(dgds_cluster* c, int64_t n, const int32_t* handles, const uint64_t
   if (N == 1) {  // one GPU: only the handles are mapped (the owner validates the rest)
     dgds_cluster::Part& p = c->part[0];
     sized(p.handles, n);
-    sized(p.idx, n);
+    sized(p.idx, n);  // only its size is read: it marks the single owner's part as the whole call
     for (int64_t i = 0; i < n; ++i) {
       if (int rc = owner_check(c, handles[i])) return rc;
       p.handles[i] = c->owner_of[handles[i]].second;

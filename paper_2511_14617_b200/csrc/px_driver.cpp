@@ -17,8 +17,6 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
-#include <cstring>
-#include <deque>
 #include <map>
 #include <string>
 #include <vector>
